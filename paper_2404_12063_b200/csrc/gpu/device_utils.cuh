@@ -1,0 +1,92 @@
+// Small sm_100a device helpers: vector shared-memory access, mbarrier and
+// bulk-copy (TMA 1-D, cp.async.bulk) primitives, exact activations.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace vpg {
+
+constexpr int kThreads = 128;  // threads per CTA of the step kernels
+constexpr int kWarps = kThreads / 32;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ float4 lds4(const float* p) {
+  return *reinterpret_cast<const float4*>(p);
+}
+__device__ __forceinline__ void sts4(float* p, float4 v) {
+  *reinterpret_cast<float4*>(p) = v;
+}
+
+// ---- mbarrier + cp.async.bulk (1-D TMA) ------------------------------------
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
+               : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
+                                         uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, "
+      "[%3];" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+      " selp.u32 %0, 1, 0, p;\n}\n"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  while (!mbar_try_wait(bar, parity)) {
+  }
+}
+
+__device__ __forceinline__ uint64_t globaltimer() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// ---- activations (ActDerivs, network.hpp:171-192, from the OUTPUT z) --------
+// s1 = act', kap = act''/act' so that s2 = kap * s1:
+//   tanh:    s1 = 1 - z^2,   kap = -2 z
+//   sigmoid: s1 = z (1 - z), kap = 1 - 2 z
+// Accurate libdevice tanhf/expf (no fast-math): fp32 parity needs < 2^-20.
+__device__ __forceinline__ float act_value(int sig, float a) {
+  return sig ? 1.0f / (1.0f + expf(-a)) : tanhf(a);
+}
+__device__ __forceinline__ float act_s1(int sig, float z) {
+  return sig ? z * (1.0f - z) : 1.0f - z * z;
+}
+__device__ __forceinline__ float act_kap(int sig, float z) {
+  return sig ? 1.0f - 2.0f * z : -2.0f * z;
+}
+
+// network.hpp:130-138
+__device__ __forceinline__ float softplusf(float x) {
+  return log1pf(expf(-fabsf(x))) + fmaxf(x, 0.0f);
+}
+__device__ __forceinline__ float sigmoidf(float x) { return 1.0f / (1.0f + expf(-x)); }
+
+__device__ __forceinline__ bool finitef(float x) { return isfinite(x); }
+
+}  // namespace vpg

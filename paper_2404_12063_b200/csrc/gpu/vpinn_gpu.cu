@@ -1,0 +1,1088 @@
+// C-ABI implementation of include/vpinn_gpu.h: device context, uploads,
+// kernel-variant dispatch, CUDA-graph-captured epochs, NCCL all-reduce.
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <climits>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <limits>
+#include <map>
+#include <memory>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include <nccl.h>
+
+#include "aux_kernels.cuh"
+#include "variant.h"
+#include "vpinn_gpu.h"
+
+namespace {
+
+thread_local std::string g_err;
+
+struct Fail {
+  int code;
+  std::string msg;
+};
+
+#define CK(x)                                                                           \
+  do {                                                                                  \
+    cudaError_t e_ = (x);                                                               \
+    if (e_ != cudaSuccess)                                                              \
+      throw Fail{VPINN_ERR_DEVICE, std::string(#x) + ": " + cudaGetErrorString(e_)};    \
+  } while (0)
+
+template <typename F>
+int guarded(F&& f) {
+  try {
+    f();
+    return VPINN_OK;
+  } catch (const Fail& e) {
+    g_err = e.msg;
+    return e.code;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return VPINN_ERR_NUMERIC;
+  }
+}
+
+template <typename T>
+struct DBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  DBuf() = default;
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+  ~DBuf() { release(); }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+  // 64 bytes of slack: 1-D bulk copies read 16-byte aligned supersets
+  void alloc(size_t count) {
+    release();
+    n = count;
+    CK(cudaMalloc(&p, std::max<size_t>(count, 1) * sizeof(T) + 64));
+    CK(cudaMemset(p, 0, std::max<size_t>(count, 1) * sizeof(T) + 64));
+  }
+  void upload(const T* h, size_t count, cudaStream_t s) {
+    if (count) CK(cudaMemcpyAsync(p, h, count * sizeof(T), cudaMemcpyHostToDevice, s));
+  }
+};
+
+// ---------------------------------------------------------------------------
+// kernel variants: (hidden width H, hidden layers D, output channels C), each
+// instantiated in its own translation unit (variant_H_D_C.cu)
+using vpg::Variant;
+const std::vector<Variant>& variants() {
+#define VPG_ITEM(H, D, C) vpg::variant_##H##_##D##_##C(),
+  static const std::vector<Variant> v = {VPG_VARIANTS(VPG_ITEM)};
+#undef VPG_ITEM
+  return v;
+}
+
+// ---------------------------------------------------------------------------
+// NCCL through dlopen: no link-time dependency, reuses a libnccl already
+// loaded into the process (e.g. by torch) when there is one.
+struct NcclUid {
+  char b[NCCL_UNIQUE_ID_BYTES];
+};
+struct NcclApi {
+  void* h = nullptr;
+  ncclResult_t (*get_unique_id)(NcclUid*) = nullptr;
+  ncclResult_t (*comm_init_rank)(void**, int, NcclUid, int) = nullptr;
+  ncclResult_t (*all_reduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, void*,
+                             cudaStream_t) = nullptr;
+  ncclResult_t (*comm_destroy)(void*) = nullptr;
+  const char* (*get_error)(ncclResult_t) = nullptr;
+};
+NcclApi& nccl() {
+  static NcclApi api;
+  if (!api.h) {
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) throw Fail{VPINN_ERR_DEVICE, std::string("cannot load libnccl: ") + dlerror()};
+    api.get_unique_id = reinterpret_cast<decltype(api.get_unique_id)>(dlsym(h, "ncclGetUniqueId"));
+    api.comm_init_rank = reinterpret_cast<decltype(api.comm_init_rank)>(dlsym(h, "ncclCommInitRank"));
+    api.all_reduce = reinterpret_cast<decltype(api.all_reduce)>(dlsym(h, "ncclAllReduce"));
+    api.comm_destroy = reinterpret_cast<decltype(api.comm_destroy)>(dlsym(h, "ncclCommDestroy"));
+    api.get_error = reinterpret_cast<decltype(api.get_error)>(dlsym(h, "ncclGetErrorString"));
+    if (!api.get_unique_id || !api.comm_init_rank || !api.all_reduce || !api.comm_destroy)
+      throw Fail{VPINN_ERR_DEVICE, "libnccl lacks the required symbols"};
+    api.h = h;
+  }
+  return api;
+}
+#define NK(x)                                                                         \
+  do {                                                                                \
+    ncclResult_t r_ = (x);                                                            \
+    if (r_ != ncclSuccess)                                                            \
+      throw Fail{VPINN_ERR_DEVICE, std::string("nccl: ") +                            \
+                                       (nccl().get_error ? nccl().get_error(r_) : "?")}; \
+  } while (0)
+
+inline int ceil_div(long long a, long long b) { return (int)((a + b - 1) / b); }
+inline int round4(int x) { return (x + 3) & ~3; }
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+struct vpinn_gpu_ctx {
+  int device = 0;
+  int sm_count = 0;
+  cudaStream_t stream = nullptr;
+  Variant var{};
+  vpg::NetDesc net{};
+  int n_params = 0;
+  // problem (local partition)
+  int E = 0, T = 0, Q = 0, nt = 2;
+  int n_int = 0, n_bnd = 0, n_sen = 0;
+  long long nb_global = 0, ns_global = 0;
+  float eps = 1, bx = 0, by = 0;
+  int eps_source = 0, eps_idx = 0;
+  double tau = 10, gamma = 10;
+  DBuf<float> tens[3], forcing, bval, sval;
+  DBuf<float2> pts;
+  // parameters / optimiser
+  DBuf<float> params, m, v;
+  // per-CTA partials and the reduced vector [grad | loss words]
+  DBuf<float> grad_part;
+  DBuf<double> loss_part, red;
+  int grad_rows = 0, loss_rows = 0;
+  // trainer
+  DBuf<vpg::TrainState> st;
+  DBuf<vpg::StepRecord> rec;
+  DBuf<float> lr_tab, c1_tab, c2_tab;
+  int* h_flag = nullptr;  // pinned
+  // step configuration
+  bool split = false;
+  vpg::StepArgs sargs{};  // template (fused or reverse)
+  int grid_step = 0;
+  size_t smem_step = 0;
+  // split path
+  DBuf<float> fu, fux, fuy, feps, uxb, uyb, eb, ub, e_scalar;
+  vpg::ContractArgs cargs{};
+  int grid_contract = 0, grid_pen = 0, grid_fwd = 0;
+  size_t smem_contract = 0, smem_fwd = 0;
+  // graphs
+  std::map<std::tuple<int, int, double>, cudaGraphExec_t> graphs;
+  // nccl
+  void* comm = nullptr;
+  int nranks = 1, rank = 0;
+  long long launches = 0;
+  bool adam_fresh = true;
+
+  ~vpinn_gpu_ctx() {
+    if (device >= 0) cudaSetDevice(device);
+    for (auto& kv : graphs) cudaGraphExecDestroy(kv.second);
+    if (comm && nccl().comm_destroy) nccl().comm_destroy(comm);
+    if (h_flag) cudaFreeHost(h_flag);
+    if (stream) cudaStreamDestroy(stream);
+  }
+};
+
+namespace {
+
+void set_dev(vpinn_gpu_ctx* c) { CK(cudaSetDevice(c->device)); }
+
+void configure(vpinn_gpu_ctx* c) {
+  // ---- fused path when a cell fits a CTA, split path otherwise ----
+  const int P_local = c->n_int + c->n_bnd + c->n_sen;
+  c->split = c->Q > vpg::kThreads;
+  const Variant& V = c->var;
+  vpg::StepArgs& a = c->sargs;
+  std::memset(&a, 0, sizeof(a));
+  for (int t = 0; t < 3; ++t) a.tens[t] = c->tens[t].p;
+  a.forcing = c->forcing.p;
+  a.E = c->E;
+  a.T = c->T;
+  a.Q = c->Q;
+  a.nt = c->nt;
+  a.pts = c->pts.p;
+  a.n_int = c->n_int;
+  a.n_bnd = c->n_bnd;
+  a.n_sen = c->n_sen;
+  a.bval = c->bval.p;
+  a.sval = c->sval.p;
+  a.eps = c->eps;
+  a.bx = c->bx;
+  a.by = c->by;
+  a.eps_source = c->eps_source;
+  a.eps_scalar_index = c->eps_idx;
+  a.inv_nt = 1.0f / (float)c->T;
+  a.rscale = (2.0f * 1.0f) * a.inv_nt;
+  a.bscale = c->nb_global ? 2.0f * (float)c->tau / (float)c->nb_global : 0.0f;
+  a.sscale = c->ns_global ? 2.0f * (float)c->gamma / (float)c->ns_global : 0.0f;
+  a.net = c->net;
+  a.params = c->params.p;
+
+  const size_t two_cta = 113 * 1024;
+  int occ = 0;
+  if (!c->split) {
+    a.cells_per_tile = std::max(1, vpg::kThreads / c->Q);
+    a.n_int_tiles = c->E ? ceil_div(c->E, a.cells_per_tile) : 0;
+    a.n_tiles = a.n_int_tiles + ceil_div(c->n_bnd + c->n_sen, vpg::kThreads);
+    const int tile_rows = a.cells_per_tile * c->T;
+    const size_t min_smem = V.smem(V.rev_need, 1);
+    const size_t budget = min_smem <= two_cta ? two_cta : (size_t)227 * 1024;
+    int rows = (tile_rows + 1) / 2;
+    for (;;) {
+      const int tstride = round4(rows * c->Q + 8);
+      const int stage = c->nt * tstride;
+      const int uni = std::max(V.rev_need, 2 * stage);
+      if (V.smem(uni, rows) <= budget || rows == 1) {
+        a.chunk_rows = rows;
+        a.tstride = tstride;
+        a.stage_floats = stage;
+        a.union_floats = uni;
+        break;
+      }
+      rows = std::max(1, rows * 3 / 4);
+    }
+    c->smem_step = V.smem(a.union_floats, a.chunk_rows);
+    if (c->smem_step > (size_t)227 * 1024)
+      throw Fail{VPINN_ERR_CONFIG, "fused step kernel does not fit shared memory"};
+    CK(cudaFuncSetAttribute(V.fused, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem_step));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, V.fused, vpg::kThreads, c->smem_step));
+    if (occ < 1) throw Fail{VPINN_ERR_DEVICE, "fused step kernel cannot be resident"};
+    c->grid_step = std::max(1, std::min(a.n_tiles, occ * c->sm_count));
+    c->grad_rows = c->grid_step;
+    c->loss_rows = c->grid_step;
+  } else {
+    // reverse kernel over all local points
+    a.n_tiles = ceil_div(P_local, vpg::kThreads);
+    a.chunk_rows = 1;
+    a.union_floats = V.rev_need;
+    c->smem_step = V.smem(a.union_floats, 1);
+    CK(cudaFuncSetAttribute(V.reverse, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem_step));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, V.reverse, vpg::kThreads, c->smem_step));
+    if (occ < 1) throw Fail{VPINN_ERR_DEVICE, "reverse kernel cannot be resident"};
+    c->grid_step = std::max(1, std::min(a.n_tiles, occ * c->sm_count));
+    c->grad_rows = c->grid_step;
+  }
+
+  // ---- forward kernel (evaluate; split-path first stage) ----
+  c->smem_fwd = V.smem(0, 1);
+  CK(cudaFuncSetAttribute(V.forward, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem_fwd));
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, V.forward, vpg::kThreads, c->smem_fwd));
+  c->grid_fwd = std::max(1, occ) * c->sm_count;
+
+  // ---- standalone contraction (split path, roofline) ----
+  {
+    vpg::ContractArgs& ca = c->cargs;
+    std::memset(&ca, 0, sizeof(ca));
+    for (int t = 0; t < 3; ++t) ca.tens[t] = c->tens[t].p;
+    ca.forcing = c->forcing.p;
+    ca.E = c->E;
+    ca.T = c->T;
+    ca.Q = c->Q;
+    ca.nt = c->nt;
+    ca.e_fixed = c->eps;
+    ca.eps_source = c->eps_source;
+    ca.bx = c->bx;
+    ca.by = c->by;
+    ca.rscale = a.rscale;
+    ca.inv_nt = a.inv_nt;
+    ca.cells_per_tile = std::max(1, std::min(1024, 1024 / std::max(1, c->Q)));
+    ca.cells_per_tile = std::max(1, std::min(ca.cells_per_tile, c->E));
+    ca.n_tiles = c->E ? ceil_div(c->E, ca.cells_per_tile) : 0;
+    ca.pmax = ca.cells_per_tile * c->Q;
+    ca.nstage = 4;
+    const size_t fixed = vpg::contract_smem_bytes(ca.pmax, 0, 0, ca.nstage);
+    const size_t ring_budget = fixed < 200 * 1024 ? 200 * 1024 - fixed : 16 * 1024;
+    const size_t stage_bytes = ring_budget / ca.nstage;
+    ca.chunk_rows = (int)std::max<size_t>(1, stage_bytes / ((size_t)c->nt * (c->Q * 4 + 32)));
+    ca.chunk_rows = std::min(ca.chunk_rows, ca.cells_per_tile * c->T);
+    ca.tstride = round4(ca.chunk_rows * c->Q + 8);
+    ca.stage_floats = c->nt * ca.tstride;
+    c->smem_contract = vpg::contract_smem_bytes(ca.pmax, ca.chunk_rows, ca.stage_floats, ca.nstage);
+    if (c->smem_contract > (size_t)227 * 1024) {
+      ca.nstage = 2;
+      c->smem_contract = vpg::contract_smem_bytes(ca.pmax, ca.chunk_rows, ca.stage_floats, ca.nstage);
+    }
+    if (c->smem_contract > (size_t)227 * 1024)
+      throw Fail{VPINN_ERR_CONFIG, "contraction kernel does not fit shared memory"};
+    CK(cudaFuncSetAttribute(vpg::contract_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)c->smem_contract));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, vpg::contract_kernel, vpg::kCThreads,
+                                                     c->smem_contract));
+    c->grid_contract = std::max(1, std::min(std::max(1, ca.n_tiles), std::max(1, occ) * c->sm_count));
+    c->grid_pen = (c->n_bnd + c->n_sen) ? std::min(64, ceil_div(c->n_bnd + c->n_sen, 256)) : 0;
+  }
+  if (c->split) c->loss_rows = c->grid_contract + c->grid_pen + c->grid_step;
+
+  // ---- buffers sized by the grids ----
+  c->grad_part.alloc((size_t)c->grad_rows * c->n_params);
+  c->loss_part.alloc((size_t)std::max(c->loss_rows, c->grid_contract) * vpg::kLpWords);
+  c->red.alloc((size_t)c->n_params + vpg::kLpWords);
+  a.grad_part = c->grad_part.p;
+  if (c->split) {
+    const size_t ni = (size_t)c->n_int;
+    c->fu.alloc(P_local);
+    c->fux.alloc(P_local);
+    c->fuy.alloc(P_local);
+    c->feps.alloc(P_local);
+    c->uxb.alloc(ni);
+    c->uyb.alloc(ni);
+    c->eb.alloc(ni);
+    c->ub.alloc((size_t)c->n_bnd + c->n_sen);
+    a.loss_part = c->loss_part.p + (size_t)(c->grid_contract + c->grid_pen) * vpg::kLpWords;
+    a.in_ub = c->ub.p;
+    a.in_uxb = c->uxb.p;
+    a.in_uyb = c->uyb.p;
+    a.in_eb = c->eb.p;
+  } else {
+    a.loss_part = c->loss_part.p;
+  }
+  c->e_scalar.alloc(1);
+}
+
+// ---- one epoch: loss + gradient (+ Adam) enqueued on the context stream ----
+void enqueue_grad(vpinn_gpu_ctx* c, const int* stop) {
+  const Variant& V = c->var;
+  vpg::StepArgs a = c->sargs;
+  a.stop_flag = stop;
+  if (!c->split) {
+    V.fused<<<c->grid_step, vpg::kThreads, c->smem_step, c->stream>>>(a);
+    CK(cudaGetLastError());
+    c->launches += 1;
+  } else {
+    const int P_local = c->n_int + c->n_bnd + c->n_sen;
+    vpg::StepArgs f = a;
+    f.fwd_pts = c->pts.p;
+    f.n_fwd = P_local;
+    f.out_u = c->fu.p;
+    f.out_ux = c->fux.p;
+    f.out_uy = c->fuy.p;
+    f.out_eps = c->feps.p;
+    f.union_floats = 0;
+    const int grid_f = std::max(1, std::min(c->grid_fwd, ceil_div(P_local, vpg::kThreads)));
+    V.forward<<<grid_f, vpg::kThreads, c->smem_fwd, c->stream>>>(f);
+    CK(cudaGetLastError());
+    vpg::ContractArgs ca = c->cargs;
+    ca.ux = c->fux.p;
+    ca.uy = c->fuy.p;
+    ca.eps = c->feps.p;
+    ca.uxb = c->uxb.p;
+    ca.uyb = c->uyb.p;
+    ca.eb = c->eb.p;
+    ca.e_param = c->params.p + c->net.scal_off + c->eps_idx;
+    ca.loss_part = c->loss_part.p;
+    ca.stop_flag = stop;
+    c->launches += 1;
+    if (ca.n_tiles > 0) {
+      vpg::contract_kernel<<<c->grid_contract, vpg::kCThreads, c->smem_contract, c->stream>>>(ca);
+      CK(cudaGetLastError());
+      c->launches += 1;
+    }
+    if (c->grid_pen) {
+      vpg::penalty_kernel<<<c->grid_pen, 256, 0, c->stream>>>(
+          c->fu.p + c->n_int, c->n_bnd, c->n_sen, c->bval.p, c->sval.p, a.bscale, a.sscale,
+          c->ub.p, c->loss_part.p + (size_t)c->grid_contract * vpg::kLpWords, stop);
+      CK(cudaGetLastError());
+      c->launches += 1;
+    }
+    V.reverse<<<c->grid_step, vpg::kThreads, c->smem_step, c->stream>>>(a);
+    CK(cudaGetLastError());
+    c->launches += 1;
+  }
+  vpg::reduce_kernel<<<ceil_div(c->n_params, 32) + 1, 256, 0, c->stream>>>(
+      c->grad_part.p, c->grad_rows, c->n_params, c->loss_part.p, c->loss_rows, c->red.p, stop);
+  CK(cudaGetLastError());
+  c->launches += 1;
+  if (c->comm)
+    NK(nccl().all_reduce(c->red.p, c->red.p, (size_t)c->n_params + vpg::kLpWords, ncclFloat64,
+                         ncclSum, c->comm, c->stream));
+}
+
+vpg::AdamArgs adam_args(vpinn_gpu_ctx* c, bool tables, float lr_const, bool records,
+                        int rec_cap) {
+  vpg::AdamArgs aa{};
+  aa.red = c->red.p;
+  aa.n_params = c->n_params;
+  aa.params = c->params.p;
+  aa.m = c->m.p;
+  aa.v = c->v.p;
+  aa.st = c->st.p;
+  aa.lr_tab = tables ? c->lr_tab.p : nullptr;
+  aa.c1_tab = tables ? c->c1_tab.p : nullptr;
+  aa.c2_tab = tables ? c->c2_tab.p : nullptr;
+  aa.lr_const = lr_const;
+  aa.rec = records ? c->rec.p : nullptr;
+  aa.rec_cap = rec_cap;
+  aa.n_bnd = (double)c->nb_global;
+  aa.n_sen = (double)c->ns_global;
+  aa.tau_f = (float)c->tau;
+  aa.gamma_f = (float)c->gamma;
+  aa.eps_grad_slot = c->eps_source == VPINN_EPS_SCALAR ? c->net.scal_off + c->eps_idx : -1;
+  return aa;
+}
+
+void enqueue_epoch(vpinn_gpu_ctx* c, const vpg::AdamArgs& aa) {
+  enqueue_grad(c, &c->st.p->stopped);
+  vpg::adam_kernel<<<1, 1024, 0, c->stream>>>(aa);
+  CK(cudaGetLastError());
+  c->launches += 1;
+}
+
+void reset_state(vpinn_gpu_ctx* c, long long iterations, const vpinn_gpu_train_spec* spec) {
+  vpg::TrainState s{};
+  s.step = 0;
+  s.iterations = iterations;
+  s.stopped = 0;
+  s.stop_reason = 0;
+  s.best_loss = std::numeric_limits<double>::infinity();
+  s.best_step = 0;
+  s.tracks_eps = c->eps_source == VPINN_EPS_SCALAR;
+  s.eps_slot = c->net.scal_off + c->eps_idx;
+  if (spec) {
+    s.has_eps_tol = spec->has_eps_abs_tol;
+    s.has_eps_actual = spec->has_eps_actual;
+    s.has_loss_tol = spec->has_loss_tol;
+    s.eps_abs_tol = spec->eps_abs_tol;
+    s.eps_actual = spec->eps_actual;
+    s.loss_tol = spec->loss_tol;
+    s.plateau_window = spec->plateau_window;
+  }
+  CK(cudaMemcpyAsync(c->st.p, &s, sizeof(s), cudaMemcpyHostToDevice, c->stream));
+  CK(cudaMemsetAsync(c->m.p, 0, sizeof(float) * c->n_params, c->stream));
+  CK(cudaMemsetAsync(c->v.p, 0, sizeof(float) * c->n_params, c->stream));
+  vpg::mark_start_kernel<<<1, 1, 0, c->stream>>>(c->st.p);
+  CK(cudaGetLastError());
+}
+
+cudaGraphExec_t graph_for(vpinn_gpu_ctx* c, int kind, int steps, double lr, bool tables,
+                          int rec_cap) {
+  auto key = std::make_tuple(kind, steps, lr);
+  auto it = c->graphs.find(key);
+  if (it != c->graphs.end()) return it->second;
+  const vpg::AdamArgs aa = adam_args(c, tables, (float)lr, tables, rec_cap);
+  cudaGraph_t g;
+  CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+  const long long before = c->launches;
+  for (int s = 0; s < steps; ++s) enqueue_epoch(c, aa);
+  c->launches = before;  // counted at replay
+  CK(cudaStreamEndCapture(c->stream, &g));
+  cudaGraphExec_t ex;
+  CK(cudaGraphInstantiate(&ex, g, 0));
+  cudaGraphDestroy(g);
+  c->graphs[key] = ex;
+  return ex;
+}
+
+long long launches_per_epoch(const vpinn_gpu_ctx* c) {
+  long long n = 3;  // step kernel(s) + reduce + adam
+  if (c->split) n = 2 + 2 + (c->cargs.n_tiles > 0) + (c->grid_pen > 0);
+  return n;
+}
+
+}  // namespace
+
+// ===========================================================================
+extern "C" {
+
+const char* vpinn_gpu_last_error(void) { return g_err.c_str(); }
+
+const char* vpinn_gpu_version(void) { return "vpinn-b200 0.1 (sm_100a)"; }
+
+int vpinn_gpu_device_ok(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || n < 1) {
+    cudaGetLastError();
+    return 0;
+  }
+  cudaDeviceProp p;
+  if (cudaGetDeviceProperties(&p, 0) != cudaSuccess) return 0;
+  return p.major == 10 ? 1 : 0;
+}
+
+int vpinn_gpu_create(const vpinn_gpu_problem* pb, vpinn_gpu_ctx** out) {
+  if (out) *out = nullptr;
+  return guarded([&] {
+    if (!pb || !out) throw Fail{VPINN_ERR_CONFIG, "vpinn_gpu_create: null argument"};
+    // ---- validation (contract checks of losses.hpp:70-84, network.hpp:66-76) ----
+    if (pb->n_elem < 1 || pb->n_test < 1 || pb->n_quad < 1)
+      throw Fail{VPINN_ERR_CONFIG, "n_elem, n_test, n_quad must be >= 1"};
+    if (!pb->grad_x || !pb->grad_y || !pb->forcing || !pb->points)
+      throw Fail{VPINN_ERR_NUMERIC, "tensor kernel: tensors/forcing/points missing"};
+    if (pb->n_interior != (int64_t)pb->n_elem * pb->n_quad)
+      throw Fail{VPINN_ERR_NUMERIC, "evaluation does not cover the interior quadrature points"};
+    if (pb->n_layer_sizes < 3 || pb->n_layer_sizes > vpg::kMaxLayers)
+      throw Fail{VPINN_ERR_CONFIG, "layer_sizes: need [2, hidden..., n_out]"};
+    std::vector<int> sizes(pb->layer_sizes, pb->layer_sizes + pb->n_layer_sizes);
+    if (sizes.front() != 2) throw Fail{VPINN_ERR_CONFIG, "init_network: input dimension must be 2"};
+    for (int s : sizes)
+      if (s < 1) throw Fail{VPINN_ERR_CONFIG, "init_network: layer sizes must be >= 1"};
+    const int D = (int)sizes.size() - 2, C = sizes.back();
+    int maxH = 0;
+    for (int l = 1; l <= D; ++l) maxH = std::max(maxH, sizes[l]);
+    if (pb->eps_source == VPINN_EPS_SPATIAL && C < 2)
+      throw Fail{VPINN_ERR_NUMERIC, "spatial coefficient requested but the network has no positive head"};
+    if (pb->eps_source == VPINN_EPS_SCALAR &&
+        (pb->eps_scalar_index < 0 || pb->eps_scalar_index >= pb->n_scalars))
+      throw Fail{VPINN_ERR_NUMERIC, "coefficient scalar index out of range"};
+    if (pb->activation != VPINN_ACT_TANH && pb->activation != VPINN_ACT_SIGMOID)
+      throw Fail{VPINN_ERR_CONFIG, "activation must be tanh or sigmoid"};
+    const Variant* var = nullptr;
+    for (const auto& v : variants())
+      if (v.D == D && v.C == C && v.H >= maxH && (!var || v.H < var->H)) var = &v;
+    if (!var)
+      throw Fail{VPINN_ERR_CONFIG, "network shape not instantiated for the GPU path (hidden layers " +
+                                       std::to_string(D) + ", width " + std::to_string(maxH) +
+                                       ", outputs " + std::to_string(C) + ")"};
+    const bool conv = pb->bx != 0.0f || pb->by != 0.0f;
+    if (conv && !pb->test) throw Fail{VPINN_ERR_NUMERIC, "convection needs the test tensor"};
+    const int W = std::max(1, pb->world_size), R = pb->rank;
+    if (R < 0 || R >= W) throw Fail{VPINN_ERR_CONFIG, "rank out of range"};
+
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev < 1) {
+      cudaGetLastError();
+      throw Fail{VPINN_ERR_DEVICE, "no CUDA device: the B200 path has no CPU fallback"};
+    }
+    if (pb->device < 0 || pb->device >= ndev) throw Fail{VPINN_ERR_DEVICE, "device ordinal out of range"};
+
+    auto c = std::make_unique<vpinn_gpu_ctx>();
+    c->device = pb->device;
+    set_dev(c.get());
+    cudaDeviceProp prop;
+    CK(cudaGetDeviceProperties(&prop, c->device));
+    if (prop.major != 10)
+      throw Fail{VPINN_ERR_DEVICE, std::string("device ") + prop.name + " is not sm_100 (B200)"};
+    c->sm_count = prop.multiProcessorCount;
+    CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    CK(cudaMallocHost(&c->h_flag, sizeof(int) * 4));
+    c->var = *var;
+
+    // ---- network descriptor (network.hpp:98-128 offsets) ----
+    vpg::NetDesc& nd = c->net;
+    std::memset(&nd, 0, sizeof(nd));
+    nd.n_layers = (int)sizes.size() - 1;
+    int off = 0;
+    for (int l = 0; l < nd.n_layers; ++l) {
+      nd.in_w[l] = sizes[l];
+      nd.out_w[l] = sizes[l + 1];
+      nd.w_off[l] = off;
+      off += sizes[l + 1] * sizes[l];
+      nd.b_off[l] = off;
+      off += sizes[l + 1];
+    }
+    nd.scal_off = off;
+    nd.n_params = off + pb->n_scalars;
+    nd.sigmoid = pb->activation == VPINN_ACT_SIGMOID;
+    c->n_params = nd.n_params;
+
+    // ---- partition (rank r owns contiguous cells / penalty points) ----
+    const long long E = pb->n_elem, NB = pb->n_boundary, NS = pb->n_sensors;
+    const long long e0 = E * R / W, e1 = E * (R + 1) / W;
+    const long long b0 = NB * R / W, b1 = NB * (R + 1) / W;
+    const long long s0 = NS * R / W, s1 = NS * (R + 1) / W;
+    c->E = (int)(e1 - e0);
+    c->T = pb->n_test;
+    c->Q = pb->n_quad;
+    c->nt = conv ? 3 : 2;
+    c->n_int = (int)((e1 - e0) * pb->n_quad);
+    c->n_bnd = (int)(b1 - b0);
+    c->n_sen = (int)(s1 - s0);
+    c->nb_global = NB;
+    c->ns_global = NS;
+    c->eps = pb->eps;
+    c->bx = pb->bx;
+    c->by = pb->by;
+    c->eps_source = pb->eps_source;
+    c->eps_idx = pb->eps_scalar_index;
+    c->tau = pb->tau;
+    c->gamma = pb->gamma;
+    c->rank = R;
+    c->nranks = W;
+
+    const size_t TQ = (size_t)c->T * c->Q;
+    const float* src[3] = {pb->grad_x, pb->grad_y, pb->test};
+    for (int t = 0; t < c->nt; ++t) {
+      c->tens[t].alloc(TQ * c->E);
+      c->tens[t].upload(src[t] + TQ * e0, TQ * c->E, c->stream);
+    }
+    c->forcing.alloc((size_t)c->T * c->E);
+    c->forcing.upload(pb->forcing + (size_t)c->T * e0, (size_t)c->T * c->E, c->stream);
+    // points: cast double -> Real exactly like points_to_matrix (network.hpp:376-384)
+    std::vector<float2> hp;
+    hp.reserve((size_t)c->n_int + c->n_bnd + c->n_sen);
+    auto push = [&](long long i) {
+      hp.push_back(make_float2((float)pb->points[2 * i], (float)pb->points[2 * i + 1]));
+    };
+    for (long long i = e0 * pb->n_quad; i < e1 * pb->n_quad; ++i) push(i);
+    for (long long i = b0; i < b1; ++i) push(pb->n_interior + i);
+    for (long long i = s0; i < s1; ++i) push(pb->n_interior + NB + i);
+    c->pts.alloc(hp.size());
+    c->pts.upload(hp.data(), hp.size(), c->stream);
+    std::vector<float> bv, sv;
+    for (long long i = b0; i < b1; ++i) bv.push_back((float)pb->boundary_values[i]);
+    for (long long i = s0; i < s1; ++i) sv.push_back((float)pb->sensor_values[i]);
+    c->bval.alloc(bv.size());
+    c->bval.upload(bv.data(), bv.size(), c->stream);
+    c->sval.alloc(sv.size());
+    c->sval.upload(sv.data(), sv.size(), c->stream);
+
+    c->params.alloc(c->n_params);
+    c->m.alloc(c->n_params);
+    c->v.alloc(c->n_params);
+    c->st.alloc(1);
+    configure(c.get());
+    reset_state(c.get(), LLONG_MAX, nullptr);
+    CK(cudaStreamSynchronize(c->stream));
+    *out = c.release();
+  });
+}
+
+void vpinn_gpu_destroy(vpinn_gpu_ctx* ctx) { delete ctx; }
+
+int vpinn_gpu_param_count(const vpinn_gpu_ctx* ctx) { return ctx ? ctx->n_params : -1; }
+
+int vpinn_gpu_set_params(vpinn_gpu_ctx* c, const float* p, int n) {
+  return guarded([&] {
+    if (n != c->n_params) throw Fail{VPINN_ERR_NUMERIC, "from_parameters: size mismatch"};
+    set_dev(c);
+    CK(cudaMemcpyAsync(c->params.p, p, sizeof(float) * n, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+  });
+}
+
+int vpinn_gpu_get_params(vpinn_gpu_ctx* c, float* p, int n) {
+  return guarded([&] {
+    if (n != c->n_params) throw Fail{VPINN_ERR_NUMERIC, "to_parameters: size mismatch"};
+    set_dev(c);
+    CK(cudaMemcpyAsync(p, c->params.p, sizeof(float) * n, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+  });
+}
+
+int vpinn_gpu_loss_and_grad(vpinn_gpu_ctx* c, double* loss_parts, double* grad) {
+  return guarded([&] {
+    set_dev(c);
+    enqueue_grad(c, nullptr);
+    std::vector<double> red(c->n_params + vpg::kLpWords);
+    CK(cudaMemcpyAsync(red.data(), c->red.p, sizeof(double) * red.size(), cudaMemcpyDeviceToHost,
+                       c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    const double* lw = red.data() + c->n_params;
+    if (lw[vpg::kLpBad] != 0.0)
+      throw Fail{VPINN_ERR_NUMERIC, "evaluate: non-finite network output"};
+    const float Lv = (float)lw[vpg::kLpVar];
+    const float Lb = c->nb_global ? (float)(lw[vpg::kLpBnd] / (double)c->nb_global) : 0.0f;
+    const float Ls = c->ns_global ? (float)(lw[vpg::kLpSen] / (double)c->ns_global) : 0.0f;
+    if (loss_parts) {
+      loss_parts[0] = (double)(Lv + (float)c->tau * Lb + (float)c->gamma * Ls);
+      loss_parts[1] = lw[vpg::kLpVar];
+      loss_parts[2] = c->nb_global ? lw[vpg::kLpBnd] / (double)c->nb_global : 0.0;
+      loss_parts[3] = c->ns_global ? lw[vpg::kLpSen] / (double)c->ns_global : 0.0;
+    }
+    if (grad) {
+      for (int p = 0; p < c->n_params; ++p) grad[p] = red[p];
+      if (c->eps_source == VPINN_EPS_SCALAR) grad[c->net.scal_off + c->eps_idx] += lw[vpg::kLpEpsGrad];
+    }
+  });
+}
+
+int vpinn_gpu_adam_reset(vpinn_gpu_ctx* c) {
+  return guarded([&] {
+    set_dev(c);
+    reset_state(c, LLONG_MAX, nullptr);
+    CK(cudaStreamSynchronize(c->stream));
+  });
+}
+
+int vpinn_gpu_run_steps(vpinn_gpu_ctx* c, int n_steps, double lr) {
+  return guarded([&] {
+    set_dev(c);
+    if (n_steps <= 0) return;
+    const int chunk = std::min(n_steps, 64);
+    cudaGraphExec_t g = graph_for(c, 1, chunk, lr, false, 0);
+    int done = 0;
+    while (done + chunk <= n_steps) {
+      CK(cudaGraphLaunch(g, c->stream));
+      c->launches += launches_per_epoch(c) * chunk;
+      done += chunk;
+    }
+    if (done < n_steps) {
+      cudaGraphExec_t g2 = graph_for(c, 1, n_steps - done, lr, false, 0);
+      CK(cudaGraphLaunch(g2, c->stream));
+      c->launches += launches_per_epoch(c) * (n_steps - done);
+    }
+  });
+}
+
+int vpinn_gpu_synchronize(vpinn_gpu_ctx* c) {
+  return guarded([&] {
+    set_dev(c);
+    CK(cudaStreamSynchronize(c->stream));
+    vpg::TrainState s;
+    CK(cudaMemcpy(&s, c->st.p, sizeof(s), cudaMemcpyDeviceToHost));
+    if (s.stopped && s.stop_reason == 3)
+      throw Fail{VPINN_ERR_NUMERIC, "step " + std::to_string(s.abort_step) + ": non-finite gradient"};
+  });
+}
+
+int vpinn_gpu_time_steps(vpinn_gpu_ctx* c, int n_steps, double lr, double* ms_total) {
+  return guarded([&] {
+    set_dev(c);
+    cudaEvent_t e0, e1;
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    CK(cudaEventRecord(e0, c->stream));
+    if (vpinn_gpu_run_steps(c, n_steps, lr) != 0) throw Fail{VPINN_ERR_DEVICE, g_err};
+    CK(cudaEventRecord(e1, c->stream));
+    CK(cudaEventSynchronize(e1));
+    float ms = 0;
+    CK(cudaEventElapsedTime(&ms, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    *ms_total = ms;
+  });
+}
+
+int vpinn_gpu_train(vpinn_gpu_ctx* c, const vpinn_gpu_train_spec* spec,
+                    vpinn_gpu_step_record* records, vpinn_gpu_train_result* result) {
+  return guarded([&] {
+    if (!spec || spec->iterations < 1)
+      throw Fail{VPINN_ERR_CONFIG, "train: iterations must be >= 1"};
+    if (spec->lr_exponential && spec->every < 1)
+      throw Fail{VPINN_ERR_CONFIG, "lr_at: every must be >= 1"};
+    set_dev(c);
+    const long long iters = spec->iterations;
+    if (iters > INT_MAX / 2) throw Fail{VPINN_ERR_CONFIG, "train: iteration budget too large"};
+    // lr_at (trainer.hpp:73-78) and the bias corrections (trainer.hpp:49-52),
+    // double pow then cast, exactly as the reference computes them
+    std::vector<float> lr(iters), c1(iters), c2(iters);
+    for (long long t = 1; t <= iters; ++t) {
+      const double l = spec->lr_exponential
+                           ? spec->lr0 * std::pow(spec->decay, double((t - 1) / spec->every))
+                           : spec->lr0;
+      lr[t - 1] = (float)l;
+      c1[t - 1] = 1.0f - (float)std::pow(0.9, double(t));
+      c2[t - 1] = 1.0f - (float)std::pow(0.999, double(t));
+    }
+    c->lr_tab.alloc(iters);
+    c->c1_tab.alloc(iters);
+    c->c2_tab.alloc(iters);
+    c->lr_tab.upload(lr.data(), iters, c->stream);
+    c->c1_tab.upload(c1.data(), iters, c->stream);
+    c->c2_tab.upload(c2.data(), iters, c->stream);
+    c->rec.alloc(iters);
+    // tables were reallocated: drop graphs that captured the old pointers
+    for (auto it = c->graphs.begin(); it != c->graphs.end();) {
+      if (std::get<0>(it->first) == 2) {
+        cudaGraphExecDestroy(it->second);
+        it = c->graphs.erase(it);
+      } else {
+        ++it;
+      }
+    }
+    reset_state(c, iters, spec);
+    const int S = spec->steps_per_graph > 0 ? spec->steps_per_graph : 50;
+    const int per = (int)std::min<long long>(S, iters);
+    cudaGraphExec_t g = graph_for(c, 2, per, 0.0, true, (int)iters);
+    long long launched = 0;
+    int since_check = 0;
+    while (launched < iters) {
+      CK(cudaGraphLaunch(g, c->stream));
+      c->launches += launches_per_epoch(c) * per;
+      launched += per;
+      if (++since_check >= 20 && launched < iters) {
+        since_check = 0;
+        CK(cudaMemcpyAsync(c->h_flag, &c->st.p->stopped, sizeof(int), cudaMemcpyDeviceToHost,
+                           c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        if (*c->h_flag) break;
+      }
+    }
+    vpg::TrainState s;
+    CK(cudaMemcpyAsync(&s, c->st.p, sizeof(s), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    const long long ran = s.step;
+    if (records && ran > 0) {
+      std::vector<vpg::StepRecord> r(ran);
+      CK(cudaMemcpy(r.data(), c->rec.p, sizeof(vpg::StepRecord) * ran, cudaMemcpyDeviceToHost));
+      for (long long i = 0; i < ran; ++i) {
+        records[i].total = r[i].total;
+        records[i].variational = r[i].v;
+        records[i].boundary = r[i].b;
+        records[i].sensor = r[i].s;
+        records[i].lr = r[i].lr;
+        records[i].eps = r[i].eps;
+        records[i].seconds = r[i].seconds;
+      }
+    }
+    if (result) {
+      result->steps_run = ran;
+      result->converged = (s.stop_reason == 1 || s.stop_reason == 2) ? 1 : 0;
+      result->stop_reason = s.stop_reason == 3 ? 0 : s.stop_reason;
+      result->abort_step = s.stop_reason == 3 ? s.abort_step : 0;
+      result->final_eps = std::numeric_limits<double>::quiet_NaN();
+      if (c->eps_source == VPINN_EPS_SCALAR) {
+        float e = 0;
+        CK(cudaMemcpy(&e, c->params.p + c->net.scal_off + c->eps_idx, sizeof(float),
+                      cudaMemcpyDeviceToHost));
+        result->final_eps = e;
+      }
+    }
+    if (s.stop_reason == 3)
+      throw Fail{VPINN_ERR_NUMERIC, "step " + std::to_string(s.abort_step) +
+                                        ": non-finite network output or gradient"};
+  });
+}
+
+int vpinn_gpu_forward(vpinn_gpu_ctx* c, const double* points, int64_t n, int order, float* u,
+                      float* du_dx, float* du_dy, float* eps) {
+  return guarded([&] {
+    if (order < 0 || order > 1)
+      throw Fail{VPINN_ERR_CONFIG, "evaluate: order must be 0 or 1 on the GPU path"};
+    if (n <= 0) return;
+    set_dev(c);
+    std::vector<float2> hp(n);
+    for (int64_t i = 0; i < n; ++i) hp[i] = make_float2((float)points[2 * i], (float)points[2 * i + 1]);
+    DBuf<float2> dp;
+    DBuf<float> du, dux, duy, de;
+    dp.alloc(n);
+    du.alloc(n);
+    dux.alloc(n);
+    duy.alloc(n);
+    de.alloc(n);
+    dp.upload(hp.data(), n, c->stream);
+    vpg::StepArgs f = c->sargs;
+    f.fwd_pts = dp.p;
+    f.n_fwd = (int)n;
+    f.out_u = du.p;
+    f.out_ux = dux.p;
+    f.out_uy = duy.p;
+    f.out_eps = de.p;
+    f.union_floats = 0;
+    f.stop_flag = nullptr;
+    const int grid = std::max(1, std::min(c->grid_fwd, ceil_div(n, vpg::kThreads)));
+    c->var.forward<<<grid, vpg::kThreads, c->smem_fwd, c->stream>>>(f);
+    CK(cudaGetLastError());
+    c->launches += 1;
+    CK(cudaMemcpyAsync(u, du.p, sizeof(float) * n, cudaMemcpyDeviceToHost, c->stream));
+    if (order >= 1 && du_dx) CK(cudaMemcpyAsync(du_dx, dux.p, sizeof(float) * n, cudaMemcpyDeviceToHost, c->stream));
+    if (order >= 1 && du_dy) CK(cudaMemcpyAsync(du_dy, duy.p, sizeof(float) * n, cudaMemcpyDeviceToHost, c->stream));
+    if (eps && c->var.C >= 2) CK(cudaMemcpyAsync(eps, de.p, sizeof(float) * n, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    std::vector<float> chk(n);
+    // network.hpp:443-447: non-finite outputs are a numeric error
+    for (int64_t i = 0; i < n; ++i)
+      if (!std::isfinite(u[i]) || (order >= 1 && du_dx && !std::isfinite(du_dx[i])) ||
+          (order >= 1 && du_dy && !std::isfinite(du_dy[i])))
+        throw Fail{VPINN_ERR_NUMERIC, "evaluate: non-finite network output"};
+  });
+}
+
+int vpinn_gpu_contract(vpinn_gpu_ctx* c, const float* du_dx, const float* du_dy, const float* eps,
+                       const float* scalars, float weight, double* loss, float* residuals,
+                       float* du_dx_bar, float* du_dy_bar, float* eps_bar, double* scalar_bar) {
+  return guarded([&] {
+    set_dev(c);
+    if (c->eps_source == VPINN_EPS_SPATIAL && !eps)
+      throw Fail{VPINN_ERR_NUMERIC, "spatial coefficient requested but no eps given"};
+    if (c->eps_source == VPINN_EPS_SCALAR && !scalars)
+      throw Fail{VPINN_ERR_NUMERIC, "coefficient scalar index out of range"};
+    const size_t ni = (size_t)c->n_int;
+    DBuf<float> ux, uy, ep, oxb, oyb, oeb, res, es;
+    DBuf<double> lp;
+    ux.alloc(ni);
+    uy.alloc(ni);
+    ep.alloc(ni);
+    oxb.alloc(ni);
+    oyb.alloc(ni);
+    oeb.alloc(ni);
+    res.alloc((size_t)c->E * c->T);
+    es.alloc(1);
+    lp.alloc((size_t)c->grid_contract * vpg::kLpWords);
+    ux.upload(du_dx, ni, c->stream);
+    uy.upload(du_dy, ni, c->stream);
+    if (eps) ep.upload(eps, ni, c->stream);
+    if (scalars) es.upload(scalars + c->eps_idx, 1, c->stream);
+    vpg::ContractArgs ca = c->cargs;
+    ca.ux = ux.p;
+    ca.uy = uy.p;
+    ca.eps = ep.p;
+    ca.uxb = oxb.p;
+    ca.uyb = oyb.p;
+    ca.eb = oeb.p;
+    ca.res = res.p;
+    ca.e_param = es.p;
+    ca.rscale = (2.0f * weight) * ca.inv_nt;
+    ca.loss_part = lp.p;
+    ca.stop_flag = nullptr;
+    if (ca.n_tiles > 0) {
+      vpg::contract_kernel<<<c->grid_contract, vpg::kCThreads, c->smem_contract, c->stream>>>(ca);
+      CK(cudaGetLastError());
+      c->launches += 1;
+    }
+    std::vector<double> hl((size_t)c->grid_contract * vpg::kLpWords);
+    CK(cudaMemcpyAsync(hl.data(), lp.p, sizeof(double) * hl.size(), cudaMemcpyDeviceToHost, c->stream));
+    if (residuals) CK(cudaMemcpyAsync(residuals, res.p, sizeof(float) * c->E * c->T, cudaMemcpyDeviceToHost, c->stream));
+    if (du_dx_bar) CK(cudaMemcpyAsync(du_dx_bar, oxb.p, sizeof(float) * ni, cudaMemcpyDeviceToHost, c->stream));
+    if (du_dy_bar) CK(cudaMemcpyAsync(du_dy_bar, oyb.p, sizeof(float) * ni, cudaMemcpyDeviceToHost, c->stream));
+    if (eps_bar && c->eps_source == VPINN_EPS_SPATIAL)
+      CK(cudaMemcpyAsync(eps_bar, oeb.p, sizeof(float) * ni, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    double l = 0.0, g = 0.0;
+    for (int b = 0; b < c->grid_contract; ++b) {
+      l += hl[(size_t)b * vpg::kLpWords + vpg::kLpVar];
+      g += hl[(size_t)b * vpg::kLpWords + vpg::kLpEpsGrad];
+    }
+    if (loss) *loss = l;
+    if (scalar_bar && c->eps_source == VPINN_EPS_SCALAR) scalar_bar[c->eps_idx] = g;
+  });
+}
+
+int vpinn_gpu_time_contract(vpinn_gpu_ctx* c, int reps, double* ms_per_launch, double* bytes) {
+  return guarded([&] {
+    set_dev(c);
+    const size_t ni = (size_t)c->n_int;
+    DBuf<float> ux, uy, ep, oxb, oyb, oeb, es;
+    DBuf<double> lp;
+    ux.alloc(ni);
+    uy.alloc(ni);
+    ep.alloc(ni);
+    oxb.alloc(ni);
+    oyb.alloc(ni);
+    oeb.alloc(ni);
+    es.alloc(1);
+    lp.alloc((size_t)c->grid_contract * vpg::kLpWords);
+    vpg::ContractArgs ca = c->cargs;
+    ca.ux = ux.p;
+    ca.uy = uy.p;
+    ca.eps = ep.p;
+    ca.uxb = oxb.p;
+    ca.uyb = oyb.p;
+    ca.eb = oeb.p;
+    ca.res = nullptr;
+    ca.e_param = es.p;
+    ca.loss_part = lp.p;
+    ca.stop_flag = nullptr;
+    // L2 flush buffer (> 126 MB L2) between launches so each launch streams HBM
+    DBuf<char> flush;
+    flush.alloc((size_t)256 << 20);
+    cudaEvent_t e0, e1;
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    double total = 0.0;
+    for (int r = 0; r < reps + 2; ++r) {
+      CK(cudaMemsetAsync(flush.p, r & 0xff, (size_t)256 << 20, c->stream));
+      CK(cudaEventRecord(e0, c->stream));
+      vpg::contract_kernel<<<c->grid_contract, vpg::kCThreads, c->smem_contract, c->stream>>>(ca);
+      CK(cudaGetLastError());
+      CK(cudaEventRecord(e1, c->stream));
+      CK(cudaEventSynchronize(e1));
+      c->launches += 1;
+      float ms = 0;
+      CK(cudaEventElapsedTime(&ms, e0, e1));
+      if (r >= 2) total += ms;
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    *ms_per_launch = total / std::max(1, reps);
+    const double EQ = (double)c->E * c->Q;
+    double b = 4.0 * ((double)c->nt * c->E * c->T * c->Q + (double)c->E * c->T + 4.0 * EQ);
+    if (c->eps_source == VPINN_EPS_SPATIAL) b += 8.0 * EQ;
+    *bytes = b;
+  });
+}
+
+int vpinn_gpu_download_tensor(vpinn_gpu_ctx* c, int which, float* out, int64_t n) {
+  return guarded([&] {
+    set_dev(c);
+    const DBuf<float>* b = which <= 2 ? &c->tens[which] : &c->forcing;
+    if (which < 0 || which > 3) throw Fail{VPINN_ERR_CONFIG, "download: selector"};
+    if (which == 2 && c->nt < 3) throw Fail{VPINN_ERR_CONFIG, "download: no test tensor uploaded"};
+    if ((size_t)n != b->n) throw Fail{VPINN_ERR_CONFIG, "download: size mismatch"};
+    CK(cudaMemcpy(out, b->p, sizeof(float) * n, cudaMemcpyDeviceToHost));
+  });
+}
+
+int64_t vpinn_gpu_launch_count(const vpinn_gpu_ctx* c) { return c ? c->launches : -1; }
+
+int vpinn_gpu_profile_step(vpinn_gpu_ctx* c, int reps, double* ms_mlp, double* ms_reduce,
+                           double* ms_adam) {
+  return guarded([&] {
+    set_dev(c);
+    reset_state(c, LLONG_MAX, nullptr);
+    const vpg::AdamArgs aa = adam_args(c, false, 1e-4f, false, 0);
+    cudaEvent_t ev[4];
+    for (auto& e : ev) CK(cudaEventCreate(&e));
+    double t[3] = {0, 0, 0};
+    for (int r = 0; r < reps + 2; ++r) {
+      CK(cudaEventRecord(ev[0], c->stream));
+      // the step kernels (fused, or the split chain) then reduce: time separately
+      const Variant& V = c->var;
+      vpg::StepArgs a = c->sargs;
+      a.stop_flag = &c->st.p->stopped;
+      if (!c->split) {
+        V.fused<<<c->grid_step, vpg::kThreads, c->smem_step, c->stream>>>(a);
+        CK(cudaGetLastError());
+        c->launches += 1;
+        CK(cudaEventRecord(ev[1], c->stream));
+        vpg::reduce_kernel<<<ceil_div(c->n_params, 32) + 1, 256, 0, c->stream>>>(
+            c->grad_part.p, c->grad_rows, c->n_params, c->loss_part.p, c->loss_rows, c->red.p,
+            a.stop_flag);
+        CK(cudaGetLastError());
+        c->launches += 1;
+        if (c->comm)
+          NK(nccl().all_reduce(c->red.p, c->red.p, (size_t)c->n_params + vpg::kLpWords,
+                               ncclFloat64, ncclSum, c->comm, c->stream));
+      } else {
+        enqueue_grad(c, a.stop_flag);
+        CK(cudaEventRecord(ev[1], c->stream));
+      }
+      CK(cudaEventRecord(ev[2], c->stream));
+      vpg::adam_kernel<<<1, 1024, 0, c->stream>>>(aa);
+      CK(cudaGetLastError());
+      c->launches += 1;
+      CK(cudaEventRecord(ev[3], c->stream));
+      CK(cudaEventSynchronize(ev[3]));
+      if (r >= 2) {
+        float a1, a2, a3;
+        CK(cudaEventElapsedTime(&a1, ev[0], ev[1]));
+        CK(cudaEventElapsedTime(&a2, ev[1], ev[2]));
+        CK(cudaEventElapsedTime(&a3, ev[2], ev[3]));
+        t[0] += a1;
+        t[1] += a2;
+        t[2] += a3;
+      }
+    }
+    for (auto& e : ev) cudaEventDestroy(e);
+    *ms_mlp = t[0] / reps;
+    *ms_reduce = t[1] / reps;
+    *ms_adam = t[2] / reps;
+  });
+}
+
+int vpinn_gpu_nccl_unique_id(void* id128) {
+  return guarded([&] {
+    NcclUid u;
+    NK(nccl().get_unique_id(&u));
+    std::memcpy(id128, u.b, sizeof(u.b));
+  });
+}
+
+int vpinn_gpu_attach_comm(vpinn_gpu_ctx* c, const void* id128, int nranks, int rank) {
+  return guarded([&] {
+    if (nranks != c->nranks || rank != c->rank)
+      throw Fail{VPINN_ERR_CONFIG, "attach_comm: rank/world differ from the partition"};
+    set_dev(c);
+    NcclUid u;
+    std::memcpy(u.b, id128, sizeof(u.b));
+    void* comm = nullptr;
+    NK(nccl().comm_init_rank(&comm, nranks, u, rank));
+    c->comm = comm;
+    for (auto& kv : c->graphs) cudaGraphExecDestroy(kv.second);
+    c->graphs.clear();
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,180 @@
+"""Python handle over the C-ABI step (vpinn_gpu_*), numpy in / numpy out.
+
+This is the binding the tests and bench.py use; the reference-facing host
+side is the C++ layer in csrc/host (vpinn::gpu::train etc.).
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+from typing import Optional, Sequence
+
+import numpy as np
+
+from . import _capi
+
+EPS_FIXED, EPS_SCALAR, EPS_SPATIAL = 0, 1, 2
+
+
+def _p(a):
+    return None if a is None else a.ctypes.data_as(C.c_void_p)
+
+
+@dataclass
+class TrainReport:
+    records: np.ndarray  # structured: total, variational, boundary, sensor, lr, eps, seconds
+    steps_run: int
+    converged: bool
+    stop_reason: int
+    abort_step: int
+    final_eps: float
+
+
+class GpuStep:
+    """One device context: the uploaded ProblemAssembly + network parameters."""
+
+    def __init__(self, *, grad_x, grad_y, test, forcing, n_elem, n_test, n_quad, points,
+                 n_interior, n_boundary, n_sensors, boundary_values=None, sensor_values=None,
+                 layer_sizes: Sequence[int] = (2, 30, 30, 30, 1), sigmoid=False, n_scalars=0,
+                 eps=1.0, bx=0.0, by=0.0, eps_source=EPS_FIXED, eps_scalar_index=0,
+                 tau=10.0, gamma=10.0, device=0, rank=0, world_size=1):
+        L = _capi.lib()
+        f32 = lambda a: None if a is None else np.ascontiguousarray(a, dtype=np.float32)
+        f64 = lambda a: None if a is None else np.ascontiguousarray(a, dtype=np.float64)
+        self._keep = [f32(grad_x), f32(grad_y), f32(test), f32(forcing), f64(points),
+                      f64(boundary_values), f64(sensor_values),
+                      np.ascontiguousarray(layer_sizes, dtype=np.int32)]
+        gx, gy, tv, fc, pts, bv, sv, ls = self._keep
+        pb = _capi.Problem()
+        pb.n_elem, pb.n_test, pb.n_quad = n_elem, n_test, n_quad
+        pb.grad_x, pb.grad_y, pb.test, pb.forcing, pb.points = _p(gx), _p(gy), _p(tv), _p(fc), _p(pts)
+        pb.n_interior, pb.n_boundary, pb.n_sensors = n_interior, n_boundary, n_sensors
+        pb.boundary_values, pb.sensor_values = _p(bv), _p(sv)
+        pb.n_layer_sizes, pb.layer_sizes = len(ls), _p(ls)
+        pb.activation = 1 if sigmoid else 0
+        pb.n_scalars = n_scalars
+        pb.eps, pb.bx, pb.by = eps, bx, by
+        pb.eps_source, pb.eps_scalar_index = eps_source, eps_scalar_index
+        pb.tau, pb.gamma = tau, gamma
+        pb.device, pb.rank, pb.world_size = device, rank, world_size
+        h = C.c_void_p()
+        _capi.check(L.vpinn_gpu_create(C.byref(pb), C.byref(h)))
+        self.h = h
+        self.n_elem, self.n_test, self.n_quad = n_elem, n_test, n_quad
+        self.n_params = L.vpinn_gpu_param_count(h)
+        self.layer_sizes = tuple(layer_sizes)
+
+    def close(self):
+        if getattr(self, "h", None):
+            _capi.lib().vpinn_gpu_destroy(self.h)
+            self.h = None
+
+    __del__ = close
+
+    # ---- parameters ----
+    def set_params(self, p):
+        p = np.ascontiguousarray(p, dtype=np.float32)
+        _capi.check(_capi.lib().vpinn_gpu_set_params(self.h, _p(p), p.size))
+
+    def get_params(self):
+        p = np.zeros(self.n_params, dtype=np.float32)
+        _capi.check(_capi.lib().vpinn_gpu_get_params(self.h, _p(p), p.size))
+        return p
+
+    # ---- probes ----
+    def loss_and_grad(self):
+        parts = np.zeros(4)
+        g = np.zeros(self.n_params)
+        _capi.check(_capi.lib().vpinn_gpu_loss_and_grad(self.h, _p(parts), _p(g)))
+        return parts, g
+
+    def forward(self, points, order=1):
+        pts = np.ascontiguousarray(points, dtype=np.float64).reshape(-1, 2)
+        n = pts.shape[0]
+        u, ux, uy, e = (np.zeros(n, dtype=np.float32) for _ in range(4))
+        _capi.check(_capi.lib().vpinn_gpu_forward(self.h, _p(pts), n, order, _p(u), _p(ux), _p(uy), _p(e)))
+        return u, ux, uy, (e if self.layer_sizes[-1] >= 2 else None)
+
+    def contract(self, ux, uy, eps=None, scalars=None, weight=1.0):
+        ni = self.n_elem * self.n_quad
+        ux = np.ascontiguousarray(ux, dtype=np.float32)
+        uy = np.ascontiguousarray(uy, dtype=np.float32)
+        e = None if eps is None else np.ascontiguousarray(eps, dtype=np.float32)
+        sc = None if scalars is None else np.ascontiguousarray(scalars, dtype=np.float32)
+        loss = C.c_double()
+        res = np.zeros(self.n_elem * self.n_test, dtype=np.float32)
+        uxb = np.zeros(ni, dtype=np.float32)
+        uyb = np.zeros(ni, dtype=np.float32)
+        eb = np.zeros(ni, dtype=np.float32)
+        sb = np.zeros(max(1, 0 if scalars is None else len(scalars)))
+        _capi.check(_capi.lib().vpinn_gpu_contract(self.h, _p(ux), _p(uy), _p(e), _p(sc), weight,
+                                                   C.byref(loss), _p(res), _p(uxb), _p(uyb), _p(eb), _p(sb)))
+        return loss.value, res.reshape(self.n_elem, self.n_test), uxb, uyb, eb, sb
+
+    def download_tensor(self, which: int, n: int):
+        out = np.zeros(n, dtype=np.float32)
+        _capi.check(_capi.lib().vpinn_gpu_download_tensor(self.h, which, _p(out), n))
+        return out
+
+    # ---- training ----
+    def train(self, iterations, lr0=1e-3, lr_exponential=False, decay=0.99, every=1000,
+              eps_abs_tol=None, eps_actual=None, loss_tol=None, plateau_window=2000,
+              steps_per_graph=0) -> TrainReport:
+        s = _capi.TrainSpec()
+        s.iterations, s.lr_exponential, s.lr0, s.decay, s.every = iterations, int(lr_exponential), lr0, decay, every
+        s.has_eps_abs_tol, s.eps_abs_tol = int(eps_abs_tol is not None), eps_abs_tol or 0.0
+        s.has_eps_actual, s.eps_actual = int(eps_actual is not None), eps_actual or 0.0
+        s.has_loss_tol, s.loss_tol = int(loss_tol is not None), loss_tol or 0.0
+        s.plateau_window, s.steps_per_graph = plateau_window, steps_per_graph
+        recs = (_capi.StepRecord * iterations)()
+        res = _capi.TrainResult()
+        rc = _capi.lib().vpinn_gpu_train(self.h, C.byref(s), recs, C.byref(res))
+        arr = np.ctypeslib.as_array(recs)[: res.steps_run].copy() if res.steps_run else np.zeros(0)
+        rep = TrainReport(arr, res.steps_run, bool(res.converged), res.stop_reason, res.abort_step,
+                          res.final_eps)
+        if rc != 0:
+            err = _capi.VpinnError(rc, _capi.lib().vpinn_gpu_last_error().decode())
+            err.report = rep
+            raise err
+        return rep
+
+    def adam_reset(self):
+        _capi.check(_capi.lib().vpinn_gpu_adam_reset(self.h))
+
+    def run_steps(self, n, lr=1e-3):
+        _capi.check(_capi.lib().vpinn_gpu_run_steps(self.h, n, lr))
+
+    def synchronize(self):
+        _capi.check(_capi.lib().vpinn_gpu_synchronize(self.h))
+
+    def time_steps(self, n, lr=1e-3):
+        ms = C.c_double()
+        _capi.check(_capi.lib().vpinn_gpu_time_steps(self.h, n, lr, C.byref(ms)))
+        return ms.value
+
+    def time_contract(self, reps=20):
+        ms, b = C.c_double(), C.c_double()
+        _capi.check(_capi.lib().vpinn_gpu_time_contract(self.h, reps, C.byref(ms), C.byref(b)))
+        return ms.value, b.value
+
+    def profile_step(self, reps=10):
+        a, b, c = C.c_double(), C.c_double(), C.c_double()
+        _capi.check(_capi.lib().vpinn_gpu_profile_step(self.h, reps, C.byref(a), C.byref(b), C.byref(c)))
+        return a.value, b.value, c.value
+
+    def launch_count(self):
+        return _capi.lib().vpinn_gpu_launch_count(self.h)
+
+    def attach_comm(self, uid: bytes, nranks: int, rank: int):
+        buf = C.create_string_buffer(uid, 128)
+        _capi.check(_capi.lib().vpinn_gpu_attach_comm(self.h, buf, nranks, rank))
+
+
+def nccl_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    _capi.check(_capi.lib().vpinn_gpu_nccl_unique_id(buf))
+    return buf.raw
+
+
+def device_ok() -> bool:
+    return bool(_capi.lib().vpinn_gpu_device_ok())

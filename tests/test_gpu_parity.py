@@ -1,0 +1,156 @@
+"""GPU parity: the B200 C-ABI path against the CPU oracle on identical inputs.
+
+Tolerances (north star, BASELINE.json): fp32 loss within 1e-5 relative per
+epoch; gradients are compared against the fp64 oracle with the fp32-oracle's
+own distance as the noise floor.  Integer/layout work is bit-exact.
+"""
+import os
+
+import numpy as np
+import pytest
+
+from oracle import pyoracle as po
+from tests.gpu_helpers import c1_spec, gpu_from_oracle, make_pair
+from tests.refutil import read_msh, synthetic_eval
+
+pytestmark = pytest.mark.gpu
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden", "meshes")
+
+
+def rel(a, b):
+    return abs(a - b) / max(abs(b), 1e-30)
+
+
+def grad_close(g_gpu, spec, params, tol=2e-4):
+    """Gradient vs the fp64 oracle at the same (float) parameters."""
+    o64 = po.OracleProblem(spec, double=True)
+    _, g64 = o64.loss_and_grad(params.astype(np.float64))
+    scale = np.abs(g64).max()
+    err = np.abs(g_gpu - g64).max() / scale
+    assert err < tol, (err, scale)
+    return err
+
+
+def gear_spec(**over):
+    nodes, cells = read_msh(os.path.join(GOLD, "gearlike_v41.msh"))
+    kw = dict(n_test_1d=5, n_quad_1d=5, forcing="gear_f", boundary_g="zero", n_boundary=800,
+              eps=1.0, bx=0.1, by=0.0, layers=(2, 30, 30, 30, 1), seed=42)
+    kw.update(over)
+    return po.ProblemSpec(nodes=nodes, cells=cells, **kw)
+
+
+CASES = {
+    "c1_poisson": lambda: c1_spec(),
+    "gear576_cd2d": lambda: gear_spec(),
+    "skewed_cd2d_sigmoid": lambda: po.ProblemSpec(
+        *read_msh(os.path.join(GOLD, "skewed_12x12_v22.msh")), n_test_1d=3, n_quad_1d=6,
+        forcing="sin2pi_f", boundary_g="sin2pi_u", n_boundary=200, eps=0.3, bx=1.1, by=0.2,
+        layers=(2, 16, 1), sigmoid=True, seed=5),
+    "spatial_eps_head": lambda: c1_spec(layers=(2, 30, 30, 30, 2), eps_source=2, bx=1.0,
+                                        forcing="sinpi_vareps_f", boundary_g="sinpi_u"),
+    "inverse_scalar_eps": lambda: po.ProblemSpec(
+        *po.structured_mesh(2, 2, (-1.0, 1.0), (-1.0, 1.0)), n_test_1d=5, n_quad_1d=10,
+        forcing="bump_f", boundary_g="bump_u", n_boundary=400, n_sensors=50, sensor_seed=7,
+        sensor_field="bump_u", eps_source=1, scalars=(2.0,), layers=(2, 20, 20, 1), seed=42),
+    "split_path_q400": lambda: po.ProblemSpec(
+        *po.structured_mesh(2, 2), n_test_1d=6, n_quad_1d=20, forcing="sin4pi_f",
+        boundary_g="sin4pi_u", n_boundary=400, layers=(2, 30, 30, 30, 1), seed=42),
+}
+
+
+@pytest.mark.parametrize("name", list(CASES))
+def test_loss_and_gradient_match_oracle(name):
+    spec = CASES[name]()
+    ob, g, p0 = make_pair(spec)
+    parts_o, _ = ob.loss_and_grad(p0)
+    parts_g, grad_g = g.loss_and_grad()
+    assert rel(parts_g[0], parts_o[0]) < 1e-5, (parts_g, parts_o)
+    for k in (1, 2, 3):
+        if parts_o[k] != 0.0:
+            assert rel(parts_g[k], parts_o[k]) < 1e-5, (k, parts_g, parts_o)
+    grad_close(grad_g, spec, p0)
+
+
+def test_forward_matches_oracle_evaluate():
+    spec = c1_spec()
+    ob, g, p0 = make_pair(spec)
+    rng = np.random.default_rng(3)
+    pts = rng.uniform(-1.5, 1.5, size=(3000, 2))
+    u_o, ux_o, uy_o, _ = ob.evaluate(p0, pts, 1)
+    u, ux, uy, _ = g.forward(pts, 1)
+    for a, b in ((u, u_o), (ux, ux_o), (uy, uy_o)):
+        assert np.abs(a - b).max() <= 2e-5 * max(1.0, np.abs(b).max())
+
+
+@pytest.mark.parametrize("kind", ["fixed_conv", "scalar", "spatial"])
+def test_standalone_contraction_matches_oracle(kind):
+    over = {"fixed_conv": dict(eps=0.9, bx=-0.5, by=0.25),
+            "scalar": dict(eps_source=1, scalars=(0.7,), layers=(2, 20, 20, 1)),
+            "spatial": dict(eps_source=2, bx=0.6, layers=(2, 30, 30, 30, 2))}[kind]
+    spec = gear_spec(**over)
+    ob, g, _ = make_pair(spec)
+    n = ob.E * ob.Q
+    _, ux, uy, eps, scal = synthetic_eval(n, 1234, kind == "spatial", 1 if kind == "scalar" else 0)
+    ux32, uy32 = ux.astype(np.float32), uy.astype(np.float32)
+    e32 = None if eps is None else eps.astype(np.float32)
+    lo, ro, uxo, uyo, eo, so = ob.var_loss(ux32, uy32, e32, scal, weight=1.0)
+    lg, rg, uxg, uyg, eg, sg = g.contract(ux32, uy32, e32, np.array(scal, dtype=np.float32) if scal else None)
+    assert rel(lg, lo) < 1e-5
+    assert np.abs(rg - ro).max() <= 1e-5 * np.abs(ro).max()
+    assert np.abs(uxg - uxo).max() <= 1e-5 * np.abs(uxo).max()
+    assert np.abs(uyg - uyo).max() <= 1e-5 * np.abs(uyo).max()
+    if kind == "spatial":
+        assert np.abs(eg - eo).max() <= 1e-5 * np.abs(eo).max()
+    if kind == "scalar":
+        assert rel(sg[0], so[0]) < 1e-5
+
+
+def test_uploaded_tensor_layout_is_bit_exact():
+    spec = gear_spec()
+    ob, g, _ = make_pair(spec)
+    n = ob.E * ob.T * ob.Q
+    for which, name in enumerate(("grad_x", "grad_y", "test")):
+        assert np.array_equal(g.download_tensor(which, n).view(np.uint32),
+                              ob.array(name).astype(np.float32).view(np.uint32))
+    assert np.array_equal(g.download_tensor(3, ob.E * ob.T).view(np.uint32),
+                          ob.array("forcing").view(np.uint32))
+
+
+def test_training_trajectory_matches_oracle_c1():
+    """Per-epoch loss within 1e-5 relative over the first 100 epochs (north star)."""
+    spec = c1_spec()
+    ob, g, p0 = make_pair(spec)
+    ref = ob.train(p0, 100, lr0=1e-3, log_every=1)
+    rep = g.train(100, lr0=1e-3)
+    assert rep.steps_run == 100
+    tot_o = ref["every_step"][:, 0]
+    tot_g = rep.records["total"]
+    r = np.abs(tot_g - tot_o) / np.abs(tot_o)
+    assert r.max() < 1e-5, (r.max(), int(r.argmax()))
+    pg = g.get_params()
+    assert np.abs(pg - ref["params"]).max() < 1e-4
+
+
+def test_training_trajectory_matches_oracle_gear_inverse_stop():
+    spec = CASES["inverse_scalar_eps"]()
+    ob, g, p0 = make_pair(spec)
+    ref = ob.train(p0, 60, lr0=1e-3, eps_abs_tol=1.695, eps_actual=0.3)
+    rep = g.train(60, lr0=1e-3, eps_abs_tol=1.695, eps_actual=0.3)
+    assert rep.steps_run == ref["steps_run"]
+    assert rep.stop_reason == ref["stop_reason"]
+    r = np.abs(rep.records["total"] - ref["every_step"][:, 0]) / np.abs(ref["every_step"][:, 0])
+    assert r.max() < 1e-5
+    assert abs(rep.final_eps - ref["final_eps"]) < 1e-5
+
+
+def test_nonfinite_gradient_aborts_with_step_index():
+    spec = c1_spec(layers=(2, 16, 1))
+    ob, g, p0 = make_pair(spec)
+    bad = p0.copy()
+    bad[0] = np.inf
+    g.set_params(bad)
+    from paper_2404_12063_b200._capi import VpinnError
+    with pytest.raises(VpinnError) as e:
+        g.train(5)
+    assert e.value.code == 4 and e.value.report.abort_step == 1
