@@ -64,6 +64,20 @@ class GpuStep:
         self.n_params = L.vpinn_gpu_param_count(h)
         self.layer_sizes = tuple(layer_sizes)
 
+    @classmethod
+    def from_problem(cls, pb: "_capi.Problem", keepalive=None) -> "GpuStep":
+        """Create from an already filled vpinn_gpu_problem (e.g. the C++ host view)."""
+        self = cls.__new__(cls)
+        self._keep = [keepalive, pb]
+        h = C.c_void_p()
+        _capi.check(_capi.lib().vpinn_gpu_create(C.byref(pb), C.byref(h)))
+        self.h = h
+        self.n_elem, self.n_test, self.n_quad = pb.n_elem, pb.n_test, pb.n_quad
+        self.n_params = _capi.lib().vpinn_gpu_param_count(h)
+        sizes = C.cast(pb.layer_sizes, C.POINTER(C.c_int32))
+        self.layer_sizes = tuple(sizes[i] for i in range(pb.n_layer_sizes))
+        return self
+
     def close(self):
         if getattr(self, "h", None):
             _capi.lib().vpinn_gpu_destroy(self.h)

@@ -70,6 +70,12 @@ def main():
             "last_lines": gear14k.splitlines()[-6:],
         }
     }
+    # the reference's own run configs (must keep loading unchanged)
+    import shutil
+    cfg_out = os.path.join(HERE, "configs")
+    os.makedirs(cfg_out, exist_ok=True)
+    for name in sorted(os.listdir("/root/reference/proj/configs")):
+        shutil.copy(os.path.join("/root/reference/proj/configs", name), os.path.join(cfg_out, name))
     with open(os.path.join(HERE, "gear_14192.json"), "w") as fh:
         json.dump(info, fh, indent=1)
     print("golden meshes and gear_14192.json written")
