@@ -195,6 +195,14 @@ int64_t vpinn_gpu_launch_count(const vpinn_gpu_ctx* ctx);
 int vpinn_gpu_profile_step(vpinn_gpu_ctx* ctx, int reps, double* ms_mlp, double* ms_reduce,
                            double* ms_adam);
 
+/* Write 256 MB (> the 126 MB L2) on the context stream: benchmarks call it
+ * between timed epochs so every epoch streams its tensors from HBM. */
+int vpinn_gpu_flush_l2(vpinn_gpu_ctx* ctx);
+
+/* FP32 FFMA throughput of `device` (TFLOP/s, best of 4 timed launches):
+ * the roofline denominator of the FFMA-bound step kernel. */
+int vpinn_gpu_measure_ffma_peak(int device, double* tflops);
+
 /* Multi-GPU: rank 0 creates an NCCL unique id (128 bytes), every rank
  * attaches with the same id.  One ncclAllReduce(sum, f64) of
  * [gradient | loss parts] per epoch over NVLink. */

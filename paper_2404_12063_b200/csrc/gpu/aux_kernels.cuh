@@ -482,3 +482,27 @@ __global__ void __launch_bounds__(256) penalty_kernel(const float* __restrict__ 
 }
 
 }  // namespace vpg
+
+namespace vpg {
+
+// FP32 FFMA throughput microbenchmark (roofline denominator for the
+// FFMA-bound step kernel): 8 independent chains per thread, register
+// operands, 2 flops per FFMA.
+__global__ void __launch_bounds__(256) ffma_peak_kernel(float* out, int iters, float a, float b) {
+  float x[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) x[k] = threadIdx.x * 1e-7f + k;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int r = 0; r < 16; ++r) {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) x[k] = fmaf(x[k], a, b);
+    }
+  }
+  float s = 0.f;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) s += x[k];
+  if (s == 1234.5f) out[threadIdx.x] = s;  // keep the chains alive
+}
+
+}  // namespace vpg

@@ -70,16 +70,59 @@ __device__ __forceinline__ uint64_t globaltimer() {
 // s1 = act', kap = act''/act' so that s2 = kap * s1:
 //   tanh:    s1 = 1 - z^2,   kap = -2 z
 //   sigmoid: s1 = z (1 - z), kap = 1 - 2 z
-// Accurate libdevice tanhf/expf (no fast-math): fp32 parity needs < 2^-20.
-__device__ __forceinline__ float act_value(int sig, float a) {
-  return sig ? 1.0f / (1.0f + expf(-a)) : tanhf(a);
+// Branch-free, compact evaluations (the step kernel inlines ~100 of them, so
+// code size matters as much as latency):
+//   tanh |x| <  0.4 : x + x^3 P(x^2), degree-4 minimax, <= 0.63 ulp
+//   tanh |x| >= 0.4 : 1 - 2 / (2^(2|x| log2 e) + 1) with MUFU ex2/rcp and one
+//                     Newton step; the ex2 error is attenuated by
+//                     2e/(e^2-1) <= 1.13 at the switch point
+__device__ __forceinline__ float ex2_approx(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
 }
-__device__ __forceinline__ float act_s1(int sig, float z) {
-  return sig ? z * (1.0f - z) : 1.0f - z * z;
+__device__ __forceinline__ float rcp_newton(float d) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(d));
+  return fmaf(r, fmaf(-d, r, 1.0f), r);  // one Newton step
 }
-__device__ __forceinline__ float act_kap(int sig, float z) {
-  return sig ? 1.0f - 2.0f * z : -2.0f * z;
-}
+
+constexpr int kActTanh = 0;
+constexpr int kActSigmoid = 1;
+
+template <int ACT>
+struct Act;
+
+template <>
+struct Act<kActTanh> {
+  static __device__ __forceinline__ float value(float x) {
+    const float ax = fabsf(x);
+    const float x2 = x * x;
+    float p = -0.007364633358913433f;
+    p = fmaf(p, x2, 0.021618979731563185f);
+    p = fmaf(p, x2, -0.05394892778111454f);
+    p = fmaf(p, x2, 0.1333326813390213f);
+    p = fmaf(p, x2, -0.3333333262496359f);
+    const float small = fmaf(x * x2, p, x);
+    // |x| >= 9 gives 1.0f exactly; the clamp keeps e finite for the Newton step
+    const float e = ex2_approx(fminf(ax, 9.0f) * 2.8853900817779268f);
+    const float big = fmaf(-2.0f, rcp_newton(e + 1.0f), 1.0f);
+    return ax < 0.4f ? small : copysignf(big, x);
+  }
+  static __device__ __forceinline__ float s1(float z) { return fmaf(-z, z, 1.0f); }
+  static __device__ __forceinline__ float kap(float z) { return -2.0f * z; }
+};
+
+template <>
+struct Act<kActSigmoid> {
+  static __device__ __forceinline__ float value(float x) {
+    // 1 / (1 + exp(-x)); exp via ex2 (rel. err ~2^-22), overflow -> 0
+    const float e = ex2_approx(fminf(-x * 1.4426950408889634f, 126.0f));
+    return rcp_newton(1.0f + e);
+  }
+  static __device__ __forceinline__ float s1(float z) { return z * (1.0f - z); }
+  static __device__ __forceinline__ float kap(float z) { return 1.0f - 2.0f * z; }
+};
 
 // network.hpp:130-138
 __device__ __forceinline__ float softplusf(float x) {

@@ -2,7 +2,7 @@
 //
 // One CTA (128 threads, one quadrature/penalty point per thread) owns a
 // TILE of whole cells.  Per tile it runs, without leaving the SM:
-//   1. forward with x/y tangents through the tanh MLP (network.hpp:204-282),
+//   1. forward with x/y tangents through the MLP (network.hpp:204-282),
 //      weights in shared memory, activations in registers, per-point layer
 //      state in shared memory (point-major rows, 128-bit conflict-free);
 //   2. the Algorithm-3 contraction of the tile's premultiplier slabs
@@ -12,10 +12,14 @@
 //      penalty tiles (boundary / sensors, losses.hpp:406-415) instead;
 //   3. the reverse sweep (network.hpp:287-372) with parameter-gradient
 //      outer products computed as per-warp 4x8 register-tiled products over
-//      the warp's 32 points, combined across warps in a fixed order into a
-//      per-CTA shared-memory gradient (deterministic, no atomics).
+//      the warp's 32 points, combined across warps in a fixed order into
+//      per-thread gradient registers (deterministic, no atomics).
 // The per-CTA gradient and loss parts are reduced across CTAs by
 // reduce_kernel (fp64, fixed order) and applied by adam_kernel.
+//
+// Every loop whose body is large is rolled and every fully unrolled region
+// is short: the kernel is FFMA-bound only if its instruction stream stays in
+// the instruction cache (the first profile showed no_instruction stalls).
 //
 // The same template also provides the split-path kernels (forward only,
 // reverse from adjoints in global memory) used when a cell has more
@@ -43,9 +47,7 @@ enum : int { kModeForward = 0, kModeFused = 1, kModeReverse = 2 };
 enum : int { kLpVar = 0, kLpBnd = 1, kLpSen = 2, kLpEpsGrad = 3, kLpBad = 4, kLpWords = 8 };
 
 // exchange rows (kThreads floats each, feature-major)
-enum : int {
-  kExX = 0, kExY, kExU, kExUx, kExUy, kExE, kExY1, kExSx, kExSy, kExCv, kExRows
-};
+enum : int { kExX = 0, kExY, kExU, kExUx, kExUy, kExE, kExY1, kExSx, kExSy, kExCv, kExRows };
 
 struct StepArgs {
   // premultipliers of this rank's cells, [k][j][q]; forcing [k][j]
@@ -96,17 +98,26 @@ struct Layout {
   static_assert(D >= 1 && D <= 4, "hidden layers");
   static_assert(C == 1 || C == 2, "output channels");
   static constexpr int HP = (H + 3) & ~3;
+  // the last hidden layer's state lives in registers when it fits
   static constexpr bool kLastRegs = (3 * H <= 96);
+  // state blocks (z | TXx | TXy of one hidden layer, 3*HP floats each):
+  // hidden h (1 <= h <= D-2) in block h-1; the last hidden layer in the last
+  // block when it does not live in registers; block 0 always exists (forward
+  // scratch for D == 2, G_0 in the reverse).
   static constexpr int kBlocksMid = (D >= 3 ? D - 2 : 0) + (kLastRegs ? 0 : 1);
   static constexpr int kBlocks = kBlocksMid > 0 ? kBlocksMid : 1;
   static constexpr int SROW0 = kBlocks * 3 * HP;
   static constexpr int SROW = ((SROW0 / 4) % 2 == 1) ? SROW0 : SROW0 + 4;
   static constexpr int SG0 = (H + 1 + 3) & ~3;
   static constexpr int SG = ((SG0 / 4) % 2 == 1) ? SG0 : SG0 + 4;
+  // weights: L0 as float4 rows; hidden layers [HP][HP] + bias[HP]; the last
+  // hidden layer also transposed (input-major) when it feeds registers;
+  // output [C][HP] + bias[4]
   static constexpr int W0F = 4 * H;
   static constexpr int WHF = HP * HP + HP;
+  static constexpr int WTF = (D >= 2 && kLastRegs) ? HP * HP : 0;
   static constexpr int WDF = C * HP + 4;
-  static constexpr int WTOT = W0F + (D - 1) * WHF + WDF;
+  static constexpr int WTOT = W0F + (D - 1) * WHF + WTF + WDF;
   // parameter-gradient registers per thread: thread t owns compact indices
   // t + kThreads*m (deterministic single-owner accumulation)
   static constexpr int NPMAX = 3 * H + (D - 1) * (H * H + H) + C * (H + 1) + 8;
@@ -114,7 +125,6 @@ struct Layout {
   static constexpr int REV_UNION = kThreads * SG;
   static constexpr int PART_FLOATS_H = kWarps * (HP * HP + HP);
   static constexpr int REV_NEED = REV_UNION > PART_FLOATS_H ? REV_UNION : PART_FLOATS_H;
-  // fixed part of the shared-memory carve (floats), union + rows appended
   static constexpr int OFF_W = 0;
   static constexpr int OFF_EX = OFF_W + WTOT;
   static constexpr int OFF_RED = OFF_EX + kExRows * kThreads;  // 64 doubles
@@ -123,7 +133,6 @@ struct Layout {
   static constexpr int OFF_UNION = OFF_STATE + kThreads * SROW + 4;
 };
 
-// Shared memory bytes for given union/rows sizes (host and device agree).
 template <int H, int D, int C>
 __host__ __device__ constexpr size_t step_smem_bytes(int union_floats, int chunk_rows) {
   using LY = Layout<H, D, C>;
@@ -132,8 +141,38 @@ __host__ __device__ constexpr size_t step_smem_bytes(int union_floats, int chunk
 }
 
 // ---------------------------------------------------------------------------
+// small vector helpers
+template <int N>
+__device__ __forceinline__ void load_vec(const float* row, float (&v)[N]) {
+#pragma unroll
+  for (int j = 0; j < (N / 4) * 4; j += 4) {
+    const float4 a = lds4(row + j);
+    v[j] = a.x;
+    v[j + 1] = a.y;
+    v[j + 2] = a.z;
+    v[j + 3] = a.w;
+  }
+#pragma unroll
+  for (int j = (N / 4) * 4; j < N; ++j) v[j] = row[j];
+}
+
+// stores v[0..N) and zeroes the padding up to the next multiple of 4
+template <int N>
+__device__ __forceinline__ void store_vec(float* row, const float (&v)[N]) {
+#pragma unroll
+  for (int j = 0; j < (N / 4) * 4; j += 4) sts4(row + j, make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]));
+  if constexpr (N % 4 != 0) {
+    constexpr int j = (N / 4) * 4;
+    float t[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+    for (int r = 0; r < N % 4; ++r) t[r] = v[j + r];
+    sts4(row + j, make_float4(t[0], t[1], t[2], t[3]));
+  }
+}
+
+// ---------------------------------------------------------------------------
 // forward helpers
-// 4 output rows (i0..i0+3) x 3 streams of y = W x over H inputs
+// 4 output rows (i0..i0+3) x 3 streams of y = W x over H register inputs
 template <int H, int HP>
 __device__ __forceinline__ void mv3_rows4(const float* __restrict__ W, int i0, const float (&xz)[H],
                                           const float (&xt)[H], const float (&xu)[H],
@@ -171,29 +210,10 @@ __device__ __forceinline__ void mv3_rows4(const float* __restrict__ W, int i0, c
   }
 }
 
-template <int H>
-__device__ __forceinline__ void load3(const float* row, int HP, float (&z)[H], float (&t)[H],
-                                      float (&u)[H]) {
-#pragma unroll
-  for (int j = 0; j < (H / 4) * 4; j += 4) {
-    const float4 a = lds4(row + j), b = lds4(row + HP + j), c = lds4(row + 2 * HP + j);
-    z[j] = a.x; z[j + 1] = a.y; z[j + 2] = a.z; z[j + 3] = a.w;
-    t[j] = b.x; t[j + 1] = b.y; t[j + 2] = b.z; t[j + 3] = b.w;
-    u[j] = c.x; u[j + 1] = c.y; u[j + 2] = c.z; u[j + 3] = c.w;
-  }
-#pragma unroll
-  for (int j = (H / 4) * 4; j < H; ++j) {
-    z[j] = row[j];
-    t[j] = row[HP + j];
-    u[j] = row[2 * HP + j];
-  }
-}
-
-// hidden layer (H -> H) with outputs written to a state block (z|tx|ty)
-template <int H, int HP>
-__device__ __forceinline__ void hidden_to_block(int sig, const float* W, const float (&xz)[H],
-                                                const float (&xt)[H], const float (&xu)[H],
-                                                float* blk) {
+// hidden layer (register inputs) -> state block (z | TXx | TXy), output rows rolled
+template <int H, int HP, int ACT>
+__device__ __forceinline__ void hidden_to_block(const float* W, const float (&xz)[H], const float (&xt)[H],
+                                                const float (&xu)[H], float* blk) {
   const float* B = W + HP * HP;
 #pragma unroll 1
   for (int i0 = 0; i0 < HP; i0 += 4) {
@@ -202,8 +222,8 @@ __device__ __forceinline__ void hidden_to_block(int sig, const float* W, const f
     float z[4], gx[4], gy[4];
 #pragma unroll
     for (int r = 0; r < 4; ++r) {
-      z[r] = act_value(sig, a[r] + B[i0 + r]);
-      const float s1 = act_s1(sig, z[r]);
+      z[r] = Act<ACT>::value(a[r] + B[i0 + r]);
+      const float s1 = Act<ACT>::s1(z[r]);
       gx[r] = s1 * tx[r];
       gy[r] = s1 * ty[r];
     }
@@ -213,25 +233,45 @@ __device__ __forceinline__ void hidden_to_block(int sig, const float* W, const f
   }
 }
 
-// hidden layer (H -> H) with outputs kept in registers (arrays sized HP)
-template <int H, int HP>
-__device__ __forceinline__ void hidden_to_regs(int sig, const float* W, const float (&xz)[H],
-                                               const float (&xt)[H], const float (&xu)[H],
-                                               float (&oz)[H], float (&ot)[H], float (&ou)[H]) {
-  const float* B = W + HP * HP;
+// hidden layer with inputs from a state block (own row) and outputs in
+// registers: input-major, the input loop rolled, W transposed in SMEM
+// ([in][out], rows of HP); accumulators oz/ot/ou sized HP.
+template <int H, int HP, int ACT>
+__device__ __forceinline__ void hidden_block_to_regs(const float* WT, const float* B, const float* blk,
+                                                     float (&oz)[HP], float (&ot)[HP], float (&ou)[HP]) {
 #pragma unroll
-  for (int i0 = 0; i0 < HP; i0 += 4) {
-    float a[4], tx[4], ty[4];
-    mv3_rows4<H, HP>(W, i0, xz, xt, xu, a, tx, ty);
+  for (int i = 0; i < HP; ++i) oz[i] = ot[i] = ou[i] = 0.0f;
+#pragma unroll 1
+  for (int j0 = 0; j0 < H; j0 += 2) {
+    const float2 zz = *reinterpret_cast<const float2*>(blk + j0);
+    const float2 tt = *reinterpret_cast<const float2*>(blk + HP + j0);
+    const float2 uu = *reinterpret_cast<const float2*>(blk + 2 * HP + j0);
+    const float zi[2] = {zz.x, zz.y}, ti[2] = {tt.x, tt.y}, ui[2] = {uu.x, uu.y};
 #pragma unroll
-    for (int r = 0; r < 4; ++r) {
-      if (i0 + r < H) {
-        const float z = act_value(sig, a[r] + B[i0 + r]);
-        const float s1 = act_s1(sig, z);
-        oz[i0 + r] = z;
-        ot[i0 + r] = s1 * tx[r];
-        ou[i0 + r] = s1 * ty[r];
+    for (int jj = 0; jj < 2; ++jj) {
+#pragma unroll
+      for (int i = 0; i < HP; i += 4) {
+        const float4 w = lds4(WT + (j0 + jj) * HP + i);
+        const float wv[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          oz[i + r] = fmaf(wv[r], zi[jj], oz[i + r]);
+          ot[i + r] = fmaf(wv[r], ti[jj], ot[i + r]);
+          ou[i + r] = fmaf(wv[r], ui[jj], ou[i + r]);
+        }
       }
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < HP; ++i) {
+    if (i < H) {
+      const float z = Act<ACT>::value(oz[i] + B[i]);
+      const float s1 = Act<ACT>::s1(z);
+      oz[i] = z;
+      ot[i] = s1 * ot[i];
+      ou[i] = s1 * ou[i];
+    } else {
+      oz[i] = ot[i] = ou[i] = 0.0f;
     }
   }
 }
@@ -257,20 +297,6 @@ __device__ __forceinline__ void warp_outer_tile(const float* __restrict__ G, int
   }
 }
 
-// stores v[0..H) and zeroes the padding up to the next multiple of 4
-template <int H>
-__device__ __forceinline__ void store_vec(float* row, const float (&v)[H]) {
-#pragma unroll
-  for (int j = 0; j < (H / 4) * 4; j += 4) sts4(row + j, make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]));
-  if constexpr (H % 4 != 0) {
-    constexpr int j = (H / 4) * 4;
-    float t[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-    for (int r = 0; r < H % 4; ++r) t[r] = v[j + r];
-    sts4(row + j, make_float4(t[0], t[1], t[2], t[3]));
-  }
-}
-
 // block-wide deterministic sum of one double per thread (result valid in
 // thread 0); red has >= kWarps doubles
 __device__ __forceinline__ double block_sum_d(double v, double* red) {
@@ -286,16 +312,24 @@ __device__ __forceinline__ double block_sum_d(double v, double* red) {
   return s;
 }
 
-// ---------------------------------------------------------------------------
-// contraction over one tile of whole cells (losses.hpp:111-166).
-// Slab rows of the tile are streamed in chunks of a.chunk_rows through a
-// two-stage ring; thread 0 issues, everyone consumes.
-struct RingState {
-  uint32_t parity[2];
-};
+// greg[m] (compact index tid + kThreads*m) += val(e) for e = index - lo in
+// [0, cnt); only the m that can hit the range are visited (rolled loop;
+// greg lives in L1-resident local memory)
+template <int NGR, typename F>
+__device__ __forceinline__ void own_add(float (&greg)[NGR], int tid, int lo, int cnt, F&& val) {
+  const int m0 = max(0, (lo - tid + kThreads - 1) / kThreads);
+  const int m1 = min(NGR, (lo + cnt - tid + kThreads - 1) / kThreads);
+#pragma unroll 1
+  for (int m = m0; m < m1; ++m) {
+    const int e = tid + kThreads * m - lo;
+    if (e >= 0 && e < cnt) greg[m] += val(e);
+  }
+}
 
-__device__ __forceinline__ void issue_chunk(const StepArgs& a, int cell0, int row0, int nrows,
-                                            float* stage, uint64_t* bar) {
+// ---------------------------------------------------------------------------
+// slab chunk copies (thread 0): aligned superset of each tensor's rows
+static __device__ __noinline__ void issue_chunk(const StepArgs& a, int cell0, int row0, int nrows, float* stage,
+                                         uint64_t* bar) {
   const size_t grow0 = (size_t)cell0 * a.T + row0;
   uint32_t total = 0;
   const char* src[3];
@@ -313,24 +347,14 @@ __device__ __forceinline__ void issue_chunk(const StepArgs& a, int cell0, int ro
   for (int t = 0; t < a.nt; ++t) bulk_g2s(stage + t * a.tstride, src[t], n16[t], bar);
 }
 
-__device__ __forceinline__ const float* chunk_ptr(const StepArgs& a, int cell0, int row0,
-                                                  const float* stage, int t) {
+__device__ __forceinline__ const float* chunk_ptr(const StepArgs& a, int cell0, int row0, const float* stage,
+                                                  int t) {
   const size_t grow0 = (size_t)cell0 * a.T + row0;
   const uintptr_t s = reinterpret_cast<uintptr_t>(a.tens[t] + grow0 * a.Q);
   return stage + t * a.tstride + ((s & 15u) >> 2);
 }
 
-
-// greg[m] (compact index tid + kThreads*m) += val(e) for e = index - lo in [0, cnt)
-template <int NGR, typename F>
-__device__ __forceinline__ void own_add(float (&greg)[NGR], int tid, int lo, int cnt, F&& val) {
-#pragma unroll
-  for (int m = 0; m < NGR; ++m) {
-    const int e = tid + kThreads * m - lo;
-    if (e >= 0 && e < cnt) greg[m] += val(e);
-  }
-}
-
+// ---------------------------------------------------------------------------
 struct RevCtx {
   float* sState;
   float* srow;
@@ -339,7 +363,6 @@ struct RevCtx {
   const float* sW0;
   const float* sWh;
   const NetDesc* netp;
-  int sig;
   float px, py;
   int tid, lane, warp;
 };
@@ -348,9 +371,9 @@ struct RevCtx {
 // gradient (three streams) + propagation to hidden l-1 (network.hpp:320-358).
 // On entry gA/gX/gY hold G_l for l == D-1; otherwise G_l sits in the state
 // block of hidden l (written in place by the previous call).
-template <int H, int D, int C, int l, int NGR>
-__device__ __forceinline__ void reverse_hidden(RevCtx& rc, float (&gA)[H], float (&gX)[H],
-                                             float (&gY)[H], float (&greg)[NGR]) {
+template <int H, int D, int C, int ACT, int l, int NGR>
+__device__ __forceinline__ void reverse_hidden(RevCtx& rc, float (&gA)[H], float (&gX)[H], float (&gY)[H],
+                                               float (&greg)[NGR]) {
   using LY = Layout<H, D, C>;
   constexpr int HP = LY::HP;
   constexpr int SROW = LY::SROW;
@@ -360,173 +383,177 @@ __device__ __forceinline__ void reverse_hidden(RevCtx& rc, float (&gA)[H], float
   float* Gbuf = rc.Gbuf;
   float* Part = rc.Part;
   const float* sW0 = rc.sW0;
-  const float* sWh = rc.sWh;
   const NetDesc& net = *rc.netp;
-  const int sig = rc.sig;
-  const float px = rc.px, py = rc.py;
   const int tid = rc.tid, lane = rc.lane, warp = rc.warp;
   const int wrow = warp * 32;
-    if constexpr (l != D - 1) {
-      // G_l was written in place into the block of hidden l
-      load3<H>(srow + (l - 1) * 3 * HP, HP, gA, gX, gY);
+  if constexpr (l != D - 1) {
+    load_vec<H>(srow + (l - 1) * 3 * HP, gA);
+    load_vec<H>(srow + (l - 1) * 3 * HP + HP, gX);
+    load_vec<H>(srow + (l - 1) * 3 * HP + 2 * HP, gY);
+  }
+  const float* W = rc.sWh + (l - 1) * LY::WHF;
+  // H operand rows: hidden l-1 = block l-2 (l >= 2) or the recomputed layer-0
+  // state staged in block 0 (l == 1; block 0 is free here)
+  const float* Hm;
+  float z0r[l == 1 ? H : 1];
+  if constexpr (l >= 2) {
+    Hm = sState + wrow * SROW + (l - 2) * 3 * HP;
+  } else {
+#pragma unroll
+    for (int i = 0; i < H; ++i) {
+      const float4 w = lds4(sW0 + 4 * i);
+      z0r[i] = Act<ACT>::value(fmaf(w.y, rc.py, w.x * rc.px) + w.z);
     }
-    const float* W = sWh + (l - 1) * LY::WHF;
-    // H operand rows: hidden l-1 = block l-2 (l >= 2) or recomputed z0 (l == 1)
-    float z0r[l == 1 ? H : 1];
-    const float* Hm = nullptr;
-    int sh = SROW;
-    if constexpr (l >= 2) {
-      Hm = sState + wrow * SROW + (l - 2) * 3 * HP;
-    } else {
+    Hm = sState + wrow * SROW;
+  }
+  constexpr int NOB = (H + 3) / 4, NIB = (H + 7) / 8, NTILE = NOB * NIB;
+  constexpr int NROUND = (NTILE + 31) / 32;
+  float accr[NROUND][32];
+#pragma unroll
+  for (int rr = 0; rr < NROUND; ++rr)
+#pragma unroll
+    for (int k = 0; k < 32; ++k) accr[rr][k] = 0.f;
+  float bsum[(H + 31) / 32];
+  // three passes: value, x-tangent, y-tangent streams
+#pragma unroll 1
+  for (int pass = 0; pass < 3; ++pass) {
+    {
+      float gsel[H];
+#pragma unroll
+      for (int i = 0; i < H; ++i) gsel[i] = pass == 0 ? gA[i] : (pass == 1 ? gX[i] : gY[i]);
+      store_vec<H>(Gbuf + tid * SG, gsel);
+    }
+    if constexpr (l == 1) {
+      float tv[H];
 #pragma unroll
       for (int i = 0; i < H; ++i) {
         const float4 w = lds4(sW0 + 4 * i);
-        z0r[i] = act_value(sig, fmaf(w.y, py, w.x * px) + w.z);
+        const float wsel = pass == 1 ? w.x : w.y;
+        tv[i] = pass == 0 ? z0r[i] : Act<ACT>::s1(z0r[i]) * wsel;
       }
-      // block 0 is free here: its G_1 was loaded above (or G_1 is in registers)
-      store_vec<H>(srow, z0r);
-      Hm = sState + wrow * SROW;
+      store_vec<H>(srow, tv);
     }
-    // three passes: value, x-tangent, y-tangent streams
-    constexpr int NOB = (H + 3) / 4, NIB = (H + 7) / 8, NTILE = NOB * NIB;
-    constexpr int NROUND = (NTILE + 31) / 32;
-    float accr[NROUND][32];
+    __syncthreads();
+    const float* Hp = (l >= 2) ? Hm + pass * HP : Hm;
 #pragma unroll
-    for (int rr = 0; rr < NROUND; ++rr)
-#pragma unroll
-      for (int k = 0; k < 32; ++k) accr[rr][k] = 0.f;
-    float bsum[(H + 31) / 32];
-#pragma unroll
-    for (int pass = 0; pass < 3; ++pass) {
-      if (pass == 0) store_vec<H>(Gbuf + tid * SG, gA);
-      else if (pass == 1) store_vec<H>(Gbuf + tid * SG, gX);
-      else store_vec<H>(Gbuf + tid * SG, gY);
-      if constexpr (l == 1) if (pass > 0) {
-        float tv[H];
-#pragma unroll
-        for (int i = 0; i < H; ++i) {
-          const float4 w = lds4(sW0 + 4 * i);
-          tv[i] = act_s1(sig, z0r[i]) * (pass == 1 ? w.x : w.y);
-        }
-        store_vec<H>(srow, tv);
+    for (int rr = 0; rr < NROUND; ++rr) {
+      const int t = lane + 32 * rr;
+      if (t < NTILE) {
+        const int ob = t % NOB, ib = t / NOB;
+        warp_outer_tile(Gbuf + wrow * SG, SG, Hp, SROW, ob * 4, ib * 8, accr[rr]);
       }
-      __syncthreads();
-      const float* Hp = (l >= 2) ? Hm + pass * HP : Hm;
-#pragma unroll
-      for (int rr = 0; rr < NROUND; ++rr) {
-        const int t = lane + 32 * rr;
-        if (t < NTILE) {
-          const int ob = t % NOB, ib = t / NOB;
-          warp_outer_tile(Gbuf + wrow * SG, SG, Hp, sh, ob * 4, ib * 8, accr[rr]);
-        }
-      }
-      if (pass == 0) {
-#pragma unroll
-        for (int s = 0; s < (H + 31) / 32; ++s) {
-          const int col = lane + 32 * s;
-          float acc = 0.f;
-          if (col < H)
-            for (int p = 0; p < 32; ++p) acc += Gbuf[(wrow + p) * SG + col];
-          bsum[s] = acc;
-        }
-      }
-      __syncthreads();
     }
-    // partials [warp][HP][HP] + bias [warp][HP]
-    {
-      float* pw = Part + warp * (HP * HP + HP);
-#pragma unroll
-      for (int rr = 0; rr < NROUND; ++rr) {
-        const int t = lane + 32 * rr;
-        if (t < NTILE) {
-          const int ob = t % NOB, ib = t / NOB;
-#pragma unroll
-          for (int a4 = 0; a4 < 4; ++a4)
-#pragma unroll
-            for (int b8 = 0; b8 < 8; ++b8) {
-              const int o = ob * 4 + a4, i = ib * 8 + b8;
-              if (o < HP && i < HP) pw[o * HP + i] = accr[rr][a4 * 8 + b8];
-            }
-        }
-      }
+    if (pass == 0) {
 #pragma unroll
       for (int s = 0; s < (H + 31) / 32; ++s) {
         const int col = lane + 32 * s;
-        if (col < H) pw[HP * HP + col] = bsum[s];
+        float acc = 0.f;
+        if (col < H)
+#pragma unroll 4
+          for (int p = 0; p < 32; ++p) acc += Gbuf[(wrow + p) * SG + col];
+        bsum[s] = acc;
       }
     }
     __syncthreads();
-    {
-      const int fi = net.in_w[l], fo = net.out_w[l];
-      own_add(greg, tid, net.w_off[l], fo * fi, [&](int e) {
-        const int o = e / fi, i = e - o * fi;
-        float s = Part[o * HP + i];
+  }
+  // partials [warp][HP][HP] + bias [warp][HP]
+  {
+    float* pw = Part + warp * (HP * HP + HP);
 #pragma unroll
-        for (int w = 1; w < kWarps; ++w) s += Part[w * (HP * HP + HP) + o * HP + i];
-        return s;
-      });
-      own_add(greg, tid, net.b_off[l], fo, [&](int o) {
-        float s = Part[HP * HP + o];
+    for (int rr = 0; rr < NROUND; ++rr) {
+      const int t = lane + 32 * rr;
+      if (t < NTILE) {
+        const int ob = t % NOB, ib = t / NOB;
 #pragma unroll
-        for (int w = 1; w < kWarps; ++w) s += Part[w * (HP * HP + HP) + HP * HP + o];
-        return s;
-      });
+        for (int a4 = 0; a4 < 4; ++a4) {
+          const int o = ob * 4 + a4;
+          if (o < HP && ib * 8 < HP)
+            sts4(pw + o * HP + ib * 8, make_float4(accr[rr][a4 * 8], accr[rr][a4 * 8 + 1], accr[rr][a4 * 8 + 2],
+                                                   accr[rr][a4 * 8 + 3]));
+          if (o < HP && ib * 8 + 4 < HP)
+            sts4(pw + o * HP + ib * 8 + 4, make_float4(accr[rr][a4 * 8 + 4], accr[rr][a4 * 8 + 5],
+                                                       accr[rr][a4 * 8 + 6], accr[rr][a4 * 8 + 7]));
+        }
+      }
     }
-    __syncthreads();
-    // propagate: Xbar = W^T Abar etc.; through hidden l-1's activation
-    if constexpr (l == 1) store_vec<H>(Gbuf + tid * SG, z0r);  // own row: z0 for the chunks
+#pragma unroll
+    for (int s = 0; s < (H + 31) / 32; ++s) {
+      const int col = lane + 32 * s;
+      if (col < H) pw[HP * HP + col] = bsum[s];
+    }
+  }
+  __syncthreads();
+  {
+    const int fi = net.in_w[l], fo = net.out_w[l];
+    own_add(greg, tid, net.w_off[l], fo * fi, [&](int e) {
+      const int o = e / fi, i = e - o * fi;
+      float s = Part[o * HP + i];
+#pragma unroll
+      for (int w = 1; w < kWarps; ++w) s += Part[w * (HP * HP + HP) + o * HP + i];
+      return s;
+    });
+    own_add(greg, tid, net.b_off[l], fo, [&](int o) {
+      float s = Part[HP * HP + o];
+#pragma unroll
+      for (int w = 1; w < kWarps; ++w) s += Part[w * (HP * HP + HP) + HP * HP + o];
+      return s;
+    });
+  }
+  __syncthreads();
+  // propagate: Xbar = W^T Abar etc.; through hidden l-1's activation
+  if constexpr (l == 1) store_vec<H>(Gbuf + tid * SG, z0r);  // own row: z0 for the chunks
 #pragma unroll 1
-    for (int j0 = 0; j0 < HP; j0 += 4) {
-      float xb[4] = {0.f, 0.f, 0.f, 0.f}, zx[4] = {0.f, 0.f, 0.f, 0.f}, zy[4] = {0.f, 0.f, 0.f, 0.f};
+  for (int j0 = 0; j0 < HP; j0 += 4) {
+    float xb[4] = {0.f, 0.f, 0.f, 0.f}, zx[4] = {0.f, 0.f, 0.f, 0.f}, zy[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-      for (int i = 0; i < H; ++i) {
-        const float4 w = lds4(W + i * HP + j0);
-        const float wv[4] = {w.x, w.y, w.z, w.w};
-#pragma unroll
-        for (int r = 0; r < 4; ++r) {
-          xb[r] = fmaf(wv[r], gA[i], xb[r]);
-          zx[r] = fmaf(wv[r], gX[i], zx[r]);
-          zy[r] = fmaf(wv[r], gY[i], zy[r]);
-        }
-      }
-      float z[4], txv[4], tyv[4];
-      float* dst;
-      if constexpr (l >= 2) {
-        float* blk = srow + (l - 2) * 3 * HP;
-        const float4 a4 = lds4(blk + j0), b4 = lds4(blk + HP + j0), c4 = lds4(blk + 2 * HP + j0);
-        z[0] = a4.x; z[1] = a4.y; z[2] = a4.z; z[3] = a4.w;
-        txv[0] = b4.x; txv[1] = b4.y; txv[2] = b4.z; txv[3] = b4.w;
-        tyv[0] = c4.x; tyv[1] = c4.y; tyv[2] = c4.z; tyv[3] = c4.w;
-        dst = blk;
-      } else {
-        const float4 a4 = lds4(Gbuf + tid * SG + j0);
-        z[0] = a4.x; z[1] = a4.y; z[2] = a4.z; z[3] = a4.w;
-#pragma unroll
-        for (int r = 0; r < 4; ++r) {
-          const int j = min(j0 + r, H - 1);
-          const float4 w = lds4(sW0 + 4 * j);
-          const float s1 = act_s1(sig, z[r]);
-          txv[r] = s1 * w.x;
-          tyv[r] = s1 * w.y;
-        }
-        dst = srow;  // G_0 goes to block 0 (free by now)
-      }
-      float oa[4], ox[4], oy[4];
+    for (int i = 0; i < H; ++i) {
+      const float4 w = lds4(W + i * HP + j0);
+      const float wv[4] = {w.x, w.y, w.z, w.w};
 #pragma unroll
       for (int r = 0; r < 4; ++r) {
-        const float s1 = act_s1(sig, z[r]), kp = act_kap(sig, z[r]);
-        oa[r] = fmaf(s1, xb[r], kp * fmaf(txv[r], zx[r], tyv[r] * zy[r]));
-        ox[r] = s1 * zx[r];
-        oy[r] = s1 * zy[r];
+        xb[r] = fmaf(wv[r], gA[i], xb[r]);
+        zx[r] = fmaf(wv[r], gX[i], zx[r]);
+        zy[r] = fmaf(wv[r], gY[i], zy[r]);
       }
-      sts4(dst + j0, make_float4(oa[0], oa[1], oa[2], oa[3]));
-      sts4(dst + HP + j0, make_float4(ox[0], ox[1], ox[2], ox[3]));
-      sts4(dst + 2 * HP + j0, make_float4(oy[0], oy[1], oy[2], oy[3]));
     }
+    float z[4], txv[4], tyv[4];
+    float* dst;
+    if constexpr (l >= 2) {
+      float* blk = srow + (l - 2) * 3 * HP;
+      const float4 a4 = lds4(blk + j0), b4 = lds4(blk + HP + j0), c4 = lds4(blk + 2 * HP + j0);
+      z[0] = a4.x; z[1] = a4.y; z[2] = a4.z; z[3] = a4.w;
+      txv[0] = b4.x; txv[1] = b4.y; txv[2] = b4.z; txv[3] = b4.w;
+      tyv[0] = c4.x; tyv[1] = c4.y; tyv[2] = c4.z; tyv[3] = c4.w;
+      dst = blk;
+    } else {
+      const float4 a4 = lds4(Gbuf + tid * SG + j0);
+      z[0] = a4.x; z[1] = a4.y; z[2] = a4.z; z[3] = a4.w;
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const int j = min(j0 + r, H - 1);
+        const float4 w = lds4(sW0 + 4 * j);
+        const float s1 = Act<ACT>::s1(z[r]);
+        txv[r] = s1 * w.x;
+        tyv[r] = s1 * w.y;
+      }
+      dst = srow;  // G_0 goes to block 0
     }
+    float oa[4], ox[4], oy[4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const float s1 = Act<ACT>::s1(z[r]), kp = Act<ACT>::kap(z[r]);
+      oa[r] = fmaf(s1, xb[r], kp * fmaf(txv[r], zx[r], tyv[r] * zy[r]));
+      ox[r] = s1 * zx[r];
+      oy[r] = s1 * zy[r];
+    }
+    sts4(dst + j0, make_float4(oa[0], oa[1], oa[2], oa[3]));
+    sts4(dst + HP + j0, make_float4(ox[0], ox[1], ox[2], ox[3]));
+    sts4(dst + 2 * HP + j0, make_float4(oy[0], oy[1], oy[2], oy[3]));
+  }
+}
 
 // ---------------------------------------------------------------------------
-template <int H, int D, int C, int MODE>
+template <int H, int D, int C, int ACT, int MODE>
 __global__ void __launch_bounds__(kThreads, 2) step_kernel(const StepArgs a) {
   using LY = Layout<H, D, C>;
   constexpr int HP = LY::HP;
@@ -539,7 +566,8 @@ __global__ void __launch_bounds__(kThreads, 2) step_kernel(const StepArgs a) {
   extern __shared__ __align__(128) float smem[];
   float* sW0 = smem + LY::OFF_W;
   float* sWh = sW0 + LY::W0F;
-  float* sWd = sWh + (D - 1) * LY::WHF;
+  float* sWT = sWh + (D - 1) * LY::WHF;  // transposed last hidden layer
+  float* sWd = sWT + LY::WTF;
   float* sEx = smem + LY::OFF_EX;
   double* sRed = reinterpret_cast<double*>(smem + LY::OFF_RED);
   float* sCell = smem + LY::OFF_CELL;  // [0,128) r^2 sums, [128,256) eps-grad sums
@@ -551,7 +579,6 @@ __global__ void __launch_bounds__(kThreads, 2) step_kernel(const StepArgs a) {
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const NetDesc& net = a.net;
-  const int sig = net.sigmoid;
   const float* P = a.params;
 
   // ---- weights -> SMEM (zero-padded to the template width) ----
@@ -567,11 +594,13 @@ __global__ void __launch_bounds__(kThreads, 2) step_kernel(const StepArgs a) {
   for (int l = 1; l < D; ++l) {
     float* W = sWh + (l - 1) * LY::WHF;
     const int fi = net.in_w[l], fo = net.out_w[l];
+    const bool transpose = (LY::WTF > 0) && l == D - 1;
     for (int e = tid; e < LY::WHF; e += kThreads) {
       float v = 0.f;
       if (e < HP * HP) {
         const int i = e / HP, j = e - i * HP;
         if (i < fo && j < fi) v = P[net.w_off[l] + i * fi + j];
+        if (transpose) sWT[j * HP + i] = v;
       } else {
         const int i = e - HP * HP;
         if (i < fo) v = P[net.b_off[l] + i];
@@ -611,6 +640,7 @@ __global__ void __launch_bounds__(kThreads, 2) step_kernel(const StepArgs a) {
   const int n_tiles = (MODE == kModeForward) ? (a.n_fwd + kThreads - 1) / kThreads : a.n_tiles;
   const int n_pts_all = a.n_int + a.n_bnd + a.n_sen;
 
+#pragma unroll 1
   for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
     // ---- tile geometry ----
     bool interior = false;
@@ -640,90 +670,104 @@ __global__ void __launch_bounds__(kThreads, 2) step_kernel(const StepArgs a) {
     if (MODE == kModeFused && interior && tid == 0) {
       for (int c = 0; c < 2 && c < nchunks; ++c) {
         const int r0 = c * a.chunk_rows;
-        issue_chunk(a, cell0, r0, min(a.chunk_rows, nrows_tile - r0), sUnion + c * a.stage_floats,
-                    &bars[c]);
+        issue_chunk(a, cell0, r0, min(a.chunk_rows, nrows_tile - r0), sUnion + c * a.stage_floats, &bars[c]);
       }
     }
 
     const bool valid = tid < np;
-    {
-      float2 xy = make_float2(0.f, 0.f);
-      if (valid) xy = (MODE == kModeForward) ? a.fwd_pts[pbase + tid] : a.pts[pbase + tid];
-      sEx[kExX * kThreads + tid] = xy.x;
-      sEx[kExY * kThreads + tid] = xy.y;
+    float px = 0.f, py = 0.f;
+    if (valid) {
+      const float2 xy = (MODE == kModeForward) ? a.fwd_pts[pbase + tid] : a.pts[pbase + tid];
+      px = xy.x;
+      py = xy.y;
     }
+    sEx[kExX * kThreads + tid] = px;
+    sEx[kExY * kThreads + tid] = py;
 
     // =================== forward (network.hpp:239-281) ===================
     float* srow = sState + tid * SROW;
-    const float px = sEx[kExX * kThreads + tid], py = sEx[kExY * kThreads + tid];
-    float lz[kLastRegs ? H : 1], lt[kLastRegs ? H : 1], lu[kLastRegs ? H : 1];
+    float lz[kLastRegs ? HP : 1], lt[kLastRegs ? HP : 1], lu[kLastRegs ? HP : 1];
     {
       float z0[H], t0[H], u0[H];
 #pragma unroll
       for (int i = 0; i < H; ++i) {
         const float4 w = lds4(sW0 + 4 * i);
-        const float A = fmaf(w.y, py, w.x * px) + w.z;
-        const float z = act_value(sig, A);
-        const float s1 = act_s1(sig, z);
+        const float z = Act<ACT>::value(fmaf(w.y, py, w.x * px) + w.z);
+        const float s1 = Act<ACT>::s1(z);
         z0[i] = z;
-        t0[i] = s1 * w.x;  // TAx_0 = W0 e_x
+        t0[i] = s1 * w.x;  // TX_1 = s1 (W0 e_x)
         u0[i] = s1 * w.y;
       }
       if constexpr (D == 1) {
         if constexpr (kLastRegs) {
 #pragma unroll
-          for (int i = 0; i < H; ++i) { lz[i] = z0[i]; lt[i] = t0[i]; lu[i] = u0[i]; }
-        } else {
-          float* blk = srow + (LY::kBlocks - 1) * 3 * HP;
-          store_vec<H>(blk, z0); store_vec<H>(blk + HP, t0); store_vec<H>(blk + 2 * HP, u0);
-        }
-      } else {
-        // layer 1 consumes the layer-0 registers directly
-        const float* W1 = sWh;
-        if constexpr (D == 2) {
-          if constexpr (kLastRegs) {
-            hidden_to_regs<H, HP>(sig, W1, z0, t0, u0, lz, lt, lu);
-          } else {
-            hidden_to_block<H, HP>(sig, W1, z0, t0, u0, srow + (LY::kBlocks - 1) * 3 * HP);
+          for (int i = 0; i < HP; ++i) {
+            lz[i] = i < H ? z0[i] : 0.f;
+            lt[i] = i < H ? t0[i] : 0.f;
+            lu[i] = i < H ? u0[i] : 0.f;
           }
         } else {
-          hidden_to_block<H, HP>(sig, W1, z0, t0, u0, srow);  // block 0 = hidden 1
+          float* blk = srow + (LY::kBlocks - 1) * 3 * HP;
+          store_vec<H>(blk, z0);
+          store_vec<H>(blk + HP, t0);
+          store_vec<H>(blk + 2 * HP, u0);
         }
+      } else if constexpr (D == 2 && kLastRegs) {
+        // layer 1 is the last hidden layer: stage the layer-0 state in block 0
+        store_vec<H>(srow, z0);
+        store_vec<H>(srow + HP, t0);
+        store_vec<H>(srow + 2 * HP, u0);
+      } else if constexpr (D == 2) {
+        hidden_to_block<H, HP, ACT>(sWh, z0, t0, u0, srow + (LY::kBlocks - 1) * 3 * HP);
+      } else {
+        hidden_to_block<H, HP, ACT>(sWh, z0, t0, u0, srow);  // block 0 = hidden 1
       }
     }
-#pragma unroll
-    for (int l = 2; l < D; ++l) {
-      // input = hidden l-1 in block l-2
+    // middle hidden layers 2..D-2 (register inputs loaded from the previous block)
+#pragma unroll 1
+    for (int l = 2; l < D - 1; ++l) {
       float xz[H], xt[H], xu[H];
-      load3<H>(srow + (l - 2) * 3 * HP, HP, xz, xt, xu);
-      const float* W = sWh + (l - 1) * LY::WHF;
-      if (l == D - 1) {
-        if constexpr (kLastRegs) {
-          hidden_to_regs<H, HP>(sig, W, xz, xt, xu, lz, lt, lu);
-        } else {
-          hidden_to_block<H, HP>(sig, W, xz, xt, xu, srow + (LY::kBlocks - 1) * 3 * HP);
-        }
-      } else {
-        hidden_to_block<H, HP>(sig, W, xz, xt, xu, srow + (l - 1) * 3 * HP);
+      load_vec<H>(srow + (l - 2) * 3 * HP, xz);
+      load_vec<H>(srow + (l - 2) * 3 * HP + HP, xt);
+      load_vec<H>(srow + (l - 2) * 3 * HP + 2 * HP, xu);
+      hidden_to_block<H, HP, ACT>(sWh + (l - 1) * LY::WHF, xz, xt, xu, srow + (l - 1) * 3 * HP);
+    }
+    // last hidden layer D-1 >= 1
+    if constexpr (D >= 2) {
+      const float* Wl = sWh + (D - 2) * LY::WHF;
+      if constexpr (kLastRegs) {
+        const float* in_blk = (D == 2) ? srow : srow + (D - 3) * 3 * HP;
+        hidden_block_to_regs<H, HP, ACT>(sWT, Wl + HP * HP, in_blk, lz, lt, lu);
+      } else if constexpr (D >= 3) {
+        float xz[H], xt[H], xu[H];
+        load_vec<H>(srow + (D - 3) * 3 * HP, xz);
+        load_vec<H>(srow + (D - 3) * 3 * HP + HP, xt);
+        load_vec<H>(srow + (D - 3) * 3 * HP + 2 * HP, xu);
+        hidden_to_block<H, HP, ACT>(Wl, xz, xt, xu, srow + (LY::kBlocks - 1) * 3 * HP);
       }
     }
     // output layer (linear): u, du/dx, du/dy; channel 1 -> eps head
     {
-      float hz[H], ht[H], hu[H];
+      float u = 0.f, ux = 0.f, uy = 0.f, y1 = 0.f;
       if constexpr (kLastRegs) {
 #pragma unroll
-        for (int j = 0; j < H; ++j) { hz[j] = lz[j]; ht[j] = lt[j]; hu[j] = lu[j]; }
+        for (int j = 0; j < H; ++j) {
+          const float w = sWd[j];
+          u = fmaf(w, lz[j], u);
+          ux = fmaf(w, lt[j], ux);
+          uy = fmaf(w, lu[j], uy);
+          if constexpr (C == 2) y1 = fmaf(sWd[HP + j], lz[j], y1);
+        }
       } else {
-        load3<H>(srow + (LY::kBlocks - 1) * 3 * HP, HP, hz, ht, hu);
-      }
-      float u = 0.f, ux = 0.f, uy = 0.f, y1 = 0.f;
-#pragma unroll
-      for (int j = 0; j < H; ++j) {
-        const float w = sWd[j];
-        u = fmaf(w, hz[j], u);
-        ux = fmaf(w, ht[j], ux);
-        uy = fmaf(w, hu[j], uy);
-        if constexpr (C == 2) y1 = fmaf(sWd[HP + j], hz[j], y1);
+        const float* blk = srow + (LY::kBlocks - 1) * 3 * HP;
+#pragma unroll 2
+        for (int j = 0; j < H; ++j) {
+          const float w = sWd[j];
+          u = fmaf(w, blk[j], u);
+          ux = fmaf(w, blk[HP + j], ux);
+          uy = fmaf(w, blk[2 * HP + j], uy);
+          if constexpr (C == 2) y1 = fmaf(sWd[HP + j], blk[j], y1);
+        }
       }
       u += sWd[C * HP];
       if constexpr (C == 2) y1 += sWd[C * HP + 1];
@@ -779,6 +823,7 @@ __global__ void __launch_bounds__(kThreads, 2) step_kernel(const StepArgs a) {
       float* rbarv = sRows;
       float* rsqv = sRows + rows4;
       float* rgev = sRows + 2 * rows4;
+#pragma unroll 1
       for (int c = 0; c < nchunks; ++c) {
         const int st = c & 1;
         const int r0 = c * a.chunk_rows;
@@ -799,6 +844,7 @@ __global__ void __launch_bounds__(kThreads, 2) step_kernel(const StepArgs a) {
           const float* gxr = Gx + r * a.Q;
           const float* gyr = Gy + r * a.Q;
           float gx = 0.f, gy = 0.f;
+#pragma unroll 5
           for (int q = 0; q < a.Q; ++q) {
             gx = fmaf(gxr[q], sx[q], gx);
             gy = fmaf(gyr[q], sy[q], gy);
@@ -808,6 +854,7 @@ __global__ void __launch_bounds__(kThreads, 2) step_kernel(const StepArgs a) {
             const float* cv = sEx + kExCv * kThreads + kk * a.Q;
             const float* tr = Tv + r * a.Q;
             float t = 0.f;
+#pragma unroll 5
             for (int q = 0; q < a.Q; ++q) t = fmaf(tr[q], cv[q], t);
             res += t;
           }
@@ -821,6 +868,7 @@ __global__ void __launch_bounds__(kThreads, 2) step_kernel(const StepArgs a) {
         // phase B: one thread per point: adjoint contributions of the chunk rows
         if (valid) {
           const int lo = max(r0, myk * a.T), hi = min(r0 + nr, (myk + 1) * a.T);
+#pragma unroll 5
           for (int gr = lo; gr < hi; ++gr) {
             const int r = gr - r0;
             const float rb = rbarv[r];
@@ -910,9 +958,16 @@ __global__ void __launch_bounds__(kThreads, 2) step_kernel(const StepArgs a) {
       float hz[H], ht[H], hu[H];
       if constexpr (kLastRegs) {
 #pragma unroll
-        for (int j = 0; j < H; ++j) { hz[j] = lz[j]; ht[j] = lt[j]; hu[j] = lu[j]; }
+        for (int j = 0; j < H; ++j) {
+          hz[j] = lz[j];
+          ht[j] = lt[j];
+          hu[j] = lu[j];
+        }
       } else {
-        load3<H>(srow + (LY::kBlocks - 1) * 3 * HP, HP, hz, ht, hu);
+        const float* blk = srow + (LY::kBlocks - 1) * 3 * HP;
+        load_vec<H>(blk, hz);
+        load_vec<H>(blk + HP, ht);
+        load_vec<H>(blk + 2 * HP, hu);
       }
       __syncthreads();  // union (slab) free; exchange reads done
       float csum[C][(H + 32) / 32];
@@ -931,6 +986,7 @@ __global__ void __launch_bounds__(kThreads, 2) step_kernel(const StepArgs a) {
           const int col = lane + 32 * s;
           float acc = 0.f;
           if (col <= H)
+#pragma unroll 4
             for (int p = 0; p < 32; ++p) acc += Gbuf[(wrow + p) * SG + col];
           csum[c][s] = acc;
         }
@@ -967,7 +1023,7 @@ __global__ void __launch_bounds__(kThreads, 2) step_kernel(const StepArgs a) {
         float xb = sWd[j] * ub;
         if constexpr (C == 2) xb = fmaf(sWd[HP + j], ab1, xb);
         const float zx = sWd[j] * uxb, zy = sWd[j] * uyb;
-        const float s1 = act_s1(sig, hz[j]), kp = act_kap(sig, hz[j]);
+        const float s1 = Act<ACT>::s1(hz[j]), kp = Act<ACT>::kap(hz[j]);
         gA[j] = fmaf(s1, xb, kp * fmaf(ht[j], zx, hu[j] * zy));
         gX[j] = s1 * zx;
         gY[j] = s1 * zy;
@@ -977,10 +1033,10 @@ __global__ void __launch_bounds__(kThreads, 2) step_kernel(const StepArgs a) {
 
     // ---- hidden layers l = D-1 .. 1 ----
     {
-      RevCtx rc{sState, srow, Gbuf, Part, sW0, sWh, &net, sig, px, py, tid, lane, warp};
-      if constexpr (D >= 4) reverse_hidden<H, D, C, 3>(rc, gA, gX, gY, greg);
-      if constexpr (D >= 3) reverse_hidden<H, D, C, 2>(rc, gA, gX, gY, greg);
-      if constexpr (D >= 2) reverse_hidden<H, D, C, 1>(rc, gA, gX, gY, greg);
+      RevCtx rc{sState, srow, Gbuf, Part, sW0, sWh, &net, px, py, tid, lane, warp};
+      if constexpr (D >= 4) reverse_hidden<H, D, C, ACT, 3>(rc, gA, gX, gY, greg);
+      if constexpr (D >= 3) reverse_hidden<H, D, C, ACT, 2>(rc, gA, gX, gY, greg);
+      if constexpr (D >= 2) reverse_hidden<H, D, C, ACT, 1>(rc, gA, gX, gY, greg);
     }
     if constexpr (D == 1) {
       // G_0 came straight from the output layer (registers)
@@ -998,6 +1054,7 @@ __global__ void __launch_bounds__(kThreads, 2) step_kernel(const StepArgs a) {
         const int i = lane + 32 * s;
         float ax = 0.f, ay = 0.f, aa = 0.f, tx = 0.f, ty = 0.f;
         if (i < H) {
+#pragma unroll 4
           for (int p = 0; p < 32; ++p) {
             const float* row = sState + (wrow + p) * SROW;
             const float ga = row[i];
@@ -1044,7 +1101,7 @@ __global__ void __launch_bounds__(kThreads, 2) step_kernel(const StepArgs a) {
   if constexpr (MODE != kModeForward) {
     // ---- per-CTA outputs ----
     float* gout = a.grad_part + (size_t)blockIdx.x * net.n_params;
-#pragma unroll
+#pragma unroll 1
     for (int m = 0; m < LY::NGR; ++m) {
       const int e = tid + kThreads * m;
       if (e < net.n_params) gout[e] = greg[m];

@@ -12,38 +12,41 @@ namespace vpg {
 using StepFn = void (*)(StepArgs);
 
 struct Variant {
-  int H, D, C;
+  int H, D, C, ACT;
   StepFn fused, forward, reverse;
   int off_union;  // floats before the union
   int rev_need;   // floats the reverse phase needs in the union
   size_t (*smem)(int, int);
 };
 
-#define VPG_VARIANTS(X) \
-  X(30, 3, 1) X(30, 3, 2) X(20, 2, 1) X(20, 2, 2) X(50, 3, 1) X(16, 1, 1) X(16, 1, 2) X(16, 2, 1)
+// (hidden width, hidden layers, output channels, activation 0 tanh / 1 sigmoid)
+#define VPG_VARIANTS(X)                                                                          \
+  X(30, 3, 1, 0) X(30, 3, 2, 0) X(20, 2, 1, 0) X(20, 2, 2, 0) X(50, 3, 1, 0) X(16, 1, 1, 0)      \
+  X(16, 1, 2, 0) X(16, 2, 1, 0) X(16, 1, 1, 1) X(16, 2, 1, 1) X(30, 3, 1, 1)
 
-#define VPG_DECL(H, D, C) Variant variant_##H##_##D##_##C();
+#define VPG_DECL(H, D, C, A) Variant variant_##H##_##D##_##C##_##A();
 VPG_VARIANTS(VPG_DECL)
 #undef VPG_DECL
 
 #ifdef VPG_DEFINE_VARIANT
-template <int H, int D, int C>
+template <int H, int D, int C, int A>
 Variant make_variant() {
   using LY = Layout<H, D, C>;
   Variant v;
   v.H = H;
   v.D = D;
   v.C = C;
-  v.fused = step_kernel<H, D, C, kModeFused>;
-  v.forward = step_kernel<H, D, C, kModeForward>;
-  v.reverse = step_kernel<H, D, C, kModeReverse>;
+  v.ACT = A;
+  v.fused = step_kernel<H, D, C, A, kModeFused>;
+  v.forward = step_kernel<H, D, C, A, kModeForward>;
+  v.reverse = step_kernel<H, D, C, A, kModeReverse>;
   v.off_union = LY::OFF_UNION;
   v.rev_need = LY::REV_NEED;
   v.smem = [](int u, int r) { return step_smem_bytes<H, D, C>(u, r); };
   return v;
 }
-#define VPG_DEFINE(H, D, C) \
-  Variant variant_##H##_##D##_##C() { return make_variant<H, D, C>(); }
+#define VPG_DEFINE(H, D, C, A) \
+  Variant variant_##H##_##D##_##C##_##A() { return make_variant<H, D, C, A>(); }
 #endif
 
 }  // namespace vpg

@@ -80,7 +80,7 @@ struct DBuf {
 // instantiated in its own translation unit (variant_H_D_C.cu)
 using vpg::Variant;
 const std::vector<Variant>& variants() {
-#define VPG_ITEM(H, D, C) vpg::variant_##H##_##D##_##C(),
+#define VPG_ITEM(H, D, C, A) vpg::variant_##H##_##D##_##C##_##A(),
   static const std::vector<Variant> v = {VPG_VARIANTS(VPG_ITEM)};
 #undef VPG_ITEM
   return v;
@@ -175,7 +175,7 @@ struct vpinn_gpu_ctx {
   void* comm = nullptr;
   int nranks = 1, rank = 0;
   long long launches = 0;
-  bool adam_fresh = true;
+  DBuf<char> flush;  // L2 flush scratch (bench)
 
   ~vpinn_gpu_ctx() {
     if (device >= 0) cudaSetDevice(device);
@@ -529,12 +529,14 @@ int vpinn_gpu_create(const vpinn_gpu_problem* pb, vpinn_gpu_ctx** out) {
     if (pb->activation != VPINN_ACT_TANH && pb->activation != VPINN_ACT_SIGMOID)
       throw Fail{VPINN_ERR_CONFIG, "activation must be tanh or sigmoid"};
     const Variant* var = nullptr;
+    const int act = pb->activation == VPINN_ACT_SIGMOID ? 1 : 0;
     for (const auto& v : variants())
-      if (v.D == D && v.C == C && v.H >= maxH && (!var || v.H < var->H)) var = &v;
+      if (v.D == D && v.C == C && v.ACT == act && v.H >= maxH && (!var || v.H < var->H)) var = &v;
     if (!var)
       throw Fail{VPINN_ERR_CONFIG, "network shape not instantiated for the GPU path (hidden layers " +
                                        std::to_string(D) + ", width " + std::to_string(maxH) +
-                                       ", outputs " + std::to_string(C) + ")"};
+                                       ", outputs " + std::to_string(C) + ", activation " +
+                                       (act ? "sigmoid" : "tanh") + ")"};
     const bool conv = pb->bx != 0.0f || pb->by != 0.0f;
     if (conv && !pb->test) throw Fail{VPINN_ERR_NUMERIC, "convection needs the test tensor"};
     const int W = std::max(1, pb->world_size), R = pb->rank;
@@ -1059,6 +1061,43 @@ int vpinn_gpu_profile_step(vpinn_gpu_ctx* c, int reps, double* ms_mlp, double* m
     *ms_mlp = t[0] / reps;
     *ms_reduce = t[1] / reps;
     *ms_adam = t[2] / reps;
+  });
+}
+
+int vpinn_gpu_flush_l2(vpinn_gpu_ctx* c) {
+  return guarded([&] {
+    set_dev(c);
+    if (!c->flush.p) c->flush.alloc((size_t)256 << 20);
+    CK(cudaMemsetAsync(c->flush.p, (int)(c->launches & 0xff), (size_t)256 << 20, c->stream));
+  });
+}
+
+int vpinn_gpu_measure_ffma_peak(int device, double* tflops) {
+  return guarded([&] {
+    CK(cudaSetDevice(device));
+    cudaDeviceProp prop;
+    CK(cudaGetDeviceProperties(&prop, device));
+    DBuf<float> out;
+    out.alloc(256);
+    const int blocks = prop.multiProcessorCount * 8, iters = 4096;
+    cudaEvent_t e0, e1;
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    double best = 0.0;
+    for (int r = 0; r < 5; ++r) {
+      CK(cudaEventRecord(e0));
+      vpg::ffma_peak_kernel<<<blocks, 256>>>(out.p, iters, 0.999999f, 1e-7f);
+      CK(cudaGetLastError());
+      CK(cudaEventRecord(e1));
+      CK(cudaEventSynchronize(e1));
+      float ms = 0;
+      CK(cudaEventElapsedTime(&ms, e0, e1));
+      const double flops = 2.0 * 8 * 16 * (double)iters * 256.0 * blocks;
+      if (r > 0) best = std::max(best, flops / (ms * 1e-3) / 1e12);
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    *tflops = best;
   });
 }
 

@@ -176,6 +176,9 @@ class GpuStep:
         _capi.check(_capi.lib().vpinn_gpu_profile_step(self.h, reps, C.byref(a), C.byref(b), C.byref(c)))
         return a.value, b.value, c.value
 
+    def flush_l2(self):
+        _capi.check(_capi.lib().vpinn_gpu_flush_l2(self.h))
+
     def launch_count(self):
         return _capi.lib().vpinn_gpu_launch_count(self.h)
 
