@@ -134,6 +134,12 @@ const char* vpinn_gpu_version(void);
 /* 1 if a device the kernels were built for is present, else 0. */
 int vpinn_gpu_device_ok(void);
 
+/* The multi-GPU partition vpinn_gpu_create applies (pure host function):
+ * out6 = {e0, e1, b0, b1, s0, s1}, rank owns cells [e0, e1), boundary
+ * points [b0, b1), sensors [s0, s1): floor(r*N/W) .. floor((r+1)*N/W). */
+void vpinn_gpu_partition(int64_t n_elem, int64_t n_boundary, int64_t n_sensors, int rank, int world,
+                         int64_t* out6);
+
 int vpinn_gpu_create(const vpinn_gpu_problem* problem, vpinn_gpu_ctx** out);
 void vpinn_gpu_destroy(vpinn_gpu_ctx* ctx);
 

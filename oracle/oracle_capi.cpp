@@ -338,6 +338,31 @@ int vo_loss_and_grad(void* h, const void* params, double* parts, void* grad) {
   });
 }
 
+// objective + gradient of the rank sub-problem (cells [e0,e1), boundary
+// [b0,b1), sensors [s0,s1)), penalties normalised by the global counts
+int vo_loss_and_grad_part(void* h, const void* params, long long e0, long long e1, long long b0,
+                          long long b1, long long s0, long long s1, double* parts, void* grad) {
+  return guard([&] {
+    auto run = [&](auto tag) {
+      using Real = decltype(tag);
+      auto& pb = prob<Real>(h);
+      const vo::Problem<Real> sub = vo::partition(pb, e0, e1, b0, b1, s0, s1);
+      std::vector<Real> par = vec_of<Real>(params, pb.shape.count()), g;
+      vo::Parts<Real> pp;
+      const Real tot = vo::loss_and_grad(sub, par, g, pp);
+      parts[0] = tot;
+      parts[1] = pp.v;
+      parts[2] = pp.b;
+      parts[3] = pp.s;
+      copy_out(g, grad);
+    };
+    if (vo_is_double(h))
+      run(double{});
+    else
+      run(float{});
+  });
+}
+
 int vo_evaluate(void* h, const void* params, const double* xy, long long n, int order, void* u,
                 void* ux, void* uy, void* eps) {
   return guard([&] {

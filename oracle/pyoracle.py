@@ -73,6 +73,8 @@ def _declare(L):
     L.vo_get_array.argtypes = [vp, C.c_int, vp]
     L.vo_loss_and_grad.argtypes = [vp, vp, C.POINTER(C.c_double), vp]
     L.vo_evaluate.argtypes = [vp, vp, vp, C.c_longlong, C.c_int, vp, vp, vp, vp]
+    ll = C.c_longlong
+    L.vo_loss_and_grad_part.argtypes = [vp, vp, ll, ll, ll, ll, ll, ll, C.POINTER(C.c_double), vp]
     L.vo_var_loss.argtypes = [vp, C.c_int, vp, vp, vp, vp, C.c_int, C.c_double,
                               C.POINTER(C.c_double), vp, vp, vp, vp, vp]
     L.vo_train.argtypes = [vp, vp, C.POINTER(OracleTrainSpec), vp, C.POINTER(C.c_longlong),
@@ -270,6 +272,14 @@ class OracleProblem:
         parts = (C.c_double * 4)()
         grad = np.zeros(self.n_params, dtype=self.dtype)
         _check(lib().vo_loss_and_grad(self.h, _p(par), parts, _p(grad)))
+        return np.array(list(parts)), grad
+
+    def loss_and_grad_part(self, params, e0, e1, b0, b1, s0, s1):
+        """Rank sub-problem objective (global penalty normalisation)."""
+        par = np.ascontiguousarray(params, dtype=self.dtype)
+        parts = (C.c_double * 4)()
+        grad = np.zeros(self.n_params, dtype=self.dtype)
+        _check(lib().vo_loss_and_grad_part(self.h, _p(par), e0, e1, b0, b1, s0, s1, parts, _p(grad)))
         return np.array(list(parts)), grad
 
     def evaluate(self, params, points, order=1):

@@ -69,6 +69,7 @@ def _declare(L):
         "vpinn_gpu_last_error": (C.c_char_p, []),
         "vpinn_gpu_version": (C.c_char_p, []),
         "vpinn_gpu_device_ok": (i32, []),
+        "vpinn_gpu_partition": (None, [i64, i64, i64, i32, i32, vp]),
         "vpinn_gpu_create": (i32, [C.POINTER(Problem), C.POINTER(vp)]),
         "vpinn_gpu_destroy": (None, [vp]),
         "vpinn_gpu_param_count": (i32, [vp]),
@@ -115,6 +116,13 @@ class VpinnError(RuntimeError):
     def __init__(self, code: int, msg: str):
         super().__init__(f"[{code}] {msg}")
         self.code = code
+
+
+def partition(n_elem, n_boundary, n_sensors, rank, world):
+    """The rank's (e0, e1, b0, b1, s0, s1) exactly as vpinn_gpu_create splits."""
+    out = (C.c_int64 * 6)()
+    lib().vpinn_gpu_partition(n_elem, n_boundary, n_sensors, rank, world, out)
+    return tuple(out)
 
 
 def check(rc: int):

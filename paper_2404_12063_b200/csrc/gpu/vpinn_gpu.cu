@@ -7,6 +7,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <cstdlib>
 #include <limits>
 #include <map>
 #include <memory>
@@ -17,6 +18,7 @@
 #include <nccl.h>
 
 #include "aux_kernels.cuh"
+#include "contract_cells.cuh"
 #include "variant.h"
 #include "vpinn_gpu.h"
 
@@ -167,6 +169,10 @@ struct vpinn_gpu_ctx {
   // split path
   DBuf<float> fu, fux, fuy, feps, uxb, uyb, eb, ub, e_scalar;
   vpg::ContractArgs cargs{};
+  vpg::CellContractArgs ccargs{};  // fast path when Q <= 128
+  bool cell_contract = false;
+  int grid_cc = 0;
+  size_t smem_cc = 0;
   int grid_contract = 0, grid_pen = 0, grid_fwd = 0;
   size_t smem_contract = 0, smem_fwd = 0;
   // graphs
@@ -314,11 +320,53 @@ void configure(vpinn_gpu_ctx* c) {
     c->grid_contract = std::max(1, std::min(std::max(1, ca.n_tiles), std::max(1, occ) * c->sm_count));
     c->grid_pen = (c->n_bnd + c->n_sen) ? std::min(64, ceil_div(c->n_bnd + c->n_sen, 256)) : 0;
   }
+  // ---- whole-cell HBM-streaming contraction (Q <= 128) ----
+  c->cell_contract = c->Q <= vpg::kCCThreads && c->T <= vpg::kCCThreads && c->E > 0;
+  if (c->cell_contract) {
+    vpg::CellContractArgs& cc = c->ccargs;
+    std::memset(&cc, 0, sizeof(cc));
+    for (int t = 0; t < 3; ++t) cc.tens[t] = c->tens[t].p;
+    cc.forcing = c->forcing.p;
+    cc.E = c->E;
+    cc.T = c->T;
+    cc.Q = c->Q;
+    cc.nt = c->nt;
+    cc.cc = std::max(1, std::min(vpg::kCCThreads / c->Q, vpg::kCCThreads / c->T));
+    if (const char* e = std::getenv("VPINN_CC_CELLS")) cc.cc = std::max(1, std::min(cc.cc, std::atoi(e)));
+    cc.tstride = round4(cc.cc * c->T * c->Q + 8);
+    cc.vstride = round4(cc.cc * c->Q + 8);
+    cc.fstride = round4(cc.cc * c->T + 8);
+    cc.stage_floats = c->nt * cc.tstride + 3 * cc.vstride + cc.fstride;
+    cc.e_fixed = c->eps;
+    cc.eps_source = c->eps_source;
+    cc.bx = c->bx;
+    cc.by = c->by;
+    cc.rscale = a.rscale;
+    cc.inv_nt = a.inv_nt;
+    cc.nstage = 4;
+    size_t cc_budget = two_cta;
+    if (const char* e = std::getenv("VPINN_CC_ONE_CTA")) cc_budget = std::atoi(e) ? (size_t)227 * 1024 : two_cta;
+    while (cc.nstage > 2 && vpg::cell_contract_smem_bytes(cc.stage_floats, cc.nstage) > cc_budget) --cc.nstage;
+    if (const char* e = std::getenv("VPINN_CC_STAGES")) cc.nstage = std::max(2, std::min(4, std::atoi(e)));
+    cc.use_ldgsts = 0;  // TMA bulk by default; LDGSTS measured equal
+    if (const char* e = std::getenv("VPINN_CC_LDGSTS")) cc.use_ldgsts = std::atoi(e);
+    c->smem_cc = vpg::cell_contract_smem_bytes(cc.stage_floats, cc.nstage);
+    if (c->smem_cc > (size_t)227 * 1024) {
+      c->cell_contract = false;
+    } else {
+      CK(cudaFuncSetAttribute(vpg::contract_cells_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)c->smem_cc));
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, vpg::contract_cells_kernel, vpg::kCCThreads,
+                                                       c->smem_cc));
+      const int chunks = ceil_div(c->E, cc.cc);
+      c->grid_cc = std::max(1, std::min(chunks, std::max(1, occ) * c->sm_count));
+    }
+  }
   if (c->split) c->loss_rows = c->grid_contract + c->grid_pen + c->grid_step;
 
   // ---- buffers sized by the grids ----
   c->grad_part.alloc((size_t)c->grad_rows * c->n_params);
-  c->loss_part.alloc((size_t)std::max(c->loss_rows, c->grid_contract) * vpg::kLpWords);
+  c->loss_part.alloc((size_t)std::max(c->loss_rows, std::max(c->grid_contract, c->grid_cc)) * vpg::kLpWords);
   c->red.alloc((size_t)c->n_params + vpg::kLpWords);
   a.grad_part = c->grad_part.p;
   if (c->split) {
@@ -475,6 +523,50 @@ cudaGraphExec_t graph_for(vpinn_gpu_ctx* c, int kind, int steps, double lr, bool
   return ex;
 }
 
+// standalone contraction on device-resident derivatives: the whole-cell
+// streaming kernel when a cell fits a CTA, the generic row-chunked one else.
+// Returns the number of loss rows written.
+int launch_contract(vpinn_gpu_ctx* c, const float* ux, const float* uy, const float* eps, float* uxb,
+                    float* uyb, float* eb, float* res, const float* e_param, float rscale, double* loss_part,
+                    const int* stop) {
+  if (c->cell_contract) {
+    vpg::CellContractArgs a = c->ccargs;
+    a.ux = ux;
+    a.uy = uy;
+    a.eps = eps;
+    a.uxb = uxb;
+    a.uyb = uyb;
+    a.eb = eb;
+    a.res = res;
+    a.e_param = e_param;
+    a.rscale = rscale;
+    a.loss_part = loss_part;
+    a.stop_flag = stop;
+    vpg::contract_cells_kernel<<<c->grid_cc, vpg::kCCThreads, c->smem_cc, c->stream>>>(a);
+    CK(cudaGetLastError());
+    c->launches += 1;
+    return c->grid_cc;
+  }
+  vpg::ContractArgs ca = c->cargs;
+  ca.ux = ux;
+  ca.uy = uy;
+  ca.eps = eps;
+  ca.uxb = uxb;
+  ca.uyb = uyb;
+  ca.eb = eb;
+  ca.res = res;
+  ca.e_param = e_param;
+  ca.rscale = rscale;
+  ca.loss_part = loss_part;
+  ca.stop_flag = stop;
+  if (ca.n_tiles > 0) {
+    vpg::contract_kernel<<<c->grid_contract, vpg::kCThreads, c->smem_contract, c->stream>>>(ca);
+    CK(cudaGetLastError());
+    c->launches += 1;
+  }
+  return c->grid_contract;
+}
+
 long long launches_per_epoch(const vpinn_gpu_ctx* c) {
   long long n = 3;  // step kernel(s) + reduce + adam
   if (c->split) n = 2 + 2 + (c->cargs.n_tiles > 0) + (c->grid_pen > 0);
@@ -489,6 +581,17 @@ extern "C" {
 const char* vpinn_gpu_last_error(void) { return g_err.c_str(); }
 
 const char* vpinn_gpu_version(void) { return "vpinn-b200 0.1 (sm_100a)"; }
+
+void vpinn_gpu_partition(int64_t n_elem, int64_t n_boundary, int64_t n_sensors, int rank, int world,
+                         int64_t* out6) {
+  const int64_t W = world < 1 ? 1 : world, r = rank;
+  out6[0] = n_elem * r / W;
+  out6[1] = n_elem * (r + 1) / W;
+  out6[2] = n_boundary * r / W;
+  out6[3] = n_boundary * (r + 1) / W;
+  out6[4] = n_sensors * r / W;
+  out6[5] = n_sensors * (r + 1) / W;
+}
 
 int vpinn_gpu_device_ok(void) {
   int n = 0;
@@ -581,9 +684,9 @@ int vpinn_gpu_create(const vpinn_gpu_problem* pb, vpinn_gpu_ctx** out) {
 
     // ---- partition (rank r owns contiguous cells / penalty points) ----
     const long long E = pb->n_elem, NB = pb->n_boundary, NS = pb->n_sensors;
-    const long long e0 = E * R / W, e1 = E * (R + 1) / W;
-    const long long b0 = NB * R / W, b1 = NB * (R + 1) / W;
-    const long long s0 = NS * R / W, s1 = NS * (R + 1) / W;
+    int64_t part[6];
+    vpinn_gpu_partition(E, NB, NS, R, W, part);
+    const long long e0 = part[0], e1 = part[1], b0 = part[2], b1 = part[3], s0 = part[4], s1 = part[5];
     c->E = (int)(e1 - e0);
     c->T = pb->n_test;
     c->Q = pb->n_quad;
@@ -902,29 +1005,14 @@ int vpinn_gpu_contract(vpinn_gpu_ctx* c, const float* du_dx, const float* du_dy,
     oeb.alloc(ni);
     res.alloc((size_t)c->E * c->T);
     es.alloc(1);
-    lp.alloc((size_t)c->grid_contract * vpg::kLpWords);
+    lp.alloc((size_t)std::max(c->grid_contract, c->grid_cc) * vpg::kLpWords);
     ux.upload(du_dx, ni, c->stream);
     uy.upload(du_dy, ni, c->stream);
     if (eps) ep.upload(eps, ni, c->stream);
     if (scalars) es.upload(scalars + c->eps_idx, 1, c->stream);
-    vpg::ContractArgs ca = c->cargs;
-    ca.ux = ux.p;
-    ca.uy = uy.p;
-    ca.eps = ep.p;
-    ca.uxb = oxb.p;
-    ca.uyb = oyb.p;
-    ca.eb = oeb.p;
-    ca.res = res.p;
-    ca.e_param = es.p;
-    ca.rscale = (2.0f * weight) * ca.inv_nt;
-    ca.loss_part = lp.p;
-    ca.stop_flag = nullptr;
-    if (ca.n_tiles > 0) {
-      vpg::contract_kernel<<<c->grid_contract, vpg::kCThreads, c->smem_contract, c->stream>>>(ca);
-      CK(cudaGetLastError());
-      c->launches += 1;
-    }
-    std::vector<double> hl((size_t)c->grid_contract * vpg::kLpWords);
+    const int rows = launch_contract(c, ux.p, uy.p, ep.p, oxb.p, oyb.p, oeb.p, res.p, es.p,
+                                     (2.0f * weight) * c->sargs.inv_nt, lp.p, nullptr);
+    std::vector<double> hl((size_t)rows * vpg::kLpWords);
     CK(cudaMemcpyAsync(hl.data(), lp.p, sizeof(double) * hl.size(), cudaMemcpyDeviceToHost, c->stream));
     if (residuals) CK(cudaMemcpyAsync(residuals, res.p, sizeof(float) * c->E * c->T, cudaMemcpyDeviceToHost, c->stream));
     if (du_dx_bar) CK(cudaMemcpyAsync(du_dx_bar, oxb.p, sizeof(float) * ni, cudaMemcpyDeviceToHost, c->stream));
@@ -933,7 +1021,7 @@ int vpinn_gpu_contract(vpinn_gpu_ctx* c, const float* du_dx, const float* du_dy,
       CK(cudaMemcpyAsync(eps_bar, oeb.p, sizeof(float) * ni, cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));
     double l = 0.0, g = 0.0;
-    for (int b = 0; b < c->grid_contract; ++b) {
+    for (int b = 0; b < rows; ++b) {
       l += hl[(size_t)b * vpg::kLpWords + vpg::kLpVar];
       g += hl[(size_t)b * vpg::kLpWords + vpg::kLpEpsGrad];
     }
@@ -955,18 +1043,7 @@ int vpinn_gpu_time_contract(vpinn_gpu_ctx* c, int reps, double* ms_per_launch, d
     oyb.alloc(ni);
     oeb.alloc(ni);
     es.alloc(1);
-    lp.alloc((size_t)c->grid_contract * vpg::kLpWords);
-    vpg::ContractArgs ca = c->cargs;
-    ca.ux = ux.p;
-    ca.uy = uy.p;
-    ca.eps = ep.p;
-    ca.uxb = oxb.p;
-    ca.uyb = oyb.p;
-    ca.eb = oeb.p;
-    ca.res = nullptr;
-    ca.e_param = es.p;
-    ca.loss_part = lp.p;
-    ca.stop_flag = nullptr;
+    lp.alloc((size_t)std::max(c->grid_contract, c->grid_cc) * vpg::kLpWords);
     // L2 flush buffer (> 126 MB L2) between launches so each launch streams HBM
     DBuf<char> flush;
     flush.alloc((size_t)256 << 20);
@@ -977,11 +1054,9 @@ int vpinn_gpu_time_contract(vpinn_gpu_ctx* c, int reps, double* ms_per_launch, d
     for (int r = 0; r < reps + 2; ++r) {
       CK(cudaMemsetAsync(flush.p, r & 0xff, (size_t)256 << 20, c->stream));
       CK(cudaEventRecord(e0, c->stream));
-      vpg::contract_kernel<<<c->grid_contract, vpg::kCThreads, c->smem_contract, c->stream>>>(ca);
-      CK(cudaGetLastError());
+      launch_contract(c, ux.p, uy.p, ep.p, oxb.p, oyb.p, oeb.p, nullptr, es.p, c->sargs.rscale, lp.p, nullptr);
       CK(cudaEventRecord(e1, c->stream));
       CK(cudaEventSynchronize(e1));
-      c->launches += 1;
       float ms = 0;
       CK(cudaEventElapsedTime(&ms, e0, e1));
       if (r >= 2) total += ms;
