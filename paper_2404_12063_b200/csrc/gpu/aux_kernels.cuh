@@ -8,49 +8,42 @@
 namespace vpg {
 
 // ---------------------------------------------------------------------------
-// reduce_kernel: red[p] = sum over CTA partials (fp64, fixed order);
-// red[n_params + w] = sum of loss word w over loss rows.
-// grid = ceil(n_params/32) + 1 CTAs of 256 threads; the last CTA reduces the
-// loss words.
-__global__ void __launch_bounds__(256) reduce_kernel(const float* __restrict__ grad_part,
-                                                     int n_grad_rows, int n_params,
-                                                     const double* __restrict__ loss_part,
-                                                     int n_loss_rows, double* __restrict__ red,
-                                                     const int* stop_flag) {
+// Cross-CTA reduction of the per-CTA partials (fp64, fixed order): one warp
+// per parameter over the param-major partial rows (all loads of a lane in
+// flight at once, then a fixed shuffle tree); the last warp of the grid sums
+// the loss words.  red = [gradient | loss words].
+constexpr int kRedThreads = 256;
+constexpr int kRedWarps = kRedThreads / 32;
+
+__device__ __forceinline__ void reduce_body(const float* __restrict__ grad_part, int n_rows, int stride,
+                                            int n_params, const double* __restrict__ loss_part, int n_loss_rows,
+                                            double* __restrict__ red) {
+  const int lane = threadIdx.x & 31;
+  const int gw = blockIdx.x * kRedWarps + (threadIdx.x >> 5);
+  if (gw < n_params) {
+    const float* row = grad_part + (size_t)gw * stride;
+    double acc = 0.0;
+#pragma unroll 4
+    for (int c = lane; c < n_rows; c += 32) acc += (double)row[c];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) red[gw] = acc;
+  } else if (gw == n_params && lane < kLpWords) {
+    double acc = 0.0;
+    for (int c = 0; c < n_loss_rows; ++c) acc += loss_part[(size_t)c * kLpWords + lane];
+    red[n_params + lane] = acc;
+  }
+}
+
+__host__ __device__ constexpr int reduce_grid(int n_params) { return (n_params + 1 + kRedWarps - 1) / kRedWarps; }
+
+__global__ void __launch_bounds__(kRedThreads) reduce_kernel(const float* __restrict__ grad_part, int n_rows,
+                                                             int stride, int n_params,
+                                                             const double* __restrict__ loss_part,
+                                                             int n_loss_rows, double* __restrict__ red,
+                                                             const int* stop_flag) {
   if (stop_flag != nullptr && *stop_flag != 0) return;
-  __shared__ double s[8][33];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const bool loss_block = blockIdx.x == gridDim.x - 1;
-  const int p = blockIdx.x * 32 + lane;
-  double acc = 0.0;
-  if (!loss_block) {
-    if (p < n_params) {
-      int c = warp;
-      // four independent loads in flight per thread
-      double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-      for (; c + 24 < n_grad_rows; c += 32) {
-        a0 += grad_part[(size_t)c * n_params + p];
-        a1 += grad_part[(size_t)(c + 8) * n_params + p];
-        a2 += grad_part[(size_t)(c + 16) * n_params + p];
-        a3 += grad_part[(size_t)(c + 24) * n_params + p];
-      }
-      for (; c < n_grad_rows; c += 8) a0 += grad_part[(size_t)c * n_params + p];
-      acc = (a0 + a1) + (a2 + a3);
-    }
-  } else if (lane < kLpWords) {
-    for (int c = warp; c < n_loss_rows; c += 8) acc += loss_part[(size_t)c * kLpWords + lane];
-  }
-  s[warp][lane] = acc;
-  __syncthreads();
-  if (warp == 0) {
-    double t = 0.0;
-    for (int w = 0; w < 8; ++w) t += s[w][lane];
-    if (!loss_block) {
-      if (p < n_params) red[p] = t;
-    } else if (lane < kLpWords) {
-      red[n_params + lane] = t;
-    }
-  }
+  reduce_body(grad_part, n_rows, stride, n_params, loss_part, n_loss_rows, red);
 }
 
 // ---------------------------------------------------------------------------
@@ -93,9 +86,8 @@ struct AdamArgs {
 // adam_step (trainer.hpp:34-59) + train-loop bookkeeping (trainer.hpp:316-370)
 // for one epoch.  One CTA of 1024 threads.  IEEE intrinsics keep the update
 // in the reference's operation order (no FMA contraction).
-__global__ void __launch_bounds__(1024) adam_kernel(const AdamArgs a) {
+__device__ __forceinline__ void adam_body(const AdamArgs& a) {
   TrainState* st = a.st;
-  if (st->stopped) return;
   const long long t = st->step + 1;
   const int n = a.n_params;
   const double* red = a.red;
@@ -201,6 +193,31 @@ __global__ void __launch_bounds__(1024) adam_kernel(const AdamArgs a) {
       st->stop_reason = reason;
     }
   }
+}
+
+__global__ void __launch_bounds__(1024) adam_kernel(const AdamArgs a) {
+  if (a.st->stopped) return;
+  adam_body(a);
+}
+
+// single-GPU epoch tail: the cross-CTA reduction of reduce_kernel, then the
+// last CTA to finish (atomic ticket, release/acquire fences) applies Adam
+__global__ void __launch_bounds__(kRedThreads) reduce_adam_kernel(const float* __restrict__ grad_part, int n_rows,
+                                                                   int stride, int n_params,
+                                                                   const double* __restrict__ loss_part,
+                                                                   int n_loss_rows, double* __restrict__ red,
+                                                                   unsigned* ticket, const AdamArgs a) {
+  if (a.st->stopped) return;
+  __shared__ int last;
+  reduce_body(grad_part, n_rows, stride, n_params, loss_part, n_loss_rows, red);
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  if (threadIdx.x == 0) *ticket = 0u;  // re-arm for the next epoch (graph replay)
+  adam_body(a);
 }
 
 __global__ void mark_start_kernel(TrainState* st) { st->t_prev = globaltimer(); }

@@ -75,7 +75,8 @@ struct StepArgs {
   NetDesc net;
   const float* params;
   // outputs (per CTA)
-  float* grad_part;   // [gridDim.x][n_params]
+  float* grad_part;   // param-major [n_params][part_stride]: entry p*part_stride + cta
+  int part_stride;    // >= gridDim.x
   double* loss_part;  // [gridDim.x][kLpWords]
   // forward mode: arbitrary points in, outputs out
   const float2* fwd_pts;
@@ -1100,11 +1101,10 @@ __global__ void __launch_bounds__(kThreads, 2) step_kernel(const StepArgs a) {
 
   if constexpr (MODE != kModeForward) {
     // ---- per-CTA outputs ----
-    float* gout = a.grad_part + (size_t)blockIdx.x * net.n_params;
 #pragma unroll 1
     for (int m = 0; m < LY::NGR; ++m) {
       const int e = tid + kThreads * m;
-      if (e < net.n_params) gout[e] = greg[m];
+      if (e < net.n_params) a.grad_part[(size_t)e * a.part_stride + blockIdx.x] = greg[m];
     }
     const int any_bad = __syncthreads_or(bad);
     if (tid == 0) {

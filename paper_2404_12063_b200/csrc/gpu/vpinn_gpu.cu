@@ -155,9 +155,10 @@ struct vpinn_gpu_ctx {
   // per-CTA partials and the reduced vector [grad | loss words]
   DBuf<float> grad_part;
   DBuf<double> loss_part, red;
-  int grad_rows = 0, loss_rows = 0;
+  int grad_rows = 0, loss_rows = 0, part_stride = 0;
   // trainer
   DBuf<vpg::TrainState> st;
+  DBuf<unsigned> ticket;  // reduce_adam_kernel last-CTA ticket
   DBuf<vpg::StepRecord> rec;
   DBuf<float> lr_tab, c1_tab, c2_tab;
   int* h_flag = nullptr;  // pinned
@@ -236,11 +237,19 @@ void configure(vpinn_gpu_ctx* c) {
     const int tile_rows = a.cells_per_tile * c->T;
     const size_t min_smem = V.smem(V.rev_need, 1);
     const size_t budget = min_smem <= two_cta ? two_cta : (size_t)227 * 1024;
-    int rows = (tile_rows + 1) / 2;
+    // the whole tile slab in one stage when it fits (one contraction chunk,
+    // fewer barriers); otherwise a two-stage ring of half tiles or smaller
+    bool single = true;
+    int rows = tile_rows;
     for (;;) {
       const int tstride = round4(rows * c->Q + 8);
       const int stage = c->nt * tstride;
-      const int uni = std::max(V.rev_need, 2 * stage);
+      const int uni = std::max(V.rev_need, single ? stage : 2 * stage);
+      if (single && V.smem(uni, rows) > budget) {
+        single = false;
+        rows = (tile_rows + 1) / 2;
+        continue;
+      }
       if (V.smem(uni, rows) <= budget || rows == 1) {
         a.chunk_rows = rows;
         a.tstride = tstride;
@@ -365,7 +374,9 @@ void configure(vpinn_gpu_ctx* c) {
   if (c->split) c->loss_rows = c->grid_contract + c->grid_pen + c->grid_step;
 
   // ---- buffers sized by the grids ----
-  c->grad_part.alloc((size_t)c->grad_rows * c->n_params);
+  c->part_stride = (c->grad_rows + 31) & ~31;
+  c->grad_part.alloc((size_t)c->part_stride * c->n_params);
+  a.part_stride = c->part_stride;
   c->loss_part.alloc((size_t)std::max(c->loss_rows, std::max(c->grid_contract, c->grid_cc)) * vpg::kLpWords);
   c->red.alloc((size_t)c->n_params + vpg::kLpWords);
   a.grad_part = c->grad_part.p;
@@ -391,7 +402,7 @@ void configure(vpinn_gpu_ctx* c) {
 }
 
 // ---- one epoch: loss + gradient (+ Adam) enqueued on the context stream ----
-void enqueue_grad(vpinn_gpu_ctx* c, const int* stop) {
+void enqueue_grad(vpinn_gpu_ctx* c, const int* stop, bool with_reduce = true) {
   const Variant& V = c->var;
   vpg::StepArgs a = c->sargs;
   a.stop_flag = stop;
@@ -439,8 +450,9 @@ void enqueue_grad(vpinn_gpu_ctx* c, const int* stop) {
     CK(cudaGetLastError());
     c->launches += 1;
   }
-  vpg::reduce_kernel<<<ceil_div(c->n_params, 32) + 1, 256, 0, c->stream>>>(
-      c->grad_part.p, c->grad_rows, c->n_params, c->loss_part.p, c->loss_rows, c->red.p, stop);
+  if (!with_reduce) return;
+  vpg::reduce_kernel<<<vpg::reduce_grid(c->n_params), vpg::kRedThreads, 0, c->stream>>>(
+      c->grad_part.p, c->grad_rows, c->part_stride, c->n_params, c->loss_part.p, c->loss_rows, c->red.p, stop);
   CK(cudaGetLastError());
   c->launches += 1;
   if (c->comm)
@@ -472,8 +484,18 @@ vpg::AdamArgs adam_args(vpinn_gpu_ctx* c, bool tables, float lr_const, bool reco
 }
 
 void enqueue_epoch(vpinn_gpu_ctx* c, const vpg::AdamArgs& aa) {
-  enqueue_grad(c, &c->st.p->stopped);
-  vpg::adam_kernel<<<1, 1024, 0, c->stream>>>(aa);
+  if (c->comm) {
+    // reduce -> ncclAllReduce -> Adam (the all-reduce sits between them)
+    enqueue_grad(c, &c->st.p->stopped);
+    vpg::adam_kernel<<<1, 1024, 0, c->stream>>>(aa);
+    CK(cudaGetLastError());
+    c->launches += 1;
+    return;
+  }
+  enqueue_grad(c, &c->st.p->stopped, /*with_reduce=*/false);
+  vpg::reduce_adam_kernel<<<vpg::reduce_grid(c->n_params), vpg::kRedThreads, 0, c->stream>>>(
+      c->grad_part.p, c->grad_rows, c->part_stride, c->n_params, c->loss_part.p, c->loss_rows, c->red.p,
+      c->ticket.p, aa);
   CK(cudaGetLastError());
   c->launches += 1;
 }
@@ -568,8 +590,9 @@ int launch_contract(vpinn_gpu_ctx* c, const float* ux, const float* uy, const fl
 }
 
 long long launches_per_epoch(const vpinn_gpu_ctx* c) {
-  long long n = 3;  // step kernel(s) + reduce + adam
-  if (c->split) n = 2 + 2 + (c->cargs.n_tiles > 0) + (c->grid_pen > 0);
+  // step kernel(s) + reduce + adam (fused into one kernel without a communicator)
+  long long n = c->comm ? 3 : 2;
+  if (c->split) n += 1 + (c->cargs.n_tiles > 0) + (c->grid_pen > 0);  // forward, contraction, penalty
   return n;
 }
 
@@ -737,6 +760,7 @@ int vpinn_gpu_create(const vpinn_gpu_problem* pb, vpinn_gpu_ctx** out) {
     c->m.alloc(c->n_params);
     c->v.alloc(c->n_params);
     c->st.alloc(1);
+    c->ticket.alloc(1);
     configure(c.get());
     reset_state(c.get(), LLONG_MAX, nullptr);
     CK(cudaStreamSynchronize(c->stream));
@@ -1104,8 +1128,8 @@ int vpinn_gpu_profile_step(vpinn_gpu_ctx* c, int reps, double* ms_mlp, double* m
         CK(cudaGetLastError());
         c->launches += 1;
         CK(cudaEventRecord(ev[1], c->stream));
-        vpg::reduce_kernel<<<ceil_div(c->n_params, 32) + 1, 256, 0, c->stream>>>(
-            c->grad_part.p, c->grad_rows, c->n_params, c->loss_part.p, c->loss_rows, c->red.p,
+        vpg::reduce_kernel<<<vpg::reduce_grid(c->n_params), vpg::kRedThreads, 0, c->stream>>>(
+            c->grad_part.p, c->grad_rows, c->part_stride, c->n_params, c->loss_part.p, c->loss_rows, c->red.p,
             a.stop_flag);
         CK(cudaGetLastError());
         c->launches += 1;
