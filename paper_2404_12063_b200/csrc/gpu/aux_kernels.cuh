@@ -10,8 +10,8 @@ namespace vpg {
 // ---------------------------------------------------------------------------
 // Cross-CTA reduction of the per-CTA partials (fp64, fixed order): one warp
 // per parameter over the param-major partial rows (all loads of a lane in
-// flight at once, then a fixed shuffle tree); the last warp of the grid sums
-// the loss words.  red = [gradient | loss words].
+// flight at once, then a fixed shuffle tree); the trailing kLpWords warps sum
+// the loss words the same way.  red = [gradient | loss words].
 constexpr int kRedThreads = 256;
 constexpr int kRedWarps = kRedThreads / 32;
 
@@ -20,22 +20,33 @@ __device__ __forceinline__ void reduce_body(const float* __restrict__ grad_part,
                                             double* __restrict__ red) {
   const int lane = threadIdx.x & 31;
   const int gw = blockIdx.x * kRedWarps + (threadIdx.x >> 5);
+  const double* src_d = nullptr;
+  const float* src_f = nullptr;
+  int n = 0, step = 1;
   if (gw < n_params) {
-    const float* row = grad_part + (size_t)gw * stride;
-    double acc = 0.0;
-#pragma unroll 4
-    for (int c = lane; c < n_rows; c += 32) acc += (double)row[c];
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-    if (lane == 0) red[gw] = acc;
-  } else if (gw == n_params && lane < kLpWords) {
-    double acc = 0.0;
-    for (int c = 0; c < n_loss_rows; ++c) acc += loss_part[(size_t)c * kLpWords + lane];
-    red[n_params + lane] = acc;
+    src_f = grad_part + (size_t)gw * stride;
+    n = n_rows;
+  } else if (gw < n_params + kLpWords) {
+    src_d = loss_part + (gw - n_params);
+    n = n_loss_rows;
+    step = kLpWords;
+  } else {
+    return;
   }
+  double acc = 0.0;
+  if (src_f != nullptr) {
+#pragma unroll 8
+    for (int c = lane; c < n; c += 32) acc += (double)src_f[c];
+  } else {
+#pragma unroll 8
+    for (int c = lane; c < n; c += 32) acc += src_d[(size_t)c * step];
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (lane == 0) red[gw] = acc;
 }
 
-__host__ __device__ constexpr int reduce_grid(int n_params) { return (n_params + 1 + kRedWarps - 1) / kRedWarps; }
+__host__ __device__ constexpr int reduce_grid(int n_params) { return (n_params + kLpWords + kRedWarps - 1) / kRedWarps; }
 
 __global__ void __launch_bounds__(kRedThreads) reduce_kernel(const float* __restrict__ grad_part, int n_rows,
                                                              int stride, int n_params,
