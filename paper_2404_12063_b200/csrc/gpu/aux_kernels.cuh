@@ -233,6 +233,18 @@ __global__ void __launch_bounds__(kRedThreads) reduce_adam_kernel(const float* _
 
 __global__ void mark_start_kernel(TrainState* st) { st->t_prev = globaltimer(); }
 
+// L2 flush, second half: after the flush buffer (> L2) has been written, read
+// it back so L2 holds clean lines of the flush buffer and no dirty write-back
+// of it is left to compete with the next timed kernel.
+__global__ void flush_read_kernel(const int4* __restrict__ buf, size_t n16, int* sink) {
+  int acc = 0;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n16; i += (size_t)gridDim.x * blockDim.x) {
+    const int4 v = __ldcg(buf + i);
+    acc ^= v.x ^ v.y ^ v.z ^ v.w;
+  }
+  if (acc == 0x7fffffff) *sink = acc;  // keeps the loads; practically never taken
+}
+
 // ---------------------------------------------------------------------------
 // Standalone contraction (losses.hpp:91-168) over device-resident ux/uy/eps:
 // split path (Q > 128) and the HBM-roofline measurement.  256 threads; a

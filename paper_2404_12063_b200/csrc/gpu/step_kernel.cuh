@@ -328,24 +328,27 @@ __device__ __forceinline__ void own_add(float (&greg)[NGR], int tid, int lo, int
 }
 
 // ---------------------------------------------------------------------------
-// slab chunk copies (thread 0): aligned superset of each tensor's rows
-static __device__ __noinline__ void issue_chunk(const StepArgs& a, int cell0, int row0, int nrows, float* stage,
-                                         uint64_t* bar) {
+// slab chunk copies (thread 0): aligned superset of each tensor's rows.
+// Inlined and array-free so the kernel-parameter struct is never copied to
+// the stack (local-memory round trips on every issue).
+__device__ __forceinline__ void issue_chunk(const StepArgs& a, int cell0, int row0, int nrows, float* stage,
+                                            uint64_t* bar) {
   const size_t grow0 = (size_t)cell0 * a.T + row0;
-  uint32_t total = 0;
-  const char* src[3];
-  uint32_t n16[3];
-  for (int t = 0; t < a.nt; ++t) {
+  auto seg = [&](int t, const char*& src) {
     const char* s = reinterpret_cast<const char*>(a.tens[t] + grow0 * a.Q);
-    const char* al = reinterpret_cast<const char*>(reinterpret_cast<uintptr_t>(s) & ~uintptr_t(15));
-    const uint32_t pre = (uint32_t)(s - al);
-    n16[t] = (pre + (uint32_t)nrows * a.Q * 4u + 15u) & ~15u;
-    src[t] = al;
-    total += n16[t];
-  }
+    src = reinterpret_cast<const char*>(reinterpret_cast<uintptr_t>(s) & ~uintptr_t(15));
+    const uint32_t pre = (uint32_t)(s - src);
+    return (pre + (uint32_t)nrows * a.Q * 4u + 15u) & ~15u;
+  };
+  const char* s0;
+  const char* s1;
+  const char* s2 = nullptr;
+  const uint32_t n0 = seg(0, s0), n1 = seg(1, s1), n2 = a.nt == 3 ? seg(2, s2) : 0u;
   fence_proxy_async();
-  mbar_arrive_expect_tx(bar, total);
-  for (int t = 0; t < a.nt; ++t) bulk_g2s(stage + t * a.tstride, src[t], n16[t], bar);
+  mbar_arrive_expect_tx(bar, n0 + n1 + n2);
+  bulk_g2s(stage, s0, n0, bar);
+  bulk_g2s(stage + a.tstride, s1, n1, bar);
+  if (a.nt == 3) bulk_g2s(stage + 2 * a.tstride, s2, n2, bar);
 }
 
 __device__ __forceinline__ const float* chunk_ptr(const StepArgs& a, int cell0, int row0, const float* stage,

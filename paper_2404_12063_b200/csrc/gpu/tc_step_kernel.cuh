@@ -1,0 +1,704 @@
+// Tensor-core (tcgen05, 3xTF32) FastVPINNs training step for sm_100a.
+//
+// Same per-tile semantics as step_kernel<..., kModeFused> (step_kernel.cuh):
+// forward with x/y tangents (network.hpp:204-282), the Algorithm-3
+// contraction (losses.hpp:91-168) or the penalty terms (losses.hpp:406-415),
+// and the reverse sweep (network.hpp:287-372) — but every hidden->hidden
+// GEMM runs on the 5th-generation tensor cores:
+//   forward      D_s[p][o]  = X_s[p][:] . W[o][:]      M = 128 points, N = 64 (W hi | W lo), K = 32
+//   propagation  D_s[p][i]  = G_s[p][:] . W[:][i]      M = 128 points, N = 64, K = 32 (B MN-major)
+//   param grad   Wbar[o][i] += sum_{s,p} G_s[p][o] X_s[p][i]
+//                                                     M = 64 (G hi | G lo), N = 64 (X hi | X lo),
+//                                                     K = 3 streams x 128 points, accumulated in
+//                                                     TMEM across all tiles of the CTA
+// s = value / x-tangent / y-tangent stream.  Products are 3xTF32
+// (tc_utils.cuh): hi*hi + hi*lo + lo*hi, fp32 accumulation, so the result
+// is fp32-faithful (the parity tolerance of the north star holds).  The
+// value stream carries a constant-one column at index H, which turns the
+// parameter-gradient GEMM's column H into the bias gradient.
+//
+// CTA = 256 threads; thread t owns point p = t % 128 (= its TMEM lane) and
+// hidden units [16*(t/128), +16).  One CTA per SM (TMEM 512 columns,
+// ~220 KB shared memory).  Hidden layers D in {2, 3}, H <= 31, one output.
+// Every phase is separated by a CTA barrier or an MMA-completion mbarrier;
+// one elected thread issues all MMAs.
+#pragma once
+
+#include "step_kernel.cuh"
+#include "tc_utils.cuh"
+
+namespace vpg {
+
+constexpr int kTcThreads = 256;
+constexpr int kTcTile = 16384;              // one [128][32] fp32 operand tile
+constexpr int kTcBuf = 6 * kTcTile;         // 3 streams x (hi, lo)
+constexpr int kTcW = 8192;                  // [64][32]: W hi rows 0..31, W lo rows 32..63
+constexpr uint32_t kTcCols = 512;           // TMEM columns allocated
+constexpr int kTcAccCol = 192;              // parameter-gradient accumulators start here
+
+// exchange rows of the tensor-core kernel ([row][128] floats)
+enum : int { kTxX = 0, kTxY, kTxU, kTxUx, kTxUy, kTxSx, kTxSy, kTxCv, kTxUb, kTxUxb, kTxUyb, kTxPu, kTxPx, kTxPy,
+             kTxRows };
+
+template <int D>
+struct TcLayout {
+  static constexpr int NL = D - 1;                      // MMA (hidden->hidden) layers
+  static constexpr int OFF_W = 0;                       // NL x kTcW
+  static constexpr int OFF_A = OFF_W + NL * kTcW;       // buffer A (1024-aligned)
+  static constexpr int OFF_B = OFF_A + kTcBuf;          // buffer B
+  static constexpr int OFF_SMALL = OFF_B + kTcBuf;      // floats from here
+  // small region, in floats
+  static constexpr int S_W0 = 0;                        // [32][4] (w_x, w_y, b, 0)
+  static constexpr int S_BIAS = S_W0 + 128;             // [NL][32]
+  static constexpr int S_WD = S_BIAS + NL * 32;         // [32] output weights + [4] bias
+  static constexpr int S_EX = S_WD + 36;                // [kTxRows][128]
+  static constexpr int S_CSUM = S_EX + kTxRows * 128;   // [8][96] column-sum partials
+  static constexpr int S_GACC = S_CSUM + 8 * 96;        // [128] small-gradient accumulators
+  static constexpr int S_CELL = S_GACC + 128;           // [256] per-cell sums
+  static constexpr int S_ROWS = S_CELL + 256;           // [3][128] rbar | rsq | rge
+  static constexpr int S_RED = S_ROWS + 3 * 128;        // 64 doubles (128 floats)
+  static constexpr int S_BAR = S_RED + 128;             // mbarriers + TMEM slot (16 floats)
+  static constexpr int S_END = S_BAR + 16;
+  static constexpr size_t BYTES = (size_t)OFF_SMALL + sizeof(float) * S_END + 1024;  // + alignment slack
+};
+
+// small-gradient accumulator slots (S_GACC)
+enum : int { kGaW0x = 0, kGaW0y = 32, kGaB0 = 64, kGaWd = 96 };  // kGaWd: 32 slots (H weights + bias at H)
+
+template <int H, int D>
+__host__ __device__ constexpr size_t tc_step_smem_bytes() {
+  return TcLayout<D>::BYTES;
+}
+
+// column sums over the tile's 128 points of up to 96 per-point values
+// (src row p at src + p * ld), added in a fixed order to acc[0..ncols);
+// 256 threads: 8 point groups of 16, then the 8 partials in order.
+static __device__ __forceinline__ void tc_colsum(const float* src, int ld, int ncols, float* part, float* acc) {
+  const int tid = threadIdx.x;
+  for (int e = tid; e < 8 * ncols; e += kTcThreads) {
+    const int g = e / ncols, c = e - g * ncols;
+    float s = 0.f;
+#pragma unroll 4
+    for (int p = 16 * g; p < 16 * g + 16; ++p) s += src[p * ld + c];
+    part[g * 96 + c] = s;
+  }
+  __syncthreads();
+  for (int c = tid; c < ncols; c += kTcThreads) {
+    float s = part[c];
+#pragma unroll
+    for (int g = 1; g < 8; ++g) s += part[g * 96 + c];
+    acc[c] += s;
+  }
+  __syncthreads();
+}
+
+template <int H, int D, int ACT>
+__global__ void __launch_bounds__(kTcThreads, 1) tc_step_kernel(const StepArgs a) {
+  static_assert(H <= 31 && (D == 2 || D == 3), "tensor-core step: H <= 31, 2 or 3 hidden layers");
+  using LY = TcLayout<D>;
+  constexpr int NL = LY::NL;
+  using AC = Act<ACT>;
+
+  if (a.stop_flag != nullptr && *a.stop_flag != 0) return;
+
+  extern __shared__ __align__(1024) char tc_raw[];
+  char* sm = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(tc_raw) + 1023) & ~uintptr_t(1023));
+  char* sWB = sm + LY::OFF_W;
+  char* bufA = sm + LY::OFF_A;
+  char* bufB = sm + LY::OFF_B;
+  float* sf = reinterpret_cast<float*>(sm + LY::OFF_SMALL);
+  float* sW0 = sf + LY::S_W0;
+  float* sBias = sf + LY::S_BIAS;
+  float* sWd = sf + LY::S_WD;
+  float* sEx = sf + LY::S_EX;
+  float* sCsum = sf + LY::S_CSUM;
+  float* sGacc = sf + LY::S_GACC;
+  float* sCell = sf + LY::S_CELL;
+  float* sRows = sf + LY::S_ROWS;
+  double* sRed = reinterpret_cast<double*>(sf + LY::S_RED);
+  uint64_t* mma_bar = reinterpret_cast<uint64_t*>(sf + LY::S_BAR);
+  uint64_t* tma_bar = mma_bar + 1;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(mma_bar + 2);
+
+  const int tid = threadIdx.x, warp = tid >> 5;
+  const int p = tid & 127;          // point of this thread == TMEM lane
+  const int hh = tid >> 7;          // unit half
+  const int u0 = 16 * hh;           // first hidden unit of this thread
+  const NetDesc& net = a.net;
+  const float* P = a.params;
+
+  // ---- one-time setup: TMEM, barriers, weights ----
+  if (warp == 0) tc::tmem_alloc(tslot, kTcCols);
+  if (tid == 0) {
+    mbar_init(mma_bar, 1);
+    mbar_init(tma_bar, 1);
+    fence_mbar_init();
+  }
+  for (int i = tid; i < 32; i += kTcThreads) {
+    float w0 = 0.f, w1 = 0.f, b = 0.f, wd = 0.f;
+    if (i < H) {
+      w0 = P[net.w_off[0] + 2 * i];
+      w1 = P[net.w_off[0] + 2 * i + 1];
+      b = P[net.b_off[0] + i];
+      wd = P[net.w_off[D] + i];
+    }
+    sW0[4 * i] = w0;
+    sW0[4 * i + 1] = w1;
+    sW0[4 * i + 2] = b;
+    sW0[4 * i + 3] = 0.f;
+    sWd[i] = wd;
+  }
+  if (tid == 0) sWd[32] = P[net.b_off[D]];
+  for (int l = 1; l <= NL; ++l) {
+    char* wb = sWB + (l - 1) * kTcW;
+    // row o, 4 columns per item (hi rows 0..31, lo rows 32..63)
+    for (int e = tid; e < 32 * 8; e += kTcThreads) {
+      const int o = e >> 3, c0 = (e & 7) * 4;
+      float v[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) v[k] = (o < H && c0 + k < H) ? P[net.w_off[l] + o * H + c0 + k] : 0.f;
+      tc::st_split4(wb, wb + 4096, o, c0, v[0], v[1], v[2], v[3]);
+    }
+    for (int o = tid; o < 32; o += kTcThreads) sBias[(l - 1) * 32 + o] = o < H ? P[net.b_off[l] + o] : 0.f;
+  }
+  for (int e = tid; e < 128; e += kTcThreads) sGacc[e] = 0.f;
+  for (int e = tid; e < 256; e += kTcThreads) sCell[e] = 0.f;
+  tc::fence_smem_to_async();
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
+  const uint32_t tmem = *tslot;
+  const uint32_t lane_q = (uint32_t)(32 * (warp & 3)) << 16;  // TMEM lane quarter of this warp
+
+  // MMA helpers (thread 0 only) -------------------------------------------------
+  const uint32_t sA = smem_u32(bufA), sB = smem_u32(bufB), sW = smem_u32(sWB);
+  // forward / propagation of layer l: A tiles (K-major) from buffer abuf, stream-major
+  auto issue_point_gemm = [&](uint32_t abuf, int l, bool propagate) {
+    const uint32_t wbase = sW + (uint32_t)(l - 1) * kTcW;
+    const uint32_t i64 = tc::idesc_tf32(128, 64, 0, propagate ? 1 : 0);
+    const uint32_t i32 = tc::idesc_tf32(128, 32, 0, propagate ? 1 : 0);
+#pragma unroll 1
+    for (int s = 0; s < 3; ++s) {
+      const uint32_t d = tmem + 64 * s;
+      const uint32_t ahi = abuf + 2 * s * kTcTile, alo = ahi + kTcTile;
+#pragma unroll
+      for (int ks = 0; ks < 4; ++ks) {
+        const uint64_t bd = propagate ? tc::sdesc(wbase + 1024 * ks, 4096, 1024) : tc::sdesc(wbase + 32 * ks, 16, 1024);
+        tc::mma_tf32(d, tc::sdesc(ahi + 32 * ks, 16, 1024), bd, i64, ks > 0);
+      }
+#pragma unroll
+      for (int ks = 0; ks < 4; ++ks) {
+        const uint64_t bd = propagate ? tc::sdesc(wbase + 1024 * ks, 4096, 1024) : tc::sdesc(wbase + 32 * ks, 16, 1024);
+        tc::mma_tf32(d, tc::sdesc(alo + 32 * ks, 16, 1024), bd, i32, 1);
+      }
+    }
+  };
+  // parameter gradient of layer l: G tiles in gbuf, X tiles in xbuf
+  auto issue_param_gemm = [&](uint32_t gbuf, uint32_t xbuf, int l, bool first) {
+    const uint32_t acc = tmem + kTcAccCol + 64 * (l - 1);
+    const uint32_t idesc = tc::idesc_tf32(64, 64, 1, 1);
+#pragma unroll 1
+    for (int s = 0; s < 3; ++s) {
+      const uint32_t g = gbuf + 2 * s * kTcTile, x = xbuf + 2 * s * kTcTile;
+#pragma unroll 4
+      for (int kp = 0; kp < 16; ++kp)
+        tc::mma_tf32(acc, tc::sdesc(g + 1024 * kp, kTcTile, 1024), tc::sdesc(x + 1024 * kp, kTcTile, 1024), idesc,
+                     (first && s == 0 && kp == 0) ? 0u : 1u);
+    }
+  };
+  uint32_t mma_phase = 0, tma_phase = 0;
+  auto commit_and_wait = [&]() {
+    if (tid == 0) tc::mma_commit(mma_bar);
+    mbar_wait(mma_bar, mma_phase);
+    mma_phase ^= 1u;
+    tc::fence_after_sync();
+  };
+  // all threads: make smem operand writes and TMEM reads ordered before the
+  // next MMA issue
+  auto operands_ready = [&]() {
+    tc::fence_smem_to_async();
+    tc::fence_before_sync();
+    __syncthreads();
+    tc::fence_after_sync();
+  };
+
+  // layer 0 of this thread's units for point (px, py): z, TX_x, TX_y
+  auto layer0 = [&](float px, float py, float (&z)[16], float (&tx)[16], float (&ty)[16]) {
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      const int u = u0 + k;
+      const float4 w = *reinterpret_cast<const float4*>(sW0 + 4 * u);
+      if (u < H) {
+        const float zz = AC::value(fmaf(w.y, py, w.x * px) + w.z);
+        const float s1 = AC::s1(zz);
+        z[k] = zz;
+        tx[k] = s1 * w.x;
+        ty[k] = s1 * w.y;
+      } else {
+        z[k] = (u == H) ? 1.0f : 0.0f;  // constant-one column -> bias gradient
+        tx[k] = 0.f;
+        ty[k] = 0.f;
+      }
+    }
+  };
+  auto store3 = [&](char* buf, const float (&z)[16], const float (&tx)[16], const float (&ty)[16]) {
+#pragma unroll
+    for (int c = 0; c < 16; c += 4) {
+      tc::st_split4(buf, buf + kTcTile, p, u0 + c, z[c], z[c + 1], z[c + 2], z[c + 3]);
+      tc::st_split4(buf + 2 * kTcTile, buf + 3 * kTcTile, p, u0 + c, tx[c], tx[c + 1], tx[c + 2], tx[c + 3]);
+      tc::st_split4(buf + 4 * kTcTile, buf + 5 * kTcTile, p, u0 + c, ty[c], ty[c + 1], ty[c + 2], ty[c + 3]);
+    }
+  };
+  // read back one stream of a buffer (hi + lo, exact)
+  auto load1 = [&](const char* buf, int s, float (&v)[16]) {
+    const char* hi = buf + 2 * s * kTcTile;
+    const char* lo = hi + kTcTile;
+#pragma unroll
+    for (int c = 0; c < 16; c += 4) {
+      const uint32_t off = tc::sw_off(p, u0 + c);
+      const float4 h4 = *reinterpret_cast<const float4*>(hi + off);
+      const float4 l4 = *reinterpret_cast<const float4*>(lo + off);
+      v[c] = h4.x + l4.x;
+      v[c + 1] = h4.y + l4.y;
+      v[c + 2] = h4.z + l4.z;
+      v[c + 3] = h4.w + l4.w;
+    }
+  };
+  // accumulator of stream s (hi*hi + lo*hi in columns [0,32), hi*lo in [32,64))
+  auto acc_stream = [&](int s, float (&v)[16]) {
+    float x0[16], x1[16];
+    const uint32_t col = tmem + lane_q + 64 * s + u0;
+    tc::tmem_ld2x16_wait(col, col + 32, x0, x1);
+#pragma unroll
+    for (int k = 0; k < 16; ++k) v[k] = x0[k] + x1[k];
+  };
+
+  bool first_grad = true;
+  double acc_v = 0.0, acc_b = 0.0, acc_s = 0.0, acc_eg = 0.0;  // thread 0
+  int bad = 0;
+  const int n_pts_all = a.n_int + a.n_bnd + a.n_sen;
+
+#pragma unroll 1
+  for (int tile = blockIdx.x; tile < a.n_tiles; tile += gridDim.x) {
+    bool interior = false;
+    int cell0 = 0, ncell = 0, pbase = 0, np = 0;
+    if (tile < a.n_int_tiles) {
+      interior = true;
+      cell0 = tile * a.cells_per_tile;
+      ncell = min(a.cells_per_tile, a.E - cell0);
+      pbase = cell0 * a.Q;
+      np = ncell * a.Q;
+    } else {
+      pbase = a.n_int + (tile - a.n_int_tiles) * 128;
+      np = min(128, n_pts_all - pbase);
+    }
+    const int nrows_tile = ncell * a.T;
+    const bool valid = p < np;
+    float px = 0.f, py = 0.f;
+    if (valid) {
+      const float2 xy = a.pts[pbase + p];
+      px = xy.x;
+      py = xy.y;
+    }
+    if (hh == 0) {
+      sEx[kTxX * 128 + p] = px;
+      sEx[kTxY * 128 + p] = py;
+    }
+
+    // =================== forward ===================
+    {
+      float z[16], tx[16], ty[16];
+      layer0(px, py, z, tx, ty);
+      store3(bufA, z, tx, ty);
+    }
+    operands_ready();
+    if (tid == 0) issue_point_gemm(sA, 1, false);
+    commit_and_wait();
+    // the slab buffer is free now (D == 3: layer-1 input consumed; D == 2: unused)
+    char* slab = (D == 3) ? bufA : bufB;
+    if (interior && tid == 0) {
+      fence_proxy_async();
+      issue_chunk(a, cell0, 0, nrows_tile, reinterpret_cast<float*>(slab), tma_bar);
+    }
+    float lz[16], lt[16], lu[16];  // last hidden layer (units u0..u0+15)
+    {
+      float av[16], at[16], au[16];
+      acc_stream(0, av);
+      acc_stream(1, at);
+      acc_stream(2, au);
+      const float* bias = sBias;
+#pragma unroll
+      for (int k = 0; k < 16; ++k) {
+        const int u = u0 + k;
+        if (u < H) {
+          const float zz = AC::value(av[k] + bias[u]);
+          const float s1 = AC::s1(zz);
+          lz[k] = zz;
+          lt[k] = s1 * at[k];
+          lu[k] = s1 * au[k];
+        } else {
+          lz[k] = (u == H) ? 1.0f : 0.0f;
+          lt[k] = 0.f;
+          lu[k] = 0.f;
+        }
+      }
+    }
+    if constexpr (D == 3) {
+      store3(bufB, lz, lt, lu);
+      operands_ready();
+      if (tid == 0) issue_point_gemm(sB, 2, false);
+      commit_and_wait();
+      float av[16], at[16], au[16];
+      acc_stream(0, av);
+      acc_stream(1, at);
+      acc_stream(2, au);
+      const float* bias = sBias + 32;
+#pragma unroll
+      for (int k = 0; k < 16; ++k) {
+        const int u = u0 + k;
+        if (u < H) {
+          const float zz = AC::value(av[k] + bias[u]);
+          const float s1 = AC::s1(zz);
+          lz[k] = zz;
+          lt[k] = s1 * at[k];
+          lu[k] = s1 * au[k];
+        } else {
+          lz[k] = (u == H) ? 1.0f : 0.0f;
+          lt[k] = 0.f;
+          lu[k] = 0.f;
+        }
+      }
+    }
+    // output layer (linear) over this thread's units, halves combined in order
+    {
+      float u = 0.f, ux = 0.f, uy = 0.f;
+#pragma unroll
+      for (int k = 0; k < 16; ++k) {
+        if (u0 + k < H) {
+          const float w = sWd[u0 + k];
+          u = fmaf(w, lz[k], u);
+          ux = fmaf(w, lt[k], ux);
+          uy = fmaf(w, lu[k], uy);
+        }
+      }
+      if (hh == 1) {
+        sEx[kTxPu * 128 + p] = u;
+        sEx[kTxPx * 128 + p] = ux;
+        sEx[kTxPy * 128 + p] = uy;
+      }
+      __syncthreads();
+      if (hh == 0) {
+        u = (u + sEx[kTxPu * 128 + p]) + sWd[32];
+        ux = ux + sEx[kTxPx * 128 + p];
+        uy = uy + sEx[kTxPy * 128 + p];
+        if (valid && !(finitef(u) && finitef(ux) && finitef(uy))) bad = 1;
+        sEx[kTxU * 128 + p] = u;
+        sEx[kTxUx * 128 + p] = ux;
+        sEx[kTxUy * 128 + p] = uy;
+      }
+    }
+
+    // =================== objective: adjoints of (u, ux, uy) ===================
+    float ub = 0.f, uxb = 0.f, uyb = 0.f;
+    if (interior) {
+      const bool conv = a.nt == 3;
+      const float e_fixed = a.eps_source == 1 ? P[net.scal_off + a.eps_scalar_index] : a.eps;
+      if (hh == 0) {
+        const float ux = sEx[kTxUx * 128 + p], uy = sEx[kTxUy * 128 + p];
+        sEx[kTxSx * 128 + p] = ux;
+        sEx[kTxSy * 128 + p] = uy;
+        sEx[kTxCv * 128 + p] = a.bx * ux + a.by * uy;
+      }
+      __syncthreads();
+      mbar_wait(tma_bar, tma_phase);
+      tma_phase ^= 1u;
+      const float* Gx = chunk_ptr(a, cell0, 0, reinterpret_cast<const float*>(slab), 0);
+      const float* Gy = chunk_ptr(a, cell0, 0, reinterpret_cast<const float*>(slab), 1);
+      const float* Tv = conv ? chunk_ptr(a, cell0, 0, reinterpret_cast<const float*>(slab), 2) : nullptr;
+      float* rbarv = sRows;
+      float* rsqv = sRows + 128;
+      float* rgev = sRows + 256;
+      // phase A: one slab row per thread (nrows_tile <= 128)
+      if (tid < nrows_tile) {
+        const int kk = tid / a.T;
+        const int j = tid - kk * a.T;
+        const float* sx = sEx + kTxSx * 128 + kk * a.Q;
+        const float* sy = sEx + kTxSy * 128 + kk * a.Q;
+        const float* gxr = Gx + tid * a.Q;
+        const float* gyr = Gy + tid * a.Q;
+        float gx = 0.f, gy = 0.f;
+#pragma unroll 5
+        for (int q = 0; q < a.Q; ++q) {
+          gx = fmaf(gxr[q], sx[q], gx);
+          gy = fmaf(gyr[q], sy[q], gy);
+        }
+        float res = e_fixed * (gx + gy);
+        if (conv) {
+          const float* cv = sEx + kTxCv * 128 + kk * a.Q;
+          const float* tr = Tv + tid * a.Q;
+          float t = 0.f;
+#pragma unroll 5
+          for (int q = 0; q < a.Q; ++q) t = fmaf(tr[q], cv[q], t);
+          res += t;
+        }
+        res -= a.forcing[(size_t)(cell0 + kk) * a.T + j];
+        rsqv[tid] = res * res;
+        const float rb = a.rscale * res;
+        rbarv[tid] = rb;
+        rgev[tid] = rb * (gx + gy);
+      }
+      __syncthreads();
+      // phase B: one point per thread (hh == 0)
+      if (hh == 0 && valid) {
+        const int myk = p / a.Q, myq = p - myk * a.Q;
+        float tx = 0.f, ty = 0.f, tt = 0.f;
+#pragma unroll 5
+        for (int r = myk * a.T; r < (myk + 1) * a.T; ++r) {
+          const float rb = rbarv[r];
+          tx = fmaf(Gx[r * a.Q + myq], rb, tx);
+          ty = fmaf(Gy[r * a.Q + myq], rb, ty);
+          if (conv) tt = fmaf(Tv[r * a.Q + myq], rb, tt);
+        }
+        float ox = e_fixed * tx, oy = e_fixed * ty;
+        if (conv) {
+          ox = fmaf(a.bx, tt, ox);
+          oy = fmaf(a.by, tt, oy);
+        }
+        sEx[kTxUb * 128 + p] = 0.f;
+        sEx[kTxUxb * 128 + p] = ox;
+        sEx[kTxUyb * 128 + p] = oy;
+      } else if (hh == 0) {
+        sEx[kTxUb * 128 + p] = 0.f;
+        sEx[kTxUxb * 128 + p] = 0.f;
+        sEx[kTxUyb * 128 + p] = 0.f;
+      }
+      // per-cell squared residual / eps-gradient sums in row order
+      if (hh == 1 && p < ncell) {
+        float s = 0.f, g = 0.f;
+        for (int r = p * a.T; r < (p + 1) * a.T; ++r) {
+          s += rsqv[r];
+          g += rgev[r];
+        }
+        sCell[p] = s;
+        sCell[128 + p] = g;
+      }
+      __syncthreads();
+      if (tid == 0) {
+        for (int k = 0; k < ncell; ++k) {
+          acc_v += (double)(sCell[k] * a.inv_nt);
+          acc_eg += (double)sCell[128 + k];
+        }
+      }
+    } else {
+      // ---------- penalty tile (losses.hpp:389-415) ----------
+      double sb = 0.0, ss = 0.0;
+      float ubv = 0.f;
+      if (hh == 0 && valid) {
+        const int pi = pbase + p - a.n_int;
+        const float u = sEx[kTxU * 128 + p];
+        if (pi < a.n_bnd) {
+          const float d = u - a.bval[pi];
+          sb = (double)(d * d);
+          ubv = a.bscale * d;
+        } else {
+          const float d = u - a.sval[pi - a.n_bnd];
+          ss = (double)(d * d);
+          ubv = a.sscale * d;
+        }
+      }
+      if (hh == 0) {
+        sEx[kTxUb * 128 + p] = ubv;
+        sEx[kTxUxb * 128 + p] = 0.f;
+        sEx[kTxUyb * 128 + p] = 0.f;
+      }
+      // block sums of the penalty squares (warps 0-3 hold the points)
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        sb += __shfl_down_sync(0xffffffffu, sb, o);
+        ss += __shfl_down_sync(0xffffffffu, ss, o);
+      }
+      if ((tid & 31) == 0 && warp < 4) {
+        sRed[warp] = sb;
+        sRed[8 + warp] = ss;
+      }
+      __syncthreads();
+      if (tid == 0) {
+        for (int w = 0; w < 4; ++w) {
+          acc_b += sRed[w];
+          acc_s += sRed[8 + w];
+        }
+      }
+    }
+    __syncthreads();  // adjoint rows visible; slab reads done
+    ub = sEx[kTxUb * 128 + p];
+    uxb = sEx[kTxUxb * 128 + p];
+    uyb = sEx[kTxUyb * 128 + p];
+
+    // =================== reverse ===================
+    // ---- output layer: Wbar_out, bbar_out (column H: lz == 1) and G of the last hidden layer ----
+    char* gbuf = slab;  // free buffer
+    {
+      float* vrow = reinterpret_cast<float*>(gbuf);  // [128][33] scratch (before G is written)
+#pragma unroll
+      for (int k = 0; k < 16; ++k) vrow[p * 33 + u0 + k] = fmaf(uyb, lu[k], fmaf(uxb, lt[k], ub * lz[k]));
+      __syncthreads();
+      tc_colsum(vrow, 33, H + 1, sCsum, sGacc + kGaWd);
+      float gA[16], gX[16], gY[16];
+#pragma unroll
+      for (int k = 0; k < 16; ++k) {
+        const int u = u0 + k;
+        if (u < H) {
+          const float wd = sWd[u];
+          const float xb = wd * ub, zx = wd * uxb, zy = wd * uyb;
+          const float s1 = AC::s1(lz[k]), kp = AC::kap(lz[k]);
+          gA[k] = fmaf(s1, xb, kp * fmaf(lt[k], zx, lu[k] * zy));
+          gX[k] = s1 * zx;
+          gY[k] = s1 * zy;
+        } else {
+          gA[k] = gX[k] = gY[k] = 0.f;
+        }
+      }
+      store3(gbuf, gA, gX, gY);
+    }
+    operands_ready();
+    // ---- hidden->hidden layers, last first ----
+    {
+      // layer NL: G in gbuf, its input X in the other buffer
+      char* xbuf = (gbuf == bufA) ? bufB : bufA;
+      if (tid == 0) {
+        issue_param_gemm(smem_u32(gbuf), smem_u32(xbuf), NL, first_grad);
+        issue_point_gemm(smem_u32(gbuf), NL, true);
+      }
+      commit_and_wait();
+      if constexpr (D == 3) {
+        // G of hidden 2 from the propagated adjoints and hidden-2 state (xbuf)
+        float xa[16], xx[16], xy[16];
+        acc_stream(0, xa);
+        acc_stream(1, xx);
+        acc_stream(2, xy);
+        float z[16], tx[16], ty[16];
+        load1(xbuf, 0, z);
+        load1(xbuf, 1, tx);
+        load1(xbuf, 2, ty);
+        float gA[16], gX[16], gY[16];
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+          if (u0 + k < H) {
+            const float s1 = AC::s1(z[k]), kp = AC::kap(z[k]);
+            gA[k] = fmaf(s1, xa[k], kp * fmaf(tx[k], xx[k], ty[k] * xy[k]));
+            gX[k] = s1 * xx[k];
+            gY[k] = s1 * xy[k];
+          } else {
+            gA[k] = gX[k] = gY[k] = 0.f;
+          }
+        }
+        __syncthreads();  // every thread has read hidden-2 state from xbuf
+        store3(gbuf, gA, gX, gY);
+        {
+          float z1[16], t1x[16], t1y[16];
+          layer0(px, py, z1, t1x, t1y);
+          store3(xbuf, z1, t1x, t1y);  // layer-1 input (recomputed)
+        }
+        operands_ready();
+        if (tid == 0) {
+          issue_param_gemm(smem_u32(gbuf), smem_u32(xbuf), 1, first_grad);
+          issue_point_gemm(smem_u32(gbuf), 1, true);
+        }
+        commit_and_wait();
+      }
+    }
+    first_grad = false;
+    // ---- input layer: G of hidden 1 -> Wbar_0, bbar_0 ----
+    {
+      float xa[16], xx[16], xy[16];
+      acc_stream(0, xa);
+      acc_stream(1, xx);
+      acc_stream(2, xy);
+      float z1[16], t1x[16], t1y[16];
+      layer0(px, py, z1, t1x, t1y);
+      float* vrow = reinterpret_cast<float*>(bufA);  // [128][97] scratch (both buffers are free now)
+#pragma unroll
+      for (int k = 0; k < 16; ++k) {
+        const int u = u0 + k;
+        float ga = 0.f, gx = 0.f, gy = 0.f;
+        if (u < H) {
+          const float s1 = AC::s1(z1[k]), kp = AC::kap(z1[k]);
+          ga = fmaf(s1, xa[k], kp * fmaf(t1x[k], xx[k], t1y[k] * xy[k]));
+          gx = s1 * xx[k];
+          gy = s1 * xy[k];
+        }
+        // Wbar_0 += Abar x^T + TAxbar e_x^T + TAybar e_y^T ; bbar_0 += Abar
+        vrow[p * 97 + u] = fmaf(ga, px, gx);
+        vrow[p * 97 + 32 + u] = fmaf(ga, py, gy);
+        vrow[p * 97 + 64 + u] = ga;
+      }
+      tc::fence_before_sync();
+      __syncthreads();
+      tc_colsum(vrow, 97, 96, sCsum, sGacc);
+    }
+  }
+
+  // =================== per-CTA outputs ===================
+  // parameter-gradient accumulators (TMEM, M = 64 layout: row m -> lane
+  // (m % 16) + 32 (m / 16)) -> smem [64][64] -> Wbar = hi.hi + hi.lo + lo.hi
+  float* scr = reinterpret_cast<float*>(bufA);
+  for (int l = 1; l <= NL; ++l) {
+    tc::fence_after_sync();
+    if (warp < 4 && !first_grad) {
+      float v0[16], v1[16], v2[16], v3[16];
+      const uint32_t col = tmem + lane_q + kTcAccCol + 64 * (l - 1);
+      tc::tmem_ld2x16_wait(col, col + 16, v0, v1);
+      tc::tmem_ld2x16_wait(col + 32, col + 48, v2, v3);
+      const int lane = tid & 31;
+      if (lane < 16) {
+        const int m = 16 * warp + lane;
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+          scr[m * 65 + k] = v0[k];
+          scr[m * 65 + 16 + k] = v1[k];
+          scr[m * 65 + 32 + k] = v2[k];
+          scr[m * 65 + 48 + k] = v3[k];
+        }
+      }
+    }
+    tc::fence_before_sync();
+    __syncthreads();
+    const int fo = net.out_w[l], fi = net.in_w[l];
+    for (int e = tid; e < fo * (fi + 1); e += kTcThreads) {
+      const int o = e / (fi + 1), i = e - o * (fi + 1);
+      float g = 0.f;
+      if (!first_grad) g = scr[o * 65 + i] + scr[o * 65 + 32 + i] + scr[(32 + o) * 65 + i];
+      const int idx = (i < fi) ? net.w_off[l] + o * fi + i : net.b_off[l] + o;
+      a.grad_part[(size_t)idx * a.part_stride + blockIdx.x] = g;
+    }
+    __syncthreads();
+  }
+  for (int i = tid; i < H; i += kTcThreads) {
+    a.grad_part[(size_t)(net.w_off[0] + 2 * i) * a.part_stride + blockIdx.x] = sGacc[kGaW0x + i];
+    a.grad_part[(size_t)(net.w_off[0] + 2 * i + 1) * a.part_stride + blockIdx.x] = sGacc[kGaW0y + i];
+    a.grad_part[(size_t)(net.b_off[0] + i) * a.part_stride + blockIdx.x] = sGacc[kGaB0 + i];
+    a.grad_part[(size_t)(net.w_off[D] + i) * a.part_stride + blockIdx.x] = sGacc[kGaWd + i];
+  }
+  if (tid == 0) {
+    a.grad_part[(size_t)net.b_off[D] * a.part_stride + blockIdx.x] = sGacc[kGaWd + H];
+    for (int e = net.scal_off; e < net.n_params; ++e) a.grad_part[(size_t)e * a.part_stride + blockIdx.x] = 0.f;
+  }
+  const int any_bad = __syncthreads_or(bad);
+  if (tid == 0) {
+    double* lp = a.loss_part + (size_t)blockIdx.x * kLpWords;
+    lp[kLpVar] = acc_v;
+    lp[kLpBnd] = acc_b;
+    lp[kLpSen] = acc_s;
+    lp[kLpEpsGrad] = acc_eg;
+    lp[kLpBad] = any_bad ? 1.0 : 0.0;
+    for (int w = kLpBad + 1; w < kLpWords; ++w) lp[w] = 0.0;
+  }
+  tc::fence_before_sync();
+  __syncthreads();
+  if (warp == 0) {
+    tc::fence_after_sync();
+    tc::tmem_dealloc(tmem, kTcCols);
+  }
+}
+
+}  // namespace vpg

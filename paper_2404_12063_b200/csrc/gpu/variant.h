@@ -14,6 +14,8 @@ using StepFn = void (*)(StepArgs);
 struct Variant {
   int H, D, C, ACT;
   StepFn fused, forward, reverse;
+  StepFn tc;       // tensor-core fused step (tc_step_kernel.cuh), nullptr if the shape has none
+  size_t tc_smem;
   int off_union;  // floats before the union
   int rev_need;   // floats the reverse phase needs in the union
   size_t (*smem)(int, int);
@@ -29,6 +31,9 @@ VPG_VARIANTS(VPG_DECL)
 #undef VPG_DECL
 
 #ifdef VPG_DEFINE_VARIANT
+}  // namespace vpg
+#include "tc_step_kernel.cuh"
+namespace vpg {
 template <int H, int D, int C, int A>
 Variant make_variant() {
   using LY = Layout<H, D, C>;
@@ -43,6 +48,13 @@ Variant make_variant() {
   v.off_union = LY::OFF_UNION;
   v.rev_need = LY::REV_NEED;
   v.smem = [](int u, int r) { return step_smem_bytes<H, D, C>(u, r); };
+  if constexpr (C == 1 && (D == 2 || D == 3) && H <= 31) {
+    v.tc = tc_step_kernel<H, D, A>;
+    v.tc_smem = tc_step_smem_bytes<H, D>();
+  } else {
+    v.tc = nullptr;
+    v.tc_smem = 0;
+  }
   return v;
 }
 #define VPG_DEFINE(H, D, C, A) \

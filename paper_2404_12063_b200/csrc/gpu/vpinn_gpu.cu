@@ -19,6 +19,8 @@
 
 #include "aux_kernels.cuh"
 #include "contract_cells.cuh"
+#include "tc_selftest.cuh"
+#include "tc_step_kernel.cuh"
 #include "variant.h"
 #include "vpinn_gpu.h"
 
@@ -164,6 +166,7 @@ struct vpinn_gpu_ctx {
   int* h_flag = nullptr;  // pinned
   // step configuration
   bool split = false;
+  bool tc = false;  // tensor-core fused step
   vpg::StepArgs sargs{};  // template (fused or reverse)
   int grid_step = 0;
   size_t smem_step = 0;
@@ -235,37 +238,53 @@ void configure(vpinn_gpu_ctx* c) {
     a.n_int_tiles = c->E ? ceil_div(c->E, a.cells_per_tile) : 0;
     a.n_tiles = a.n_int_tiles + ceil_div(c->n_bnd + c->n_sen, vpg::kThreads);
     const int tile_rows = a.cells_per_tile * c->T;
-    const size_t min_smem = V.smem(V.rev_need, 1);
-    const size_t budget = min_smem <= two_cta ? two_cta : (size_t)227 * 1024;
-    // the whole tile slab in one stage when it fits (one contraction chunk,
-    // fewer barriers); otherwise a two-stage ring of half tiles or smaller
-    bool single = true;
-    int rows = tile_rows;
-    for (;;) {
-      const int tstride = round4(rows * c->Q + 8);
-      const int stage = c->nt * tstride;
-      const int uni = std::max(V.rev_need, single ? stage : 2 * stage);
-      if (single && V.smem(uni, rows) > budget) {
-        single = false;
-        rows = (tile_rows + 1) / 2;
-        continue;
+    // tensor-core step: whole-tile slab in one of its operand buffers
+    const char* tc_env = std::getenv("VPINN_TC");
+    c->tc = V.tc != nullptr && !(tc_env && std::atoi(tc_env) == 0) && c->eps_source != VPINN_EPS_SPATIAL &&
+            tile_rows <= 128 && (size_t)c->nt * round4(tile_rows * c->Q + 8) * sizeof(float) <= (size_t)vpg::kTcBuf;
+    if (c->tc) {
+      a.chunk_rows = tile_rows;
+      a.tstride = round4(tile_rows * c->Q + 8);
+      a.stage_floats = c->nt * a.tstride;
+      a.union_floats = 0;
+      c->smem_step = V.tc_smem;
+      CK(cudaFuncSetAttribute(V.tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem_step));
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, V.tc, vpg::kTcThreads, c->smem_step));
+      if (occ < 1) throw Fail{VPINN_ERR_DEVICE, "tensor-core step kernel cannot be resident"};
+      c->grid_step = std::max(1, std::min(a.n_tiles, c->sm_count));
+    } else {
+      const size_t min_smem = V.smem(V.rev_need, 1);
+      const size_t budget = min_smem <= two_cta ? two_cta : (size_t)227 * 1024;
+      // the whole tile slab in one stage when it fits (one contraction chunk,
+      // fewer barriers); otherwise a two-stage ring of half tiles or smaller
+      bool single = true;
+      int rows = tile_rows;
+      for (;;) {
+        const int tstride = round4(rows * c->Q + 8);
+        const int stage = c->nt * tstride;
+        const int uni = std::max(V.rev_need, single ? stage : 2 * stage);
+        if (single && V.smem(uni, rows) > budget) {
+          single = false;
+          rows = (tile_rows + 1) / 2;
+          continue;
+        }
+        if (V.smem(uni, rows) <= budget || rows == 1) {
+          a.chunk_rows = rows;
+          a.tstride = tstride;
+          a.stage_floats = stage;
+          a.union_floats = uni;
+          break;
+        }
+        rows = std::max(1, rows * 3 / 4);
       }
-      if (V.smem(uni, rows) <= budget || rows == 1) {
-        a.chunk_rows = rows;
-        a.tstride = tstride;
-        a.stage_floats = stage;
-        a.union_floats = uni;
-        break;
-      }
-      rows = std::max(1, rows * 3 / 4);
+      c->smem_step = V.smem(a.union_floats, a.chunk_rows);
+      if (c->smem_step > (size_t)227 * 1024)
+        throw Fail{VPINN_ERR_CONFIG, "fused step kernel does not fit shared memory"};
+      CK(cudaFuncSetAttribute(V.fused, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem_step));
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, V.fused, vpg::kThreads, c->smem_step));
+      if (occ < 1) throw Fail{VPINN_ERR_DEVICE, "fused step kernel cannot be resident"};
+      c->grid_step = std::max(1, std::min(a.n_tiles, occ * c->sm_count));
     }
-    c->smem_step = V.smem(a.union_floats, a.chunk_rows);
-    if (c->smem_step > (size_t)227 * 1024)
-      throw Fail{VPINN_ERR_CONFIG, "fused step kernel does not fit shared memory"};
-    CK(cudaFuncSetAttribute(V.fused, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem_step));
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, V.fused, vpg::kThreads, c->smem_step));
-    if (occ < 1) throw Fail{VPINN_ERR_DEVICE, "fused step kernel cannot be resident"};
-    c->grid_step = std::max(1, std::min(a.n_tiles, occ * c->sm_count));
     c->grad_rows = c->grid_step;
     c->loss_rows = c->grid_step;
   } else {
@@ -329,8 +348,8 @@ void configure(vpinn_gpu_ctx* c) {
     c->grid_contract = std::max(1, std::min(std::max(1, ca.n_tiles), std::max(1, occ) * c->sm_count));
     c->grid_pen = (c->n_bnd + c->n_sen) ? std::min(64, ceil_div(c->n_bnd + c->n_sen, 256)) : 0;
   }
-  // ---- whole-cell HBM-streaming contraction (Q <= 128) ----
-  c->cell_contract = c->Q <= vpg::kCCThreads && c->T <= vpg::kCCThreads && c->E > 0;
+  // ---- whole-cell HBM-streaming contraction (warp per cell) ----
+  c->cell_contract = c->E > 0;
   if (c->cell_contract) {
     vpg::CellContractArgs& cc = c->ccargs;
     std::memset(&cc, 0, sizeof(cc));
@@ -340,11 +359,10 @@ void configure(vpinn_gpu_ctx* c) {
     cc.T = c->T;
     cc.Q = c->Q;
     cc.nt = c->nt;
-    cc.cc = std::max(1, std::min(vpg::kCCThreads / c->Q, vpg::kCCThreads / c->T));
-    if (const char* e = std::getenv("VPINN_CC_CELLS")) cc.cc = std::max(1, std::min(cc.cc, std::atoi(e)));
-    cc.tstride = round4(cc.cc * c->T * c->Q + 8);
-    cc.vstride = round4(cc.cc * c->Q + 8);
-    cc.fstride = round4(cc.cc * c->T + 8);
+    cc.cc = 1;
+    cc.tstride = round4(c->T * c->Q + 8);
+    cc.vstride = round4(c->Q + 8);
+    cc.fstride = round4(c->T + 8);
     cc.stage_floats = c->nt * cc.tstride + 3 * cc.vstride + cc.fstride;
     cc.e_fixed = c->eps;
     cc.eps_source = c->eps_source;
@@ -352,23 +370,19 @@ void configure(vpinn_gpu_ctx* c) {
     cc.by = c->by;
     cc.rscale = a.rscale;
     cc.inv_nt = a.inv_nt;
-    cc.nstage = 4;
-    size_t cc_budget = two_cta;
-    if (const char* e = std::getenv("VPINN_CC_ONE_CTA")) cc_budget = std::atoi(e) ? (size_t)227 * 1024 : two_cta;
-    while (cc.nstage > 2 && vpg::cell_contract_smem_bytes(cc.stage_floats, cc.nstage) > cc_budget) --cc.nstage;
-    if (const char* e = std::getenv("VPINN_CC_STAGES")) cc.nstage = std::max(2, std::min(4, std::atoi(e)));
-    cc.use_ldgsts = 0;  // TMA bulk by default; LDGSTS measured equal
-    if (const char* e = std::getenv("VPINN_CC_LDGSTS")) cc.use_ldgsts = std::atoi(e);
-    c->smem_cc = vpg::cell_contract_smem_bytes(cc.stage_floats, cc.nstage);
-    if (c->smem_cc > (size_t)227 * 1024) {
-      c->cell_contract = false;
+    const size_t budget = (size_t)227 * 1024;
+    cc.nstage = 3;
+    while (cc.nstage > 2 && vpg::cell_warp_smem_bytes(cc.stage_floats, cc.nstage, c->T, c->Q) > budget) --cc.nstage;
+    if (const char* e = std::getenv("VPINN_CW_STAGES")) cc.nstage = std::max(2, std::min(vpg::kCCMaxStages, std::atoi(e)));
+    c->smem_cc = vpg::cell_warp_smem_bytes(cc.stage_floats, cc.nstage, c->T, c->Q);
+    if (c->smem_cc > budget) {
+      c->cell_contract = false;  // cell larger than a warp's ring: row-chunked kernel
     } else {
-      CK(cudaFuncSetAttribute(vpg::contract_cells_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      CK(cudaFuncSetAttribute(vpg::contract_warp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               (int)c->smem_cc));
-      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, vpg::contract_cells_kernel, vpg::kCCThreads,
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, vpg::contract_warp_kernel, vpg::kCWThreads,
                                                        c->smem_cc));
-      const int chunks = ceil_div(c->E, cc.cc);
-      c->grid_cc = std::max(1, std::min(chunks, std::max(1, occ) * c->sm_count));
+      c->grid_cc = std::max(1, std::min(ceil_div(c->E, vpg::kCWWarps), std::max(1, occ) * c->sm_count));
     }
   }
   if (c->split) c->loss_rows = c->grid_contract + c->grid_pen + c->grid_step;
@@ -401,15 +415,22 @@ void configure(vpinn_gpu_ctx* c) {
   c->e_scalar.alloc(1);
 }
 
+void launch_fused(vpinn_gpu_ctx* c, const vpg::StepArgs& a) {
+  if (c->tc)
+    c->var.tc<<<c->grid_step, vpg::kTcThreads, c->smem_step, c->stream>>>(a);
+  else
+    c->var.fused<<<c->grid_step, vpg::kThreads, c->smem_step, c->stream>>>(a);
+  CK(cudaGetLastError());
+  c->launches += 1;
+}
+
 // ---- one epoch: loss + gradient (+ Adam) enqueued on the context stream ----
 void enqueue_grad(vpinn_gpu_ctx* c, const int* stop, bool with_reduce = true) {
   const Variant& V = c->var;
   vpg::StepArgs a = c->sargs;
   a.stop_flag = stop;
   if (!c->split) {
-    V.fused<<<c->grid_step, vpg::kThreads, c->smem_step, c->stream>>>(a);
-    CK(cudaGetLastError());
-    c->launches += 1;
+    launch_fused(c, a);
   } else {
     const int P_local = c->n_int + c->n_bnd + c->n_sen;
     vpg::StepArgs f = a;
@@ -564,7 +585,7 @@ int launch_contract(vpinn_gpu_ctx* c, const float* ux, const float* uy, const fl
     a.rscale = rscale;
     a.loss_part = loss_part;
     a.stop_flag = stop;
-    vpg::contract_cells_kernel<<<c->grid_cc, vpg::kCCThreads, c->smem_cc, c->stream>>>(a);
+    vpg::contract_warp_kernel<<<c->grid_cc, vpg::kCWThreads, c->smem_cc, c->stream>>>(a);
     CK(cudaGetLastError());
     c->launches += 1;
     return c->grid_cc;
@@ -587,6 +608,17 @@ int launch_contract(vpinn_gpu_ctx* c, const float* ux, const float* uy, const fl
     c->launches += 1;
   }
   return c->grid_contract;
+}
+
+// L2 flush between timed launches: write a 256 MB buffer (> 126 MB L2), then
+// read it back so the write-back of the dirty lines happens here and not
+// inside the next timed kernel.
+void flush_l2_now(vpinn_gpu_ctx* c, char* buf) {
+  const size_t bytes = (size_t)256 << 20;
+  CK(cudaMemsetAsync(buf, (int)(c->launches & 0xff), bytes, c->stream));
+  vpg::flush_read_kernel<<<4 * c->sm_count, 512, 0, c->stream>>>(reinterpret_cast<const int4*>(buf), bytes / 16,
+                                                                 reinterpret_cast<int*>(buf));
+  CK(cudaGetLastError());
 }
 
 long long launches_per_epoch(const vpinn_gpu_ctx* c) {
@@ -1076,7 +1108,7 @@ int vpinn_gpu_time_contract(vpinn_gpu_ctx* c, int reps, double* ms_per_launch, d
     CK(cudaEventCreate(&e1));
     double total = 0.0;
     for (int r = 0; r < reps + 2; ++r) {
-      CK(cudaMemsetAsync(flush.p, r & 0xff, (size_t)256 << 20, c->stream));
+      flush_l2_now(c, flush.p);
       CK(cudaEventRecord(e0, c->stream));
       launch_contract(c, ux.p, uy.p, ep.p, oxb.p, oyb.p, oeb.p, nullptr, es.p, c->sargs.rscale, lp.p, nullptr);
       CK(cudaEventRecord(e1, c->stream));
@@ -1124,9 +1156,7 @@ int vpinn_gpu_profile_step(vpinn_gpu_ctx* c, int reps, double* ms_mlp, double* m
       vpg::StepArgs a = c->sargs;
       a.stop_flag = &c->st.p->stopped;
       if (!c->split) {
-        V.fused<<<c->grid_step, vpg::kThreads, c->smem_step, c->stream>>>(a);
-        CK(cudaGetLastError());
-        c->launches += 1;
+        launch_fused(c, a);
         CK(cudaEventRecord(ev[1], c->stream));
         vpg::reduce_kernel<<<vpg::reduce_grid(c->n_params), vpg::kRedThreads, 0, c->stream>>>(
             c->grad_part.p, c->grad_rows, c->part_stride, c->n_params, c->loss_part.p, c->loss_rows, c->red.p,
@@ -1167,7 +1197,27 @@ int vpinn_gpu_flush_l2(vpinn_gpu_ctx* c) {
   return guarded([&] {
     set_dev(c);
     if (!c->flush.p) c->flush.alloc((size_t)256 << 20);
-    CK(cudaMemsetAsync(c->flush.p, (int)(c->launches & 0xff), (size_t)256 << 20, c->stream));
+    flush_l2_now(c, c->flush.p);
+  });
+}
+
+int vpinn_gpu_tc_probe(int device, int mode, const float* A, const float* W, const float* H, float* out) {
+  return guarded([&] {
+    if (mode < 0 || mode > 2) throw Fail{VPINN_ERR_CONFIG, "tc_probe: mode must be 0, 1 or 2"};
+    CK(cudaSetDevice(device));
+    DBuf<float> dA, dW, dH, dO;
+    dA.alloc(128 * 32);
+    dW.alloc(32 * 32);
+    dH.alloc(128 * 32);
+    dO.alloc(128 * 32 + 64 * 64);
+    CK(cudaMemcpy(dA.p, A, sizeof(float) * 128 * 32, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(dW.p, W, sizeof(float) * 32 * 32, cudaMemcpyHostToDevice));
+    if (H) CK(cudaMemcpy(dH.p, H, sizeof(float) * 128 * 32, cudaMemcpyHostToDevice));
+    CK(cudaFuncSetAttribute(vpg::tc_probe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, vpg::kTcProbeSmem));
+    vpg::tc_probe_kernel<<<1, 128, vpg::kTcProbeSmem>>>(mode, dA.p, dW.p, dH.p, dO.p);
+    CK(cudaGetLastError());
+    CK(cudaDeviceSynchronize());
+    CK(cudaMemcpy(out, dO.p, sizeof(float) * (mode == 2 ? 32 * 32 : 128 * 32), cudaMemcpyDeviceToHost));
   });
 }
 

@@ -1,5 +1,5 @@
-"""Sweep the standalone contraction's chunk/ring configuration (env vars)."""
-import itertools
+"""Sweep the standalone warp-per-cell contraction's ring depth (env var
+VPINN_CW_STAGES) on the C5 gear workload; prints ms/launch and GB/s."""
 import json
 import os
 import subprocess
@@ -12,16 +12,13 @@ import bench
 from paper_2404_12063_b200 import gpu as G
 hp, _ = bench.build_problem()
 g = G.GpuStep.from_problem(hp.view(0, 0, 1), keepalive=hp)
-ms, b = g.time_contract(20)
+ms, b = g.time_contract(50)
 print(ms, b / (ms * 1e-3) / 1e9)
 ''' % ROOT
-for ldg, cells, stages, one in itertools.product([1, 0], [5, 3, 2], [2, 3, 4], [0, 1]):
-    if ldg == 0 and (stages != 2 or one):
-        continue
-    env = dict(os.environ, VPINN_CC_CELLS=str(cells), VPINN_CC_STAGES=str(stages), VPINN_CC_ONE_CTA=str(one),
-               VPINN_CC_LDGSTS=str(ldg))
+for stages in [2, 3, 4]:
+    env = dict(os.environ, VPINN_CW_STAGES=str(stages))
     r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True)
     out = r.stdout.strip().split()
-    print(json.dumps({"ldgsts": ldg, "cells": cells, "stages": stages, "one_cta_budget": one,
-                      "ms": float(out[0]) if out else None, "GBs": float(out[1]) if out else None,
-                      "err": r.stderr.strip()[-200:] if r.returncode else ""}), flush=True)
+    print(json.dumps({"stages": stages, "ms": float(out[0]) if out else None,
+                      "GBs": float(out[1]) if out else None,
+                      "err": r.stderr.strip()[-300:] if r.returncode else ""}), flush=True)
