@@ -209,10 +209,11 @@ int vpinn_gpu_flush_l2(vpinn_gpu_ctx* ctx);
  * the roofline denominator of the FFMA-bound step kernel. */
 int vpinn_gpu_measure_ffma_peak(int device, double* tflops);
 
-/* Known-answer probe of the tcgen05 3xTF32 GEMM shapes used by the
+/* Known-answer probe of the tcgen05 split-bf16 GEMM shapes used by the
  * tensor-core MLP (diagnostic).  A, H: [128][32]; W: [32][32] row-major.
  * mode 0: out[128][32] = A W^T;  mode 1: out[128][32] = A W;
- * mode 2: out[32][32] = A^T H. */
+ * mode 2: out[32][32] = A^T H.  out holds 128*32 + 128*96 floats (the raw
+ * [128][96] accumulator follows the result). */
 int vpinn_gpu_tc_probe(int device, int mode, const float* A, const float* W, const float* H, float* out);
 
 /* Multi-GPU: rank 0 creates an NCCL unique id (128 bytes), every rank

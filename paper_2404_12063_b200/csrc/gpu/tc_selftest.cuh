@@ -1,48 +1,39 @@
 // Known-answer probe of the three tcgen05 GEMM shapes the tensor-core MLP
-// uses (one CTA, 128 threads), 3xTF32 throughout:
-//   mode 0  forward      out[p][o] = sum_i A[p][i] W[o][i]   (K-major A, K-major B, N = 64 hi|lo)
+// uses (one CTA, 128 threads), bf16x3 split / six products throughout:
+//   mode 0  forward      out[p][o] = sum_i A[p][i] W[o][i]   (K-major A, K-major B, N = 96 h|m|l)
 //   mode 1  propagation  out[p][i] = sum_o A[p][o] W[o][i]   (K-major A, MN-major B)
-//   mode 2  param grad   out[o][i] = sum_p A[p][o] H[p][i]   (MN-major A, M = 64 hi|lo; MN-major B)
-// A and H are [128][32], W is [32][32], all row-major fp32.
+//   mode 2  param grad   out[o][i] = sum_p A[p][o] H[p][i]   (MN-major A, M = 128 h|m|l|-; MN-major B)
+// A and H are [128][32], W is [32][32], all row-major fp32.  out needs
+// 128*32 + 128*96 floats (the raw accumulator follows the result).
 #pragma once
 
 #include "tc_utils.cuh"
 
 namespace vpg {
 
-constexpr int kTcProbeSmem = 6 * 16384 + 8192 + 1024 + 64;
+constexpr int kTcProbeSmem = 24576 * 2 + 6144 + 8192 + 1024 + 64;
 
 __global__ void __launch_bounds__(128, 1) tc_probe_kernel(int mode, const float* __restrict__ A,
                                                           const float* __restrict__ W,
                                                           const float* __restrict__ H, float* __restrict__ out) {
   extern __shared__ __align__(1024) char tp_raw[];
   char* base = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(tp_raw) + 1023) & ~uintptr_t(1023));
-  char* a_hi = base;
-  char* a_lo = base + 16384;
-  char* h_hi = base + 2 * 16384;
-  char* h_lo = base + 3 * 16384;
-  char* wbuf = base + 4 * 16384;  // rows 0..31 hi, 32..63 lo
-  uint64_t* bar = reinterpret_cast<uint64_t*>(base + 4 * 16384 + 8192);
+  char* a_t = base;                   // 3 part tiles of [128][32]
+  char* h_t = base + 24576;           // 3 part tiles
+  char* w_t = base + 2 * 24576;       // [96][32]: W h | m | l rows
+  uint64_t* bar = reinterpret_cast<uint64_t*>(base + 2 * 24576 + 6144 + 8192);
   uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 1);
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int tid = threadIdx.x, warp = tid >> 5;
 
   if (warp == 0) tc::tmem_alloc(tslot, 128);
   if (tid == 0) {
     mbar_init(bar, 1);
     fence_mbar_init();
   }
-  // operand tiles (row = tid)
-  for (int c = 0; c < 32; c += 4) {
-    const float* ar = A + tid * 32 + c;
-    tc::st_split4(a_hi, a_lo, tid, c, ar[0], ar[1], ar[2], ar[3]);
-    if (mode == 2) {
-      const float* hr = H + tid * 32 + c;
-      tc::st_split4(h_hi, h_lo, tid, c, hr[0], hr[1], hr[2], hr[3]);
-    }
-    if (tid < 32) {
-      const float* wr = W + tid * 32 + c;
-      tc::st_split4(wbuf, wbuf + 4096, tid, c, wr[0], wr[1], wr[2], wr[3]);
-    }
+  for (int c = 0; c < 4; ++c) {
+    tc::st_split8(a_t, 8192, tid, c, A + tid * 32 + 8 * c);
+    tc::st_split8(h_t, 8192, tid, c, H + tid * 32 + 8 * c);
+    if (tid < 32) tc::st_split8(w_t, 2048, tid, c, W + tid * 32 + 8 * c);
   }
   tc::fence_smem_to_async();
   tc::fence_before_sync();
@@ -50,58 +41,47 @@ __global__ void __launch_bounds__(128, 1) tc_probe_kernel(int mode, const float*
   tc::fence_after_sync();
   const uint32_t tmem = *tslot;
   if (tid == 0) {
-    const uint32_t sa_hi = smem_u32(a_hi), sa_lo = smem_u32(a_lo), sh_hi = smem_u32(h_hi), sw = smem_u32(wbuf);
-    if (mode == 0) {
-      const uint32_t i64 = tc::idesc_tf32(128, 64, 0, 0), i32 = tc::idesc_tf32(128, 32, 0, 0);
-      for (int ks = 0; ks < 4; ++ks)
-        tc::mma_tf32(tmem, tc::sdesc(sa_hi + 32 * ks, 16, 1024), tc::sdesc(sw + 32 * ks, 16, 1024), i64, ks > 0);
-      for (int ks = 0; ks < 4; ++ks)
-        tc::mma_tf32(tmem, tc::sdesc(sa_lo + 32 * ks, 16, 1024), tc::sdesc(sw + 32 * ks, 16, 1024), i32, 1);
-    } else if (mode == 1) {
-      const uint32_t i64 = tc::idesc_tf32(128, 64, 0, 1), i32 = tc::idesc_tf32(128, 32, 0, 1);
-      for (int ks = 0; ks < 4; ++ks)
-        tc::mma_tf32(tmem, tc::sdesc(sa_hi + 32 * ks, 16, 1024), tc::sdesc(sw + 1024 * ks, 4096, 1024), i64,
-                     ks > 0);
-      for (int ks = 0; ks < 4; ++ks)
-        tc::mma_tf32(tmem, tc::sdesc(sa_lo + 32 * ks, 16, 1024), tc::sdesc(sw + 1024 * ks, 4096, 1024), i32, 1);
+    const uint32_t sa = smem_u32(a_t), sh = smem_u32(h_t), sw = smem_u32(w_t);
+    if (mode == 0 || mode == 1) {
+      const int mn = mode == 1;
+      for (int part = 0; part < 3; ++part) {
+        const uint32_t idesc = tc::idesc_bf16(128, 96 - 32 * part, 0, mn);
+        for (int ks = 0; ks < 2; ++ks) {
+          const uint64_t bd = mn ? tc::mndesc(sw + 1024 * ks, 2048) : tc::kdesc(sw + 32 * ks);
+          tc::mma_bf16(tmem, tc::kdesc(sa + part * 8192 + 32 * ks), bd, idesc, (part > 0 || ks > 0) ? 1u : 0u);
+        }
+      }
     } else {
-      const uint32_t i6464 = tc::idesc_tf32(64, 64, 1, 1);
-      for (int ks = 0; ks < 16; ++ks)
-        tc::mma_tf32(tmem, tc::sdesc(sa_hi + 1024 * ks, sa_lo - sa_hi, 1024),
-                     tc::sdesc(sh_hi + 1024 * ks, smem_u32(h_lo) - sh_hi, 1024), i6464, ks > 0);
+      const uint32_t idesc = tc::idesc_bf16(128, 96, 1, 1);
+      for (int kp = 0; kp < 8; ++kp)
+        tc::mma_bf16(tmem, tc::mndesc(sa + 1024 * kp, 8192), tc::mndesc(sh + 1024 * kp, 8192), idesc, kp > 0);
     }
     tc::mma_commit(bar);
   }
   mbar_wait(bar, 0);
   tc::fence_after_sync();
   const uint32_t lane_base = (uint32_t)(32 * warp) << 16;
-  float v0[16], v1[16], v2[16], v3[16];
-  tc::tmem_ld2x16_wait(tmem + lane_base + 0, tmem + lane_base + 16, v0, v1);
-  tc::tmem_ld2x16_wait(tmem + lane_base + 32, tmem + lane_base + 48, v2, v3);
-  if (mode != 2) {
-    for (int i = 0; i < 16; ++i) {
-      out[tid * 32 + i] = v0[i] + v2[i];
-      out[tid * 32 + 16 + i] = v1[i] + v3[i];
-    }
-  } else if (lane < 16) {
-    // M = 64 accumulator: row m = 16 * warp + lane (rows 32..63 = lo part of A)
-    const int m = 16 * warp + lane;
-    float* o = out + 128 * 32;  // raw 64 x 64 block after the first 128*32 floats
-    for (int i = 0; i < 16; ++i) {
-      o[m * 64 + i] = v0[i];
-      o[m * 64 + 16 + i] = v1[i];
-      o[m * 64 + 32 + i] = v2[i];
-      o[m * 64 + 48 + i] = v3[i];
-    }
+  float v0[16], v1[16], v2[16], v3[16], v4[16], v5[16];
+  tc::tmem_ld3x16_wait(tmem + lane_base + 0, tmem + lane_base + 32, tmem + lane_base + 64, v0, v1, v2);
+  tc::tmem_ld3x16_wait(tmem + lane_base + 16, tmem + lane_base + 48, tmem + lane_base + 80, v3, v4, v5);
+  float* raw = out + 128 * 32;  // [128][96]
+  for (int i = 0; i < 16; ++i) {
+    raw[tid * 96 + i] = v0[i];
+    raw[tid * 96 + 16 + i] = v3[i];
+    raw[tid * 96 + 32 + i] = v1[i];
+    raw[tid * 96 + 48 + i] = v4[i];
+    raw[tid * 96 + 64 + i] = v2[i];
+    raw[tid * 96 + 80 + i] = v5[i];
   }
   tc::fence_before_sync();
   __syncthreads();
-  if (mode == 2) {
-    const float* o = out + 128 * 32;
-    __threadfence_block();
+  if (mode != 2) {
+    for (int i = 0; i < 32; ++i) out[tid * 32 + i] = raw[tid * 96 + i] + raw[tid * 96 + 32 + i] + raw[tid * 96 + 64 + i];
+  } else {
     for (int e = tid; e < 32 * 32; e += 128) {
-      const int r = e / 32, c = e % 32;
-      out[e] = o[r * 64 + c] + o[r * 64 + 32 + c] + o[(32 + r) * 64 + c];
+      const int o = e / 32, i = e % 32;
+      out[e] = raw[o * 96 + i] + raw[o * 96 + 32 + i] + raw[o * 96 + 64 + i] + raw[(32 + o) * 96 + i] +
+               raw[(32 + o) * 96 + 32 + i] + raw[(64 + o) * 96 + i];
     }
   }
   if (warp == 0) {

@@ -1,25 +1,26 @@
-// Tensor-core (tcgen05, 3xTF32) FastVPINNs training step for sm_100a.
+// Tensor-core (tcgen05, split-bf16) FastVPINNs training step for sm_100a.
 //
 // Same per-tile semantics as step_kernel<..., kModeFused> (step_kernel.cuh):
 // forward with x/y tangents (network.hpp:204-282), the Algorithm-3
 // contraction (losses.hpp:91-168) or the penalty terms (losses.hpp:406-415),
 // and the reverse sweep (network.hpp:287-372) — but every hidden->hidden
 // GEMM runs on the 5th-generation tensor cores:
-//   forward      D_s[p][o]  = X_s[p][:] . W[o][:]      M = 128 points, N = 64 (W hi | W lo), K = 32
-//   propagation  D_s[p][i]  = G_s[p][:] . W[:][i]      M = 128 points, N = 64, K = 32 (B MN-major)
+//   forward      D_s[p][o]  = X_s[p][:] . W[o][:]      M = 128 points, N = 96 (W h | m | l), K = 32
+//   propagation  D_s[p][i]  = G_s[p][:] . W[:][i]      M = 128 points, N = 96, K = 32 (B MN-major)
 //   param grad   Wbar[o][i] += sum_{s,p} G_s[p][o] X_s[p][i]
-//                                                     M = 64 (G hi | G lo), N = 64 (X hi | X lo),
+//                                                     M = 128 (G h | m | l | -), N = 96 (X h | m | l),
 //                                                     K = 3 streams x 128 points, accumulated in
 //                                                     TMEM across all tiles of the CTA
-// s = value / x-tangent / y-tangent stream.  Products are 3xTF32
-// (tc_utils.cuh): hi*hi + hi*lo + lo*hi, fp32 accumulation, so the result
-// is fp32-faithful (the parity tolerance of the north star holds).  The
+// s = value / x-tangent / y-tangent stream.  Operands are split three ways
+// into bf16 and each product is the six-term sum of tc_utils.cuh with fp32
+// accumulation, so the result is fp32-faithful (the parity tolerance of the
+// north star holds).  The
 // value stream carries a constant-one column at index H, which turns the
 // parameter-gradient GEMM's column H into the bias gradient.
 //
 // CTA = 256 threads; thread t owns point p = t % 128 (= its TMEM lane) and
 // hidden units [16*(t/128), +16).  One CTA per SM (TMEM 512 columns,
-// ~220 KB shared memory).  Hidden layers D in {2, 3}, H <= 31, one output.
+// ~170 KB shared memory).  Hidden layers D in {2, 3}, H <= 31, one output.
 // Every phase is separated by a CTA barrier or an MMA-completion mbarrier;
 // one elected thread issues all MMAs.
 #pragma once
@@ -30,11 +31,13 @@
 namespace vpg {
 
 constexpr int kTcThreads = 256;
-constexpr int kTcTile = 16384;              // one [128][32] fp32 operand tile
-constexpr int kTcBuf = 6 * kTcTile;         // 3 streams x (hi, lo)
-constexpr int kTcW = 8192;                  // [64][32]: W hi rows 0..31, W lo rows 32..63
+constexpr int kTcPart = 8192;               // one [128][32] bf16 operand tile
+constexpr int kTcStream = 3 * kTcPart;      // h | m | l parts of one stream
+constexpr int kTcBuf = 3 * kTcStream;       // 3 streams
+constexpr int kTcW = 6144;                  // [96][32] bf16: W h | m | l rows
 constexpr uint32_t kTcCols = 512;           // TMEM columns allocated
-constexpr int kTcAccCol = 192;              // parameter-gradient accumulators start here
+constexpr int kTcDCols = 96;                // accumulator columns per stream (h | m | l products)
+constexpr int kTcAccCol = 3 * kTcDCols;     // parameter-gradient accumulators start here
 
 // exchange rows of the tensor-core kernel ([row][128] floats)
 enum : int { kTxX = 0, kTxY, kTxU, kTxUx, kTxUy, kTxSx, kTxSy, kTxCv, kTxUb, kTxUxb, kTxUyb, kTxPu, kTxPx, kTxPy,
@@ -46,7 +49,9 @@ struct TcLayout {
   static constexpr int OFF_W = 0;                       // NL x kTcW
   static constexpr int OFF_A = OFF_W + NL * kTcW;       // buffer A (1024-aligned)
   static constexpr int OFF_B = OFF_A + kTcBuf;          // buffer B
-  static constexpr int OFF_SMALL = OFF_B + kTcBuf;      // floats from here
+  static constexpr int OFF_SMALL = OFF_B + kTcBuf;      // floats from here (>= 8 KB: the
+                                                        // unused 4th M block of a param-grad
+                                                        // A operand in buffer B reads it)
   // small region, in floats
   static constexpr int S_W0 = 0;                        // [32][4] (w_x, w_y, b, 0)
   static constexpr int S_BIAS = S_W0 + 128;             // [NL][32]
@@ -60,6 +65,8 @@ struct TcLayout {
   static constexpr int S_BAR = S_RED + 128;             // mbarriers + TMEM slot (16 floats)
   static constexpr int S_END = S_BAR + 16;
   static constexpr size_t BYTES = (size_t)OFF_SMALL + sizeof(float) * S_END + 1024;  // + alignment slack
+  static_assert(S_END * 4 >= kTcPart, "small region must cover one operand tile");
+  static_assert(OFF_A % 1024 == 0, "operand buffers must be 1024-byte aligned");
 };
 
 // small-gradient accumulator slots (S_GACC)
@@ -151,13 +158,16 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_step_kernel(const StepArgs a
   if (tid == 0) sWd[32] = P[net.b_off[D]];
   for (int l = 1; l <= NL; ++l) {
     char* wb = sWB + (l - 1) * kTcW;
-    // row o, 4 columns per item (hi rows 0..31, lo rows 32..63)
-    for (int e = tid; e < 32 * 8; e += kTcThreads) {
-      const int o = e >> 3, c0 = (e & 7) * 4;
-      float v[4];
+    // row o, 8 columns per item; parts h | m | l at rows 0 | 32 | 64
+    for (int e = tid; e < 32 * 4; e += kTcThreads) {
+      const int o = e >> 2, c = e & 3;
+      float v[8];
 #pragma unroll
-      for (int k = 0; k < 4; ++k) v[k] = (o < H && c0 + k < H) ? P[net.w_off[l] + o * H + c0 + k] : 0.f;
-      tc::st_split4(wb, wb + 4096, o, c0, v[0], v[1], v[2], v[3]);
+      for (int k = 0; k < 8; ++k) {
+        const int i = 8 * c + k;
+        v[k] = (o < H && i < H) ? P[net.w_off[l] + o * H + i] : 0.f;
+      }
+      tc::st_split8(wb, 32 * tc::kRowBytes, o, c, v);
     }
     for (int o = tid; o < 32; o += kTcThreads) sBias[(l - 1) * 32 + o] = o < H ? P[net.b_off[l] + o] : 0.f;
   }
@@ -172,37 +182,35 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_step_kernel(const StepArgs a
 
   // MMA helpers (thread 0 only) -------------------------------------------------
   const uint32_t sA = smem_u32(bufA), sB = smem_u32(bufB), sW = smem_u32(sWB);
-  // forward / propagation of layer l: A tiles (K-major) from buffer abuf, stream-major
+  // forward (propagate == false) or propagation of layer l; A parts (K-major)
+  // from buffer abuf: D_s[0:96) = h.[Wh|Wm|Wl], D_s[0:64) += m.[Wh|Wm], D_s[0:32) += l.Wh
   auto issue_point_gemm = [&](uint32_t abuf, int l, bool propagate) {
     const uint32_t wbase = sW + (uint32_t)(l - 1) * kTcW;
-    const uint32_t i64 = tc::idesc_tf32(128, 64, 0, propagate ? 1 : 0);
-    const uint32_t i32 = tc::idesc_tf32(128, 32, 0, propagate ? 1 : 0);
 #pragma unroll 1
     for (int s = 0; s < 3; ++s) {
-      const uint32_t d = tmem + 64 * s;
-      const uint32_t ahi = abuf + 2 * s * kTcTile, alo = ahi + kTcTile;
+      const uint32_t d = tmem + kTcDCols * s;
 #pragma unroll
-      for (int ks = 0; ks < 4; ++ks) {
-        const uint64_t bd = propagate ? tc::sdesc(wbase + 1024 * ks, 4096, 1024) : tc::sdesc(wbase + 32 * ks, 16, 1024);
-        tc::mma_tf32(d, tc::sdesc(ahi + 32 * ks, 16, 1024), bd, i64, ks > 0);
-      }
+      for (int part = 0; part < 3; ++part) {
+        const uint32_t idesc = tc::idesc_bf16(128, 96 - 32 * part, 0, propagate ? 1 : 0);
+        const uint32_t abase = abuf + s * kTcStream + part * kTcPart;
 #pragma unroll
-      for (int ks = 0; ks < 4; ++ks) {
-        const uint64_t bd = propagate ? tc::sdesc(wbase + 1024 * ks, 4096, 1024) : tc::sdesc(wbase + 32 * ks, 16, 1024);
-        tc::mma_tf32(d, tc::sdesc(alo + 32 * ks, 16, 1024), bd, i32, 1);
+        for (int ks = 0; ks < 2; ++ks) {
+          const uint64_t bd = propagate ? tc::mndesc(wbase + 1024 * ks, 32 * tc::kRowBytes) : tc::kdesc(wbase + 32 * ks);
+          tc::mma_bf16(d, tc::kdesc(abase + 32 * ks), bd, idesc, (part > 0 || ks > 0) ? 1u : 0u);
+        }
       }
     }
   };
-  // parameter gradient of layer l: G tiles in gbuf, X tiles in xbuf
+  // parameter gradient of layer l: G parts in gbuf (M = h|m|l|-), X parts in xbuf (N = h|m|l)
   auto issue_param_gemm = [&](uint32_t gbuf, uint32_t xbuf, int l, bool first) {
-    const uint32_t acc = tmem + kTcAccCol + 64 * (l - 1);
-    const uint32_t idesc = tc::idesc_tf32(64, 64, 1, 1);
+    const uint32_t acc = tmem + kTcAccCol + kTcDCols * (l - 1);
+    const uint32_t idesc = tc::idesc_bf16(128, 96, 1, 1);
 #pragma unroll 1
     for (int s = 0; s < 3; ++s) {
-      const uint32_t g = gbuf + 2 * s * kTcTile, x = xbuf + 2 * s * kTcTile;
-#pragma unroll 4
-      for (int kp = 0; kp < 16; ++kp)
-        tc::mma_tf32(acc, tc::sdesc(g + 1024 * kp, kTcTile, 1024), tc::sdesc(x + 1024 * kp, kTcTile, 1024), idesc,
+      const uint32_t g = gbuf + s * kTcStream, x = xbuf + s * kTcStream;
+#pragma unroll
+      for (int kp = 0; kp < 8; ++kp)
+        tc::mma_bf16(acc, tc::mndesc(g + 1024 * kp, kTcPart), tc::mndesc(x + 1024 * kp, kTcPart), idesc,
                      (first && s == 0 && kp == 0) ? 0u : 1u);
     }
   };
@@ -241,36 +249,27 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_step_kernel(const StepArgs a
       }
     }
   };
+  // the three streams of this thread's row, split into bf16 parts
   auto store3 = [&](char* buf, const float (&z)[16], const float (&tx)[16], const float (&ty)[16]) {
 #pragma unroll
-    for (int c = 0; c < 16; c += 4) {
-      tc::st_split4(buf, buf + kTcTile, p, u0 + c, z[c], z[c + 1], z[c + 2], z[c + 3]);
-      tc::st_split4(buf + 2 * kTcTile, buf + 3 * kTcTile, p, u0 + c, tx[c], tx[c + 1], tx[c + 2], tx[c + 3]);
-      tc::st_split4(buf + 4 * kTcTile, buf + 5 * kTcTile, p, u0 + c, ty[c], ty[c + 1], ty[c + 2], ty[c + 3]);
+    for (int j = 0; j < 2; ++j) {
+      tc::st_split8(buf, kTcPart, p, 2 * hh + j, z + 8 * j);
+      tc::st_split8(buf + kTcStream, kTcPart, p, 2 * hh + j, tx + 8 * j);
+      tc::st_split8(buf + 2 * kTcStream, kTcPart, p, 2 * hh + j, ty + 8 * j);
     }
   };
-  // read back one stream of a buffer (hi + lo, exact)
+  // read back one stream of a buffer (h + m + l)
   auto load1 = [&](const char* buf, int s, float (&v)[16]) {
-    const char* hi = buf + 2 * s * kTcTile;
-    const char* lo = hi + kTcTile;
 #pragma unroll
-    for (int c = 0; c < 16; c += 4) {
-      const uint32_t off = tc::sw_off(p, u0 + c);
-      const float4 h4 = *reinterpret_cast<const float4*>(hi + off);
-      const float4 l4 = *reinterpret_cast<const float4*>(lo + off);
-      v[c] = h4.x + l4.x;
-      v[c + 1] = h4.y + l4.y;
-      v[c + 2] = h4.z + l4.z;
-      v[c + 3] = h4.w + l4.w;
-    }
+    for (int j = 0; j < 2; ++j) tc::ld_join8(buf + s * kTcStream, kTcPart, p, 2 * hh + j, v + 8 * j);
   };
-  // accumulator of stream s (hi*hi + lo*hi in columns [0,32), hi*lo in [32,64))
+  // accumulator of stream s: columns [0,32) + [32,64) + [64,96)
   auto acc_stream = [&](int s, float (&v)[16]) {
-    float x0[16], x1[16];
-    const uint32_t col = tmem + lane_q + 64 * s + u0;
-    tc::tmem_ld2x16_wait(col, col + 32, x0, x1);
+    float x0[16], x1[16], x2[16];
+    const uint32_t col = tmem + lane_q + kTcDCols * s + u0;
+    tc::tmem_ld3x16_wait(col, col + 32, col + 64, x0, x1, x2);
 #pragma unroll
-    for (int k = 0; k < 16; ++k) v[k] = x0[k] + x1[k];
+    for (int k = 0; k < 16; ++k) v[k] = (x0[k] + x1[k]) + x2[k];
   };
 
   bool first_grad = true;
@@ -639,25 +638,23 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_step_kernel(const StepArgs a
   }
 
   // =================== per-CTA outputs ===================
-  // parameter-gradient accumulators (TMEM, M = 64 layout: row m -> lane
-  // (m % 16) + 32 (m / 16)) -> smem [64][64] -> Wbar = hi.hi + hi.lo + lo.hi
+  // parameter-gradient accumulators (TMEM, M = 128: row m = lane m; rows
+  // 0..31 / 32..63 / 64..95 = G parts h / m / l, columns [0,32) [32,64) [64,96)
+  // = X parts h / m / l) -> smem [128][97] -> the six-term sum
   float* scr = reinterpret_cast<float*>(bufA);
   for (int l = 1; l <= NL; ++l) {
     tc::fence_after_sync();
     if (warp < 4 && !first_grad) {
-      float v0[16], v1[16], v2[16], v3[16];
-      const uint32_t col = tmem + lane_q + kTcAccCol + 64 * (l - 1);
-      tc::tmem_ld2x16_wait(col, col + 16, v0, v1);
-      tc::tmem_ld2x16_wait(col + 32, col + 48, v2, v3);
-      const int lane = tid & 31;
-      if (lane < 16) {
-        const int m = 16 * warp + lane;
+      float v0[16], v1[16], v2[16];
+      const uint32_t col = tmem + lane_q + kTcAccCol + kTcDCols * (l - 1);
+#pragma unroll 1
+      for (int h2 = 0; h2 < 2; ++h2) {
+        tc::tmem_ld3x16_wait(col + 16 * h2, col + 32 + 16 * h2, col + 64 + 16 * h2, v0, v1, v2);
 #pragma unroll
         for (int k = 0; k < 16; ++k) {
-          scr[m * 65 + k] = v0[k];
-          scr[m * 65 + 16 + k] = v1[k];
-          scr[m * 65 + 32 + k] = v2[k];
-          scr[m * 65 + 48 + k] = v3[k];
+          scr[p * 97 + 16 * h2 + k] = v0[k];
+          scr[p * 97 + 32 + 16 * h2 + k] = v1[k];
+          scr[p * 97 + 64 + 16 * h2 + k] = v2[k];
         }
       }
     }
@@ -667,7 +664,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_step_kernel(const StepArgs a
     for (int e = tid; e < fo * (fi + 1); e += kTcThreads) {
       const int o = e / (fi + 1), i = e - o * (fi + 1);
       float g = 0.f;
-      if (!first_grad) g = scr[o * 65 + i] + scr[o * 65 + 32 + i] + scr[(32 + o) * 65 + i];
+      if (!first_grad)
+        g = ((scr[o * 97 + i] + scr[o * 97 + 32 + i]) + (scr[o * 97 + 64 + i] + scr[(32 + o) * 97 + i])) +
+            (scr[(32 + o) * 97 + 32 + i] + scr[(64 + o) * 97 + i]);
       const int idx = (i < fi) ? net.w_off[l] + o * fi + i : net.b_off[l] + o;
       a.grad_part[(size_t)idx * a.part_stride + blockIdx.x] = g;
     }

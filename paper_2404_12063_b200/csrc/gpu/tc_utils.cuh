@@ -1,16 +1,24 @@
 // tcgen05 / TMEM building blocks for the tensor-core MLP (sm_100a).
 //
-// Operand tiles live in shared memory in the 128-byte-swizzled layout: a
-// tile is R rows of 32 fp32 values (128 B per row), 16-byte chunk c of row r
-// stored at chunk position c ^ (r & 7), rows contiguous, 1024-byte aligned.
-// One buffer serves two MMA views:
-//   K-major  (rows = M or N, the 32 values = K): A of the point-major GEMMs
-//   MN-major (rows = K, the 32 values = M or N): operands of the
-//            parameter-gradient GEMMs, where K runs over points.
-// fp32-faithful products use the 3xTF32 split: x = hi + lo with
-// hi = x truncated to TF32 (exact in TF32) and lo = x - hi (exact in fp32),
-// x*y ~ hi*hi + hi*lo + lo*hi (the dropped lo*lo term is 2^-22 relative).
+// fp32-faithful products on the bf16 tensor cores: every operand x is split
+// into three bf16 parts x = h + m + l (h = bf16(x), m = bf16(x - h),
+// l = bf16(x - h - m); 24 significant bits in total) and a product is the
+// sum of the six terms hh + hm + mh + mm + hl + lh (the dropped ml, lm, ll
+// terms are below 2^-26 relative), accumulated in fp32 in TMEM.  Six bf16
+// MMAs cost the same tensor time as three TF32 ones.
+//
+// Operand tiles live in shared memory as R rows of 32 bf16 (64 B per row)
+// in the 64-byte-swizzled layout (16-byte chunk c of row r stored at chunk
+// c ^ ((r >> 1) & 3)), rows contiguous, 8-row atoms of 512 B, 1024-byte
+// aligned.  The same tile is a valid operand in both majors:
+//   K-major  (rows = M or N, the 32 values = K): point-major GEMM operands
+//   MN-major (rows = K, the 32 values = M or N): the parameter-gradient GEMM,
+//            whose K runs over points.
+// (MN-major TF32 operands would need a different swizzle than K-major ones,
+// which is why the split is bf16 and not TF32.)
 #pragma once
+
+#include <cuda_bf16.h>
 
 #include <cstdint>
 
@@ -19,46 +27,101 @@
 namespace vpg {
 namespace tc {
 
-// ---- TF32 split --------------------------------------------------------------
-__device__ __forceinline__ float tf32_hi(float x) { return __uint_as_float(__float_as_uint(x) & 0xffffe000u); }
+constexpr int kRowBytes = 64;  // 32 bf16
 
-// byte offset of element (row, col) inside a swizzled 32-column tile
-__host__ __device__ __forceinline__ uint32_t sw_off(int row, int col) {
-  return (uint32_t)row * 128u + ((((uint32_t)col >> 2) ^ ((uint32_t)row & 7u)) << 4) + (((uint32_t)col & 3u) << 2);
+// byte offset of the 16-byte chunk holding columns [8 chunk, 8 chunk + 8) of row
+__host__ __device__ __forceinline__ uint32_t sw_chunk(int row, int chunk) {
+  return (uint32_t)row * kRowBytes + ((((uint32_t)chunk) ^ (((uint32_t)row >> 1) & 3u)) << 4);
 }
 
-// store 4 consecutive columns c0..c0+3 (c0 % 4 == 0) of one row as hi / lo
-__device__ __forceinline__ void st_split4(char* hi_tile, char* lo_tile, int row, int c0, float a, float b, float c,
-                                          float d) {
-  const uint32_t off = sw_off(row, c0);
-  const float ha = tf32_hi(a), hb = tf32_hi(b), hc = tf32_hi(c), hd = tf32_hi(d);
-  *reinterpret_cast<float4*>(hi_tile + off) = make_float4(ha, hb, hc, hd);
-  *reinterpret_cast<float4*>(lo_tile + off) = make_float4(a - ha, b - hb, c - hc, d - hd);
+struct Split8 {
+  uint4 h, m, l;
+};
+
+__device__ __forceinline__ uint32_t pack2(__nv_bfloat16 a, __nv_bfloat16 b) {
+  return (uint32_t)__bfloat16_as_ushort(a) | ((uint32_t)__bfloat16_as_ushort(b) << 16);
+}
+
+// three-way bf16 split of 8 consecutive values
+__device__ __forceinline__ Split8 split8(const float* v) {
+  uint32_t h[4], m[4], l[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    __nv_bfloat16 hb[2], mb[2], lb[2];
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const float x = v[2 * k + e];
+      hb[e] = __float2bfloat16_rn(x);
+      const float r1 = x - __bfloat162float(hb[e]);
+      mb[e] = __float2bfloat16_rn(r1);
+      const float r2 = r1 - __bfloat162float(mb[e]);
+      lb[e] = __float2bfloat16_rn(r2);
+    }
+    h[k] = pack2(hb[0], hb[1]);
+    m[k] = pack2(mb[0], mb[1]);
+    l[k] = pack2(lb[0], lb[1]);
+  }
+  return {make_uint4(h[0], h[1], h[2], h[3]), make_uint4(m[0], m[1], m[2], m[3]), make_uint4(l[0], l[1], l[2], l[3])};
+}
+
+// store 8 consecutive columns [8 chunk, +8) of one row into the three part
+// tiles at base, base + part_stride, base + 2 part_stride
+__device__ __forceinline__ void st_split8(char* base, uint32_t part_stride, int row, int chunk, const float* v) {
+  const Split8 s = split8(v);
+  const uint32_t off = sw_chunk(row, chunk);
+  *reinterpret_cast<uint4*>(base + off) = s.h;
+  *reinterpret_cast<uint4*>(base + part_stride + off) = s.m;
+  *reinterpret_cast<uint4*>(base + 2 * part_stride + off) = s.l;
+}
+
+__device__ __forceinline__ void unpack8(uint4 q, float* v) {
+  const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    v[2 * k] = __uint_as_float(w[k] << 16);
+    v[2 * k + 1] = __uint_as_float(w[k] & 0xffff0000u);
+  }
+}
+
+// read back 8 columns as h + m + l
+__device__ __forceinline__ void ld_join8(const char* base, uint32_t part_stride, int row, int chunk, float* v) {
+  const uint32_t off = sw_chunk(row, chunk);
+  float h[8], m[8], l[8];
+  unpack8(*reinterpret_cast<const uint4*>(base + off), h);
+  unpack8(*reinterpret_cast<const uint4*>(base + part_stride + off), m);
+  unpack8(*reinterpret_cast<const uint4*>(base + 2 * part_stride + off), l);
+#pragma unroll
+  for (int k = 0; k < 8; ++k) v[k] = h[k] + (m[k] + l[k]);
 }
 
 // ---- descriptors ---------------------------------------------------------------
-// shared-memory matrix descriptor (sm100 layout): start >> 4 [0,14), LBO >> 4
+// shared-memory matrix descriptor (sm100): start >> 4 [0,14), LBO >> 4
 // [16,30), SBO >> 4 [32,46), version 1 [46,48), base offset 0, layout type
-// SWIZZLE_128B (= 2) [61,64)
+// SWIZZLE_64B (= 4) [61,64)
 __device__ __forceinline__ uint64_t sdesc(uint32_t smem_addr, uint32_t lbo_bytes, uint32_t sbo_bytes) {
   uint64_t d = 0;
   d |= (uint64_t)((smem_addr >> 4) & 0x3fffu);
   d |= (uint64_t)((lbo_bytes >> 4) & 0x3fffu) << 16;
   d |= (uint64_t)((sbo_bytes >> 4) & 0x3fffu) << 32;
   d |= (uint64_t)1u << 46;
-  d |= (uint64_t)2u << 61;
+  d |= (uint64_t)4u << 61;
   return d;
 }
+// K-major operand: rows = M/N at 64 B, 8-row groups 512 B apart; K step of
+// 16 bf16 = +32 B inside the row
+__device__ __forceinline__ uint64_t kdesc(uint32_t smem_addr) { return sdesc(smem_addr, 16, 512); }
+// MN-major operand: rows = K, MN blocks of 32 at lbo; K step of 16 rows = +1024 B
+__device__ __forceinline__ uint64_t mndesc(uint32_t smem_addr, uint32_t lbo) { return sdesc(smem_addr, lbo, 512); }
 
-// instruction descriptor, kind::tf32, fp32 accumulate
-__host__ __device__ constexpr uint32_t idesc_tf32(int M, int N, int a_mn_major, int b_mn_major) {
-  return (1u << 4)                          // D format f32
-         | (2u << 7)                        // A tf32
-         | (2u << 10)                       // B tf32
-         | ((uint32_t)a_mn_major << 15)     // A major
-         | ((uint32_t)b_mn_major << 16)     // B major
-         | ((uint32_t)(N >> 3) << 17)       // N
-         | ((uint32_t)(M >> 4) << 24);      // M
+// instruction descriptor, kind::f16 with bf16 inputs, fp32 accumulate
+__host__ __device__ constexpr uint32_t idesc_bf16(int M, int N, int a_mn_major, int b_mn_major) {
+  return (1u << 4)                       // D format f32
+         | (1u << 7)                     // A bf16
+         | (1u << 10)                    // B bf16
+         | ((uint32_t)a_mn_major << 15)  // A major
+         | ((uint32_t)b_mn_major << 16)  // B major
+         | ((uint32_t)(N >> 3) << 17)    // N
+         | ((uint32_t)(M >> 4) << 24);   // M
 }
 
 // ---- tcgen05 -------------------------------------------------------------------
@@ -77,12 +140,12 @@ __device__ __forceinline__ void fence_after_sync() { asm volatile("tcgen05.fence
 __device__ __forceinline__ void fence_smem_to_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
 // D[tmem] (+)= A[smem] * B[smem]; issued by ONE thread
-__device__ __forceinline__ void mma_tf32(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+__device__ __forceinline__ void mma_bf16(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
                                          uint32_t accumulate) {
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
       "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(d_tmem),
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(d_tmem),
       "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
@@ -100,36 +163,27 @@ __device__ __forceinline__ void mma_commit(uint64_t* bar) {
   "=r"(r[b + 0]), "=r"(r[b + 1]), "=r"(r[b + 2]), "=r"(r[b + 3]), "=r"(r[b + 4]), "=r"(r[b + 5]),          \
       "=r"(r[b + 6]), "=r"(r[b + 7]), "=r"(r[b + 8]), "=r"(r[b + 9]), "=r"(r[b + 10]), "=r"(r[b + 11]),    \
       "=r"(r[b + 12]), "=r"(r[b + 13]), "=r"(r[b + 14]), "=r"(r[b + 15])
+#define VPG_LD16 "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
 
-__device__ __forceinline__ void tmem_ld16_wait(uint32_t taddr, float (&v)[16]) {
-  uint32_t r[16];
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n\t"
-      "tcgen05.wait::ld.sync.aligned;"
-      : VPG_R16(0)
-      : "r"(taddr)
-      : "memory");
-#pragma unroll
-  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
-}
-
-// two 16-column loads, one wait
-__device__ __forceinline__ void tmem_ld2x16_wait(uint32_t ta, uint32_t tb, float (&va)[16], float (&vb)[16]) {
-  uint32_t r[32];
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%32];\n\t"
-      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, "
-      "[%33];\n\t"
-      "tcgen05.wait::ld.sync.aligned;"
-      : VPG_R16(0), VPG_R16(16)
-      : "r"(ta), "r"(tb)
-      : "memory");
+// three 16-column loads, one wait
+__device__ __forceinline__ void tmem_ld3x16_wait(uint32_t ta, uint32_t tb, uint32_t tc_, float (&va)[16],
+                                                 float (&vb)[16], float (&vc)[16]) {
+  uint32_t r[48];
+  asm volatile(VPG_LD16 "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%48];\n\t" VPG_LD16
+                        "{%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%49];\n\t" VPG_LD16
+                        "{%32,%33,%34,%35,%36,%37,%38,%39,%40,%41,%42,%43,%44,%45,%46,%47}, [%50];\n\t"
+                        "tcgen05.wait::ld.sync.aligned;"
+               : VPG_R16(0), VPG_R16(16), VPG_R16(32)
+               : "r"(ta), "r"(tb), "r"(tc_)
+               : "memory");
 #pragma unroll
   for (int i = 0; i < 16; ++i) {
     va[i] = __uint_as_float(r[i]);
     vb[i] = __uint_as_float(r[16 + i]);
+    vc[i] = __uint_as_float(r[32 + i]);
   }
 }
+#undef VPG_LD16
 #undef VPG_R16
 
 }  // namespace tc

@@ -1209,7 +1209,7 @@ int vpinn_gpu_tc_probe(int device, int mode, const float* A, const float* W, con
     dA.alloc(128 * 32);
     dW.alloc(32 * 32);
     dH.alloc(128 * 32);
-    dO.alloc(128 * 32 + 64 * 64);
+    dO.alloc(128 * 32 + 128 * 96);
     CK(cudaMemcpy(dA.p, A, sizeof(float) * 128 * 32, cudaMemcpyHostToDevice));
     CK(cudaMemcpy(dW.p, W, sizeof(float) * 32 * 32, cudaMemcpyHostToDevice));
     if (H) CK(cudaMemcpy(dH.p, H, sizeof(float) * 128 * 32, cudaMemcpyHostToDevice));
@@ -1217,7 +1217,7 @@ int vpinn_gpu_tc_probe(int device, int mode, const float* A, const float* W, con
     vpg::tc_probe_kernel<<<1, 128, vpg::kTcProbeSmem>>>(mode, dA.p, dW.p, dH.p, dO.p);
     CK(cudaGetLastError());
     CK(cudaDeviceSynchronize());
-    CK(cudaMemcpy(out, dO.p, sizeof(float) * (mode == 2 ? 32 * 32 : 128 * 32), cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(out, dO.p, sizeof(float) * (128 * 32 + 128 * 96), cudaMemcpyDeviceToHost));
   });
 }
 
