@@ -63,9 +63,10 @@ struct TcLayout {
   static constexpr int S_ROWS = S_CELL + 256;           // [3][128] rbar | rsq | rge
   static constexpr int S_RED = S_ROWS + 3 * 128;        // 64 doubles (128 floats)
   static constexpr int S_BAR = S_RED + 128;             // mbarriers + TMEM slot (16 floats)
-  static constexpr int S_END = S_BAR + 16;
+  static constexpr int S_END = S_BAR + 16;               // then the dedicated slab, if any
   static constexpr size_t BYTES = (size_t)OFF_SMALL + sizeof(float) * S_END + 1024;  // + alignment slack
   static_assert(S_END * 4 >= kTcPart, "small region must cover one operand tile");
+  static_assert(S_END % 4 == 0, "dedicated slab must be 16-byte aligned");
   static_assert(OFF_A % 1024 == 0, "operand buffers must be 1024-byte aligned");
 };
 
@@ -272,6 +273,15 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_step_kernel(const StepArgs a
     for (int k = 0; k < 16; ++k) v[k] = (x0[k] + x1[k]) + x2[k];
   };
 
+  // dedicated slab region after the small region (a.union_floats floats), or
+  // none (0): the slab then aliases a free operand buffer
+  const bool dedicated = a.union_floats > 0;
+  char* dslab = reinterpret_cast<char*>(sf + LY::S_END);
+  if (dedicated && tid == 0 && (int)blockIdx.x < a.n_int_tiles) {
+    const int c0 = blockIdx.x * a.cells_per_tile;
+    issue_chunk(a, c0, 0, min(a.cells_per_tile, a.E - c0) * a.T, reinterpret_cast<float*>(dslab), tma_bar);
+  }
+
   bool first_grad = true;
   double acc_v = 0.0, acc_b = 0.0, acc_s = 0.0, acc_eg = 0.0;  // thread 0
   int bad = 0;
@@ -313,12 +323,11 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_step_kernel(const StepArgs a
     operands_ready();
     if (tid == 0) issue_point_gemm(sA, 1, false);
     commit_and_wait();
-    // the slab buffer is free now (D == 3: layer-1 input consumed; D == 2: unused)
-    char* slab = (D == 3) ? bufA : bufB;
-    if (interior && tid == 0) {
-      fence_proxy_async();
+    // aliased slab: its operand buffer is free now (D == 3: layer-1 input
+    // consumed; D == 2: unused); a dedicated slab was prefetched already
+    char* slab = dedicated ? dslab : ((D == 3) ? bufA : bufB);
+    if (!dedicated && interior && tid == 0)
       issue_chunk(a, cell0, 0, nrows_tile, reinterpret_cast<float*>(slab), tma_bar);
-    }
     float lz[16], lt[16], lu[16];  // last hidden layer (units u0..u0+15)
     {
       float av[16], at[16], au[16];
@@ -529,13 +538,21 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_step_kernel(const StepArgs a
       }
     }
     __syncthreads();  // adjoint rows visible; slab reads done
+    if (dedicated && tid == 0) {
+      // prefetch the next tile's slab: it lands during this reverse and the next forward
+      const int nt = tile + gridDim.x;
+      if (nt < a.n_int_tiles) {
+        const int c0 = nt * a.cells_per_tile;
+        issue_chunk(a, c0, 0, min(a.cells_per_tile, a.E - c0) * a.T, reinterpret_cast<float*>(dslab), tma_bar);
+      }
+    }
     ub = sEx[kTxUb * 128 + p];
     uxb = sEx[kTxUxb * 128 + p];
     uyb = sEx[kTxUyb * 128 + p];
 
     // =================== reverse ===================
     // ---- output layer: Wbar_out, bbar_out (column H: lz == 1) and G of the last hidden layer ----
-    char* gbuf = slab;  // free buffer
+    char* gbuf = (D == 3) ? bufA : bufB;  // free buffer
     {
       float* vrow = reinterpret_cast<float*>(gbuf);  // [128][33] scratch (before G is written)
 #pragma unroll

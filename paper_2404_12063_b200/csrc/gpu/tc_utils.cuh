@@ -2,7 +2,8 @@
 //
 // fp32-faithful products on the bf16 tensor cores: every operand x is split
 // into three bf16 parts x = h + m + l (h = bf16(x), m = bf16(x - h),
-// l = bf16(x - h - m); 24 significant bits in total) and a product is the
+// l = bf16(x - h - m), rounded with integer ops; 24+ significant bits in
+// total) and a product is the
 // sum of the six terms hh + hm + mh + mm + hl + lh (the dropped ml, lm, ll
 // terms are below 2^-26 relative), accumulated in fp32 in TMEM.  Six bf16
 // MMAs cost the same tensor time as three TF32 ones.
@@ -38,28 +39,34 @@ struct Split8 {
   uint4 h, m, l;
 };
 
-__device__ __forceinline__ uint32_t pack2(__nv_bfloat16 a, __nv_bfloat16 b) {
-  return (uint32_t)__bfloat16_as_ushort(a) | ((uint32_t)__bfloat16_as_ushort(b) << 16);
+// x rounded to 8 significant bits (round half away from zero on the
+// magnitude), as a float whose low 16 bits are zero, i.e. a bf16 value.
+// Integer ops only: the F2F conversion path is a quarter-rate pipe.
+__device__ __forceinline__ float bf16_hi(float x) { return __uint_as_float((__float_as_uint(x) + 0x8000u) & 0xffff0000u); }
+
+// two bf16-valued floats -> packed bf16x2 (a in the low half)
+__device__ __forceinline__ uint32_t pack2f(float a, float b) {
+  return __byte_perm(__float_as_uint(a), __float_as_uint(b), 0x7632);
 }
 
-// three-way bf16 split of 8 consecutive values
+// three-way bf16 split of 8 consecutive values: x = h + m + l up to
+// 2^-27 |x| (each remainder is exact in fp32)
 __device__ __forceinline__ Split8 split8(const float* v) {
   uint32_t h[4], m[4], l[4];
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
-    __nv_bfloat16 hb[2], mb[2], lb[2];
+    float hf[2], mf[2], lf[2];
 #pragma unroll
     for (int e = 0; e < 2; ++e) {
       const float x = v[2 * k + e];
-      hb[e] = __float2bfloat16_rn(x);
-      const float r1 = x - __bfloat162float(hb[e]);
-      mb[e] = __float2bfloat16_rn(r1);
-      const float r2 = r1 - __bfloat162float(mb[e]);
-      lb[e] = __float2bfloat16_rn(r2);
+      hf[e] = bf16_hi(x);
+      const float r1 = x - hf[e];
+      mf[e] = bf16_hi(r1);
+      lf[e] = bf16_hi(r1 - mf[e]);
     }
-    h[k] = pack2(hb[0], hb[1]);
-    m[k] = pack2(mb[0], mb[1]);
-    l[k] = pack2(lb[0], lb[1]);
+    h[k] = pack2f(hf[0], hf[1]);
+    m[k] = pack2f(mf[0], mf[1]);
+    l[k] = pack2f(lf[0], lf[1]);
   }
   return {make_uint4(h[0], h[1], h[2], h[3]), make_uint4(m[0], m[1], m[2], m[3]), make_uint4(l[0], l[1], l[2], l[3])};
 }

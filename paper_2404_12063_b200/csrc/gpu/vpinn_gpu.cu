@@ -246,8 +246,13 @@ void configure(vpinn_gpu_ctx* c) {
       a.chunk_rows = tile_rows;
       a.tstride = round4(tile_rows * c->Q + 8);
       a.stage_floats = c->nt * a.tstride;
-      a.union_floats = 0;
-      c->smem_step = V.tc_smem;
+      // a dedicated slab region when it fits next to the operand buffers
+      // (prefetched one tile ahead), else the slab aliases a free buffer
+      const size_t slab_bytes = sizeof(float) * (size_t)a.stage_floats;
+      const size_t tc_limit = (size_t)227 * 1024 - 1024;  // - static shared
+      a.union_floats = (V.tc_smem + slab_bytes <= tc_limit) ? a.stage_floats : 0;
+      if (const char* e = std::getenv("VPINN_TC_SLAB")) if (std::atoi(e) == 0) a.union_floats = 0;
+      c->smem_step = V.tc_smem + sizeof(float) * (size_t)a.union_floats;
       CK(cudaFuncSetAttribute(V.tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem_step));
       CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, V.tc, vpg::kTcThreads, c->smem_step));
       if (occ < 1) throw Fail{VPINN_ERR_DEVICE, "tensor-core step kernel cannot be resident"};

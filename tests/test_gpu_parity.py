@@ -174,3 +174,21 @@ def test_tcgen05_3xtf32_probe(mode):
     got = out[:ref.size].reshape(ref.shape)
     err = np.abs(got - ref).max() / np.abs(ref).max()
     assert err < 2e-6, err
+
+
+@pytest.mark.parametrize("name", ["c1_poisson", "gear576_cd2d", "inverse_scalar_eps"])
+@pytest.mark.parametrize("mode", ["ffma", "tc_aliased_slab"])
+def test_alternate_step_kernels_match_oracle(name, mode, monkeypatch):
+    """The CUDA-core (FFMA) fused kernel and the tensor-core kernel with its
+    slab aliased into an operand buffer are selectable by environment; both
+    must meet the same parity bar as the default path."""
+    if mode == "ffma":
+        monkeypatch.setenv("VPINN_TC", "0")
+    else:
+        monkeypatch.setenv("VPINN_TC_SLAB", "0")
+    spec = CASES[name]()
+    ob, g, p0 = make_pair(spec)
+    parts_o, _ = ob.loss_and_grad(p0)
+    parts_g, grad_g = g.loss_and_grad()
+    assert rel(parts_g[0], parts_o[0]) < 1e-5, (parts_g, parts_o)
+    grad_close(grad_g, spec, p0)
