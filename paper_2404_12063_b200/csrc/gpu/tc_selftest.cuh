@@ -17,7 +17,7 @@ __global__ void __launch_bounds__(128, 1) tc_probe_kernel(int mode, const float*
                                                           const float* __restrict__ W,
                                                           const float* __restrict__ H, float* __restrict__ out) {
   extern __shared__ __align__(1024) char tp_raw[];
-  char* base = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(tp_raw) + 1023) & ~uintptr_t(1023));
+  char* base = tp_raw + ((1024u - (smem_u32(tp_raw) & 1023u)) & 1023u);
   char* a_t = base;                   // 3 part tiles of [128][32]
   char* h_t = base + 24576;           // 3 part tiles
   char* w_t = base + 2 * 24576;       // [96][32]: W h | m | l rows

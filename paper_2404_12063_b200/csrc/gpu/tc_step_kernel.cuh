@@ -110,7 +110,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_step_kernel(const StepArgs a
   if (a.stop_flag != nullptr && *a.stop_flag != 0) return;
 
   extern __shared__ __align__(1024) char tc_raw[];
-  char* sm = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(tc_raw) + 1023) & ~uintptr_t(1023));
+  // 1024-byte alignment by an offset on the __shared__ array itself (a cast
+  // through uintptr_t would lose the address space: generic LD/ST)
+  char* sm = tc_raw + ((1024u - (smem_u32(tc_raw) & 1023u)) & 1023u);
   char* sWB = sm + LY::OFF_W;
   char* bufA = sm + LY::OFF_A;
   char* bufB = sm + LY::OFF_B;

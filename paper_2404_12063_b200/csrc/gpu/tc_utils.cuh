@@ -5,7 +5,7 @@
 // l = bf16(x - h - m), rounded with integer ops; 24+ significant bits in
 // total) and a product is the
 // sum of the six terms hh + hm + mh + mm + hl + lh (the dropped ml, lm, ll
-// terms are below 2^-26 relative), accumulated in fp32 in TMEM.  Six bf16
+// terms are below 2^-23 relative), accumulated in fp32 in TMEM.  Six bf16
 // MMAs cost the same tensor time as three TF32 ones.
 //
 // Operand tiles live in shared memory as R rows of 32 bf16 (64 B per row)
@@ -49,8 +49,11 @@ __device__ __forceinline__ uint32_t pack2f(float a, float b) {
   return __byte_perm(__float_as_uint(a), __float_as_uint(b), 0x7632);
 }
 
-// three-way bf16 split of 8 consecutive values: x = h + m + l up to
-// 2^-27 |x| (each remainder is exact in fp32)
+// three-way bf16 split of 8 consecutive values, exact: h = x rounded to 8
+// bits, r = x - h (exact, <= 16 significant bits), m = r truncated to 8 bits,
+// l = r - m (exact and already 8 bits).  |m| <= 2^-8 |x|, |l| <= 2^-16 |x|,
+// so the dropped ml + lm + ll terms are below 2^-23 relative.  Integer and
+// FADD ops only (5 per value).
 __device__ __forceinline__ Split8 split8(const float* v) {
   uint32_t h[4], m[4], l[4];
 #pragma unroll
@@ -60,9 +63,9 @@ __device__ __forceinline__ Split8 split8(const float* v) {
     for (int e = 0; e < 2; ++e) {
       const float x = v[2 * k + e];
       hf[e] = bf16_hi(x);
-      const float r1 = x - hf[e];
-      mf[e] = bf16_hi(r1);
-      lf[e] = bf16_hi(r1 - mf[e]);
+      const float r = x - hf[e];
+      mf[e] = __uint_as_float(__float_as_uint(r) & 0xffff0000u);
+      lf[e] = r - mf[e];
     }
     h[k] = pack2f(hf[0], hf[1]);
     m[k] = pack2f(mf[0], mf[1]);

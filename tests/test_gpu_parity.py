@@ -135,8 +135,11 @@ def test_training_trajectory_matches_oracle_c1():
 def test_training_trajectory_matches_oracle_gear_inverse_stop():
     spec = CASES["inverse_scalar_eps"]()
     ob, g, p0 = make_pair(spec)
-    ref = ob.train(p0, 60, lr0=1e-3, eps_abs_tol=1.695, eps_actual=0.3)
-    rep = g.train(60, lr0=1e-3, eps_abs_tol=1.695, eps_actual=0.3)
+    # the trainable eps moves ~lr per Adam step from 2.0: a tolerance whose
+    # crossing lies half a step away from any iterate (not on the knife edge
+    # eps == 1.995) makes the stop step well defined under fp32 noise
+    ref = ob.train(p0, 60, lr0=1e-3, eps_abs_tol=1.6955, eps_actual=0.3)
+    rep = g.train(60, lr0=1e-3, eps_abs_tol=1.6955, eps_actual=0.3)
     assert rep.steps_run == ref["steps_run"]
     assert rep.stop_reason == ref["stop_reason"]
     r = np.abs(rep.records["total"] - ref["every_step"][:, 0]) / np.abs(ref["every_step"][:, 0])
