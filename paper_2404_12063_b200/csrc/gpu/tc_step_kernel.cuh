@@ -62,7 +62,7 @@ struct TcLayout {
   static constexpr int S_CELL = S_GACC + 128;           // [256] per-cell sums
   static constexpr int S_ROWS = S_CELL + 256;           // [3][128] rbar | rsq | rge
   static constexpr int S_RED = S_ROWS + 3 * 128;        // 64 doubles (128 floats)
-  static constexpr int S_BAR = S_RED + 128;             // mbarriers + TMEM slot (16 floats)
+  static constexpr int S_BAR = S_RED + 128;             // 4 mbarriers + TMEM slot (16 floats)
   static constexpr int S_END = S_BAR + 16;               // then the dedicated slab, if any
   static constexpr size_t BYTES = (size_t)OFF_SMALL + sizeof(float) * S_END + 1024;  // + alignment slack
   static_assert(S_END * 4 >= kTcPart, "small region must cover one operand tile");
@@ -126,9 +126,13 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_step_kernel(const StepArgs a
   float* sCell = sf + LY::S_CELL;
   float* sRows = sf + LY::S_ROWS;
   double* sRed = reinterpret_cast<double*>(sf + LY::S_RED);
-  uint64_t* mma_bar = reinterpret_cast<uint64_t*>(sf + LY::S_BAR);
-  uint64_t* tma_bar = mma_bar + 1;
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(mma_bar + 2);
+  // MMA-completion barriers: value stream (bar_v), tangent streams (bar_t),
+  // parameter-gradient GEMM (bar_w); slab TMA (tma_bar)
+  uint64_t* bar_v = reinterpret_cast<uint64_t*>(sf + LY::S_BAR);
+  uint64_t* bar_t = bar_v + 1;
+  uint64_t* bar_w = bar_v + 2;
+  uint64_t* tma_bar = bar_v + 3;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bar_v + 4);
 
   const int tid = threadIdx.x, warp = tid >> 5;
   const int p = tid & 127;          // point of this thread == TMEM lane
@@ -140,7 +144,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_step_kernel(const StepArgs a
   // ---- one-time setup: TMEM, barriers, weights ----
   if (warp == 0) tc::tmem_alloc(tslot, kTcCols);
   if (tid == 0) {
-    mbar_init(mma_bar, 1);
+    mbar_init(bar_v, 1);
+    mbar_init(bar_t, 1);
+    mbar_init(bar_w, 1);
     mbar_init(tma_bar, 1);
     fence_mbar_init();
   }
@@ -187,6 +193,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_step_kernel(const StepArgs a
   const uint32_t sA = smem_u32(bufA), sB = smem_u32(bufB), sW = smem_u32(sWB);
   // forward (propagate == false) or propagation of layer l; A parts (K-major)
   // from buffer abuf: D_s[0:96) = h.[Wh|Wm|Wl], D_s[0:64) += m.[Wh|Wm], D_s[0:32) += l.Wh
+  // commits: bar_v after the value stream, bar_t after the tangent streams
+  // (a commit tracks every earlier MMA of the thread, so the propagation is
+  // issued before the parameter-gradient GEMM)
   auto issue_point_gemm = [&](uint32_t abuf, int l, bool propagate) {
     const uint32_t wbase = sW + (uint32_t)(l - 1) * kTcW;
 #pragma unroll 1
@@ -202,7 +211,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_step_kernel(const StepArgs a
           tc::mma_bf16(d, tc::kdesc(abase + 32 * ks), bd, idesc, (part > 0 || ks > 0) ? 1u : 0u);
         }
       }
+      if (s == 0) tc::mma_commit(bar_v);
     }
+    tc::mma_commit(bar_t);
   };
   // parameter gradient of layer l: G parts in gbuf (M = h|m|l|-), X parts in xbuf (N = h|m|l)
   auto issue_param_gemm = [&](uint32_t gbuf, uint32_t xbuf, int l, bool first) {
@@ -216,12 +227,12 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_step_kernel(const StepArgs a
         tc::mma_bf16(acc, tc::mndesc(g + 1024 * kp, kTcPart), tc::mndesc(x + 1024 * kp, kTcPart), idesc,
                      (first && s == 0 && kp == 0) ? 0u : 1u);
     }
+    tc::mma_commit(bar_w);
   };
-  uint32_t mma_phase = 0, tma_phase = 0;
-  auto commit_and_wait = [&]() {
-    if (tid == 0) tc::mma_commit(mma_bar);
-    mbar_wait(mma_bar, mma_phase);
-    mma_phase ^= 1u;
+  uint32_t ph_v = 0, ph_t = 0, ph_w = 0, tma_phase = 0;
+  auto wait_bar = [&](uint64_t* bar, uint32_t& ph) {
+    mbar_wait(bar, ph);
+    ph ^= 1u;
     tc::fence_after_sync();
   };
   // all threads: make smem operand writes and TMEM reads ordered before the
@@ -324,60 +335,42 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_step_kernel(const StepArgs a
     }
     operands_ready();
     if (tid == 0) issue_point_gemm(sA, 1, false);
-    commit_and_wait();
-    // aliased slab: its operand buffer is free now (D == 3: layer-1 input
-    // consumed; D == 2: unused); a dedicated slab was prefetched already
-    char* slab = dedicated ? dslab : ((D == 3) ? bufA : bufB);
-    if (!dedicated && interior && tid == 0)
-      issue_chunk(a, cell0, 0, nrows_tile, reinterpret_cast<float*>(slab), tma_bar);
-    float lz[16], lt[16], lu[16];  // last hidden layer (units u0..u0+15)
-    {
-      float av[16], at[16], au[16];
+    // epilogue of hidden layer l (bias index bofs): the activation of the value
+    // stream overlaps the tangent-stream MMAs
+    auto hidden_epilogue = [&](int bofs, float (&oz)[16], float (&ot)[16], float (&ou)[16]) {
+      float av[16];
+      wait_bar(bar_v, ph_v);
       acc_stream(0, av);
-      acc_stream(1, at);
-      acc_stream(2, au);
-      const float* bias = sBias;
+      const float* bias = sBias + bofs;
+      float s1v[16];
 #pragma unroll
       for (int k = 0; k < 16; ++k) {
         const int u = u0 + k;
-        if (u < H) {
-          const float zz = AC::value(av[k] + bias[u]);
-          const float s1 = AC::s1(zz);
-          lz[k] = zz;
-          lt[k] = s1 * at[k];
-          lu[k] = s1 * au[k];
-        } else {
-          lz[k] = (u == H) ? 1.0f : 0.0f;
-          lt[k] = 0.f;
-          lu[k] = 0.f;
-        }
+        const float zz = (u < H) ? AC::value(av[k] + bias[u]) : ((u == H) ? 1.0f : 0.0f);
+        oz[k] = zz;
+        s1v[k] = (u < H) ? AC::s1(zz) : 0.f;
       }
-    }
+      wait_bar(bar_t, ph_t);
+      acc_stream(1, ot);
+      acc_stream(2, ou);
+#pragma unroll
+      for (int k = 0; k < 16; ++k) {
+        ot[k] = s1v[k] * ot[k];
+        ou[k] = s1v[k] * ou[k];
+      }
+    };
+    // aliased slab: its operand buffer is free once layer 1 is done (D == 3:
+    // layer-1 input consumed; D == 2: unused); a dedicated slab was prefetched
+    char* slab = dedicated ? dslab : ((D == 3) ? bufA : bufB);
+    float lz[16], lt[16], lu[16];  // last hidden layer (units u0..u0+15)
+    hidden_epilogue(0, lz, lt, lu);
+    if (!dedicated && interior && tid == 0)
+      issue_chunk(a, cell0, 0, nrows_tile, reinterpret_cast<float*>(slab), tma_bar);
     if constexpr (D == 3) {
       store3(bufB, lz, lt, lu);
       operands_ready();
       if (tid == 0) issue_point_gemm(sB, 2, false);
-      commit_and_wait();
-      float av[16], at[16], au[16];
-      acc_stream(0, av);
-      acc_stream(1, at);
-      acc_stream(2, au);
-      const float* bias = sBias + 32;
-#pragma unroll
-      for (int k = 0; k < 16; ++k) {
-        const int u = u0 + k;
-        if (u < H) {
-          const float zz = AC::value(av[k] + bias[u]);
-          const float s1 = AC::s1(zz);
-          lz[k] = zz;
-          lt[k] = s1 * at[k];
-          lu[k] = s1 * au[k];
-        } else {
-          lz[k] = (u == H) ? 1.0f : 0.0f;
-          lt[k] = 0.f;
-          lu[k] = 0.f;
-        }
-      }
+      hidden_epilogue(32, lz, lt, lu);
     }
     // output layer (linear) over this thread's units, halves combined in order
     {
@@ -580,75 +573,71 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_step_kernel(const StepArgs a
     }
     operands_ready();
     // ---- hidden->hidden layers, last first ----
-    {
-      // layer NL: G in gbuf, its input X in the other buffer
-      char* xbuf = (gbuf == bufA) ? bufB : bufA;
-      if (tid == 0) {
-        issue_param_gemm(smem_u32(gbuf), smem_u32(xbuf), NL, first_grad);
-        issue_point_gemm(smem_u32(gbuf), NL, true);
+    // propagation first (bar_v / bar_t), then the parameter-gradient GEMM
+    // (bar_w); elementwise work that does not need them runs in their shadow
+    char* xbuf = (gbuf == bufA) ? bufB : bufA;  // input of layer NL
+    if (tid == 0) {
+      issue_point_gemm(smem_u32(gbuf), NL, true);
+      issue_param_gemm(smem_u32(gbuf), smem_u32(xbuf), NL, first_grad);
+    }
+    float z1[16], t1x[16], t1y[16];  // hidden-1 state, recomputed once per tile
+    // G of hidden h from the propagated adjoints (TMEM) and the state (z, tx, ty)
+    auto hidden_adjoint = [&](const float (&z)[16], const float (&tx)[16], const float (&ty)[16], float (&gA)[16],
+                              float (&gX)[16], float (&gY)[16]) {
+      float xa[16], xx[16], xy[16];
+      wait_bar(bar_v, ph_v);
+      acc_stream(0, xa);
+      wait_bar(bar_t, ph_t);
+      acc_stream(1, xx);
+      acc_stream(2, xy);
+#pragma unroll
+      for (int k = 0; k < 16; ++k) {
+        if (u0 + k < H) {
+          const float s1 = AC::s1(z[k]), kp = AC::kap(z[k]);
+          gA[k] = fmaf(s1, xa[k], kp * fmaf(tx[k], xx[k], ty[k] * xy[k]));
+          gX[k] = s1 * xx[k];
+          gY[k] = s1 * xy[k];
+        } else {
+          gA[k] = gX[k] = gY[k] = 0.f;
+        }
       }
-      commit_and_wait();
-      if constexpr (D == 3) {
-        // G of hidden 2 from the propagated adjoints and hidden-2 state (xbuf)
-        float xa[16], xx[16], xy[16];
-        acc_stream(0, xa);
-        acc_stream(1, xx);
-        acc_stream(2, xy);
+    };
+    if constexpr (D == 3) {
+      float gA[16], gX[16], gY[16];
+      {
         float z[16], tx[16], ty[16];
-        load1(xbuf, 0, z);
+        load1(xbuf, 0, z);  // hidden-2 state (read-only for the MMAs too)
         load1(xbuf, 1, tx);
         load1(xbuf, 2, ty);
-        float gA[16], gX[16], gY[16];
-#pragma unroll
-        for (int k = 0; k < 16; ++k) {
-          if (u0 + k < H) {
-            const float s1 = AC::s1(z[k]), kp = AC::kap(z[k]);
-            gA[k] = fmaf(s1, xa[k], kp * fmaf(tx[k], xx[k], ty[k] * xy[k]));
-            gX[k] = s1 * xx[k];
-            gY[k] = s1 * xy[k];
-          } else {
-            gA[k] = gX[k] = gY[k] = 0.f;
-          }
-        }
-        __syncthreads();  // every thread has read hidden-2 state from xbuf
-        store3(gbuf, gA, gX, gY);
-        {
-          float z1[16], t1x[16], t1y[16];
-          layer0(px, py, z1, t1x, t1y);
-          store3(xbuf, z1, t1x, t1y);  // layer-1 input (recomputed)
-        }
-        operands_ready();
-        if (tid == 0) {
-          issue_param_gemm(smem_u32(gbuf), smem_u32(xbuf), 1, first_grad);
-          issue_point_gemm(smem_u32(gbuf), 1, true);
-        }
-        commit_and_wait();
+        layer0(px, py, z1, t1x, t1y);
+        hidden_adjoint(z, tx, ty, gA, gX, gY);
       }
+      wait_bar(bar_w, ph_w);  // both operand buffers free
+      __syncthreads();        // every thread has read hidden-2 state from xbuf
+      store3(gbuf, gA, gX, gY);
+      store3(xbuf, z1, t1x, t1y);  // layer-1 input (recomputed)
+      operands_ready();
+      if (tid == 0) {
+        issue_point_gemm(smem_u32(gbuf), 1, true);
+        issue_param_gemm(smem_u32(gbuf), smem_u32(xbuf), 1, first_grad);
+      }
+    } else {
+      layer0(px, py, z1, t1x, t1y);
     }
     first_grad = false;
     // ---- input layer: G of hidden 1 -> Wbar_0, bbar_0 ----
     {
-      float xa[16], xx[16], xy[16];
-      acc_stream(0, xa);
-      acc_stream(1, xx);
-      acc_stream(2, xy);
-      float z1[16], t1x[16], t1y[16];
-      layer0(px, py, z1, t1x, t1y);
-      float* vrow = reinterpret_cast<float*>(bufA);  // [128][97] scratch (both buffers are free now)
+      float ga[16], gx[16], gy[16];
+      hidden_adjoint(z1, t1x, t1y, ga, gx, gy);
+      wait_bar(bar_w, ph_w);  // the parameter-gradient GEMM has read bufA / bufB
+      float* vrow = reinterpret_cast<float*>(bufA);  // [128][97] scratch
 #pragma unroll
       for (int k = 0; k < 16; ++k) {
         const int u = u0 + k;
-        float ga = 0.f, gx = 0.f, gy = 0.f;
-        if (u < H) {
-          const float s1 = AC::s1(z1[k]), kp = AC::kap(z1[k]);
-          ga = fmaf(s1, xa[k], kp * fmaf(t1x[k], xx[k], t1y[k] * xy[k]));
-          gx = s1 * xx[k];
-          gy = s1 * xy[k];
-        }
         // Wbar_0 += Abar x^T + TAxbar e_x^T + TAybar e_y^T ; bbar_0 += Abar
-        vrow[p * 97 + u] = fmaf(ga, px, gx);
-        vrow[p * 97 + 32 + u] = fmaf(ga, py, gy);
-        vrow[p * 97 + 64 + u] = ga;
+        vrow[p * 97 + u] = fmaf(ga[k], px, gx[k]);
+        vrow[p * 97 + 32 + u] = fmaf(ga[k], py, gy[k]);
+        vrow[p * 97 + 64 + u] = ga[k];
       }
       tc::fence_before_sync();
       __syncthreads();
