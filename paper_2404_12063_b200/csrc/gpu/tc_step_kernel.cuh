@@ -18,8 +18,9 @@
 // value stream carries a constant-one column at index H, which turns the
 // parameter-gradient GEMM's column H into the bias gradient.
 //
-// CTA = 256 threads; thread t owns point p = t % 128 (= its TMEM lane) and
-// hidden units [16*(t/128), +16).  One CTA per SM (TMEM 512 columns,
+// CTA = 128*NQ threads; thread t owns point p = t % 128 (= its TMEM lane)
+// and hidden units [UPT*(t/128), +UPT), UPT = 32/NQ (NQ = 4: 16 warps, the
+// elementwise phases are latency-bound and need the warps).  One CTA per SM (TMEM 512 columns,
 // ~170 KB shared memory).  Hidden layers D in {2, 3}, H <= 31, one output.
 // Every phase is separated by a CTA barrier or an MMA-completion mbarrier;
 // one elected thread issues all MMAs.
@@ -30,7 +31,6 @@
 
 namespace vpg {
 
-constexpr int kTcThreads = 256;
 constexpr int kTcPart = 8192;               // one [128][32] bf16 operand tile
 constexpr int kTcStream = 3 * kTcPart;      // h | m | l parts of one stream
 constexpr int kTcBuf = 3 * kTcStream;       // 3 streams
@@ -40,8 +40,8 @@ constexpr int kTcDCols = 96;                // accumulator columns per stream (h
 constexpr int kTcAccCol = 3 * kTcDCols;     // parameter-gradient accumulators start here
 
 // exchange rows of the tensor-core kernel ([row][128] floats)
-enum : int { kTxX = 0, kTxY, kTxU, kTxUx, kTxUy, kTxSx, kTxSy, kTxCv, kTxUb, kTxUxb, kTxUyb, kTxPu, kTxPx, kTxPy,
-             kTxRows };
+// (kTxP0.. : output-layer partials of unit groups 1..3, 3 rows each)
+enum : int { kTxX = 0, kTxY, kTxU, kTxUx, kTxUy, kTxSx, kTxSy, kTxCv, kTxUb, kTxUxb, kTxUyb, kTxP0, kTxRows = kTxP0 + 9 };
 
 template <int D>
 struct TcLayout {
@@ -73,6 +73,8 @@ struct TcLayout {
 // small-gradient accumulator slots (S_GACC)
 enum : int { kGaW0x = 0, kGaW0y = 32, kGaB0 = 64, kGaWd = 96 };  // kGaWd: 32 slots (H weights + bias at H)
 
+constexpr int kTcNQ = 4;  // unit groups per point in the instantiated kernels
+
 template <int H, int D>
 __host__ __device__ constexpr size_t tc_step_smem_bytes() {
   return TcLayout<D>::BYTES;
@@ -80,10 +82,11 @@ __host__ __device__ constexpr size_t tc_step_smem_bytes() {
 
 // column sums over the tile's 128 points of up to 96 per-point values
 // (src row p at src + p * ld), added in a fixed order to acc[0..ncols);
-// 256 threads: 8 point groups of 16, then the 8 partials in order.
-static __device__ __forceinline__ void tc_colsum(const float* src, int ld, int ncols, float* part, float* acc) {
+// 8 point groups of 16, then the 8 partials in order.
+template <int NT>
+__device__ __forceinline__ void tc_colsum(const float* src, int ld, int ncols, float* part, float* acc) {
   const int tid = threadIdx.x;
-  for (int e = tid; e < 8 * ncols; e += kTcThreads) {
+  for (int e = tid; e < 8 * ncols; e += NT) {
     const int g = e / ncols, c = e - g * ncols;
     float s = 0.f;
 #pragma unroll 4
@@ -91,7 +94,7 @@ static __device__ __forceinline__ void tc_colsum(const float* src, int ld, int n
     part[g * 96 + c] = s;
   }
   __syncthreads();
-  for (int c = tid; c < ncols; c += kTcThreads) {
+  for (int c = tid; c < ncols; c += NT) {
     float s = part[c];
 #pragma unroll
     for (int g = 1; g < 8; ++g) s += part[g * 96 + c];
@@ -100,9 +103,12 @@ static __device__ __forceinline__ void tc_colsum(const float* src, int ld, int n
   __syncthreads();
 }
 
-template <int H, int D, int ACT>
-__global__ void __launch_bounds__(kTcThreads, 1) tc_step_kernel(const StepArgs a) {
+template <int H, int D, int ACT, int NQ>
+__global__ void __launch_bounds__(128 * NQ, 1) tc_step_kernel(const StepArgs a) {
   static_assert(H <= 31 && (D == 2 || D == 3), "tensor-core step: H <= 31, 2 or 3 hidden layers");
+  static_assert(NQ == 2 || NQ == 4, "unit groups per point");
+  constexpr int UPT = 32 / NQ;  // hidden units per thread
+  constexpr int NT = 128 * NQ;  // threads
   using LY = TcLayout<D>;
   constexpr int NL = LY::NL;
   using AC = Act<ACT>;
@@ -136,8 +142,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_step_kernel(const StepArgs a
 
   const int tid = threadIdx.x, warp = tid >> 5;
   const int p = tid & 127;          // point of this thread == TMEM lane
-  const int hh = tid >> 7;          // unit half
-  const int u0 = 16 * hh;           // first hidden unit of this thread
+  const int hh = tid >> 7;          // unit group
+  const int u0 = UPT * hh;          // first hidden unit of this thread
   const NetDesc& net = a.net;
   const float* P = a.params;
 
@@ -150,7 +156,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_step_kernel(const StepArgs a
     mbar_init(tma_bar, 1);
     fence_mbar_init();
   }
-  for (int i = tid; i < 32; i += kTcThreads) {
+  for (int i = tid; i < 32; i += NT) {
     float w0 = 0.f, w1 = 0.f, b = 0.f, wd = 0.f;
     if (i < H) {
       w0 = P[net.w_off[0] + 2 * i];
@@ -168,7 +174,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_step_kernel(const StepArgs a
   for (int l = 1; l <= NL; ++l) {
     char* wb = sWB + (l - 1) * kTcW;
     // row o, 8 columns per item; parts h | m | l at rows 0 | 32 | 64
-    for (int e = tid; e < 32 * 4; e += kTcThreads) {
+    for (int e = tid; e < 32 * 4; e += NT) {
       const int o = e >> 2, c = e & 3;
       float v[8];
 #pragma unroll
@@ -178,10 +184,10 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_step_kernel(const StepArgs a
       }
       tc::st_split8(wb, 32 * tc::kRowBytes, o, c, v);
     }
-    for (int o = tid; o < 32; o += kTcThreads) sBias[(l - 1) * 32 + o] = o < H ? P[net.b_off[l] + o] : 0.f;
+    for (int o = tid; o < 32; o += NT) sBias[(l - 1) * 32 + o] = o < H ? P[net.b_off[l] + o] : 0.f;
   }
-  for (int e = tid; e < 128; e += kTcThreads) sGacc[e] = 0.f;
-  for (int e = tid; e < 256; e += kTcThreads) sCell[e] = 0.f;
+  for (int e = tid; e < 128; e += NT) sGacc[e] = 0.f;
+  for (int e = tid; e < 256; e += NT) sCell[e] = 0.f;
   tc::fence_smem_to_async();
   tc::fence_before_sync();
   __syncthreads();
@@ -245,9 +251,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_step_kernel(const StepArgs a
   };
 
   // layer 0 of this thread's units for point (px, py): z, TX_x, TX_y
-  auto layer0 = [&](float px, float py, float (&z)[16], float (&tx)[16], float (&ty)[16]) {
+  auto layer0 = [&](float px, float py, float (&z)[UPT], float (&tx)[UPT], float (&ty)[UPT]) {
 #pragma unroll
-    for (int k = 0; k < 16; ++k) {
+    for (int k = 0; k < UPT; ++k) {
       const int u = u0 + k;
       const float4 w = *reinterpret_cast<const float4*>(sW0 + 4 * u);
       if (u < H) {
@@ -264,26 +270,26 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_step_kernel(const StepArgs a
     }
   };
   // the three streams of this thread's row, split into bf16 parts
-  auto store3 = [&](char* buf, const float (&z)[16], const float (&tx)[16], const float (&ty)[16]) {
+  auto store3 = [&](char* buf, const float (&z)[UPT], const float (&tx)[UPT], const float (&ty)[UPT]) {
 #pragma unroll
-    for (int j = 0; j < 2; ++j) {
-      tc::st_split8(buf, kTcPart, p, 2 * hh + j, z + 8 * j);
-      tc::st_split8(buf + kTcStream, kTcPart, p, 2 * hh + j, tx + 8 * j);
-      tc::st_split8(buf + 2 * kTcStream, kTcPart, p, 2 * hh + j, ty + 8 * j);
+    for (int j = 0; j < UPT / 8; ++j) {
+      tc::st_split8(buf, kTcPart, p, u0 / 8 + j, z + 8 * j);
+      tc::st_split8(buf + kTcStream, kTcPart, p, u0 / 8 + j, tx + 8 * j);
+      tc::st_split8(buf + 2 * kTcStream, kTcPart, p, u0 / 8 + j, ty + 8 * j);
     }
   };
   // read back one stream of a buffer (h + m + l)
-  auto load1 = [&](const char* buf, int s, float (&v)[16]) {
+  auto load1 = [&](const char* buf, int s, float (&v)[UPT]) {
 #pragma unroll
-    for (int j = 0; j < 2; ++j) tc::ld_join8(buf + s * kTcStream, kTcPart, p, 2 * hh + j, v + 8 * j);
+    for (int j = 0; j < UPT / 8; ++j) tc::ld_join8(buf + s * kTcStream, kTcPart, p, u0 / 8 + j, v + 8 * j);
   };
   // accumulator of stream s: columns [0,32) + [32,64) + [64,96)
-  auto acc_stream = [&](int s, float (&v)[16]) {
-    float x0[16], x1[16], x2[16];
+  auto acc_stream = [&](int s, float (&v)[UPT]) {
+    float x0[UPT], x1[UPT], x2[UPT];
     const uint32_t col = tmem + lane_q + kTcDCols * s + u0;
-    tc::tmem_ld3x16_wait(col, col + 32, col + 64, x0, x1, x2);
+    tc::tmem_ld3_wait<UPT>(col, col + 32, col + 64, x0, x1, x2);
 #pragma unroll
-    for (int k = 0; k < 16; ++k) v[k] = (x0[k] + x1[k]) + x2[k];
+    for (int k = 0; k < UPT; ++k) v[k] = (x0[k] + x1[k]) + x2[k];
   };
 
   // dedicated slab region after the small region (a.union_floats floats), or
@@ -329,7 +335,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_step_kernel(const StepArgs a
 
     // =================== forward ===================
     {
-      float z[16], tx[16], ty[16];
+      float z[UPT], tx[UPT], ty[UPT];
       layer0(px, py, z, tx, ty);
       store3(bufA, z, tx, ty);
     }
@@ -337,14 +343,14 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_step_kernel(const StepArgs a
     if (tid == 0) issue_point_gemm(sA, 1, false);
     // epilogue of hidden layer l (bias index bofs): the activation of the value
     // stream overlaps the tangent-stream MMAs
-    auto hidden_epilogue = [&](int bofs, float (&oz)[16], float (&ot)[16], float (&ou)[16]) {
-      float av[16];
+    auto hidden_epilogue = [&](int bofs, float (&oz)[UPT], float (&ot)[UPT], float (&ou)[UPT]) {
+      float av[UPT];
       wait_bar(bar_v, ph_v);
       acc_stream(0, av);
       const float* bias = sBias + bofs;
-      float s1v[16];
+      float s1v[UPT];
 #pragma unroll
-      for (int k = 0; k < 16; ++k) {
+      for (int k = 0; k < UPT; ++k) {
         const int u = u0 + k;
         const float zz = (u < H) ? AC::value(av[k] + bias[u]) : ((u == H) ? 1.0f : 0.0f);
         oz[k] = zz;
@@ -354,7 +360,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_step_kernel(const StepArgs a
       acc_stream(1, ot);
       acc_stream(2, ou);
 #pragma unroll
-      for (int k = 0; k < 16; ++k) {
+      for (int k = 0; k < UPT; ++k) {
         ot[k] = s1v[k] * ot[k];
         ou[k] = s1v[k] * ou[k];
       }
@@ -362,7 +368,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_step_kernel(const StepArgs a
     // aliased slab: its operand buffer is free once layer 1 is done (D == 3:
     // layer-1 input consumed; D == 2: unused); a dedicated slab was prefetched
     char* slab = dedicated ? dslab : ((D == 3) ? bufA : bufB);
-    float lz[16], lt[16], lu[16];  // last hidden layer (units u0..u0+15)
+    float lz[UPT], lt[UPT], lu[UPT];  // last hidden layer (units u0..u0+15)
     hidden_epilogue(0, lz, lt, lu);
     if (!dedicated && interior && tid == 0)
       issue_chunk(a, cell0, 0, nrows_tile, reinterpret_cast<float*>(slab), tma_bar);
@@ -376,7 +382,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_step_kernel(const StepArgs a
     {
       float u = 0.f, ux = 0.f, uy = 0.f;
 #pragma unroll
-      for (int k = 0; k < 16; ++k) {
+      for (int k = 0; k < UPT; ++k) {
         if (u0 + k < H) {
           const float w = sWd[u0 + k];
           u = fmaf(w, lz[k], u);
@@ -384,16 +390,20 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_step_kernel(const StepArgs a
           uy = fmaf(w, lu[k], uy);
         }
       }
-      if (hh == 1) {
-        sEx[kTxPu * 128 + p] = u;
-        sEx[kTxPx * 128 + p] = ux;
-        sEx[kTxPy * 128 + p] = uy;
+      if (hh > 0) {
+        sEx[(kTxP0 + 3 * (hh - 1)) * 128 + p] = u;
+        sEx[(kTxP0 + 3 * (hh - 1) + 1) * 128 + p] = ux;
+        sEx[(kTxP0 + 3 * (hh - 1) + 2) * 128 + p] = uy;
       }
       __syncthreads();
       if (hh == 0) {
-        u = (u + sEx[kTxPu * 128 + p]) + sWd[32];
-        ux = ux + sEx[kTxPx * 128 + p];
-        uy = uy + sEx[kTxPy * 128 + p];
+#pragma unroll
+        for (int g = 0; g < NQ - 1; ++g) {
+          u += sEx[(kTxP0 + 3 * g) * 128 + p];
+          ux += sEx[(kTxP0 + 3 * g + 1) * 128 + p];
+          uy += sEx[(kTxP0 + 3 * g + 2) * 128 + p];
+        }
+        u += sWd[32];
         if (valid && !(finitef(u) && finitef(ux) && finitef(uy))) bad = 1;
         sEx[kTxU * 128 + p] = u;
         sEx[kTxUx * 128 + p] = ux;
@@ -551,12 +561,12 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_step_kernel(const StepArgs a
     {
       float* vrow = reinterpret_cast<float*>(gbuf);  // [128][33] scratch (before G is written)
 #pragma unroll
-      for (int k = 0; k < 16; ++k) vrow[p * 33 + u0 + k] = fmaf(uyb, lu[k], fmaf(uxb, lt[k], ub * lz[k]));
+      for (int k = 0; k < UPT; ++k) vrow[p * 33 + u0 + k] = fmaf(uyb, lu[k], fmaf(uxb, lt[k], ub * lz[k]));
       __syncthreads();
-      tc_colsum(vrow, 33, H + 1, sCsum, sGacc + kGaWd);
-      float gA[16], gX[16], gY[16];
+      tc_colsum<NT>(vrow, 33, H + 1, sCsum, sGacc + kGaWd);
+      float gA[UPT], gX[UPT], gY[UPT];
 #pragma unroll
-      for (int k = 0; k < 16; ++k) {
+      for (int k = 0; k < UPT; ++k) {
         const int u = u0 + k;
         if (u < H) {
           const float wd = sWd[u];
@@ -580,18 +590,18 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_step_kernel(const StepArgs a
       issue_point_gemm(smem_u32(gbuf), NL, true);
       issue_param_gemm(smem_u32(gbuf), smem_u32(xbuf), NL, first_grad);
     }
-    float z1[16], t1x[16], t1y[16];  // hidden-1 state, recomputed once per tile
+    float z1[UPT], t1x[UPT], t1y[UPT];  // hidden-1 state, recomputed once per tile
     // G of hidden h from the propagated adjoints (TMEM) and the state (z, tx, ty)
-    auto hidden_adjoint = [&](const float (&z)[16], const float (&tx)[16], const float (&ty)[16], float (&gA)[16],
-                              float (&gX)[16], float (&gY)[16]) {
-      float xa[16], xx[16], xy[16];
+    auto hidden_adjoint = [&](const float (&z)[UPT], const float (&tx)[UPT], const float (&ty)[UPT], float (&gA)[UPT],
+                              float (&gX)[UPT], float (&gY)[UPT]) {
+      float xa[UPT], xx[UPT], xy[UPT];
       wait_bar(bar_v, ph_v);
       acc_stream(0, xa);
       wait_bar(bar_t, ph_t);
       acc_stream(1, xx);
       acc_stream(2, xy);
 #pragma unroll
-      for (int k = 0; k < 16; ++k) {
+      for (int k = 0; k < UPT; ++k) {
         if (u0 + k < H) {
           const float s1 = AC::s1(z[k]), kp = AC::kap(z[k]);
           gA[k] = fmaf(s1, xa[k], kp * fmaf(tx[k], xx[k], ty[k] * xy[k]));
@@ -603,9 +613,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_step_kernel(const StepArgs a
       }
     };
     if constexpr (D == 3) {
-      float gA[16], gX[16], gY[16];
+      float gA[UPT], gX[UPT], gY[UPT];
       {
-        float z[16], tx[16], ty[16];
+        float z[UPT], tx[UPT], ty[UPT];
         load1(xbuf, 0, z);  // hidden-2 state (read-only for the MMAs too)
         load1(xbuf, 1, tx);
         load1(xbuf, 2, ty);
@@ -627,12 +637,12 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_step_kernel(const StepArgs a
     first_grad = false;
     // ---- input layer: G of hidden 1 -> Wbar_0, bbar_0 ----
     {
-      float ga[16], gx[16], gy[16];
+      float ga[UPT], gx[UPT], gy[UPT];
       hidden_adjoint(z1, t1x, t1y, ga, gx, gy);
       wait_bar(bar_w, ph_w);  // the parameter-gradient GEMM has read bufA / bufB
       float* vrow = reinterpret_cast<float*>(bufA);  // [128][97] scratch
 #pragma unroll
-      for (int k = 0; k < 16; ++k) {
+      for (int k = 0; k < UPT; ++k) {
         const int u = u0 + k;
         // Wbar_0 += Abar x^T + TAxbar e_x^T + TAybar e_y^T ; bbar_0 += Abar
         vrow[p * 97 + u] = fmaf(ga[k], px, gx[k]);
@@ -641,7 +651,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_step_kernel(const StepArgs a
       }
       tc::fence_before_sync();
       __syncthreads();
-      tc_colsum(vrow, 97, 96, sCsum, sGacc);
+      tc_colsum<NT>(vrow, 97, 96, sCsum, sGacc);
     }
   }
 
@@ -669,7 +679,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_step_kernel(const StepArgs a
     tc::fence_before_sync();
     __syncthreads();
     const int fo = net.out_w[l], fi = net.in_w[l];
-    for (int e = tid; e < fo * (fi + 1); e += kTcThreads) {
+    for (int e = tid; e < fo * (fi + 1); e += NT) {
       const int o = e / (fi + 1), i = e - o * (fi + 1);
       float g = 0.f;
       if (!first_grad)
@@ -680,7 +690,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_step_kernel(const StepArgs a
     }
     __syncthreads();
   }
-  for (int i = tid; i < H; i += kTcThreads) {
+  for (int i = tid; i < H; i += NT) {
     a.grad_part[(size_t)(net.w_off[0] + 2 * i) * a.part_stride + blockIdx.x] = sGacc[kGaW0x + i];
     a.grad_part[(size_t)(net.w_off[0] + 2 * i + 1) * a.part_stride + blockIdx.x] = sGacc[kGaW0y + i];
     a.grad_part[(size_t)(net.b_off[0] + i) * a.part_stride + blockIdx.x] = sGacc[kGaB0 + i];

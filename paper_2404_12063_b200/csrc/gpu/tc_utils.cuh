@@ -193,6 +193,39 @@ __device__ __forceinline__ void tmem_ld3x16_wait(uint32_t ta, uint32_t tb, uint3
     vc[i] = __uint_as_float(r[32 + i]);
   }
 }
+#define VPG_R8(b)                                                                                           \
+  "=r"(r[b + 0]), "=r"(r[b + 1]), "=r"(r[b + 2]), "=r"(r[b + 3]), "=r"(r[b + 4]), "=r"(r[b + 5]),          \
+      "=r"(r[b + 6]), "=r"(r[b + 7])
+#define VPG_LD8 "tcgen05.ld.sync.aligned.32x32b.x8.b32 "
+// three 8-column loads, one wait
+__device__ __forceinline__ void tmem_ld3x8_wait(uint32_t ta, uint32_t tb, uint32_t tc_, float (&va)[8],
+                                                float (&vb)[8], float (&vc)[8]) {
+  uint32_t r[24];
+  asm volatile(VPG_LD8 "{%0,%1,%2,%3,%4,%5,%6,%7}, [%24];\n\t" VPG_LD8
+                       "{%8,%9,%10,%11,%12,%13,%14,%15}, [%25];\n\t" VPG_LD8
+                       "{%16,%17,%18,%19,%20,%21,%22,%23}, [%26];\n\t"
+                       "tcgen05.wait::ld.sync.aligned;"
+               : VPG_R8(0), VPG_R8(8), VPG_R8(16)
+               : "r"(ta), "r"(tb), "r"(tc_)
+               : "memory");
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    va[i] = __uint_as_float(r[i]);
+    vb[i] = __uint_as_float(r[8 + i]);
+    vc[i] = __uint_as_float(r[16 + i]);
+  }
+}
+// N in {8, 16} columns per load
+template <int N>
+__device__ __forceinline__ void tmem_ld3_wait(uint32_t ta, uint32_t tb, uint32_t tc_, float (&va)[N], float (&vb)[N],
+                                              float (&vc)[N]) {
+  if constexpr (N == 16)
+    tmem_ld3x16_wait(ta, tb, tc_, va, vb, vc);
+  else
+    tmem_ld3x8_wait(ta, tb, tc_, va, vb, vc);
+}
+#undef VPG_LD8
+#undef VPG_R8
 #undef VPG_LD16
 #undef VPG_R16
 

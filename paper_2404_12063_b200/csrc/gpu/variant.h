@@ -49,7 +49,7 @@ Variant make_variant() {
   v.rev_need = LY::REV_NEED;
   v.smem = [](int u, int r) { return step_smem_bytes<H, D, C>(u, r); };
   if constexpr (C == 1 && (D == 2 || D == 3) && H <= 31) {
-    v.tc = tc_step_kernel<H, D, A>;
+    v.tc = tc_step_kernel<H, D, A, kTcNQ>;
     v.tc_smem = tc_step_smem_bytes<H, D>();
   } else {
     v.tc = nullptr;

@@ -254,7 +254,7 @@ void configure(vpinn_gpu_ctx* c) {
       if (const char* e = std::getenv("VPINN_TC_SLAB")) if (std::atoi(e) == 0) a.union_floats = 0;
       c->smem_step = V.tc_smem + sizeof(float) * (size_t)a.union_floats;
       CK(cudaFuncSetAttribute(V.tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem_step));
-      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, V.tc, vpg::kTcThreads, c->smem_step));
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, V.tc, 128 * vpg::kTcNQ, c->smem_step));
       if (occ < 1) throw Fail{VPINN_ERR_DEVICE, "tensor-core step kernel cannot be resident"};
       c->grid_step = std::max(1, std::min(a.n_tiles, c->sm_count));
     } else {
@@ -422,7 +422,7 @@ void configure(vpinn_gpu_ctx* c) {
 
 void launch_fused(vpinn_gpu_ctx* c, const vpg::StepArgs& a) {
   if (c->tc)
-    c->var.tc<<<c->grid_step, vpg::kTcThreads, c->smem_step, c->stream>>>(a);
+    c->var.tc<<<c->grid_step, 128 * vpg::kTcNQ, c->smem_step, c->stream>>>(a);
   else
     c->var.fused<<<c->grid_step, vpg::kThreads, c->smem_step, c->stream>>>(a);
   CK(cudaGetLastError());
