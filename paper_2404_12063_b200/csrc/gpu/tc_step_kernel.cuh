@@ -60,8 +60,8 @@ struct TcLayout {
   static constexpr int S_CSUM = S_EX + kTxRows * 128;   // [8][96] column-sum partials
   static constexpr int S_GACC = S_CSUM + 8 * 96;        // [128] small-gradient accumulators
   static constexpr int S_CELL = S_GACC + 128;           // [256] per-cell sums
-  static constexpr int S_ROWS = S_CELL + 256;           // [3][128] rbar | rsq | rge
-  static constexpr int S_RED = S_ROWS + 3 * 128;        // 64 doubles (128 floats)
+  static constexpr int S_ROWS = S_CELL + 256;           // [6][128] rbar | rsq | rge | per-tensor partials
+  static constexpr int S_RED = S_ROWS + 6 * 128;        // 64 doubles (128 floats)
   static constexpr int S_BAR = S_RED + 128;             // 4 mbarriers + TMEM slot (16 floats)
   static constexpr int S_END = S_BAR + 16;               // then the dedicated slab, if any
   static constexpr size_t BYTES = (size_t)OFF_SMALL + sizeof(float) * S_END + 1024;  // + alignment slack
@@ -106,7 +106,7 @@ __device__ __forceinline__ void tc_colsum(const float* src, int ld, int ncols, f
 template <int H, int D, int ACT, int NQ>
 __global__ void __launch_bounds__(128 * NQ, 1) tc_step_kernel(const StepArgs a) {
   static_assert(H <= 31 && (D == 2 || D == 3), "tensor-core step: H <= 31, 2 or 3 hidden layers");
-  static_assert(NQ == 2 || NQ == 4, "unit groups per point");
+  static_assert(NQ == 4, "unit groups per point (the contraction maps tensors to groups 0..2)");
   constexpr int UPT = 32 / NQ;  // hidden units per thread
   constexpr int NT = 128 * NQ;  // threads
   using LY = TcLayout<D>;
@@ -431,62 +431,56 @@ __global__ void __launch_bounds__(128 * NQ, 1) tc_step_kernel(const StepArgs a) 
       float* rbarv = sRows;
       float* rsqv = sRows + 128;
       float* rgev = sRows + 256;
-      // phase A: one slab row per thread (nrows_tile <= 128)
-      if (tid < nrows_tile) {
-        const int kk = tid / a.T;
-        const int j = tid - kk * a.T;
-        const float* sx = sEx + kTxSx * 128 + kk * a.Q;
-        const float* sy = sEx + kTxSy * 128 + kk * a.Q;
-        const float* gxr = Gx + tid * a.Q;
-        const float* gyr = Gy + tid * a.Q;
-        float gx = 0.f, gy = 0.f;
-#pragma unroll 5
-        for (int q = 0; q < a.Q; ++q) {
-          gx = fmaf(gxr[q], sx[q], gx);
-          gy = fmaf(gyr[q], sy[q], gy);
+      float* part = sRows + 384;  // [3][128]: one dot product per (tensor, row) / (tensor, point)
+      const int nt = a.nt;
+      const float* Gt = hh == 0 ? Gx : (hh == 1 ? Gy : Tv);  // this group's tensor (hh < nt)
+      // phase A: unit group g < nt computes tensor g's row dot products
+      if (hh < nt && p < nrows_tile) {
+        const int kk = p / a.T;
+        const float* sv = sEx + (hh == 0 ? kTxSx : (hh == 1 ? kTxSy : kTxCv)) * 128 + kk * a.Q;
+        const float* gr = Gt + p * a.Q;
+        float acc4[4] = {0.f, 0.f, 0.f, 0.f};
+        int q = 0;
+#pragma unroll 2
+        for (; q + 3 < a.Q; q += 4) {
+#pragma unroll
+          for (int u = 0; u < 4; ++u) acc4[u] = fmaf(gr[q + u], sv[q + u], acc4[u]);
         }
-        float res = e_fixed * (gx + gy);
-        if (conv) {
-          const float* cv = sEx + kTxCv * 128 + kk * a.Q;
-          const float* tr = Tv + tid * a.Q;
-          float t = 0.f;
-#pragma unroll 5
-          for (int q = 0; q < a.Q; ++q) t = fmaf(tr[q], cv[q], t);
-          res += t;
-        }
-        res -= a.forcing[(size_t)(cell0 + kk) * a.T + j];
-        rsqv[tid] = res * res;
-        const float rb = a.rscale * res;
-        rbarv[tid] = rb;
-        rgev[tid] = rb * (gx + gy);
+        for (; q < a.Q; ++q) acc4[0] = fmaf(gr[q], sv[q], acc4[0]);
+        part[hh * 128 + p] = (acc4[0] + acc4[1]) + (acc4[2] + acc4[3]);
       }
       __syncthreads();
-      // phase B: one point per thread (hh == 0)
-      if (hh == 0 && valid) {
-        const int myk = p / a.Q, myq = p - myk * a.Q;
-        float tx = 0.f, ty = 0.f, tt = 0.f;
-#pragma unroll 5
-        for (int r = myk * a.T; r < (myk + 1) * a.T; ++r) {
-          const float rb = rbarv[r];
-          tx = fmaf(Gx[r * a.Q + myq], rb, tx);
-          ty = fmaf(Gy[r * a.Q + myq], rb, ty);
-          if (conv) tt = fmaf(Tv[r * a.Q + myq], rb, tt);
-        }
-        float ox = e_fixed * tx, oy = e_fixed * ty;
-        if (conv) {
-          ox = fmaf(a.bx, tt, ox);
-          oy = fmaf(a.by, tt, oy);
-        }
-        sEx[kTxUb * 128 + p] = 0.f;
-        sEx[kTxUxb * 128 + p] = ox;
-        sEx[kTxUyb * 128 + p] = oy;
-      } else if (hh == 0) {
-        sEx[kTxUb * 128 + p] = 0.f;
-        sEx[kTxUxb * 128 + p] = 0.f;
-        sEx[kTxUyb * 128 + p] = 0.f;
+      // residuals r_j (losses.hpp:122-136)
+      if (hh == 0 && p < nrows_tile) {
+        const int kk = p / a.T;
+        const int j = p - kk * a.T;
+        const float gx = part[p], gy = part[128 + p];
+        float res = e_fixed * (gx + gy);
+        if (conv) res += part[256 + p];
+        res -= a.forcing[(size_t)(cell0 + kk) * a.T + j];
+        rsqv[p] = res * res;
+        const float rb = a.rscale * res;
+        rbarv[p] = rb;
+        rgev[p] = rb * (gx + gy);
       }
-      // per-cell squared residual / eps-gradient sums in row order
-      if (hh == 1 && p < ncell) {
+      __syncthreads();
+      // phase B: unit group g < nt computes tensor g's adjoint column per
+      // point; group 3 the per-cell sums in row order
+      if (hh < nt && valid) {
+        const int myk = p / a.Q, myq = p - myk * a.Q;
+        const float* gc = Gt + myq;
+        float acc4[4] = {0.f, 0.f, 0.f, 0.f};
+        int r = myk * a.T;
+        const int r1 = r + a.T;
+#pragma unroll 2
+        for (; r + 3 < r1; r += 4) {
+#pragma unroll
+          for (int u = 0; u < 4; ++u) acc4[u] = fmaf(gc[(r + u) * a.Q], rbarv[r + u], acc4[u]);
+        }
+        for (; r < r1; ++r) acc4[0] = fmaf(gc[r * a.Q], rbarv[r], acc4[0]);
+        part[hh * 128 + p] = (acc4[0] + acc4[1]) + (acc4[2] + acc4[3]);
+      }
+      if (hh == 3 && p < ncell) {
         float s = 0.f, g = 0.f;
         for (int r = p * a.T; r < (p + 1) * a.T; ++r) {
           s += rsqv[r];
@@ -496,6 +490,21 @@ __global__ void __launch_bounds__(128 * NQ, 1) tc_step_kernel(const StepArgs a) 
         sCell[128 + p] = g;
       }
       __syncthreads();
+      if (hh == 0) {
+        float ox = 0.f, oy = 0.f;
+        if (valid) {
+          ox = e_fixed * part[p];
+          oy = e_fixed * part[128 + p];
+          if (conv) {
+            const float tt = part[256 + p];
+            ox = fmaf(a.bx, tt, ox);
+            oy = fmaf(a.by, tt, oy);
+          }
+        }
+        sEx[kTxUb * 128 + p] = 0.f;
+        sEx[kTxUxb * 128 + p] = ox;
+        sEx[kTxUyb * 128 + p] = oy;
+      }
       if (tid == 0) {
         for (int k = 0; k < ncell; ++k) {
           acc_v += (double)(sCell[k] * a.inv_nt);
