@@ -268,6 +268,7 @@ def main():
     ffma = C.c_double()
     _capi.check(L.vpinn_gpu_measure_ffma_peak(device, C.byref(ffma)))
     ms_c, bytes_c = step.time_contract(20)
+    kernel_name = step.step_kernel()
     pk = peaks()
     # algorithmic MLP flops per epoch of this rank: 33,180 per
     # interior point + 11,220 per boundary/sensor point at H=30
@@ -308,14 +309,8 @@ def main():
         "median_ms_per_epoch": med_epoch_ms,
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
-        "roofline": {"bound": "fp32_fma", "kernel": "step_kernel<30,3,1,fused>",
-                     "achieved": mlp_tflops, "peak": ffma.value, "unit": "TFLOP/s",
-                     "frac": mlp_tflops / ffma.value if ffma.value else None, "traffic": None,
-                     "share_of_step": ms_mlp / (ms_mlp + ms_red + ms_adam),
-                     "algorithmic": "33,180 flop/interior pt + 11,220 flop/penalty pt (SURVEY 8d)",
-                     "peak_source": "FFMA microbenchmark measured in this run (no FP32 peak in MEASURED_PEAKS.json)",
-                     "note": "the dominant kernel is FP32-FFMA bound (neither hbm nor tensor)"},
-        "roofline_contraction": {"bound": "hbm", "kernel": "contract_kernel (standalone)",
+        "roofline": _step_roofline(kernel_name, mlp_tflops, ffma.value, pk, ms_mlp / (ms_mlp + ms_red + ms_adam)),
+        "roofline_contraction": {"bound": "hbm", "kernel": "contract_warp_kernel (standalone, warp per cell)",
                                  "achieved": contract_gbs, "peak": pk.get("hbm_gbs"), "unit": "GB/s",
                                  "frac": contract_gbs / pk["hbm_gbs"], "traffic": None,
                                  "bytes_per_launch": bytes_c, "ms_per_launch": ms_c,
@@ -327,6 +322,52 @@ def main():
     if sweep:
         line["sweep_c2"] = sweep
     print(json.dumps(line), flush=True)
+
+
+def _traffic(kernel_prefix):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of the kernel
+    from the round's committed ncu --set full capture (profiles/*traffic.json),
+    or None."""
+    import glob
+    for path in sorted(glob.glob(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles",
+                                              "*traffic.json")), reverse=True):
+        try:
+            d = json.load(open(path))
+        except Exception:
+            continue
+        for k, v in d.items():
+            if k.startswith(kernel_prefix):
+                return {"bytes": v, "source": os.path.relpath(path, os.path.dirname(os.path.abspath(__file__)))}
+    return None
+
+
+def _step_roofline(kernel_name, mlp_tflops, ffma_peak, pk, share):
+    """Roofline of the dominant (fused step) kernel.  The tensor-core kernel
+    computes every fp32 GEMM product as six bf16 tensor products (split-bf16,
+    tc_utils.cuh), so its roofline peak is the measured bf16 tensor peak / 6
+    in fp32-equivalent flop/s; the CUDA-core kernel's peak is the measured
+    FFMA throughput.  'achieved' is always the ALGORITHMIC fp32 MLP flops
+    (33,180 per interior point + 11,220 per penalty point) per
+    launch over the launch time."""
+    tc = kernel_name.startswith("tc_step")
+    tr = _traffic("tc_step" if tc else "step_kernel")
+    if tc:
+        peak = pk["bf16_tflops"] / 6.0
+        out = {"bound": "tensor", "kernel": kernel_name, "achieved": mlp_tflops, "peak": peak,
+               "unit": "TFLOP/s", "frac": mlp_tflops / peak,
+               "peak_source": "MEASURED_PEAKS.json bf16_tflops (burst) / 6 products per fp32-faithful product",
+               "fp32_ffma_equivalent": {"peak": ffma_peak, "frac": mlp_tflops / ffma_peak if ffma_peak else None,
+                                        "peak_source": "FFMA microbenchmark measured in this run"}}
+    else:
+        out = {"bound": "fp32_fma", "kernel": kernel_name, "achieved": mlp_tflops, "peak": ffma_peak,
+               "unit": "TFLOP/s", "frac": mlp_tflops / ffma_peak if ffma_peak else None,
+               "peak_source": "FFMA microbenchmark measured in this run (no FP32 peak in MEASURED_PEAKS.json)"}
+    out["traffic"] = tr["bytes"] if tr else None
+    if tr:
+        out["traffic_source"] = tr["source"]
+    out["share_of_step"] = share
+    out["algorithmic"] = "33,180 flop/interior pt + 11,220 flop/penalty pt (SURVEY 8d)"
+    return out
 
 
 def _global_interior(hp):

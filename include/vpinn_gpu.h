@@ -130,6 +130,9 @@ typedef struct vpinn_gpu_train_result {
 
 const char* vpinn_gpu_last_error(void);
 const char* vpinn_gpu_version(void);
+/* Name of the kernel that runs the epoch's fused step on this context
+ * (tensor-core or CUDA-core variant; diagnostics and bench reporting). */
+const char* vpinn_gpu_step_kernel(const vpinn_gpu_ctx* ctx);
 
 /* 1 if a device the kernels were built for is present, else 0. */
 int vpinn_gpu_device_ok(void);

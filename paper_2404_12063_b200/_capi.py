@@ -68,6 +68,7 @@ def _declare(L):
     sig = {
         "vpinn_gpu_last_error": (C.c_char_p, []),
         "vpinn_gpu_version": (C.c_char_p, []),
+        "vpinn_gpu_step_kernel": (C.c_char_p, [vp]),
         "vpinn_gpu_device_ok": (i32, []),
         "vpinn_gpu_partition": (None, [i64, i64, i64, i32, i32, vp]),
         "vpinn_gpu_create": (i32, [C.POINTER(Problem), C.POINTER(vp)]),

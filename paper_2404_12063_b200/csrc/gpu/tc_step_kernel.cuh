@@ -306,28 +306,49 @@ __global__ void __launch_bounds__(128 * NQ, 1) tc_step_kernel(const StepArgs a) 
   int bad = 0;
   const int n_pts_all = a.n_int + a.n_bnd + a.n_sen;
 
+  // tile geometry; the point coordinates of a tile are loaded one tile ahead
+  // (register prefetch) so their DRAM latency hides behind the previous tile
+  struct TileGeo {
+    bool interior;
+    int cell0, ncell, pbase, np;
+  };
+  auto geo = [&](int tile) {
+    TileGeo g{false, 0, 0, 0, 0};
+    if (tile < a.n_int_tiles) {
+      g.interior = true;
+      g.cell0 = tile * a.cells_per_tile;
+      g.ncell = min(a.cells_per_tile, a.E - g.cell0);
+      g.pbase = g.cell0 * a.Q;
+      g.np = g.ncell * a.Q;
+    } else if (tile < a.n_tiles) {
+      g.pbase = a.n_int + (tile - a.n_int_tiles) * 128;
+      g.np = min(128, n_pts_all - g.pbase);
+    }
+    return g;
+  };
+  auto load_xy = [&](const TileGeo& g, float& x, float& y) {
+    x = 0.f;
+    y = 0.f;
+    if (p < g.np) {
+      const float2 xy = a.pts[g.pbase + p];
+      x = xy.x;
+      y = xy.y;
+    }
+  };
+  float nx, ny;
+  load_xy(geo(blockIdx.x), nx, ny);
+
 #pragma unroll 1
   for (int tile = blockIdx.x; tile < a.n_tiles; tile += gridDim.x) {
-    bool interior = false;
-    int cell0 = 0, ncell = 0, pbase = 0, np = 0;
-    if (tile < a.n_int_tiles) {
-      interior = true;
-      cell0 = tile * a.cells_per_tile;
-      ncell = min(a.cells_per_tile, a.E - cell0);
-      pbase = cell0 * a.Q;
-      np = ncell * a.Q;
-    } else {
-      pbase = a.n_int + (tile - a.n_int_tiles) * 128;
-      np = min(128, n_pts_all - pbase);
-    }
+    const TileGeo G = geo(tile);
+    const bool interior = G.interior;
+    const int cell0 = G.cell0, ncell = G.ncell, pbase = G.pbase, np = G.np;
     const int nrows_tile = ncell * a.T;
     const bool valid = p < np;
-    float px = 0.f, py = 0.f;
-    if (valid) {
-      const float2 xy = a.pts[pbase + p];
-      px = xy.x;
-      py = xy.y;
-    }
+    const float px = nx, py = ny;
+    // forcing of this thread's residual row (used after the forward)
+    float frow = 0.f;
+    if (interior && hh == 0 && p < nrows_tile) frow = a.forcing[(size_t)cell0 * a.T + p];
     if (hh == 0) {
       sEx[kTxX * 128 + p] = px;
       sEx[kTxY * 128 + p] = py;
@@ -457,7 +478,7 @@ __global__ void __launch_bounds__(128 * NQ, 1) tc_step_kernel(const StepArgs a) 
         const float gx = part[p], gy = part[128 + p];
         float res = e_fixed * (gx + gy);
         if (conv) res += part[256 + p];
-        res -= a.forcing[(size_t)(cell0 + kk) * a.T + j];
+        res -= frow;  // forcing[(cell0 + kk) * T + j], prefetched
         rsqv[p] = res * res;
         const float rb = a.rscale * res;
         rbarv[p] = rb;
@@ -551,6 +572,7 @@ __global__ void __launch_bounds__(128 * NQ, 1) tc_step_kernel(const StepArgs a) 
         }
       }
     }
+    load_xy(geo(tile + gridDim.x), nx, ny);  // next tile's points, in flight during the reverse
     __syncthreads();  // adjoint rows visible; slab reads done
     if (dedicated && tid == 0) {
       // prefetch the next tile's slab: it lands during this reverse and the next forward

@@ -167,6 +167,7 @@ struct vpinn_gpu_ctx {
   // step configuration
   bool split = false;
   bool tc = false;  // tensor-core fused step
+  std::string kernel_name;  // the epoch's dominant kernel (diagnostics)
   vpg::StepArgs sargs{};  // template (fused or reverse)
   int grid_step = 0;
   size_t smem_step = 0;
@@ -257,7 +258,11 @@ void configure(vpinn_gpu_ctx* c) {
       CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, V.tc, 128 * vpg::kTcNQ, c->smem_step));
       if (occ < 1) throw Fail{VPINN_ERR_DEVICE, "tensor-core step kernel cannot be resident"};
       c->grid_step = std::max(1, std::min(a.n_tiles, c->sm_count));
+      c->kernel_name = "tc_step_kernel<" + std::to_string(V.H) + "," + std::to_string(V.D) + "," +
+                       (V.ACT ? "sigmoid" : "tanh") + ">" + (a.union_floats ? " (dedicated slab)" : " (aliased slab)");
     } else {
+      c->kernel_name = "step_kernel<" + std::to_string(V.H) + "," + std::to_string(V.D) + "," + std::to_string(V.C) +
+                       "," + (V.ACT ? "sigmoid" : "tanh") + ",fused> (CUDA cores)";
       const size_t min_smem = V.smem(V.rev_need, 1);
       const size_t budget = min_smem <= two_cta ? two_cta : (size_t)227 * 1024;
       // the whole tile slab in one stage when it fits (one contraction chunk,
@@ -294,6 +299,8 @@ void configure(vpinn_gpu_ctx* c) {
     c->loss_rows = c->grid_step;
   } else {
     // reverse kernel over all local points
+    c->kernel_name = "step_kernel<" + std::to_string(V.H) + "," + std::to_string(V.D) + "," + std::to_string(V.C) +
+                     ",reverse> (split path)";
     a.n_tiles = ceil_div(P_local, vpg::kThreads);
     a.chunk_rows = 1;
     a.union_floats = V.rev_need;
@@ -641,6 +648,11 @@ extern "C" {
 const char* vpinn_gpu_last_error(void) { return g_err.c_str(); }
 
 const char* vpinn_gpu_version(void) { return "vpinn-b200 0.1 (sm_100a)"; }
+
+const char* vpinn_gpu_step_kernel(const vpinn_gpu_ctx* c) {
+  if (!c) return "";
+  return c->kernel_name.c_str();
+}
 
 void vpinn_gpu_partition(int64_t n_elem, int64_t n_boundary, int64_t n_sensors, int rank, int world,
                          int64_t* out6) {

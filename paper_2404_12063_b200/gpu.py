@@ -171,6 +171,10 @@ class GpuStep:
         _capi.check(_capi.lib().vpinn_gpu_time_contract(self.h, reps, C.byref(ms), C.byref(b)))
         return ms.value, b.value
 
+    def step_kernel(self) -> str:
+        """Name of the kernel running this context's fused epoch step."""
+        return _capi.lib().vpinn_gpu_step_kernel(self.h).decode()
+
     def profile_step(self, reps=10):
         a, b, c = C.c_double(), C.c_double(), C.c_double()
         _capi.check(_capi.lib().vpinn_gpu_profile_step(self.h, reps, C.byref(a), C.byref(b), C.byref(c)))
