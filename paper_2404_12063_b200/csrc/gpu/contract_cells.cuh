@@ -89,19 +89,19 @@ __device__ __forceinline__ uint32_t pre_of(const float* p) {
 //   phase B lanes over quadrature points q: adjoints (losses.hpp:145-156)
 // Loss words: fp32 per cell (fixed xor-shuffle tree), fp64 across cells,
 // CTA partials in warp order.
-constexpr int kCWWarps = 8;
-constexpr int kCWThreads = 32 * kCWWarps;
+constexpr int kCWMaxWarps = 16;  // warps per CTA: 8, 12 or 16, the most that fit (latency-bound lanes)
 
 __host__ __device__ constexpr int cw_scratch_floats(int T, int Q) {
   return 3 * ((Q + 3) & ~3) + ((T + 3) & ~3);
 }
 
-__host__ __device__ constexpr size_t cell_warp_smem_bytes(int stage_floats, int nstage, int T, int Q) {
-  return sizeof(float) * (size_t)kCWWarps * ((size_t)nstage * stage_floats + cw_scratch_floats(T, Q)) +
-         sizeof(uint64_t) * kCWWarps * kCCMaxStages + sizeof(double) * 2 * kCWWarps + 64;
+__host__ __device__ constexpr size_t cell_warp_smem_bytes(int nwarps, int stage_floats, int nstage, int T, int Q) {
+  return sizeof(float) * (size_t)nwarps * ((size_t)nstage * stage_floats + cw_scratch_floats(T, Q)) +
+         sizeof(uint64_t) * nwarps * kCCMaxStages + sizeof(double) * 2 * nwarps + 64;
 }
 
-__global__ void __launch_bounds__(kCWThreads, 1) contract_warp_kernel(const CellContractArgs a) {
+template <int kCWWarps>
+__global__ void __launch_bounds__(32 * kCWWarps, 1) contract_warp_kernel(const CellContractArgs a) {
   if (a.stop_flag != nullptr && *a.stop_flag != 0) return;
   extern __shared__ __align__(128) float cs[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;

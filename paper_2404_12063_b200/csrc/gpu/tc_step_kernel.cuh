@@ -81,26 +81,26 @@ __host__ __device__ constexpr size_t tc_step_smem_bytes() {
 }
 
 // column sums over the tile's 128 points of up to 96 per-point values
-// (src row p at src + p * ld), added in a fixed order to acc[0..ncols);
-// 8 point groups of 16, then the 8 partials in order.
+// (src row p at src + p * ld), added in a fixed order to acc[0..ncols):
+// lane (c, g) of a warp sums rows [16g, 16g + 16) of column c (4 columns x 8
+// groups per warp), then a fixed xor tree over the 8 groups.  No barrier
+// inside: the caller syncs before (src written) and orders later writes
+// to src behind its next barrier; acc[c] has a single owner lane.
 template <int NT>
-__device__ __forceinline__ void tc_colsum(const float* src, int ld, int ncols, float* part, float* acc) {
-  const int tid = threadIdx.x;
-  for (int e = tid; e < 8 * ncols; e += NT) {
-    const int g = e / ncols, c = e - g * ncols;
+__device__ __forceinline__ void tc_colsum(const float* src, int ld, int ncols, float* acc) {
+  const int ncp = (ncols + 3) & ~3;
+  for (int e = threadIdx.x; e < 8 * ncp; e += NT) {
+    const int c = (e >> 5) * 4 + ((e & 31) >> 3), g = e & 7;
     float s = 0.f;
+    if (c < ncols) {
 #pragma unroll 4
-    for (int p = 16 * g; p < 16 * g + 16; ++p) s += src[p * ld + c];
-    part[g * 96 + c] = s;
+      for (int p = 16 * g; p < 16 * g + 16; ++p) s += src[p * ld + c];
+    }
+    s += __shfl_xor_sync(0xffffffffu, s, 4);
+    s += __shfl_xor_sync(0xffffffffu, s, 2);
+    s += __shfl_xor_sync(0xffffffffu, s, 1);
+    if (g == 0 && c < ncols) acc[c] += s;
   }
-  __syncthreads();
-  for (int c = tid; c < ncols; c += NT) {
-    float s = part[c];
-#pragma unroll
-    for (int g = 1; g < 8; ++g) s += part[g * 96 + c];
-    acc[c] += s;
-  }
-  __syncthreads();
 }
 
 template <int H, int D, int ACT, int NQ>
@@ -127,7 +127,6 @@ __global__ void __launch_bounds__(128 * NQ, 1) tc_step_kernel(const StepArgs a) 
   float* sBias = sf + LY::S_BIAS;
   float* sWd = sf + LY::S_WD;
   float* sEx = sf + LY::S_EX;
-  float* sCsum = sf + LY::S_CSUM;
   float* sGacc = sf + LY::S_GACC;
   float* sCell = sf + LY::S_CELL;
   float* sRows = sf + LY::S_ROWS;
@@ -574,14 +573,6 @@ __global__ void __launch_bounds__(128 * NQ, 1) tc_step_kernel(const StepArgs a) 
     }
     load_xy(geo(tile + gridDim.x), nx, ny);  // next tile's points, in flight during the reverse
     __syncthreads();  // adjoint rows visible; slab reads done
-    if (dedicated && tid == 0) {
-      // prefetch the next tile's slab: it lands during this reverse and the next forward
-      const int nt = tile + gridDim.x;
-      if (nt < a.n_int_tiles) {
-        const int c0 = nt * a.cells_per_tile;
-        issue_chunk(a, c0, 0, min(a.cells_per_tile, a.E - c0) * a.T, reinterpret_cast<float*>(dslab), tma_bar);
-      }
-    }
     ub = sEx[kTxUb * 128 + p];
     uxb = sEx[kTxUxb * 128 + p];
     uyb = sEx[kTxUyb * 128 + p];
@@ -590,11 +581,14 @@ __global__ void __launch_bounds__(128 * NQ, 1) tc_step_kernel(const StepArgs a) 
     // ---- output layer: Wbar_out, bbar_out (column H: lz == 1) and G of the last hidden layer ----
     char* gbuf = (D == 3) ? bufA : bufB;  // free buffer
     {
-      float* vrow = reinterpret_cast<float*>(gbuf);  // [128][33] scratch (before G is written)
+      // [128][33] scratch: the consumed dedicated slab (refilled only after
+      // the next barrier), else the G buffer before G is written
+      float* vrow = reinterpret_cast<float*>(dedicated ? dslab : gbuf);
 #pragma unroll
       for (int k = 0; k < UPT; ++k) vrow[p * 33 + u0 + k] = fmaf(uyb, lu[k], fmaf(uxb, lt[k], ub * lz[k]));
       __syncthreads();
-      tc_colsum<NT>(vrow, 33, H + 1, sCsum, sGacc + kGaWd);
+      tc_colsum<NT>(vrow, 33, H + 1, sGacc + kGaWd);
+      if (!dedicated) __syncthreads();  // scratch reads done before G overwrites it
       float gA[UPT], gX[UPT], gY[UPT];
 #pragma unroll
       for (int k = 0; k < UPT; ++k) {
@@ -620,6 +614,14 @@ __global__ void __launch_bounds__(128 * NQ, 1) tc_step_kernel(const StepArgs a) 
     if (tid == 0) {
       issue_point_gemm(smem_u32(gbuf), NL, true);
       issue_param_gemm(smem_u32(gbuf), smem_u32(xbuf), NL, first_grad);
+      if (dedicated) {
+        // prefetch the next tile's slab: it lands during this reverse and the next forward
+        const int nt = tile + gridDim.x;
+        if (nt < a.n_int_tiles) {
+          const int c0 = nt * a.cells_per_tile;
+          issue_chunk(a, c0, 0, min(a.cells_per_tile, a.E - c0) * a.T, reinterpret_cast<float*>(dslab), tma_bar);
+        }
+      }
     }
     float z1[UPT], t1x[UPT], t1y[UPT];  // hidden-1 state, recomputed once per tile
     // G of hidden h from the propagated adjoints (TMEM) and the state (z, tx, ty)
@@ -671,7 +673,9 @@ __global__ void __launch_bounds__(128 * NQ, 1) tc_step_kernel(const StepArgs a) 
       float ga[UPT], gx[UPT], gy[UPT];
       hidden_adjoint(z1, t1x, t1y, ga, gx, gy);
       wait_bar(bar_w, ph_w);  // the parameter-gradient GEMM has read bufA / bufB
-      float* vrow = reinterpret_cast<float*>(bufA);  // [128][97] scratch
+      // [128][97] scratch in buffer B: its next writer comes after the next
+      // tile's first barrier
+      float* vrow = reinterpret_cast<float*>(bufB);
 #pragma unroll
       for (int k = 0; k < UPT; ++k) {
         const int u = u0 + k;
@@ -682,7 +686,7 @@ __global__ void __launch_bounds__(128 * NQ, 1) tc_step_kernel(const StepArgs a) 
       }
       tc::fence_before_sync();
       __syncthreads();
-      tc_colsum<NT>(vrow, 97, 96, sCsum, sGacc);
+      tc_colsum<NT>(vrow, 97, 96, sGacc);
     }
   }
 

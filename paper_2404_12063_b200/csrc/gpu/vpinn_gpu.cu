@@ -177,6 +177,7 @@ struct vpinn_gpu_ctx {
   vpg::CellContractArgs ccargs{};  // fast path when Q <= 128
   bool cell_contract = false;
   int grid_cc = 0;
+  int cw_warps = 8;  // warps per CTA of the warp-per-cell contraction
   size_t smem_cc = 0;
   int grid_contract = 0, grid_pen = 0, grid_fwd = 0;
   size_t smem_contract = 0, smem_fwd = 0;
@@ -382,19 +383,23 @@ void configure(vpinn_gpu_ctx* c) {
     cc.by = c->by;
     cc.rscale = a.rscale;
     cc.inv_nt = a.inv_nt;
-    const size_t budget = (size_t)227 * 1024;
-    cc.nstage = 3;
-    while (cc.nstage > 2 && vpg::cell_warp_smem_bytes(cc.stage_floats, cc.nstage, c->T, c->Q) > budget) --cc.nstage;
-    if (const char* e = std::getenv("VPINN_CW_STAGES")) cc.nstage = std::max(2, std::min(vpg::kCCMaxStages, std::atoi(e)));
-    c->smem_cc = vpg::cell_warp_smem_bytes(cc.stage_floats, cc.nstage, c->T, c->Q);
+    // the most warps per CTA (8 / 12 / 16) with a >= 2-stage ring each
+    const size_t budget = (size_t)227 * 1024 - 1024;
+    int nw = 16, ns = 2;
+    if (const char* e = std::getenv("VPINN_CW_STAGES")) ns = std::max(2, std::min(vpg::kCCMaxStages, std::atoi(e)));
+    while (nw > 8 && vpg::cell_warp_smem_bytes(nw, cc.stage_floats, ns, c->T, c->Q) > budget) nw -= 4;
+    if (const char* e = std::getenv("VPINN_CW_WARPS")) nw = std::atoi(e) >= 16 ? 16 : (std::atoi(e) >= 12 ? 12 : 8);
+    cc.nstage = ns;
+    c->cw_warps = nw;
+    c->smem_cc = vpg::cell_warp_smem_bytes(nw, cc.stage_floats, cc.nstage, c->T, c->Q);
     if (c->smem_cc > budget) {
       c->cell_contract = false;  // cell larger than a warp's ring: row-chunked kernel
     } else {
-      CK(cudaFuncSetAttribute(vpg::contract_warp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              (int)c->smem_cc));
-      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, vpg::contract_warp_kernel, vpg::kCWThreads,
-                                                       c->smem_cc));
-      c->grid_cc = std::max(1, std::min(ceil_div(c->E, vpg::kCWWarps), std::max(1, occ) * c->sm_count));
+      const void* fn = nw == 16 ? (const void*)vpg::contract_warp_kernel<16>
+                                : (nw == 12 ? (const void*)vpg::contract_warp_kernel<12> : (const void*)vpg::contract_warp_kernel<8>);
+      CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem_cc));
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, 32 * nw, c->smem_cc));
+      c->grid_cc = std::max(1, std::min(ceil_div(c->E, nw), std::max(1, occ) * c->sm_count));
     }
   }
   if (c->split) c->loss_rows = c->grid_contract + c->grid_pen + c->grid_step;
@@ -597,7 +602,12 @@ int launch_contract(vpinn_gpu_ctx* c, const float* ux, const float* uy, const fl
     a.rscale = rscale;
     a.loss_part = loss_part;
     a.stop_flag = stop;
-    vpg::contract_warp_kernel<<<c->grid_cc, vpg::kCWThreads, c->smem_cc, c->stream>>>(a);
+    if (c->cw_warps == 16)
+      vpg::contract_warp_kernel<16><<<c->grid_cc, 32 * 16, c->smem_cc, c->stream>>>(a);
+    else if (c->cw_warps == 12)
+      vpg::contract_warp_kernel<12><<<c->grid_cc, 32 * 12, c->smem_cc, c->stream>>>(a);
+    else
+      vpg::contract_warp_kernel<8><<<c->grid_cc, 32 * 8, c->smem_cc, c->stream>>>(a);
     CK(cudaGetLastError());
     c->launches += 1;
     return c->grid_cc;
