@@ -312,7 +312,8 @@ def main():
         "roofline": _step_roofline(kernel_name, mlp_tflops, ffma.value, pk, ms_mlp / (ms_mlp + ms_red + ms_adam)),
         "roofline_contraction": {"bound": "hbm", "kernel": "contract_warp_kernel (standalone, warp per cell)",
                                  "achieved": contract_gbs, "peak": pk.get("hbm_gbs"), "unit": "GB/s",
-                                 "frac": contract_gbs / pk["hbm_gbs"], "traffic": None,
+                                 "frac": contract_gbs / pk["hbm_gbs"],
+                                 "traffic": (_traffic("contract_warp") or {}).get("bytes"),
                                  "bytes_per_launch": bytes_c, "ms_per_launch": ms_c,
                                  "peak_source": "MEASURED_PEAKS.json hbm_gbs"},
         "kernel_ms": {"fused_step": ms_mlp, "reduce": ms_red, "adam": ms_adam},

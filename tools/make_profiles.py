@@ -51,6 +51,24 @@ def launch_table(path):
     return "\n".join(out)
 
 
+def traffic(rep):
+    """dram__bytes_read.sum + dram__bytes_write.sum (bytes) per captured kernel."""
+    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv", "--metrics",
+                          "dram__bytes_read.sum,dram__bytes_write.sum"], capture_output=True, text=True,
+                         check=True).stdout
+    r = list(csv.reader(out.splitlines()))
+    head, units = r[0], r[1]
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    res = {}
+    for row in r[2:]:
+        d = dict(zip(head, row))
+        u = dict(zip(head, units))
+        name = d["Kernel Name"].replace("void ", "").split("(")[0].replace(" ", "")
+        tot = sum(float(d[k].replace(",", "")) * scale[u[k]] for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
+        res[name] = tot
+    return res
+
+
 def main():
     rnd = sys.argv[1]
     os.makedirs(os.path.join(ROOT, "profiles"), exist_ok=True)
@@ -61,8 +79,8 @@ def main():
             with open(path) as f, open(dst, "w") as g:
                 g.write(f.read())
             with open(os.path.join(ROOT, "profiles", f"{rnd}_launches.md"), "w") as g:
-                g.write(f"# {rnd}: launch list of `tools/profile_step.py` under "
-                        "`ncu --metrics gpu__time_duration.sum --clock-control none`\n\n")
+                g.write(f"# {rnd}: launch list of `python bench.py --steps 3 --warmup 3 --no-cpu-baseline` under "
+                        "`ncu --metrics gpu__time_duration.sum --clock-control none -c 400`\n\n")
                 g.write("Cold-cache, serialised per-launch times (ncu replay); only the kernels' "
                         "relative share is meaningful, not the absolute step time.\n\n")
                 g.write(launch_table(path) + "\n")
@@ -71,6 +89,11 @@ def main():
             with open(os.path.join(ROOT, "profiles", f"{rnd}_bench.json"), "w") as g:
                 json.dump(d, g, indent=1)
         else:
+            tp = os.path.join(ROOT, "profiles", f"{rnd}_traffic.json")
+            tr = json.load(open(tp)) if os.path.exists(tp) else {}
+            tr.update(traffic(path))
+            with open(tp, "w") as g:
+                json.dump(tr, g, indent=1)
             with open(os.path.join(ROOT, "profiles", f"{rnd}_{key}.md"), "w") as g:
                 g.write(f"# {rnd}: `{key}` — ncu --set full --import-source on (one launch)\n\n")
                 g.write(summarise(path) + "\n")
