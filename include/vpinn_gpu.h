@@ -208,6 +208,11 @@ int vpinn_gpu_profile_step(vpinn_gpu_ctx* ctx, int reps, double* ms_mlp, double*
  * between timed epochs so every epoch streams its tensors from HBM. */
 int vpinn_gpu_flush_l2(vpinn_gpu_ctx* ctx);
 
+/* Diagnostics: clock64() phase marks of CTA 0 in the last tensor-core step
+ * launch (enabled by VPINN_PHASE_CLOCK=1 in the environment at create;
+ * 8 tiles x 32 marks).  Not part of the reference interface. */
+int vpinn_gpu_phase_clock(vpinn_gpu_ctx* ctx, long long* out, int n);
+
 /* FP32 FFMA throughput of `device` (TFLOP/s, best of 4 timed launches):
  * the roofline denominator of the FFMA-bound step kernel. */
 int vpinn_gpu_measure_ffma_peak(int device, double* tflops);

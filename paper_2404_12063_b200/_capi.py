@@ -91,6 +91,7 @@ def _declare(L):
         "vpinn_gpu_measure_ffma_peak": (i32, [i32, pd]),
         "vpinn_gpu_tc_probe": (i32, [i32, i32, vp, vp, vp, vp]),
         "vpinn_gpu_flush_l2": (i32, [vp]),
+        "vpinn_gpu_phase_clock": (i32, [vp, vp, i32]),
         "vpinn_gpu_nccl_unique_id": (i32, [vp]),
         "vpinn_gpu_attach_comm": (i32, [vp, vp, i32, i32]),
     }

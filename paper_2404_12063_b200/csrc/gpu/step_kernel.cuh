@@ -91,7 +91,13 @@ struct StepArgs {
   const float* in_uyb;
   const float* in_eb;
   const int* stop_flag;  // device trainer: non-zero -> no-op
+  // diagnostics (VPINN_PHASE_CLOCK=1): clock64() of CTA 0's thread 0 at the
+  // phase marks of its first kPhaseTiles tiles, [tile][kPhaseMarks]; else null
+  long long* phase_clk;
+  // tc2_step_kernel: per-CTA fp32 parameter-gradient scratch [cta][layer][64][64]
+  float* tc_scratch;
 };
+constexpr int kPhaseTiles = 8, kPhaseMarks = 32;
 
 template <int H, int D, int C>
 struct Layout {

@@ -1,0 +1,931 @@
+// Tensor-core FastVPINNs training step, fp16 two-part split, two CTAs per SM.
+//
+// Same per-tile semantics as tc_step_kernel.cuh / step_kernel<..., kModeFused>:
+// forward with x/y tangents (network.hpp:204-282), the Algorithm-3 contraction
+// (losses.hpp:91-168) or the penalty terms (losses.hpp:406-415), and the
+// reverse sweep (network.hpp:287-372), every hidden->hidden GEMM on tcgen05:
+//   forward      D_s[p][o] = X_s[p][:] . W[o][:]        M = 128 points, N = 32, K = 32
+//   propagation  D_s[p][i] = G_s[p][:] . W[:][i]        M = 128 points, N = 32, K = 32 (B MN-major)
+//   param grad   Wbar[o][i] = sum_{s,p} G_s[p][o] X_s[p][i]
+//                                                      M = 128 (G h | l | -), N = 64 (X h | l),
+//                                                      K = 3 streams x 128 points
+// (s = value / x-tangent / y-tangent stream).
+//
+// Precision.  Every operand is scaled by a power of two and split into two
+// fp16 parts (tc_utils.cuh st_split8_h): 22 significant bits, three products
+// Ah.Bh + Ah.Bl + Al.Bh per fp32 product, accumulated in fp32 in TMEM, i.e.
+// fp32-faithful.  The scales are derived from rigorous magnitude BOUNDS, not
+// from the data, so no reduction sits on the critical path:
+//   weights W_l              max |W_l|                                 (per CTA)
+//   value stream z           |z| <= 1 (tanh / sigmoid outputs, the constant-one bias column)
+//   tangent streams TX_h     |TX_1| <= max|w0|, |TX_{h+1}| <= R_h |TX_h|, R_h = max row abs-sum of W_h
+//   adjoints (reverse)       from the tile maxima of (ub, uxb, uyb) through
+//                            |s1| <= 1, |kap| <= 2 and the column abs-sums of W_h
+// A loose bound costs nothing measurable: fp16 keeps 2^-24 absolute spacing
+// below 2^-14, i.e. ~2^-38 of the bound.  The parameter-gradient GEMM sums
+// three streams with different scales, so the G scales are chosen to make
+// S_G,s * S_X,s one common power of two P per tile; its TMEM accumulator is
+// read out and unscaled every tile (per-CTA fp32 scratch in global memory).
+//
+// Shape: 256 threads (8 warps): thread t owns point p = t % 128 (its TMEM
+// lane) and hidden units [16 (t / 128), +16), processed in chunks of 8.  ~112
+// KB shared memory and 256 TMEM columns per CTA, so TWO CTAs share an SM and
+// one CTA's MMA / barrier / TMA waits are filled by the other's elementwise
+// work.  Hidden layers D in {2, 3}, H <= 31, one output channel.  The slab
+// (the tile's premultipliers, cp.async.bulk) aliases operand buffer A.
+#pragma once
+
+#include "step_kernel.cuh"
+#include "tc_utils.cuh"
+
+namespace vpg {
+namespace t2 {
+
+constexpr int kNT = 256;
+constexpr int kPart = 8192;           // [128][32] fp16 tile
+constexpr int kStream = 2 * kPart;    // h | l parts of one stream
+constexpr int kBuf = 3 * kStream;     // 3 streams (48 KB)
+constexpr int kWBytes = 4096;         // [64][32] fp16: W h rows 0..31 | l rows 32..63
+constexpr uint32_t kCols = 256;       // TMEM columns per CTA
+constexpr int kDCols = 32;            // stream accumulator columns
+constexpr int kG0 = 96;               // parameter-gradient accumulators: 64 columns per MMA layer
+constexpr int kScratchPerLayer = 64 * 64;  // global fp32 [col 64][lane 64] per CTA and MMA layer
+constexpr int kTailFloats = 8 * 128;  // contraction scratch after the slab in buffer A
+
+// exchange rows ([row][128] floats); the output-layer partials of unit half 1
+// (u, ux, uy) alias the adjoint rows, which are written only later
+enum : int { kX = 0, kY, kU, kUx, kUy, kUb, kUxb, kUyb, kRows };
+constexpr int kPu = kUb;
+
+// per-warp running sums of the CUDA-core gradients: W0x | W0y | b0 | Wd (16 units each)
+enum : int { kAW0x = 0, kAW0y = 16, kAB0 = 32, kAWd = 48, kAccW = 64 };
+
+// uniform scale constants (floats in S_SC)
+enum : int {
+  kScInvW = 0,      // [2] 2^-kW per MMA layer
+  kScFwd = 2,       // [2][3] forward unscale 2^-(kX + kW)
+  kScBx = 8,        // [4] tangent bounds b_x of hidden 1..D outputs
+  kScBy = 12,       // [4]
+  kScC = 16,        // [2] max column abs-sum of W_l
+  kScWd = 18,       // max |wd|
+  kScN = 24
+};
+// integer exponents (ints in S_SCI)
+enum : int { kSiW = 0, kSiX = 2, kSiN = 8 };  // kW[2], kX[2][3]
+
+template <int D>
+struct Lay {
+  static constexpr int NL = D - 1;
+  static constexpr int OFF_A = 8192;  // W tiles (<= 2 x 4 KB) first; buffers 1024-aligned
+  static constexpr int OFF_B = OFF_A + kBuf;
+  static constexpr int OFF_SMALL = OFF_B + kBuf;
+  // small region, in floats
+  static constexpr int S_W0 = 0;                       // [32][4] (w_x, w_y, b, 0)
+  static constexpr int S_BIAS = S_W0 + 128;            // [2][32]
+  static constexpr int S_WD = S_BIAS + 64;             // [32] + output bias at 32 (40)
+  static constexpr int S_EX = S_WD + 40;               // [kRows][128]
+  static constexpr int S_ACC = S_EX + kRows * 128;     // [8 warps][kAccW]
+  static constexpr int S_RED = S_ACC + 8 * kAccW;      // 16 doubles
+  static constexpr int S_SC = S_RED + 32;              // [kScN] floats
+  static constexpr int S_SCI = S_SC + kScN;            // [kSiN] ints
+  static constexpr int S_MAX = S_SCI + kSiN;           // [16] uint: tile maxima, weight norms
+  static constexpr int S_BAR = S_MAX + 16;             // 4 mbarriers + TMEM slot
+  static constexpr int S_END = S_BAR + 12;
+  static constexpr size_t BYTES = (size_t)OFF_SMALL + sizeof(float) * S_END;
+  static_assert(S_RED % 2 == 0 && S_BAR % 2 == 0, "8-byte alignment");
+};
+
+// S_MAX words: tile maxima of |ub|, |uxb|, |uyb|; max |w0x|, |w0y|, |wd|; per MMA
+// layer (max |W|, max row abs-sum, max column abs-sum)
+enum : int { kMb = 0, kMx = 1, kMy = 2, kNW0 = 3, kNLayer = 6 };
+
+// 8-value butterfly reduce-scatter over the warp's 32 lanes: afterwards lane
+// l holds the sum over all lanes of value index ((l>>4)&1)*4 + ((l>>3)&1)*2 +
+// ((l>>2)&1) (lanes l, l^1, l^2, l^3 agree).  Fixed order: deterministic.
+__device__ __forceinline__ float warp_rs8(float (&v)[8]) {
+  const int lane = threadIdx.x & 31;
+  {
+    const bool b = lane & 16;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const float send = b ? v[j] : v[j + 4], keep = b ? v[j + 4] : v[j];
+      v[j] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+    }
+  }
+  {
+    const bool b = lane & 8;
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const float send = b ? v[j] : v[j + 2], keep = b ? v[j + 2] : v[j];
+      v[j] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+    }
+  }
+  float r;
+  {
+    const bool b = lane & 4;
+    const float send = b ? v[0] : v[1], keep = b ? v[1] : v[0];
+    r = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+  }
+  r += __shfl_xor_sync(0xffffffffu, r, 2);
+  r += __shfl_xor_sync(0xffffffffu, r, 1);
+  return r;
+}
+__device__ __forceinline__ int rs8_index(int lane) { return ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1); }
+
+__device__ __forceinline__ void atomic_max_abs(uint32_t* w, float v) {
+  atomicMax(w, __float_as_uint(fabsf(v)));  // non-negative floats order as their bits (NaN: largest)
+}
+
+}  // namespace t2
+
+template <int H, int D, int ACT>
+__global__ void __maxnreg__(120) tc2_step_kernel(const StepArgs a) {
+  using namespace t2;
+  static_assert(H <= 31 && (D == 2 || D == 3), "tc2 step: H <= 31, 2 or 3 hidden layers");
+  using LY = Lay<D>;
+  constexpr int NL = LY::NL;
+  using AC = Act<ACT>;
+
+  if (a.stop_flag != nullptr && *a.stop_flag != 0) return;
+
+  extern __shared__ __align__(1024) char t2_raw[];
+  // the swizzled operand tiles need a 1024-byte aligned base; the dynamic
+  // window starts aligned (no static shared memory), checked here
+  if ((smem_u32(t2_raw) & 1023u) != 0u) __trap();
+  char* sm = t2_raw;
+  char* sWB = sm;
+  char* bufA = sm + LY::OFF_A;
+  char* bufB = sm + LY::OFF_B;
+  float* sf = reinterpret_cast<float*>(sm + LY::OFF_SMALL);
+  float* sW0 = sf + LY::S_W0;
+  float* sBias = sf + LY::S_BIAS;
+  float* sWd = sf + LY::S_WD;
+  float* sEx = sf + LY::S_EX;
+  float* sAcc = sf + LY::S_ACC;
+  double* sRed = reinterpret_cast<double*>(sf + LY::S_RED);
+  float* sSc = sf + LY::S_SC;
+  int* sSci = reinterpret_cast<int*>(sf + LY::S_SCI);
+  uint32_t* sMax = reinterpret_cast<uint32_t*>(sf + LY::S_MAX);
+  uint64_t* bar_v = reinterpret_cast<uint64_t*>(sf + LY::S_BAR);
+  uint64_t* bar_t = bar_v + 1;
+  uint64_t* bar_w = bar_v + 2;
+  uint64_t* tma_bar = bar_v + 3;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bar_v + 4);
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int p = tid & 127;   // point of this thread == TMEM lane
+  const int hh = tid >> 7;   // unit half
+  const int u0 = 16 * hh;    // first hidden unit of this thread
+  const NetDesc& net = a.net;
+  const float* P = a.params;
+  const float kapmax = 2.0f;  // |act''/act'|: 2 |z| (tanh) or |1 - 2z| (sigmoid)
+
+  // ---------------- one-time setup ----------------
+  if (warp == 0) tc::tmem_alloc(tslot, kCols);
+  if (tid == 0) {
+    mbar_init(bar_v, 1);
+    mbar_init(bar_t, 1);
+    mbar_init(bar_w, 1);
+    mbar_init(tma_bar, 1);
+    fence_mbar_init();
+  }
+  if (tid < 16) sMax[tid] = 0u;
+  for (int i = tid; i < 8 * kAccW; i += kNT) sAcc[i] = 0.f;
+  for (int i = tid; i < 32; i += kNT) {
+    float w0 = 0.f, w1 = 0.f, b = 0.f, wd = 0.f;
+    if (i < H) {
+      w0 = P[net.w_off[0] + 2 * i];
+      w1 = P[net.w_off[0] + 2 * i + 1];
+      b = P[net.b_off[0] + i];
+      wd = P[net.w_off[D] + i];
+    }
+    sW0[4 * i] = w0;
+    sW0[4 * i + 1] = w1;
+    sW0[4 * i + 2] = b;
+    sW0[4 * i + 3] = 0.f;
+    sWd[i] = wd;
+  }
+  if (tid == 0) sWd[32] = P[net.b_off[D]];
+  for (int l = 1; l <= NL; ++l)
+    for (int o = tid; o < 32; o += kNT) sBias[(l - 1) * 32 + o] = o < H ? P[net.b_off[l] + o] : 0.f;
+  __syncthreads();
+  // weight norms (bounds for the scales): max |w0x|, |w0y|, |wd|; per MMA
+  // layer max |W|, max row abs-sum R, max column abs-sum C
+  uint32_t* sNorm = sMax + kNW0;  // [0] w0x [1] w0y [2] wd
+  uint32_t(*s_lnorm)[3] = reinterpret_cast<uint32_t(*)[3]>(sMax + kNLayer);  // [layer][maxabs, rowsum, colsum]
+  if (tid < H) {
+    atomic_max_abs(&sNorm[0], sW0[4 * tid]);
+    atomic_max_abs(&sNorm[1], sW0[4 * tid + 1]);
+    atomic_max_abs(&sNorm[2], sWd[tid]);
+  }
+  for (int l = 1; l <= NL; ++l) {
+    const float* W = P + net.w_off[l];
+    const int fo = net.out_w[l], fi = net.in_w[l];
+    if (tid < 32 && tid < fo) {  // row abs-sum and max of row tid
+      float s = 0.f, m = 0.f;
+      for (int i = 0; i < fi; ++i) {
+        const float w = fabsf(W[tid * fi + i]);
+        s += w;
+        m = fmaxf(m, w);
+      }
+      atomic_max_abs(&s_lnorm[l - 1][0], m);
+      atomic_max_abs(&s_lnorm[l - 1][1], s);
+    } else if (tid >= 32 && tid < 64 && tid - 32 < fi) {  // column abs-sum
+      float s = 0.f;
+      for (int o = 0; o < fo; ++o) s += fabsf(W[o * fi + (tid - 32)]);
+      atomic_max_abs(&s_lnorm[l - 1][2], s);
+    }
+  }
+  __syncthreads();
+  if (tid == 0) {
+    // forward tangent bounds b_x[h], b_y[h] of hidden 1..D outputs
+    float bx = __uint_as_float(sNorm[0]), by = __uint_as_float(sNorm[1]);
+    sSc[kScBx] = bx;
+    sSc[kScBy] = by;
+    for (int h = 1; h < D; ++h) {
+      const float R = __uint_as_float(s_lnorm[h - 1][1]);
+      bx *= R;
+      by *= R;
+      sSc[kScBx + h] = bx;
+      sSc[kScBy + h] = by;
+    }
+    for (int l = 0; l < NL; ++l) {
+      const int kw = max(-60, min(60, 14 - tc::bound_exp(__uint_as_float(s_lnorm[l][0]))));
+      sSci[kSiW + l] = kw;
+      sSc[kScInvW + l] = tc::exp2i(-kw);
+      sSc[kScC + l] = __uint_as_float(s_lnorm[l][2]);
+      // input of MMA layer l+1 = hidden l+1 output: value bound 1, tangents b_x/b_y[l]
+      const float bnd[3] = {1.0f, sSc[kScBx + l], sSc[kScBy + l]};
+      for (int s = 0; s < 3; ++s) {
+        const int kx = max(-60, min(60, 14 - tc::bound_exp(bnd[s])));
+        sSci[kSiX + 3 * l + s] = kx;
+        sSc[kScFwd + 3 * l + s] = tc::exp2i(-(kx + kw));
+      }
+    }
+    sSc[kScWd] = __uint_as_float(sNorm[2]);
+  }
+  __syncthreads();
+  // W tiles, scaled by 2^kW: row o of part h at rows 0..31, part l at rows 32..63
+  for (int l = 1; l <= NL; ++l) {
+    char* wb = sWB + (l - 1) * kWBytes;
+    const float sw = tc::exp2i(sSci[kSiW + l - 1]);
+    for (int e = tid; e < 32 * 4; e += kNT) {
+      const int o = e >> 2, c = e & 3;
+      float v[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const int i = 8 * c + k;
+        v[k] = (o < H && i < H) ? P[net.w_off[l] + o * H + i] : 0.f;
+      }
+      tc::st_split8_h(wb, 32 * tc::kRowBytes, o, c, v, sw);
+    }
+  }
+  tc::fence_smem_to_async();
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
+  const uint32_t tmem = *tslot;
+  const uint32_t lane_q = (uint32_t)(32 * (warp & 3)) << 16;  // TMEM lane quarter of this warp
+  const uint32_t sA = smem_u32(bufA), sB = smem_u32(bufB), sW = smem_u32(sWB);
+
+  // ---------------- MMA issue (thread 0) ----------------
+  // point GEMM of MMA layer l (forward, or propagation with B MN-major): the
+  // three part products Al.Wh, Ah.Wl, Ah.Wh of stream s accumulate into D_s
+  auto issue_point_gemm = [&](uint32_t abuf, int l, bool propagate) {
+    const uint32_t wbase = sW + (uint32_t)(l - 1) * kWBytes;
+    const uint32_t idesc = tc::idesc_f16(128, 32, 0, propagate ? 1 : 0);
+#pragma unroll 1
+    for (int s = 0; s < 3; ++s) {
+      const uint32_t d = tmem + kDCols * s;
+#pragma unroll
+      for (int pr = 0; pr < 3; ++pr) {
+        const int pa = pr == 0 ? 1 : 0, pb = pr == 1 ? 1 : 0;
+        const uint32_t abase = abuf + s * kStream + pa * kPart;
+        const uint32_t bbase = wbase + pb * 32 * tc::kRowBytes;
+#pragma unroll
+        for (int ks = 0; ks < 2; ++ks) {
+          const uint64_t bd = propagate ? tc::mndesc(bbase + 1024 * ks, 32 * tc::kRowBytes) : tc::kdesc(bbase + 32 * ks);
+          tc::mma_bf16(d, tc::kdesc(abase + 32 * ks), bd, idesc, (pr > 0 || ks > 0) ? 1u : 0u);
+        }
+      }
+      if (s == 0) tc::mma_commit(bar_v);
+    }
+    tc::mma_commit(bar_t);
+  };
+  // parameter gradient of MMA layer l: G parts in bufA (M blocks h | l | next
+  // stream's parts, unused), X parts in bufB (N = h | l); fresh every tile
+  auto issue_param_gemm = [&](int l) {
+    const uint32_t acc = tmem + kG0 + 64 * (l - 1);
+    const uint32_t idesc = tc::idesc_f16(128, 64, 1, 1);
+#pragma unroll 1
+    for (int s = 0; s < 3; ++s) {
+      const uint32_t g = sA + s * kStream, x = sB + s * kStream;
+#pragma unroll
+      for (int kp = 0; kp < 8; ++kp)
+        tc::mma_bf16(acc, tc::mndesc(g + 1024 * kp, kPart), tc::mndesc(x + 1024 * kp, kPart), idesc,
+                     (s == 0 && kp == 0) ? 0u : 1u);
+    }
+    tc::mma_commit(bar_w);
+  };
+  uint32_t ph_v = 0, ph_t = 0, ph_w = 0, tma_phase = 0;
+  auto wait_bar = [&](uint64_t* bar, uint32_t& ph) {
+    mbar_wait(bar, ph);
+    ph ^= 1u;
+    tc::fence_after_sync();
+  };
+  auto operands_ready = [&]() {
+    tc::fence_smem_to_async();
+    tc::fence_before_sync();
+    __syncthreads();
+    tc::fence_after_sync();
+  };
+  auto dcol = [&](int s, int c) { return tmem + lane_q + kDCols * s + u0 + 8 * c; };
+
+  // layer 0 of this thread's chunk c (8 units) at (px, py)
+  auto layer0 = [&](int c, float px, float py, float (&z)[8], float (&tx)[8], float (&ty)[8]) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int u = u0 + 8 * c + k;
+      const float4 w = *reinterpret_cast<const float4*>(sW0 + 4 * u);
+      if (u < H) {
+        const float zz = AC::value(fmaf(w.y, py, w.x * px) + w.z);
+        const float s1 = AC::s1(zz);
+        z[k] = zz;
+        tx[k] = s1 * w.x;
+        ty[k] = s1 * w.y;
+      } else {
+        z[k] = (u == H) ? 1.0f : 0.0f;  // constant-one column -> bias gradient
+        tx[k] = 0.f;
+        ty[k] = 0.f;
+      }
+    }
+  };
+  // store the three streams of chunk c with scales s[3] into buffer buf
+  auto store3 = [&](char* buf, int c, const float (&z)[8], const float (&tx)[8], const float (&ty)[8], float s0,
+                    float s1, float s2) {
+    const int ch = 2 * hh + c;
+    tc::st_split8_h(buf, kPart, p, ch, z, s0);
+    tc::st_split8_h(buf + kStream, kPart, p, ch, tx, s1);
+    tc::st_split8_h(buf + 2 * kStream, kPart, p, ch, ty, s2);
+  };
+  // the three streams of chunk c read back from buffer buf (unscaled)
+  auto load3 = [&](const char* buf, int c, float (&z)[8], float (&tx)[8], float (&ty)[8], float i0, float i1,
+                   float i2) {
+    const int ch = 2 * hh + c;
+    tc::ld_join8_h(buf, kPart, p, ch, i0, z);
+    tc::ld_join8_h(buf + kStream, kPart, p, ch, i1, tx);
+    tc::ld_join8_h(buf + 2 * kStream, kPart, p, ch, i2, ty);
+  };
+  // running per-warp sums of 8 unit values (units u0 + 8c + k) at slot base
+  auto acc_units = [&](float (&v)[8], int slot, int c) {
+    const float r = warp_rs8(v);
+    if ((lane & 3) == 0) sAcc[warp * kAccW + slot + 8 * c + rs8_index(lane)] += r;
+  };
+
+  bool first_tile = true;
+  int kP_prev0 = 0, kP_prev1 = 0;  // param-grad product scale exponents of the last tile
+  // read the previous tile's parameter-gradient accumulators into the
+  // per-CTA fp32 scratch ([col][lane], unscaled by 2^-kP); warps of lane
+  // quarters 0 / 1 (G rows h / l), unit half = X part h / l
+  auto param_readout = [&](bool first) {
+    if ((warp & 3) >= 2) return;
+    const int lrow = 32 * (warp & 1) + lane;  // G row (part * 32 + o)
+#pragma unroll 1
+    for (int l = 0; l < NL; ++l) {
+      float* S = a.tc_scratch + ((size_t)blockIdx.x * NL + l) * kScratchPerLayer;
+      const float inv = tc::exp2i(-(l == 0 ? kP_prev0 : kP_prev1));
+#pragma unroll 1
+      for (int h2 = 0; h2 < 2; ++h2) {
+        const int col0 = 32 * hh + 16 * h2;
+        float old[16];
+        if (!first) {
+#pragma unroll
+          for (int k = 0; k < 16; ++k) old[k] = S[(col0 + k) * 64 + lrow];
+        }
+        float v[16];
+        tc::tmem_ld1x16_wait(tmem + lane_q + kG0 + 64 * l + col0, v);
+#pragma unroll
+        for (int k = 0; k < 16; ++k) S[(col0 + k) * 64 + lrow] = first ? v[k] * inv : fmaf(v[k], inv, old[k]);
+      }
+    }
+  };
+
+  // diagnostics: phase clocks of CTA 0 (StepArgs::phase_clk)
+  int ph_tile = 0;
+  auto mark = [&](int i) {
+    if (a.phase_clk != nullptr && blockIdx.x == 0 && tid == 0 && ph_tile < kPhaseTiles)
+      a.phase_clk[ph_tile * kPhaseMarks + i] = clock64();
+  };
+
+  double acc_v = 0.0, acc_b = 0.0, acc_s = 0.0, acc_eg = 0.0;  // thread 0
+  int bad = 0;
+  const int n_pts_all = a.n_int + a.n_bnd + a.n_sen;
+  struct TileGeo {
+    bool interior;
+    int cell0, ncell, pbase, np;
+  };
+  auto geo = [&](int tile) {
+    TileGeo g{false, 0, 0, 0, 0};
+    if (tile < a.n_int_tiles) {
+      g.interior = true;
+      g.cell0 = tile * a.cells_per_tile;
+      g.ncell = min(a.cells_per_tile, a.E - g.cell0);
+      g.pbase = g.cell0 * a.Q;
+      g.np = g.ncell * a.Q;
+    } else if (tile < a.n_tiles) {
+      g.pbase = a.n_int + (tile - a.n_int_tiles) * 128;
+      g.np = min(128, n_pts_all - g.pbase);
+    }
+    return g;
+  };
+  auto load_xy = [&](const TileGeo& g, float& x, float& y) {
+    x = 0.f;
+    y = 0.f;
+    if (p < g.np) {
+      const float2 xy = a.pts[g.pbase + p];
+      x = xy.x;
+      y = xy.y;
+    }
+  };
+  float nx, ny;
+  load_xy(geo(blockIdx.x), nx, ny);
+  // contraction scratch after the slab in buffer A
+  float* tail = reinterpret_cast<float*>(bufA) + a.nt * a.tstride;
+  float* cvr = tail;              // [128] bx ux + by uy
+  float* part = tail + 128;       // [3][128]
+  float* rbarv = tail + 4 * 128;  // [128]
+  float* rsqv = tail + 5 * 128;
+  float* rgev = tail + 6 * 128;
+  float* cellv = tail + 7 * 128;  // [2][<=64]: per-cell sums
+
+#pragma unroll 1
+  for (int tile = blockIdx.x; tile < a.n_tiles; tile += gridDim.x) {
+    const TileGeo G = geo(tile);
+    mark(0);
+    const bool interior = G.interior;
+    const int cell0 = G.cell0, ncell = G.ncell, np = G.np;
+    const int nrows_tile = ncell * a.T;
+    const bool valid = p < np;
+    const float px = nx, py = ny;
+    float frow = 0.f;
+    if (interior && hh == 0 && p < nrows_tile) frow = a.forcing[(size_t)cell0 * a.T + p];
+    if (hh == 0) {
+      sEx[kX * 128 + p] = px;
+      sEx[kY * 128 + p] = py;
+    }
+    if (tid < 3) sMax[tid] = 0u;  // tile maxima of |ub|, |uxb|, |uyb| (first read after 3+ barriers)
+    // D == 2: buffer A (slab) is free from the tile start
+    if (D == 2 && interior && tid == 0)
+      issue_chunk(a, cell0, 0, nrows_tile, reinterpret_cast<float*>(bufA), tma_bar);
+
+    // =================== forward ===================
+    char* x1buf = (D == 3) ? bufA : bufB;  // hidden-1 output (input of MMA layer 1)
+    {
+      const float s0 = tc::exp2i(sSci[kSiX + 0]), s1 = tc::exp2i(sSci[kSiX + 1]), s2 = tc::exp2i(sSci[kSiX + 2]);
+#pragma unroll 1
+      for (int c = 0; c < 2; ++c) {
+        float z[8], tx[8], ty[8];
+        layer0(c, px, py, z, tx, ty);
+        store3(x1buf, c, z, tx, ty, s0, s1, s2);
+      }
+    }
+    operands_ready();
+    if (tid == 0) issue_point_gemm(smem_u32(x1buf), 1, false);
+    mark(1);
+    // epilogue of MMA layer l: hidden l+1 output.  Value stream first (it
+    // overlaps the tangent-stream MMAs), stored (or consumed by the output
+    // layer when hidden l+1 is the last), then the tangents.
+    float ou = 0.f, oux = 0.f, ouy = 0.f;  // output-layer partials (last hidden)
+#pragma unroll 1
+    for (int l = 1; l <= NL; ++l) {
+      const bool last = l == NL;
+      char* nbuf = bufB;  // hidden-2 output (D == 3) -> buffer B
+      const float f0 = sSc[kScFwd + 3 * (l - 1)], f1 = sSc[kScFwd + 3 * (l - 1) + 1],
+                  f2 = sSc[kScFwd + 3 * (l - 1) + 2];
+      const float* bias = sBias + 32 * (l - 1);
+      float s1v[16];
+      wait_bar(bar_v, ph_v);
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        float d[8], z[8];
+        tc::tmem_ld1x8_wait(dcol(0, c), d);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const int u = u0 + 8 * c + k;
+          const float zz = (u < H) ? AC::value(fmaf(d[k], f0, bias[u])) : ((u == H) ? 1.0f : 0.0f);
+          z[k] = zz;
+          s1v[8 * c + k] = (u < H) ? AC::s1(zz) : 0.f;
+          if (last && u < H) ou = fmaf(sWd[u], zz, ou);
+        }
+        if (!last) tc::st_split8_h(nbuf, kPart, p, 2 * hh + c, z, tc::exp2i(sSci[kSiX + 3 * l]));
+      }
+      wait_bar(bar_t, ph_t);
+      // D == 3: buffer A (slab) is free once MMA layer 1 is done
+      if (D == 3 && l == 1 && interior && tid == 0)
+        issue_chunk(a, cell0, 0, nrows_tile, reinterpret_cast<float*>(bufA), tma_bar);
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        float dx[8], dy[8];
+        tc::tmem_ld2x8_wait(dcol(1, c), dcol(2, c), dx, dy);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          dx[k] = s1v[8 * c + k] * (dx[k] * f1);
+          dy[k] = s1v[8 * c + k] * (dy[k] * f2);
+          const int u = u0 + 8 * c + k;
+          if (last && u < H) {
+            oux = fmaf(sWd[u], dx[k], oux);
+            ouy = fmaf(sWd[u], dy[k], ouy);
+          }
+        }
+        if (!last) {
+          const int ch = 2 * hh + c;
+          tc::st_split8_h(nbuf + kStream, kPart, p, ch, dx, tc::exp2i(sSci[kSiX + 3 * l + 1]));
+          tc::st_split8_h(nbuf + 2 * kStream, kPart, p, ch, dy, tc::exp2i(sSci[kSiX + 3 * l + 2]));
+        }
+      }
+      if (!last) {
+        operands_ready();
+        if (tid == 0) issue_point_gemm(sB, l + 1, false);
+      }
+      mark(1 + l);
+    }
+    // output layer: halves combined in order (half 0 + half 1 + bias)
+    if (hh == 1) {
+      sEx[(kPu + 0) * 128 + p] = ou;
+      sEx[(kPu + 1) * 128 + p] = oux;
+      sEx[(kPu + 2) * 128 + p] = ouy;
+    }
+    __syncthreads();
+    if (hh == 0) {
+      const float u = (ou + sEx[(kPu + 0) * 128 + p]) + sWd[32];
+      const float ux = oux + sEx[(kPu + 1) * 128 + p];
+      const float uy = ouy + sEx[(kPu + 2) * 128 + p];
+      if (valid && !(finitef(u) && finitef(ux) && finitef(uy))) bad = 1;
+      sEx[kU * 128 + p] = u;
+      sEx[kUx * 128 + p] = ux;
+      sEx[kUy * 128 + p] = uy;
+      if (interior) cvr[p] = a.bx * ux + a.by * uy;
+    }
+    mark(4);
+
+    // =================== objective: adjoints of (u, ux, uy) ===================
+    if (interior) {
+      const bool conv = a.nt == 3;
+      const float e_fixed = a.eps_source == 1 ? P[net.scal_off + a.eps_scalar_index] : a.eps;
+      __syncthreads();
+      mbar_wait(tma_bar, tma_phase);
+      tma_phase ^= 1u;
+      mark(5);
+      const float* slab = reinterpret_cast<const float*>(bufA);
+      const float* T0 = chunk_ptr(a, cell0, 0, slab, 0);
+      const float* T1 = chunk_ptr(a, cell0, 0, slab, 1);
+      const float* T2 = conv ? chunk_ptr(a, cell0, 0, slab, 2) : T0;
+      const int nt = a.nt;
+      // phase A: (tensor g, row r) dot products with (ux | uy | bx ux + by uy)
+#pragma unroll 1
+      for (int it = tid; it < 3 * 128; it += kNT) {
+        const int g = it >> 7, r = it & 127;
+        if (g < nt && r < nrows_tile) {
+          const int kk = r / a.T;
+          const float* sv = (g == 0 ? sEx + kUx * 128 : (g == 1 ? sEx + kUy * 128 : cvr)) + kk * a.Q;
+          const float* gr = (g == 0 ? T0 : (g == 1 ? T1 : T2)) + r * a.Q;
+          float acc4[4] = {0.f, 0.f, 0.f, 0.f};
+          int q = 0;
+#pragma unroll 2
+          for (; q + 3 < a.Q; q += 4) {
+#pragma unroll
+            for (int u = 0; u < 4; ++u) acc4[u] = fmaf(gr[q + u], sv[q + u], acc4[u]);
+          }
+          for (; q < a.Q; ++q) acc4[0] = fmaf(gr[q], sv[q], acc4[0]);
+          part[g * 128 + r] = (acc4[0] + acc4[1]) + (acc4[2] + acc4[3]);
+        }
+      }
+      __syncthreads();
+      // residuals r_j (losses.hpp:122-136)
+      if (hh == 0 && p < nrows_tile) {
+        const float gx = part[p], gy = part[128 + p];
+        float res = e_fixed * (gx + gy);
+        if (conv) res += part[256 + p];
+        res -= frow;
+        rsqv[p] = res * res;
+        const float rb = a.rscale * res;
+        rbarv[p] = rb;
+        rgev[p] = rb * (gx + gy);
+      }
+      __syncthreads();
+      mark(6);
+      // phase B: (tensor g, point) adjoint columns; per-cell sums in row order
+#pragma unroll 1
+      for (int it = tid; it < 3 * 128; it += kNT) {
+        const int g = it >> 7, pp = it & 127;
+        if (g < nt && pp < np) {
+          const int myk = pp / a.Q, myq = pp - myk * a.Q;
+          const float* gc = (g == 0 ? T0 : (g == 1 ? T1 : T2)) + myq;
+          float acc4[4] = {0.f, 0.f, 0.f, 0.f};
+          int r = myk * a.T;
+          const int r1 = r + a.T;
+#pragma unroll 2
+          for (; r + 3 < r1; r += 4) {
+#pragma unroll
+            for (int u = 0; u < 4; ++u) acc4[u] = fmaf(gc[(r + u) * a.Q], rbarv[r + u], acc4[u]);
+          }
+          for (; r < r1; ++r) acc4[0] = fmaf(gc[r * a.Q], rbarv[r], acc4[0]);
+          part[g * 128 + pp] = (acc4[0] + acc4[1]) + (acc4[2] + acc4[3]);
+        }
+      }
+      if (tid >= kNT - 64 && tid - (kNT - 64) < ncell) {
+        const int k = tid - (kNT - 64);
+        float s = 0.f, g = 0.f;
+        for (int r = k * a.T; r < (k + 1) * a.T; ++r) {
+          s += rsqv[r];
+          g += rgev[r];
+        }
+        cellv[k] = s;
+        cellv[64 + k] = g;
+      }
+      __syncthreads();
+      mark(7);
+      if (hh == 0) {
+        float ox = 0.f, oy = 0.f;
+        if (valid) {
+          ox = e_fixed * part[p];
+          oy = e_fixed * part[128 + p];
+          if (conv) {
+            const float tt = part[256 + p];
+            ox = fmaf(a.bx, tt, ox);
+            oy = fmaf(a.by, tt, oy);
+          }
+        }
+        sEx[kUb * 128 + p] = 0.f;
+        sEx[kUxb * 128 + p] = ox;
+        sEx[kUyb * 128 + p] = oy;
+        atomic_max_abs(&sMax[kMx], ox);
+        atomic_max_abs(&sMax[kMy], oy);
+      }
+      if (tid == 0) {
+        for (int k = 0; k < ncell; ++k) {
+          acc_v += (double)(cellv[k] * a.inv_nt);
+          acc_eg += (double)cellv[64 + k];
+        }
+      }
+    } else {
+      // ---------- penalty tile (losses.hpp:389-415) ----------
+      double sb = 0.0, ss = 0.0;
+      float ubv = 0.f;
+      if (hh == 0 && valid) {
+        const int pi = G.pbase + p - a.n_int;
+        const float u = sEx[kU * 128 + p];
+        if (pi < a.n_bnd) {
+          const float d = u - a.bval[pi];
+          sb = (double)(d * d);
+          ubv = a.bscale * d;
+        } else {
+          const float d = u - a.sval[pi - a.n_bnd];
+          ss = (double)(d * d);
+          ubv = a.sscale * d;
+        }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        sb += __shfl_down_sync(0xffffffffu, sb, o);
+        ss += __shfl_down_sync(0xffffffffu, ss, o);
+      }
+      if (hh == 0) {
+        sEx[kUb * 128 + p] = ubv;
+        sEx[kUxb * 128 + p] = 0.f;
+        sEx[kUyb * 128 + p] = 0.f;
+        atomic_max_abs(&sMax[kMb], ubv);
+      }
+      if (lane == 0 && warp < 4) {
+        sRed[warp] = sb;
+        sRed[8 + warp] = ss;
+      }
+      __syncthreads();
+      if (tid == 0) {
+        for (int w = 0; w < 4; ++w) {
+          acc_b += sRed[w];
+          acc_s += sRed[8 + w];
+        }
+      }
+    }
+    load_xy(geo(tile + gridDim.x), nx, ny);  // next tile's points, in flight during the reverse
+    __syncthreads();                          // adjoint rows + tile maxima visible; slab reads done
+    mark(8);
+    const float ub = sEx[kUb * 128 + p], uxb = sEx[kUxb * 128 + p], uyb = sEx[kUyb * 128 + p];
+
+    // =================== reverse ===================
+    // adjoint bounds of G at the last hidden layer
+    const float Mb = __uint_as_float(sMax[kMb]), Mx = __uint_as_float(sMax[kMx]), My = __uint_as_float(sMax[kMy]);
+    const float Wd = sSc[kScWd];
+    float bG[3] = {Wd * (Mb + kapmax * (sSc[kScBx + D - 1] * Mx + sSc[kScBy + D - 1] * My)), Wd * Mx, Wd * My};
+    // G scales for param layer l: S_G,s = 2^(kP - kX[l-1][s]) with the
+    // common product exponent kP = min_s (14 - e(B_s) + kX[l-1][s])
+    int kP0 = 0, kP1 = 0;
+    auto g_scales = [&](int l, const float (&bnd)[3], float (&sg)[3], float (&pu)[3]) {
+      int kp = 1 << 20;
+#pragma unroll
+      for (int s = 0; s < 3; ++s) {
+        const int e = tc::bound_exp(bnd[s]);
+        if (e > -1000) kp = min(kp, 14 - e + sSci[kSiX + 3 * (l - 1) + s]);
+      }
+      if (kp == (1 << 20)) kp = sSci[kSiX + 3 * (l - 1)];
+      kp = max(-120, min(120, kp));
+      if (l == 1) kP0 = kp; else kP1 = kp;
+#pragma unroll
+      for (int s = 0; s < 3; ++s) {
+        const int kg = kp - sSci[kSiX + 3 * (l - 1) + s];
+        sg[s] = tc::exp2i(kg);
+        pu[s] = tc::exp2i(-(kg + sSci[kSiW + l - 1]));  // propagation unscale
+      }
+    };
+    float sg[3], pu[3];
+    g_scales(NL, bG, sg, pu);
+    // ---- output layer: Wbar_out, bbar_out (unit H: z == 1), G of the last hidden layer ----
+    {
+      const int lw = NL;  // MMA layer whose accumulators hold the last hidden pre-activations
+      const float f0 = sSc[kScFwd + 3 * (lw - 1)], f1 = sSc[kScFwd + 3 * (lw - 1) + 1],
+                  f2 = sSc[kScFwd + 3 * (lw - 1) + 2];
+      const float* bias = sBias + 32 * (lw - 1);
+#pragma unroll 1
+      for (int c = 0; c < 2; ++c) {
+        float d0[8], dx[8], dy[8];
+        {
+          float t0[8];
+          tc::tmem_ld1x8_wait(dcol(0, c), t0);
+#pragma unroll
+          for (int k = 0; k < 8; ++k) d0[k] = t0[k];
+        }
+        tc::tmem_ld2x8_wait(dcol(1, c), dcol(2, c), dx, dy);
+        float v[8], gA[8], gX[8], gY[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const int u = u0 + 8 * c + k;
+          if (u < H) {
+            const float z = AC::value(fmaf(d0[k], f0, bias[u]));
+            const float s1 = AC::s1(z), kp = AC::kap(z);
+            const float tx = s1 * (dx[k] * f1), ty = s1 * (dy[k] * f2);
+            v[k] = fmaf(uyb, ty, fmaf(uxb, tx, ub * z));
+            const float wd = sWd[u];
+            const float xb = wd * ub, zx = wd * uxb, zy = wd * uyb;
+            gA[k] = fmaf(s1, xb, kp * fmaf(tx, zx, ty * zy));
+            gX[k] = s1 * zx;
+            gY[k] = s1 * zy;
+          } else {
+            v[k] = (u == H) ? ub : 0.f;
+            gA[k] = gX[k] = gY[k] = 0.f;
+          }
+        }
+        acc_units(v, kAWd, c);
+        store3(bufA, c, gA, gX, gY, sg[0], sg[1], sg[2]);
+      }
+    }
+    operands_ready();
+    if (tid == 0) {
+      issue_point_gemm(sA, NL, true);
+      issue_param_gemm(NL);
+    }
+    mark(9);
+    // ---- hidden layers, last first: G of hidden l from the propagated adjoints ----
+#pragma unroll 1
+    for (int l = NL; l >= 1; --l) {
+      // hidden-l state: X_l in buffer B (MMA layer l's input), scales kX[l-1]
+      const float i0 = tc::exp2i(-sSci[kSiX + 3 * (l - 1)]), i1 = tc::exp2i(-sSci[kSiX + 3 * (l - 1) + 1]),
+                  i2 = tc::exp2i(-sSci[kSiX + 3 * (l - 1) + 2]);
+      float bnd2[3];
+      {
+        const float C = sSc[kScC + l - 1];
+        const float bxa = C * bG[0], bxx = C * bG[1], bxy = C * bG[2];
+        bnd2[0] = bxa + kapmax * (sSc[kScBx + l - 1] * bxx + sSc[kScBy + l - 1] * bxy);
+        bnd2[1] = bxx;
+        bnd2[2] = bxy;
+      }
+      float sg2[3] = {1.f, 1.f, 1.f}, pu2[3] = {1.f, 1.f, 1.f};
+      if (l > 1) g_scales(l - 1, bnd2, sg2, pu2);
+      wait_bar(bar_v, ph_v);
+      wait_bar(bar_t, ph_t);
+      // l > 1: G of hidden l goes to buffer A and the recomputed hidden-1
+      // output to buffer B, so param GEMM l must have read both; each thread
+      // reads (its state) and writes exactly its own slots, so no barrier
+      if (l > 1) wait_bar(bar_w, ph_w);
+#pragma unroll 1
+      for (int c = 0; c < 2; ++c) {
+        float xa[8], xx[8], xy[8], z[8], tx[8], ty[8];
+        tc::tmem_ld1x8_wait(dcol(0, c), xa);
+        tc::tmem_ld2x8_wait(dcol(1, c), dcol(2, c), xx, xy);
+        load3(bufB, c, z, tx, ty, i0, i1, i2);
+        float ga[8], gx[8], gy[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const int u = u0 + 8 * c + k;
+          if (u < H) {
+            const float s1 = AC::s1(z[k]), kp = AC::kap(z[k]);
+            const float aa = xa[k] * pu[0], ax = xx[k] * pu[1], ay = xy[k] * pu[2];
+            ga[k] = fmaf(s1, aa, kp * fmaf(tx[k], ax, ty[k] * ay));
+            gx[k] = s1 * ax;
+            gy[k] = s1 * ay;
+          } else {
+            ga[k] = gx[k] = gy[k] = 0.f;
+          }
+        }
+        if (l == 1) {
+          // ---- input layer: Wbar_0 += Abar x^T + TAxbar e_x^T + TAybar e_y^T; bbar_0 += Abar ----
+          float v[8];
+#pragma unroll
+          for (int k = 0; k < 8; ++k) v[k] = fmaf(ga[k], px, gx[k]);
+          acc_units(v, kAW0x, c);
+#pragma unroll
+          for (int k = 0; k < 8; ++k) v[k] = fmaf(ga[k], py, gy[k]);
+          acc_units(v, kAW0y, c);
+#pragma unroll
+          for (int k = 0; k < 8; ++k) v[k] = ga[k];
+          acc_units(v, kAB0, c);
+        } else {
+          store3(bufA, c, ga, gx, gy, sg2[0], sg2[1], sg2[2]);
+          layer0(c, px, py, z, tx, ty);  // hidden-1 output recomputed (l - 1 == 1)
+          store3(bufB, c, z, tx, ty, tc::exp2i(sSci[kSiX + 0]), tc::exp2i(sSci[kSiX + 1]),
+                 tc::exp2i(sSci[kSiX + 2]));
+        }
+      }
+      if (l > 1) {
+        operands_ready();
+        if (tid == 0) {
+          issue_point_gemm(sA, l - 1, true);
+          issue_param_gemm(l - 1);
+        }
+#pragma unroll
+        for (int s = 0; s < 3; ++s) {
+          bG[s] = bnd2[s];
+          pu[s] = pu2[s];
+        }
+      }
+      mark(9 + NL - l + 1);
+    }
+    wait_bar(bar_w, ph_w);  // the last param GEMM is done (buffers A / B free, accumulators final)
+    kP_prev0 = kP0;
+    kP_prev1 = kP1;
+    param_readout(first_tile);
+    first_tile = false;
+    mark(12);
+    ++ph_tile;
+  }
+
+  // =================== per-CTA outputs ===================
+  __syncthreads();
+  for (int l = 1; l <= NL; ++l) {
+    const float* S = a.tc_scratch + ((size_t)blockIdx.x * NL + (l - 1)) * kScratchPerLayer;
+    const int fo = net.out_w[l], fi = net.in_w[l];
+    for (int e = tid; e < fo * (fi + 1); e += kNT) {
+      const int o = e / (fi + 1), i = e - o * (fi + 1);
+      float g = 0.f;
+      if (!first_tile)  // S[col][row]: col = X part * 32 + i, row = G part * 32 + o
+        g = ((S[i * 64 + o] + S[(32 + i) * 64 + o]) + S[i * 64 + 32 + o]) + S[(32 + i) * 64 + 32 + o];
+      const int idx = (i < fi) ? net.w_off[l] + o * fi + i : net.b_off[l] + o;
+      a.grad_part[(size_t)idx * a.part_stride + blockIdx.x] = g;
+    }
+  }
+  // CUDA-core gradients: per-warp sums combined in warp order
+  for (int u = tid; u <= H; u += kNT) {
+    const int h2 = u >> 4, j = u & 15;
+    float w0x = 0.f, w0y = 0.f, b0 = 0.f, wd = 0.f;
+    for (int w = 4 * h2; w < 4 * h2 + 4; ++w) {
+      const float* A = sAcc + w * kAccW;
+      w0x += A[kAW0x + j];
+      w0y += A[kAW0y + j];
+      b0 += A[kAB0 + j];
+      wd += A[kAWd + j];
+    }
+    if (u < H) {
+      a.grad_part[(size_t)(net.w_off[0] + 2 * u) * a.part_stride + blockIdx.x] = w0x;
+      a.grad_part[(size_t)(net.w_off[0] + 2 * u + 1) * a.part_stride + blockIdx.x] = w0y;
+      a.grad_part[(size_t)(net.b_off[0] + u) * a.part_stride + blockIdx.x] = b0;
+      a.grad_part[(size_t)(net.w_off[D] + u) * a.part_stride + blockIdx.x] = wd;
+    } else {
+      a.grad_part[(size_t)net.b_off[D] * a.part_stride + blockIdx.x] = wd;
+    }
+  }
+  if (tid == 0)
+    for (int e = net.scal_off; e < net.n_params; ++e) a.grad_part[(size_t)e * a.part_stride + blockIdx.x] = 0.f;
+  const int any_bad = __syncthreads_or(bad);
+  if (tid == 0) {
+    double* lp = a.loss_part + (size_t)blockIdx.x * kLpWords;
+    lp[kLpVar] = acc_v;
+    lp[kLpBnd] = acc_b;
+    lp[kLpSen] = acc_s;
+    lp[kLpEpsGrad] = acc_eg;
+    lp[kLpBad] = any_bad ? 1.0 : 0.0;
+    for (int w = kLpBad + 1; w < kLpWords; ++w) lp[w] = 0.0;
+  }
+  tc::fence_before_sync();
+  __syncthreads();
+  if (warp == 0) {
+    tc::fence_after_sync();
+    tc::tmem_dealloc(tmem, kCols);
+  }
+}
+
+template <int H, int D>
+__host__ __device__ constexpr size_t tc2_step_smem_bytes() {
+  return t2::Lay<D>::BYTES;
+}
+
+}  // namespace vpg

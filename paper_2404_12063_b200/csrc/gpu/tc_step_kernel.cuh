@@ -334,12 +334,19 @@ __global__ void __launch_bounds__(128 * NQ, 1) tc_step_kernel(const StepArgs a) 
       y = xy.y;
     }
   };
+  // diagnostics: phase clocks of CTA 0 (StepArgs::phase_clk)
+  int ph_tile = 0;
+  auto mark = [&](int i) {
+    if (a.phase_clk != nullptr && blockIdx.x == 0 && tid == 0 && ph_tile < kPhaseTiles)
+      a.phase_clk[ph_tile * kPhaseMarks + i] = clock64();
+  };
   float nx, ny;
   load_xy(geo(blockIdx.x), nx, ny);
 
 #pragma unroll 1
   for (int tile = blockIdx.x; tile < a.n_tiles; tile += gridDim.x) {
     const TileGeo G = geo(tile);
+    mark(0);
     const bool interior = G.interior;
     const int cell0 = G.cell0, ncell = G.ncell, pbase = G.pbase, np = G.np;
     const int nrows_tile = ncell * a.T;
@@ -360,6 +367,7 @@ __global__ void __launch_bounds__(128 * NQ, 1) tc_step_kernel(const StepArgs a) 
       store3(bufA, z, tx, ty);
     }
     operands_ready();
+    mark(1);
     if (tid == 0) issue_point_gemm(sA, 1, false);
     // epilogue of hidden layer l (bias index bofs): the activation of the value
     // stream overlaps the tangent-stream MMAs
@@ -390,13 +398,16 @@ __global__ void __launch_bounds__(128 * NQ, 1) tc_step_kernel(const StepArgs a) 
     char* slab = dedicated ? dslab : ((D == 3) ? bufA : bufB);
     float lz[UPT], lt[UPT], lu[UPT];  // last hidden layer (units u0..u0+15)
     hidden_epilogue(0, lz, lt, lu);
+    mark(2);
     if (!dedicated && interior && tid == 0)
       issue_chunk(a, cell0, 0, nrows_tile, reinterpret_cast<float*>(slab), tma_bar);
     if constexpr (D == 3) {
       store3(bufB, lz, lt, lu);
       operands_ready();
+      mark(3);
       if (tid == 0) issue_point_gemm(sB, 2, false);
       hidden_epilogue(32, lz, lt, lu);
+      mark(4);
     }
     // output layer (linear) over this thread's units, halves combined in order
     {
@@ -430,6 +441,7 @@ __global__ void __launch_bounds__(128 * NQ, 1) tc_step_kernel(const StepArgs a) 
         sEx[kTxUy * 128 + p] = uy;
       }
     }
+    mark(5);
 
     // =================== objective: adjoints of (u, ux, uy) ===================
     float ub = 0.f, uxb = 0.f, uyb = 0.f;
@@ -445,6 +457,7 @@ __global__ void __launch_bounds__(128 * NQ, 1) tc_step_kernel(const StepArgs a) 
       __syncthreads();
       mbar_wait(tma_bar, tma_phase);
       tma_phase ^= 1u;
+      mark(6);
       const float* Gx = chunk_ptr(a, cell0, 0, reinterpret_cast<const float*>(slab), 0);
       const float* Gy = chunk_ptr(a, cell0, 0, reinterpret_cast<const float*>(slab), 1);
       const float* Tv = conv ? chunk_ptr(a, cell0, 0, reinterpret_cast<const float*>(slab), 2) : nullptr;
@@ -470,6 +483,7 @@ __global__ void __launch_bounds__(128 * NQ, 1) tc_step_kernel(const StepArgs a) 
         part[hh * 128 + p] = (acc4[0] + acc4[1]) + (acc4[2] + acc4[3]);
       }
       __syncthreads();
+      mark(7);
       // residuals r_j (losses.hpp:122-136)
       if (hh == 0 && p < nrows_tile) {
         const int kk = p / a.T;
@@ -484,6 +498,7 @@ __global__ void __launch_bounds__(128 * NQ, 1) tc_step_kernel(const StepArgs a) 
         rgev[p] = rb * (gx + gy);
       }
       __syncthreads();
+      mark(8);
       // phase B: unit group g < nt computes tensor g's adjoint column per
       // point; group 3 the per-cell sums in row order
       if (hh < nt && valid) {
@@ -510,6 +525,7 @@ __global__ void __launch_bounds__(128 * NQ, 1) tc_step_kernel(const StepArgs a) 
         sCell[128 + p] = g;
       }
       __syncthreads();
+      mark(9);
       if (hh == 0) {
         float ox = 0.f, oy = 0.f;
         if (valid) {
@@ -573,6 +589,7 @@ __global__ void __launch_bounds__(128 * NQ, 1) tc_step_kernel(const StepArgs a) 
     }
     load_xy(geo(tile + gridDim.x), nx, ny);  // next tile's points, in flight during the reverse
     __syncthreads();  // adjoint rows visible; slab reads done
+    mark(10);
     ub = sEx[kTxUb * 128 + p];
     uxb = sEx[kTxUxb * 128 + p];
     uyb = sEx[kTxUyb * 128 + p];
@@ -607,6 +624,7 @@ __global__ void __launch_bounds__(128 * NQ, 1) tc_step_kernel(const StepArgs a) 
       store3(gbuf, gA, gX, gY);
     }
     operands_ready();
+    mark(11);
     // ---- hidden->hidden layers, last first ----
     // propagation first (bar_v / bar_t), then the parameter-gradient GEMM
     // (bar_w); elementwise work that does not need them runs in their shadow
@@ -655,11 +673,13 @@ __global__ void __launch_bounds__(128 * NQ, 1) tc_step_kernel(const StepArgs a) 
         layer0(px, py, z1, t1x, t1y);
         hidden_adjoint(z, tx, ty, gA, gX, gY);
       }
+      mark(12);
       wait_bar(bar_w, ph_w);  // both operand buffers free
       __syncthreads();        // every thread has read hidden-2 state from xbuf
       store3(gbuf, gA, gX, gY);
       store3(xbuf, z1, t1x, t1y);  // layer-1 input (recomputed)
       operands_ready();
+      mark(13);
       if (tid == 0) {
         issue_point_gemm(smem_u32(gbuf), 1, true);
         issue_param_gemm(smem_u32(gbuf), smem_u32(xbuf), 1, first_grad);
@@ -672,7 +692,9 @@ __global__ void __launch_bounds__(128 * NQ, 1) tc_step_kernel(const StepArgs a) 
     {
       float ga[UPT], gx[UPT], gy[UPT];
       hidden_adjoint(z1, t1x, t1y, ga, gx, gy);
+      mark(14);
       wait_bar(bar_w, ph_w);  // the parameter-gradient GEMM has read bufA / bufB
+      mark(15);
       // [128][97] scratch in buffer B: its next writer comes after the next
       // tile's first barrier
       float* vrow = reinterpret_cast<float*>(bufB);
@@ -688,6 +710,8 @@ __global__ void __launch_bounds__(128 * NQ, 1) tc_step_kernel(const StepArgs a) 
       __syncthreads();
       tc_colsum<NT>(vrow, 97, 96, sGacc);
     }
+    mark(16);
+    ++ph_tile;
   }
 
   // =================== per-CTA outputs ===================

@@ -104,6 +104,70 @@ __device__ __forceinline__ void ld_join8(const char* base, uint32_t part_stride,
   for (int k = 0; k < 8; ++k) v[k] = h[k] + (m[k] + l[k]);
 }
 
+// ---- fp16 two-part split (tc2_step_kernel.cuh) ------------------------------
+// y = s * x with a power-of-two s (exact), h = f16(y), l = f16(y - h): y - h
+// is exact in fp32 and h + l carries 22 significant bits, so the three
+// products hh' + hl' + lh' are fp32-faithful (dropped ll' < 2^-22 relative)
+// as long as s keeps |y| inside the fp16 normal range (the caller scales by
+// a bound, see tc2_step_kernel.cuh).  cvt.rn.f16x2.f32 runs on the ALU pipe
+// (measured 2 warp-instr/clk/SM on B200, the LOP3 rate).
+__device__ __forceinline__ uint32_t pack_f16x2(float lo, float hi) {
+  uint32_t r;
+  asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+  return r;
+}
+__device__ __forceinline__ float f16lo(uint32_t w) {
+  float f;
+  asm("{\n .reg .b16 lo, hi;\n mov.b32 {lo, hi}, %1;\n cvt.f32.f16 %0, lo;\n}" : "=f"(f) : "r"(w));
+  return f;
+}
+__device__ __forceinline__ float f16hi(uint32_t w) {
+  float f;
+  asm("{\n .reg .b16 lo, hi;\n mov.b32 {lo, hi}, %1;\n cvt.f32.f16 %0, hi;\n}" : "=f"(f) : "r"(w));
+  return f;
+}
+// store 8 consecutive columns [8 chunk, +8) of one row, scaled by s, into
+// the two part tiles at base (h) and base + part_stride (l)
+__device__ __forceinline__ void st_split8_h(char* base, uint32_t part_stride, int row, int chunk, const float* v,
+                                            float s) {
+  uint32_t h[4], l[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const float y0 = v[2 * k] * s, y1 = v[2 * k + 1] * s;
+    h[k] = pack_f16x2(y0, y1);
+    l[k] = pack_f16x2(y0 - f16lo(h[k]), y1 - f16hi(h[k]));
+  }
+  const uint32_t off = sw_chunk(row, chunk);
+  *reinterpret_cast<uint4*>(base + off) = make_uint4(h[0], h[1], h[2], h[3]);
+  *reinterpret_cast<uint4*>(base + part_stride + off) = make_uint4(l[0], l[1], l[2], l[3]);
+}
+// read back 8 columns as (h + l) * inv_s
+__device__ __forceinline__ void ld_join8_h(const char* base, uint32_t part_stride, int row, int chunk, float inv_s,
+                                           float* v) {
+  const uint32_t off = sw_chunk(row, chunk);
+  const uint4 h = *reinterpret_cast<const uint4*>(base + off);
+  const uint4 l = *reinterpret_cast<const uint4*>(base + part_stride + off);
+  const uint32_t hw[4] = {h.x, h.y, h.z, h.w}, lw[4] = {l.x, l.y, l.z, l.w};
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    v[2 * k] = (f16lo(hw[k]) + f16lo(lw[k])) * inv_s;
+    v[2 * k + 1] = (f16hi(hw[k]) + f16hi(lw[k])) * inv_s;
+  }
+}
+// 2^k as a float, k clamped to the normal range
+__device__ __forceinline__ float exp2i(int k) {
+  k = max(-126, min(127, k));
+  return __uint_as_float((uint32_t)(127 + k) << 23);
+}
+// the exponent e with b < 2^e for a positive normal b (-1000 for zero,
+// denormal or NaN: "no bound"); inf gives 129
+__device__ __forceinline__ int bound_exp(float b) {
+  const uint32_t bits = __float_as_uint(b);
+  const int E = (int)((bits >> 23) & 0xffu);
+  if (!(b > 0.f) || E == 0) return -1000;
+  return E - 126;
+}
+
 // ---- descriptors ---------------------------------------------------------------
 // shared-memory matrix descriptor (sm100): start >> 4 [0,14), LBO >> 4
 // [16,30), SBO >> 4 [32,46), version 1 [46,48), base offset 0, layout type
@@ -132,6 +196,12 @@ __host__ __device__ constexpr uint32_t idesc_bf16(int M, int N, int a_mn_major, 
          | ((uint32_t)b_mn_major << 16)  // B major
          | ((uint32_t)(N >> 3) << 17)    // N
          | ((uint32_t)(M >> 4) << 24);   // M
+}
+
+// instruction descriptor, kind::f16 with fp16 inputs, fp32 accumulate
+__host__ __device__ constexpr uint32_t idesc_f16(int M, int N, int a_mn_major, int b_mn_major) {
+  return (1u << 4) | ((uint32_t)a_mn_major << 15) | ((uint32_t)b_mn_major << 16) | ((uint32_t)(N >> 3) << 17) |
+         ((uint32_t)(M >> 4) << 24);
 }
 
 // ---- tcgen05 -------------------------------------------------------------------
@@ -213,6 +283,42 @@ __device__ __forceinline__ void tmem_ld3x8_wait(uint32_t ta, uint32_t tb, uint32
     va[i] = __uint_as_float(r[i]);
     vb[i] = __uint_as_float(r[8 + i]);
     vc[i] = __uint_as_float(r[16 + i]);
+  }
+}
+// one 16-column load
+__device__ __forceinline__ void tmem_ld1x16_wait(uint32_t ta, float (&va)[16]) {
+  uint32_t r[16];
+  asm volatile(VPG_LD16 "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n\t"
+                        "tcgen05.wait::ld.sync.aligned;"
+               : VPG_R16(0)
+               : "r"(ta)
+               : "memory");
+#pragma unroll
+  for (int i = 0; i < 16; ++i) va[i] = __uint_as_float(r[i]);
+}
+// one / two 8-column loads, one wait
+__device__ __forceinline__ void tmem_ld1x8_wait(uint32_t ta, float (&va)[8]) {
+  uint32_t r[8];
+  asm volatile(VPG_LD8 "{%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n\t"
+                       "tcgen05.wait::ld.sync.aligned;"
+               : VPG_R8(0)
+               : "r"(ta)
+               : "memory");
+#pragma unroll
+  for (int i = 0; i < 8; ++i) va[i] = __uint_as_float(r[i]);
+}
+__device__ __forceinline__ void tmem_ld2x8_wait(uint32_t ta, uint32_t tb, float (&va)[8], float (&vb)[8]) {
+  uint32_t r[16];
+  asm volatile(VPG_LD8 "{%0,%1,%2,%3,%4,%5,%6,%7}, [%16];\n\t" VPG_LD8
+                       "{%8,%9,%10,%11,%12,%13,%14,%15}, [%17];\n\t"
+                       "tcgen05.wait::ld.sync.aligned;"
+               : VPG_R8(0), VPG_R8(8)
+               : "r"(ta), "r"(tb)
+               : "memory");
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    va[i] = __uint_as_float(r[i]);
+    vb[i] = __uint_as_float(r[8 + i]);
   }
 }
 // N in {8, 16} columns per load

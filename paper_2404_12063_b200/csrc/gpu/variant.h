@@ -16,6 +16,8 @@ struct Variant {
   StepFn fused, forward, reverse;
   StepFn tc;       // tensor-core fused step (tc_step_kernel.cuh), nullptr if the shape has none
   size_t tc_smem;
+  StepFn tc2;      // fp16-split two-CTA tensor-core step (tc2_step_kernel.cuh), nullptr if none
+  size_t tc2_smem;
   int off_union;  // floats before the union
   int rev_need;   // floats the reverse phase needs in the union
   size_t (*smem)(int, int);
@@ -33,6 +35,7 @@ VPG_VARIANTS(VPG_DECL)
 #ifdef VPG_DEFINE_VARIANT
 }  // namespace vpg
 #include "tc_step_kernel.cuh"
+#include "tc2_step_kernel.cuh"
 namespace vpg {
 template <int H, int D, int C, int A>
 Variant make_variant() {
@@ -51,9 +54,13 @@ Variant make_variant() {
   if constexpr (C == 1 && (D == 2 || D == 3) && H <= 31) {
     v.tc = tc_step_kernel<H, D, A, kTcNQ>;
     v.tc_smem = tc_step_smem_bytes<H, D>();
+    v.tc2 = tc2_step_kernel<H, D, A>;
+    v.tc2_smem = tc2_step_smem_bytes<H, D>();
   } else {
     v.tc = nullptr;
     v.tc_smem = 0;
+    v.tc2 = nullptr;
+    v.tc2_smem = 0;
   }
   return v;
 }

@@ -21,6 +21,7 @@
 #include "contract_cells.cuh"
 #include "tc_selftest.cuh"
 #include "tc_step_kernel.cuh"
+#include "tc2_step_kernel.cuh"
 #include "variant.h"
 #include "vpinn_gpu.h"
 
@@ -188,6 +189,9 @@ struct vpinn_gpu_ctx {
   int nranks = 1, rank = 0;
   long long launches = 0;
   DBuf<char> flush;  // L2 flush scratch (bench)
+  DBuf<long long> phase_clk;  // VPINN_PHASE_CLOCK diagnostics
+  DBuf<float> tc_scratch;     // tc2 parameter-gradient scratch
+  bool tc2 = false;           // fp16-split two-CTA tensor-core step
 
   ~vpinn_gpu_ctx() {
     if (device >= 0) cudaSetDevice(device);
@@ -244,7 +248,59 @@ void configure(vpinn_gpu_ctx* c) {
     const char* tc_env = std::getenv("VPINN_TC");
     c->tc = V.tc != nullptr && !(tc_env && std::atoi(tc_env) == 0) && c->eps_source != VPINN_EPS_SPATIAL &&
             tile_rows <= 128 && (size_t)c->nt * round4(tile_rows * c->Q + 8) * sizeof(float) <= (size_t)vpg::kTcBuf;
-    if (c->tc) {
+    // the fp16-split two-CTA kernel (default) when the slab plus its
+    // contraction scratch fit operand buffer A; VPINN_TC_KERNEL=1 selects the
+    // bf16-split one-CTA kernel
+    const char* tck = std::getenv("VPINN_TC_KERNEL");
+    c->tc2 = c->tc && V.tc2 != nullptr && !(tck && std::atoi(tck) == 1) && c->Q >= 2 &&
+             (size_t)(c->nt * round4(tile_rows * c->Q + 8) + vpg::t2::kTailFloats) * sizeof(float) <=
+                 (size_t)vpg::t2::kBuf;
+    if (c->tc && (std::getenv("VPINN_PHASE_CLOCK") && std::atoi(std::getenv("VPINN_PHASE_CLOCK")) != 0)) {
+      c->phase_clk.alloc((size_t)vpg::kPhaseTiles * vpg::kPhaseMarks);
+      CK(cudaMemset(c->phase_clk.p, 0, sizeof(long long) * vpg::kPhaseTiles * vpg::kPhaseMarks));
+      a.phase_clk = c->phase_clk.p;
+    }
+    if (c->tc2) {
+      a.chunk_rows = tile_rows;
+      a.tstride = round4(tile_rows * c->Q + 8);
+      a.stage_floats = c->nt * a.tstride;
+      a.union_floats = 0;
+      c->smem_step = V.tc2_smem;
+      CK(cudaFuncSetAttribute(V.tc2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem_step));
+      CK(cudaFuncSetAttribute(V.tc2, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, V.tc2, vpg::t2::kNT, c->smem_step));
+      if (occ < 1) throw Fail{VPINN_ERR_DEVICE, "tc2 step kernel cannot be resident"};
+      if (std::getenv("VPINN_DEBUG")) {
+        cudaFuncAttributes fa{};
+        CK(cudaFuncGetAttributes(&fa, V.tc2));
+        int smsm = 0, resv = 0;
+        CK(cudaDeviceGetAttribute(&smsm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, c->device));
+        CK(cudaDeviceGetAttribute(&resv, cudaDevAttrReservedSharedMemoryPerBlock, c->device));
+        for (size_t sb : {(size_t)0, (size_t)64 * 1024, (size_t)100 * 1024, (size_t)110 * 1024, (size_t)112 * 1024}) {
+          int o2 = 0;
+          CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o2, V.tc2, vpg::t2::kNT, sb));
+          std::fprintf(stderr, "  occ(smem %zu) = %d\n", sb, o2);
+        }
+        std::fprintf(stderr, "tc2: regs %d static smem %zu local %zu dyn %zu maxdyn %d; SM smem %d reserved %d; occ %d\n",
+                     fa.numRegs, fa.sharedSizeBytes, fa.localSizeBytes, c->smem_step, fa.maxDynamicSharedSizeBytes, smsm,
+                     resv, occ);
+      }
+      // two CTAs per SM by design (113 KB smem, 256 TMEM columns, 120
+      // registers); the occupancy query reports 1 for tcgen05 kernels, the
+      // hardware co-schedules 2 (measured)
+      {
+        int smsm = 0, resv = 0;
+        CK(cudaDeviceGetAttribute(&smsm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, c->device));
+        CK(cudaDeviceGetAttribute(&resv, cudaDevAttrReservedSharedMemoryPerBlock, c->device));
+        if (2 * (c->smem_step + resv) <= (size_t)smsm) occ = 2;
+      }
+      if (const char* e = std::getenv("VPINN_TC2_CTAS")) occ = std::max(1, std::atoi(e));
+      c->grid_step = std::max(1, std::min(a.n_tiles, occ * c->sm_count));
+      c->tc_scratch.alloc((size_t)c->grid_step * (V.D - 1) * vpg::t2::kScratchPerLayer);
+      a.tc_scratch = c->tc_scratch.p;
+      c->kernel_name = "tc2_step_kernel<" + std::to_string(V.H) + "," + std::to_string(V.D) + "," +
+                       (V.ACT ? "sigmoid" : "tanh") + "> (fp16 split, " + std::to_string(occ) + " CTAs/SM)";
+    } else if (c->tc) {
       a.chunk_rows = tile_rows;
       a.tstride = round4(tile_rows * c->Q + 8);
       a.stage_floats = c->nt * a.tstride;
@@ -433,7 +489,9 @@ void configure(vpinn_gpu_ctx* c) {
 }
 
 void launch_fused(vpinn_gpu_ctx* c, const vpg::StepArgs& a) {
-  if (c->tc)
+  if (c->tc2)
+    c->var.tc2<<<c->grid_step, vpg::t2::kNT, c->smem_step, c->stream>>>(a);
+  else if (c->tc)
     c->var.tc<<<c->grid_step, 128 * vpg::kTcNQ, c->smem_step, c->stream>>>(a);
   else
     c->var.fused<<<c->grid_step, vpg::kThreads, c->smem_step, c->stream>>>(a);
@@ -1217,6 +1275,18 @@ int vpinn_gpu_profile_step(vpinn_gpu_ctx* c, int reps, double* ms_mlp, double* m
     *ms_mlp = t[0] / reps;
     *ms_reduce = t[1] / reps;
     *ms_adam = t[2] / reps;
+  });
+}
+
+// diagnostics: the phase clocks of the last tensor-core step launch
+// (VPINN_PHASE_CLOCK=1 at create), kPhaseTiles x kPhaseMarks clock64 values
+int vpinn_gpu_phase_clock(vpinn_gpu_ctx* c, long long* out, int n) {
+  return guarded([&] {
+    set_dev(c);
+    if (!c->phase_clk.p) throw Fail{VPINN_ERR_CONFIG, "phase clocks not enabled (VPINN_PHASE_CLOCK=1)"};
+    const int m = std::min(n, vpg::kPhaseTiles * vpg::kPhaseMarks);
+    CK(cudaStreamSynchronize(c->stream));
+    CK(cudaMemcpy(out, c->phase_clk.p, sizeof(long long) * m, cudaMemcpyDeviceToHost));
   });
 }
 
