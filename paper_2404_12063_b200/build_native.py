@@ -51,7 +51,10 @@ def _compile(cmd):
     return cmd, r.returncode, r.stdout + r.stderr
 
 
-def build(verbose: bool = False, jobs: int | None = None) -> str:
+def build(verbose: bool = False, jobs: int | None = None, force: bool = False) -> str:
+    # diagnostics builds (e.g. VPINN_EXTRA_NVCC=-DVPG_PHASE_CLOCK=1) rebuild everything
+    extra = os.environ.get("VPINN_EXTRA_NVCC", "").split()
+    force = force or bool(extra)
     os.makedirs(OBJ, exist_ok=True)
     os.makedirs(LIB_DIR, exist_ok=True)
     hdr_mtime = max([os.path.getmtime(h) for h in _headers()] + [0.0])
@@ -61,14 +64,14 @@ def build(verbose: bool = False, jobs: int | None = None) -> str:
     for s in cu:
         o = os.path.join(OBJ, os.path.basename(s) + ".o")
         objs.append(o)
-        if _stale(s, o, hdr_mtime):
-            cmds.append([NVCC, "-std=c++20", *ARCH, "-O3", "-lineinfo", "-Xptxas", "-v",
+        if force or _stale(s, o, hdr_mtime):
+            cmds.append([NVCC, "-std=c++20", *ARCH, "-O3", "-lineinfo", "-Xptxas", "-v", *extra,
                          "-Xcompiler", "-fPIC", "-Xcompiler", "-ffp-contract=off",
                          "--expt-relaxed-constexpr", *INCLUDES, "-c", s, "-o", o])
     for s in cpp:
         o = os.path.join(OBJ, os.path.basename(s) + ".o")
         objs.append(o)
-        if _stale(s, o, hdr_mtime):
+        if force or _stale(s, o, hdr_mtime):
             cmds.append([CXX, "-std=c++20", "-O2", "-fPIC", "-ffp-contract=off", "-Wall",
                          "-Wno-unused-parameter", *INCLUDES, "-I/usr/local/cuda/include",
                          "-c", s, "-o", o])
@@ -80,7 +83,7 @@ def build(verbose: bool = False, jobs: int | None = None) -> str:
                 if rc != 0:
                     raise RuntimeError(f"native build failed: {cmd[-3]}")
     newest = max(os.path.getmtime(o) for o in objs)
-    if not os.path.exists(LIB) or os.path.getmtime(LIB) < newest:
+    if force or not os.path.exists(LIB) or os.path.getmtime(LIB) < newest:
         link = [NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-ldl", "-lpthread"]
         r = subprocess.run(link, capture_output=True, text=True)
         if r.returncode != 0:
@@ -89,4 +92,4 @@ def build(verbose: bool = False, jobs: int | None = None) -> str:
 
 
 if __name__ == "__main__":
-    print(build(verbose="-v" in sys.argv))
+    print(build(verbose="-v" in sys.argv, force="--force" in sys.argv))

@@ -106,8 +106,9 @@ struct Act<kActTanh> {
     p = fmaf(p, x2, 0.1333326813390213f);
     p = fmaf(p, x2, -0.3333333262496359f);
     const float small = fmaf(x * x2, p, x);
-    // |x| >= 9 gives 1.0f exactly; the clamp keeps e finite for the Newton step
-    const float e = ex2_approx(fminf(ax, 9.0f) * 2.8853900817779268f);
+    // |x| >= 9.1 rounds to 1.0f (as the correctly rounded tanh does); the
+    // clamp at 15 keeps e finite for the Newton step
+    const float e = ex2_approx(fminf(ax, 15.0f) * 2.8853900817779268f);
     const float big = fmaf(-2.0f, rcp_newton(e + 1.0f), 1.0f);
     return ax < 0.4f ? small : copysignf(big, x);
   }

@@ -12,13 +12,14 @@
 // (s = value / x-tangent / y-tangent stream).
 //
 // Precision.  Every operand is scaled by a power of two and split into two
-// fp16 parts (tc_utils.cuh st_split8_h): 22 significant bits, three products
+// fp16 parts (tc_utils.cuh st_split8_ho): 22 significant bits, three products
 // Ah.Bh + Ah.Bl + Al.Bh per fp32 product, accumulated in fp32 in TMEM, i.e.
 // fp32-faithful.  The scales are derived from rigorous magnitude BOUNDS, not
 // from the data, so no reduction sits on the critical path:
 //   weights W_l              max |W_l|                                 (per CTA)
 //   value stream z           |z| <= 1 (tanh / sigmoid outputs, the constant-one bias column)
-//   tangent streams TX_h     |TX_1| <= max|w0|, |TX_{h+1}| <= R_h |TX_h|, R_h = max row abs-sum of W_h
+//   tangent streams TX_h     |TX_1| <= max|w0|, |TX_{h+1}| <= R_h |TX_h|, R_h = max row abs-sum
+//                            of W_h (one bound for the x and y tangents)
 //   adjoints (reverse)       from the tile maxima of (ub, uxb, uyb) through
 //                            |s1| <= 1, |kap| <= 2 and the column abs-sums of W_h
 // A loose bound costs nothing measurable: fp16 keeps 2^-24 absolute spacing
@@ -26,17 +27,25 @@
 // three streams with different scales, so the G scales are chosen to make
 // S_G,s * S_X,s one common power of two P per tile; its TMEM accumulator is
 // read out and unscaled every tile (per-CTA fp32 scratch in global memory).
+// All scale factors are folded into per-layer / per-tile constants.
 //
 // Shape: 256 threads (8 warps): thread t owns point p = t % 128 (its TMEM
-// lane) and hidden units [16 (t / 128), +16), processed in chunks of 8.  ~112
-// KB shared memory and 256 TMEM columns per CTA, so TWO CTAs share an SM and
-// one CTA's MMA / barrier / TMA waits are filled by the other's elementwise
-// work.  Hidden layers D in {2, 3}, H <= 31, one output channel.  The slab
-// (the tile's premultipliers, cp.async.bulk) aliases operand buffer A.
+// lane) and hidden units [16 (t / 128), +16), processed in chunks of 8.
+// Every unit runs the same branch-free code: the constant-one (bias) column H
+// is a unit with zero weights and bias 20 (act(20) == 1 exactly, act' == 0),
+// padding units have zero weights.  ~112 KB shared memory and 256 TMEM
+// columns per CTA, so TWO CTAs share an SM and one CTA's MMA / barrier / TMA
+// waits are filled by the other's elementwise work.  Hidden layers D in
+// {2, 3}, H <= 31, one output channel.  The slab (the tile's premultipliers,
+// cp.async.bulk) aliases operand buffer A.
 #pragma once
 
 #include "step_kernel.cuh"
 #include "tc_utils.cuh"
+
+#ifndef VPG_PHASE_CLOCK
+#define VPG_PHASE_CLOCK 0  // build with -DVPG_PHASE_CLOCK=1 for tools/phase_clock.py
+#endif
 
 namespace vpg {
 namespace t2 {
@@ -51,6 +60,7 @@ constexpr int kDCols = 32;            // stream accumulator columns
 constexpr int kG0 = 96;               // parameter-gradient accumulators: 64 columns per MMA layer
 constexpr int kScratchPerLayer = 64 * 64;  // global fp32 [col 64][lane 64] per CTA and MMA layer
 constexpr int kTailFloats = 8 * 128;  // contraction scratch after the slab in buffer A
+constexpr float kOneBias = 20.0f;     // bias of the constant-one unit: act(20) == 1.0f
 
 // exchange rows ([row][128] floats); the output-layer partials of unit half 1
 // (u, ux, uy) alias the adjoint rows, which are written only later
@@ -60,18 +70,21 @@ constexpr int kPu = kUb;
 // per-warp running sums of the CUDA-core gradients: W0x | W0y | b0 | Wd (16 units each)
 enum : int { kAW0x = 0, kAW0y = 16, kAB0 = 32, kAWd = 48, kAccW = 64 };
 
-// uniform scale constants (floats in S_SC)
+// uniform constants (floats in S_SC)
 enum : int {
-  kScInvW = 0,      // [2] 2^-kW per MMA layer
-  kScFwd = 2,       // [2][3] forward unscale 2^-(kX + kW)
-  kScBx = 8,        // [4] tangent bounds b_x of hidden 1..D outputs
-  kScBy = 12,       // [4]
-  kScC = 16,        // [2] max column abs-sum of W_l
-  kScWd = 18,       // max |wd|
-  kScN = 24
+  kScF0 = 0,   // [2] value-stream forward unscale 2^-(kXv + kW) of MMA layer l
+  kScF1 = 2,   // [2] tangent-stream forward unscale 2^-(kXt + kW)
+  kScSv = 4,   // [2] value-stream scale 2^kXv of X_l (input of MMA layer l)
+  kScSt = 6,   // [2] tangent-stream scale 2^kXt
+  kScIt = 8,   // [2] 2^-kXt
+  kScIv = 10,  // [2] 2^-kXv
+  kScBt = 12,  // [4] tangent bounds of hidden 1..D outputs
+  kScC = 16,   // [2] max column abs-sum of W_l
+  kScWd = 18,  // max |wd|
+  kScN = 20
 };
-// integer exponents (ints in S_SCI)
-enum : int { kSiW = 0, kSiX = 2, kSiN = 8 };  // kW[2], kX[2][3]
+// integer exponents (ints in S_SCI): kW[2], kXv[2], kXt[2]
+enum : int { kSiW = 0, kSiXv = 2, kSiXt = 4, kSiN = 6 };
 
 template <int D>
 struct Lay {
@@ -81,7 +94,8 @@ struct Lay {
   static constexpr int OFF_SMALL = OFF_B + kBuf;
   // small region, in floats
   static constexpr int S_W0 = 0;                       // [32][4] (w_x, w_y, b, 0)
-  static constexpr int S_BIAS = S_W0 + 128;            // [2][32]
+  static constexpr int S_W0S = S_W0 + 128;             // [32][2] (w_x, w_y) * 2^kXt of X_1
+  static constexpr int S_BIAS = S_W0S + 64;            // [2][32]
   static constexpr int S_WD = S_BIAS + 64;             // [32] + output bias at 32 (40)
   static constexpr int S_EX = S_WD + 40;               // [kRows][128]
   static constexpr int S_ACC = S_EX + kRows * 128;     // [8 warps][kAccW]
@@ -92,7 +106,7 @@ struct Lay {
   static constexpr int S_BAR = S_MAX + 16;             // 4 mbarriers + TMEM slot
   static constexpr int S_END = S_BAR + 12;
   static constexpr size_t BYTES = (size_t)OFF_SMALL + sizeof(float) * S_END;
-  static_assert(S_RED % 2 == 0 && S_BAR % 2 == 0, "8-byte alignment");
+  static_assert(S_RED % 2 == 0 && S_BAR % 2 == 0 && S_W0 % 4 == 0, "alignment");
 };
 
 // S_MAX words: tile maxima of |ub|, |uxb|, |uyb|; max |w0x|, |w0y|, |wd|; per MMA
@@ -135,6 +149,7 @@ __device__ __forceinline__ int rs8_index(int lane) { return ((lane >> 4) & 1) * 
 __device__ __forceinline__ void atomic_max_abs(uint32_t* w, float v) {
   atomicMax(w, __float_as_uint(fabsf(v)));  // non-negative floats order as their bits (NaN: largest)
 }
+__device__ __forceinline__ int clamp_exp(int k) { return max(-60, min(60, k)); }
 
 }  // namespace t2
 
@@ -148,9 +163,9 @@ __global__ void __maxnreg__(120) tc2_step_kernel(const StepArgs a) {
 
   if (a.stop_flag != nullptr && *a.stop_flag != 0) return;
 
-  extern __shared__ __align__(1024) char t2_raw[];
   // the swizzled operand tiles need a 1024-byte aligned base; the dynamic
   // window starts aligned (no static shared memory), checked here
+  extern __shared__ __align__(1024) char t2_raw[];
   if ((smem_u32(t2_raw) & 1023u) != 0u) __trap();
   char* sm = t2_raw;
   char* sWB = sm;
@@ -158,6 +173,7 @@ __global__ void __maxnreg__(120) tc2_step_kernel(const StepArgs a) {
   char* bufB = sm + LY::OFF_B;
   float* sf = reinterpret_cast<float*>(sm + LY::OFF_SMALL);
   float* sW0 = sf + LY::S_W0;
+  float* sW0s = sf + LY::S_W0S;
   float* sBias = sf + LY::S_BIAS;
   float* sWd = sf + LY::S_WD;
   float* sEx = sf + LY::S_EX;
@@ -192,7 +208,7 @@ __global__ void __maxnreg__(120) tc2_step_kernel(const StepArgs a) {
   if (tid < 16) sMax[tid] = 0u;
   for (int i = tid; i < 8 * kAccW; i += kNT) sAcc[i] = 0.f;
   for (int i = tid; i < 32; i += kNT) {
-    float w0 = 0.f, w1 = 0.f, b = 0.f, wd = 0.f;
+    float w0 = 0.f, w1 = 0.f, b = (i == H) ? kOneBias : 0.f, wd = 0.f;
     if (i < H) {
       w0 = P[net.w_off[0] + 2 * i];
       w1 = P[net.w_off[0] + 2 * i + 1];
@@ -207,7 +223,8 @@ __global__ void __maxnreg__(120) tc2_step_kernel(const StepArgs a) {
   }
   if (tid == 0) sWd[32] = P[net.b_off[D]];
   for (int l = 1; l <= NL; ++l)
-    for (int o = tid; o < 32; o += kNT) sBias[(l - 1) * 32 + o] = o < H ? P[net.b_off[l] + o] : 0.f;
+    for (int o = tid; o < 32; o += kNT)
+      sBias[(l - 1) * 32 + o] = o < H ? P[net.b_off[l] + o] : ((o == H) ? kOneBias : 0.f);
   __syncthreads();
   // weight norms (bounds for the scales): max |w0x|, |w0y|, |wd|; per MMA
   // layer max |W|, max row abs-sum R, max column abs-sum C
@@ -238,33 +255,37 @@ __global__ void __maxnreg__(120) tc2_step_kernel(const StepArgs a) {
   }
   __syncthreads();
   if (tid == 0) {
-    // forward tangent bounds b_x[h], b_y[h] of hidden 1..D outputs
-    float bx = __uint_as_float(sNorm[0]), by = __uint_as_float(sNorm[1]);
-    sSc[kScBx] = bx;
-    sSc[kScBy] = by;
+    // forward tangent bounds of hidden 1..D outputs (x and y together)
+    float bt = fmaxf(__uint_as_float(sNorm[0]), __uint_as_float(sNorm[1]));
+    sSc[kScBt] = bt;
     for (int h = 1; h < D; ++h) {
-      const float R = __uint_as_float(s_lnorm[h - 1][1]);
-      bx *= R;
-      by *= R;
-      sSc[kScBx + h] = bx;
-      sSc[kScBy + h] = by;
+      bt *= __uint_as_float(s_lnorm[h - 1][1]);
+      sSc[kScBt + h] = bt;
     }
     for (int l = 0; l < NL; ++l) {
-      const int kw = max(-60, min(60, 14 - tc::bound_exp(__uint_as_float(s_lnorm[l][0]))));
+      const int kw = clamp_exp(14 - tc::bound_exp(__uint_as_float(s_lnorm[l][0])));
+      // X_{l+1} (input of MMA layer l+1 = hidden l+1 output): value bound 1,
+      // tangent bound bt[l]
+      const int kxv = clamp_exp(14 - tc::bound_exp(1.0f));
+      const int kxt = clamp_exp(14 - tc::bound_exp(sSc[kScBt + l]));
       sSci[kSiW + l] = kw;
-      sSc[kScInvW + l] = tc::exp2i(-kw);
+      sSci[kSiXv + l] = kxv;
+      sSci[kSiXt + l] = kxt;
+      sSc[kScF0 + l] = tc::exp2i(-(kxv + kw));
+      sSc[kScF1 + l] = tc::exp2i(-(kxt + kw));
+      sSc[kScSv + l] = tc::exp2i(kxv);
+      sSc[kScSt + l] = tc::exp2i(kxt);
+      sSc[kScIv + l] = tc::exp2i(-kxv);
+      sSc[kScIt + l] = tc::exp2i(-kxt);
       sSc[kScC + l] = __uint_as_float(s_lnorm[l][2]);
-      // input of MMA layer l+1 = hidden l+1 output: value bound 1, tangents b_x/b_y[l]
-      const float bnd[3] = {1.0f, sSc[kScBx + l], sSc[kScBy + l]};
-      for (int s = 0; s < 3; ++s) {
-        const int kx = max(-60, min(60, 14 - tc::bound_exp(bnd[s])));
-        sSci[kSiX + 3 * l + s] = kx;
-        sSc[kScFwd + 3 * l + s] = tc::exp2i(-(kx + kw));
-      }
     }
     sSc[kScWd] = __uint_as_float(sNorm[2]);
   }
   __syncthreads();
+  for (int i = tid; i < 32; i += kNT) {  // layer-0 tangent weights pre-scaled for X_1
+    sW0s[2 * i] = sW0[4 * i] * sSc[kScSt];
+    sW0s[2 * i + 1] = sW0[4 * i + 1] * sSc[kScSt];
+  }
   // W tiles, scaled by 2^kW: row o of part h at rows 0..31, part l at rows 32..63
   for (int l = 1; l <= NL; ++l) {
     char* wb = sWB + (l - 1) * kWBytes;
@@ -287,6 +308,8 @@ __global__ void __maxnreg__(120) tc2_step_kernel(const StepArgs a) {
   const uint32_t tmem = *tslot;
   const uint32_t lane_q = (uint32_t)(32 * (warp & 3)) << 16;  // TMEM lane quarter of this warp
   const uint32_t sA = smem_u32(bufA), sB = smem_u32(bufB), sW = smem_u32(sWB);
+  // swizzled byte offsets of this thread's two 8-unit chunks in a [128][32] fp16 tile
+  const uint32_t off0 = tc::sw_chunk(p, 2 * hh), off1 = tc::sw_chunk(p, 2 * hh + 1);
 
   // ---------------- MMA issue (thread 0) ----------------
   // point GEMM of MMA layer l (forward, or propagation with B MN-major): the
@@ -340,41 +363,31 @@ __global__ void __maxnreg__(120) tc2_step_kernel(const StepArgs a) {
     tc::fence_after_sync();
   };
   auto dcol = [&](int s, int c) { return tmem + lane_q + kDCols * s + u0 + 8 * c; };
+  auto coff = [&](int c) { return c ? off1 : off0; };
 
-  // layer 0 of this thread's chunk c (8 units) at (px, py)
-  auto layer0 = [&](int c, float px, float py, float (&z)[8], float (&tx)[8], float (&ty)[8]) {
+  // layer 0 of this thread's chunk c (8 units) at (px, py): z and s1
+  auto layer0 = [&](int c, float px, float py, float (&z)[8], float (&s1)[8]) {
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
-      const int u = u0 + 8 * c + k;
-      const float4 w = *reinterpret_cast<const float4*>(sW0 + 4 * u);
-      if (u < H) {
-        const float zz = AC::value(fmaf(w.y, py, w.x * px) + w.z);
-        const float s1 = AC::s1(zz);
-        z[k] = zz;
-        tx[k] = s1 * w.x;
-        ty[k] = s1 * w.y;
-      } else {
-        z[k] = (u == H) ? 1.0f : 0.0f;  // constant-one column -> bias gradient
-        tx[k] = 0.f;
-        ty[k] = 0.f;
-      }
+      const float4 w = *reinterpret_cast<const float4*>(sW0 + 4 * (u0 + 8 * c + k));
+      z[k] = AC::value(fmaf(w.y, py, w.x * px) + w.z);
+      s1[k] = AC::s1(z[k]);
     }
   };
-  // store the three streams of chunk c with scales s[3] into buffer buf
-  auto store3 = [&](char* buf, int c, const float (&z)[8], const float (&tx)[8], const float (&ty)[8], float s0,
-                    float s1, float s2) {
-    const int ch = 2 * hh + c;
-    tc::st_split8_h(buf, kPart, p, ch, z, s0);
-    tc::st_split8_h(buf + kStream, kPart, p, ch, tx, s1);
-    tc::st_split8_h(buf + 2 * kStream, kPart, p, ch, ty, s2);
-  };
-  // the three streams of chunk c read back from buffer buf (unscaled)
-  auto load3 = [&](const char* buf, int c, float (&z)[8], float (&tx)[8], float (&ty)[8], float i0, float i1,
-                   float i2) {
-    const int ch = 2 * hh + c;
-    tc::ld_join8_h(buf, kPart, p, ch, i0, z);
-    tc::ld_join8_h(buf + kStream, kPart, p, ch, i1, tx);
-    tc::ld_join8_h(buf + 2 * kStream, kPart, p, ch, i2, ty);
+  // X_1 (hidden-1 output) of chunk c, scaled, into buffer buf
+  auto store_x1 = [&](char* buf, int c, float px, float py) {
+    float z[8], s1[8], tx[8], ty[8];
+    layer0(c, px, py, z, s1);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const float2 ws = *reinterpret_cast<const float2*>(sW0s + 2 * (u0 + 8 * c + k));
+      tx[k] = s1[k] * ws.x;
+      ty[k] = s1[k] * ws.y;
+    }
+    const uint32_t o = coff(c);
+    tc::st_split8_ho<true>(buf, kPart, o, z, sSc[kScSv]);
+    tc::st_split8_ho<false>(buf + kStream, kPart, o, tx, 1.f);
+    tc::st_split8_ho<false>(buf + 2 * kStream, kPart, o, ty, 1.f);
   };
   // running per-warp sums of 8 unit values (units u0 + 8c + k) at slot base
   auto acc_units = [&](float (&v)[8], int slot, int c) {
@@ -384,9 +397,9 @@ __global__ void __maxnreg__(120) tc2_step_kernel(const StepArgs a) {
 
   bool first_tile = true;
   int kP_prev0 = 0, kP_prev1 = 0;  // param-grad product scale exponents of the last tile
-  // read the previous tile's parameter-gradient accumulators into the
-  // per-CTA fp32 scratch ([col][lane], unscaled by 2^-kP); warps of lane
-  // quarters 0 / 1 (G rows h / l), unit half = X part h / l
+  // read the last tile's parameter-gradient accumulators into the per-CTA
+  // fp32 scratch ([col][lane], unscaled by 2^-kP); warps of lane quarters
+  // 0 / 1 (G rows h / l), unit half = X part h / l
   auto param_readout = [&](bool first) {
     if ((warp & 3) >= 2) return;
     const int lrow = 32 * (warp & 1) + lane;  // G row (part * 32 + o)
@@ -410,11 +423,13 @@ __global__ void __maxnreg__(120) tc2_step_kernel(const StepArgs a) {
     }
   };
 
-  // diagnostics: phase clocks of CTA 0 (StepArgs::phase_clk)
+  // diagnostics: phase clocks of CTA 0 (StepArgs::phase_clk, -DVPG_PHASE_CLOCK=1)
   int ph_tile = 0;
   auto mark = [&](int i) {
-    if (a.phase_clk != nullptr && blockIdx.x == 0 && tid == 0 && ph_tile < kPhaseTiles)
-      a.phase_clk[ph_tile * kPhaseMarks + i] = clock64();
+    if constexpr (VPG_PHASE_CLOCK != 0) {
+      if (a.phase_clk != nullptr && blockIdx.x == 0 && tid == 0 && ph_tile < kPhaseTiles)
+        a.phase_clk[ph_tile * kPhaseMarks + i] = clock64();
+    }
   };
 
   double acc_v = 0.0, acc_b = 0.0, acc_s = 0.0, acc_eg = 0.0;  // thread 0
@@ -480,15 +495,8 @@ __global__ void __maxnreg__(120) tc2_step_kernel(const StepArgs a) {
 
     // =================== forward ===================
     char* x1buf = (D == 3) ? bufA : bufB;  // hidden-1 output (input of MMA layer 1)
-    {
-      const float s0 = tc::exp2i(sSci[kSiX + 0]), s1 = tc::exp2i(sSci[kSiX + 1]), s2 = tc::exp2i(sSci[kSiX + 2]);
 #pragma unroll 1
-      for (int c = 0; c < 2; ++c) {
-        float z[8], tx[8], ty[8];
-        layer0(c, px, py, z, tx, ty);
-        store3(x1buf, c, z, tx, ty, s0, s1, s2);
-      }
-    }
+    for (int c = 0; c < 2; ++c) store_x1(x1buf, c, px, py);
     operands_ready();
     if (tid == 0) issue_point_gemm(smem_u32(x1buf), 1, false);
     mark(1);
@@ -499,9 +507,10 @@ __global__ void __maxnreg__(120) tc2_step_kernel(const StepArgs a) {
 #pragma unroll 1
     for (int l = 1; l <= NL; ++l) {
       const bool last = l == NL;
-      char* nbuf = bufB;  // hidden-2 output (D == 3) -> buffer B
-      const float f0 = sSc[kScFwd + 3 * (l - 1)], f1 = sSc[kScFwd + 3 * (l - 1) + 1],
-                  f2 = sSc[kScFwd + 3 * (l - 1) + 2];
+      const float f0 = sSc[kScF0 + l - 1];
+      // tangent factor: forward unscale, times the X_{l+1} scale when stored
+      const float ft = last ? sSc[kScF1 + l - 1] : sSc[kScF1 + l - 1] * sSc[kScSt + l];
+      const float sv = last ? 1.f : sSc[kScSv + l];
       const float* bias = sBias + 32 * (l - 1);
       float s1v[16];
       wait_bar(bar_v, ph_v);
@@ -512,12 +521,11 @@ __global__ void __maxnreg__(120) tc2_step_kernel(const StepArgs a) {
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
           const int u = u0 + 8 * c + k;
-          const float zz = (u < H) ? AC::value(fmaf(d[k], f0, bias[u])) : ((u == H) ? 1.0f : 0.0f);
-          z[k] = zz;
-          s1v[8 * c + k] = (u < H) ? AC::s1(zz) : 0.f;
-          if (last && u < H) ou = fmaf(sWd[u], zz, ou);
+          z[k] = AC::value(fmaf(d[k], f0, bias[u]));
+          s1v[8 * c + k] = AC::s1(z[k]) * ft;
+          if (last) ou = fmaf(sWd[u], z[k], ou);
         }
-        if (!last) tc::st_split8_h(nbuf, kPart, p, 2 * hh + c, z, tc::exp2i(sSci[kSiX + 3 * l]));
+        if (!last) tc::st_split8_ho<true>(bufB, kPart, coff(c), z, sv);
       }
       wait_bar(bar_t, ph_t);
       // D == 3: buffer A (slab) is free once MMA layer 1 is done
@@ -527,20 +535,21 @@ __global__ void __maxnreg__(120) tc2_step_kernel(const StepArgs a) {
       for (int c = 0; c < 2; ++c) {
         float dx[8], dy[8];
         tc::tmem_ld2x8_wait(dcol(1, c), dcol(2, c), dx, dy);
+        if (last) {
 #pragma unroll
-        for (int k = 0; k < 8; ++k) {
-          dx[k] = s1v[8 * c + k] * (dx[k] * f1);
-          dy[k] = s1v[8 * c + k] * (dy[k] * f2);
-          const int u = u0 + 8 * c + k;
-          if (last && u < H) {
-            oux = fmaf(sWd[u], dx[k], oux);
-            ouy = fmaf(sWd[u], dy[k], ouy);
+          for (int k = 0; k < 8; ++k) {
+            const float w = sWd[u0 + 8 * c + k] * s1v[8 * c + k];
+            oux = fmaf(w, dx[k], oux);
+            ouy = fmaf(w, dy[k], ouy);
           }
-        }
-        if (!last) {
-          const int ch = 2 * hh + c;
-          tc::st_split8_h(nbuf + kStream, kPart, p, ch, dx, tc::exp2i(sSci[kSiX + 3 * l + 1]));
-          tc::st_split8_h(nbuf + 2 * kStream, kPart, p, ch, dy, tc::exp2i(sSci[kSiX + 3 * l + 2]));
+        } else {
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            dx[k] *= s1v[8 * c + k];
+            dy[k] *= s1v[8 * c + k];
+          }
+          tc::st_split8_ho<false>(bufB + kStream, kPart, coff(c), dx, 1.f);
+          tc::st_split8_ho<false>(bufB + 2 * kStream, kPart, coff(c), dy, 1.f);
         }
       }
       if (!last) {
@@ -714,69 +723,64 @@ __global__ void __maxnreg__(120) tc2_step_kernel(const StepArgs a) {
     const float ub = sEx[kUb * 128 + p], uxb = sEx[kUxb * 128 + p], uyb = sEx[kUyb * 128 + p];
 
     // =================== reverse ===================
-    // adjoint bounds of G at the last hidden layer
+    // magnitude bounds of G at the last hidden layer (value | tangents)
     const float Mb = __uint_as_float(sMax[kMb]), Mx = __uint_as_float(sMax[kMx]), My = __uint_as_float(sMax[kMy]);
     const float Wd = sSc[kScWd];
-    float bG[3] = {Wd * (Mb + kapmax * (sSc[kScBx + D - 1] * Mx + sSc[kScBy + D - 1] * My)), Wd * Mx, Wd * My};
-    // G scales for param layer l: S_G,s = 2^(kP - kX[l-1][s]) with the
-    // common product exponent kP = min_s (14 - e(B_s) + kX[l-1][s])
-    int kP0 = 0, kP1 = 0;
-    auto g_scales = [&](int l, const float (&bnd)[3], float (&sg)[3], float (&pu)[3]) {
+    float bGv = Wd * (Mb + kapmax * sSc[kScBt + D - 1] * (Mx + My));
+    float bGt = Wd * fmaxf(Mx, My);
+    // G scales for param layer l: S_G,s = 2^(kP - kX_s) with the common
+    // product exponent kP = min_s (14 - e(B_s) + kX_s); returns kP
+    auto g_scales = [&](int l, float bv, float bt, float& sgv, float& sgt, float& puv, float& put) {
+      const int kxv = sSci[kSiXv + l - 1], kxt = sSci[kSiXt + l - 1], kw = sSci[kSiW + l - 1];
+      const int ev = tc::bound_exp(bv), et = tc::bound_exp(bt);
       int kp = 1 << 20;
-#pragma unroll
-      for (int s = 0; s < 3; ++s) {
-        const int e = tc::bound_exp(bnd[s]);
-        if (e > -1000) kp = min(kp, 14 - e + sSci[kSiX + 3 * (l - 1) + s]);
-      }
-      if (kp == (1 << 20)) kp = sSci[kSiX + 3 * (l - 1)];
+      if (ev > -1000) kp = min(kp, 14 - ev + kxv);
+      if (et > -1000) kp = min(kp, 14 - et + kxt);
+      if (kp == (1 << 20)) kp = kxv;
       kp = max(-120, min(120, kp));
-      if (l == 1) kP0 = kp; else kP1 = kp;
-#pragma unroll
-      for (int s = 0; s < 3; ++s) {
-        const int kg = kp - sSci[kSiX + 3 * (l - 1) + s];
-        sg[s] = tc::exp2i(kg);
-        pu[s] = tc::exp2i(-(kg + sSci[kSiW + l - 1]));  // propagation unscale
-      }
+      sgv = tc::exp2i(kp - kxv);
+      sgt = tc::exp2i(kp - kxt);
+      puv = tc::exp2i(-(kp - kxv + kw));  // propagation unscale
+      put = tc::exp2i(-(kp - kxt + kw));
+      return kp;
     };
-    float sg[3], pu[3];
-    g_scales(NL, bG, sg, pu);
-    // ---- output layer: Wbar_out, bbar_out (unit H: z == 1), G of the last hidden layer ----
+    int kP0 = 0, kP1 = 0;
+    float sgv, sgt, puv, put;
     {
-      const int lw = NL;  // MMA layer whose accumulators hold the last hidden pre-activations
-      const float f0 = sSc[kScFwd + 3 * (lw - 1)], f1 = sSc[kScFwd + 3 * (lw - 1) + 1],
-                  f2 = sSc[kScFwd + 3 * (lw - 1) + 2];
-      const float* bias = sBias + 32 * (lw - 1);
+      const int kp = g_scales(NL, bGv, bGt, sgv, sgt, puv, put);
+      if (NL == 1) kP0 = kp; else kP1 = kp;
+    }
+    // ---- output layer: Wbar_out, bbar_out (unit H: z == 1), G of the last hidden layer ----
+    // the last hidden state is recomputed from MMA layer NL's accumulators
+    {
+      const float f0 = sSc[kScF0 + NL - 1], f1 = sSc[kScF1 + NL - 1];
+      const float* bias = sBias + 32 * (NL - 1);
+      const float Ub = ub * sgv, Uxv = uxb * sgv, Uyv = uyb * sgv, Uxt = uxb * sgt, Uyt = uyb * sgt;
 #pragma unroll 1
       for (int c = 0; c < 2; ++c) {
         float d0[8], dx[8], dy[8];
-        {
-          float t0[8];
-          tc::tmem_ld1x8_wait(dcol(0, c), t0);
-#pragma unroll
-          for (int k = 0; k < 8; ++k) d0[k] = t0[k];
-        }
+        tc::tmem_ld1x8_wait(dcol(0, c), d0);
         tc::tmem_ld2x8_wait(dcol(1, c), dcol(2, c), dx, dy);
         float v[8], gA[8], gX[8], gY[8];
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
           const int u = u0 + 8 * c + k;
-          if (u < H) {
-            const float z = AC::value(fmaf(d0[k], f0, bias[u]));
-            const float s1 = AC::s1(z), kp = AC::kap(z);
-            const float tx = s1 * (dx[k] * f1), ty = s1 * (dy[k] * f2);
-            v[k] = fmaf(uyb, ty, fmaf(uxb, tx, ub * z));
-            const float wd = sWd[u];
-            const float xb = wd * ub, zx = wd * uxb, zy = wd * uyb;
-            gA[k] = fmaf(s1, xb, kp * fmaf(tx, zx, ty * zy));
-            gX[k] = s1 * zx;
-            gY[k] = s1 * zy;
-          } else {
-            v[k] = (u == H) ? ub : 0.f;
-            gA[k] = gX[k] = gY[k] = 0.f;
-          }
+          const float z = AC::value(fmaf(d0[k], f0, bias[u]));
+          const float s1 = AC::s1(z), kp = AC::kap(z);
+          const float cc = s1 * f1;
+          const float tx = cc * dx[k], ty = cc * dy[k];
+          v[k] = fmaf(ub, z, fmaf(uxb, tx, uyb * ty));
+          const float wd = sWd[u];
+          gA[k] = wd * fmaf(s1, Ub, kp * fmaf(tx, Uxv, ty * Uyv));
+          const float sw = s1 * wd;
+          gX[k] = sw * Uxt;
+          gY[k] = sw * Uyt;
         }
         acc_units(v, kAWd, c);
-        store3(bufA, c, gA, gX, gY, sg[0], sg[1], sg[2]);
+        const uint32_t o = coff(c);
+        tc::st_split8_ho<false>(bufA, kPart, o, gA, 1.f);
+        tc::st_split8_ho<false>(bufA + kStream, kPart, o, gX, 1.f);
+        tc::st_split8_ho<false>(bufA + 2 * kStream, kPart, o, gY, 1.f);
       }
     }
     operands_ready();
@@ -788,44 +792,43 @@ __global__ void __maxnreg__(120) tc2_step_kernel(const StepArgs a) {
     // ---- hidden layers, last first: G of hidden l from the propagated adjoints ----
 #pragma unroll 1
     for (int l = NL; l >= 1; --l) {
-      // hidden-l state: X_l in buffer B (MMA layer l's input), scales kX[l-1]
-      const float i0 = tc::exp2i(-sSci[kSiX + 3 * (l - 1)]), i1 = tc::exp2i(-sSci[kSiX + 3 * (l - 1) + 1]),
-                  i2 = tc::exp2i(-sSci[kSiX + 3 * (l - 1) + 2]);
-      float bnd2[3];
-      {
-        const float C = sSc[kScC + l - 1];
-        const float bxa = C * bG[0], bxx = C * bG[1], bxy = C * bG[2];
-        bnd2[0] = bxa + kapmax * (sSc[kScBx + l - 1] * bxx + sSc[kScBy + l - 1] * bxy);
-        bnd2[1] = bxx;
-        bnd2[2] = bxy;
+      // hidden-l state: X_l in buffer B (MMA layer l's input)
+      const float iv = sSc[kScIv + l - 1], it = sSc[kScIt + l - 1];
+      // bounds of G at hidden l: propagation through W_l, then the activation
+      const float C = sSc[kScC + l - 1];
+      const float bxa = C * bGv, bxt = C * bGt;
+      const float bv2 = bxa + kapmax * sSc[kScBt + l - 1] * 2.f * bxt, bt2 = bxt;
+      float sgv2 = 1.f, sgt2 = 1.f, puv2 = 1.f, put2 = 1.f;
+      if (l > 1) {
+        const int kp = g_scales(l - 1, bv2, bt2, sgv2, sgt2, puv2, put2);
+        if (l - 1 == 1) kP0 = kp; else kP1 = kp;
       }
-      float sg2[3] = {1.f, 1.f, 1.f}, pu2[3] = {1.f, 1.f, 1.f};
-      if (l > 1) g_scales(l - 1, bnd2, sg2, pu2);
+      // ga = s1 xa' + kap (tx xx' + ty xy'), gx = s1 xx', gy = s1 xy' with the
+      // propagation unscale ('), the state unscale and the store scale folded
+      const float A0 = puv * sgv2, AT = it * put * sgv2, BT = put * sgt2;
       wait_bar(bar_v, ph_v);
       wait_bar(bar_t, ph_t);
       // l > 1: G of hidden l goes to buffer A and the recomputed hidden-1
       // output to buffer B, so param GEMM l must have read both; each thread
-      // reads (its state) and writes exactly its own slots, so no barrier
+      // reads (its state) and writes exactly its own slots: no barrier
       if (l > 1) wait_bar(bar_w, ph_w);
 #pragma unroll 1
       for (int c = 0; c < 2; ++c) {
         float xa[8], xx[8], xy[8], z[8], tx[8], ty[8];
         tc::tmem_ld1x8_wait(dcol(0, c), xa);
         tc::tmem_ld2x8_wait(dcol(1, c), dcol(2, c), xx, xy);
-        load3(bufB, c, z, tx, ty, i0, i1, i2);
+        const uint32_t o = coff(c);
+        tc::ld_join8_ho<true>(bufB, kPart, o, iv, z);
+        tc::ld_join8_ho<false>(bufB + kStream, kPart, o, 1.f, tx);
+        tc::ld_join8_ho<false>(bufB + 2 * kStream, kPart, o, 1.f, ty);
         float ga[8], gx[8], gy[8];
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
-          const int u = u0 + 8 * c + k;
-          if (u < H) {
-            const float s1 = AC::s1(z[k]), kp = AC::kap(z[k]);
-            const float aa = xa[k] * pu[0], ax = xx[k] * pu[1], ay = xy[k] * pu[2];
-            ga[k] = fmaf(s1, aa, kp * fmaf(tx[k], ax, ty[k] * ay));
-            gx[k] = s1 * ax;
-            gy[k] = s1 * ay;
-          } else {
-            ga[k] = gx[k] = gy[k] = 0.f;
-          }
+          const float s1 = AC::s1(z[k]), kp = AC::kap(z[k]);
+          ga[k] = fmaf(s1 * A0, xa[k], (kp * AT) * fmaf(tx[k], xx[k], ty[k] * xy[k]));
+          const float sb = s1 * BT;
+          gx[k] = sb * xx[k];
+          gy[k] = sb * xy[k];
         }
         if (l == 1) {
           // ---- input layer: Wbar_0 += Abar x^T + TAxbar e_x^T + TAybar e_y^T; bbar_0 += Abar ----
@@ -836,14 +839,12 @@ __global__ void __maxnreg__(120) tc2_step_kernel(const StepArgs a) {
 #pragma unroll
           for (int k = 0; k < 8; ++k) v[k] = fmaf(ga[k], py, gy[k]);
           acc_units(v, kAW0y, c);
-#pragma unroll
-          for (int k = 0; k < 8; ++k) v[k] = ga[k];
-          acc_units(v, kAB0, c);
+          acc_units(ga, kAB0, c);
         } else {
-          store3(bufA, c, ga, gx, gy, sg2[0], sg2[1], sg2[2]);
-          layer0(c, px, py, z, tx, ty);  // hidden-1 output recomputed (l - 1 == 1)
-          store3(bufB, c, z, tx, ty, tc::exp2i(sSci[kSiX + 0]), tc::exp2i(sSci[kSiX + 1]),
-                 tc::exp2i(sSci[kSiX + 2]));
+          tc::st_split8_ho<false>(bufA, kPart, o, ga, 1.f);
+          tc::st_split8_ho<false>(bufA + kStream, kPart, o, gx, 1.f);
+          tc::st_split8_ho<false>(bufA + 2 * kStream, kPart, o, gy, 1.f);
+          store_x1(bufB, c, px, py);  // hidden-1 output recomputed (l - 1 == 1)
         }
       }
       if (l > 1) {
@@ -852,11 +853,10 @@ __global__ void __maxnreg__(120) tc2_step_kernel(const StepArgs a) {
           issue_point_gemm(sA, l - 1, true);
           issue_param_gemm(l - 1);
         }
-#pragma unroll
-        for (int s = 0; s < 3; ++s) {
-          bG[s] = bnd2[s];
-          pu[s] = pu2[s];
-        }
+        bGv = bv2;
+        bGt = bt2;
+        puv = puv2;
+        put = put2;
       }
       mark(9 + NL - l + 1);
     }

@@ -141,6 +141,33 @@ __device__ __forceinline__ void st_split8_h(char* base, uint32_t part_stride, in
   *reinterpret_cast<uint4*>(base + off) = make_uint4(h[0], h[1], h[2], h[3]);
   *reinterpret_cast<uint4*>(base + part_stride + off) = make_uint4(l[0], l[1], l[2], l[3]);
 }
+// the same with a precomputed swizzled byte offset; SCALE = false skips the
+// multiply (values already scaled)
+template <bool SCALE>
+__device__ __forceinline__ void st_split8_ho(char* base, uint32_t part_stride, uint32_t off, const float* v, float s) {
+  uint32_t h[4], l[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const float y0 = SCALE ? v[2 * k] * s : v[2 * k], y1 = SCALE ? v[2 * k + 1] * s : v[2 * k + 1];
+    h[k] = pack_f16x2(y0, y1);
+    l[k] = pack_f16x2(y0 - f16lo(h[k]), y1 - f16hi(h[k]));
+  }
+  *reinterpret_cast<uint4*>(base + off) = make_uint4(h[0], h[1], h[2], h[3]);
+  *reinterpret_cast<uint4*>(base + part_stride + off) = make_uint4(l[0], l[1], l[2], l[3]);
+}
+template <bool UNSCALE>
+__device__ __forceinline__ void ld_join8_ho(const char* base, uint32_t part_stride, uint32_t off, float inv_s,
+                                            float* v) {
+  const uint4 h = *reinterpret_cast<const uint4*>(base + off);
+  const uint4 l = *reinterpret_cast<const uint4*>(base + part_stride + off);
+  const uint32_t hw[4] = {h.x, h.y, h.z, h.w}, lw[4] = {l.x, l.y, l.z, l.w};
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const float a0 = f16lo(hw[k]) + f16lo(lw[k]), a1 = f16hi(hw[k]) + f16hi(lw[k]);
+    v[2 * k] = UNSCALE ? a0 * inv_s : a0;
+    v[2 * k + 1] = UNSCALE ? a1 * inv_s : a1;
+  }
+}
 // read back 8 columns as (h + l) * inv_s
 __device__ __forceinline__ void ld_join8_h(const char* base, uint32_t part_stride, int row, int chunk, float inv_s,
                                            float* v) {

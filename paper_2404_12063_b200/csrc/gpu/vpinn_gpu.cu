@@ -73,7 +73,12 @@ struct DBuf {
     release();
     n = count;
     CK(cudaMalloc(&p, std::max<size_t>(count, 1) * sizeof(T) + 64));
+    // cudaMemset runs on the legacy default stream, which does NOT order with
+    // the context's non-blocking stream: finish it before any upload is
+    // enqueued there (else the zero fill can land after, and overwrite, the
+    // upload)
     CK(cudaMemset(p, 0, std::max<size_t>(count, 1) * sizeof(T) + 64));
+    CK(cudaDeviceSynchronize());
   }
   void upload(const T* h, size_t count, cudaStream_t s) {
     if (count) CK(cudaMemcpyAsync(p, h, count * sizeof(T), cudaMemcpyHostToDevice, s));
@@ -257,7 +262,6 @@ void configure(vpinn_gpu_ctx* c) {
                  (size_t)vpg::t2::kBuf;
     if (c->tc && (std::getenv("VPINN_PHASE_CLOCK") && std::atoi(std::getenv("VPINN_PHASE_CLOCK")) != 0)) {
       c->phase_clk.alloc((size_t)vpg::kPhaseTiles * vpg::kPhaseMarks);
-      CK(cudaMemset(c->phase_clk.p, 0, sizeof(long long) * vpg::kPhaseTiles * vpg::kPhaseMarks));
       a.phase_clk = c->phase_clk.p;
     }
     if (c->tc2) {
