@@ -96,6 +96,7 @@ struct StepArgs {
   long long* phase_clk;
   // tc2_step_kernel: per-CTA fp32 parameter-gradient scratch [cta][layer][64][64]
   float* tc_scratch;
+  int tc_force_spill;  // test hook (VPINN_TC2_FORCE_SPILL=1): spill the accumulators every tile
 };
 constexpr int kPhaseTiles = 8, kPhaseMarks = 32;
 

@@ -336,17 +336,24 @@ __global__ void __maxnreg__(120) tc2_step_kernel(const StepArgs a) {
     tc::mma_commit(bar_t);
   };
   // parameter gradient of MMA layer l: G parts in bufA (M blocks h | l | next
-  // stream's parts, unused), X parts in bufB (N = h | l); fresh every tile
-  auto issue_param_gemm = [&](int l) {
+  // stream's parts, unused), X parts in bufB (N = h | l).  Accumulates in
+  // TMEM across the CTA's tiles: fresh (first), or onto the accumulator
+  // scaled down by 2^-shift (scale-input-d) when this tile's product scale is
+  // smaller than the accumulated one
+  auto issue_param_gemm = [&](int l, bool first, int shift) {
     const uint32_t acc = tmem + kG0 + 64 * (l - 1);
     const uint32_t idesc = tc::idesc_f16(128, 64, 1, 1);
 #pragma unroll 1
     for (int s = 0; s < 3; ++s) {
       const uint32_t g = sA + s * kStream, x = sB + s * kStream;
 #pragma unroll
-      for (int kp = 0; kp < 8; ++kp)
-        tc::mma_bf16(acc, tc::mndesc(g + 1024 * kp, kPart), tc::mndesc(x + 1024 * kp, kPart), idesc,
-                     (s == 0 && kp == 0) ? 0u : 1u);
+      for (int kp = 0; kp < 8; ++kp) {
+        const uint64_t ad = tc::mndesc(g + 1024 * kp, kPart), bd = tc::mndesc(x + 1024 * kp, kPart);
+        if (s == 0 && kp == 0 && !first && shift > 0)
+          tc::mma_f16_sd(acc, ad, bd, idesc, shift);
+        else
+          tc::mma_bf16(acc, ad, bd, idesc, (s == 0 && kp == 0 && first) ? 0u : 1u);
+      }
     }
     tc::mma_commit(bar_w);
   };
@@ -395,32 +402,65 @@ __global__ void __maxnreg__(120) tc2_step_kernel(const StepArgs a) {
     if ((lane & 3) == 0) sAcc[warp * kAccW + slot + 8 * c + rs8_index(lane)] += r;
   };
 
-  bool first_tile = true;
-  int kP_prev0 = 0, kP_prev1 = 0;  // param-grad product scale exponents of the last tile
-  // read the last tile's parameter-gradient accumulators into the per-CTA
-  // fp32 scratch ([col][lane], unscaled by 2^-kP); warps of lane quarters
-  // 0 / 1 (G rows h / l), unit half = X part h / l
-  auto param_readout = [&](bool first) {
+  // parameter-gradient accumulators: product scale exponent kacc of what
+  // TMEM holds per MMA layer, and whether it holds anything yet
+  int kacc0 = 0, kacc1 = 0;
+  bool has0 = false, has1 = false, spill0 = false, spill1 = false;
+  // rare path (an accumulator would need more than 2^-15): add the layer-l
+  // accumulator, unscaled, into the per-CTA fp32 scratch ([col][lane]) and
+  // restart it; warps of lane quarters 0 / 1 (G rows h / l), unit half = X
+  // part h / l
+  auto spill_accumulator = [&](int l, int kacc, bool first) {
     if ((warp & 3) >= 2) return;
     const int lrow = 32 * (warp & 1) + lane;  // G row (part * 32 + o)
+    float* S = a.tc_scratch + ((size_t)blockIdx.x * NL + (l - 1)) * kScratchPerLayer;
+    const float inv = tc::exp2i(-kacc);
 #pragma unroll 1
-    for (int l = 0; l < NL; ++l) {
-      float* S = a.tc_scratch + ((size_t)blockIdx.x * NL + l) * kScratchPerLayer;
-      const float inv = tc::exp2i(-(l == 0 ? kP_prev0 : kP_prev1));
-#pragma unroll 1
-      for (int h2 = 0; h2 < 2; ++h2) {
-        const int col0 = 32 * hh + 16 * h2;
-        float old[16];
-        if (!first) {
+    for (int h2 = 0; h2 < 2; ++h2) {
+      const int col0 = 32 * hh + 16 * h2;
+      float v[16];
+      tc::tmem_ld1x16_wait(tmem + lane_q + kG0 + 64 * (l - 1) + col0, v);
 #pragma unroll
-          for (int k = 0; k < 16; ++k) old[k] = S[(col0 + k) * 64 + lrow];
-        }
-        float v[16];
-        tc::tmem_ld1x16_wait(tmem + lane_q + kG0 + 64 * l + col0, v);
-#pragma unroll
-        for (int k = 0; k < 16; ++k) S[(col0 + k) * 64 + lrow] = first ? v[k] * inv : fmaf(v[k], inv, old[k]);
+      for (int k = 0; k < 16; ++k) {
+        float* d = S + (col0 + k) * 64 + lrow;
+        *d = first ? v[k] * inv : fmaf(v[k], inv, *d);
       }
     }
+  };
+  // this tile's product exponent for param layer l: the natural kp_nat, or
+  // the accumulated one when smaller; sets how the GEMM joins the accumulator
+  auto join_acc = [&](int l, int kp_nat, bool& first, int& shift) {
+    const int kacc = (l == 1) ? kacc0 : kacc1;
+    const bool has = (l == 1) ? has0 : has1;
+    bool spill = (l == 1) ? spill0 : spill1;
+    shift = 0;
+    first = false;
+    int kp = kp_nat;
+    if (!has) {
+      first = true;
+    } else if (a.tc_force_spill) {
+      spill_accumulator(l, kacc, !spill);
+      spill = true;
+      first = true;
+    } else if (kp_nat >= kacc) {
+      kp = kacc;
+    } else if (kacc - kp_nat <= 15) {
+      shift = kacc - kp_nat;
+    } else {
+      spill_accumulator(l, kacc, !spill);
+      spill = true;
+      first = true;
+    }
+    if (l == 1) {
+      kacc0 = kp;
+      has0 = true;
+      spill0 = spill;
+    } else {
+      kacc1 = kp;
+      has1 = true;
+      spill1 = spill;
+    }
+    return kp;
   };
 
   // diagnostics: phase clocks of CTA 0 (StepArgs::phase_clk, -DVPG_PHASE_CLOCK=1)
@@ -730,26 +770,25 @@ __global__ void __maxnreg__(120) tc2_step_kernel(const StepArgs a) {
     float bGt = Wd * fmaxf(Mx, My);
     // G scales for param layer l: S_G,s = 2^(kP - kX_s) with the common
     // product exponent kP = min_s (14 - e(B_s) + kX_s); returns kP
-    auto g_scales = [&](int l, float bv, float bt, float& sgv, float& sgt, float& puv, float& put) {
+    auto g_scales = [&](int l, float bv, float bt, float& sgv, float& sgt, float& puv, float& put, bool& first,
+                        int& shift) {
       const int kxv = sSci[kSiXv + l - 1], kxt = sSci[kSiXt + l - 1], kw = sSci[kSiW + l - 1];
       const int ev = tc::bound_exp(bv), et = tc::bound_exp(bt);
       int kp = 1 << 20;
       if (ev > -1000) kp = min(kp, 14 - ev + kxv);
       if (et > -1000) kp = min(kp, 14 - et + kxt);
       if (kp == (1 << 20)) kp = kxv;
-      kp = max(-120, min(120, kp));
+      kp = join_acc(l, max(-120, min(120, kp)), first, shift);
       sgv = tc::exp2i(kp - kxv);
       sgt = tc::exp2i(kp - kxt);
       puv = tc::exp2i(-(kp - kxv + kw));  // propagation unscale
       put = tc::exp2i(-(kp - kxt + kw));
       return kp;
     };
-    int kP0 = 0, kP1 = 0;
     float sgv, sgt, puv, put;
-    {
-      const int kp = g_scales(NL, bGv, bGt, sgv, sgt, puv, put);
-      if (NL == 1) kP0 = kp; else kP1 = kp;
-    }
+    bool pfirst;
+    int pshift;
+    g_scales(NL, bGv, bGt, sgv, sgt, puv, put, pfirst, pshift);
     // ---- output layer: Wbar_out, bbar_out (unit H: z == 1), G of the last hidden layer ----
     // the last hidden state is recomputed from MMA layer NL's accumulators
     {
@@ -786,7 +825,7 @@ __global__ void __maxnreg__(120) tc2_step_kernel(const StepArgs a) {
     operands_ready();
     if (tid == 0) {
       issue_point_gemm(sA, NL, true);
-      issue_param_gemm(NL);
+      issue_param_gemm(NL, pfirst, pshift);
     }
     mark(9);
     // ---- hidden layers, last first: G of hidden l from the propagated adjoints ----
@@ -799,10 +838,9 @@ __global__ void __maxnreg__(120) tc2_step_kernel(const StepArgs a) {
       const float bxa = C * bGv, bxt = C * bGt;
       const float bv2 = bxa + kapmax * sSc[kScBt + l - 1] * 2.f * bxt, bt2 = bxt;
       float sgv2 = 1.f, sgt2 = 1.f, puv2 = 1.f, put2 = 1.f;
-      if (l > 1) {
-        const int kp = g_scales(l - 1, bv2, bt2, sgv2, sgt2, puv2, put2);
-        if (l - 1 == 1) kP0 = kp; else kP1 = kp;
-      }
+      bool pfirst2 = false;
+      int pshift2 = 0;
+      if (l > 1) g_scales(l - 1, bv2, bt2, sgv2, sgt2, puv2, put2, pfirst2, pshift2);
       // ga = s1 xa' + kap (tx xx' + ty xy'), gx = s1 xx', gy = s1 xy' with the
       // propagation unscale ('), the state unscale and the store scale folded
       const float A0 = puv * sgv2, AT = it * put * sgv2, BT = put * sgt2;
@@ -851,7 +889,7 @@ __global__ void __maxnreg__(120) tc2_step_kernel(const StepArgs a) {
         operands_ready();
         if (tid == 0) {
           issue_point_gemm(sA, l - 1, true);
-          issue_param_gemm(l - 1);
+          issue_param_gemm(l - 1, pfirst2, pshift2);
         }
         bGv = bv2;
         bGt = bt2;
@@ -860,28 +898,49 @@ __global__ void __maxnreg__(120) tc2_step_kernel(const StepArgs a) {
       }
       mark(9 + NL - l + 1);
     }
-    wait_bar(bar_w, ph_w);  // the last param GEMM is done (buffers A / B free, accumulators final)
-    kP_prev0 = kP0;
-    kP_prev1 = kP1;
-    param_readout(first_tile);
-    first_tile = false;
+    wait_bar(bar_w, ph_w);  // the last param GEMM is done (buffers A / B free)
     mark(12);
     ++ph_tile;
   }
 
   // =================== per-CTA outputs ===================
-  __syncthreads();
+  // parameter-gradient accumulators (TMEM lanes 0..63 = G rows h | l, columns
+  // 0..63 = X parts h | l), unscaled by 2^-kacc, plus any spilled part ->
+  // smem [64][65] (buffer A is free) -> the four-block sum
+  float* scr = reinterpret_cast<float*>(bufA);
   for (int l = 1; l <= NL; ++l) {
+    const int kacc = (l == 1) ? kacc0 : kacc1;
+    const bool has = (l == 1) ? has0 : has1, spill = (l == 1) ? spill0 : spill1;
     const float* S = a.tc_scratch + ((size_t)blockIdx.x * NL + (l - 1)) * kScratchPerLayer;
+    tc::fence_after_sync();
+    if ((warp & 3) < 2 && has) {
+      const int lrow = 32 * (warp & 1) + lane;
+      const float inv = tc::exp2i(-kacc);
+#pragma unroll 1
+      for (int h2 = 0; h2 < 2; ++h2) {
+        const int col0 = 32 * hh + 16 * h2;
+        float v[16];
+        tc::tmem_ld1x16_wait(tmem + lane_q + kG0 + 64 * (l - 1) + col0, v);
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+          float x = v[k] * inv;
+          if (spill) x += S[(col0 + k) * 64 + lrow];
+          scr[lrow * 65 + col0 + k] = x;
+        }
+      }
+    }
+    tc::fence_before_sync();
+    __syncthreads();
     const int fo = net.out_w[l], fi = net.in_w[l];
     for (int e = tid; e < fo * (fi + 1); e += kNT) {
       const int o = e / (fi + 1), i = e - o * (fi + 1);
       float g = 0.f;
-      if (!first_tile)  // S[col][row]: col = X part * 32 + i, row = G part * 32 + o
-        g = ((S[i * 64 + o] + S[(32 + i) * 64 + o]) + S[i * 64 + 32 + o]) + S[(32 + i) * 64 + 32 + o];
+      if (has)  // scr[row][col]: row = G part * 32 + o, col = X part * 32 + i
+        g = ((scr[o * 65 + i] + scr[o * 65 + 32 + i]) + scr[(32 + o) * 65 + i]) + scr[(32 + o) * 65 + 32 + i];
       const int idx = (i < fi) ? net.w_off[l] + o * fi + i : net.b_off[l] + o;
       a.grad_part[(size_t)idx * a.part_stride + blockIdx.x] = g;
     }
+    __syncthreads();
   }
   // CUDA-core gradients: per-warp sums combined in warp order
   for (int u = tid; u <= H; u += kNT) {

@@ -51,6 +51,21 @@ __global__ void __launch_bounds__(128, 1) tc_probe_kernel(int mode, const float*
           tc::mma_bf16(tmem, tc::kdesc(sa + part * 8192 + 32 * ks), bd, idesc, (part > 0 || ks > 0) ? 1u : 0u);
         }
       }
+    } else if (mode == 3) {
+      // scale-input-d: the forward product twice, the second pass scaling the
+      // accumulated first pass by 2^-2 on its first MMA: D = AW^T / 4 + AW^T
+      const uint32_t idesc = tc::idesc_bf16(128, 32, 0, 0);
+      for (int pass = 0; pass < 2; ++pass)
+        for (int pr = 0; pr < 6; ++pr) {
+          const uint32_t bb = sw + tc::kProdB[pr] * 2048;
+          for (int ks = 0; ks < 2; ++ks) {
+            const uint64_t ad = tc::kdesc(sa + tc::kProdA[pr] * 8192 + 32 * ks), bd = tc::kdesc(bb + 32 * ks);
+            if (pass == 1 && pr == 0 && ks == 0)
+              tc::mma_f16_sd(tmem, ad, bd, idesc, 2);
+            else
+              tc::mma_bf16(tmem, ad, bd, idesc, (pass > 0 || pr > 0 || ks > 0) ? 1u : 0u);
+          }
+        }
     } else {
       const uint32_t idesc = tc::idesc_bf16(128, 96, 1, 1);
       for (int kp = 0; kp < 8; ++kp)
@@ -75,7 +90,9 @@ __global__ void __launch_bounds__(128, 1) tc_probe_kernel(int mode, const float*
   }
   tc::fence_before_sync();
   __syncthreads();
-  if (mode != 2) {
+  if (mode == 3) {
+    for (int i = 0; i < 32; ++i) out[tid * 32 + i] = raw[tid * 96 + i];
+  } else if (mode != 2) {
     for (int i = 0; i < 32; ++i) out[tid * 32 + i] = raw[tid * 96 + i] + raw[tid * 96 + 32 + i] + raw[tid * 96 + 64 + i];
   } else {
     for (int e = tid; e < 32 * 32; e += 128) {

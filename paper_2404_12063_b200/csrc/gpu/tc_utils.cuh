@@ -195,6 +195,10 @@ __device__ __forceinline__ int bound_exp(float b) {
   return E - 126;
 }
 
+// the six bf16x3 part products (a part, b part), smallest first (probe mode 3)
+__device__ constexpr int kProdA[6] = {2, 0, 1, 1, 0, 0};
+__device__ constexpr int kProdB[6] = {0, 2, 1, 0, 1, 0};
+
 // ---- descriptors ---------------------------------------------------------------
 // shared-memory matrix descriptor (sm100): start >> 4 [0,14), LBO >> 4
 // [16,30), SBO >> 4 [32,46), version 1 [46,48), base offset 0, layout type
@@ -255,6 +259,30 @@ __device__ __forceinline__ void mma_bf16(uint32_t d_tmem, uint64_t a_desc, uint6
       "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(d_tmem),
       "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
       : "memory");
+}
+// D[tmem] = A * B + D * 2^-S (scale-input-d, kind::f16): accumulates onto a
+// scaled-down accumulator, S in [0, 15]
+template <int S>
+__device__ __forceinline__ void mma_f16_sd(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc) {
+  static_assert(S >= 0 && S <= 15, "scale-input-d range");
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, 1, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p, %4;\n\t}\n" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "n"(S)
+      : "memory");
+}
+// runtime S in [0, 15]
+__device__ __forceinline__ void mma_f16_sd(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, int s) {
+  switch (s) {
+#define VPG_SD(k) \
+  case k:         \
+    mma_f16_sd<k>(d, a, b, idesc); \
+    break;
+    VPG_SD(0) VPG_SD(1) VPG_SD(2) VPG_SD(3) VPG_SD(4) VPG_SD(5) VPG_SD(6) VPG_SD(7)
+    VPG_SD(8) VPG_SD(9) VPG_SD(10) VPG_SD(11) VPG_SD(12) VPG_SD(13) VPG_SD(14) default: mma_f16_sd<15>(d, a, b, idesc);
+#undef VPG_SD
+  }
 }
 // arrive on an mbarrier when all previously issued MMAs of this thread are done
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {

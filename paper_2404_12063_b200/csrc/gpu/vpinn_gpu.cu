@@ -302,6 +302,7 @@ void configure(vpinn_gpu_ctx* c) {
       c->grid_step = std::max(1, std::min(a.n_tiles, occ * c->sm_count));
       c->tc_scratch.alloc((size_t)c->grid_step * (V.D - 1) * vpg::t2::kScratchPerLayer);
       a.tc_scratch = c->tc_scratch.p;
+      if (const char* e = std::getenv("VPINN_TC2_FORCE_SPILL")) a.tc_force_spill = std::atoi(e);
       c->kernel_name = "tc2_step_kernel<" + std::to_string(V.H) + "," + std::to_string(V.D) + "," +
                        (V.ACT ? "sigmoid" : "tanh") + "> (fp16 split, " + std::to_string(occ) + " CTAs/SM)";
     } else if (c->tc) {
@@ -1304,7 +1305,7 @@ int vpinn_gpu_flush_l2(vpinn_gpu_ctx* c) {
 
 int vpinn_gpu_tc_probe(int device, int mode, const float* A, const float* W, const float* H, float* out) {
   return guarded([&] {
-    if (mode < 0 || mode > 2) throw Fail{VPINN_ERR_CONFIG, "tc_probe: mode must be 0, 1 or 2"};
+    if (mode < 0 || mode > 3) throw Fail{VPINN_ERR_CONFIG, "tc_probe: mode must be 0..3"};
     CK(cudaSetDevice(device));
     DBuf<float> dA, dW, dH, dO;
     dA.alloc(128 * 32);

@@ -159,7 +159,7 @@ def test_nonfinite_gradient_aborts_with_step_index():
     assert e.value.code == 4 and e.value.report.abort_step == 1
 
 
-@pytest.mark.parametrize("mode", [0, 1, 2])
+@pytest.mark.parametrize("mode", [0, 1, 2, 3])
 def test_tcgen05_3xtf32_probe(mode):
     """The three tcgen05 GEMM shapes of the tensor-core MLP (bf16x3 split,
     six products) against fp64: fp32-level accuracy."""
@@ -173,22 +173,28 @@ def test_tcgen05_3xtf32_probe(mode):
     ptr = lambda a: a.ctypes.data_as(C.c_void_p)
     _capi.check(_capi.lib().vpinn_gpu_tc_probe(0, mode, ptr(A), ptr(W), ptr(H), ptr(out)))
     a, w, h = A.astype(np.float64), W.astype(np.float64), H.astype(np.float64)
-    ref = {0: a @ w.T, 1: a @ w, 2: a.T @ h}[mode]
+    ref = {0: a @ w.T, 1: a @ w, 2: a.T @ h, 3: 1.25 * (a @ w.T)}[mode]
     got = out[:ref.size].reshape(ref.shape)
     err = np.abs(got - ref).max() / np.abs(ref).max()
     assert err < 2e-6, err
 
 
 @pytest.mark.parametrize("name", ["c1_poisson", "gear576_cd2d", "inverse_scalar_eps"])
-@pytest.mark.parametrize("mode", ["ffma", "tc_aliased_slab"])
+@pytest.mark.parametrize("mode", ["ffma", "tc_aliased_slab", "tc_bf16", "tc2_spill"])
 def test_alternate_step_kernels_match_oracle(name, mode, monkeypatch):
-    """The CUDA-core (FFMA) fused kernel and the tensor-core kernel with its
-    slab aliased into an operand buffer are selectable by environment; both
-    must meet the same parity bar as the default path."""
+    """The CUDA-core (FFMA) fused kernel, the bf16x3 tensor-core kernel (slab
+    dedicated or aliased into an operand buffer) and the tc2 kernel's spill
+    path are selectable by environment; all must meet the same parity bar as
+    the default path."""
     if mode == "ffma":
         monkeypatch.setenv("VPINN_TC", "0")
-    else:
+    elif mode == "tc_bf16":  # the bf16x3 one-CTA tensor-core kernel (dedicated slab)
+        monkeypatch.setenv("VPINN_TC_KERNEL", "1")
+    elif mode == "tc_aliased_slab":
+        monkeypatch.setenv("VPINN_TC_KERNEL", "1")
         monkeypatch.setenv("VPINN_TC_SLAB", "0")
+    else:  # tc2 with its parameter-gradient accumulators spilled every tile (rare path)
+        monkeypatch.setenv("VPINN_TC2_FORCE_SPILL", "1")
     spec = CASES[name]()
     ob, g, p0 = make_pair(spec)
     parts_o, _ = ob.loss_and_grad(p0)
