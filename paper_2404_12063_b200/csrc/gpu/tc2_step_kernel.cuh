@@ -58,6 +58,7 @@ constexpr int kWBytes = 4096;         // [64][32] fp16: W h rows 0..31 | l rows 
 constexpr uint32_t kCols = 256;       // TMEM columns per CTA
 constexpr int kDCols = 32;            // stream accumulator columns
 constexpr int kG0 = 96;               // parameter-gradient accumulators: 64 columns per MMA layer
+constexpr int kZ0 = 224;              // last hidden layer's activations z (32 columns), forward -> reverse
 constexpr int kScratchPerLayer = 64 * 64;  // global fp32 [col 64][lane 64] per CTA and MMA layer
 constexpr int kTailFloats = 8 * 128;  // contraction scratch after the slab in buffer A
 constexpr float kOneBias = 20.0f;     // bias of the constant-one unit: act(20) == 1.0f
@@ -358,9 +359,20 @@ __global__ void __maxnreg__(120) tc2_step_kernel(const StepArgs a) {
     tc::mma_commit(bar_w);
   };
   uint32_t ph_v = 0, ph_t = 0, ph_w = 0, tma_phase = 0;
-  auto wait_bar = [&](uint64_t* bar, uint32_t& ph) {
-    mbar_wait(bar, ph);
-    ph ^= 1u;
+  // CTA-wide wait for MMA completion: ONE warp polls the mbarrier(s), the
+  // others sleep in the CTA barrier instead of spinning on issue slots the
+  // co-resident CTA needs
+  auto cta_wait = [&](uint64_t* b1, uint32_t& p1, uint64_t* b2, uint32_t* p2, uint64_t* b3, uint32_t* p3) {
+    if (warp == 0) {
+      mbar_wait(b1, p1);
+      if (b2) mbar_wait(b2, *p2);
+      if (b3) mbar_wait(b3, *p3);
+    }
+    p1 ^= 1u;
+    if (b2) *p2 ^= 1u;
+    if (b3) *p3 ^= 1u;
+    tc::fence_before_sync();
+    __syncthreads();
     tc::fence_after_sync();
   };
   auto operands_ready = [&]() {
@@ -553,7 +565,7 @@ __global__ void __maxnreg__(120) tc2_step_kernel(const StepArgs a) {
       const float sv = last ? 1.f : sSc[kScSv + l];
       const float* bias = sBias + 32 * (l - 1);
       float s1v[16];
-      wait_bar(bar_v, ph_v);
+      cta_wait(bar_v, ph_v, nullptr, nullptr, nullptr, nullptr);
 #pragma unroll
       for (int c = 0; c < 2; ++c) {
         float d[8], z[8];
@@ -565,9 +577,12 @@ __global__ void __maxnreg__(120) tc2_step_kernel(const StepArgs a) {
           s1v[8 * c + k] = AC::s1(z[k]) * ft;
           if (last) ou = fmaf(sWd[u], z[k], ou);
         }
-        if (!last) tc::st_split8_ho<true>(bufB, kPart, coff(c), z, sv);
+        if (!last)
+          tc::st_split8_ho<true>(bufB, kPart, coff(c), z, sv);
+        else
+          tc::tmem_st1x8_wait(tmem + lane_q + kZ0 + u0 + 8 * c, z);  // kept for the reverse
       }
-      wait_bar(bar_t, ph_t);
+      cta_wait(bar_t, ph_t, nullptr, nullptr, nullptr, nullptr);
       // D == 3: buffer A (slab) is free once MMA layer 1 is done
       if (D == 3 && l == 1 && interior && tid == 0)
         issue_chunk(a, cell0, 0, nrows_tile, reinterpret_cast<float*>(bufA), tma_bar);
@@ -621,9 +636,9 @@ __global__ void __maxnreg__(120) tc2_step_kernel(const StepArgs a) {
     if (interior) {
       const bool conv = a.nt == 3;
       const float e_fixed = a.eps_source == 1 ? P[net.scal_off + a.eps_scalar_index] : a.eps;
-      __syncthreads();
-      mbar_wait(tma_bar, tma_phase);
+      if (warp == 0) mbar_wait(tma_bar, tma_phase);  // the slab has landed
       tma_phase ^= 1u;
+      __syncthreads();
       mark(5);
       const float* slab = reinterpret_cast<const float*>(bufA);
       const float* T0 = chunk_ptr(a, cell0, 0, slab, 0);
@@ -790,21 +805,21 @@ __global__ void __maxnreg__(120) tc2_step_kernel(const StepArgs a) {
     int pshift;
     g_scales(NL, bGv, bGt, sgv, sgt, puv, put, pfirst, pshift);
     // ---- output layer: Wbar_out, bbar_out (unit H: z == 1), G of the last hidden layer ----
-    // the last hidden state is recomputed from MMA layer NL's accumulators
+    // the last hidden state: z kept in TMEM by the forward, the tangents
+    // from MMA layer NL's accumulators
     {
-      const float f0 = sSc[kScF0 + NL - 1], f1 = sSc[kScF1 + NL - 1];
-      const float* bias = sBias + 32 * (NL - 1);
+      const float f1 = sSc[kScF1 + NL - 1];
       const float Ub = ub * sgv, Uxv = uxb * sgv, Uyv = uyb * sgv, Uxt = uxb * sgt, Uyt = uyb * sgt;
 #pragma unroll 1
       for (int c = 0; c < 2; ++c) {
-        float d0[8], dx[8], dy[8];
-        tc::tmem_ld1x8_wait(dcol(0, c), d0);
+        float zs[8], dx[8], dy[8];
+        tc::tmem_ld1x8_wait(tmem + lane_q + kZ0 + u0 + 8 * c, zs);
         tc::tmem_ld2x8_wait(dcol(1, c), dcol(2, c), dx, dy);
         float v[8], gA[8], gX[8], gY[8];
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
           const int u = u0 + 8 * c + k;
-          const float z = AC::value(fmaf(d0[k], f0, bias[u]));
+          const float z = zs[k];
           const float s1 = AC::s1(z), kp = AC::kap(z);
           const float cc = s1 * f1;
           const float tx = cc * dx[k], ty = cc * dy[k];
@@ -844,12 +859,11 @@ __global__ void __maxnreg__(120) tc2_step_kernel(const StepArgs a) {
       // ga = s1 xa' + kap (tx xx' + ty xy'), gx = s1 xx', gy = s1 xy' with the
       // propagation unscale ('), the state unscale and the store scale folded
       const float A0 = puv * sgv2, AT = it * put * sgv2, BT = put * sgt2;
-      wait_bar(bar_v, ph_v);
-      wait_bar(bar_t, ph_t);
       // l > 1: G of hidden l goes to buffer A and the recomputed hidden-1
-      // output to buffer B, so param GEMM l must have read both; each thread
-      // reads (its state) and writes exactly its own slots: no barrier
-      if (l > 1) wait_bar(bar_w, ph_w);
+      // output to buffer B, so param GEMM l must have read both (bar_w)
+      // (param GEMM l is waited for per thread right before the first store,
+      // so the first chunk's G computation overlaps it)
+      cta_wait(bar_v, ph_v, bar_t, &ph_t, nullptr, nullptr);
 #pragma unroll 1
       for (int c = 0; c < 2; ++c) {
         float xa[8], xx[8], xy[8], z[8], tx[8], ty[8];
@@ -879,6 +893,11 @@ __global__ void __maxnreg__(120) tc2_step_kernel(const StepArgs a) {
           acc_units(v, kAW0y, c);
           acc_units(ga, kAB0, c);
         } else {
+          if (c == 0) {
+            mbar_wait(bar_w, ph_w);
+            ph_w ^= 1u;
+            tc::fence_after_sync();
+          }
           tc::st_split8_ho<false>(bufA, kPart, o, ga, 1.f);
           tc::st_split8_ho<false>(bufA + kStream, kPart, o, gx, 1.f);
           tc::st_split8_ho<false>(bufA + 2 * kStream, kPart, o, gy, 1.f);
@@ -898,7 +917,7 @@ __global__ void __maxnreg__(120) tc2_step_kernel(const StepArgs a) {
       }
       mark(9 + NL - l + 1);
     }
-    wait_bar(bar_w, ph_w);  // the last param GEMM is done (buffers A / B free)
+    cta_wait(bar_w, ph_w, nullptr, nullptr, nullptr, nullptr);  // last param GEMM done: buffers A / B free
     mark(12);
     ++ph_tile;
   }

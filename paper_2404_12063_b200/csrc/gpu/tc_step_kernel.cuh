@@ -487,7 +487,6 @@ __global__ void __launch_bounds__(128 * NQ, 1) tc_step_kernel(const StepArgs a) 
       // residuals r_j (losses.hpp:122-136)
       if (hh == 0 && p < nrows_tile) {
         const int kk = p / a.T;
-        const int j = p - kk * a.T;
         const float gx = part[p], gy = part[128 + p];
         float res = e_fixed * (gx + gy);
         if (conv) res += part[256 + p];

@@ -376,6 +376,16 @@ __device__ __forceinline__ void tmem_ld2x8_wait(uint32_t ta, uint32_t tb, float 
     vb[i] = __uint_as_float(r[8 + i]);
   }
 }
+// store 8 consecutive columns of this warp's lane quarter (thread i: lane
+// base + i), then wait for the store to complete
+__device__ __forceinline__ void tmem_st1x8_wait(uint32_t ta, const float (&v)[8]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};\n\t"
+      "tcgen05.wait::st.sync.aligned;" ::"r"(ta),
+      "r"(__float_as_uint(v[0])), "r"(__float_as_uint(v[1])), "r"(__float_as_uint(v[2])), "r"(__float_as_uint(v[3])),
+      "r"(__float_as_uint(v[4])), "r"(__float_as_uint(v[5])), "r"(__float_as_uint(v[6])), "r"(__float_as_uint(v[7]))
+      : "memory");
+}
 // N in {8, 16} columns per load
 template <int N>
 __device__ __forceinline__ void tmem_ld3_wait(uint32_t ta, uint32_t tb, uint32_t tc_, float (&va)[N], float (&vb)[N],
