@@ -644,24 +644,36 @@ __global__ void __maxnreg__(120) tc2_step_kernel(const StepArgs a) {
       const float* T0 = chunk_ptr(a, cell0, 0, slab, 0);
       const float* T1 = chunk_ptr(a, cell0, 0, slab, 1);
       const float* T2 = conv ? chunk_ptr(a, cell0, 0, slab, 2) : T0;
-      const int nt = a.nt;
-      // phase A: (tensor g, row r) dot products with (ux | uy | bx ux + by uy)
-#pragma unroll 1
-      for (int it = tid; it < 3 * 128; it += kNT) {
-        const int g = it >> 7, r = it & 127;
-        if (g < nt && r < nrows_tile) {
-          const int kk = r / a.T;
-          const float* sv = (g == 0 ? sEx + kUx * 128 : (g == 1 ? sEx + kUy * 128 : cvr)) + kk * a.Q;
-          const float* gr = (g == 0 ? T0 : (g == 1 ? T1 : T2)) + r * a.Q;
-          float acc4[4] = {0.f, 0.f, 0.f, 0.f};
-          int q = 0;
+      // phase A: (tensor g, row r) dot products with (ux | uy | bx ux + by uy).
+      // Unit half 0 does tensors 0 and 2 (interleaved: two independent
+      // chains), half 1 tensor 1 (plus a discarded duplicate, keeping the
+      // loop uniform).  Each dot: four accumulators, combined in a fixed order.
+      {
+        const int r = p;
+        const bool rok = r < nrows_tile;
+        const int kk = rok ? r / a.T : 0;
+        const float* sv1 = (hh == 0 ? sEx + kUx * 128 : sEx + kUy * 128) + kk * a.Q;
+        const float* g1 = (hh == 0 ? T0 : T1) + (rok ? r : 0) * a.Q;
+        const bool two = hh == 0 && conv;
+        const float* sv2 = two ? cvr + kk * a.Q : sv1;
+        const float* g2 = two ? T2 + (rok ? r : 0) * a.Q : g1;
+        float a1[4] = {0.f, 0.f, 0.f, 0.f}, a2[4] = {0.f, 0.f, 0.f, 0.f};
+        int q = 0;
 #pragma unroll 2
-          for (; q + 3 < a.Q; q += 4) {
+        for (; q + 3 < a.Q; q += 4) {
 #pragma unroll
-            for (int u = 0; u < 4; ++u) acc4[u] = fmaf(gr[q + u], sv[q + u], acc4[u]);
+          for (int u = 0; u < 4; ++u) {
+            a1[u] = fmaf(g1[q + u], sv1[q + u], a1[u]);
+            a2[u] = fmaf(g2[q + u], sv2[q + u], a2[u]);
           }
-          for (; q < a.Q; ++q) acc4[0] = fmaf(gr[q], sv[q], acc4[0]);
-          part[g * 128 + r] = (acc4[0] + acc4[1]) + (acc4[2] + acc4[3]);
+        }
+        for (; q < a.Q; ++q) {
+          a1[0] = fmaf(g1[q], sv1[q], a1[0]);
+          a2[0] = fmaf(g2[q], sv2[q], a2[0]);
+        }
+        if (rok) {
+          part[hh * 128 + r] = (a1[0] + a1[1]) + (a1[2] + a1[3]);
+          if (two) part[256 + r] = (a2[0] + a2[1]) + (a2[2] + a2[3]);
         }
       }
       __syncthreads();
@@ -678,23 +690,34 @@ __global__ void __maxnreg__(120) tc2_step_kernel(const StepArgs a) {
       }
       __syncthreads();
       mark(6);
-      // phase B: (tensor g, point) adjoint columns; per-cell sums in row order
-#pragma unroll 1
-      for (int it = tid; it < 3 * 128; it += kNT) {
-        const int g = it >> 7, pp = it & 127;
-        if (g < nt && pp < np) {
-          const int myk = pp / a.Q, myq = pp - myk * a.Q;
-          const float* gc = (g == 0 ? T0 : (g == 1 ? T1 : T2)) + myq;
-          float acc4[4] = {0.f, 0.f, 0.f, 0.f};
-          int r = myk * a.T;
-          const int r1 = r + a.T;
+      // phase B: (tensor g, point) adjoint columns, same split as phase A;
+      // then half 1 does the per-cell sums in row order
+      {
+        const int pp = p;
+        const bool pok = pp < np;
+        const int myk = pok ? pp / a.Q : 0, myq = pok ? pp - myk * a.Q : 0;
+        const float* c1 = (hh == 0 ? T0 : T1) + myq;
+        const bool two = hh == 0 && conv;
+        const float* c2 = two ? T2 + myq : c1;
+        float b1[4] = {0.f, 0.f, 0.f, 0.f}, b2[4] = {0.f, 0.f, 0.f, 0.f};
+        int r = myk * a.T;
+        const int r1 = r + a.T;
 #pragma unroll 2
-          for (; r + 3 < r1; r += 4) {
+        for (; r + 3 < r1; r += 4) {
 #pragma unroll
-            for (int u = 0; u < 4; ++u) acc4[u] = fmaf(gc[(r + u) * a.Q], rbarv[r + u], acc4[u]);
+          for (int u = 0; u < 4; ++u) {
+            const float rb = rbarv[r + u];
+            b1[u] = fmaf(c1[(r + u) * a.Q], rb, b1[u]);
+            b2[u] = fmaf(c2[(r + u) * a.Q], rb, b2[u]);
           }
-          for (; r < r1; ++r) acc4[0] = fmaf(gc[r * a.Q], rbarv[r], acc4[0]);
-          part[g * 128 + pp] = (acc4[0] + acc4[1]) + (acc4[2] + acc4[3]);
+        }
+        for (; r < r1; ++r) {
+          b1[0] = fmaf(c1[r * a.Q], rbarv[r], b1[0]);
+          b2[0] = fmaf(c2[r * a.Q], rbarv[r], b2[0]);
+        }
+        if (pok) {
+          part[hh * 128 + pp] = (b1[0] + b1[1]) + (b1[2] + b1[3]);
+          if (two) part[256 + pp] = (b2[0] + b2[1]) + (b2[2] + b2[3]);
         }
       }
       if (tid >= kNT - 64 && tid - (kNT - 64) < ncell) {
