@@ -312,11 +312,17 @@ __global__ void __maxnreg__(120) tc2_step_kernel(const StepArgs a) {
   // swizzled byte offsets of this thread's two 8-unit chunks in a [128][32] fp16 tile
   const uint32_t off0 = tc::sw_chunk(p, 2 * hh), off1 = tc::sw_chunk(p, 2 * hh + 1);
 
-  // ---------------- MMA issue (thread 0) ----------------
+  // ---------------- MMA issue (warp 0, one elected lane) ----------------
+  // descriptors: start address >> 4 in the low 14 bits, so an address offset
+  // is added as offset >> 4 (addresses < 256 KB: no carry out of the field)
+  const uint64_t dA_k = tc::kdesc(sA), dB_k = tc::kdesc(sB);           // K-major point operands
+  const uint64_t dA_mn = tc::mndesc(sA, kPart), dB_mn = tc::mndesc(sB, kPart);  // MN-major (param GEMM)
+  const uint64_t dW_k = tc::kdesc(sW), dW_mn = tc::mndesc(sW, 32 * tc::kRowBytes);
   // point GEMM of MMA layer l (forward, or propagation with B MN-major): the
   // three part products Al.Wh, Ah.Wl, Ah.Wh of stream s accumulate into D_s
-  auto issue_point_gemm = [&](uint32_t abuf, int l, bool propagate) {
-    const uint32_t wbase = sW + (uint32_t)(l - 1) * kWBytes;
+  auto issue_point_gemm = [&](bool bufb, int l, bool propagate) {
+    const uint64_t abase = bufb ? dB_k : dA_k;
+    const uint64_t wbase = (propagate ? dW_mn : dW_k) + (uint64_t)(((l - 1) * kWBytes) >> 4);
     const uint32_t idesc = tc::idesc_f16(128, 32, 0, propagate ? 1 : 0);
 #pragma unroll 1
     for (int s = 0; s < 3; ++s) {
@@ -324,17 +330,16 @@ __global__ void __maxnreg__(120) tc2_step_kernel(const StepArgs a) {
 #pragma unroll
       for (int pr = 0; pr < 3; ++pr) {
         const int pa = pr == 0 ? 1 : 0, pb = pr == 1 ? 1 : 0;
-        const uint32_t abase = abuf + s * kStream + pa * kPart;
-        const uint32_t bbase = wbase + pb * 32 * tc::kRowBytes;
 #pragma unroll
         for (int ks = 0; ks < 2; ++ks) {
-          const uint64_t bd = propagate ? tc::mndesc(bbase + 1024 * ks, 32 * tc::kRowBytes) : tc::kdesc(bbase + 32 * ks);
-          tc::mma_bf16(d, tc::kdesc(abase + 32 * ks), bd, idesc, (pr > 0 || ks > 0) ? 1u : 0u);
+          const uint64_t ad = abase + (uint64_t)((s * kStream + pa * kPart + 32 * ks) >> 4);
+          const uint64_t bd = wbase + (uint64_t)((pb * 32 * tc::kRowBytes + (propagate ? 1024 : 32) * ks) >> 4);
+          tc::mma_warp(d, ad, bd, idesc, (pr > 0 || ks > 0) ? 1u : 0u);
         }
       }
-      if (s == 0) tc::mma_commit(bar_v);
+      if (s == 0) tc::commit_warp(bar_v);
     }
-    tc::mma_commit(bar_t);
+    tc::commit_warp(bar_t);
   };
   // parameter gradient of MMA layer l: G parts in bufA (M blocks h | l | next
   // stream's parts, unused), X parts in bufB (N = h | l).  Accumulates in
@@ -346,17 +351,23 @@ __global__ void __maxnreg__(120) tc2_step_kernel(const StepArgs a) {
     const uint32_t idesc = tc::idesc_f16(128, 64, 1, 1);
 #pragma unroll 1
     for (int s = 0; s < 3; ++s) {
-      const uint32_t g = sA + s * kStream, x = sB + s * kStream;
 #pragma unroll
       for (int kp = 0; kp < 8; ++kp) {
-        const uint64_t ad = tc::mndesc(g + 1024 * kp, kPart), bd = tc::mndesc(x + 1024 * kp, kPart);
-        if (s == 0 && kp == 0 && !first && shift > 0)
-          tc::mma_f16_sd(acc, ad, bd, idesc, shift);
-        else
-          tc::mma_bf16(acc, ad, bd, idesc, (s == 0 && kp == 0 && first) ? 0u : 1u);
+        const uint64_t off = (uint64_t)((s * kStream + 1024 * kp) >> 4);
+        const uint64_t ad = dA_mn + off, bd = dB_mn + off;
+        if (s == 0 && kp == 0) {
+          if (first)
+            tc::mma_warp(acc, ad, bd, idesc, 0u);
+          else if (shift > 0)
+            tc::mma_warp_sd(acc, ad, bd, idesc, shift);
+          else
+            tc::mma_warp(acc, ad, bd, idesc, 1u);
+        } else {
+          tc::mma_warp(acc, ad, bd, idesc, 1u);
+        }
       }
     }
-    tc::mma_commit(bar_w);
+    tc::commit_warp(bar_w);
   };
   uint32_t ph_v = 0, ph_t = 0, ph_w = 0, tma_phase = 0;
   // CTA-wide wait for MMA completion: ONE warp polls the mbarrier(s), the
@@ -550,7 +561,7 @@ __global__ void __maxnreg__(120) tc2_step_kernel(const StepArgs a) {
 #pragma unroll 1
     for (int c = 0; c < 2; ++c) store_x1(x1buf, c, px, py);
     operands_ready();
-    if (tid == 0) issue_point_gemm(smem_u32(x1buf), 1, false);
+    if (warp == 0) issue_point_gemm(D == 2, 1, false);
     mark(1);
     // epilogue of MMA layer l: hidden l+1 output.  Value stream first (it
     // overlaps the tangent-stream MMAs), stored (or consumed by the output
@@ -609,7 +620,7 @@ __global__ void __maxnreg__(120) tc2_step_kernel(const StepArgs a) {
       }
       if (!last) {
         operands_ready();
-        if (tid == 0) issue_point_gemm(sB, l + 1, false);
+        if (warp == 0) issue_point_gemm(true, l + 1, false);
       }
       mark(1 + l);
     }
@@ -861,8 +872,8 @@ __global__ void __maxnreg__(120) tc2_step_kernel(const StepArgs a) {
       }
     }
     operands_ready();
-    if (tid == 0) {
-      issue_point_gemm(sA, NL, true);
+    if (warp == 0) {
+      issue_point_gemm(false, NL, true);
       issue_param_gemm(NL, pfirst, pshift);
     }
     mark(9);
@@ -929,8 +940,8 @@ __global__ void __maxnreg__(120) tc2_step_kernel(const StepArgs a) {
       }
       if (l > 1) {
         operands_ready();
-        if (tid == 0) {
-          issue_point_gemm(sA, l - 1, true);
+        if (warp == 0) {
+          issue_point_gemm(false, l - 1, true);
           issue_param_gemm(l - 1, pfirst2, pshift2);
         }
         bGv = bv2;

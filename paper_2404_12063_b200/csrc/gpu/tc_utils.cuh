@@ -260,6 +260,49 @@ __device__ __forceinline__ void mma_bf16(uint32_t d_tmem, uint64_t a_desc, uint6
       "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
+// warp-collective forms: called by all 32 threads of ONE converged warp, one
+// elected lane issues (no divergent single-thread branch around the MMA, so
+// the descriptors stay warp-uniform and no elect loop is generated)
+__device__ __forceinline__ void mma_warp(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+                                         uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+template <int S>
+__device__ __forceinline__ void mma_warp_sd(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc) {
+  static_assert(S >= 0 && S <= 15, "scale-input-d range");
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t"
+      "setp.ne.b32 p, 1, 0;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p, %4;\n\t}\n" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "n"(S)
+      : "memory");
+}
+__device__ __forceinline__ void mma_warp_sd(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, int s) {
+  switch (s) {
+#define VPG_SDW(k) \
+  case k:          \
+    mma_warp_sd<k>(d, a, b, idesc); \
+    break;
+    VPG_SDW(0) VPG_SDW(1) VPG_SDW(2) VPG_SDW(3) VPG_SDW(4) VPG_SDW(5) VPG_SDW(6) VPG_SDW(7)
+    VPG_SDW(8) VPG_SDW(9) VPG_SDW(10) VPG_SDW(11) VPG_SDW(12) VPG_SDW(13) VPG_SDW(14) default: mma_warp_sd<15>(d, a, b, idesc);
+#undef VPG_SDW
+  }
+}
+__device__ __forceinline__ void commit_warp(uint64_t* bar) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}\n" ::"r"(smem_u32(bar))
+      : "memory");
+}
+
 // D[tmem] = A * B + D * 2^-S (scale-input-d, kind::f16): accumulates onto a
 // scaled-down accumulator, S in [0, 15]
 template <int S>
