@@ -350,13 +350,18 @@ def _step_roofline(kernel_name, mlp_tflops, ffma_peak, pk, share):
     FFMA throughput.  'achieved' is always the ALGORITHMIC fp32 MLP flops
     (33,180 per interior point + 11,220 per penalty point) per
     launch over the launch time."""
-    tc = kernel_name.startswith("tc_step")
-    tr = _traffic("tc_step" if tc else "step_kernel")
+    tc = kernel_name.startswith("tc_step") or kernel_name.startswith("tc2_step")
+    tc2 = kernel_name.startswith("tc2_step")
+    tr = _traffic("tc2_step" if tc2 else ("tc_step" if tc else "step_kernel"))
     if tc:
-        peak = pk["bf16_tflops"] / 6.0
+        # tc2: fp16 two-part split, 3 tensor products per fp32 product (fp16
+        # runs at the bf16 rate); tc: bf16 three-part split, 6 products
+        nprod = 3.0 if tc2 else 6.0
+        peak = pk["bf16_tflops"] / nprod
         out = {"bound": "tensor", "kernel": kernel_name, "achieved": mlp_tflops, "peak": peak,
                "unit": "TFLOP/s", "frac": mlp_tflops / peak,
-               "peak_source": "MEASURED_PEAKS.json bf16_tflops (burst) / 6 products per fp32-faithful product",
+               "peak_source": f"MEASURED_PEAKS.json bf16_tflops (burst) / {nprod:.0f} tensor products per "
+                              "fp32-faithful product",
                "fp32_ffma_equivalent": {"peak": ffma_peak, "frac": mlp_tflops / ffma_peak if ffma_peak else None,
                                         "peak_source": "FFMA microbenchmark measured in this run"}}
     else:

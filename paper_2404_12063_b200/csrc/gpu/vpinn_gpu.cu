@@ -69,16 +69,14 @@ struct DBuf {
     n = 0;
   }
   // 64 bytes of slack: 1-D bulk copies read 16-byte aligned supersets
-  void alloc(size_t count) {
+  // zero-filled on stream s, i.e. ordered before anything later enqueued on s
+  // (a legacy-default-stream memset does NOT order with a non-blocking
+  // stream: it could land after, and overwrite, an upload)
+  void alloc(size_t count, cudaStream_t s) {
     release();
     n = count;
     CK(cudaMalloc(&p, std::max<size_t>(count, 1) * sizeof(T) + 64));
-    // cudaMemset runs on the legacy default stream, which does NOT order with
-    // the context's non-blocking stream: finish it before any upload is
-    // enqueued there (else the zero fill can land after, and overwrite, the
-    // upload)
-    CK(cudaMemset(p, 0, std::max<size_t>(count, 1) * sizeof(T) + 64));
-    CK(cudaDeviceSynchronize());
+    CK(cudaMemsetAsync(p, 0, std::max<size_t>(count, 1) * sizeof(T) + 64, s));
   }
   void upload(const T* h, size_t count, cudaStream_t s) {
     if (count) CK(cudaMemcpyAsync(p, h, count * sizeof(T), cudaMemcpyHostToDevice, s));
@@ -261,7 +259,7 @@ void configure(vpinn_gpu_ctx* c) {
              (size_t)(c->nt * round4(tile_rows * c->Q + 8) + vpg::t2::kTailFloats) * sizeof(float) <=
                  (size_t)vpg::t2::kBuf;
     if (c->tc && (std::getenv("VPINN_PHASE_CLOCK") && std::atoi(std::getenv("VPINN_PHASE_CLOCK")) != 0)) {
-      c->phase_clk.alloc((size_t)vpg::kPhaseTiles * vpg::kPhaseMarks);
+      c->phase_clk.alloc((size_t)vpg::kPhaseTiles * vpg::kPhaseMarks, c->stream);
       a.phase_clk = c->phase_clk.p;
     }
     if (c->tc2) {
@@ -300,7 +298,7 @@ void configure(vpinn_gpu_ctx* c) {
       }
       if (const char* e = std::getenv("VPINN_TC2_CTAS")) occ = std::max(1, std::atoi(e));
       c->grid_step = std::max(1, std::min(a.n_tiles, occ * c->sm_count));
-      c->tc_scratch.alloc((size_t)c->grid_step * (V.D - 1) * vpg::t2::kScratchPerLayer);
+      c->tc_scratch.alloc((size_t)c->grid_step * (V.D - 1) * vpg::t2::kScratchPerLayer, c->stream);
       a.tc_scratch = c->tc_scratch.p;
       if (const char* e = std::getenv("VPINN_TC2_FORCE_SPILL")) a.tc_force_spill = std::atoi(e);
       c->kernel_name = "tc2_step_kernel<" + std::to_string(V.H) + "," + std::to_string(V.D) + "," +
@@ -467,21 +465,21 @@ void configure(vpinn_gpu_ctx* c) {
 
   // ---- buffers sized by the grids ----
   c->part_stride = (c->grad_rows + 31) & ~31;
-  c->grad_part.alloc((size_t)c->part_stride * c->n_params);
+  c->grad_part.alloc((size_t)c->part_stride * c->n_params, c->stream);
   a.part_stride = c->part_stride;
-  c->loss_part.alloc((size_t)std::max(c->loss_rows, std::max(c->grid_contract, c->grid_cc)) * vpg::kLpWords);
-  c->red.alloc((size_t)c->n_params + vpg::kLpWords);
+  c->loss_part.alloc((size_t)std::max(c->loss_rows, std::max(c->grid_contract, c->grid_cc)) * vpg::kLpWords, c->stream);
+  c->red.alloc((size_t)c->n_params + vpg::kLpWords, c->stream);
   a.grad_part = c->grad_part.p;
   if (c->split) {
     const size_t ni = (size_t)c->n_int;
-    c->fu.alloc(P_local);
-    c->fux.alloc(P_local);
-    c->fuy.alloc(P_local);
-    c->feps.alloc(P_local);
-    c->uxb.alloc(ni);
-    c->uyb.alloc(ni);
-    c->eb.alloc(ni);
-    c->ub.alloc((size_t)c->n_bnd + c->n_sen);
+    c->fu.alloc(P_local, c->stream);
+    c->fux.alloc(P_local, c->stream);
+    c->fuy.alloc(P_local, c->stream);
+    c->feps.alloc(P_local, c->stream);
+    c->uxb.alloc(ni, c->stream);
+    c->uyb.alloc(ni, c->stream);
+    c->eb.alloc(ni, c->stream);
+    c->ub.alloc((size_t)c->n_bnd + c->n_sen, c->stream);
     a.loss_part = c->loss_part.p + (size_t)(c->grid_contract + c->grid_pen) * vpg::kLpWords;
     a.in_ub = c->ub.p;
     a.in_uxb = c->uxb.p;
@@ -490,7 +488,7 @@ void configure(vpinn_gpu_ctx* c) {
   } else {
     a.loss_part = c->loss_part.p;
   }
-  c->e_scalar.alloc(1);
+  c->e_scalar.alloc(1, c->stream);
 }
 
 void launch_fused(vpinn_gpu_ctx* c, const vpg::StepArgs& a) {
@@ -854,10 +852,10 @@ int vpinn_gpu_create(const vpinn_gpu_problem* pb, vpinn_gpu_ctx** out) {
     const size_t TQ = (size_t)c->T * c->Q;
     const float* src[3] = {pb->grad_x, pb->grad_y, pb->test};
     for (int t = 0; t < c->nt; ++t) {
-      c->tens[t].alloc(TQ * c->E);
+      c->tens[t].alloc(TQ * c->E, c->stream);
       c->tens[t].upload(src[t] + TQ * e0, TQ * c->E, c->stream);
     }
-    c->forcing.alloc((size_t)c->T * c->E);
+    c->forcing.alloc((size_t)c->T * c->E, c->stream);
     c->forcing.upload(pb->forcing + (size_t)c->T * e0, (size_t)c->T * c->E, c->stream);
     // points: cast double -> Real exactly like points_to_matrix (network.hpp:376-384)
     std::vector<float2> hp;
@@ -868,21 +866,21 @@ int vpinn_gpu_create(const vpinn_gpu_problem* pb, vpinn_gpu_ctx** out) {
     for (long long i = e0 * pb->n_quad; i < e1 * pb->n_quad; ++i) push(i);
     for (long long i = b0; i < b1; ++i) push(pb->n_interior + i);
     for (long long i = s0; i < s1; ++i) push(pb->n_interior + NB + i);
-    c->pts.alloc(hp.size());
+    c->pts.alloc(hp.size(), c->stream);
     c->pts.upload(hp.data(), hp.size(), c->stream);
     std::vector<float> bv, sv;
     for (long long i = b0; i < b1; ++i) bv.push_back((float)pb->boundary_values[i]);
     for (long long i = s0; i < s1; ++i) sv.push_back((float)pb->sensor_values[i]);
-    c->bval.alloc(bv.size());
+    c->bval.alloc(bv.size(), c->stream);
     c->bval.upload(bv.data(), bv.size(), c->stream);
-    c->sval.alloc(sv.size());
+    c->sval.alloc(sv.size(), c->stream);
     c->sval.upload(sv.data(), sv.size(), c->stream);
 
-    c->params.alloc(c->n_params);
-    c->m.alloc(c->n_params);
-    c->v.alloc(c->n_params);
-    c->st.alloc(1);
-    c->ticket.alloc(1);
+    c->params.alloc(c->n_params, c->stream);
+    c->m.alloc(c->n_params, c->stream);
+    c->v.alloc(c->n_params, c->stream);
+    c->st.alloc(1, c->stream);
+    c->ticket.alloc(1, c->stream);
     configure(c.get());
     reset_state(c.get(), LLONG_MAX, nullptr);
     CK(cudaStreamSynchronize(c->stream));
@@ -1017,13 +1015,13 @@ int vpinn_gpu_train(vpinn_gpu_ctx* c, const vpinn_gpu_train_spec* spec,
       c1[t - 1] = 1.0f - (float)std::pow(0.9, double(t));
       c2[t - 1] = 1.0f - (float)std::pow(0.999, double(t));
     }
-    c->lr_tab.alloc(iters);
-    c->c1_tab.alloc(iters);
-    c->c2_tab.alloc(iters);
+    c->lr_tab.alloc(iters, c->stream);
+    c->c1_tab.alloc(iters, c->stream);
+    c->c2_tab.alloc(iters, c->stream);
     c->lr_tab.upload(lr.data(), iters, c->stream);
     c->c1_tab.upload(c1.data(), iters, c->stream);
     c->c2_tab.upload(c2.data(), iters, c->stream);
-    c->rec.alloc(iters);
+    c->rec.alloc(iters, c->stream);
     // tables were reallocated: drop graphs that captured the old pointers
     for (auto it = c->graphs.begin(); it != c->graphs.end();) {
       if (std::get<0>(it->first) == 2) {
@@ -1098,11 +1096,11 @@ int vpinn_gpu_forward(vpinn_gpu_ctx* c, const double* points, int64_t n, int ord
     for (int64_t i = 0; i < n; ++i) hp[i] = make_float2((float)points[2 * i], (float)points[2 * i + 1]);
     DBuf<float2> dp;
     DBuf<float> du, dux, duy, de;
-    dp.alloc(n);
-    du.alloc(n);
-    dux.alloc(n);
-    duy.alloc(n);
-    de.alloc(n);
+    dp.alloc(n, c->stream);
+    du.alloc(n, c->stream);
+    dux.alloc(n, c->stream);
+    duy.alloc(n, c->stream);
+    de.alloc(n, c->stream);
     dp.upload(hp.data(), n, c->stream);
     vpg::StepArgs f = c->sargs;
     f.fwd_pts = dp.p;
@@ -1143,15 +1141,15 @@ int vpinn_gpu_contract(vpinn_gpu_ctx* c, const float* du_dx, const float* du_dy,
     const size_t ni = (size_t)c->n_int;
     DBuf<float> ux, uy, ep, oxb, oyb, oeb, res, es;
     DBuf<double> lp;
-    ux.alloc(ni);
-    uy.alloc(ni);
-    ep.alloc(ni);
-    oxb.alloc(ni);
-    oyb.alloc(ni);
-    oeb.alloc(ni);
-    res.alloc((size_t)c->E * c->T);
-    es.alloc(1);
-    lp.alloc((size_t)std::max(c->grid_contract, c->grid_cc) * vpg::kLpWords);
+    ux.alloc(ni, c->stream);
+    uy.alloc(ni, c->stream);
+    ep.alloc(ni, c->stream);
+    oxb.alloc(ni, c->stream);
+    oyb.alloc(ni, c->stream);
+    oeb.alloc(ni, c->stream);
+    res.alloc((size_t)c->E * c->T, c->stream);
+    es.alloc(1, c->stream);
+    lp.alloc((size_t)std::max(c->grid_contract, c->grid_cc) * vpg::kLpWords, c->stream);
     ux.upload(du_dx, ni, c->stream);
     uy.upload(du_dy, ni, c->stream);
     if (eps) ep.upload(eps, ni, c->stream);
@@ -1182,17 +1180,17 @@ int vpinn_gpu_time_contract(vpinn_gpu_ctx* c, int reps, double* ms_per_launch, d
     const size_t ni = (size_t)c->n_int;
     DBuf<float> ux, uy, ep, oxb, oyb, oeb, es;
     DBuf<double> lp;
-    ux.alloc(ni);
-    uy.alloc(ni);
-    ep.alloc(ni);
-    oxb.alloc(ni);
-    oyb.alloc(ni);
-    oeb.alloc(ni);
-    es.alloc(1);
-    lp.alloc((size_t)std::max(c->grid_contract, c->grid_cc) * vpg::kLpWords);
+    ux.alloc(ni, c->stream);
+    uy.alloc(ni, c->stream);
+    ep.alloc(ni, c->stream);
+    oxb.alloc(ni, c->stream);
+    oyb.alloc(ni, c->stream);
+    oeb.alloc(ni, c->stream);
+    es.alloc(1, c->stream);
+    lp.alloc((size_t)std::max(c->grid_contract, c->grid_cc) * vpg::kLpWords, c->stream);
     // L2 flush buffer (> 126 MB L2) between launches so each launch streams HBM
     DBuf<char> flush;
-    flush.alloc((size_t)256 << 20);
+    flush.alloc((size_t)256 << 20, c->stream);
     cudaEvent_t e0, e1;
     CK(cudaEventCreate(&e0));
     CK(cudaEventCreate(&e1));
@@ -1298,7 +1296,7 @@ int vpinn_gpu_phase_clock(vpinn_gpu_ctx* c, long long* out, int n) {
 int vpinn_gpu_flush_l2(vpinn_gpu_ctx* c) {
   return guarded([&] {
     set_dev(c);
-    if (!c->flush.p) c->flush.alloc((size_t)256 << 20);
+    if (!c->flush.p) c->flush.alloc((size_t)256 << 20, c->stream);
     flush_l2_now(c, c->flush.p);
   });
 }
@@ -1308,10 +1306,10 @@ int vpinn_gpu_tc_probe(int device, int mode, const float* A, const float* W, con
     if (mode < 0 || mode > 3) throw Fail{VPINN_ERR_CONFIG, "tc_probe: mode must be 0..3"};
     CK(cudaSetDevice(device));
     DBuf<float> dA, dW, dH, dO;
-    dA.alloc(128 * 32);
-    dW.alloc(32 * 32);
-    dH.alloc(128 * 32);
-    dO.alloc(128 * 32 + 128 * 96);
+    dA.alloc(128 * 32, 0);
+    dW.alloc(32 * 32, 0);
+    dH.alloc(128 * 32, 0);
+    dO.alloc(128 * 32 + 128 * 96, 0);
     CK(cudaMemcpy(dA.p, A, sizeof(float) * 128 * 32, cudaMemcpyHostToDevice));
     CK(cudaMemcpy(dW.p, W, sizeof(float) * 32 * 32, cudaMemcpyHostToDevice));
     if (H) CK(cudaMemcpy(dH.p, H, sizeof(float) * 128 * 32, cudaMemcpyHostToDevice));
@@ -1329,7 +1327,7 @@ int vpinn_gpu_measure_ffma_peak(int device, double* tflops) {
     cudaDeviceProp prop;
     CK(cudaGetDeviceProperties(&prop, device));
     DBuf<float> out;
-    out.alloc(256);
+    out.alloc(256, 0);
     const int blocks = prop.multiProcessorCount * 8, iters = 4096;
     cudaEvent_t e0, e1;
     CK(cudaEventCreate(&e0));
