@@ -65,6 +65,26 @@ extern "C" {
 typedef struct vpinn_gpu_ctx vpinn_gpu_ctx;
 
 /* Everything one step needs, in the reference layouts (host memory). */
+/* Device-side assembly input (replaces the host's
+ * assemble_element_tensors / assemble_forcing, reference
+ * proj/include/vpinn/assembly.hpp:58-135): the mesh, the reference
+ * tensor-product quadrature rule and the reference-square basis tables
+ * (basis.hpp:24-60, row j = jy*n + jx), from which the device builds the
+ * premultiplier tensors, the forcing and the interior quadrature points,
+ * bit-identical to the host path (double geometry, cast at store). */
+typedef struct vpinn_gpu_assembly {
+  int64_t n_nodes;
+  const double* nodes;     /* [n_nodes][2] */
+  const int32_t* elements; /* [n_elem][4], counter-clockwise */
+  const double* xi;        /* [n_quad] */
+  const double* eta;       /* [n_quad] */
+  const double* weights;   /* [n_quad] */
+  const double* basis_val; /* [n_test][n_quad] */
+  const double* basis_dxi;
+  const double* basis_deta;
+  const char* forcing; /* named field of the host library (zero, one, sin2pi_f, gear_f, ...) */
+} vpinn_gpu_assembly;
+
 typedef struct vpinn_gpu_problem {
   /* ElementTensors<float> (assembly.hpp:34-54): slices [k][j][q] row-major,
    * entry (k*n_test + j)*n_quad + q.  test may be NULL when there is no
@@ -96,6 +116,10 @@ typedef struct vpinn_gpu_problem {
    * contiguously (rank r owns [floor(r*N/W), floor((r+1)*N/W))) */
   int32_t device;
   int32_t rank, world_size;
+  /* non-NULL: tensors, forcing and the interior points are assembled on the
+   * device from this input; grad_x/grad_y/test/forcing are then ignored and
+   * points holds only [boundary | sensors] (n_interior = n_elem*n_quad) */
+  const vpinn_gpu_assembly* assembly;
 } vpinn_gpu_problem;
 
 /* TrainConfig subset (trainer.hpp:64-97) */
@@ -207,6 +231,18 @@ int vpinn_gpu_profile_step(vpinn_gpu_ctx* ctx, int reps, double* ms_mlp, double*
 /* Write 256 MB (> the 126 MB L2) on the context stream: benchmarks call it
  * between timed epochs so every epoch streams its tensors from HBM. */
 int vpinn_gpu_flush_l2(vpinn_gpu_ctx* ctx);
+
+/* Device buffers released by destroyed contexts are cached per size for
+ * the next context (no cudaMalloc / device-synchronizing cudaFree on
+ * re-creation); this returns every cached block to the driver. */
+int vpinn_gpu_release_cached_memory(void);
+
+/* Device-side assembly as a standalone call (host outputs, each may be NULL
+ * except grad_x/grad_y): the same kernels vpinn_gpu_create runs for a
+ * problem with an assembly input.  Returns 3 (mesh) for a cell with a
+ * non-positive Jacobian determinant (DegenerateElementError, first cell). */
+int vpinn_gpu_assemble(int device, int32_t n_elem, int32_t n_test, int32_t n_quad, const vpinn_gpu_assembly* in,
+                       float* grad_x, float* grad_y, float* test, float* forcing, double* quad_points);
 
 /* Diagnostics: clock64() phase marks of CTA 0 in the last tensor-core step
  * launch (enabled by VPINN_PHASE_CLOCK=1 in the environment at create;

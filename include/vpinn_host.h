@@ -70,6 +70,12 @@ int vpinn_host_gear_msh_text(int n_r, int n_t, char* buf, size_t cap, size_t* le
 /* ---- problems ---- */
 int vpinn_host_problem_from_config(const char* config_json, const char* base_dir,
                                    const vpinn_mesh_source* mesh, vpinn_host_problem** out);
+/* flags: VPINN_HOST_DEVICE_ASSEMBLY skips the host premultiplier assembly
+ * (assembly.hpp:58-135); the view then carries a vpinn_gpu_assembly input
+ * and vpinn_gpu_create builds the tensors on the device */
+#define VPINN_HOST_DEVICE_ASSEMBLY 1
+int vpinn_host_problem_from_config_ex(const char* config_json, const char* base_dir,
+                                      const vpinn_mesh_source* mesh, int flags, vpinn_host_problem** out);
 /* counts[8] = E, T, Q, n_interior, n_boundary, n_sensors, n_params, precision_downgraded */
 void vpinn_host_problem_counts(const vpinn_host_problem* p, int64_t* counts);
 /* plain-array view (pointers into p, valid while p lives) */

@@ -20,6 +20,15 @@ class NativeLibraryMissing(RuntimeError):
     pass
 
 
+class Assembly(C.Structure):
+    _fields_ = [
+        ("n_nodes", C.c_int64), ("nodes", C.c_void_p), ("elements", C.c_void_p),
+        ("xi", C.c_void_p), ("eta", C.c_void_p), ("weights", C.c_void_p),
+        ("basis_val", C.c_void_p), ("basis_dxi", C.c_void_p), ("basis_deta", C.c_void_p),
+        ("forcing", C.c_char_p),
+    ]
+
+
 class Problem(C.Structure):
     _fields_ = [
         ("n_elem", C.c_int32), ("n_test", C.c_int32), ("n_quad", C.c_int32),
@@ -33,6 +42,7 @@ class Problem(C.Structure):
         ("eps_source", C.c_int32), ("eps_scalar_index", C.c_int32),
         ("tau", C.c_double), ("gamma", C.c_double),
         ("device", C.c_int32), ("rank", C.c_int32), ("world_size", C.c_int32),
+        ("assembly", C.c_void_p),
     ]
 
 
@@ -92,6 +102,8 @@ def _declare(L):
         "vpinn_gpu_tc_probe": (i32, [i32, i32, vp, vp, vp, vp]),
         "vpinn_gpu_flush_l2": (i32, [vp]),
         "vpinn_gpu_phase_clock": (i32, [vp, vp, i32]),
+        "vpinn_gpu_assemble": (i32, [i32, i32, i32, i32, vp, vp, vp, vp, vp, vp]),
+        "vpinn_gpu_release_cached_memory": (i32, []),
         "vpinn_gpu_nccl_unique_id": (i32, [vp]),
         "vpinn_gpu_attach_comm": (i32, [vp, vp, i32, i32]),
     }

@@ -65,7 +65,10 @@ def build(verbose: bool = False, jobs: int | None = None, force: bool = False) -
         o = os.path.join(OBJ, os.path.basename(s) + ".o")
         objs.append(o)
         if force or _stale(s, o, hdr_mtime):
-            cmds.append([NVCC, "-std=c++20", *ARCH, "-O3", "-lineinfo", "-Xptxas", "-v", *extra,
+            # assemble.cu: no FMA contraction, so the double geometry is the
+            # host's bits (the host is built with -ffp-contract=off)
+            per_file = ["--fmad=false"] if os.path.basename(s) == "assemble.cu" else []
+            cmds.append([NVCC, "-std=c++20", *ARCH, "-O3", "-lineinfo", "-Xptxas", "-v", *extra, *per_file,
                          "-Xcompiler", "-fPIC", "-Xcompiler", "-ffp-contract=off",
                          "--expt-relaxed-constexpr", *INCLUDES, "-c", s, "-o", o])
     for s in cpp:

@@ -10,6 +10,7 @@
 #include <cstdlib>
 #include <limits>
 #include <map>
+#include <mutex>
 #include <memory>
 #include <string>
 #include <tuple>
@@ -17,6 +18,7 @@
 
 #include <nccl.h>
 
+#include "assemble.h"
 #include "aux_kernels.cuh"
 #include "contract_cells.cuh"
 #include "tc_selftest.cuh"
@@ -55,18 +57,67 @@ int guarded(F&& f) {
   }
 }
 
+// Device-memory block cache: blocks released by contexts are kept per device
+// and exact byte size and handed to the next allocation of that size, so
+// re-creating a context (sweeps, parameter studies, the e2e bench) costs no
+// cudaMalloc / cudaFree (cudaFree synchronizes the whole device).  Owners
+// release only idle blocks (a context synchronizes its stream first).
+struct BlockCache {
+  std::mutex mu;
+  std::map<std::pair<int, size_t>, std::vector<void*>> blocks;
+  size_t cached = 0;
+  static constexpr size_t kCap = size_t(8) << 30;
+  void* get(size_t bytes) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> g(mu);
+    auto it = blocks.find({dev, bytes});
+    if (it == blocks.end() || it->second.empty()) return nullptr;
+    void* p = it->second.back();
+    it->second.pop_back();
+    cached -= bytes;
+    return p;
+  }
+  void put(void* p, size_t bytes) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    {
+      std::lock_guard<std::mutex> g(mu);
+      if (cached + bytes <= kCap) {
+        blocks[{dev, bytes}].push_back(p);
+        cached += bytes;
+        return;
+      }
+    }
+    cudaFree(p);
+  }
+  void trim() {
+    std::lock_guard<std::mutex> g(mu);
+    for (auto& kv : blocks) {
+      cudaSetDevice(kv.first.first);
+      for (void* p : kv.second) cudaFree(p);
+    }
+    blocks.clear();
+    cached = 0;
+  }
+};
+BlockCache& block_cache() {
+  static BlockCache* c = new BlockCache;  // never destroyed: no teardown-order races at exit
+  return *c;
+}
+
 template <typename T>
 struct DBuf {
   T* p = nullptr;
-  size_t n = 0;
+  size_t n = 0, bytes = 0;
   DBuf() = default;
   DBuf(const DBuf&) = delete;
   DBuf& operator=(const DBuf&) = delete;
   ~DBuf() { release(); }
   void release() {
-    if (p) cudaFree(p);
+    if (p) block_cache().put(p, bytes);
     p = nullptr;
-    n = 0;
+    n = bytes = 0;
   }
   // 64 bytes of slack: 1-D bulk copies read 16-byte aligned supersets
   // zero-filled on stream s, i.e. ordered before anything later enqueued on s
@@ -75,11 +126,16 @@ struct DBuf {
   void alloc(size_t count, cudaStream_t s) {
     release();
     n = count;
-    CK(cudaMalloc(&p, std::max<size_t>(count, 1) * sizeof(T) + 64));
-    CK(cudaMemsetAsync(p, 0, std::max<size_t>(count, 1) * sizeof(T) + 64, s));
+    bytes = (std::max<size_t>(count, 1) * sizeof(T) + 64 + 255) & ~size_t(255);
+    p = static_cast<T*>(block_cache().get(bytes));
+    if (!p) CK(cudaMalloc(&p, bytes));
+    CK(cudaMemsetAsync(p, 0, bytes, s));
   }
   void upload(const T* h, size_t count, cudaStream_t s) {
     if (count) CK(cudaMemcpyAsync(p, h, count * sizeof(T), cudaMemcpyHostToDevice, s));
+  }
+  void upload_at(size_t at, const T* h, size_t count, cudaStream_t s) {
+    if (count) CK(cudaMemcpyAsync(p + at, h, count * sizeof(T), cudaMemcpyHostToDevice, s));
   }
 };
 
@@ -198,6 +254,7 @@ struct vpinn_gpu_ctx {
 
   ~vpinn_gpu_ctx() {
     if (device >= 0) cudaSetDevice(device);
+    if (stream) cudaStreamSynchronize(stream);  // buffers go back to the block cache idle
     for (auto& kv : graphs) cudaGraphExecDestroy(kv.second);
     if (comm && nccl().comm_destroy) nccl().comm_destroy(comm);
     if (h_flag) cudaFreeHost(h_flag);
@@ -714,6 +771,72 @@ long long launches_per_epoch(const vpinn_gpu_ctx* c) {
 }  // namespace
 
 // ===========================================================================
+namespace {
+int field_id(const char* name) {
+  static const char* names[vpg::kFieldCount] = {"zero",     "one",     "sin2pi_u", "sin2pi_f", "sin4pi_u",
+                                                "sin4pi_f", "sin8pi_u", "sin8pi_f", "gear_f",   "bump_u",
+                                                "bump_f",   "sinpi_u",  "sincos_eps", "sinpi_vareps_f"};
+  if (!name) return vpg::kFieldZero;
+  for (int i = 0; i < vpg::kFieldCount; ++i)
+    if (std::strcmp(name, names[i]) == 0) return i;
+  throw Fail{VPINN_ERR_CONFIG, std::string("device assembly: unknown field '") + name + "'"};
+}
+
+// the small assembly inputs on the device (mesh, rule, basis tables)
+struct AsmUpload {
+  DBuf<double> nodes, xi, eta, w, bval, bdxi, bdeta;
+  DBuf<int32_t> elems;
+  DBuf<int> bad;
+  vpg::AsmInput in{};
+  void load(const vpinn_gpu_assembly* a, int64_t n_elem, int T, int Q, cudaStream_t s) {
+    if (!a->nodes || !a->elements || !a->xi || !a->eta || !a->weights || !a->basis_val || !a->basis_dxi ||
+        !a->basis_deta || a->n_nodes < 1)
+      throw Fail{VPINN_ERR_CONFIG, "device assembly: incomplete input"};
+    for (int64_t i = 0; i < 4 * n_elem; ++i)
+      if (a->elements[i] < 0 || a->elements[i] >= a->n_nodes)
+        throw Fail{VPINN_ERR_MESH, "device assembly: element node index out of range"};
+    in.field = field_id(a->forcing);
+    nodes.alloc(2 * a->n_nodes, s);
+    nodes.upload(a->nodes, 2 * a->n_nodes, s);
+    elems.alloc(4 * n_elem, s);
+    elems.upload(a->elements, 4 * n_elem, s);
+    xi.alloc(Q, s);
+    xi.upload(a->xi, Q, s);
+    eta.alloc(Q, s);
+    eta.upload(a->eta, Q, s);
+    w.alloc(Q, s);
+    w.upload(a->weights, Q, s);
+    bval.alloc((size_t)T * Q, s);
+    bval.upload(a->basis_val, (size_t)T * Q, s);
+    bdxi.alloc((size_t)T * Q, s);
+    bdxi.upload(a->basis_dxi, (size_t)T * Q, s);
+    bdeta.alloc((size_t)T * Q, s);
+    bdeta.upload(a->basis_deta, (size_t)T * Q, s);
+    bad.alloc(1, s);
+    const int big = INT_MAX;
+    bad.upload(&big, 1, s);
+    in.nodes = nodes.p;
+    in.elems = elems.p;
+    in.T = T;
+    in.Q = Q;
+    in.xi = xi.p;
+    in.eta = eta.p;
+    in.w = w.p;
+    in.bval = bval.p;
+    in.bdxi = bdxi.p;
+    in.bdeta = bdeta.p;
+  }
+  void check(cudaStream_t s) {
+    int b = INT_MAX;
+    CK(cudaMemcpyAsync(&b, bad.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (b != INT_MAX)
+      throw Fail{VPINN_ERR_MESH, "assemble: element " + std::to_string(b) +
+                                     " has non-positive jacobian determinant"};
+  }
+};
+}  // namespace
+
 extern "C" {
 
 const char* vpinn_gpu_last_error(void) { return g_err.c_str(); }
@@ -754,7 +877,7 @@ int vpinn_gpu_create(const vpinn_gpu_problem* pb, vpinn_gpu_ctx** out) {
     // ---- validation (contract checks of losses.hpp:70-84, network.hpp:66-76) ----
     if (pb->n_elem < 1 || pb->n_test < 1 || pb->n_quad < 1)
       throw Fail{VPINN_ERR_CONFIG, "n_elem, n_test, n_quad must be >= 1"};
-    if (!pb->grad_x || !pb->grad_y || !pb->forcing || !pb->points)
+    if (!pb->assembly && (!pb->grad_x || !pb->grad_y || !pb->forcing || !pb->points))
       throw Fail{VPINN_ERR_NUMERIC, "tensor kernel: tensors/forcing/points missing"};
     if (pb->n_interior != (int64_t)pb->n_elem * pb->n_quad)
       throw Fail{VPINN_ERR_NUMERIC, "evaluation does not cover the interior quadrature points"};
@@ -784,7 +907,7 @@ int vpinn_gpu_create(const vpinn_gpu_problem* pb, vpinn_gpu_ctx** out) {
                                        ", outputs " + std::to_string(C) + ", activation " +
                                        (act ? "sigmoid" : "tanh") + ")"};
     const bool conv = pb->bx != 0.0f || pb->by != 0.0f;
-    if (conv && !pb->test) throw Fail{VPINN_ERR_NUMERIC, "convection needs the test tensor"};
+    if (conv && !pb->test && !pb->assembly) throw Fail{VPINN_ERR_NUMERIC, "convection needs the test tensor"};
     const int W = std::max(1, pb->world_size), R = pb->rank;
     if (R < 0 || R >= W) throw Fail{VPINN_ERR_CONFIG, "rank out of range"};
 
@@ -850,24 +973,43 @@ int vpinn_gpu_create(const vpinn_gpu_problem* pb, vpinn_gpu_ctx** out) {
     c->nranks = W;
 
     const size_t TQ = (size_t)c->T * c->Q;
-    const float* src[3] = {pb->grad_x, pb->grad_y, pb->test};
-    for (int t = 0; t < c->nt; ++t) {
-      c->tens[t].alloc(TQ * c->E, c->stream);
-      c->tens[t].upload(src[t] + TQ * e0, TQ * c->E, c->stream);
-    }
-    c->forcing.alloc((size_t)c->T * c->E, c->stream);
-    c->forcing.upload(pb->forcing + (size_t)c->T * e0, (size_t)c->T * c->E, c->stream);
     // points: cast double -> Real exactly like points_to_matrix (network.hpp:376-384)
     std::vector<float2> hp;
     hp.reserve((size_t)c->n_int + c->n_bnd + c->n_sen);
     auto push = [&](long long i) {
       hp.push_back(make_float2((float)pb->points[2 * i], (float)pb->points[2 * i + 1]));
     };
-    for (long long i = e0 * pb->n_quad; i < e1 * pb->n_quad; ++i) push(i);
-    for (long long i = b0; i < b1; ++i) push(pb->n_interior + i);
-    for (long long i = s0; i < s1; ++i) push(pb->n_interior + NB + i);
-    c->pts.alloc(hp.size(), c->stream);
-    c->pts.upload(hp.data(), hp.size(), c->stream);
+    for (int t = 0; t < c->nt; ++t) c->tens[t].alloc(TQ * c->E, c->stream);
+    c->forcing.alloc((size_t)c->T * c->E, c->stream);
+    if (!pb->assembly) {
+      const float* src[3] = {pb->grad_x, pb->grad_y, pb->test};
+      for (int t = 0; t < c->nt; ++t) c->tens[t].upload(src[t] + TQ * e0, TQ * c->E, c->stream);
+      c->forcing.upload(pb->forcing + (size_t)c->T * e0, (size_t)c->T * c->E, c->stream);
+      for (long long i = e0 * pb->n_quad; i < e1 * pb->n_quad; ++i) push(i);
+      for (long long i = b0; i < b1; ++i) push(pb->n_interior + i);
+      for (long long i = s0; i < s1; ++i) push(pb->n_interior + NB + i);
+      c->pts.alloc(hp.size(), c->stream);
+      c->pts.upload(hp.data(), hp.size(), c->stream);
+    } else {
+      // device-side assembly of this rank's cells straight into the buffers;
+      // the interior points land in the head of the evaluation batch
+      for (long long i = b0; i < b1; ++i) push(i);
+      for (long long i = s0; i < s1; ++i) push(NB + i);
+      c->pts.alloc((size_t)c->n_int + hp.size(), c->stream);
+      c->pts.upload_at(c->n_int, hp.data(), hp.size(), c->stream);
+      AsmUpload up;
+      up.load(pb->assembly, pb->n_elem, c->T, c->Q, c->stream);
+      DBuf<float> tv_tmp, fq;
+      float* tv = c->nt == 3 ? c->tens[2].p : nullptr;
+      if (!tv) {
+        tv_tmp.alloc(TQ * c->E, c->stream);
+        tv = tv_tmp.p;
+      }
+      fq.alloc((size_t)c->n_int, c->stream);
+      CK(vpg::assemble_on_device(up.in, e0, c->E, c->tens[0].p, c->tens[1].p, tv, c->forcing.p, nullptr,
+                                 c->pts.p, fq.p, up.bad.p, c->stream));
+      up.check(c->stream);
+    }
     std::vector<float> bv, sv;
     for (long long i = b0; i < b1; ++i) bv.push_back((float)pb->boundary_values[i]);
     for (long long i = s0; i < s1; ++i) sv.push_back((float)pb->sensor_values[i]);
@@ -1278,6 +1420,40 @@ int vpinn_gpu_profile_step(vpinn_gpu_ctx* c, int reps, double* ms_mlp, double* m
     *ms_mlp = t[0] / reps;
     *ms_reduce = t[1] / reps;
     *ms_adam = t[2] / reps;
+  });
+}
+
+int vpinn_gpu_release_cached_memory(void) {
+  return guarded([&] { block_cache().trim(); });
+}
+
+int vpinn_gpu_assemble(int device, int32_t n_elem, int32_t n_test, int32_t n_quad, const vpinn_gpu_assembly* in,
+                       float* grad_x, float* grad_y, float* test, float* forcing, double* quad_points) {
+  return guarded([&] {
+    if (!in || !grad_x || !grad_y || n_elem < 1 || n_test < 1 || n_quad < 1)
+      throw Fail{VPINN_ERR_CONFIG, "vpinn_gpu_assemble: bad arguments"};
+    CK(cudaSetDevice(device));
+    cudaStream_t s = nullptr;  // legacy default stream: ordered with the zero fills
+    AsmUpload up;
+    up.load(in, n_elem, n_test, n_quad, s);
+    const size_t n = (size_t)n_elem * n_test * n_quad;
+    DBuf<float> gx, gy, tv, fc, fq;
+    DBuf<double> qp;
+    gx.alloc(n, s);
+    gy.alloc(n, s);
+    tv.alloc(n, s);
+    fc.alloc((size_t)n_elem * n_test, s);
+    fq.alloc((size_t)n_elem * n_quad, s);
+    qp.alloc((size_t)2 * n_elem * n_quad, s);
+    CK(vpg::assemble_on_device(up.in, 0, n_elem, gx.p, gy.p, tv.p, forcing ? fc.p : nullptr, qp.p, nullptr, fq.p,
+                               up.bad.p, s));
+    up.check(s);
+    CK(cudaMemcpy(grad_x, gx.p, sizeof(float) * n, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(grad_y, gy.p, sizeof(float) * n, cudaMemcpyDeviceToHost));
+    if (test) CK(cudaMemcpy(test, tv.p, sizeof(float) * n, cudaMemcpyDeviceToHost));
+    if (forcing) CK(cudaMemcpy(forcing, fc.p, sizeof(float) * n_elem * n_test, cudaMemcpyDeviceToHost));
+    if (quad_points)
+      CK(cudaMemcpy(quad_points, qp.p, sizeof(double) * 2 * n_elem * n_quad, cudaMemcpyDeviceToHost));
   });
 }
 

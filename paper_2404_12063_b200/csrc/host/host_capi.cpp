@@ -139,13 +139,18 @@ int vpinn_host_gear_msh_text(int n_r, int n_t, char* buf, size_t cap, size_t* le
 
 int vpinn_host_problem_from_config(const char* json, const char* base_dir, const vpinn_mesh_source* mesh,
                                    vpinn_host_problem** out) {
+  return vpinn_host_problem_from_config_ex(json, base_dir, mesh, 0, out);
+}
+
+int vpinn_host_problem_from_config_ex(const char* json, const char* base_dir, const vpinn_mesh_source* mesh,
+                                      int flags, vpinn_host_problem** out) {
   *out = nullptr;
   return guarded([&] {
     auto p = std::make_unique<vpinn_host_problem>();
     p->cfg = vpinn::parse_config_text(json ? json : "", "<config>", base_dir ? base_dir : "");
     std::optional<vpinn::Mesh> premade;
     if (mesh && mesh->kind != VPINN_MESH_FROM_CONFIG) premade = mesh_from_source(*mesh);
-    p->bp = vpinn::build_problem(p->cfg, std::move(premade));
+    p->bp = vpinn::build_problem(p->cfg, std::move(premade), (flags & VPINN_HOST_DEVICE_ASSEMBLY) != 0);
     const vpinn::Rule1D r1 = vpinn::gauss_rule_1d(p->cfg.disc.n_quad_per_dim, p->cfg.disc.quadrature);
     p->rule = vpinn::tensor_product_rule(r1, r1);
     *out = p.release();

@@ -27,6 +27,13 @@ struct BuiltProblem {
   ProblemAssembly pa;
   LossWeights weights;
   bool precision_downgraded = false;  // config asked for double, device computes fp32
+  // device_assembly: the premultiplier tensors, the forcing and the interior
+  // points are built on the device (vpinn_gpu_assembly); pa.tensors then
+  // only carries the sizes and pa.batch only [boundary | sensors]
+  bool device_assembly = false;
+  QuadratureRule2D rule;
+  ReferenceBasis basis;
+  std::string forcing;
 };
 
 inline Mesh build_domain_mesh(const DomainSpec& d) {
@@ -48,7 +55,8 @@ inline PdeCoefficients coefficients_from_config(const FullConfig& c) {
   return k;
 }
 
-inline BuiltProblem build_problem(const FullConfig& cfg, std::optional<Mesh> premade = {}) {
+inline BuiltProblem build_problem(const FullConfig& cfg, std::optional<Mesh> premade = {},
+                                  bool device_assembly = false) {
   if (cfg.disc.form != LossForm::weak)
     throw InvalidModeError("the B200 path implements the weak form (Algorithm 3); form 'strong' has no device kernel");
   if (cfg.disc.kernel != KernelKind::tensor)
@@ -62,8 +70,20 @@ inline BuiltProblem build_problem(const FullConfig& cfg, std::optional<Mesh> pre
   if (cfg.network.eps_scalar_init) scalars.emplace_back("eps", *cfg.network.eps_scalar_init);
   bp.net = init_network(cfg.network.layers, cfg.seed, cfg.network.activation, scalars);
   auto& pa = bp.pa;
-  pa.tensors = assemble_element_tensors(bp.mesh, basis, rule);
-  assemble_forcing(pa.tensors, lookup_field(cfg.problem.forcing));
+  bp.device_assembly = device_assembly;
+  bp.rule = rule;
+  bp.basis = basis;
+  bp.forcing = cfg.problem.forcing;
+  if (!device_assembly) {
+    pa.tensors = assemble_element_tensors(bp.mesh, basis, rule);
+    assemble_forcing(pa.tensors, lookup_field(cfg.problem.forcing));
+  } else {
+    lookup_field(cfg.problem.forcing);  // same ConfigError for an unknown name
+    if (bp.mesh.n_elements() == 0) throw InvalidArgumentError("assemble: empty mesh");
+    pa.tensors.n_elem = bp.mesh.n_elements();
+    pa.tensors.n_test = basis.n_test();
+    pa.tensors.n_quad = rule.size();
+  }
   pa.coeffs = coefficients_from_config(cfg);
   pa.boundary = sample_boundary(bp.mesh, cfg.problem.n_boundary_points, lookup_field(cfg.problem.boundary_g),
                                 cfg.problem.boundary_seed);
@@ -74,6 +94,7 @@ inline BuiltProblem build_problem(const FullConfig& cfg, std::optional<Mesh> pre
                                 cfg.problem.sensors->seed);
   }
   pa.build_batch();
+  if (device_assembly) pa.n_interior = static_cast<long long>(pa.tensors.n_elem) * pa.tensors.n_quad;
   bp.weights = cfg.training.weights;
   bp.precision_downgraded = cfg.precision == Precision::f64;
   return bp;
@@ -84,6 +105,10 @@ struct GpuView {
   vpinn_gpu_problem p{};
   std::vector<double> points, bvals, svals;
   std::vector<int32_t> sizes;
+  // device assembly input (when bp.device_assembly)
+  vpinn_gpu_assembly asm_in{};
+  std::vector<double> nodes, xi, eta, w;
+  std::vector<int32_t> elems;
 };
 
 inline std::unique_ptr<GpuView> make_gpu_view(const BuiltProblem& bp, int device = 0, int rank = 0, int world = 1) {
@@ -126,6 +151,26 @@ inline std::unique_ptr<GpuView> make_gpu_view(const BuiltProblem& bp, int device
   p.device = device;
   p.rank = rank;
   p.world_size = world;
+  if (bp.device_assembly) {
+    for (const auto& n : bp.mesh.nodes) {
+      v->nodes.push_back(n.x);
+      v->nodes.push_back(n.y);
+    }
+    for (const auto& e : bp.mesh.elements) v->elems.insert(v->elems.end(), e.begin(), e.end());
+    vpinn_gpu_assembly& a = v->asm_in;
+    a.n_nodes = bp.mesh.n_nodes();
+    a.nodes = v->nodes.data();
+    a.elements = v->elems.data();
+    a.xi = bp.rule.xi.data();
+    a.eta = bp.rule.eta.data();
+    a.weights = bp.rule.weights.data();
+    a.basis_val = bp.basis.val.data();
+    a.basis_dxi = bp.basis.dxi.data();
+    a.basis_deta = bp.basis.deta.data();
+    a.forcing = bp.forcing.c_str();
+    p.assembly = &v->asm_in;
+    p.grad_x = p.grad_y = p.test = p.forcing = nullptr;
+  }
   return v;
 }
 

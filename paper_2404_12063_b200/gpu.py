@@ -125,6 +125,30 @@ class GpuStep:
                                                    C.byref(loss), _p(res), _p(uxb), _p(uyb), _p(eb), _p(sb)))
         return loss.value, res.reshape(self.n_elem, self.n_test), uxb, uyb, eb, sb
 
+    @staticmethod
+    def assemble(nodes, cells, rule, basis, forcing="zero", device=0):
+        """Device-side assembly (vpinn_gpu_assemble): nodes [n][2], cells
+        [E][4], rule = (xi, eta, w), basis = (val, dxi, deta) [T][Q] ->
+        dict of grad_x, grad_y, test ([E][T][Q] flat), forcing ([E][T] flat),
+        quad_points [E*Q][2] (double)."""
+        nodes = np.ascontiguousarray(nodes, dtype=np.float64)
+        cells = np.ascontiguousarray(cells, dtype=np.int32)
+        xi, eta, w = (np.ascontiguousarray(a, dtype=np.float64) for a in rule)
+        val, dxi, deta = (np.ascontiguousarray(a, dtype=np.float64) for a in basis)
+        E, Q, T = cells.shape[0], xi.size, val.size // xi.size
+        a = _capi.Assembly()
+        a.n_nodes = nodes.shape[0]
+        a.nodes, a.elements, a.xi, a.eta, a.weights = _p(nodes), _p(cells), _p(xi), _p(eta), _p(w)
+        a.basis_val, a.basis_dxi, a.basis_deta = _p(val), _p(dxi), _p(deta)
+        a.forcing = forcing.encode()
+        out = {k: np.zeros(E * T * Q, np.float32) for k in ("grad_x", "grad_y", "test")}
+        out["forcing"] = np.zeros(E * T, np.float32)
+        out["quad_points"] = np.zeros((E * Q, 2))
+        _capi.check(_capi.lib().vpinn_gpu_assemble(device, E, T, Q, C.byref(a), _p(out["grad_x"]),
+                                                   _p(out["grad_y"]), _p(out["test"]), _p(out["forcing"]),
+                                                   _p(out["quad_points"])))
+        return out
+
     def download_tensor(self, which: int, n: int):
         out = np.zeros(n, dtype=np.float32)
         _capi.check(_capi.lib().vpinn_gpu_download_tensor(self.h, which, _p(out), n))

@@ -41,6 +41,8 @@ def _lib():
             "vpinn_host_gear_msh_text": (i32, [i32, i32, vp, C.c_size_t, C.POINTER(C.c_size_t)]),
             "vpinn_host_problem_from_config": (i32, [C.c_char_p, C.c_char_p, C.POINTER(MeshSource),
                                                      C.POINTER(vp)]),
+            "vpinn_host_problem_from_config_ex": (i32, [C.c_char_p, C.c_char_p, C.POINTER(MeshSource), i32,
+                                                        C.POINTER(vp)]),
             "vpinn_host_problem_counts": (None, [vp, vp]),
             "vpinn_host_problem_view": (i32, [vp, i32, i32, i32, C.POINTER(_capi.Problem)]),
             "vpinn_host_problem_params": (None, [vp, vp]),
@@ -137,17 +139,20 @@ def gear_msh_text(n_r: int, n_t: int) -> str:
 
 
 class HostProblem:
-    """build_problem(config[, premade mesh]) on the C++ host side."""
+    """build_problem(config[, premade mesh]) on the C++ host side.
+    device_assembly=True skips the host premultiplier assembly: the device
+    context builds the tensors, the forcing and the interior points itself."""
 
     def __init__(self, config: Union[dict, str], base_dir: Optional[str] = None,
-                 mesh: Optional[Union[MeshSource, Mesh]] = None):
+                 mesh: Optional[Union[MeshSource, Mesh]] = None, device_assembly: bool = False):
         text = config if isinstance(config, str) else json.dumps(config)
         src = mesh.source() if isinstance(mesh, Mesh) else mesh
         self._mesh_keep = mesh
+        self.device_assembly = device_assembly
         h = C.c_void_p()
-        _check(_lib().vpinn_host_problem_from_config(text.encode(), (base_dir or "").encode(),
-                                                     C.byref(src) if src is not None else None,
-                                                     C.byref(h)))
+        _check(_lib().vpinn_host_problem_from_config_ex(text.encode(), (base_dir or "").encode(),
+                                                        C.byref(src) if src is not None else None,
+                                                        1 if device_assembly else 0, C.byref(h)))
         self.h = h
         c = np.zeros(8, dtype=np.int64)
         _lib().vpinn_host_problem_counts(h, _p(c))
