@@ -89,6 +89,14 @@ __device__ __forceinline__ float rcp_newton(float d) {
   return fmaf(r, fmaf(-d, r, 1.0f), r);  // one Newton step
 }
 
+// ---- packed fp32x2 (FFMA2 / FMUL2 / FADD2, sm_100): two lanes of work per
+// issued instruction at the same FMA throughput, i.e. half the issue slots
+__device__ __forceinline__ float2 f2(float a, float b) { return make_float2(a, b); }
+__device__ __forceinline__ float2 f2s(float a) { return make_float2(a, a); }
+__device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) { return __ffma2_rn(a, b, c); }
+__device__ __forceinline__ float2 mul2(float2 a, float2 b) { return __fmul2_rn(a, b); }
+__device__ __forceinline__ float2 add2(float2 a, float2 b) { return __fadd2_rn(a, b); }
+
 constexpr int kActTanh = 0;
 constexpr int kActSigmoid = 1;
 
@@ -114,6 +122,26 @@ struct Act<kActTanh> {
   }
   static __device__ __forceinline__ float s1(float z) { return fmaf(-z, z, 1.0f); }
   static __device__ __forceinline__ float kap(float z) { return -2.0f * z; }
+  // two values at once, the same operations as value() in packed fp32x2
+  static __device__ __forceinline__ float2 value2(float2 x) {
+    const float2 x2 = __fmul2_rn(x, x);
+    float2 p = __ffma2_rn(f2s(-0.007364633358913433f), x2, f2s(0.021618979731563185f));
+    p = __ffma2_rn(p, x2, f2s(-0.05394892778111454f));
+    p = __ffma2_rn(p, x2, f2s(0.1333326813390213f));
+    p = __ffma2_rn(p, x2, f2s(-0.3333333262496359f));
+    const float2 small = __ffma2_rn(__fmul2_rn(x, x2), p, x);
+    const float2 ax = f2(fabsf(x.x), fabsf(x.y));
+    const float2 t = __fmul2_rn(f2(fminf(ax.x, 15.0f), fminf(ax.y, 15.0f)), f2s(2.8853900817779268f));
+    const float2 d = __fadd2_rn(f2(ex2_approx(t.x), ex2_approx(t.y)), f2s(1.0f));
+    float2 r;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r.x) : "f"(d.x));
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r.y) : "f"(d.y));
+    r = __ffma2_rn(r, __ffma2_rn(f2(-d.x, -d.y), r, f2s(1.0f)), r);  // one Newton step
+    const float2 big = __ffma2_rn(f2s(-2.0f), r, f2s(1.0f));
+    return f2(ax.x < 0.4f ? small.x : copysignf(big.x, x.x), ax.y < 0.4f ? small.y : copysignf(big.y, x.y));
+  }
+  static __device__ __forceinline__ float2 s1_2(float2 z) { return __ffma2_rn(f2(-z.x, -z.y), z, f2s(1.0f)); }
+  static __device__ __forceinline__ float2 kap2(float2 z) { return __fmul2_rn(f2s(-2.0f), z); }
 };
 
 template <>
@@ -125,6 +153,9 @@ struct Act<kActSigmoid> {
   }
   static __device__ __forceinline__ float s1(float z) { return z * (1.0f - z); }
   static __device__ __forceinline__ float kap(float z) { return 1.0f - 2.0f * z; }
+  static __device__ __forceinline__ float2 value2(float2 x) { return f2(value(x.x), value(x.y)); }
+  static __device__ __forceinline__ float2 s1_2(float2 z) { return __fmul2_rn(z, __fadd2_rn(f2s(1.0f), f2(-z.x, -z.y))); }
+  static __device__ __forceinline__ float2 kap2(float2 z) { return __ffma2_rn(f2s(-2.0f), z, f2s(1.0f)); }
 };
 
 // network.hpp:130-138

@@ -396,12 +396,18 @@ __global__ void __maxnreg__(120) tc2_step_kernel(const StepArgs a) {
   auto coff = [&](int c) { return c ? off1 : off0; };
 
   // layer 0 of this thread's chunk c (8 units) at (px, py): z and s1
+  // (unit pairs in packed fp32x2: the same IEEE operations per lane)
   auto layer0 = [&](int c, float px, float py, float (&z)[8], float (&s1)[8]) {
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      const float4 w = *reinterpret_cast<const float4*>(sW0 + 4 * (u0 + 8 * c + k));
-      z[k] = AC::value(fmaf(w.y, py, w.x * px) + w.z);
-      s1[k] = AC::s1(z[k]);
+    for (int k = 0; k < 8; k += 2) {
+      const float4 wa = *reinterpret_cast<const float4*>(sW0 + 4 * (u0 + 8 * c + k));
+      const float4 wb = *reinterpret_cast<const float4*>(sW0 + 4 * (u0 + 8 * c + k + 1));
+      const float2 pre = add2(fma2(f2(wa.y, wb.y), f2s(py), mul2(f2(wa.x, wb.x), f2s(px))), f2(wa.z, wb.z));
+      const float2 zz = AC::value2(pre), ss = AC::s1_2(zz);
+      z[k] = zz.x;
+      z[k + 1] = zz.y;
+      s1[k] = ss.x;
+      s1[k + 1] = ss.y;
     }
   };
   // X_1 (hidden-1 output) of chunk c, scaled, into buffer buf
@@ -409,10 +415,14 @@ __global__ void __maxnreg__(120) tc2_step_kernel(const StepArgs a) {
     float z[8], s1[8], tx[8], ty[8];
     layer0(c, px, py, z, s1);
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      const float2 ws = *reinterpret_cast<const float2*>(sW0s + 2 * (u0 + 8 * c + k));
-      tx[k] = s1[k] * ws.x;
-      ty[k] = s1[k] * ws.y;
+    for (int k = 0; k < 8; k += 2) {
+      const float4 ws = *reinterpret_cast<const float4*>(sW0s + 2 * (u0 + 8 * c + k));  // (wx, wy) of k, k+1
+      const float2 ss = f2(s1[k], s1[k + 1]);
+      const float2 a = mul2(ss, f2(ws.x, ws.z)), b = mul2(ss, f2(ws.y, ws.w));
+      tx[k] = a.x;
+      tx[k + 1] = a.y;
+      ty[k] = b.x;
+      ty[k + 1] = b.y;
     }
     const uint32_t o = coff(c);
     tc::st_split8_ho<true>(buf, kPart, o, z, sSc[kScSv]);
@@ -582,11 +592,18 @@ __global__ void __maxnreg__(120) tc2_step_kernel(const StepArgs a) {
         float d[8], z[8];
         tc::tmem_ld1x8_wait(dcol(0, c), d);
 #pragma unroll
-        for (int k = 0; k < 8; ++k) {
+        for (int k = 0; k < 8; k += 2) {
           const int u = u0 + 8 * c + k;
-          z[k] = AC::value(fmaf(d[k], f0, bias[u]));
-          s1v[8 * c + k] = AC::s1(z[k]) * ft;
-          if (last) ou = fmaf(sWd[u], z[k], ou);
+          const float2 zz = AC::value2(fma2(f2(d[k], d[k + 1]), f2s(f0), f2(bias[u], bias[u + 1])));
+          const float2 ss = mul2(AC::s1_2(zz), f2s(ft));
+          z[k] = zz.x;
+          z[k + 1] = zz.y;
+          s1v[8 * c + k] = ss.x;
+          s1v[8 * c + k + 1] = ss.y;
+          if (last) {
+            ou = fmaf(sWd[u], zz.x, ou);
+            ou = fmaf(sWd[u + 1], zz.y, ou);
+          }
         }
         if (!last)
           tc::st_split8_ho<true>(bufB, kPart, coff(c), z, sv);
@@ -610,9 +627,13 @@ __global__ void __maxnreg__(120) tc2_step_kernel(const StepArgs a) {
           }
         } else {
 #pragma unroll
-          for (int k = 0; k < 8; ++k) {
-            dx[k] *= s1v[8 * c + k];
-            dy[k] *= s1v[8 * c + k];
+          for (int k = 0; k < 8; k += 2) {
+            const float2 ss = f2(s1v[8 * c + k], s1v[8 * c + k + 1]);
+            const float2 a = mul2(f2(dx[k], dx[k + 1]), ss), b = mul2(f2(dy[k], dy[k + 1]), ss);
+            dx[k] = a.x;
+            dx[k + 1] = a.y;
+            dy[k] = b.x;
+            dy[k + 1] = b.y;
           }
           tc::st_split8_ho<false>(bufB + kStream, kPart, coff(c), dx, 1.f);
           tc::st_split8_ho<false>(bufB + 2 * kStream, kPart, coff(c), dy, 1.f);
@@ -851,18 +872,25 @@ __global__ void __maxnreg__(120) tc2_step_kernel(const StepArgs a) {
         tc::tmem_ld2x8_wait(dcol(1, c), dcol(2, c), dx, dy);
         float v[8], gA[8], gX[8], gY[8];
 #pragma unroll
-        for (int k = 0; k < 8; ++k) {
+        for (int k = 0; k < 8; k += 2) {
           const int u = u0 + 8 * c + k;
-          const float z = zs[k];
-          const float s1 = AC::s1(z), kp = AC::kap(z);
-          const float cc = s1 * f1;
-          const float tx = cc * dx[k], ty = cc * dy[k];
-          v[k] = fmaf(ub, z, fmaf(uxb, tx, uyb * ty));
-          const float wd = sWd[u];
-          gA[k] = wd * fmaf(s1, Ub, kp * fmaf(tx, Uxv, ty * Uyv));
-          const float sw = s1 * wd;
-          gX[k] = sw * Uxt;
-          gY[k] = sw * Uyt;
+          const float2 z = f2(zs[k], zs[k + 1]);
+          const float2 s1 = AC::s1_2(z), kp = AC::kap2(z);
+          const float2 cc = mul2(s1, f2s(f1));
+          const float2 tx = mul2(cc, f2(dx[k], dx[k + 1])), ty = mul2(cc, f2(dy[k], dy[k + 1]));
+          const float2 vv = fma2(f2s(ub), z, fma2(f2s(uxb), tx, mul2(f2s(uyb), ty)));
+          const float2 wd = f2(sWd[u], sWd[u + 1]);
+          const float2 ga = mul2(wd, fma2(s1, f2s(Ub), mul2(kp, fma2(tx, f2s(Uxv), mul2(ty, f2s(Uyv))))));
+          const float2 sw = mul2(s1, wd);
+          const float2 gx = mul2(sw, f2s(Uxt)), gy = mul2(sw, f2s(Uyt));
+          v[k] = vv.x;
+          v[k + 1] = vv.y;
+          gA[k] = ga.x;
+          gA[k + 1] = ga.y;
+          gX[k] = gx.x;
+          gX[k + 1] = gx.y;
+          gY[k] = gy.x;
+          gY[k + 1] = gy.y;
         }
         acc_units(v, kAWd, c);
         const uint32_t o = coff(c);
@@ -909,12 +937,20 @@ __global__ void __maxnreg__(120) tc2_step_kernel(const StepArgs a) {
         tc::ld_join8_ho<false>(bufB + 2 * kStream, kPart, o, 1.f, ty);
         float ga[8], gx[8], gy[8];
 #pragma unroll
-        for (int k = 0; k < 8; ++k) {
-          const float s1 = AC::s1(z[k]), kp = AC::kap(z[k]);
-          ga[k] = fmaf(s1 * A0, xa[k], (kp * AT) * fmaf(tx[k], xx[k], ty[k] * xy[k]));
-          const float sb = s1 * BT;
-          gx[k] = sb * xx[k];
-          gy[k] = sb * xy[k];
+        for (int k = 0; k < 8; k += 2) {
+          const float2 zz = f2(z[k], z[k + 1]);
+          const float2 s1 = AC::s1_2(zz), kp = AC::kap2(zz);
+          const float2 xx2 = f2(xx[k], xx[k + 1]), xy2 = f2(xy[k], xy[k + 1]);
+          const float2 inner = fma2(f2(tx[k], tx[k + 1]), xx2, mul2(f2(ty[k], ty[k + 1]), xy2));
+          const float2 g = fma2(mul2(s1, f2s(A0)), f2(xa[k], xa[k + 1]), mul2(mul2(kp, f2s(AT)), inner));
+          const float2 sb = mul2(s1, f2s(BT));
+          const float2 gxx = mul2(sb, xx2), gyy = mul2(sb, xy2);
+          ga[k] = g.x;
+          ga[k + 1] = g.y;
+          gx[k] = gxx.x;
+          gx[k + 1] = gxx.y;
+          gy[k] = gyy.x;
+          gy[k + 1] = gyy.y;
         }
         if (l == 1) {
           // ---- input layer: Wbar_0 += Abar x^T + TAxbar e_x^T + TAybar e_y^T; bbar_0 += Abar ----

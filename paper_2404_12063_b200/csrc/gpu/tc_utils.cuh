@@ -148,9 +148,11 @@ __device__ __forceinline__ void st_split8_ho(char* base, uint32_t part_stride, u
   uint32_t h[4], l[4];
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
-    const float y0 = SCALE ? v[2 * k] * s : v[2 * k], y1 = SCALE ? v[2 * k + 1] * s : v[2 * k + 1];
-    h[k] = pack_f16x2(y0, y1);
-    l[k] = pack_f16x2(y0 - f16lo(h[k]), y1 - f16hi(h[k]));
+    const float2 y = SCALE ? __fmul2_rn(make_float2(v[2 * k], v[2 * k + 1]), make_float2(s, s))
+                           : make_float2(v[2 * k], v[2 * k + 1]);
+    h[k] = pack_f16x2(y.x, y.y);
+    const float2 r = __fadd2_rn(y, make_float2(-f16lo(h[k]), -f16hi(h[k])));
+    l[k] = pack_f16x2(r.x, r.y);
   }
   *reinterpret_cast<uint4*>(base + off) = make_uint4(h[0], h[1], h[2], h[3]);
   *reinterpret_cast<uint4*>(base + part_stride + off) = make_uint4(l[0], l[1], l[2], l[3]);
@@ -163,9 +165,10 @@ __device__ __forceinline__ void ld_join8_ho(const char* base, uint32_t part_stri
   const uint32_t hw[4] = {h.x, h.y, h.z, h.w}, lw[4] = {l.x, l.y, l.z, l.w};
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
-    const float a0 = f16lo(hw[k]) + f16lo(lw[k]), a1 = f16hi(hw[k]) + f16hi(lw[k]);
-    v[2 * k] = UNSCALE ? a0 * inv_s : a0;
-    v[2 * k + 1] = UNSCALE ? a1 * inv_s : a1;
+    float2 a = __fadd2_rn(make_float2(f16lo(hw[k]), f16hi(hw[k])), make_float2(f16lo(lw[k]), f16hi(lw[k])));
+    if (UNSCALE) a = __fmul2_rn(a, make_float2(inv_s, inv_s));
+    v[2 * k] = a.x;
+    v[2 * k + 1] = a.y;
   }
 }
 // read back 8 columns as (h + l) * inv_s
