@@ -11,7 +11,10 @@ cross-rank gradient all-reduce + Adam), built through the product's C++ host
 pipeline and run through the C-ABI.  Multi-GPU: cells and penalty points
 are partitioned across ranks (strong scaling), one NCCL all-reduce per epoch.
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--no-sweep]
+
+Beside the gear line, rank 0 at N=1 adds the C2 cell-count sweep (unit
+square, 1..4,096 cells, "median ms/epoch vs cell count") and a C3 p/q sweep.
 
 --impl reference times the reference algorithm's CPU implementation (the
 plain-C++ oracle port: the reference itself cannot be built here, it needs
@@ -211,7 +214,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--sweep", action="store_true", help="also run the C2 cell-count sweep")
+    ap.add_argument("--no-sweep", action="store_true",
+                    help="skip the C2 cell-count and C3 p/q sweeps (a few seconds, rank 0 only)")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     world, rank, local, pg = dist_setup()
@@ -293,7 +297,8 @@ def main():
         except Exception as ex:  # keep the GPU line even if the CPU leg fails
             cpu = {"value": None, "unit": UNIT, "cores": 1, "kind": "port", "sample": f"failed: {ex}"}
 
-    sweep = _sweep(device) if (args.sweep and rank == 0) else None
+    sweep = _sweep(device) if (not args.no_sweep and rank == 0 and world == 1) else None
+    sweep3 = _sweep_c3(device) if (not args.no_sweep and rank == 0 and world == 1) else None
     if rank != 0:
         return
     line = {
@@ -324,6 +329,8 @@ def main():
     }
     if sweep:
         line["sweep_c2"] = sweep
+    if sweep3:
+        line["sweep_c3"] = sweep3
     print(json.dumps(line), flush=True)
 
 
@@ -452,6 +459,23 @@ def _sweep(device):
         r = host.bench_case(cfg, e, 5, 10, 0.0, 15, device)
         out.append({"cells": e * e, "median_ms": 1e3 * r["median_s"], "p10_ms": 1e3 * r["p10_s"],
                     "p90_ms": 1e3 * r["p90_s"], "quad_pt_evals_per_s": e * e * 100 / r["median_s"]})
+    return out
+
+
+def _sweep_c3(device):
+    """C3: high-frequency Poisson (sin4pi) p/q refinement on 8x8 cells: test
+    functions 5..10 per dimension, quadrature 10..40 per dimension (Q > 128
+    takes the split path: forward, standalone contraction, reverse)."""
+    from paper_2404_12063_b200 import host
+    cfg = {"problem": {"forcing": "sin4pi_f", "boundary_g": "sin4pi_u", "n_boundary_points": 400},
+           "discretization": {"n_test_per_dim": 5, "n_quad_per_dim": 10},
+           "network": {"layers": [2, 30, 30, 30, 1]},
+           "training": {"learning_rate": 1e-3, "seed": 42, "precision": "single"}}
+    out = []
+    for t, q in ((5, 10), (8, 20), (10, 20), (10, 40)):
+        r = host.bench_case(cfg, 8, t, q, 0.0, 15, device)
+        out.append({"cells": 64, "n_test": t * t, "n_quad": q * q, "median_ms": 1e3 * r["median_s"],
+                    "quad_pt_evals_per_s": 64 * q * q / r["median_s"]})
     return out
 
 

@@ -379,7 +379,11 @@ __global__ void __launch_bounds__(kCThreads) contract_kernel(const ContractArgs 
       const float* Gx = c_ptr(a, cell0, r0, stage, 0);
       const float* Gy = c_ptr(a, cell0, r0, stage, 1);
       const float* Tv = conv ? c_ptr(a, cell0, r0, stage, 2) : nullptr;
-      for (int r = tid; r < nr; r += kCThreads) {
+      // row dot products, one WARP per row (lanes over q, fixed xor tree):
+      // the large cells this kernel serves (Q > 128) make a thread-serial
+      // dot of length Q the latency chain of the whole contraction
+      const int lane = tid & 31, wid = tid >> 5;
+      for (int r = wid; r < nr; r += kCThreads / 32) {
         const int gr = r0 + r;
         const int kk = gr / a.T;
         const int j = gr - kk * a.T;
@@ -387,25 +391,30 @@ __global__ void __launch_bounds__(kCThreads) contract_kernel(const ContractArgs 
         const float* ys = sy + kk * a.Q;
         const float* gxr = Gx + (size_t)r * a.Q;
         const float* gyr = Gy + (size_t)r * a.Q;
-        float gx = 0.f, gy = 0.f;
-        for (int q = 0; q < a.Q; ++q) {
+        const float* cr = cv + kk * a.Q;
+        const float* tr = conv ? Tv + (size_t)r * a.Q : gxr;
+        float gx = 0.f, gy = 0.f, t = 0.f;
+        for (int q = lane; q < a.Q; q += 32) {
           gx = fmaf(gxr[q], xs[q], gx);
           gy = fmaf(gyr[q], ys[q], gy);
+          if (conv) t = fmaf(tr[q], cr[q], t);
         }
-        float res = spatial ? gx + gy : e_fixed * (gx + gy);
-        if (conv) {
-          const float* cr = cv + kk * a.Q;
-          const float* tr = Tv + (size_t)r * a.Q;
-          float t = 0.f;
-          for (int q = 0; q < a.Q; ++q) t = fmaf(tr[q], cr[q], t);
-          res += t;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          gx += __shfl_xor_sync(0xffffffffu, gx, o);
+          gy += __shfl_xor_sync(0xffffffffu, gy, o);
+          t += __shfl_xor_sync(0xffffffffu, t, o);
         }
-        res -= a.forcing[(size_t)(cell0 + kk) * a.T + j];
-        if (a.res) a.res[(size_t)(cell0 + kk) * a.T + j] = res;
-        rsqv[r] = res * res;
-        const float rb = a.rscale * res;
-        rbarv[r] = rb;
-        rgev[r] = rb * (gx + gy);
+        if (lane == 0) {
+          float res = spatial ? gx + gy : e_fixed * (gx + gy);
+          if (conv) res += t;
+          res -= a.forcing[(size_t)(cell0 + kk) * a.T + j];
+          if (a.res) a.res[(size_t)(cell0 + kk) * a.T + j] = res;
+          rsqv[r] = res * res;
+          const float rb = a.rscale * res;
+          rbarv[r] = rb;
+          rgev[r] = rb * (gx + gy);
+        }
       }
       __syncthreads();
       // points of the cells touched by this chunk

@@ -154,7 +154,12 @@ __device__ __forceinline__ int clamp_exp(int k) { return max(-60, min(60, k)); }
 
 }  // namespace t2
 
-template <int H, int D, int ACT>
+// MODE (step_kernel.cuh): kModeFused = the whole epoch on whole-cell tiles;
+// kModeForward = forward over a.fwd_pts, (u, ux, uy) to a.out_*;
+// kModeReverse = forward recompute + reverse from the adjoints in a.in_*
+// (the split path of cells larger than a tile: forward -> contraction ->
+// penalty -> reverse)
+template <int H, int D, int ACT, int MODE = kModeFused>
 __global__ void __maxnreg__(120) tc2_step_kernel(const StepArgs a) {
   using namespace t2;
   static_assert(H <= 31 && (D == 2 || D == 3), "tc2 step: H <= 31, 2 or 3 hidden layers");
@@ -512,9 +517,16 @@ __global__ void __maxnreg__(120) tc2_step_kernel(const StepArgs a) {
     bool interior;
     int cell0, ncell, pbase, np;
   };
+  const int n_tiles = MODE == kModeForward ? (a.n_fwd + 127) / 128
+                      : (MODE == kModeReverse ? (n_pts_all + 127) / 128 : a.n_tiles);
   auto geo = [&](int tile) {
     TileGeo g{false, 0, 0, 0, 0};
-    if (tile < a.n_int_tiles) {
+    if (MODE != kModeFused) {
+      if (tile < n_tiles) {
+        g.pbase = tile * 128;
+        g.np = min(128, (MODE == kModeForward ? a.n_fwd : n_pts_all) - g.pbase);
+      }
+    } else if (tile < a.n_int_tiles) {
       g.interior = true;
       g.cell0 = tile * a.cells_per_tile;
       g.ncell = min(a.cells_per_tile, a.E - g.cell0);
@@ -530,7 +542,7 @@ __global__ void __maxnreg__(120) tc2_step_kernel(const StepArgs a) {
     x = 0.f;
     y = 0.f;
     if (p < g.np) {
-      const float2 xy = a.pts[g.pbase + p];
+      const float2 xy = MODE == kModeForward ? a.fwd_pts[g.pbase + p] : a.pts[g.pbase + p];
       x = xy.x;
       y = xy.y;
     }
@@ -547,7 +559,7 @@ __global__ void __maxnreg__(120) tc2_step_kernel(const StepArgs a) {
   float* cellv = tail + 7 * 128;  // [2][<=64]: per-cell sums
 
 #pragma unroll 1
-  for (int tile = blockIdx.x; tile < a.n_tiles; tile += gridDim.x) {
+  for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
     const TileGeo G = geo(tile);
     mark(0);
     const bool interior = G.interior;
@@ -661,11 +673,41 @@ __global__ void __maxnreg__(120) tc2_step_kernel(const StepArgs a) {
       sEx[kUx * 128 + p] = ux;
       sEx[kUy * 128 + p] = uy;
       if (interior) cvr[p] = a.bx * ux + a.by * uy;
+      if (MODE == kModeForward && valid) {
+        if (a.out_u) a.out_u[G.pbase + p] = u;
+        if (a.out_ux) a.out_ux[G.pbase + p] = ux;
+        if (a.out_uy) a.out_uy[G.pbase + p] = uy;
+      }
     }
     mark(4);
+    if constexpr (MODE == kModeForward) {
+      load_xy(geo(tile + gridDim.x), nx, ny);
+      __syncthreads();  // exchange rows read before the next tile rewrites them
+      continue;
+    }
 
     // =================== objective: adjoints of (u, ux, uy) ===================
-    if (interior) {
+    if (MODE == kModeReverse) {
+      // the split path's contraction / penalty kernels computed them
+      if (hh == 0) {
+        float ubv = 0.f, ox = 0.f, oy = 0.f;
+        if (valid) {
+          const int pi = G.pbase + p;
+          if (pi < a.n_int) {
+            ox = a.in_uxb[pi];
+            oy = a.in_uyb[pi];
+          } else {
+            ubv = a.in_ub[pi - a.n_int];
+          }
+        }
+        sEx[kUb * 128 + p] = ubv;
+        sEx[kUxb * 128 + p] = ox;
+        sEx[kUyb * 128 + p] = oy;
+        atomic_max_abs(&sMax[kMb], ubv);
+        atomic_max_abs(&sMax[kMx], ox);
+        atomic_max_abs(&sMax[kMy], oy);
+      }
+    } else if (interior) {
       const bool conv = a.nt == 3;
       const float e_fixed = a.eps_source == 1 ? P[net.scal_off + a.eps_scalar_index] : a.eps;
       if (warp == 0) mbar_wait(tma_bar, tma_phase);  // the slab has landed
@@ -993,6 +1035,15 @@ __global__ void __maxnreg__(120) tc2_step_kernel(const StepArgs a) {
   }
 
   // =================== per-CTA outputs ===================
+  if constexpr (MODE == kModeForward) {
+    tc::fence_before_sync();
+    __syncthreads();
+    if (warp == 0) {
+      tc::fence_after_sync();
+      tc::tmem_dealloc(tmem, kCols);
+    }
+    return;
+  }
   // parameter-gradient accumulators (TMEM lanes 0..63 = G rows h | l, columns
   // 0..63 = X parts h | l), unscaled by 2^-kacc, plus any spilled part ->
   // smem [64][65] (buffer A is free) -> the four-block sum

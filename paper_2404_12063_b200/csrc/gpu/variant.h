@@ -17,6 +17,8 @@ struct Variant {
   StepFn tc;       // tensor-core fused step (tc_step_kernel.cuh), nullptr if the shape has none
   size_t tc_smem;
   StepFn tc2;      // fp16-split two-CTA tensor-core step (tc2_step_kernel.cuh), nullptr if none
+  StepFn tc2_fwd;  // its forward-only / reverse-only modes (split path, evaluate)
+  StepFn tc2_rev;
   size_t tc2_smem;
   int off_union;  // floats before the union
   int rev_need;   // floats the reverse phase needs in the union
@@ -54,12 +56,16 @@ Variant make_variant() {
   if constexpr (C == 1 && (D == 2 || D == 3) && H <= 31) {
     v.tc = tc_step_kernel<H, D, A, kTcNQ>;
     v.tc_smem = tc_step_smem_bytes<H, D>();
-    v.tc2 = tc2_step_kernel<H, D, A>;
+    v.tc2 = tc2_step_kernel<H, D, A, kModeFused>;
+    v.tc2_fwd = tc2_step_kernel<H, D, A, kModeForward>;
+    v.tc2_rev = tc2_step_kernel<H, D, A, kModeReverse>;
     v.tc2_smem = tc2_step_smem_bytes<H, D>();
   } else {
     v.tc = nullptr;
     v.tc_smem = 0;
     v.tc2 = nullptr;
+    v.tc2_fwd = nullptr;
+    v.tc2_rev = nullptr;
     v.tc2_smem = 0;
   }
   return v;

@@ -251,6 +251,8 @@ struct vpinn_gpu_ctx {
   DBuf<long long> phase_clk;  // VPINN_PHASE_CLOCK diagnostics
   DBuf<float> tc_scratch;     // tc2 parameter-gradient scratch
   bool tc2 = false;           // fp16-split two-CTA tensor-core step
+  bool tc2_modes = false;     // tc2 forward / reverse modes serve the split path and evaluate
+  int grid_tc2 = 0;           // 2 CTAs per SM
 
   ~vpinn_gpu_ctx() {
     if (device >= 0) cudaSetDevice(device);
@@ -429,6 +431,36 @@ void configure(vpinn_gpu_ctx* c) {
     c->grad_rows = c->grid_step;
   }
 
+  // ---- tc2 forward / reverse modes (split path, evaluate): any point
+  // count, tanh or sigmoid, 2-3 hidden layers of width <= 31, one output ----
+  {
+    const char* tck = std::getenv("VPINN_TC_KERNEL");
+    const char* tc_env = std::getenv("VPINN_TC");
+    c->tc2_modes = V.tc2_fwd != nullptr && !(tc_env && std::atoi(tc_env) == 0) && !(tck && std::atoi(tck) == 1) &&
+                   c->eps_source != VPINN_EPS_SPATIAL;
+    if (c->tc2_modes) {
+      for (vpg::StepFn fn : {V.tc2_fwd, V.tc2_rev}) {
+        CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)V.tc2_smem));
+        CK(cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+      }
+      int smsm = 0, resv = 0;
+      CK(cudaDeviceGetAttribute(&smsm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, c->device));
+      CK(cudaDeviceGetAttribute(&resv, cudaDevAttrReservedSharedMemoryPerBlock, c->device));
+      c->grid_tc2 = (2 * (V.tc2_smem + resv) <= (size_t)smsm ? 2 : 1) * c->sm_count;
+      if (c->split) {
+        // the reverse stage on the tensor cores
+        a.n_tiles = ceil_div(P_local, 128);
+        c->smem_step = V.tc2_smem;
+        c->grid_step = std::max(1, std::min(a.n_tiles, c->grid_tc2));
+        c->grad_rows = c->grid_step;
+        c->tc_scratch.alloc((size_t)c->grid_step * (V.D - 1) * vpg::t2::kScratchPerLayer, c->stream);
+        a.tc_scratch = c->tc_scratch.p;
+        c->kernel_name = "tc2_step_kernel<" + std::to_string(V.H) + "," + std::to_string(V.D) + "," +
+                         (V.ACT ? "sigmoid" : "tanh") + ",reverse> (split path, fp16 split)";
+      }
+    }
+  }
+
   // ---- forward kernel (evaluate; split-path first stage) ----
   c->smem_fwd = V.smem(0, 1);
   CK(cudaFuncSetAttribute(V.forward, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem_fwd));
@@ -576,8 +608,13 @@ void enqueue_grad(vpinn_gpu_ctx* c, const int* stop, bool with_reduce = true) {
     f.out_uy = c->fuy.p;
     f.out_eps = c->feps.p;
     f.union_floats = 0;
-    const int grid_f = std::max(1, std::min(c->grid_fwd, ceil_div(P_local, vpg::kThreads)));
-    V.forward<<<grid_f, vpg::kThreads, c->smem_fwd, c->stream>>>(f);
+    if (c->tc2_modes) {
+      const int grid_f = std::max(1, std::min(c->grid_tc2, ceil_div(P_local, 128)));
+      V.tc2_fwd<<<grid_f, vpg::t2::kNT, V.tc2_smem, c->stream>>>(f);
+    } else {
+      const int grid_f = std::max(1, std::min(c->grid_fwd, ceil_div(P_local, vpg::kThreads)));
+      V.forward<<<grid_f, vpg::kThreads, c->smem_fwd, c->stream>>>(f);
+    }
     CK(cudaGetLastError());
     vpg::ContractArgs ca = c->cargs;
     ca.ux = c->fux.p;
@@ -602,7 +639,10 @@ void enqueue_grad(vpinn_gpu_ctx* c, const int* stop, bool with_reduce = true) {
       CK(cudaGetLastError());
       c->launches += 1;
     }
-    V.reverse<<<c->grid_step, vpg::kThreads, c->smem_step, c->stream>>>(a);
+    if (c->tc2_modes)
+      V.tc2_rev<<<c->grid_step, vpg::t2::kNT, c->smem_step, c->stream>>>(a);
+    else
+      V.reverse<<<c->grid_step, vpg::kThreads, c->smem_step, c->stream>>>(a);
     CK(cudaGetLastError());
     c->launches += 1;
   }
@@ -1253,8 +1293,13 @@ int vpinn_gpu_forward(vpinn_gpu_ctx* c, const double* points, int64_t n, int ord
     f.out_eps = de.p;
     f.union_floats = 0;
     f.stop_flag = nullptr;
-    const int grid = std::max(1, std::min(c->grid_fwd, ceil_div(n, vpg::kThreads)));
-    c->var.forward<<<grid, vpg::kThreads, c->smem_fwd, c->stream>>>(f);
+    if (c->tc2_modes) {
+      const int grid = std::max(1, std::min(c->grid_tc2, ceil_div(n, 128)));
+      c->var.tc2_fwd<<<grid, vpg::t2::kNT, c->var.tc2_smem, c->stream>>>(f);
+    } else {
+      const int grid = std::max(1, std::min(c->grid_fwd, ceil_div(n, vpg::kThreads)));
+      c->var.forward<<<grid, vpg::kThreads, c->smem_fwd, c->stream>>>(f);
+    }
     CK(cudaGetLastError());
     c->launches += 1;
     CK(cudaMemcpyAsync(u, du.p, sizeof(float) * n, cudaMemcpyDeviceToHost, c->stream));

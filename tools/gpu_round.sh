@@ -13,7 +13,7 @@ timeout 900 python -m pytest tests -m gpu -x -q > $O/${TAG}_pytest_gpu.log 2>&1;
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/${TAG}_smoke.log 2>&1; echo "smoke rc=$?" >> $O/${TAG}_smoke.log
 timeout 900 python bench.py > $O/${TAG}_bench.json 2> $O/${TAG}_bench.err
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
-  --log-file $O/${TAG}_launches.csv python bench.py --steps 3 --warmup 3 --no-cpu-baseline > $O/${TAG}_launches.log 2>&1
+  --log-file $O/${TAG}_launches.csv python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-sweep > $O/${TAG}_launches.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:'tc2?_step' -s 2 -c 1 \
   -o $O/${TAG}_step -f python tools/profile_step.py 4 > $O/${TAG}_ncu_step.log 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:contract -c 1 \
