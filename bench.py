@@ -285,6 +285,7 @@ def main():
     # ---- end to end through the C-ABI with host buffers ----
     e2e = _e2e(hp, device, rank, world, pg, args.steps)
     e2e_mesh = _e2e_from_mesh(mesh, device, rank, world, pg, args.steps)
+    mf = _matrix_free(mesh, device, rank, world) if rank == 0 else None
 
     # ---- CPU baseline (rank 0, N=1 only) ----
     cpu = None
@@ -325,6 +326,7 @@ def main():
         "kernel_ms": {"fused_step": ms_mlp, "reduce": ms_red, "adam": ms_adam},
         "e2e": e2e,
         "e2e_from_mesh": e2e_mesh,
+        "contraction_matrix_free": mf,
         "cpu_baseline": cpu,
     }
     if sweep:
@@ -445,6 +447,21 @@ def _e2e_from_mesh(mesh, device, rank, world, pg, steps):
     return {"value": dp.E * dp.Q * steps / dt, "unit": UNIT, "seconds": dt,
             "host_assembly_build_seconds": host_build,
             "path": "HostProblem(device_assembly) + vpinn_gpu_create(assembly input) + train(K) + get_params"}
+
+
+def _matrix_free(mesh, device, rank, world):
+    """the matrix-free contraction (basis tables + per-cell
+    geometry, contract_mf.cuh) on the same gear cells, L2 flushed per launch;
+    a different algorithm from the paper's premultiplier tensors, reported
+    beside the HBM-roofline contraction, not instead of it."""
+    from paper_2404_12063_b200 import gpu as G, host
+    dp = host.HostProblem(GEAR_CFG, mesh=mesh, device_assembly=True)
+    g = G.GpuStep.from_problem(dp.view(device, rank, world), keepalive=dp)
+    ms, nbytes = g.time_contract_matrix_free(20)
+    g.close()
+    return {"kernel": "contract_mf_kernel", "ms_per_launch": ms, "bytes_per_launch": nbytes,
+            "achieved_GBs": nbytes / (ms * 1e-3) / 1e9,
+            "note": "HBM bytes 14x below the premultiplier stream; latency-bound on CUDA cores"}
 
 
 def _sweep(device):

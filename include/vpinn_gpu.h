@@ -232,6 +232,17 @@ int vpinn_gpu_profile_step(vpinn_gpu_ctx* ctx, int reps, double* ms_mlp, double*
  * between timed epochs so every epoch streams its tensors from HBM. */
 int vpinn_gpu_flush_l2(vpinn_gpu_ctx* ctx);
 
+/* Matrix-free variational contraction: the same outputs
+ * as vpinn_gpu_contract (fixed / scalar coefficient, convection) computed
+ * from the reference basis tables and the per-cell geometry instead of the
+ * premultiplier tensors (~4 (4 Q + T) bytes per cell of HBM traffic instead
+ * of 4 n_t T Q).  Needs a context created with an assembly input; fp32, so it
+ * matches the tensor contraction to rounding, not bitwise. */
+int vpinn_gpu_contract_matrix_free(vpinn_gpu_ctx* ctx, const float* du_dx, const float* du_dy, const float* scalars,
+                                   float weight, double* loss, float* residuals, float* du_dx_bar,
+                                   float* du_dy_bar, double* scalar_bar);
+int vpinn_gpu_time_contract_matrix_free(vpinn_gpu_ctx* ctx, int reps, double* ms_per_launch, double* bytes);
+
 /* Device buffers released by destroyed contexts are cached per size for
  * the next context (no cudaMalloc / device-synchronizing cudaFree on
  * re-creation); this returns every cached block to the driver. */

@@ -21,6 +21,7 @@
 #include "assemble.h"
 #include "aux_kernels.cuh"
 #include "contract_cells.cuh"
+#include "contract_mf.cuh"
 #include "tc_selftest.cuh"
 #include "tc_step_kernel.cuh"
 #include "tc2_step_kernel.cuh"
@@ -195,6 +196,72 @@ inline int round4(int x) { return (x + 3) & ~3; }
 
 }  // namespace
 
+namespace {
+int field_id(const char* name) {
+  static const char* names[vpg::kFieldCount] = {"zero",     "one",     "sin2pi_u", "sin2pi_f", "sin4pi_u",
+                                                "sin4pi_f", "sin8pi_u", "sin8pi_f", "gear_f",   "bump_u",
+                                                "bump_f",   "sinpi_u",  "sincos_eps", "sinpi_vareps_f"};
+  if (!name) return vpg::kFieldZero;
+  for (int i = 0; i < vpg::kFieldCount; ++i)
+    if (std::strcmp(name, names[i]) == 0) return i;
+  throw Fail{VPINN_ERR_CONFIG, std::string("device assembly: unknown field '") + name + "'"};
+}
+
+// the small assembly inputs on the device (mesh, rule, basis tables)
+struct AsmUpload {
+  DBuf<double> nodes, xi, eta, w, bval, bdxi, bdeta;
+  DBuf<int32_t> elems;
+  DBuf<int> bad;
+  vpg::AsmInput in{};
+  void load(const vpinn_gpu_assembly* a, int64_t n_elem, int T, int Q, cudaStream_t s) {
+    if (!a->nodes || !a->elements || !a->xi || !a->eta || !a->weights || !a->basis_val || !a->basis_dxi ||
+        !a->basis_deta || a->n_nodes < 1)
+      throw Fail{VPINN_ERR_CONFIG, "device assembly: incomplete input"};
+    for (int64_t i = 0; i < 4 * n_elem; ++i)
+      if (a->elements[i] < 0 || a->elements[i] >= a->n_nodes)
+        throw Fail{VPINN_ERR_MESH, "device assembly: element node index out of range"};
+    in.field = field_id(a->forcing);
+    nodes.alloc(2 * a->n_nodes, s);
+    nodes.upload(a->nodes, 2 * a->n_nodes, s);
+    elems.alloc(4 * n_elem, s);
+    elems.upload(a->elements, 4 * n_elem, s);
+    xi.alloc(Q, s);
+    xi.upload(a->xi, Q, s);
+    eta.alloc(Q, s);
+    eta.upload(a->eta, Q, s);
+    w.alloc(Q, s);
+    w.upload(a->weights, Q, s);
+    bval.alloc((size_t)T * Q, s);
+    bval.upload(a->basis_val, (size_t)T * Q, s);
+    bdxi.alloc((size_t)T * Q, s);
+    bdxi.upload(a->basis_dxi, (size_t)T * Q, s);
+    bdeta.alloc((size_t)T * Q, s);
+    bdeta.upload(a->basis_deta, (size_t)T * Q, s);
+    bad.alloc(1, s);
+    const int big = INT_MAX;
+    bad.upload(&big, 1, s);
+    in.nodes = nodes.p;
+    in.elems = elems.p;
+    in.T = T;
+    in.Q = Q;
+    in.xi = xi.p;
+    in.eta = eta.p;
+    in.w = w.p;
+    in.bval = bval.p;
+    in.bdxi = bdxi.p;
+    in.bdeta = bdeta.p;
+  }
+  void check(cudaStream_t s) {
+    int b = INT_MAX;
+    CK(cudaMemcpyAsync(&b, bad.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (b != INT_MAX)
+      throw Fail{VPINN_ERR_MESH, "assemble: element " + std::to_string(b) +
+                                     " has non-positive jacobian determinant"};
+  }
+};
+}  // namespace
+
 // ---------------------------------------------------------------------------
 struct vpinn_gpu_ctx {
   int device = 0;
@@ -250,6 +317,11 @@ struct vpinn_gpu_ctx {
   DBuf<char> flush;  // L2 flush scratch (bench)
   DBuf<long long> phase_clk;  // VPINN_PHASE_CLOCK diagnostics
   DBuf<float> tc_scratch;     // tc2 parameter-gradient scratch
+  // device-assembly contexts keep the mesh, rule and basis tables: the
+  // matrix-free contraction (contract_mf.cuh) works from them
+  std::unique_ptr<AsmUpload> asmd;
+  DBuf<float> mf_tabs, mf_rule;
+  int64_t asm_e0 = 0;
   bool tc2 = false;           // fp16-split two-CTA tensor-core step
   bool tc2_modes = false;     // tc2 forward / reverse modes serve the split path and evaluate
   int grid_tc2 = 0;           // 2 CTAs per SM
@@ -811,71 +883,6 @@ long long launches_per_epoch(const vpinn_gpu_ctx* c) {
 }  // namespace
 
 // ===========================================================================
-namespace {
-int field_id(const char* name) {
-  static const char* names[vpg::kFieldCount] = {"zero",     "one",     "sin2pi_u", "sin2pi_f", "sin4pi_u",
-                                                "sin4pi_f", "sin8pi_u", "sin8pi_f", "gear_f",   "bump_u",
-                                                "bump_f",   "sinpi_u",  "sincos_eps", "sinpi_vareps_f"};
-  if (!name) return vpg::kFieldZero;
-  for (int i = 0; i < vpg::kFieldCount; ++i)
-    if (std::strcmp(name, names[i]) == 0) return i;
-  throw Fail{VPINN_ERR_CONFIG, std::string("device assembly: unknown field '") + name + "'"};
-}
-
-// the small assembly inputs on the device (mesh, rule, basis tables)
-struct AsmUpload {
-  DBuf<double> nodes, xi, eta, w, bval, bdxi, bdeta;
-  DBuf<int32_t> elems;
-  DBuf<int> bad;
-  vpg::AsmInput in{};
-  void load(const vpinn_gpu_assembly* a, int64_t n_elem, int T, int Q, cudaStream_t s) {
-    if (!a->nodes || !a->elements || !a->xi || !a->eta || !a->weights || !a->basis_val || !a->basis_dxi ||
-        !a->basis_deta || a->n_nodes < 1)
-      throw Fail{VPINN_ERR_CONFIG, "device assembly: incomplete input"};
-    for (int64_t i = 0; i < 4 * n_elem; ++i)
-      if (a->elements[i] < 0 || a->elements[i] >= a->n_nodes)
-        throw Fail{VPINN_ERR_MESH, "device assembly: element node index out of range"};
-    in.field = field_id(a->forcing);
-    nodes.alloc(2 * a->n_nodes, s);
-    nodes.upload(a->nodes, 2 * a->n_nodes, s);
-    elems.alloc(4 * n_elem, s);
-    elems.upload(a->elements, 4 * n_elem, s);
-    xi.alloc(Q, s);
-    xi.upload(a->xi, Q, s);
-    eta.alloc(Q, s);
-    eta.upload(a->eta, Q, s);
-    w.alloc(Q, s);
-    w.upload(a->weights, Q, s);
-    bval.alloc((size_t)T * Q, s);
-    bval.upload(a->basis_val, (size_t)T * Q, s);
-    bdxi.alloc((size_t)T * Q, s);
-    bdxi.upload(a->basis_dxi, (size_t)T * Q, s);
-    bdeta.alloc((size_t)T * Q, s);
-    bdeta.upload(a->basis_deta, (size_t)T * Q, s);
-    bad.alloc(1, s);
-    const int big = INT_MAX;
-    bad.upload(&big, 1, s);
-    in.nodes = nodes.p;
-    in.elems = elems.p;
-    in.T = T;
-    in.Q = Q;
-    in.xi = xi.p;
-    in.eta = eta.p;
-    in.w = w.p;
-    in.bval = bval.p;
-    in.bdxi = bdxi.p;
-    in.bdeta = bdeta.p;
-  }
-  void check(cudaStream_t s) {
-    int b = INT_MAX;
-    CK(cudaMemcpyAsync(&b, bad.p, sizeof(int), cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
-    if (b != INT_MAX)
-      throw Fail{VPINN_ERR_MESH, "assemble: element " + std::to_string(b) +
-                                     " has non-positive jacobian determinant"};
-  }
-};
-}  // namespace
 
 extern "C" {
 
@@ -1037,8 +1044,30 @@ int vpinn_gpu_create(const vpinn_gpu_problem* pb, vpinn_gpu_ctx** out) {
       for (long long i = s0; i < s1; ++i) push(NB + i);
       c->pts.alloc((size_t)c->n_int + hp.size(), c->stream);
       c->pts.upload_at(c->n_int, hp.data(), hp.size(), c->stream);
-      AsmUpload up;
+      c->asmd = std::make_unique<AsmUpload>();
+      AsmUpload& up = *c->asmd;
       up.load(pb->assembly, pb->n_elem, c->T, c->Q, c->stream);
+      c->asm_e0 = e0;
+      {
+        // float copies of the basis tables and the rule for the matrix-free contraction
+        const size_t TQ = (size_t)c->T * c->Q;
+        std::vector<float> tabs(3 * TQ), rule(3 * (size_t)c->Q);
+        for (size_t i = 0; i < TQ; ++i) {
+          tabs[i] = (float)pb->assembly->basis_dxi[i];
+          tabs[TQ + i] = (float)pb->assembly->basis_deta[i];
+          tabs[2 * TQ + i] = (float)pb->assembly->basis_val[i];
+        }
+        for (int q = 0; q < c->Q; ++q) {
+          rule[q] = (float)pb->assembly->xi[q];
+          rule[c->Q + q] = (float)pb->assembly->eta[q];
+          rule[2 * c->Q + q] = (float)pb->assembly->weights[q];
+        }
+        c->mf_tabs.alloc(tabs.size(), c->stream);
+        c->mf_tabs.upload(tabs.data(), tabs.size(), c->stream);
+        c->mf_rule.alloc(rule.size(), c->stream);
+        c->mf_rule.upload(rule.data(), rule.size(), c->stream);
+        CK(cudaStreamSynchronize(c->stream));  // host staging vectors go out of scope
+      }
       DBuf<float> tv_tmp, fq;
       float* tv = c->nt == 3 ? c->tens[2].p : nullptr;
       if (!tv) {
@@ -1399,6 +1428,130 @@ int vpinn_gpu_time_contract(vpinn_gpu_ctx* c, int reps, double* ms_per_launch, d
     double b = 4.0 * ((double)c->nt * c->E * c->T * c->Q + (double)c->E * c->T + 4.0 * EQ);
     if (c->eps_source == VPINN_EPS_SPATIAL) b += 8.0 * EQ;
     *bytes = b;
+  });
+}
+
+namespace {
+vpg::MfContractArgs mf_args(vpinn_gpu_ctx* c, const float* ux, const float* uy, float* oxb, float* oyb, float* res,
+                            const float* es, float rscale, double* lp) {
+  if (!c->asmd) throw Fail{VPINN_ERR_CONFIG, "matrix-free contraction needs a context created with an assembly input"};
+  if (c->eps_source == VPINN_EPS_SPATIAL)
+    throw Fail{VPINN_ERR_CONFIG, "matrix-free contraction: spatial coefficient not supported"};
+  vpg::MfContractArgs m{};
+  m.nodes = c->asmd->nodes.p;
+  m.elems = c->asmd->elems.p;
+  m.e0 = c->asm_e0;
+  m.E = c->E;
+  m.T = c->T;
+  m.Q = c->Q;
+  m.tabs = c->mf_tabs.p;
+  m.rule = c->mf_rule.p;
+  m.forcing = c->forcing.p;
+  m.ux = ux;
+  m.uy = uy;
+  m.uxb = oxb;
+  m.uyb = oyb;
+  m.res = res;
+  m.e_fixed = c->eps;
+  m.e_param = es;
+  m.eps_source = c->eps_source;
+  m.bx = c->bx;
+  m.by = c->by;
+  m.rscale = rscale;
+  m.inv_nt = c->sargs.inv_nt;
+  m.loss_part = lp;
+  return m;
+}
+int mf_grid(vpinn_gpu_ctx* c) { return std::max(1, std::min(ceil_div(c->E, vpg::kMfWarps), 8 * c->sm_count)); }
+size_t mf_prepare(vpinn_gpu_ctx* c) {  // once per call site, outside any timed region
+  const size_t smem = vpg::mf_smem_bytes(c->T, c->Q);
+  if (smem > (size_t)227 * 1024) throw Fail{VPINN_ERR_CONFIG, "matrix-free contraction: basis tables exceed shared memory"};
+  CK(cudaFuncSetAttribute(vpg::contract_mf_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  return smem;
+}
+void launch_mf(vpinn_gpu_ctx* c, const vpg::MfContractArgs& m, size_t smem) {
+  vpg::contract_mf_kernel<<<mf_grid(c), 32 * vpg::kMfWarps, smem, c->stream>>>(m);
+  CK(cudaGetLastError());
+  c->launches += 1;
+}
+}  // namespace
+
+int vpinn_gpu_contract_matrix_free(vpinn_gpu_ctx* c, const float* du_dx, const float* du_dy, const float* scalars,
+                                   float weight, double* loss, float* residuals, float* du_dx_bar,
+                                   float* du_dy_bar, double* scalar_bar) {
+  return guarded([&] {
+    set_dev(c);
+    if (c->eps_source == VPINN_EPS_SCALAR && !scalars)
+      throw Fail{VPINN_ERR_NUMERIC, "coefficient scalar index out of range"};
+    const size_t ni = (size_t)c->n_int;
+    DBuf<float> ux, uy, oxb, oyb, res, es;
+    DBuf<double> lp;
+    ux.alloc(ni, c->stream);
+    uy.alloc(ni, c->stream);
+    oxb.alloc(ni, c->stream);
+    oyb.alloc(ni, c->stream);
+    res.alloc((size_t)c->E * c->T, c->stream);
+    es.alloc(1, c->stream);
+    const int rows = mf_grid(c);
+    lp.alloc((size_t)rows * vpg::kLpWords, c->stream);
+    ux.upload(du_dx, ni, c->stream);
+    uy.upload(du_dy, ni, c->stream);
+    if (scalars) es.upload(scalars + c->eps_idx, 1, c->stream);
+    launch_mf(c, mf_args(c, ux.p, uy.p, oxb.p, oyb.p, res.p, es.p, (2.0f * weight) * c->sargs.inv_nt, lp.p),
+              mf_prepare(c));
+    std::vector<double> hl((size_t)rows * vpg::kLpWords);
+    CK(cudaMemcpyAsync(hl.data(), lp.p, sizeof(double) * hl.size(), cudaMemcpyDeviceToHost, c->stream));
+    if (residuals) CK(cudaMemcpyAsync(residuals, res.p, sizeof(float) * c->E * c->T, cudaMemcpyDeviceToHost, c->stream));
+    if (du_dx_bar) CK(cudaMemcpyAsync(du_dx_bar, oxb.p, sizeof(float) * ni, cudaMemcpyDeviceToHost, c->stream));
+    if (du_dy_bar) CK(cudaMemcpyAsync(du_dy_bar, oyb.p, sizeof(float) * ni, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    double l = 0.0, g = 0.0;
+    for (int b = 0; b < rows; ++b) {
+      l += hl[(size_t)b * vpg::kLpWords + vpg::kLpVar];
+      g += hl[(size_t)b * vpg::kLpWords + vpg::kLpEpsGrad];
+    }
+    if (loss) *loss = l;
+    if (scalar_bar && c->eps_source == VPINN_EPS_SCALAR) scalar_bar[c->eps_idx] = g;
+  });
+}
+
+int vpinn_gpu_time_contract_matrix_free(vpinn_gpu_ctx* c, int reps, double* ms_per_launch, double* bytes) {
+  return guarded([&] {
+    set_dev(c);
+    const size_t ni = (size_t)c->n_int;
+    DBuf<float> ux, uy, oxb, oyb, es;
+    DBuf<double> lp;
+    ux.alloc(ni, c->stream);
+    uy.alloc(ni, c->stream);
+    oxb.alloc(ni, c->stream);
+    oyb.alloc(ni, c->stream);
+    es.alloc(1, c->stream);
+    lp.alloc((size_t)mf_grid(c) * vpg::kLpWords, c->stream);
+    DBuf<char> flush;
+    flush.alloc((size_t)256 << 20, c->stream);
+    const vpg::MfContractArgs m = mf_args(c, ux.p, uy.p, oxb.p, oyb.p, nullptr, es.p, c->sargs.rscale, lp.p);
+    const size_t smem = mf_prepare(c);
+    cudaEvent_t e0, e1;
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    double total = 0.0;
+    for (int r = 0; r < reps + 2; ++r) {
+      flush_l2_now(c, flush.p);
+      CK(cudaEventRecord(e0, c->stream));
+      launch_mf(c, m, smem);
+      CK(cudaEventRecord(e1, c->stream));
+      CK(cudaEventSynchronize(e1));
+      float ms = 0;
+      CK(cudaEventElapsedTime(&ms, e0, e1));
+      if (r >= 2) total += ms;
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    *ms_per_launch = total / std::max(1, reps);
+    // algorithmic bytes: 4 node coordinates (double) + 4 element indices per
+    // cell, forcing column, u_x / u_y in, the two adjoints out
+    const double EQ = (double)c->E * c->Q;
+    *bytes = (double)c->E * (4 * 16 + 16) + 4.0 * ((double)c->E * c->T + 4.0 * EQ);
   });
 }
 

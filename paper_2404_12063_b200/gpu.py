@@ -125,6 +125,26 @@ class GpuStep:
                                                    C.byref(loss), _p(res), _p(uxb), _p(uyb), _p(eb), _p(sb)))
         return loss.value, res.reshape(self.n_elem, self.n_test), uxb, uyb, eb, sb
 
+    def contract_matrix_free(self, ux, uy, scalars=None, weight=1.0):
+        """vpinn_gpu_contract_matrix_free (device-assembly contexts)."""
+        ni = self.n_elem * self.n_quad
+        ux = np.ascontiguousarray(ux, dtype=np.float32)
+        uy = np.ascontiguousarray(uy, dtype=np.float32)
+        sc = None if scalars is None else np.ascontiguousarray(scalars, dtype=np.float32)
+        loss = C.c_double()
+        res = np.zeros(self.n_elem * self.n_test, dtype=np.float32)
+        uxb = np.zeros(ni, dtype=np.float32)
+        uyb = np.zeros(ni, dtype=np.float32)
+        sb = np.zeros(max(1, 0 if scalars is None else len(scalars)))
+        _capi.check(_capi.lib().vpinn_gpu_contract_matrix_free(self.h, _p(ux), _p(uy), _p(sc), weight, C.byref(loss),
+                                                               _p(res), _p(uxb), _p(uyb), _p(sb)))
+        return loss.value, res.reshape(self.n_elem, self.n_test), uxb, uyb, sb
+
+    def time_contract_matrix_free(self, reps=20):
+        ms, b = C.c_double(), C.c_double()
+        _capi.check(_capi.lib().vpinn_gpu_time_contract_matrix_free(self.h, reps, C.byref(ms), C.byref(b)))
+        return ms.value, b.value
+
     @staticmethod
     def assemble(nodes, cells, rule, basis, forcing="zero", device=0):
         """Device-side assembly (vpinn_gpu_assemble): nodes [n][2], cells

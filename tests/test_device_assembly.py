@@ -104,3 +104,34 @@ def test_device_assembly_partitions_like_the_upload(world):
         pa, ga = a.loss_and_grad()
         pb, gb = b.loss_and_grad()
         assert np.array_equal(pa, pb) and np.array_equal(ga, gb)
+
+
+@pytest.mark.parametrize("name", ["gear_cd2d", "c1_square"])
+def test_matrix_free_contraction_matches_the_tensor_contraction(name):
+    """Algorithm 3 from the basis tables + per-cell
+    geometry equals Algorithm 3 on the premultiplier tensors to fp32
+    rounding (loss 1e-5 relative; residuals / adjoints 1e-5 of their max)."""
+    cfg, mk = CASES[name]
+    dp = host.HostProblem(cfg, mesh=mk(), device_assembly=True)
+    g = dp.gpu()
+    rng = np.random.default_rng(3)
+    ni = dp.E * dp.Q
+    ux = rng.standard_normal(ni).astype(np.float32)
+    uy = rng.standard_normal(ni).astype(np.float32)
+    l1, r1, xb1, yb1, _, _ = g.contract(ux, uy)
+    l2, r2, xb2, yb2, _ = g.contract_matrix_free(ux, uy)
+    assert abs(l1 - l2) / abs(l1) < 1e-5
+    for a, b in ((r1, r2), (xb1, xb2), (yb1, yb2)):
+        assert np.abs(a - b).max() / np.abs(a).max() < 1e-5
+    ms, nbytes = g.time_contract_matrix_free(3)
+    assert ms > 0 and nbytes > 0
+
+
+def test_matrix_free_contraction_needs_the_geometry():
+    cfg, mk = CASES["c1_square"]
+    hp = host.HostProblem(cfg, mesh=mk())
+    g = hp.gpu()
+    ni = hp.E * hp.Q
+    with pytest.raises(_capi.VpinnError) as e:
+        g.contract_matrix_free(np.zeros(ni), np.zeros(ni))
+    assert e.value.code == 2
