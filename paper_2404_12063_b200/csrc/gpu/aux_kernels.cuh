@@ -19,7 +19,7 @@ __device__ __forceinline__ void reduce_body(const float* __restrict__ grad_part,
                                             int n_params, const double* __restrict__ loss_part, int n_loss_rows,
                                             double* __restrict__ red) {
   const int lane = threadIdx.x & 31;
-  const int gw = blockIdx.x * kRedWarps + (threadIdx.x >> 5);
+  const int gw = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const double* src_d = nullptr;
   const float* src_f = nullptr;
   int n = 0, step = 1;
@@ -47,6 +47,13 @@ __device__ __forceinline__ void reduce_body(const float* __restrict__ grad_part,
 }
 
 __host__ __device__ constexpr int reduce_grid(int n_params) { return (n_params + kLpWords + kRedWarps - 1) / kRedWarps; }
+// the fused reduce + Adam: 1024-thread CTAs, so the last CTA's Adam update
+// (IEEE division / square root per parameter, the epoch's serial tail) runs
+// on 1024 threads
+constexpr int kRAThreads = 1024;
+__host__ __device__ constexpr int reduce_adam_grid(int n_params) {
+  return (n_params + kLpWords + kRAThreads / 32 - 1) / (kRAThreads / 32);
+}
 
 __global__ void __launch_bounds__(kRedThreads) reduce_kernel(const float* __restrict__ grad_part, int n_rows,
                                                              int stride, int n_params,
@@ -213,7 +220,7 @@ __global__ void __launch_bounds__(1024) adam_kernel(const AdamArgs a) {
 
 // single-GPU epoch tail: the cross-CTA reduction of reduce_kernel, then the
 // last CTA to finish (atomic ticket, release/acquire fences) applies Adam
-__global__ void __launch_bounds__(kRedThreads) reduce_adam_kernel(const float* __restrict__ grad_part, int n_rows,
+__global__ void __launch_bounds__(kRAThreads) reduce_adam_kernel(const float* __restrict__ grad_part, int n_rows,
                                                                    int stride, int n_params,
                                                                    const double* __restrict__ loss_part,
                                                                    int n_loss_rows, double* __restrict__ red,

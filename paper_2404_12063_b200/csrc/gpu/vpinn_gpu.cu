@@ -761,7 +761,7 @@ void enqueue_epoch(vpinn_gpu_ctx* c, const vpg::AdamArgs& aa) {
     return;
   }
   enqueue_grad(c, &c->st.p->stopped, /*with_reduce=*/false);
-  vpg::reduce_adam_kernel<<<vpg::reduce_grid(c->n_params), vpg::kRedThreads, 0, c->stream>>>(
+  vpg::reduce_adam_kernel<<<vpg::reduce_adam_grid(c->n_params), vpg::kRAThreads, 0, c->stream>>>(
       c->grad_part.p, c->grad_rows, c->part_stride, c->n_params, c->loss_part.p, c->loss_rows, c->red.p,
       c->ticket.p, aa);
   CK(cudaGetLastError());
