@@ -168,6 +168,16 @@ __global__ void __maxnreg__(120) tc2_step_kernel(const StepArgs a) {
   using AC = Act<ACT>;
 
   if (a.stop_flag != nullptr && *a.stop_flag != 0) return;
+  if constexpr (VPG_PHASE_CLOCK != 0) {  // entry clocks (diagnostics)
+    if (a.phase_clk != nullptr && blockIdx.x == 0 && threadIdx.x == 0)
+      a.phase_clk[kPhaseTiles * kPhaseMarks - 1] = clock64();
+    if (a.phase_clk != nullptr && threadIdx.x == 0 && blockIdx.x < 1024) {
+      uint32_t smid;
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+      a.phase_clk[kPhaseTiles * kPhaseMarks + 3 * blockIdx.x] = (long long)globaltimer();
+      a.phase_clk[kPhaseTiles * kPhaseMarks + 3 * blockIdx.x + 2] = smid;
+    }
+  }
 
   // the swizzled operand tiles need a 1024-byte aligned base; the dynamic
   // window starts aligned (no static shared memory), checked here
@@ -1105,6 +1115,14 @@ __global__ void __maxnreg__(120) tc2_step_kernel(const StepArgs a) {
   if (tid == 0)
     for (int e = net.scal_off; e < net.n_params; ++e) a.grad_part[(size_t)e * a.part_stride + blockIdx.x] = 0.f;
   const int any_bad = __syncthreads_or(bad);
+  if constexpr (VPG_PHASE_CLOCK != 0)  // CTA 0 exit clock and tile count (diagnostics)
+    if (a.phase_clk != nullptr && blockIdx.x == 0 && tid == 0) {
+      a.phase_clk[kPhaseTiles * kPhaseMarks - 2] = clock64();
+      a.phase_clk[kPhaseTiles * kPhaseMarks - 3] = ph_tile;
+    }
+  if constexpr (VPG_PHASE_CLOCK != 0)
+    if (a.phase_clk != nullptr && tid == 0 && blockIdx.x < 1024)
+      a.phase_clk[kPhaseTiles * kPhaseMarks + 3 * blockIdx.x + 1] = (long long)globaltimer();
   if (tid == 0) {
     double* lp = a.loss_part + (size_t)blockIdx.x * kLpWords;
     lp[kLpVar] = acc_v;

@@ -390,7 +390,7 @@ void configure(vpinn_gpu_ctx* c) {
              (size_t)(c->nt * round4(tile_rows * c->Q + 8) + vpg::t2::kTailFloats) * sizeof(float) <=
                  (size_t)vpg::t2::kBuf;
     if (c->tc && (std::getenv("VPINN_PHASE_CLOCK") && std::atoi(std::getenv("VPINN_PHASE_CLOCK")) != 0)) {
-      c->phase_clk.alloc((size_t)vpg::kPhaseTiles * vpg::kPhaseMarks, c->stream);
+      c->phase_clk.alloc((size_t)vpg::kPhaseTiles * vpg::kPhaseMarks + 3 * 1024, c->stream);
       a.phase_clk = c->phase_clk.p;
     }
     if (c->tc2) {
@@ -1661,7 +1661,7 @@ int vpinn_gpu_phase_clock(vpinn_gpu_ctx* c, long long* out, int n) {
   return guarded([&] {
     set_dev(c);
     if (!c->phase_clk.p) throw Fail{VPINN_ERR_CONFIG, "phase clocks not enabled (VPINN_PHASE_CLOCK=1)"};
-    const int m = std::min(n, vpg::kPhaseTiles * vpg::kPhaseMarks);
+    const int m = std::min(n, vpg::kPhaseTiles * vpg::kPhaseMarks + 3 * 1024);
     CK(cudaStreamSynchronize(c->stream));
     CK(cudaMemcpy(out, c->phase_clk.p, sizeof(long long) * m, cudaMemcpyDeviceToHost));
   });

@@ -25,17 +25,32 @@ g.set_params(hp.init_params())
 g.adam_reset()
 g.run_steps(3, 1e-3)
 g.synchronize()
-buf = np.zeros(8 * 32, np.int64)
+buf = np.zeros(8 * 32 + 3 * 1024, np.int64)
 _capi.check(_capi.lib().vpinn_gpu_phase_clock(g.h, buf.ctypes.data_as(C.c_void_p), buf.size))
 tc2 = g.step_kernel().startswith("tc2")
 nm = 13 if tc2 else 17
 if tc2:
     NAMES = NAMES2
-t = buf.reshape(8, 32)[:, :nm].astype(np.float64)
+ctas = buf[256:].reshape(1024, 3)
+t = buf[:256].reshape(8, 32)[:, :nm].astype(np.float64)
 d = np.diff(t, axis=1)
 per_tile = t[1:, 0] - t[:-1, 0]
 print(g.step_kernel())
 print("tile cycles:", per_tile.astype(int).tolist())
 for i in range(nm - 1):
     print(f"{NAMES[i+1]:24s} " + " ".join(f"{int(x):6d}" for x in d[:, i]) + f"   mean {d[1:, i].mean():7.0f}")
+allv = buf[:256]
+if allv[-1]:
+    print(f"CTA 0: entry -> first tile {int(t[0, 0] - allv[-1])} cycles; entry -> exit {int(allv[-2] - allv[-1])} cycles "
+          f"({(allv[-2] - allv[-1]) / 1.965e3:.1f} us at 1965 MHz); tiles {int(allv[-3])}")
 print("sum of marks per tile", d.sum(axis=1).astype(int).tolist())
+
+cta = ctas[ctas[:, 0] > 0]
+if len(cta):
+    t0 = cta[:, 0].min()
+    st, en = (cta[:, 0] - t0) / 1e3, (cta[:, 1] - t0) / 1e3
+    print(f"CTAs {len(cta)}: start spread {st.max():.1f} us; end min/median/max {en.min():.1f} / {np.median(en):.1f} / "
+          f"{en.max():.1f} us; SMs used {len(set(cta[:, 2].tolist()))}")
+    order = np.argsort(-en)[:6]
+    print("latest CTAs (block, sm, start, end us):", [(int(i), int(cta[i, 2]), round(float(st[i]), 1),
+                                                        round(float(en[i]), 1)) for i in order])
