@@ -43,6 +43,9 @@
 #include "step_kernel.cuh"
 #include "tc_utils.cuh"
 
+#ifndef VPG_TC2_WARP_WAITS
+#define VPG_TC2_WARP_WAITS 1  // MMA completion: per-warp mbarrier polls (1) or one warp + CTA barrier (0)
+#endif
 #ifndef VPG_PHASE_CLOCK
 #define VPG_PHASE_CLOCK 0  // build with -DVPG_PHASE_CLOCK=1 for tools/phase_clock.py
 #endif
@@ -389,6 +392,16 @@ __global__ void __maxnreg__(120) tc2_step_kernel(const StepArgs a) {
   // others sleep in the CTA barrier instead of spinning on issue slots the
   // co-resident CTA needs
   auto cta_wait = [&](uint64_t* b1, uint32_t& p1, uint64_t* b2, uint32_t* p2, uint64_t* b3, uint32_t* p3) {
+#if VPG_TC2_WARP_WAITS
+    // every warp polls the mbarrier(s) itself: no CTA barrier, warps run ahead
+    mbar_wait(b1, p1);
+    if (b2) mbar_wait(b2, *p2);
+    if (b3) mbar_wait(b3, *p3);
+    p1 ^= 1u;
+    if (b2) *p2 ^= 1u;
+    if (b3) *p3 ^= 1u;
+    tc::fence_after_sync();
+#else
     if (warp == 0) {
       mbar_wait(b1, p1);
       if (b2) mbar_wait(b2, *p2);
@@ -400,6 +413,7 @@ __global__ void __maxnreg__(120) tc2_step_kernel(const StepArgs a) {
     tc::fence_before_sync();
     __syncthreads();
     tc::fence_after_sync();
+#endif
   };
   auto operands_ready = [&]() {
     tc::fence_smem_to_async();
