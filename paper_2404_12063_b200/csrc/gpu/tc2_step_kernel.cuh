@@ -46,6 +46,9 @@
 #ifndef VPG_TC2_WARP_WAITS
 #define VPG_TC2_WARP_WAITS 1  // MMA completion: per-warp mbarrier polls (1) or one warp + CTA barrier (0)
 #endif
+#ifndef VPG_TC2_MAXNREG
+#define VPG_TC2_MAXNREG 120  // two 256-thread CTAs per SM need <= 128
+#endif
 #ifndef VPG_PHASE_CLOCK
 #define VPG_PHASE_CLOCK 0  // build with -DVPG_PHASE_CLOCK=1 for tools/phase_clock.py
 #endif
@@ -163,7 +166,7 @@ __device__ __forceinline__ int clamp_exp(int k) { return max(-60, min(60, k)); }
 // (the split path of cells larger than a tile: forward -> contraction ->
 // penalty -> reverse)
 template <int H, int D, int ACT, int MODE = kModeFused>
-__global__ void __maxnreg__(120) tc2_step_kernel(const StepArgs a) {
+__global__ void __maxnreg__(VPG_TC2_MAXNREG) tc2_step_kernel(const StepArgs a) {
   using namespace t2;
   static_assert(H <= 31 && (D == 2 || D == 3), "tc2 step: H <= 31, 2 or 3 hidden layers");
   using LY = Lay<D>;

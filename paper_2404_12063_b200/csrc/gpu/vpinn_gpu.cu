@@ -1462,15 +1462,30 @@ vpg::MfContractArgs mf_args(vpinn_gpu_ctx* c, const float* ux, const float* uy, 
   m.loss_part = lp;
   return m;
 }
-int mf_grid(vpinn_gpu_ctx* c) { return std::max(1, std::min(ceil_div(c->E, vpg::kMfWarps), 8 * c->sm_count)); }
+// tile variant when a cell fits the CTA (cells_per_tile = 256 / Q), else
+// the warp-per-cell kernel
+int mf_cpt(vpinn_gpu_ctx* c) { return vpg::kMfTileThreads / c->Q; }
+int mf_grid(vpinn_gpu_ctx* c) {
+  const int cpt = mf_cpt(c);
+  static const int per_sm = std::getenv("VPINN_MF_CTAS") ? std::atoi(std::getenv("VPINN_MF_CTAS")) : 4;
+  if (cpt) return std::max(1, std::min(ceil_div(c->E, cpt), per_sm * c->sm_count));
+  return std::max(1, std::min(ceil_div(c->E, vpg::kMfWarps), 8 * c->sm_count));
+}
 size_t mf_prepare(vpinn_gpu_ctx* c) {  // once per call site, outside any timed region
-  const size_t smem = vpg::mf_smem_bytes(c->T, c->Q);
+  const int cpt = mf_cpt(c);
+  const size_t smem = cpt ? vpg::mf_tile_smem_bytes(c->T, c->Q, cpt) : vpg::mf_smem_bytes(c->T, c->Q);
   if (smem > (size_t)227 * 1024) throw Fail{VPINN_ERR_CONFIG, "matrix-free contraction: basis tables exceed shared memory"};
-  CK(cudaFuncSetAttribute(vpg::contract_mf_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  if (cpt)
+    CK(cudaFuncSetAttribute(vpg::contract_mf_tile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  else
+    CK(cudaFuncSetAttribute(vpg::contract_mf_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   return smem;
 }
 void launch_mf(vpinn_gpu_ctx* c, const vpg::MfContractArgs& m, size_t smem) {
-  vpg::contract_mf_kernel<<<mf_grid(c), 32 * vpg::kMfWarps, smem, c->stream>>>(m);
+  if (const int cpt = mf_cpt(c))
+    vpg::contract_mf_tile_kernel<<<mf_grid(c), vpg::kMfTileThreads, smem, c->stream>>>(m, cpt);
+  else
+    vpg::contract_mf_kernel<<<mf_grid(c), 32 * vpg::kMfWarps, smem, c->stream>>>(m);
   CK(cudaGetLastError());
   c->launches += 1;
 }
