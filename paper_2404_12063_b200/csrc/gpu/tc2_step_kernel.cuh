@@ -46,6 +46,9 @@
 #ifndef VPG_TC2_WARP_WAITS
 #define VPG_TC2_WARP_WAITS 1  // MMA completion: per-warp mbarrier polls (1) or one warp + CTA barrier (0)
 #endif
+#ifndef VPG_TC2_ISSUE_WARPS
+#define VPG_TC2_ISSUE_WARPS 3  // warps issuing the point GEMMs (1 or 3); the next warp issues the param GEMM
+#endif
 #ifndef VPG_TC2_MAXNREG
 #define VPG_TC2_MAXNREG 120  // two 256-thread CTAs per SM need <= 128
 #endif
@@ -222,7 +225,7 @@ __global__ void __maxnreg__(VPG_TC2_MAXNREG) tc2_step_kernel(const StepArgs a) {
   if (warp == 0) tc::tmem_alloc(tslot, kCols);
   if (tid == 0) {
     mbar_init(bar_v, 1);
-    mbar_init(bar_t, 1);
+    mbar_init(bar_t, VPG_TC2_ISSUE_WARPS == 3 ? 2 : 1);
     mbar_init(bar_w, 1);
     mbar_init(tma_bar, 1);
     fence_mbar_init();
@@ -341,26 +344,39 @@ __global__ void __maxnreg__(VPG_TC2_MAXNREG) tc2_step_kernel(const StepArgs a) {
   const uint64_t dW_k = tc::kdesc(sW), dW_mn = tc::mndesc(sW, 32 * tc::kRowBytes);
   // point GEMM of MMA layer l (forward, or propagation with B MN-major): the
   // three part products Al.Wh, Ah.Wl, Ah.Wh of stream s accumulate into D_s
-  auto issue_point_gemm = [&](bool bufb, int l, bool propagate) {
+  // VPG_TC2_ISSUE_WARPS == 3: stream s is issued by warp s (the three
+  // streams' MMAs enter the tensor pipe in parallel instead of behind one
+  // warp's ~60-cycle-per-MMA issue; each stream's accumulation order stays
+  // fixed); bar_t then expects two arrivals.  == 1: warp 0 issues all.
+  auto issue_point_stream = [&](bool bufb, int l, bool propagate, int s) {
     const uint64_t abase = bufb ? dB_k : dA_k;
     const uint64_t wbase = (propagate ? dW_mn : dW_k) + (uint64_t)(((l - 1) * kWBytes) >> 4);
     const uint32_t idesc = tc::idesc_f16(128, 32, 0, propagate ? 1 : 0);
+    const uint32_t d = tmem + kDCols * s;
+#pragma unroll
+    for (int pr = 0; pr < 3; ++pr) {
+      const int pa = pr == 0 ? 1 : 0, pb = pr == 1 ? 1 : 0;
+#pragma unroll
+      for (int ks = 0; ks < 2; ++ks) {
+        const uint64_t ad = abase + (uint64_t)((s * kStream + pa * kPart + 32 * ks) >> 4);
+        const uint64_t bd = wbase + (uint64_t)((pb * 32 * tc::kRowBytes + (propagate ? 1024 : 32) * ks) >> 4);
+        tc::mma_warp(d, ad, bd, idesc, (pr > 0 || ks > 0) ? 1u : 0u);
+      }
+    }
+  };
+  // called by warps 0..2 (or by warp 0 alone)
+  auto issue_point_gemm = [&](bool bufb, int l, bool propagate) {
+#if VPG_TC2_ISSUE_WARPS == 3
+    issue_point_stream(bufb, l, propagate, warp);
+    tc::commit_warp(warp == 0 ? bar_v : bar_t);
+#else
 #pragma unroll 1
     for (int s = 0; s < 3; ++s) {
-      const uint32_t d = tmem + kDCols * s;
-#pragma unroll
-      for (int pr = 0; pr < 3; ++pr) {
-        const int pa = pr == 0 ? 1 : 0, pb = pr == 1 ? 1 : 0;
-#pragma unroll
-        for (int ks = 0; ks < 2; ++ks) {
-          const uint64_t ad = abase + (uint64_t)((s * kStream + pa * kPart + 32 * ks) >> 4);
-          const uint64_t bd = wbase + (uint64_t)((pb * 32 * tc::kRowBytes + (propagate ? 1024 : 32) * ks) >> 4);
-          tc::mma_warp(d, ad, bd, idesc, (pr > 0 || ks > 0) ? 1u : 0u);
-        }
-      }
+      issue_point_stream(bufb, l, propagate, s);
       if (s == 0) tc::commit_warp(bar_v);
     }
     tc::commit_warp(bar_t);
+#endif
   };
   // parameter gradient of MMA layer l: G parts in bufA (M blocks h | l | next
   // stream's parts, unused), X parts in bufB (N = h | l).  Accumulates in
@@ -610,7 +626,7 @@ __global__ void __maxnreg__(VPG_TC2_MAXNREG) tc2_step_kernel(const StepArgs a) {
 #pragma unroll 1
     for (int c = 0; c < 2; ++c) store_x1(x1buf, c, px, py);
     operands_ready();
-    if (warp == 0) issue_point_gemm(D == 2, 1, false);
+    if (warp < VPG_TC2_ISSUE_WARPS) issue_point_gemm(D == 2, 1, false);
     mark(1);
     // epilogue of MMA layer l: hidden l+1 output.  Value stream first (it
     // overlaps the tangent-stream MMAs), stored (or consumed by the output
@@ -680,7 +696,7 @@ __global__ void __maxnreg__(VPG_TC2_MAXNREG) tc2_step_kernel(const StepArgs a) {
       }
       if (!last) {
         operands_ready();
-        if (warp == 0) issue_point_gemm(true, l + 1, false);
+        if (warp < VPG_TC2_ISSUE_WARPS) issue_point_gemm(true, l + 1, false);
       }
       mark(1 + l);
     }
@@ -969,9 +985,15 @@ __global__ void __maxnreg__(VPG_TC2_MAXNREG) tc2_step_kernel(const StepArgs a) {
       }
     }
     operands_ready();
-    if (warp == 0) {
+    // the parameter-gradient GEMM from the warp after the point-GEMM issuers
+    if (warp < VPG_TC2_ISSUE_WARPS) {
+      mark(13);
       issue_point_gemm(false, NL, true);
+      mark(14);
+    }
+    if (warp == VPG_TC2_ISSUE_WARPS % 8) {
       issue_param_gemm(NL, pfirst, pshift);
+      mark(15);
     }
     mark(9);
     // ---- hidden layers, last first: G of hidden l from the propagated adjoints ----
@@ -1045,10 +1067,8 @@ __global__ void __maxnreg__(VPG_TC2_MAXNREG) tc2_step_kernel(const StepArgs a) {
       }
       if (l > 1) {
         operands_ready();
-        if (warp == 0) {
-          issue_point_gemm(false, l - 1, true);
-          issue_param_gemm(l - 1, pfirst2, pshift2);
-        }
+        if (warp < VPG_TC2_ISSUE_WARPS) issue_point_gemm(false, l - 1, true);
+        if (warp == VPG_TC2_ISSUE_WARPS % 8) issue_param_gemm(l - 1, pfirst2, pshift2);
         bGv = bv2;
         bGt = bt2;
         puv = puv2;

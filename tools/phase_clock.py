@@ -40,6 +40,9 @@ print("tile cycles:", per_tile.astype(int).tolist())
 for i in range(nm - 1):
     print(f"{NAMES[i+1]:24s} " + " ".join(f"{int(x):6d}" for x in d[:, i]) + f"   mean {d[1:, i].mean():7.0f}")
 allv = buf[:256]
+tt = buf[:256].reshape(8, 32)
+if tt[1, 15]:
+    print("MMA issue (cycles): prop", (tt[1:, 14] - tt[1:, 13]).tolist(), "param", (tt[1:, 15] - tt[1:, 14]).tolist())
 if allv[-1]:
     print(f"CTA 0: entry -> first tile {int(t[0, 0] - allv[-1])} cycles; entry -> exit {int(allv[-2] - allv[-1])} cycles "
           f"({(allv[-2] - allv[-1]) / 1.965e3:.1f} us at 1965 MHz); tiles {int(allv[-3])}")
