@@ -49,6 +49,9 @@
 #ifndef VPG_TC2_ISSUE_WARPS
 #define VPG_TC2_ISSUE_WARPS 3  // warps issuing the point GEMMs (1 or 3); the next warp issues the param GEMM
 #endif
+#ifndef VPG_TC2_PARAM_M64
+#define VPG_TC2_PARAM_M64 1  // parameter-gradient GEMM with M = 64 (G parts h | l only)
+#endif
 #ifndef VPG_TC2_MAXNREG
 #define VPG_TC2_MAXNREG 120  // two 256-thread CTAs per SM need <= 128
 #endif
@@ -385,7 +388,7 @@ __global__ void __maxnreg__(VPG_TC2_MAXNREG) tc2_step_kernel(const StepArgs a) {
   // smaller than the accumulated one
   auto issue_param_gemm = [&](int l, bool first, int shift) {
     const uint32_t acc = tmem + kG0 + 64 * (l - 1);
-    const uint32_t idesc = tc::idesc_f16(128, 64, 1, 1);
+    const uint32_t idesc = tc::idesc_f16(VPG_TC2_PARAM_M64 ? 64 : 128, 64, 1, 1);
 #pragma unroll 1
     for (int s = 0; s < 3; ++s) {
 #pragma unroll
@@ -491,9 +494,14 @@ __global__ void __maxnreg__(VPG_TC2_MAXNREG) tc2_step_kernel(const StepArgs a) {
   // accumulator, unscaled, into the per-CTA fp32 scratch ([col][lane]) and
   // restart it; warps of lane quarters 0 / 1 (G rows h / l), unit half = X
   // part h / l
+  // G row (part * 32 + o) held by this thread's TMEM lane in the
+  // parameter-gradient accumulator, or -1: M = 128 puts row r in lane r
+  // (warps of lane quarters 0 / 1), M = 64 in lane 32 (r / 16) + r % 16
+  // (lanes 0..15 of every quarter)
+  const int grow = VPG_TC2_PARAM_M64 ? (lane < 16 ? 16 * (warp & 3) + lane : -1)
+                                     : ((warp & 3) < 2 ? 32 * (warp & 1) + lane : -1);
   auto spill_accumulator = [&](int l, int kacc, bool first) {
-    if ((warp & 3) >= 2) return;
-    const int lrow = 32 * (warp & 1) + lane;  // G row (part * 32 + o)
+    if (!VPG_TC2_PARAM_M64 && (warp & 3) >= 2) return;
     float* S = a.tc_scratch + ((size_t)blockIdx.x * NL + (l - 1)) * kScratchPerLayer;
     const float inv = tc::exp2i(-kacc);
 #pragma unroll 1
@@ -501,10 +509,12 @@ __global__ void __maxnreg__(VPG_TC2_MAXNREG) tc2_step_kernel(const StepArgs a) {
       const int col0 = 32 * hh + 16 * h2;
       float v[16];
       tc::tmem_ld1x16_wait(tmem + lane_q + kG0 + 64 * (l - 1) + col0, v);
+      if (grow >= 0) {
 #pragma unroll
-      for (int k = 0; k < 16; ++k) {
-        float* d = S + (col0 + k) * 64 + lrow;
-        *d = first ? v[k] * inv : fmaf(v[k], inv, *d);
+        for (int k = 0; k < 16; ++k) {
+          float* d = S + (col0 + k) * 64 + grow;
+          *d = first ? v[k] * inv : fmaf(v[k], inv, *d);
+        }
       }
     }
   };
@@ -1100,19 +1110,20 @@ __global__ void __maxnreg__(VPG_TC2_MAXNREG) tc2_step_kernel(const StepArgs a) {
     const bool has = (l == 1) ? has0 : has1, spill = (l == 1) ? spill0 : spill1;
     const float* S = a.tc_scratch + ((size_t)blockIdx.x * NL + (l - 1)) * kScratchPerLayer;
     tc::fence_after_sync();
-    if ((warp & 3) < 2 && has) {
-      const int lrow = 32 * (warp & 1) + lane;
+    if ((VPG_TC2_PARAM_M64 || (warp & 3) < 2) && has) {
       const float inv = tc::exp2i(-kacc);
 #pragma unroll 1
       for (int h2 = 0; h2 < 2; ++h2) {
         const int col0 = 32 * hh + 16 * h2;
         float v[16];
         tc::tmem_ld1x16_wait(tmem + lane_q + kG0 + 64 * (l - 1) + col0, v);
+        if (grow >= 0) {
 #pragma unroll
-        for (int k = 0; k < 16; ++k) {
-          float x = v[k] * inv;
-          if (spill) x += S[(col0 + k) * 64 + lrow];
-          scr[lrow * 65 + col0 + k] = x;
+          for (int k = 0; k < 16; ++k) {
+            float x = v[k] * inv;
+            if (spill) x += S[(col0 + k) * 64 + grow];
+            scr[grow * 65 + col0 + k] = x;
+          }
         }
       }
     }

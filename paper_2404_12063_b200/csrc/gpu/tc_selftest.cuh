@@ -51,6 +51,13 @@ __global__ void __launch_bounds__(128, 1) tc_probe_kernel(int mode, const float*
           tc::mma_bf16(tmem, tc::kdesc(sa + part * 8192 + 32 * ks), bd, idesc, (part > 0 || ks > 0) ? 1u : 0u);
         }
       }
+    } else if (mode == 4) {
+      // layout probe: one M = 64 chain, A MN-major (M blocks = A parts h | m),
+      // B = H part h (N = 32), K = 128 points; the raw TMEM dump shows where
+      // the 64 rows land
+      const uint32_t idesc = tc::idesc_bf16(64, 32, 1, 1);
+      for (int kp = 0; kp < 8; ++kp)
+        tc::mma_bf16(tmem, tc::mndesc(sa + 1024 * kp, 8192), tc::mndesc(sh + 1024 * kp, 8192), idesc, kp > 0);
     } else if (mode == 3) {
       // scale-input-d: the forward product twice, the second pass scaling the
       // accumulated first pass by 2^-2 on its first MMA: D = AW^T / 4 + AW^T
