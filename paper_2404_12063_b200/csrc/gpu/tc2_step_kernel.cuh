@@ -52,6 +52,9 @@
 #ifndef VPG_TC2_PARAM_M64
 #define VPG_TC2_PARAM_M64 1  // parameter-gradient GEMM with M = 64 (G parts h | l only)
 #endif
+#ifndef VPG_TC2_Z1_CACHE
+#define VPG_TC2_Z1_CACHE 1  // hidden-1 z kept in TMEM (needs the M = 64 shared accumulator columns)
+#endif
 #ifndef VPG_TC2_MAXNREG
 #define VPG_TC2_MAXNREG 120  // two 256-thread CTAs per SM need <= 128
 #endif
@@ -69,8 +72,14 @@ constexpr int kBuf = 3 * kStream;     // 3 streams (48 KB)
 constexpr int kWBytes = 4096;         // [64][32] fp16: W h rows 0..31 | l rows 32..63
 constexpr uint32_t kCols = 256;       // TMEM columns per CTA
 constexpr int kDCols = 32;            // stream accumulator columns
-constexpr int kG0 = 96;               // parameter-gradient accumulators: 64 columns per MMA layer
-constexpr int kZ0 = 224;              // last hidden layer's activations z (32 columns), forward -> reverse
+// TMEM columns: 0..95 stream accumulators; kG0: parameter-gradient
+// accumulators (M = 64: layer l in lanes 16 (l - 1) .. + 15 of every lane
+// quarter, both layers in the same 64 columns; M = 128: 64 columns per
+// layer); kZ0: the last hidden layer's z; kZ1: the hidden-1 z (forward ->
+// reverse, so X_1 is rebuilt without the activation)
+constexpr int kG0 = 96;
+constexpr int kZ0 = 224;
+constexpr int kZ1 = 192;
 constexpr int kScratchPerLayer = 64 * 64;  // global fp32 [col 64][lane 64] per CTA and MMA layer
 constexpr int kTailFloats = 8 * 128;  // contraction scratch after the slab in buffer A
 constexpr float kOneBias = 20.0f;     // bias of the constant-one unit: act(20) == 1.0f
@@ -175,6 +184,7 @@ template <int H, int D, int ACT, int MODE = kModeFused>
 __global__ void __maxnreg__(VPG_TC2_MAXNREG) tc2_step_kernel(const StepArgs a) {
   using namespace t2;
   static_assert(H <= 31 && (D == 2 || D == 3), "tc2 step: H <= 31, 2 or 3 hidden layers");
+  static_assert(!VPG_TC2_Z1_CACHE || VPG_TC2_PARAM_M64, "the z1 cache uses the columns the M = 64 accumulators free");
   using LY = Lay<D>;
   constexpr int NL = LY::NL;
   using AC = Act<ACT>;
@@ -345,6 +355,12 @@ __global__ void __maxnreg__(VPG_TC2_MAXNREG) tc2_step_kernel(const StepArgs a) {
   const uint64_t dA_k = tc::kdesc(sA), dB_k = tc::kdesc(sB);           // K-major point operands
   const uint64_t dA_mn = tc::mndesc(sA, kPart), dB_mn = tc::mndesc(sB, kPart);  // MN-major (param GEMM)
   const uint64_t dW_k = tc::kdesc(sW), dW_mn = tc::mndesc(sW, 32 * tc::kRowBytes);
+  // layer l's parameter-gradient accumulator (MMA address) and this warp's
+  // load address of it (lane quarter base)
+  auto gacc = [&](int l) {
+    return VPG_TC2_PARAM_M64 ? tmem + kG0 + ((uint32_t)(16 * (l - 1)) << 16) : tmem + kG0 + 64 * (l - 1);
+  };
+  auto gacc_ld = [&](int l) { return tmem + lane_q + kG0 + (VPG_TC2_PARAM_M64 ? 0 : 64 * (l - 1)); };
   // point GEMM of MMA layer l (forward, or propagation with B MN-major): the
   // three part products Al.Wh, Ah.Wl, Ah.Wh of stream s accumulate into D_s
   // VPG_TC2_ISSUE_WARPS == 3: stream s is issued by warp s (the three
@@ -387,7 +403,7 @@ __global__ void __maxnreg__(VPG_TC2_MAXNREG) tc2_step_kernel(const StepArgs a) {
   // scaled down by 2^-shift (scale-input-d) when this tile's product scale is
   // smaller than the accumulated one
   auto issue_param_gemm = [&](int l, bool first, int shift) {
-    const uint32_t acc = tmem + kG0 + 64 * (l - 1);
+    const uint32_t acc = gacc(l);
     const uint32_t idesc = tc::idesc_f16(VPG_TC2_PARAM_M64 ? 64 : 128, 64, 1, 1);
 #pragma unroll 1
     for (int s = 0; s < 3; ++s) {
@@ -461,10 +477,23 @@ __global__ void __maxnreg__(VPG_TC2_MAXNREG) tc2_step_kernel(const StepArgs a) {
       s1[k + 1] = ss.y;
     }
   };
-  // X_1 (hidden-1 output) of chunk c, scaled, into buffer buf
-  auto store_x1 = [&](char* buf, int c, float px, float py) {
+  // X_1 (hidden-1 output) of chunk c, scaled, into buffer buf: from (x, y)
+  // through layer 0 (forward; its z kept in TMEM), or from that kept z
+  // (reverse: no activation evaluation)
+  auto store_x1 = [&](char* buf, int c, float px, float py, bool from_tmem) {
     float z[8], s1[8], tx[8], ty[8];
-    layer0(c, px, py, z, s1);
+    if (VPG_TC2_Z1_CACHE && from_tmem) {
+      tc::tmem_ld1x8_wait(tmem + lane_q + kZ1 + u0 + 8 * c, z);
+#pragma unroll
+      for (int k = 0; k < 8; k += 2) {
+        const float2 ss = AC::s1_2(f2(z[k], z[k + 1]));
+        s1[k] = ss.x;
+        s1[k + 1] = ss.y;
+      }
+    } else {
+      layer0(c, px, py, z, s1);
+      if (VPG_TC2_Z1_CACHE && D == 3) tc::tmem_st1x8_wait(tmem + lane_q + kZ1 + u0 + 8 * c, z);
+    }
 #pragma unroll
     for (int k = 0; k < 8; k += 2) {
       const float4 ws = *reinterpret_cast<const float4*>(sW0s + 2 * (u0 + 8 * c + k));  // (wx, wy) of k, k+1
@@ -494,12 +523,17 @@ __global__ void __maxnreg__(VPG_TC2_MAXNREG) tc2_step_kernel(const StepArgs a) {
   // accumulator, unscaled, into the per-CTA fp32 scratch ([col][lane]) and
   // restart it; warps of lane quarters 0 / 1 (G rows h / l), unit half = X
   // part h / l
-  // G row (part * 32 + o) held by this thread's TMEM lane in the
+  // G row (part * 32 + o) held by this thread's TMEM lane in layer l's
   // parameter-gradient accumulator, or -1: M = 128 puts row r in lane r
-  // (warps of lane quarters 0 / 1), M = 64 in lane 32 (r / 16) + r % 16
-  // (lanes 0..15 of every quarter)
-  const int grow = VPG_TC2_PARAM_M64 ? (lane < 16 ? 16 * (warp & 3) + lane : -1)
-                                     : ((warp & 3) < 2 ? 32 * (warp & 1) + lane : -1);
+  // (warps of lane quarters 0 / 1), M = 64 in lane 32 (r / 16) + r % 16 +
+  // the layer's lane offset 16 (l - 1)
+  auto gacc_row = [&](int l) {
+    if (VPG_TC2_PARAM_M64) {
+      const int lo = lane - 16 * (l - 1);
+      return (lo >= 0 && lo < 16) ? 16 * (warp & 3) + lo : -1;
+    }
+    return (warp & 3) < 2 ? 32 * (warp & 1) + lane : -1;
+  };
   auto spill_accumulator = [&](int l, int kacc, bool first) {
     if (!VPG_TC2_PARAM_M64 && (warp & 3) >= 2) return;
     float* S = a.tc_scratch + ((size_t)blockIdx.x * NL + (l - 1)) * kScratchPerLayer;
@@ -508,7 +542,8 @@ __global__ void __maxnreg__(VPG_TC2_MAXNREG) tc2_step_kernel(const StepArgs a) {
     for (int h2 = 0; h2 < 2; ++h2) {
       const int col0 = 32 * hh + 16 * h2;
       float v[16];
-      tc::tmem_ld1x16_wait(tmem + lane_q + kG0 + 64 * (l - 1) + col0, v);
+      tc::tmem_ld1x16_wait(gacc_ld(l) + col0, v);
+      const int grow = gacc_row(l);
       if (grow >= 0) {
 #pragma unroll
         for (int k = 0; k < 16; ++k) {
@@ -634,7 +669,7 @@ __global__ void __maxnreg__(VPG_TC2_MAXNREG) tc2_step_kernel(const StepArgs a) {
     // =================== forward ===================
     char* x1buf = (D == 3) ? bufA : bufB;  // hidden-1 output (input of MMA layer 1)
 #pragma unroll 1
-    for (int c = 0; c < 2; ++c) store_x1(x1buf, c, px, py);
+    for (int c = 0; c < 2; ++c) store_x1(x1buf, c, px, py, false);
     operands_ready();
     if (warp < VPG_TC2_ISSUE_WARPS) issue_point_gemm(D == 2, 1, false);
     mark(1);
@@ -1072,7 +1107,7 @@ __global__ void __maxnreg__(VPG_TC2_MAXNREG) tc2_step_kernel(const StepArgs a) {
           tc::st_split8_ho<false>(bufA, kPart, o, ga, 1.f);
           tc::st_split8_ho<false>(bufA + kStream, kPart, o, gx, 1.f);
           tc::st_split8_ho<false>(bufA + 2 * kStream, kPart, o, gy, 1.f);
-          store_x1(bufB, c, px, py);  // hidden-1 output recomputed (l - 1 == 1)
+          store_x1(bufB, c, px, py, true);  // hidden-1 output rebuilt (l - 1 == 1)
         }
       }
       if (l > 1) {
@@ -1116,7 +1151,8 @@ __global__ void __maxnreg__(VPG_TC2_MAXNREG) tc2_step_kernel(const StepArgs a) {
       for (int h2 = 0; h2 < 2; ++h2) {
         const int col0 = 32 * hh + 16 * h2;
         float v[16];
-        tc::tmem_ld1x16_wait(tmem + lane_q + kG0 + 64 * (l - 1) + col0, v);
+        tc::tmem_ld1x16_wait(gacc_ld(l) + col0, v);
+        const int grow = gacc_row(l);
         if (grow >= 0) {
 #pragma unroll
           for (int k = 0; k < 16; ++k) {

@@ -58,6 +58,12 @@ __global__ void __launch_bounds__(128, 1) tc_probe_kernel(int mode, const float*
       const uint32_t idesc = tc::idesc_bf16(64, 32, 1, 1);
       for (int kp = 0; kp < 8; ++kp)
         tc::mma_bf16(tmem, tc::mndesc(sa + 1024 * kp, 8192), tc::mndesc(sh + 1024 * kp, 8192), idesc, kp > 0);
+    } else if (mode == 5) {
+      // the same M = 64 chain addressed at TMEM lane 16
+      const uint32_t idesc = tc::idesc_bf16(64, 32, 1, 1);
+      for (int kp = 0; kp < 8; ++kp)
+        tc::mma_bf16(tmem + (16u << 16), tc::mndesc(sa + 1024 * kp, 8192), tc::mndesc(sh + 1024 * kp, 8192), idesc,
+                     kp > 0);
     } else if (mode == 3) {
       // scale-input-d: the forward product twice, the second pass scaling the
       // accumulated first pass by 2^-2 on its first MMA: D = AW^T / 4 + AW^T

@@ -1692,7 +1692,7 @@ int vpinn_gpu_flush_l2(vpinn_gpu_ctx* c) {
 
 int vpinn_gpu_tc_probe(int device, int mode, const float* A, const float* W, const float* H, float* out) {
   return guarded([&] {
-    if (mode < 0 || mode > 4) throw Fail{VPINN_ERR_CONFIG, "tc_probe: mode must be 0..4"};
+    if (mode < 0 || mode > 5) throw Fail{VPINN_ERR_CONFIG, "tc_probe: mode must be 0..5"};
     CK(cudaSetDevice(device));
     DBuf<float> dA, dW, dH, dO;
     dA.alloc(128 * 32, 0);
