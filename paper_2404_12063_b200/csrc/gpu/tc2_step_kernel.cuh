@@ -492,7 +492,7 @@ __global__ void __maxnreg__(VPG_TC2_MAXNREG) tc2_step_kernel(const StepArgs a) {
       }
     } else {
       layer0(c, px, py, z, s1);
-      if (VPG_TC2_Z1_CACHE && D == 3) tc::tmem_st1x8_wait(tmem + lane_q + kZ1 + u0 + 8 * c, z);
+      if (VPG_TC2_Z1_CACHE) tc::tmem_st1x8_wait(tmem + lane_q + kZ1 + u0 + 8 * c, z);
     }
 #pragma unroll
     for (int k = 0; k < 8; k += 2) {
@@ -1068,9 +1068,24 @@ __global__ void __maxnreg__(VPG_TC2_MAXNREG) tc2_step_kernel(const StepArgs a) {
         tc::tmem_ld1x8_wait(dcol(0, c), xa);
         tc::tmem_ld2x8_wait(dcol(1, c), dcol(2, c), xx, xy);
         const uint32_t o = coff(c);
-        tc::ld_join8_ho<true>(bufB, kPart, o, iv, z);
-        tc::ld_join8_ho<false>(bufB + kStream, kPart, o, 1.f, tx);
-        tc::ld_join8_ho<false>(bufB + 2 * kStream, kPart, o, 1.f, ty);
+        if (VPG_TC2_Z1_CACHE && l == 1) {
+          // hidden-1 state from the kept z: tangents s1 * w0 (scaled like X_1)
+          tc::tmem_ld1x8_wait(tmem + lane_q + kZ1 + u0 + 8 * c, z);
+#pragma unroll
+          for (int k = 0; k < 8; k += 2) {
+            const float4 ws = *reinterpret_cast<const float4*>(sW0s + 2 * (u0 + 8 * c + k));
+            const float2 ss = AC::s1_2(f2(z[k], z[k + 1]));
+            const float2 a2 = mul2(ss, f2(ws.x, ws.z)), b2 = mul2(ss, f2(ws.y, ws.w));
+            tx[k] = a2.x;
+            tx[k + 1] = a2.y;
+            ty[k] = b2.x;
+            ty[k + 1] = b2.y;
+          }
+        } else {
+          tc::ld_join8_ho<true>(bufB, kPart, o, iv, z);
+          tc::ld_join8_ho<false>(bufB + kStream, kPart, o, 1.f, tx);
+          tc::ld_join8_ho<false>(bufB + 2 * kStream, kPart, o, 1.f, ty);
+        }
         float ga[8], gx[8], gy[8];
 #pragma unroll
         for (int k = 0; k < 8; k += 2) {
