@@ -80,6 +80,7 @@ constexpr int kDCols = 32;            // stream accumulator columns
 constexpr int kG0 = 96;
 constexpr int kZ0 = 224;
 constexpr int kZ1 = 192;
+constexpr int kZ2 = 160;  // hidden-2 z (D == 3), forward -> reverse
 constexpr int kScratchPerLayer = 64 * 64;  // global fp32 [col 64][lane 64] per CTA and MMA layer
 constexpr int kTailFloats = 8 * 128;  // contraction scratch after the slab in buffer A
 constexpr float kOneBias = 20.0f;     // bias of the constant-one unit: act(20) == 1.0f
@@ -705,9 +706,10 @@ __global__ void __maxnreg__(VPG_TC2_MAXNREG) tc2_step_kernel(const StepArgs a) {
             ou = fmaf(sWd[u + 1], zz.y, ou);
           }
         }
-        if (!last)
+        if (!last) {
           tc::st_split8_ho<true>(bufB, kPart, coff(c), z, sv);
-        else
+          if (VPG_TC2_Z1_CACHE && D == 3) tc::tmem_st1x8_wait(tmem + lane_q + kZ2 + u0 + 8 * c, z);
+        } else
           tc::tmem_st1x8_wait(tmem + lane_q + kZ0 + u0 + 8 * c, z);  // kept for the reverse
       }
       cta_wait(bar_t, ph_t, nullptr, nullptr, nullptr, nullptr);
@@ -1082,7 +1084,10 @@ __global__ void __maxnreg__(VPG_TC2_MAXNREG) tc2_step_kernel(const StepArgs a) {
             ty[k + 1] = b2.y;
           }
         } else {
-          tc::ld_join8_ho<true>(bufB, kPart, o, iv, z);
+          if (VPG_TC2_Z1_CACHE && D == 3 && l == 2)
+            tc::tmem_ld1x8_wait(tmem + lane_q + kZ2 + u0 + 8 * c, z);  // kept hidden-2 z
+          else
+            tc::ld_join8_ho<true>(bufB, kPart, o, iv, z);
           tc::ld_join8_ho<false>(bufB + kStream, kPart, o, 1.f, tx);
           tc::ld_join8_ho<false>(bufB + 2 * kStream, kPart, o, 1.f, ty);
         }
