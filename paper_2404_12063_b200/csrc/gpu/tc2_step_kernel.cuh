@@ -172,6 +172,19 @@ __device__ __forceinline__ int rs8_index(int lane) { return ((lane >> 4) & 1) * 
 __device__ __forceinline__ void atomic_max_abs(uint32_t* w, float v) {
   atomicMax(w, __float_as_uint(fabsf(v)));  // non-negative floats order as their bits (NaN: largest)
 }
+// the same from a whole converged warp: a warp max (REDUX) first, then one
+// shared-memory atomic per warp instead of 32 on the same word
+#ifndef VPG_TC2_WARP_ATOMIC
+#define VPG_TC2_WARP_ATOMIC 0
+#endif
+__device__ __forceinline__ void warp_atomic_max_abs(uint32_t* w, float v) {
+#if VPG_TC2_WARP_ATOMIC
+  const uint32_t m = __reduce_max_sync(0xffffffffu, __float_as_uint(fabsf(v)));
+  if ((threadIdx.x & 31) == 0) atomicMax(w, m);
+#else
+  atomic_max_abs(w, v);
+#endif
+}
 __device__ __forceinline__ int clamp_exp(int k) { return max(-60, min(60, k)); }
 
 }  // namespace t2
@@ -793,9 +806,9 @@ __global__ void __maxnreg__(VPG_TC2_MAXNREG) tc2_step_kernel(const StepArgs a) {
         sEx[kUb * 128 + p] = ubv;
         sEx[kUxb * 128 + p] = ox;
         sEx[kUyb * 128 + p] = oy;
-        atomic_max_abs(&sMax[kMb], ubv);
-        atomic_max_abs(&sMax[kMx], ox);
-        atomic_max_abs(&sMax[kMy], oy);
+        warp_atomic_max_abs(&sMax[kMb], ubv);
+        warp_atomic_max_abs(&sMax[kMx], ox);
+        warp_atomic_max_abs(&sMax[kMy], oy);
       }
     } else if (interior) {
       const bool conv = a.nt == 3;
@@ -910,8 +923,8 @@ __global__ void __maxnreg__(VPG_TC2_MAXNREG) tc2_step_kernel(const StepArgs a) {
         sEx[kUb * 128 + p] = 0.f;
         sEx[kUxb * 128 + p] = ox;
         sEx[kUyb * 128 + p] = oy;
-        atomic_max_abs(&sMax[kMx], ox);
-        atomic_max_abs(&sMax[kMy], oy);
+        warp_atomic_max_abs(&sMax[kMx], ox);
+        warp_atomic_max_abs(&sMax[kMy], oy);
       }
       if (tid == 0) {
         for (int k = 0; k < ncell; ++k) {
@@ -945,7 +958,7 @@ __global__ void __maxnreg__(VPG_TC2_MAXNREG) tc2_step_kernel(const StepArgs a) {
         sEx[kUb * 128 + p] = ubv;
         sEx[kUxb * 128 + p] = 0.f;
         sEx[kUyb * 128 + p] = 0.f;
-        atomic_max_abs(&sMax[kMb], ubv);
+        warp_atomic_max_abs(&sMax[kMb], ubv);
       }
       if (lane == 0 && warp < 4) {
         sRed[warp] = sb;
