@@ -55,6 +55,9 @@
 #ifndef VPG_TC2_Z1_CACHE
 #define VPG_TC2_Z1_CACHE 1  // hidden-1 z kept in TMEM (needs the M = 64 shared accumulator columns)
 #endif
+#ifndef VPG_TC2_CONTRACT3
+#define VPG_TC2_CONTRACT3 1  // one thread per row / point runs all three tensors (fewer barriers)
+#endif
 #ifndef VPG_TC2_MAXNREG
 #define VPG_TC2_MAXNREG 120  // two 256-thread CTAs per SM need <= 128
 #endif
@@ -821,6 +824,98 @@ __global__ void __maxnreg__(VPG_TC2_MAXNREG) tc2_step_kernel(const StepArgs a) {
       const float* T0 = chunk_ptr(a, cell0, 0, slab, 0);
       const float* T1 = chunk_ptr(a, cell0, 0, slab, 1);
       const float* T2 = conv ? chunk_ptr(a, cell0, 0, slab, 2) : T0;
+#if VPG_TC2_CONTRACT3
+      // phase A: one thread per row (unit half 0) runs the three dot products
+      // (G_x . ux, G_y . uy, T . (bx ux + by uy)) as interleaved chains and
+      // finishes the residual itself (losses.hpp:122-136): no exchange step
+      if (hh == 0 && p < nrows_tile) {
+        const int r = p, kk = r / a.T;
+        const float* sx = sEx + kUx * 128 + kk * a.Q;
+        const float* sy = sEx + kUy * 128 + kk * a.Q;
+        const float* sc = cvr + kk * a.Q;
+        const float* gx_r = T0 + r * a.Q;
+        const float* gy_r = T1 + r * a.Q;
+        const float* gt_r = T2 + r * a.Q;
+        float ax[4] = {0.f, 0.f, 0.f, 0.f}, ay[4] = {0.f, 0.f, 0.f, 0.f}, at[4] = {0.f, 0.f, 0.f, 0.f};
+        int q = 0;
+#pragma unroll 2
+        for (; q + 3 < a.Q; q += 4) {
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            ax[u] = fmaf(gx_r[q + u], sx[q + u], ax[u]);
+            ay[u] = fmaf(gy_r[q + u], sy[q + u], ay[u]);
+            if (conv) at[u] = fmaf(gt_r[q + u], sc[q + u], at[u]);
+          }
+        }
+        for (; q < a.Q; ++q) {
+          ax[0] = fmaf(gx_r[q], sx[q], ax[0]);
+          ay[0] = fmaf(gy_r[q], sy[q], ay[0]);
+          if (conv) at[0] = fmaf(gt_r[q], sc[q], at[0]);
+        }
+        const float gx = (ax[0] + ax[1]) + (ax[2] + ax[3]);
+        const float gy = (ay[0] + ay[1]) + (ay[2] + ay[3]);
+        float res = e_fixed * (gx + gy);
+        if (conv) res += (at[0] + at[1]) + (at[2] + at[3]);
+        res -= frow;
+        rsqv[r] = res * res;
+        const float rb = a.rscale * res;
+        rbarv[r] = rb;
+        rgev[r] = rb * (gx + gy);
+      }
+      __syncthreads();
+      mark(6);
+      // phase B: one thread per point (unit half 0) runs the three adjoint
+      // columns and writes the point's adjoints; half 1 the per-cell sums
+      if (hh == 0) {
+        float ox = 0.f, oy = 0.f;
+        if (valid) {
+          const int myk = p / a.Q, myq = p - myk * a.Q;
+          const float* cx = T0 + myq;
+          const float* cy = T1 + myq;
+          const float* ct = T2 + myq;
+          float bx4[4] = {0.f, 0.f, 0.f, 0.f}, by4[4] = {0.f, 0.f, 0.f, 0.f}, bt4[4] = {0.f, 0.f, 0.f, 0.f};
+          int r = myk * a.T;
+          const int r1 = r + a.T;
+#pragma unroll 2
+          for (; r + 3 < r1; r += 4) {
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const float rb = rbarv[r + u];
+              bx4[u] = fmaf(cx[(r + u) * a.Q], rb, bx4[u]);
+              by4[u] = fmaf(cy[(r + u) * a.Q], rb, by4[u]);
+              if (conv) bt4[u] = fmaf(ct[(r + u) * a.Q], rb, bt4[u]);
+            }
+          }
+          for (; r < r1; ++r) {
+            const float rb = rbarv[r];
+            bx4[0] = fmaf(cx[r * a.Q], rb, bx4[0]);
+            by4[0] = fmaf(cy[r * a.Q], rb, by4[0]);
+            if (conv) bt4[0] = fmaf(ct[r * a.Q], rb, bt4[0]);
+          }
+          ox = e_fixed * ((bx4[0] + bx4[1]) + (bx4[2] + bx4[3]));
+          oy = e_fixed * ((by4[0] + by4[1]) + (by4[2] + by4[3]));
+          if (conv) {
+            const float tt = (bt4[0] + bt4[1]) + (bt4[2] + bt4[3]);
+            ox = fmaf(a.bx, tt, ox);
+            oy = fmaf(a.by, tt, oy);
+          }
+        }
+        sEx[kUb * 128 + p] = 0.f;
+        sEx[kUxb * 128 + p] = ox;
+        sEx[kUyb * 128 + p] = oy;
+        warp_atomic_max_abs(&sMax[kMx], ox);
+        warp_atomic_max_abs(&sMax[kMy], oy);
+      } else if (p < ncell) {
+        float s = 0.f, g = 0.f;
+        for (int r = p * a.T; r < (p + 1) * a.T; ++r) {
+          s += rsqv[r];
+          g += rgev[r];
+        }
+        cellv[p] = s;
+        cellv[64 + p] = g;
+      }
+      mark(7);
+#else
       // phase A: (tensor g, row r) dot products with (ux | uy | bx ux + by uy).
       // Unit half 0 does tensors 0 and 2 (interleaved: two independent
       // chains), half 1 tensor 1 (plus a discarded duplicate, keeping the
@@ -932,6 +1027,7 @@ __global__ void __maxnreg__(VPG_TC2_MAXNREG) tc2_step_kernel(const StepArgs a) {
           acc_eg += (double)cellv[64 + k];
         }
       }
+#endif
     } else {
       // ---------- penalty tile (losses.hpp:389-415) ----------
       double sb = 0.0, ss = 0.0;
@@ -974,6 +1070,14 @@ __global__ void __maxnreg__(VPG_TC2_MAXNREG) tc2_step_kernel(const StepArgs a) {
     }
     load_xy(geo(tile + gridDim.x), nx, ny);  // next tile's points, in flight during the reverse
     __syncthreads();                          // adjoint rows + tile maxima visible; slab reads done
+#if VPG_TC2_CONTRACT3
+    if (MODE == kModeFused && interior && tid == 0) {
+      for (int k = 0; k < ncell; ++k) {
+        acc_v += (double)(cellv[k] * a.inv_nt);
+        acc_eg += (double)cellv[64 + k];
+      }
+    }
+#endif
     mark(8);
     const float ub = sEx[kUb * 128 + p], uxb = sEx[kUxb * 128 + p], uyb = sEx[kUyb * 128 + p];
 
