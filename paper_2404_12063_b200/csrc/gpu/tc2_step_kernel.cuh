@@ -58,6 +58,11 @@
 #ifndef VPG_TC2_CONTRACT3
 #define VPG_TC2_CONTRACT3 1  // one thread per row / point runs all three tensors (fewer barriers)
 #endif
+#define VPG_STR_(x) #x
+#define VPG_PRAGMA_UNROLL(n) _Pragma(VPG_STR_(unroll n))
+#ifndef VPG_TC2_CHUNK_UNROLL
+#define VPG_TC2_CHUNK_UNROLL 1  // (A/B: 2 is 4% slower, I-cache) unroll of the two 8-unit chunk loops (1 or 2; code size vs ILP)
+#endif
 #ifndef VPG_TC2_MAXNREG
 #define VPG_TC2_MAXNREG 120  // two 256-thread CTAs per SM need <= 128
 #endif
@@ -685,7 +690,7 @@ __global__ void __maxnreg__(VPG_TC2_MAXNREG) tc2_step_kernel(const StepArgs a) {
 
     // =================== forward ===================
     char* x1buf = (D == 3) ? bufA : bufB;  // hidden-1 output (input of MMA layer 1)
-#pragma unroll 1
+VPG_PRAGMA_UNROLL(VPG_TC2_CHUNK_UNROLL)
     for (int c = 0; c < 2; ++c) store_x1(x1buf, c, px, py, false);
     operands_ready();
     if (warp < VPG_TC2_ISSUE_WARPS) issue_point_gemm(D == 2, 1, false);
@@ -1114,7 +1119,7 @@ __global__ void __maxnreg__(VPG_TC2_MAXNREG) tc2_step_kernel(const StepArgs a) {
     {
       const float f1 = sSc[kScF1 + NL - 1];
       const float Ub = ub * sgv, Uxv = uxb * sgv, Uyv = uyb * sgv, Uxt = uxb * sgt, Uyt = uyb * sgt;
-#pragma unroll 1
+VPG_PRAGMA_UNROLL(VPG_TC2_CHUNK_UNROLL)
       for (int c = 0; c < 2; ++c) {
         float zs[8], dx[8], dy[8];
         tc::tmem_ld1x8_wait(tmem + lane_q + kZ0 + u0 + 8 * c, zs);
@@ -1181,7 +1186,7 @@ __global__ void __maxnreg__(VPG_TC2_MAXNREG) tc2_step_kernel(const StepArgs a) {
       // (param GEMM l is waited for per thread right before the first store,
       // so the first chunk's G computation overlaps it)
       cta_wait(bar_v, ph_v, bar_t, &ph_t, nullptr, nullptr);
-#pragma unroll 1
+VPG_PRAGMA_UNROLL(VPG_TC2_CHUNK_UNROLL)
       for (int c = 0; c < 2; ++c) {
         float xa[8], xx[8], xy[8], z[8], tx[8], ty[8];
         tc::tmem_ld1x8_wait(dcol(0, c), xa);
