@@ -287,7 +287,17 @@ __device__ __forceinline__ void mma_warp_sd(uint32_t d_tmem, uint64_t a_desc, ui
       "l"(a_desc), "l"(b_desc), "r"(idesc), "n"(S)
       : "memory");
 }
-__device__ __forceinline__ void mma_warp_sd(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, int s) {
+// out of line: the 16-way switch is the rare path (a tile whose product
+// scale drops below the accumulated one), kept out of the hot code's I-cache
+#ifndef VPG_SD_NOINLINE
+#define VPG_SD_NOINLINE 1
+#endif
+#if VPG_SD_NOINLINE
+static __device__ __noinline__
+#else
+__device__ __forceinline__
+#endif
+void mma_warp_sd(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, int s) {
   switch (s) {
 #define VPG_SDW(k) \
   case k:          \
