@@ -112,14 +112,21 @@ __device__ __forceinline__ void adam_body(const AdamArgs& a) {
   const double lw_v = red[n + kLpVar], lw_b = red[n + kLpBnd], lw_s = red[n + kLpSen];
   const double eg = red[n + kLpEpsGrad];
   int bad = red[n + kLpBad] != 0.0;
-  float g_loc[4];
+  // every load of this thread's parameters issued before the abort check
+  // (one round trip instead of a chain: red, then m / v / params)
+  float g_loc[4], m_loc[4], v_loc[4], p_loc[4];
   int cnt = 0;
   for (int p = threadIdx.x; p < n; p += blockDim.x, ++cnt) {
     double gd = red[p];
     if (p == a.eps_grad_slot) gd += eg;
     const float g = (float)gd;
     if (!isfinite(g)) bad = 1;
-    if (cnt < 4) g_loc[cnt] = g;
+    if (cnt < 4) {
+      g_loc[cnt] = g;
+      m_loc[cnt] = a.m[p];
+      v_loc[cnt] = a.v[p];
+      p_loc[cnt] = a.params[p];
+    }
   }
   bad = __syncthreads_or(bad);
   // loss parts in the reference's Real semantics
@@ -148,21 +155,27 @@ __device__ __forceinline__ void adam_body(const AdamArgs& a) {
   const float b1 = 0.9f, b2 = 0.999f, omb1 = 1.0f - b1, omb2 = 1.0f - b2;
   cnt = 0;
   for (int p = threadIdx.x; p < n; p += blockDim.x, ++cnt) {
-    float g;
+    float g, m0, v0, p0;
     if (cnt < 4) {
       g = g_loc[cnt];
+      m0 = m_loc[cnt];
+      v0 = v_loc[cnt];
+      p0 = p_loc[cnt];
     } else {
       double gd = red[p];
       if (p == a.eps_grad_slot) gd += eg;
       g = (float)gd;
+      m0 = a.m[p];
+      v0 = a.v[p];
+      p0 = a.params[p];
     }
-    const float m = __fadd_rn(__fmul_rn(b1, a.m[p]), __fmul_rn(omb1, g));
-    const float v = __fadd_rn(__fmul_rn(b2, a.v[p]), __fmul_rn(omb2, __fmul_rn(g, g)));
+    const float m = __fadd_rn(__fmul_rn(b1, m0), __fmul_rn(omb1, g));
+    const float v = __fadd_rn(__fmul_rn(b2, v0), __fmul_rn(omb2, __fmul_rn(g, g)));
     a.m[p] = m;
     a.v[p] = v;
     const float mh = __fdiv_rn(m, c1);
     const float vh = __fdiv_rn(v, c2);
-    a.params[p] = __fsub_rn(a.params[p], __fdiv_rn(__fmul_rn(lr, mh), __fadd_rn(__fsqrt_rn(vh), 1e-8f)));
+    a.params[p] = __fsub_rn(p0, __fdiv_rn(__fmul_rn(lr, mh), __fadd_rn(__fsqrt_rn(vh), 1e-8f)));
   }
   __syncthreads();
   if (threadIdx.x == 0) {
