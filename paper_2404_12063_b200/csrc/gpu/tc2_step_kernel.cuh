@@ -60,6 +60,9 @@
 #endif
 #define VPG_STR_(x) #x
 #define VPG_PRAGMA_UNROLL(n) _Pragma(VPG_STR_(unroll n))
+#ifndef VPG_TC2_ISSUE_UNROLL
+#define VPG_TC2_ISSUE_UNROLL 1  // (A/B: 3 is 3% slower, I-cache) MMA issue loops over streams: 3 = unrolled (constant offsets), 1 = rolled
+#endif
 #ifndef VPG_TC2_CHUNK_UNROLL
 #define VPG_TC2_CHUNK_UNROLL 1  // (A/B: 2 is 4% slower, I-cache) unroll of the two 8-unit chunk loops (1 or 2; code size vs ILP)
 #endif
@@ -408,7 +411,17 @@ __global__ void __maxnreg__(VPG_TC2_MAXNREG) tc2_step_kernel(const StepArgs a) {
   // called by warps 0..2 (or by warp 0 alone)
   auto issue_point_gemm = [&](bool bufb, int l, bool propagate) {
 #if VPG_TC2_ISSUE_WARPS == 3
+#if VPG_TC2_ISSUE_UNROLL == 3
+    // the stream index as a constant per warp (uniform descriptor offsets)
+    if (warp == 0)
+      issue_point_stream(bufb, l, propagate, 0);
+    else if (warp == 1)
+      issue_point_stream(bufb, l, propagate, 1);
+    else
+      issue_point_stream(bufb, l, propagate, 2);
+#else
     issue_point_stream(bufb, l, propagate, warp);
+#endif
     tc::commit_warp(warp == 0 ? bar_v : bar_t);
 #else
 #pragma unroll 1
@@ -427,7 +440,8 @@ __global__ void __maxnreg__(VPG_TC2_MAXNREG) tc2_step_kernel(const StepArgs a) {
   auto issue_param_gemm = [&](int l, bool first, int shift) {
     const uint32_t acc = gacc(l);
     const uint32_t idesc = tc::idesc_f16(VPG_TC2_PARAM_M64 ? 64 : 128, 64, 1, 1);
-#pragma unroll 1
+    // fully unrolled: constant descriptor offsets stay in the uniform datapath
+VPG_PRAGMA_UNROLL(VPG_TC2_ISSUE_UNROLL)
     for (int s = 0; s < 3; ++s) {
 #pragma unroll
       for (int kp = 0; kp < 8; ++kp) {
