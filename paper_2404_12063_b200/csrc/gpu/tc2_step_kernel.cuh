@@ -198,6 +198,55 @@ __device__ __forceinline__ void warp_atomic_max_abs(uint32_t* w, float v) {
 }
 __device__ __forceinline__ int clamp_exp(int k) { return max(-60, min(60, k)); }
 
+// out-of-line MMA issue sequences (called by whole converged warps): one
+// copy in the kernel's SASS instead of one per call site (the kernel is
+// I-cache sensitive)
+#ifndef VPG_TC2_ISSUE_NOINLINE
+#define VPG_TC2_ISSUE_NOINLINE 0  // (A/B: out-of-line issue is 1.6% slower)
+#endif
+#if VPG_TC2_ISSUE_NOINLINE
+#define VPG_ISSUE_ATTR static __device__ __noinline__
+#else
+#define VPG_ISSUE_ATTR static __device__ __forceinline__
+#endif
+// point GEMM of one stream: the three part products Al.Wh, Ah.Wl, Ah.Wh into D
+VPG_ISSUE_ATTR void issue_point_stream_fn(uint32_t d, uint64_t abase, uint64_t wbase, uint32_t idesc,
+                                          uint32_t wstep) {
+#pragma unroll
+  for (int pr = 0; pr < 3; ++pr) {
+    const int pa = pr == 0 ? 1 : 0, pb = pr == 1 ? 1 : 0;
+#pragma unroll
+    for (int ks = 0; ks < 2; ++ks) {
+      const uint64_t ad = abase + (uint64_t)((pa * kPart + 32 * ks) >> 4);
+      const uint64_t bd = wbase + (uint64_t)(((pb * 32 * tc::kRowBytes) >> 4) + wstep * ks);
+      tc::mma_warp(d, ad, bd, idesc, (pr > 0 || ks > 0) ? 1u : 0u);
+    }
+  }
+}
+// parameter-gradient GEMM: 3 streams x 8 point blocks of K = 16 into acc
+VPG_ISSUE_ATTR void issue_param_fn(uint32_t acc, uint64_t da, uint64_t db, uint32_t idesc, int first, int shift,
+                                   uint64_t* bar) {
+#pragma unroll 1
+  for (int s = 0; s < 3; ++s) {
+#pragma unroll
+    for (int kp = 0; kp < 8; ++kp) {
+      const uint64_t off = (uint64_t)((s * kStream + 1024 * kp) >> 4);
+      const uint64_t ad = da + off, bd = db + off;
+      if (s == 0 && kp == 0) {
+        if (first)
+          tc::mma_warp(acc, ad, bd, idesc, 0u);
+        else if (shift > 0)
+          tc::mma_warp_sd(acc, ad, bd, idesc, shift);
+        else
+          tc::mma_warp(acc, ad, bd, idesc, 1u);
+      } else {
+        tc::mma_warp(acc, ad, bd, idesc, 1u);
+      }
+    }
+  }
+  tc::commit_warp(bar);
+}
+
 }  // namespace t2
 
 // MODE (step_kernel.cuh): kModeFused = the whole epoch on whole-cell tiles;
@@ -393,20 +442,10 @@ __global__ void __maxnreg__(VPG_TC2_MAXNREG) tc2_step_kernel(const StepArgs a) {
   // warp's ~60-cycle-per-MMA issue; each stream's accumulation order stays
   // fixed); bar_t then expects two arrivals.  == 1: warp 0 issues all.
   auto issue_point_stream = [&](bool bufb, int l, bool propagate, int s) {
-    const uint64_t abase = bufb ? dB_k : dA_k;
+    const uint64_t abase = (bufb ? dB_k : dA_k) + (uint64_t)((s * kStream) >> 4);
     const uint64_t wbase = (propagate ? dW_mn : dW_k) + (uint64_t)(((l - 1) * kWBytes) >> 4);
     const uint32_t idesc = tc::idesc_f16(128, 32, 0, propagate ? 1 : 0);
-    const uint32_t d = tmem + kDCols * s;
-#pragma unroll
-    for (int pr = 0; pr < 3; ++pr) {
-      const int pa = pr == 0 ? 1 : 0, pb = pr == 1 ? 1 : 0;
-#pragma unroll
-      for (int ks = 0; ks < 2; ++ks) {
-        const uint64_t ad = abase + (uint64_t)((s * kStream + pa * kPart + 32 * ks) >> 4);
-        const uint64_t bd = wbase + (uint64_t)((pb * 32 * tc::kRowBytes + (propagate ? 1024 : 32) * ks) >> 4);
-        tc::mma_warp(d, ad, bd, idesc, (pr > 0 || ks > 0) ? 1u : 0u);
-      }
-    }
+    issue_point_stream_fn(tmem + kDCols * s, abase, wbase, idesc, propagate ? 1024u >> 4 : 32u >> 4);
   };
   // called by warps 0..2 (or by warp 0 alone)
   auto issue_point_gemm = [&](bool bufb, int l, bool propagate) {
@@ -438,28 +477,8 @@ __global__ void __maxnreg__(VPG_TC2_MAXNREG) tc2_step_kernel(const StepArgs a) {
   // scaled down by 2^-shift (scale-input-d) when this tile's product scale is
   // smaller than the accumulated one
   auto issue_param_gemm = [&](int l, bool first, int shift) {
-    const uint32_t acc = gacc(l);
-    const uint32_t idesc = tc::idesc_f16(VPG_TC2_PARAM_M64 ? 64 : 128, 64, 1, 1);
-    // fully unrolled: constant descriptor offsets stay in the uniform datapath
-VPG_PRAGMA_UNROLL(VPG_TC2_ISSUE_UNROLL)
-    for (int s = 0; s < 3; ++s) {
-#pragma unroll
-      for (int kp = 0; kp < 8; ++kp) {
-        const uint64_t off = (uint64_t)((s * kStream + 1024 * kp) >> 4);
-        const uint64_t ad = dA_mn + off, bd = dB_mn + off;
-        if (s == 0 && kp == 0) {
-          if (first)
-            tc::mma_warp(acc, ad, bd, idesc, 0u);
-          else if (shift > 0)
-            tc::mma_warp_sd(acc, ad, bd, idesc, shift);
-          else
-            tc::mma_warp(acc, ad, bd, idesc, 1u);
-        } else {
-          tc::mma_warp(acc, ad, bd, idesc, 1u);
-        }
-      }
-    }
-    tc::commit_warp(bar_w);
+    issue_param_fn(gacc(l), dA_mn, dB_mn, tc::idesc_f16(VPG_TC2_PARAM_M64 ? 64 : 128, 64, 1, 1), first ? 1 : 0,
+                   shift, bar_w);
   };
   uint32_t ph_v = 0, ph_t = 0, ph_w = 0, tma_phase = 0;
   // CTA-wide wait for MMA completion: ONE warp polls the mbarrier(s), the
