@@ -309,7 +309,13 @@ __global__ void __maxnreg__(VPG_TC2_MAXNREG) tc2_step_kernel(const StepArgs a) {
   const float kapmax = 2.0f;  // |act''/act'|: 2 |z| (tanh) or |1 - 2z| (sigmoid)
 
   // ---------------- one-time setup ----------------
+  auto smark = [&](int i) {
+    if constexpr (VPG_PHASE_CLOCK != 0)
+      if (a.phase_clk != nullptr && blockIdx.x == 0 && threadIdx.x == 0) a.phase_clk[7 * kPhaseMarks + 20 + i] = clock64();
+  };
+  smark(0);
   if (warp == 0) tc::tmem_alloc(tslot, kCols);
+  smark(1);
   if (tid == 0) {
     mbar_init(bar_v, 1);
     mbar_init(bar_t, VPG_TC2_ISSUE_WARPS == 3 ? 2 : 1);
@@ -319,6 +325,15 @@ __global__ void __maxnreg__(VPG_TC2_MAXNREG) tc2_step_kernel(const StepArgs a) {
   }
   if (tid < 16) sMax[tid] = 0u;
   for (int i = tid; i < 8 * kAccW; i += kNT) sAcc[i] = 0.f;
+  // every parameter load of the setup issued at once: thread t < 128 NL holds
+  // row (t / 4) % 32, columns [8 (t % 4), +8) of MMA layer t / 128 + 1
+  const int wl = tid >> 7, wo = (tid >> 2) & 31, wc = tid & 3;
+  float wv[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const int i = 8 * wc + k;
+    wv[k] = (wl < NL && wo < H && i < H) ? P[net.w_off[wl + 1] + wo * H + i] : 0.f;
+  }
   for (int i = tid; i < 32; i += kNT) {
     float w0 = 0.f, w1 = 0.f, b = (i == H) ? kOneBias : 0.f, wd = 0.f;
     if (i < H) {
@@ -337,33 +352,38 @@ __global__ void __maxnreg__(VPG_TC2_MAXNREG) tc2_step_kernel(const StepArgs a) {
   for (int l = 1; l <= NL; ++l)
     for (int o = tid; o < 32; o += kNT)
       sBias[(l - 1) * 32 + o] = o < H ? P[net.b_off[l] + o] : ((o == H) ? kOneBias : 0.f);
-  __syncthreads();
-  // weight norms (bounds for the scales): max |w0x|, |w0y|, |wd|; per MMA
-  // layer max |W|, max row abs-sum R, max column abs-sum C
+  // |W| into buffer A (free until the first tile) for the row / column sums
+  float* sAbs = reinterpret_cast<float*>(bufA);  // [NL][32][33] (row stride 33: no bank conflicts)
   uint32_t* sNorm = sMax + kNW0;  // [0] w0x [1] w0y [2] wd
   uint32_t(*s_lnorm)[3] = reinterpret_cast<uint32_t(*)[3]>(sMax + kNLayer);  // [layer][maxabs, rowsum, colsum]
+  if (wl < NL) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) sAbs[(wl * 32 + wo) * 33 + 8 * wc + k] = fabsf(wv[k]);
+  }
+  smark(2);
+  __syncthreads();  // (also orders the sMax zero fill before any atomic below)
+  smark(3);
+  if (wl < NL) {
+    float m = 0.f;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) m = fmaxf(m, fabsf(wv[k]));
+    atomic_max_abs(&s_lnorm[wl][0], m);  // max: order-free
+  }
+  // weight norms (bounds for the scales): max |w0x|, |w0y|, |wd|; per MMA
+  // layer max row abs-sum R and max column abs-sum C, each sum in index order
   if (tid < H) {
     atomic_max_abs(&sNorm[0], sW0[4 * tid]);
     atomic_max_abs(&sNorm[1], sW0[4 * tid + 1]);
     atomic_max_abs(&sNorm[2], sWd[tid]);
   }
-  for (int l = 1; l <= NL; ++l) {
-    const float* W = P + net.w_off[l];
-    const int fo = net.out_w[l], fi = net.in_w[l];
-    if (tid < 32 && tid < fo) {  // row abs-sum and max of row tid
-      float s = 0.f, m = 0.f;
-      for (int i = 0; i < fi; ++i) {
-        const float w = fabsf(W[tid * fi + i]);
-        s += w;
-        m = fmaxf(m, w);
-      }
-      atomic_max_abs(&s_lnorm[l - 1][0], m);
-      atomic_max_abs(&s_lnorm[l - 1][1], s);
-    } else if (tid >= 32 && tid < 64 && tid - 32 < fi) {  // column abs-sum
-      float s = 0.f;
-      for (int o = 0; o < fo; ++o) s += fabsf(W[o * fi + (tid - 32)]);
-      atomic_max_abs(&s_lnorm[l - 1][2], s);
+  if (tid < 64 * NL) {
+    const int l = tid >> 6, j = tid & 31;
+    const bool row = (tid & 32) == 0;
+    float sum = 0.f;
+    if (j < H) {
+      for (int k = 0; k < H; ++k) sum += row ? sAbs[(l * 32 + j) * 33 + k] : sAbs[(l * 32 + k) * 33 + j];
     }
+    atomic_max_abs(&s_lnorm[l][row ? 1 : 2], sum);
   }
   __syncthreads();
   if (tid == 0) {
@@ -398,21 +418,10 @@ __global__ void __maxnreg__(VPG_TC2_MAXNREG) tc2_step_kernel(const StepArgs a) {
     sW0s[2 * i] = sW0[4 * i] * sSc[kScSt];
     sW0s[2 * i + 1] = sW0[4 * i + 1] * sSc[kScSt];
   }
+  smark(4);
   // W tiles, scaled by 2^kW: row o of part h at rows 0..31, part l at rows 32..63
-  for (int l = 1; l <= NL; ++l) {
-    char* wb = sWB + (l - 1) * kWBytes;
-    const float sw = tc::exp2i(sSci[kSiW + l - 1]);
-    for (int e = tid; e < 32 * 4; e += kNT) {
-      const int o = e >> 2, c = e & 3;
-      float v[8];
-#pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        const int i = 8 * c + k;
-        v[k] = (o < H && i < H) ? P[net.w_off[l] + o * H + i] : 0.f;
-      }
-      tc::st_split8_h(wb, 32 * tc::kRowBytes, o, c, v, sw);
-    }
-  }
+  if (wl < NL)
+    tc::st_split8_h(sWB + wl * kWBytes, 32 * tc::kRowBytes, wo, wc, wv, tc::exp2i(sSci[kSiW + wl]));
   tc::fence_smem_to_async();
   tc::fence_before_sync();
   __syncthreads();
@@ -690,6 +699,7 @@ __global__ void __maxnreg__(VPG_TC2_MAXNREG) tc2_step_kernel(const StepArgs a) {
       y = xy.y;
     }
   };
+  smark(5);
   float nx, ny;
   load_xy(geo(blockIdx.x), nx, ny);
   // contraction scratch after the slab in buffer A

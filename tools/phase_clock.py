@@ -40,6 +40,9 @@ print("tile cycles:", per_tile.astype(int).tolist())
 for i in range(nm - 1):
     print(f"{NAMES[i+1]:24s} " + " ".join(f"{int(x):6d}" for x in d[:, i]) + f"   mean {d[1:, i].mean():7.0f}")
 allv = buf[:256]
+sm = buf[7 * 32 + 20: 7 * 32 + 26]
+if sm[0]:
+    print("setup marks (cycles from entry):", [int(x - allv[-1]) for x in sm])
 tt = buf[:256].reshape(8, 32)
 if tt[1, 15]:
     print("MMA issue (cycles): prop", (tt[1:, 14] - tt[1:, 13]).tolist(), "param", (tt[1:, 15] - tt[1:, 14]).tolist())
