@@ -38,6 +38,7 @@ struct OracleSpec {
   const double* scalar_init;
   unsigned long long seed;
   int use_double;
+  int strong;  // LossForm::strong (trainer.hpp:178)
 };
 
 struct OracleTrainSpec {
@@ -105,6 +106,13 @@ HandleBase* build(const OracleSpec& s) {
   pb.batch.insert(pb.batch.end(), sset.pts.begin(), sset.pts.end());
   pb.bvals = bset.vals;
   pb.svals = sset.vals;
+  // commands.hpp:147-152 — strong_forcing = f at the quadrature points
+  if (s.strong) {
+    pb.strong = true;
+    const vo::Field f = vo::named_field(s.forcing);
+    pb.strong_f.resize(pb.t.qpts.size());
+    for (size_t i = 0; i < pb.t.qpts.size(); ++i) pb.strong_f[i] = f(pb.t.qpts[i].x, pb.t.qpts[i].y);
+  }
   return h.release();
 }
 
@@ -153,7 +161,7 @@ void do_loss_and_grad(void* h, const void* params, double* parts, void* grad) {
 
 template <typename Real>
 void do_evaluate(void* h, const void* params, const double* xy, long long n, int order, void* u,
-                 void* ux, void* uy, void* eps) {
+                 void* ux, void* uy, void* eps, void* uxx = nullptr, void* uyy = nullptr) {
   auto& pb = prob<Real>(h);
   std::vector<vo::Pt> pts(n);
   for (long long i = 0; i < n; ++i) pts[i] = {xy[2 * i], xy[2 * i + 1]};
@@ -162,6 +170,40 @@ void do_evaluate(void* h, const void* params, const double* xy, long long n, int
   copy_out(ev.ux, ux);
   copy_out(ev.uy, uy);
   copy_out(ev.eps, eps);
+  copy_out(ev.uxx, uxx);
+  copy_out(ev.uyy, uyy);
+}
+
+// strong_residual_loss on caller-supplied derivatives (losses.hpp:422-467),
+// in double: the known-answer case of tests/test_losses.cpp:344-412
+int strong_loss_d(const double* u, const double* ux, const double* uy, const double* uxx,
+                  const double* uyy, long long n, long long begin, long long count, double eps,
+                  double bx, double by, int eps_source, int eps_scalar_index, const double* scalars,
+                  int n_scalars, const double* f, double weight, double* loss, double* uxb,
+                  double* uyb, double* uxxb, double* uyyb, double* sb) {
+  return guard([&] {
+    vo::Eval<double> ev;
+    ev.u.assign(u, u + n);
+    ev.ux.assign(ux, ux + n);
+    ev.uy.assign(uy, uy + n);
+    ev.uxx.assign(uxx, uxx + n);
+    ev.uyy.assign(uyy, uyy + n);
+    ev.scalars.assign(scalars, scalars + n_scalars);
+    vo::Coeffs<double> c;
+    c.eps = eps;
+    c.bx = bx;
+    c.by = by;
+    c.source = eps_source;
+    c.eps_scalar_index = eps_scalar_index;
+    vo::Adj<double> adj;
+    std::vector<double> fv(f, f + count);
+    *loss = vo::strong_loss(ev, begin, count, c, fv, weight, &adj);
+    copy_out(adj.uxb, uxb);
+    copy_out(adj.uyb, uyb);
+    copy_out(adj.uxxb, uxxb);
+    copy_out(adj.uyyb, uyyb);
+    for (size_t i = 0; i < adj.sb.size(); ++i) sb[i] = adj.sb[i];
+  });
 }
 
 template <typename Real>
@@ -288,7 +330,8 @@ void vo_counts(void* h, long long* out) {
 
 // which: 0 grad_x, 1 grad_y, 2 test, 3 forcing (Real), 4 batch points
 // (double [P][2]), 5 boundary values, 6 sensor values (double), 7 initial
-// parameters (double), 8 rule xi/eta/w (double [3][Q])
+// parameters (double), 8 rule xi/eta/w (double [3][Q]), 9 strong forcing
+// (double, n_int; strong problems only)
 int vo_get_array(void* h, int which, void* out) {
   auto* hb = static_cast<HandleBase*>(h);
   return guard([&] {
@@ -309,6 +352,7 @@ int vo_get_array(void* h, int which, void* out) {
         case 5: copy_out(pb.bvals, out); break;
         case 6: copy_out(pb.svals, out); break;
         case 7: copy_out(hb->init_params, out); break;
+        case 9: copy_out(pb.strong_f, out); break;
         case 8: {
           double* d = static_cast<double*>(out);
           const size_t Q = hb->rule.w.size();
@@ -371,6 +415,27 @@ int vo_evaluate(void* h, const void* params, const double* xy, long long n, int 
     else
       do_evaluate<float>(h, params, xy, n, order, u, ux, uy, eps);
   });
+}
+
+// evaluate() at order 2: second derivatives too (network.hpp:414-449)
+int vo_evaluate2(void* h, const void* params, const double* xy, long long n, void* u, void* ux,
+                 void* uy, void* uxx, void* uyy) {
+  return guard([&] {
+    if (vo_is_double(h))
+      do_evaluate<double>(h, params, xy, n, 2, u, ux, uy, nullptr, uxx, uyy);
+    else
+      do_evaluate<float>(h, params, xy, n, 2, u, ux, uy, nullptr, uxx, uyy);
+  });
+}
+
+int vo_strong_loss(const double* u, const double* ux, const double* uy, const double* uxx,
+                   const double* uyy, long long n, long long begin, long long count, double eps,
+                   double bx, double by, int eps_source, int eps_scalar_index,
+                   const double* scalars, int n_scalars, const double* f, double weight,
+                   double* loss, double* uxb, double* uyb, double* uxxb, double* uyyb, double* sb) {
+  return strong_loss_d(u, ux, uy, uxx, uyy, n, begin, count, eps, bx, by, eps_source,
+                       eps_scalar_index, scalars, n_scalars, f, weight, loss, uxb, uyb, uxxb, uyyb,
+                       sb);
 }
 
 int vo_var_loss(void* h, int loop, const void* ux, const void* uy, const void* eps,

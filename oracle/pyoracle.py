@@ -48,7 +48,7 @@ class OracleSpec(C.Structure):
         ("tau", C.c_double), ("gamma", C.c_double),
         ("n_sizes", C.c_int), ("sizes", C.POINTER(C.c_int)), ("sigmoid", C.c_int),
         ("n_scalars", C.c_int), ("scalar_init", C.POINTER(C.c_double)),
-        ("seed", C.c_ulonglong), ("use_double", C.c_int),
+        ("seed", C.c_ulonglong), ("use_double", C.c_int), ("strong", C.c_int),
     ]
 
 
@@ -90,6 +90,10 @@ def _declare(L):
     L.vo_structured_mesh.argtypes = [C.c_int, C.c_int, C.c_double, C.c_double, C.c_double,
                                      C.c_double, C.c_double, C.c_ulonglong, vp, vp]
     L.vo_init_params_f64.argtypes = [vp, C.c_int, C.c_ulonglong, vp]
+    L.vo_evaluate2.argtypes = [vp, vp, vp, C.c_longlong, vp, vp, vp, vp, vp]
+    L.vo_strong_loss.argtypes = [vp, vp, vp, vp, vp, ll, ll, ll, C.c_double, C.c_double,
+                                 C.c_double, C.c_int, C.c_int, vp, C.c_int, vp, C.c_double,
+                                 C.POINTER(C.c_double), vp, vp, vp, vp, vp]
 
 
 class OracleError(RuntimeError):
@@ -166,6 +170,23 @@ def adam_f32(p0, grads, lrs):
     return p
 
 
+def strong_loss(u, ux, uy, uxx, uyy, begin, count, f, eps=1.0, bx=0.0, by=0.0, eps_source=0,
+                eps_scalar_index=0, scalars=(), weight=1.0):
+    """strong_residual_loss (losses.hpp:422-467) in double on given derivatives:
+    returns (loss, uxb, uyb, uxxb, uyyb, scalar_bar)."""
+    arrs = [np.ascontiguousarray(a, dtype=np.float64) for a in (u, ux, uy, uxx, uyy)]
+    n = arrs[0].size
+    fv = np.ascontiguousarray(f, dtype=np.float64)
+    sc = np.ascontiguousarray(list(scalars) or [0.0], dtype=np.float64)
+    outs = [np.zeros(n) for _ in range(4)]
+    sb = np.zeros(max(1, len(scalars)))
+    loss = C.c_double()
+    _check(lib().vo_strong_loss(*[_p(a) for a in arrs], n, begin, count, eps, bx, by, eps_source,
+                                eps_scalar_index, _p(sc), len(scalars), _p(fv), weight,
+                                C.byref(loss), *[_p(o) for o in outs], _p(sb)))
+    return (loss.value, *outs, sb[: len(scalars)])
+
+
 # ---------------------------------------------------------------------------
 @dataclass
 class ProblemSpec:
@@ -193,6 +214,7 @@ class ProblemSpec:
     sigmoid: bool = False
     scalars: Sequence[float] = dc_field(default_factory=tuple)
     seed: int = 42
+    strong: bool = False  # LossForm::strong (trainer.hpp:178)
 
 
 class OracleProblem:
@@ -225,6 +247,7 @@ class OracleProblem:
         s.scalar_init = self._scal.ctypes.data_as(C.POINTER(C.c_double))
         s.seed = spec.seed
         s.use_double = int(double)
+        s.strong = int(spec.strong)
         self._spec_c = s
         h = lib().vo_build(C.byref(s))
         if not h:
@@ -246,7 +269,8 @@ class OracleProblem:
 
     def array(self, which: str) -> np.ndarray:
         idx = {"grad_x": 0, "grad_y": 1, "test": 2, "forcing": 3, "points": 4,
-               "boundary_values": 5, "sensor_values": 6, "init_params": 7, "rule": 8}[which]
+               "boundary_values": 5, "sensor_values": 6, "init_params": 7, "rule": 8,
+               "strong_forcing": 9}[which]
         if idx <= 2:
             out = np.zeros(self.E * self.T * self.Q, dtype=self.dtype)
         elif idx == 3:
@@ -259,6 +283,8 @@ class OracleProblem:
             out = np.zeros(self.n_sen)
         elif idx == 7:
             out = np.zeros(self.n_params)
+        elif idx == 9:
+            out = np.zeros(self.n_int)
         else:
             out = np.zeros((3, self.Q))
         _check(lib().vo_get_array(self.h, idx, _p(out)))
@@ -292,6 +318,15 @@ class OracleProblem:
                                  _p(ux) if order >= 1 else None, _p(uy) if order >= 1 else None,
                                  _p(eps) if eps is not None else None))
         return u, ux, uy, eps
+
+    def evaluate2(self, params, points):
+        """evaluate(order=2): u, u_x, u_y, u_xx, u_yy (network.hpp:414-449)."""
+        par = np.ascontiguousarray(params, dtype=self.dtype)
+        pts = np.ascontiguousarray(points, dtype=np.float64).reshape(-1, 2)
+        n = pts.shape[0]
+        outs = [np.zeros(n, dtype=self.dtype) for _ in range(5)]
+        _check(lib().vo_evaluate2(self.h, _p(par), _p(pts), n, *[_p(o) for o in outs]))
+        return tuple(outs)
 
     def var_loss(self, ux, uy, eps=None, scalars=(), weight=1.0, loop=False):
         n = self.E * self.Q

@@ -377,3 +377,124 @@ def test_sensor_sampling_deterministic():
     assert pa.shape == (50, 2) and (np.abs(pa) < 1.0).all()
     assert np.array_equal(pa, b.array("points")[b.n_int + b.n_bnd:])
     assert not np.array_equal(pa, c.array("points")[c.n_int + c.n_bnd:])
+
+
+# --- strong form (order 2): test_network.cpp, test_losses.cpp, acceptance --
+def test_one_unit_closed_form_second_derivatives():
+    # test_network.cpp:74-92 at order 2 (1e-14)
+    w11, w12, b1, w2, b2 = 0.7, -0.4, 0.2, 1.3, -0.5
+    pb, par = _one_unit(w11, w12, b1, w2, b2)
+    pts = np.array([[0.3, -0.8], [-1.1, 0.45], [2.0, 1.0]])
+    u, ux, uy, uxx, uyy = pb.evaluate2(par, pts)
+    for i, (x, y) in enumerate(pts):
+        z = math.tanh(w11 * x + w12 * y + b1)
+        s1 = 1 - z * z
+        s2 = -2.0 * z * s1
+        assert abs(u[i] - (w2 * z + b2)) < 1e-14
+        assert abs(ux[i] - w2 * s1 * w11) < 1e-14
+        assert abs(uy[i] - w2 * s1 * w12) < 1e-14
+        assert abs(uxx[i] - w2 * s2 * w11 * w11) < 1e-14
+        assert abs(uyy[i] - w2 * s2 * w12 * w12) < 1e-14
+
+
+def test_second_derivatives_match_finite_differences_of_u():
+    # test_network.cpp:137-157 (1e-7 first, 1e-3 second derivatives)
+    nodes, cells = po.structured_mesh(1, 1)
+    pb = po.OracleProblem(spec_for(nodes, cells, layers=(2, 10, 8, 1), n_test_1d=1, n_quad_1d=2,
+                                   seed=5), double=True)
+    par = pb.init_params()
+    h = 1e-6
+    for x, y in ((0.2, 0.7), (-0.5, 0.1)):
+        u, ux, uy, uxx, uyy = (a[0] for a in pb.evaluate2(par, [[x, y]]))
+        f = lambda a, b: pb.evaluate(par, [[a, b]], 0)[0][0]
+        assert abs(ux - (f(x + h, y) - f(x - h, y)) / (2 * h)) < 1e-7
+        assert abs(uy - (f(x, y + h) - f(x, y - h)) / (2 * h)) < 1e-7
+        assert abs(uxx - (f(x + h, y) - 2 * u + f(x - h, y)) / (h * h)) < 1e-3
+        assert abs(uyy - (f(x, y + h) - 2 * u + f(x, y - h)) / (h * h)) < 1e-3
+
+
+def test_strong_residual_value_and_adjoints():
+    # test_losses.cpp:344-412: six points from Rng(42), scalar eps 0.8,
+    # b = (0.5, -0.4), segment [1, 5)
+    r = SplitMix(42)
+    n = 6
+    cols = {k: np.zeros(n) for k in ("u", "ux", "uy", "uxx", "uyy")}
+    for i in range(n):
+        for k in ("u", "ux", "uy", "uxx", "uyy"):
+            cols[k][i] = r.uniform(-1, 1)
+    fs = np.array([0.1, -0.2, 0.3, 0.0])
+    args = dict(bx=0.5, by=-0.4, eps_source=1, eps_scalar_index=0, scalars=(0.8,))
+    ev = [cols[k] for k in ("u", "ux", "uy", "uxx", "uyy")]
+    got, uxb, uyb, uxxb, uyyb, sb = po.strong_loss(*ev, 1, 4, fs, **args)
+    expect = 0.0
+    for i in range(4):
+        p = 1 + i
+        P = -0.8 * (cols["uxx"][p] + cols["uyy"][p]) + 0.5 * cols["ux"][p] - 0.4 * cols["uy"][p] - fs[i]
+        expect += P * P / 4.0
+    assert abs(got - expect) <= 1e-14 * abs(expect)
+    assert uxb[0] == 0.0  # outside the segment
+    h = 1e-6
+    for p in range(1, 5):
+        ep = [a.copy() for a in ev]
+        em = [a.copy() for a in ev]
+        ep[3][p] += h
+        em[3][p] -= h
+        fd = (po.strong_loss(*ep, 1, 4, fs, **args)[0] - po.strong_loss(*em, 1, 4, fs, **args)[0]) / (2 * h)
+        assert abs(uxxb[p] - fd) <= 1e-7
+    ap = dict(args, scalars=(0.8 + h,))
+    am = dict(args, scalars=(0.8 - h,))
+    fd = (po.strong_loss(*ev, 1, 4, fs, **ap)[0] - po.strong_loss(*ev, 1, 4, fs, **am)[0]) / (2 * h)
+    assert abs(sb[0] - fd) <= 1e-7
+    with pytest.raises(po.OracleError):  # spatial coefficient rejected
+        po.strong_loss(*ev, 1, 4, fs, eps_source=2)
+
+
+def _strong_problem(**kw):
+    # acceptance_main.cpp:111-160, case 4: 2x2 mesh, 4 quad / 3 test per dim,
+    # 40 boundary points, weights 10/10, forcing 'one', g = 0, [2,12,12,1]
+    nodes, cells = po.structured_mesh(2, 2)
+    base = dict(n_test_1d=3, n_quad_1d=4, forcing="one", boundary_g="zero", n_boundary=40,
+                layers=(2, 12, 12, 1), strong=True)
+    base.update(kw)
+    return po.OracleProblem(po.ProblemSpec(nodes=nodes, cells=cells, **base), double=True)
+
+
+@pytest.mark.parametrize("variant", ["acceptance", "convection_scalar_eps", "sigmoid"])
+def test_strong_form_parameter_gradient_matches_finite_differences(variant):
+    # acceptance_main.cpp:171-214 criterion 2 (rel 1e-4, floor 1e-8) on the
+    # strong-form case, plus convection / trainable eps / sigmoid variants
+    kw = {"acceptance": {},
+          # constant forcing keeps P = O(1), above the finite-difference
+          # noise floor (acceptance_main.cpp:156-157)
+          "convection_scalar_eps": dict(bx=0.6, by=-0.3, eps_source=1, scalars=(1.3,),
+                                        n_sensors=6, sensor_field="sin2pi_u"),
+          "sigmoid": dict(sigmoid=True, layers=(2, 7, 6, 5, 1))}[variant]
+    pb = _strong_problem(**kw)
+    f = pb.array("strong_forcing")
+    pts = pb.array("points")[: pb.n_int]
+    np.testing.assert_array_equal(f, po.field("one", pts[:, 0], pts[:, 1]))
+    p0 = pb.init_params()
+    parts, g = pb.loss_and_grad(p0)
+    assert abs(parts[0] - (parts[1] + 10 * parts[2] + 10 * parts[3])) <= 1e-13 * abs(parts[0])
+    worst = 0.0
+    for i in range(p0.size):
+        step = 1e-6 * max(1.0, abs(p0[i]))
+        pp, pm = p0.copy(), p0.copy()
+        pp[i] += step
+        pm[i] -= step
+        fd = (pb.loss_and_grad(pp)[0][0] - pb.loss_and_grad(pm)[0][0]) / (2 * step)
+        allowed = max(1e-4 * max(abs(g[i]), abs(fd)), 1e-8)
+        worst = max(worst, abs(g[i] - fd) / allowed)
+    assert worst <= 1.0, worst
+
+
+def test_strong_residual_is_mean_square_of_pointwise_operator():
+    # trainer.hpp:246-248 + losses.hpp:446-455 recomputed from evaluate(order 2)
+    pb = _strong_problem(bx=0.6, by=-0.3, eps=0.7, forcing="sin2pi_f")
+    p0 = pb.init_params()
+    parts, _ = pb.loss_and_grad(p0)
+    pts = pb.array("points")[: pb.n_int]
+    u, ux, uy, uxx, uyy = pb.evaluate2(p0, pts)
+    f = pb.array("strong_forcing")
+    P = -0.7 * (uxx + uyy) + 0.6 * ux - 0.3 * uy - f
+    assert abs(parts[1] - np.mean(P * P)) <= 1e-12 * parts[1]
