@@ -58,6 +58,10 @@ extern "C" {
 #define VPINN_EPS_SCALAR 1
 #define VPINN_EPS_SPATIAL 2
 
+/* LossForm (trainer.hpp:178) */
+#define VPINN_FORM_WEAK 0
+#define VPINN_FORM_STRONG 1
+
 /* Activation (network.hpp:31) */
 #define VPINN_ACT_TANH 0
 #define VPINN_ACT_SIGMOID 1
@@ -120,6 +124,16 @@ typedef struct vpinn_gpu_problem {
    * device from this input; grad_x/grad_y/test/forcing are then ignored and
    * points holds only [boundary | sensors] (n_interior = n_elem*n_quad) */
   const vpinn_gpu_assembly* assembly;
+  /* LossForm (trainer.hpp:178, 246-248).  VPINN_FORM_STRONG replaces the
+   * variational residual by the strong-form collocation residual at the
+   * interior points (strong_residual_loss, losses.hpp:422-467) with order-2
+   * network derivatives; grad_x/grad_y/test/forcing are then unused and
+   * strong_forcing holds f at the n_interior points (commands.hpp:147-152,
+   * cast to float), or is NULL with assembly set (f evaluated on the device
+   * at the assembled points).  Hidden widths <= 32, one output channel,
+   * fixed or scalar eps. */
+  int32_t form;
+  const float* strong_forcing;
 } vpinn_gpu_problem;
 
 /* TrainConfig subset (trainer.hpp:64-97) */
@@ -205,6 +219,12 @@ int vpinn_gpu_forward(vpinn_gpu_ctx* ctx, const double* points, int64_t n, int o
  * (n_elem*n_quad each; eps for the spatial source; scalars for the scalar
  * source).  Outputs: loss, residuals (n_test x n_elem column-major, may be
  * NULL), adjoints (may be NULL), scalar_bar (n_scalars, may be NULL). */
+/* evaluate(net, points, 2) (network.hpp:414-449): u, first and second
+ * derivatives at n points; NULL outputs skipped.  Strong-form contexts only
+ * (the order-2 kernel is the strong-form one). */
+int vpinn_gpu_forward2(vpinn_gpu_ctx* ctx, const double* points, int64_t n, float* u, float* du_dx,
+                       float* du_dy, float* d2u_dx2, float* d2u_dy2);
+
 int vpinn_gpu_contract(vpinn_gpu_ctx* ctx, const float* du_dx, const float* du_dy,
                        const float* eps, const float* scalars, float weight, double* loss,
                        float* residuals, float* du_dx_bar, float* du_dy_bar, float* eps_bar,

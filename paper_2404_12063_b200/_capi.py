@@ -43,7 +43,11 @@ class Problem(C.Structure):
         ("tau", C.c_double), ("gamma", C.c_double),
         ("device", C.c_int32), ("rank", C.c_int32), ("world_size", C.c_int32),
         ("assembly", C.c_void_p),
+        ("form", C.c_int32), ("strong_forcing", C.c_void_p),
     ]
+
+
+FORM_WEAK, FORM_STRONG = 0, 1
 
 
 class TrainSpec(C.Structure):
@@ -93,6 +97,7 @@ def _declare(L):
         "vpinn_gpu_synchronize": (i32, [vp]),
         "vpinn_gpu_time_steps": (i32, [vp, i32, d, pd]),
         "vpinn_gpu_forward": (i32, [vp, vp, i64, i32, vp, vp, vp, vp]),
+        "vpinn_gpu_forward2": (i32, [vp, vp, i64, vp, vp, vp, vp, vp]),
         "vpinn_gpu_contract": (i32, [vp, vp, vp, vp, vp, C.c_float, pd, vp, vp, vp, vp, vp]),
         "vpinn_gpu_time_contract": (i32, [vp, i32, pd, pd]),
         "vpinn_gpu_download_tensor": (i32, [vp, i32, vp, i64]),

@@ -183,7 +183,7 @@ cudaError_t assemble_on_device(const AsmInput& in, int64_t e0, int E, float* gx,
   a.qp = qp;
   a.qpf = qpf;
   a.fq = fq_scratch;
-  a.field = forcing ? in.field : -1;
+  a.field = fq_scratch ? in.field : -1;  // f at the points when a scratch is given
   a.bad = bad;
   const int64_t n = (int64_t)E * in.Q;
   if (n > 0) {

@@ -44,8 +44,8 @@ struct AsmInput {
 
 // assemble cells [e0, e0 + E) into gx/gy/tv ([E][T][Q]), forcing ([E][T]),
 // quadrature points qp (double [E*Q][2]) / qpf (float2), all optional except
-// gx/gy; tv is required when forcing is assembled; fq_scratch holds E*Q
-// floats; *bad receives the smallest degenerate global cell index (atomicMin)
+// gx/gy; tv is required when forcing is assembled; fq_scratch (E*Q floats)
+// receives (float)f at the points when non-null (required with forcing); *bad receives the smallest degenerate global cell index (atomicMin)
 cudaError_t assemble_on_device(const AsmInput& in, int64_t e0, int E, float* gx, float* gy, float* tv,
                                float* forcing, double* qp, float2* qpf, float* fq_scratch, int* bad,
                                cudaStream_t s);

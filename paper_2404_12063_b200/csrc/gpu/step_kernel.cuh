@@ -97,6 +97,12 @@ struct StepArgs {
   // tc2_step_kernel: per-CTA fp32 parameter-gradient scratch [cta][layer][64][64]
   float* tc_scratch;
   int tc_force_spill;  // test hook (VPINN_TC2_FORCE_SPILL=1): spill the accumulators every tile
+  // strong form (sf_step_kernel.cuh): f at the interior points, 1/N_int
+  // (global) and Real(2)*weight*inv_n; order-2 evaluate outputs
+  const float* sforce;
+  float inv_ni, rscale_s;
+  float* out_uxx;
+  float* out_uyy;
 };
 constexpr int kPhaseTiles = 8, kPhaseMarks = 32;
 

@@ -22,6 +22,7 @@
 #include "aux_kernels.cuh"
 #include "contract_cells.cuh"
 #include "contract_mf.cuh"
+#include "sf_step.h"
 #include "tc_selftest.cuh"
 #include "tc_step_kernel.cuh"
 #include "tc2_step_kernel.cuh"
@@ -322,6 +323,12 @@ struct vpinn_gpu_ctx {
   std::unique_ptr<AsmUpload> asmd;
   DBuf<float> mf_tabs, mf_rule;
   int64_t asm_e0 = 0;
+  // strong form (sf_step_kernel.cuh): no tensors, f at the interior points
+  bool strong = false;
+  DBuf<float> sforce;
+  vpg::SfKernels sfk{};
+  int sf_warps = 0;
+  long long n_int_global = 0;
   bool tc2 = false;           // fp16-split two-CTA tensor-core step
   bool tc2_modes = false;     // tc2 forward / reverse modes serve the split path and evaluate
   int grid_tc2 = 0;           // 2 CTAs per SM
@@ -340,7 +347,75 @@ namespace {
 
 void set_dev(vpinn_gpu_ctx* c) { CK(cudaSetDevice(c->device)); }
 
+// entry points that work on the premultiplier tensors
+void weak_only(const vpinn_gpu_ctx* c, const char* what) {
+  if (c && c->strong) throw Fail{VPINN_ERR_CONFIG, std::string(what) + ": the context is strong-form (no tensors)"};
+}
+
+// strong form: one persistent warp-tiled kernel (1 CTA per SM, as many warps
+// as the per-warp layer state fits), then the same reduce + Adam kernels
+void configure_strong(vpinn_gpu_ctx* c) {
+  vpg::StepArgs& a = c->sargs;
+  std::memset(&a, 0, sizeof(a));
+  a.E = c->E;
+  a.T = c->T;
+  a.Q = c->Q;
+  a.pts = c->pts.p;
+  a.n_int = c->n_int;
+  a.n_bnd = c->n_bnd;
+  a.n_sen = c->n_sen;
+  a.bval = c->bval.p;
+  a.sval = c->sval.p;
+  a.eps = c->eps;
+  a.bx = c->bx;
+  a.by = c->by;
+  a.eps_source = c->eps_source;
+  a.eps_scalar_index = c->eps_idx;
+  a.bscale = c->nb_global ? 2.0f * (float)c->tau / (float)c->nb_global : 0.0f;
+  a.sscale = c->ns_global ? 2.0f * (float)c->gamma / (float)c->ns_global : 0.0f;
+  // losses.hpp:445, 452: inv_n = Real(1)/Real(count), pbar = Real(2)*weight*inv_n*P
+  a.inv_ni = c->n_int_global ? 1.0f / (float)c->n_int_global : 0.0f;
+  a.rscale_s = (2.0f * 1.0f) * a.inv_ni;
+  a.sforce = c->sforce.p;
+  a.net = c->net;
+  a.params = c->params.p;
+  const int D = c->net.n_layers - 1;
+  int optin = 0;
+  CK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, c->device));
+  int w = vpg::kSfMaxWarps;
+  if (const char* e = std::getenv("VPINN_SF_WARPS")) w = std::max(1, std::min(vpg::kSfMaxWarps, std::atoi(e)));
+  while (w > 1 && vpg::sf_smem_bytes(D, w) > (size_t)optin) --w;
+  if (vpg::sf_smem_bytes(D, w) > (size_t)optin) throw Fail{VPINN_ERR_CONFIG, "strong-form kernel does not fit shared memory"};
+  c->sf_warps = w;
+  c->smem_step = vpg::sf_smem_bytes(D, w);
+  for (auto fn : {c->sfk.fused, c->sfk.forward}) {
+    CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem_step));
+    CK(cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+  }
+  int occ = 0;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, c->sfk.fused, 32 * w, c->smem_step));
+  if (occ < 1) throw Fail{VPINN_ERR_DEVICE, "strong-form kernel cannot be resident"};
+  const int P_local = c->n_int + c->n_bnd + c->n_sen;
+  const int tiles = ceil_div(P_local, 16);
+  c->grid_step = std::max(1, std::min(occ * c->sm_count, ceil_div(tiles, w)));
+  c->grad_rows = c->loss_rows = c->grid_step;
+  c->kernel_name = "sf_step_kernel<" + std::to_string(D) + "," + (c->net.sigmoid ? "sigmoid" : "tanh") +
+                   "> (strong form, mma.sync 3xTF32, " + std::to_string(w) + " warps/CTA)";
+  c->part_stride = (c->grad_rows + 31) & ~31;
+  c->grad_part.alloc((size_t)c->part_stride * c->n_params, c->stream);
+  a.part_stride = c->part_stride;
+  a.grad_part = c->grad_part.p;
+  c->loss_part.alloc((size_t)c->loss_rows * vpg::kLpWords, c->stream);
+  a.loss_part = c->loss_part.p;
+  c->red.alloc((size_t)c->n_params + vpg::kLpWords, c->stream);
+  c->e_scalar.alloc(1, c->stream);
+}
+
 void configure(vpinn_gpu_ctx* c) {
+  if (c->strong) {
+    configure_strong(c);
+    return;
+  }
   // ---- fused path when a cell fits a CTA, split path otherwise ----
   const int P_local = c->n_int + c->n_bnd + c->n_sen;
   c->split = c->Q > vpg::kThreads;
@@ -653,7 +728,9 @@ void configure(vpinn_gpu_ctx* c) {
 }
 
 void launch_fused(vpinn_gpu_ctx* c, const vpg::StepArgs& a) {
-  if (c->tc2)
+  if (c->strong)
+    c->sfk.fused<<<c->grid_step, 32 * c->sf_warps, c->smem_step, c->stream>>>(a);
+  else if (c->tc2)
     c->var.tc2<<<c->grid_step, vpg::t2::kNT, c->smem_step, c->stream>>>(a);
   else if (c->tc)
     c->var.tc<<<c->grid_step, 128 * vpg::kTcNQ, c->smem_step, c->stream>>>(a);
@@ -924,8 +1001,13 @@ int vpinn_gpu_create(const vpinn_gpu_problem* pb, vpinn_gpu_ctx** out) {
     // ---- validation (contract checks of losses.hpp:70-84, network.hpp:66-76) ----
     if (pb->n_elem < 1 || pb->n_test < 1 || pb->n_quad < 1)
       throw Fail{VPINN_ERR_CONFIG, "n_elem, n_test, n_quad must be >= 1"};
-    if (!pb->assembly && (!pb->grad_x || !pb->grad_y || !pb->forcing || !pb->points))
+    if (pb->form != VPINN_FORM_WEAK && pb->form != VPINN_FORM_STRONG)
+      throw Fail{VPINN_ERR_CONFIG, "form must be weak or strong"};
+    const bool strong = pb->form == VPINN_FORM_STRONG;
+    if (!strong && !pb->assembly && (!pb->grad_x || !pb->grad_y || !pb->forcing || !pb->points))
       throw Fail{VPINN_ERR_NUMERIC, "tensor kernel: tensors/forcing/points missing"};
+    if (strong && !pb->assembly && (!pb->strong_forcing || !pb->points))
+      throw Fail{VPINN_ERR_NUMERIC, "strong residual: forcing/points missing"};
     if (pb->n_interior != (int64_t)pb->n_elem * pb->n_quad)
       throw Fail{VPINN_ERR_NUMERIC, "evaluation does not cover the interior quadrature points"};
     if (pb->n_layer_sizes < 3 || pb->n_layer_sizes > vpg::kMaxLayers)
@@ -948,13 +1030,20 @@ int vpinn_gpu_create(const vpinn_gpu_problem* pb, vpinn_gpu_ctx** out) {
     const int act = pb->activation == VPINN_ACT_SIGMOID ? 1 : 0;
     for (const auto& v : variants())
       if (v.D == D && v.C == C && v.ACT == act && v.H >= maxH && (!var || v.H < var->H)) var = &v;
-    if (!var)
+    if (strong) {
+      // losses.hpp:437-441 and the strong-form kernel's shape range
+      if (pb->eps_source == VPINN_EPS_SPATIAL)
+        throw Fail{VPINN_ERR_NUMERIC, "strong residual does not support a spatial coefficient"};
+      if (C != 1) throw Fail{VPINN_ERR_CONFIG, "strong form on the GPU path: one output channel"};
+      if (maxH > 32 || D > 4)
+        throw Fail{VPINN_ERR_CONFIG, "strong form on the GPU path: hidden widths <= 32, at most 4 hidden layers"};
+    } else if (!var)
       throw Fail{VPINN_ERR_CONFIG, "network shape not instantiated for the GPU path (hidden layers " +
                                        std::to_string(D) + ", width " + std::to_string(maxH) +
                                        ", outputs " + std::to_string(C) + ", activation " +
                                        (act ? "sigmoid" : "tanh") + ")"};
     const bool conv = pb->bx != 0.0f || pb->by != 0.0f;
-    if (conv && !pb->test && !pb->assembly) throw Fail{VPINN_ERR_NUMERIC, "convection needs the test tensor"};
+    if (!strong && conv && !pb->test && !pb->assembly) throw Fail{VPINN_ERR_NUMERIC, "convection needs the test tensor"};
     const int W = std::max(1, pb->world_size), R = pb->rank;
     if (R < 0 || R >= W) throw Fail{VPINN_ERR_CONFIG, "rank out of range"};
 
@@ -975,7 +1064,13 @@ int vpinn_gpu_create(const vpinn_gpu_problem* pb, vpinn_gpu_ctx** out) {
     c->sm_count = prop.multiProcessorCount;
     CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
     CK(cudaMallocHost(&c->h_flag, sizeof(int) * 4));
-    c->var = *var;
+    if (var) c->var = *var;
+    c->strong = strong;
+    if (strong) {
+      c->sfk = vpg::sf_kernels(D, act);
+      if (!c->sfk.fused) throw Fail{VPINN_ERR_CONFIG, "strong form: no kernel for this depth"};
+    }
+    c->n_int_global = pb->n_interior;
 
     // ---- network descriptor (network.hpp:98-128 offsets) ----
     vpg::NetDesc& nd = c->net;
@@ -1026,12 +1121,20 @@ int vpinn_gpu_create(const vpinn_gpu_problem* pb, vpinn_gpu_ctx** out) {
     auto push = [&](long long i) {
       hp.push_back(make_float2((float)pb->points[2 * i], (float)pb->points[2 * i + 1]));
     };
-    for (int t = 0; t < c->nt; ++t) c->tens[t].alloc(TQ * c->E, c->stream);
-    c->forcing.alloc((size_t)c->T * c->E, c->stream);
+    if (!strong) {
+      for (int t = 0; t < c->nt; ++t) c->tens[t].alloc(TQ * c->E, c->stream);
+      c->forcing.alloc((size_t)c->T * c->E, c->stream);
+    }
     if (!pb->assembly) {
       const float* src[3] = {pb->grad_x, pb->grad_y, pb->test};
-      for (int t = 0; t < c->nt; ++t) c->tens[t].upload(src[t] + TQ * e0, TQ * c->E, c->stream);
-      c->forcing.upload(pb->forcing + (size_t)c->T * e0, (size_t)c->T * c->E, c->stream);
+      if (!strong) {
+        for (int t = 0; t < c->nt; ++t) c->tens[t].upload(src[t] + TQ * e0, TQ * c->E, c->stream);
+        c->forcing.upload(pb->forcing + (size_t)c->T * e0, (size_t)c->T * c->E, c->stream);
+      } else {
+        // commands.hpp:147-152: this rank's slice of f at the interior points
+        c->sforce.alloc((size_t)c->n_int, c->stream);
+        c->sforce.upload(pb->strong_forcing + e0 * pb->n_quad, (size_t)c->n_int, c->stream);
+      }
       for (long long i = e0 * pb->n_quad; i < e1 * pb->n_quad; ++i) push(i);
       for (long long i = b0; i < b1; ++i) push(pb->n_interior + i);
       for (long long i = s0; i < s1; ++i) push(pb->n_interior + NB + i);
@@ -1068,15 +1171,25 @@ int vpinn_gpu_create(const vpinn_gpu_problem* pb, vpinn_gpu_ctx** out) {
         c->mf_rule.upload(rule.data(), rule.size(), c->stream);
         CK(cudaStreamSynchronize(c->stream));  // host staging vectors go out of scope
       }
-      DBuf<float> tv_tmp, fq;
-      float* tv = c->nt == 3 ? c->tens[2].p : nullptr;
-      if (!tv) {
-        tv_tmp.alloc(TQ * c->E, c->stream);
-        tv = tv_tmp.p;
+      DBuf<float> tv_tmp, fq, gx_tmp, gy_tmp;
+      if (!strong) {
+        float* tv = c->nt == 3 ? c->tens[2].p : nullptr;
+        if (!tv) {
+          tv_tmp.alloc(TQ * c->E, c->stream);
+          tv = tv_tmp.p;
+        }
+        fq.alloc((size_t)c->n_int, c->stream);
+        CK(vpg::assemble_on_device(up.in, e0, c->E, c->tens[0].p, c->tens[1].p, tv, c->forcing.p, nullptr,
+                                   c->pts.p, fq.p, up.bad.p, c->stream));
+      } else {
+        // the points and f at them ((float)f(x_q), commands.hpp:147-152); the
+        // premultipliers are built and dropped (the geometry checks still run)
+        gx_tmp.alloc(TQ * c->E, c->stream);
+        gy_tmp.alloc(TQ * c->E, c->stream);
+        c->sforce.alloc((size_t)c->n_int, c->stream);
+        CK(vpg::assemble_on_device(up.in, e0, c->E, gx_tmp.p, gy_tmp.p, nullptr, nullptr, nullptr, c->pts.p,
+                                   c->sforce.p, up.bad.p, c->stream));
       }
-      fq.alloc((size_t)c->n_int, c->stream);
-      CK(vpg::assemble_on_device(up.in, e0, c->E, c->tens[0].p, c->tens[1].p, tv, c->forcing.p, nullptr,
-                                 c->pts.p, fq.p, up.bad.p, c->stream));
       up.check(c->stream);
     }
     std::vector<float> bv, sv;
@@ -1322,7 +1435,10 @@ int vpinn_gpu_forward(vpinn_gpu_ctx* c, const double* points, int64_t n, int ord
     f.out_eps = de.p;
     f.union_floats = 0;
     f.stop_flag = nullptr;
-    if (c->tc2_modes) {
+    if (c->strong) {
+      const int grid = std::max(1, std::min(c->grid_step, ceil_div(n, 16 * c->sf_warps)));
+      c->sfk.forward<<<grid, 32 * c->sf_warps, c->smem_step, c->stream>>>(f);
+    } else if (c->tc2_modes) {
       const int grid = std::max(1, std::min(c->grid_tc2, ceil_div(n, 128)));
       c->var.tc2_fwd<<<grid, vpg::t2::kNT, c->var.tc2_smem, c->stream>>>(f);
     } else {
@@ -1334,7 +1450,7 @@ int vpinn_gpu_forward(vpinn_gpu_ctx* c, const double* points, int64_t n, int ord
     CK(cudaMemcpyAsync(u, du.p, sizeof(float) * n, cudaMemcpyDeviceToHost, c->stream));
     if (order >= 1 && du_dx) CK(cudaMemcpyAsync(du_dx, dux.p, sizeof(float) * n, cudaMemcpyDeviceToHost, c->stream));
     if (order >= 1 && du_dy) CK(cudaMemcpyAsync(du_dy, duy.p, sizeof(float) * n, cudaMemcpyDeviceToHost, c->stream));
-    if (eps && c->var.C >= 2) CK(cudaMemcpyAsync(eps, de.p, sizeof(float) * n, cudaMemcpyDeviceToHost, c->stream));
+    if (eps && !c->strong && c->var.C >= 2) CK(cudaMemcpyAsync(eps, de.p, sizeof(float) * n, cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));
     std::vector<float> chk(n);
     // network.hpp:443-447: non-finite outputs are a numeric error
@@ -1345,10 +1461,49 @@ int vpinn_gpu_forward(vpinn_gpu_ctx* c, const double* points, int64_t n, int ord
   });
 }
 
+int vpinn_gpu_forward2(vpinn_gpu_ctx* c, const double* points, int64_t n, float* u, float* du_dx, float* du_dy,
+                       float* d2u_dx2, float* d2u_dy2) {
+  return guarded([&] {
+    if (!c->strong) throw Fail{VPINN_ERR_CONFIG, "evaluate order 2: strong-form contexts only"};
+    if (n <= 0) return;
+    set_dev(c);
+    std::vector<float2> hp(n);
+    for (int64_t i = 0; i < n; ++i) hp[i] = make_float2((float)points[2 * i], (float)points[2 * i + 1]);
+    DBuf<float2> dp;
+    DBuf<float> o[5];
+    dp.alloc(n, c->stream);
+    dp.upload(hp.data(), n, c->stream);
+    float* host[5] = {u, du_dx, du_dy, d2u_dx2, d2u_dy2};
+    for (int k = 0; k < 5; ++k)
+      if (host[k]) o[k].alloc(n, c->stream);
+    vpg::StepArgs f = c->sargs;
+    f.fwd_pts = dp.p;
+    f.n_fwd = (int)n;
+    f.out_u = o[0].p;
+    f.out_ux = o[1].p;
+    f.out_uy = o[2].p;
+    f.out_uxx = o[3].p;
+    f.out_uyy = o[4].p;
+    f.stop_flag = nullptr;
+    const int grid = std::max(1, std::min(c->grid_step, ceil_div(n, 16 * c->sf_warps)));
+    c->sfk.forward<<<grid, 32 * c->sf_warps, c->smem_step, c->stream>>>(f);
+    CK(cudaGetLastError());
+    c->launches += 1;
+    for (int k = 0; k < 5; ++k)
+      if (host[k]) CK(cudaMemcpyAsync(host[k], o[k].p, sizeof(float) * n, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    for (int k = 0; k < 5; ++k)
+      if (host[k])
+        for (int64_t i = 0; i < n; ++i)
+          if (!std::isfinite(host[k][i])) throw Fail{VPINN_ERR_NUMERIC, "evaluate: non-finite network output"};
+  });
+}
+
 int vpinn_gpu_contract(vpinn_gpu_ctx* c, const float* du_dx, const float* du_dy, const float* eps,
                        const float* scalars, float weight, double* loss, float* residuals,
                        float* du_dx_bar, float* du_dy_bar, float* eps_bar, double* scalar_bar) {
   return guarded([&] {
+    weak_only(c, "vpinn_gpu_contract");
     set_dev(c);
     if (c->eps_source == VPINN_EPS_SPATIAL && !eps)
       throw Fail{VPINN_ERR_NUMERIC, "spatial coefficient requested but no eps given"};
@@ -1392,6 +1547,7 @@ int vpinn_gpu_contract(vpinn_gpu_ctx* c, const float* du_dx, const float* du_dy,
 
 int vpinn_gpu_time_contract(vpinn_gpu_ctx* c, int reps, double* ms_per_launch, double* bytes) {
   return guarded([&] {
+    weak_only(c, "vpinn_gpu_time_contract");
     set_dev(c);
     const size_t ni = (size_t)c->n_int;
     DBuf<float> ux, uy, ep, oxb, oyb, oeb, es;
@@ -1495,6 +1651,7 @@ int vpinn_gpu_contract_matrix_free(vpinn_gpu_ctx* c, const float* du_dx, const f
                                    float weight, double* loss, float* residuals, float* du_dx_bar,
                                    float* du_dy_bar, double* scalar_bar) {
   return guarded([&] {
+    weak_only(c, "vpinn_gpu_contract_matrix_free");
     set_dev(c);
     if (c->eps_source == VPINN_EPS_SCALAR && !scalars)
       throw Fail{VPINN_ERR_NUMERIC, "coefficient scalar index out of range"};
@@ -1532,6 +1689,7 @@ int vpinn_gpu_contract_matrix_free(vpinn_gpu_ctx* c, const float* du_dx, const f
 
 int vpinn_gpu_time_contract_matrix_free(vpinn_gpu_ctx* c, int reps, double* ms_per_launch, double* bytes) {
   return guarded([&] {
+    weak_only(c, "vpinn_gpu_time_contract_matrix_free");
     set_dev(c);
     const size_t ni = (size_t)c->n_int;
     DBuf<float> ux, uy, oxb, oyb, es;
@@ -1572,6 +1730,7 @@ int vpinn_gpu_time_contract_matrix_free(vpinn_gpu_ctx* c, int reps, double* ms_p
 
 int vpinn_gpu_download_tensor(vpinn_gpu_ctx* c, int which, float* out, int64_t n) {
   return guarded([&] {
+    weak_only(c, "vpinn_gpu_download_tensor");
     set_dev(c);
     const DBuf<float>* b = which <= 2 ? &c->tens[which] : &c->forcing;
     if (which < 0 || which > 3) throw Fail{VPINN_ERR_CONFIG, "download: selector"};
@@ -1586,6 +1745,7 @@ int64_t vpinn_gpu_launch_count(const vpinn_gpu_ctx* c) { return c ? c->launches 
 int vpinn_gpu_profile_step(vpinn_gpu_ctx* c, int reps, double* ms_mlp, double* ms_reduce,
                            double* ms_adam) {
   return guarded([&] {
+    weak_only(c, "vpinn_gpu_profile_step");
     set_dev(c);
     reset_state(c, LLONG_MAX, nullptr);
     const vpg::AdamArgs aa = adam_args(c, false, 1e-4f, false, 0);

@@ -37,14 +37,16 @@ class GpuStep:
                  n_interior, n_boundary, n_sensors, boundary_values=None, sensor_values=None,
                  layer_sizes: Sequence[int] = (2, 30, 30, 30, 1), sigmoid=False, n_scalars=0,
                  eps=1.0, bx=0.0, by=0.0, eps_source=EPS_FIXED, eps_scalar_index=0,
-                 tau=10.0, gamma=10.0, device=0, rank=0, world_size=1):
+                 tau=10.0, gamma=10.0, device=0, rank=0, world_size=1, strong_forcing=None):
+        """strong_forcing (f at the n_interior points) selects LossForm::strong
+        (trainer.hpp:246-248); the tensors and forcing may then be None."""
         L = _capi.lib()
         f32 = lambda a: None if a is None else np.ascontiguousarray(a, dtype=np.float32)
         f64 = lambda a: None if a is None else np.ascontiguousarray(a, dtype=np.float64)
         self._keep = [f32(grad_x), f32(grad_y), f32(test), f32(forcing), f64(points),
                       f64(boundary_values), f64(sensor_values),
-                      np.ascontiguousarray(layer_sizes, dtype=np.int32)]
-        gx, gy, tv, fc, pts, bv, sv, ls = self._keep
+                      np.ascontiguousarray(layer_sizes, dtype=np.int32), f32(strong_forcing)]
+        gx, gy, tv, fc, pts, bv, sv, ls, sf = self._keep
         pb = _capi.Problem()
         pb.n_elem, pb.n_test, pb.n_quad = n_elem, n_test, n_quad
         pb.grad_x, pb.grad_y, pb.test, pb.forcing, pb.points = _p(gx), _p(gy), _p(tv), _p(fc), _p(pts)
@@ -57,6 +59,8 @@ class GpuStep:
         pb.eps_source, pb.eps_scalar_index = eps_source, eps_scalar_index
         pb.tau, pb.gamma = tau, gamma
         pb.device, pb.rank, pb.world_size = device, rank, world_size
+        if sf is not None:
+            pb.form, pb.strong_forcing = _capi.FORM_STRONG, _p(sf)
         h = C.c_void_p()
         _capi.check(L.vpinn_gpu_create(C.byref(pb), C.byref(h)))
         self.h = h
@@ -108,6 +112,14 @@ class GpuStep:
         u, ux, uy, e = (np.zeros(n, dtype=np.float32) for _ in range(4))
         _capi.check(_capi.lib().vpinn_gpu_forward(self.h, _p(pts), n, order, _p(u), _p(ux), _p(uy), _p(e)))
         return u, ux, uy, (e if self.layer_sizes[-1] >= 2 else None)
+
+    def forward2(self, points):
+        """evaluate(order 2): u, u_x, u_y, u_xx, u_yy (strong-form contexts)."""
+        pts = np.ascontiguousarray(points, dtype=np.float64).reshape(-1, 2)
+        n = pts.shape[0]
+        outs = [np.zeros(n, dtype=np.float32) for _ in range(5)]
+        _capi.check(_capi.lib().vpinn_gpu_forward2(self.h, _p(pts), n, *[_p(o) for o in outs]))
+        return tuple(outs)
 
     def contract(self, ux, uy, eps=None, scalars=None, weight=1.0):
         ni = self.n_elem * self.n_quad

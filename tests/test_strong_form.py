@@ -1,0 +1,152 @@
+"""Strong-form collocation on the GPU against the oracle.
+
+The oracle's strong form is pinned by the reference's order-2 / strong-residual
+known answers (tests/test_oracle_golden.py).  Here the B200 kernel
+(sf_step_kernel.cuh, mma.sync 3xTF32) must reproduce, on the same inputs:
+order-2 evaluate(), the composite objective and its gradient, and a 100-epoch
+training trajectory (loss within 1e-5 relative per epoch, the north-star
+tolerance).  CPU-side tests check the host plumbing only.
+"""
+import os
+
+import numpy as np
+import pytest
+
+from oracle import pyoracle as po
+from tests.refutil import read_msh
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden", "meshes")
+
+
+def rel(a, b):
+    return abs(a - b) / max(abs(b), 1e-30)
+
+
+def strong_spec(mesh=(4, 4), **over):
+    nodes, cells = po.structured_mesh(*mesh)
+    kw = dict(n_test_1d=3, n_quad_1d=5, forcing="sin2pi_f", boundary_g="sin2pi_u", n_boundary=120,
+              layers=(2, 30, 30, 30, 1), seed=42, strong=True)
+    kw.update(over)
+    return po.ProblemSpec(nodes=nodes, cells=cells, **kw)
+
+
+def make_strong_pair(spec, **kw):
+    from paper_2404_12063_b200.gpu import GpuStep
+    ob = po.OracleProblem(spec, double=False)
+    g = GpuStep(grad_x=None, grad_y=None, test=None, forcing=None, n_elem=ob.E, n_test=ob.T,
+                n_quad=ob.Q, points=ob.array("points"), n_interior=ob.n_int, n_boundary=ob.n_bnd,
+                n_sensors=ob.n_sen, boundary_values=ob.array("boundary_values"),
+                sensor_values=ob.array("sensor_values"), layer_sizes=spec.layers,
+                sigmoid=spec.sigmoid, n_scalars=len(spec.scalars), eps=spec.eps, bx=spec.bx,
+                by=spec.by, eps_source=spec.eps_source, eps_scalar_index=spec.eps_scalar_index,
+                tau=spec.tau, gamma=spec.gamma,
+                strong_forcing=ob.array("strong_forcing").astype(np.float32), **kw)
+    p0 = ob.init_params().astype(np.float32)
+    g.set_params(p0)
+    return ob, g, p0
+
+
+CASES = {
+    "poisson_d3": lambda: strong_spec(),
+    "acceptance_case4": lambda: strong_spec(mesh=(2, 2), n_test_1d=3, n_quad_1d=4, forcing="one",
+                                            boundary_g="zero", n_boundary=40, layers=(2, 12, 12, 1)),
+    "cd2d_sensors_scalar_eps": lambda: strong_spec(bx=0.7, by=-0.4, eps_source=1, scalars=(1.5,),
+                                                   n_sensors=37, sensor_field="sin2pi_u",
+                                                   layers=(2, 20, 20, 1)),
+    "sigmoid_d3_ragged": lambda: strong_spec(mesh=(3, 5), layers=(2, 7, 13, 5, 1), sigmoid=True,
+                                             n_boundary=33, eps=0.6),
+    "one_hidden": lambda: strong_spec(layers=(2, 24, 1), bx=0.3),
+    "four_hidden": lambda: strong_spec(layers=(2, 16, 16, 16, 16, 1), forcing="one",
+                                       boundary_g="zero"),
+    "gear_many_tiles": lambda: po.ProblemSpec(
+        *read_msh(os.path.join(GOLD, "gearlike_v41.msh")), n_test_1d=5, n_quad_1d=5, forcing="gear_f",
+        boundary_g="zero", n_boundary=800, eps=1.0, bx=0.1, layers=(2, 30, 30, 30, 1), seed=42,
+        strong=True),
+}
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", list(CASES))
+def test_strong_loss_and_gradient_match_oracle(name):
+    spec = CASES[name]()
+    ob, g, p0 = make_strong_pair(spec)
+    assert "sf_step_kernel" in g.step_kernel()
+    parts_o, _ = ob.loss_and_grad(p0)
+    parts_g, grad_g = g.loss_and_grad()
+    assert rel(parts_g[0], parts_o[0]) < 1e-5, (parts_g, parts_o)
+    for k in (1, 2, 3):
+        if parts_o[k] != 0.0:
+            assert rel(parts_g[k], parts_o[k]) < 1e-5, (k, parts_g, parts_o)
+    o64 = po.OracleProblem(spec, double=True)
+    _, g64 = o64.loss_and_grad(p0.astype(np.float64))
+    err = np.abs(grad_g - g64).max() / np.abs(g64).max()
+    assert err < 2e-4, err
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["poisson_d3", "sigmoid_d3_ragged", "four_hidden"])
+def test_order2_evaluate_matches_oracle(name):
+    spec = CASES[name]()
+    ob, g, p0 = make_strong_pair(spec)
+    rng = np.random.default_rng(7)
+    pts = rng.uniform(-1.2, 1.2, size=(2001, 2))
+    ref = ob.evaluate2(p0, pts)
+    got = g.forward2(pts)
+    for a, b in zip(got, ref):
+        assert np.abs(a - b).max() <= 3e-5 * max(1.0, np.abs(b).max())
+    # order 0/1 through the same kernel
+    u, ux, uy, _ = g.forward(pts, 1)
+    assert np.array_equal(u, got[0]) and np.array_equal(ux, got[1]) and np.array_equal(uy, got[2])
+
+
+@pytest.mark.gpu
+def test_strong_training_trajectory_matches_oracle():
+    """Per-epoch loss within 1e-5 relative over 100 epochs (north-star tolerance)."""
+    spec = CASES["cd2d_sensors_scalar_eps"]()
+    ob, g, p0 = make_strong_pair(spec)
+    ref = ob.train(p0, 100, lr0=1e-3, log_every=1)
+    rep = g.train(100, lr0=1e-3)
+    assert rep.steps_run == 100
+    tot_o = ref["every_step"][:, 0]
+    r = np.abs(rep.records["total"] - tot_o) / np.abs(tot_o)
+    assert r.max() < 1e-5, (r.max(), int(r.argmax()))
+    assert np.abs(g.get_params() - ref["params"]).max() < 1e-4
+    assert abs(rep.final_eps - ref["final_eps"]) < 1e-5
+
+
+@pytest.mark.gpu
+def test_strong_fresh_contexts_are_bitwise_identical():
+    spec = CASES["gear_many_tiles"]()
+    _, g1, _ = make_strong_pair(spec)
+    _, g2, _ = make_strong_pair(spec)
+    a, ga = g1.loss_and_grad()
+    b, gb = g2.loss_and_grad()
+    assert np.array_equal(a, b) and np.array_equal(ga, gb)
+
+
+@pytest.mark.gpu
+def test_strong_rank_partition_sums_to_whole():
+    """Two rank sub-contexts on one device: parts and gradients add up."""
+    spec = CASES["cd2d_sensors_scalar_eps"]()
+    ob, g, p0 = make_strong_pair(spec)
+    whole, gw = g.loss_and_grad()
+    acc = np.zeros(4)
+    gacc = np.zeros_like(gw)
+    for r in range(2):
+        _, gr, _ = make_strong_pair(spec, rank=r, world_size=2)
+        pr, grr = gr.loss_and_grad()
+        acc += pr
+        gacc += grr
+    assert np.allclose(acc, whole, rtol=1e-5)
+    assert np.abs(gacc - gw).max() <= 1e-5 * np.abs(gw).max()
+
+
+@pytest.mark.gpu
+def test_strong_rejects_unsupported_shapes():
+    from paper_2404_12063_b200._capi import VpinnError
+    with pytest.raises(VpinnError) as e:
+        make_strong_pair(strong_spec(layers=(2, 40, 1)))
+    assert e.value.code == 2
+    with pytest.raises(VpinnError) as e:
+        make_strong_pair(strong_spec(layers=(2, 16, 2), eps_source=2))
+    assert e.value.code == 4
