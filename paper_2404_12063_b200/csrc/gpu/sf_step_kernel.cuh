@@ -32,6 +32,14 @@
 
 #include "step_kernel.cuh"
 
+// rolled GEMM k-loops keep the kernel's instruction stream small enough for
+// the instruction cache (fully unrolled: 13k instructions, 44% of the stall
+// samples were no_instruction)
+#ifndef VPG_SF_ROLL
+#define VPG_SF_ROLL 1
+#endif
+#define VPG_SF_STR_(x) #x
+#define VPG_SF_PRAGMA_UNROLL(n) _Pragma(VPG_SF_STR_(unroll n))
 #ifndef VPG_SF_SPLIT_ONCE
 #define VPG_SF_SPLIT_ONCE 0
 #endif
@@ -273,7 +281,7 @@ __global__ void __launch_bounds__(32 * sf::kMaxWarps, 1) sf_step_kernel(const St
             for (int c = 0; c < 4; ++c) acc[s][n][c] = 0.0f;
         const float* Wl = sW + (l - 1) * NU * WS;
         const float* Sprev = slot + TILE_F + (l - 2) * 5 * TILE_F;  // hidden l-1 state (l >= 2)
-#pragma unroll
+VPG_SF_PRAGMA_UNROLL(VPG_SF_ROLL)
         for (int kt = 0; kt < 4; ++kt) {
           // A fragments of the five input streams: positions (g, k0), (g+8, k0),
           // (g, k0+1), (g+8, k0+1) with k0 = 8 kt + 2 t (the permuted K order)
@@ -509,10 +517,10 @@ __global__ void __launch_bounds__(32 * sf::kMaxWarps, 1) sf_step_kernel(const St
         float* Sp = slot + (h >= 2 ? TILE_F + (h - 2) * 5 * TILE_F : 0);
         __syncwarp();
         // ---- weight gradient of layer h: sum_s Abar_s^T X_s (M = i, N = k, K = points)
-#pragma unroll
+VPG_SF_PRAGMA_UNROLL(VPG_SF_ROLL)
         for (int kt = 0; kt < 2; ++kt) {
           const int pa = 8 * kt + t, pb = pa + 4;
-#pragma unroll
+VPG_SF_PRAGMA_UNROLL(VPG_SF_ROLL)
           for (int s = 0; s < 5; ++s) {
             const float* As = Ah + s * TILE_F;
             uint32_t ah[2][4], al[2][4];
@@ -562,7 +570,7 @@ __global__ void __launch_bounds__(32 * sf::kMaxWarps, 1) sf_step_kernel(const St
 #pragma unroll
             for (int c = 0; c < 4; ++c) zacc[s][n][c] = 0.0f;
         const float* WT = sWT + (h - 1) * NU * WS;
-#pragma unroll
+VPG_SF_PRAGMA_UNROLL(VPG_SF_ROLL)
         for (int kt = 0; kt < 4; ++kt) {
           uint32_t bh[4][2], bl[4][2];
 #pragma unroll
