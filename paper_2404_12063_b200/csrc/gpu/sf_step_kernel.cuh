@@ -41,7 +41,10 @@
 #define VPG_SF_STR_(x) #x
 #define VPG_SF_PRAGMA_UNROLL(n) _Pragma(VPG_SF_STR_(unroll n))
 #ifndef VPG_SF_SPLIT_ONCE
-#define VPG_SF_SPLIT_ONCE 0
+#define VPG_SF_SPLIT_ONCE 1
+#endif
+#ifndef VPG_SF_CVT_RNA
+#define VPG_SF_CVT_RNA 0
 #endif
 
 namespace vpg {
@@ -63,10 +66,18 @@ __host__ __device__ constexpr size_t smem_bytes(int D, int warps) {
   return sizeof(float) * ((size_t)fixed_floats(D) + (size_t)warps * warp_floats(D)) + 64;
 }
 
+// round to nearest (ties away) onto the tf32 grid: two integer ops instead of
+// cvt.rna.tf32.f32, which sm_100 expands to ~5 instructions with NaN / Inf
+// handling (the operands here are finite; an overflowing |x| near FLT_MAX
+// would round to Inf either way)
 __device__ __forceinline__ uint32_t to_tf32(float x) {
+#if VPG_SF_CVT_RNA
   uint32_t r;
   asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
   return r;
+#else
+  return (__float_as_uint(x) + 0x1000u) & 0xffffe000u;
+#endif
 }
 // x = hi + lo, both rounded to tf32
 __device__ __forceinline__ void split(float x, uint32_t& hi, uint32_t& lo) {
@@ -119,33 +130,92 @@ __device__ __forceinline__ void derivs12(float z, float& s1, float& s2) {
   }
 }
 
-// reduce-scatter of v[8] (index j = 2*nt + e <-> unit 8 nt + 2 t + e) over
-// the eight lanes sharing t: returns the warp sum of index j = g in lane g
-__device__ __forceinline__ float rs8(const float (&v)[8], int g) {
-  const bool b2 = (g & 4) != 0, b1 = (g & 2) != 0, b0 = (g & 1) != 0;
-  float w[4];
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const float send = b2 ? v[i] : v[i + 4];
-    const float keep = b2 ? v[i + 4] : v[i];
-    w[i] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
-  }
-  float x[2];
-#pragma unroll
-  for (int i = 0; i < 2; ++i) {
-    const float send = b1 ? w[i] : w[i + 2];
-    const float keep = b1 ? w[i + 2] : w[i];
-    x[i] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
-  }
-  const float send = b0 ? x[0] : x[1];
-  const float keep = b0 ? x[1] : x[0];
-  return keep + __shfl_xor_sync(0xffffffffu, send, 4);
-}
-
 __device__ __forceinline__ double warp_sum_d(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
   return v;
+}
+
+// warp sums of the per-lane values v0 (unit 8 nt + 2 t) and v1 (unit
+// 8 nt + 2 t + 1) over the eight lanes sharing t, added to the owner lane's
+// accumulator (owner of unit 8 (g >> 1) + 2 t + (g & 1))
+__device__ __forceinline__ void owner_add(float v0, float v1, int nt, int g, float& own) {
+#pragma unroll
+  for (int o = 4; o <= 16; o <<= 1) {
+    v0 += __shfl_xor_sync(0xffffffffu, v0, o);
+    v1 += __shfl_xor_sync(0xffffffffu, v1, o);
+  }
+  if ((g >> 1) == nt) own += (g & 1) ? v1 : v0;
+}
+
+// slot of hidden layer l: hidden 0 keeps z only (TA0 = W0, T2A0 = 0)
+__device__ __forceinline__ float* state_slot(float* slot, int l) {
+  return l == 0 ? slot : slot + TILE_F + (l - 1) * 5 * TILE_F;
+}
+
+// state (z, TAx, TAy, T2Ax, T2Ay) of column tile nt at the lane's four C
+// positions c = 2 r + e (row g + 8 r, unit 8 nt + 2 t + e); first: hidden 0
+__device__ __forceinline__ void load_state_c(const float* S, const float2* sW0, int nt, int g, int t,
+                                             float (&st)[5][4], bool first) {
+#pragma unroll
+  for (int r = 0; r < 2; ++r) {
+    const int o = (g + 8 * r) * RS + 8 * nt + 2 * t;
+    const float2 zz = lds2(S + o);
+    st[0][2 * r] = zz.x;
+    st[0][2 * r + 1] = zz.y;
+    if (first) {
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const float2 w = sW0[8 * nt + 2 * t + e];
+        st[1][2 * r + e] = w.x;
+        st[2][2 * r + e] = w.y;
+        st[3][2 * r + e] = 0.f;
+        st[4][2 * r + e] = 0.f;
+      }
+    } else {
+#pragma unroll
+      for (int s = 1; s < 5; ++s) {
+        const float2 v = lds2(S + s * TILE_F + o);
+        st[s][2 * r] = v.x;
+        st[s][2 * r + 1] = v.y;
+      }
+    }
+  }
+}
+// the same positions read as k-tile kt of a GEMM A operand
+__device__ __forceinline__ void load_state(const float* S, const float2* sW0, int kt, int g, int t,
+                                           float (&st)[5][4], bool first) {
+  load_state_c(S, sW0, kt, g, t, st, first);
+}
+
+// layer outputs (network.hpp:262-276): X = z, TX = s1 TA, T2X = s2 TA^2 + s1 T2A
+template <int ACT>
+__device__ __forceinline__ void x_streams(float z, float tax, float tay, float t2x, float t2y, float& xv,
+                                          float& xtx, float& xty, float& xt2x, float& xt2y) {
+  float s1, s2;
+  derivs12<ACT>(z, s1, s2);
+  xv = z;
+  xtx = s1 * tax;
+  xty = s1 * tay;
+  xt2x = s2 * (tax * tax) + s1 * t2x;
+  xt2y = s2 * (tay * tay) + s1 * t2y;
+}
+
+// through the activation (network.hpp:350-370): adjoints (zb, tzx, tzy,
+// t2zx, t2zy) of the layer outputs -> (Abar, TAxbar, TAybar, T2Axbar, T2Aybar)
+template <int ACT>
+__device__ __forceinline__ void act_reverse(float z, float tax, float tay, float t2x, float t2y, float zb, float tzx,
+                                            float tzy, float t2zx, float t2zy, float (&o)[5]) {
+  float s1, s2, s3;
+  derivs<ACT>(z, s1, s2, s3);
+  float av = s1 * zb;
+  av += s2 * (tax * tzx) + s2 * (tay * tzy);
+  av += s3 * ((tax * tax) * t2zx) + s2 * (t2x * t2zx) + s3 * ((tay * tay) * t2zy) + s2 * (t2y * t2zy);
+  o[0] = av;
+  o[1] = s1 * tzx + 2.0f * (s2 * (tax * t2zx));
+  o[2] = s1 * tzy + 2.0f * (s2 * (tay * t2zy));
+  o[3] = s1 * t2zx;
+  o[4] = s1 * t2zy;
 }
 
 }  // namespace sf
@@ -237,39 +307,21 @@ __global__ void __launch_bounds__(32 * sf::kMaxWarps, 1) sf_step_kernel(const St
     }
 
     // ================= forward, order 2 (network.hpp:204-282) =================
-    // C-layout position (nt, c): row g + 8 (c >> 1), unit 8 nt + 2 t + (c & 1)
-    // layer 0: A = W0 (x, y) + b0, TA = W0 columns, T2A = 0
-    float z0[16];
+    // C-layout position (nt, c): row g + 8 (c >> 1), unit 8 nt + 2 t + (c & 1).
+    // Every hidden layer's state (z, TA, T2A) goes to its slot; the loops
+    // over the 4 column tiles are rolled (instruction-cache footprint).
+    // layer 0: z0 = act(W0 (x, y) + b0) -> slot 0; TA0 = W0 columns, T2A0 = 0
+#pragma unroll 1
+    for (int nt = 0; nt < 4; ++nt) {
+      const int u = 8 * nt + 2 * t;
+      const float2 w0 = sW0[u], w1 = sW0[u + 1];
+      const float b0v = sB[u], b1v = sB[u + 1];
 #pragma unroll
-    for (int nt = 0; nt < 4; ++nt)
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        const int u = 8 * nt + 2 * t + (c & 1);
-        const float2 w = sW0[u];
-        const int r = c >> 1;
-        z0[nt * 4 + c] = Act<ACT>::value(fmaf(w.y, py[r], w.x * px[r]) + sB[u]);
-      }
-    if constexpr (D >= 2) {
-#pragma unroll
-      for (int nt = 0; nt < 4; ++nt) {
-        sts2(slot + g * RS + 8 * nt + 2 * t, z0[nt * 4 + 0], z0[nt * 4 + 1]);
-        sts2(slot + (g + 8) * RS + 8 * nt + 2 * t, z0[nt * 4 + 2], z0[nt * 4 + 3]);
-      }
+      for (int r = 0; r < 2; ++r)
+        sts2(slot + (g + 8 * r) * RS + u, Act<ACT>::value(fmaf(w0.y, py[r], w0.x * px[r]) + b0v),
+             Act<ACT>::value(fmaf(w1.y, py[r], w1.x * px[r]) + b1v));
     }
-
-    // last hidden layer's z / TA / T2A at the lane's 16 positions
-    float hz[16], htx[16], hty[16], ht2x[16], ht2y[16];
-    if constexpr (D == 1) {
-#pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        const int u = 8 * (j >> 2) + 2 * t + (j & 1);
-        hz[j] = z0[j];
-        htx[j] = sW0[u].x;
-        hty[j] = sW0[u].y;
-        ht2x[j] = 0.f;
-        ht2y[j] = 0.f;
-      }
-    } else {
+    if constexpr (D >= 2) {
 #pragma unroll
       for (int l = 1; l < D; ++l) {
         float acc[5][4][4];
@@ -280,39 +332,19 @@ __global__ void __launch_bounds__(32 * sf::kMaxWarps, 1) sf_step_kernel(const St
 #pragma unroll
             for (int c = 0; c < 4; ++c) acc[s][n][c] = 0.0f;
         const float* Wl = sW + (l - 1) * NU * WS;
-        const float* Sprev = slot + TILE_F + (l - 2) * 5 * TILE_F;  // hidden l-1 state (l >= 2)
+        const float* Sprev = state_slot(slot, l - 1);
 VPG_SF_PRAGMA_UNROLL(VPG_SF_ROLL)
         for (int kt = 0; kt < 4; ++kt) {
           // A fragments of the five input streams: positions (g, k0), (g+8, k0),
           // (g, k0+1), (g+8, k0+1) with k0 = 8 kt + 2 t (the permuted K order)
+          float st[5][4];
+          load_state(Sprev, sW0, kt, g, t, st, l == 1);
           float xs[5][4];
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
-            const int r = q & 1, e = q >> 1;
-            const int u = 8 * kt + 2 * t + e;
-            float z, tax, tay, t2x, t2y;
-            if (l == 1) {
-              z = slot[(g + 8 * r) * RS + u];
-              const float2 w = sW0[u];
-              tax = w.x;
-              tay = w.y;
-              t2x = 0.f;
-              t2y = 0.f;
-            } else {
-              const int o = (g + 8 * r) * RS + u;
-              z = Sprev[o];
-              tax = Sprev[TILE_F + o];
-              tay = Sprev[2 * TILE_F + o];
-              t2x = Sprev[3 * TILE_F + o];
-              t2y = Sprev[4 * TILE_F + o];
-            }
-            float s1, s2;
-            derivs12<ACT>(z, s1, s2);
-            xs[0][q] = z;
-            xs[1][q] = s1 * tax;
-            xs[2][q] = s1 * tay;
-            xs[3][q] = s2 * (tax * tax) + s1 * t2x;
-            xs[4][q] = s2 * (tay * tay) + s1 * t2y;
+            const int c = 2 * (q & 1) + (q >> 1);  // fragment slot q <- C position c
+            x_streams<ACT>(st[0][c], st[1][c], st[2][c], st[3][c], st[4][c], xs[0][q], xs[1][q], xs[2][q],
+                           xs[3][q], xs[4][q]);
           }
 #if VPG_SF_SPLIT_ONCE
           uint32_t ah[5][4], al[5][4];
@@ -338,8 +370,8 @@ VPG_SF_PRAGMA_UNROLL(VPG_SF_ROLL)
             }
           }
         }
-        // epilogue: z = act(A + b); state of hidden l
-        float* Sl = slot + TILE_F + (l - 1) * 5 * TILE_F;
+        // epilogue: z = act(A + b); state of hidden l into its slot
+        float* Sl = state_slot(slot, l);
 #pragma unroll
         for (int nt = 0; nt < 4; ++nt)
 #pragma unroll
@@ -347,44 +379,34 @@ VPG_SF_PRAGMA_UNROLL(VPG_SF_ROLL)
             const int u = 8 * nt + 2 * t + (c & 1);
             acc[0][nt][c] = Act<ACT>::value(acc[0][nt][c] + sB[l * NU + u]);
           }
-        if (l < D - 1) {
 #pragma unroll
-          for (int s = 0; s < 5; ++s)
+        for (int s = 0; s < 5; ++s)
 #pragma unroll
-            for (int nt = 0; nt < 4; ++nt) {
-              sts2(Sl + s * TILE_F + g * RS + 8 * nt + 2 * t, acc[s][nt][0], acc[s][nt][1]);
-              sts2(Sl + s * TILE_F + (g + 8) * RS + 8 * nt + 2 * t, acc[s][nt][2], acc[s][nt][3]);
-            }
-        } else {
-#pragma unroll
-          for (int nt = 0; nt < 4; ++nt)
-#pragma unroll
-            for (int c = 0; c < 4; ++c) {
-              hz[nt * 4 + c] = acc[0][nt][c];
-              htx[nt * 4 + c] = acc[1][nt][c];
-              hty[nt * 4 + c] = acc[2][nt][c];
-              ht2x[nt * 4 + c] = acc[3][nt][c];
-              ht2y[nt * 4 + c] = acc[4][nt][c];
-            }
-        }
+          for (int nt = 0; nt < 4; ++nt) {
+            sts2(Sl + s * TILE_F + g * RS + 8 * nt + 2 * t, acc[s][nt][0], acc[s][nt][1]);
+            sts2(Sl + s * TILE_F + (g + 8) * RS + 8 * nt + 2 * t, acc[s][nt][2], acc[s][nt][3]);
+          }
       }
     }
 
     // ---- output layer (linear): u_s = w_out . X_s (+ b_out) ----
+    float* SL = state_slot(slot, D - 1);
     float part[5][2];
 #pragma unroll
     for (int s = 0; s < 5; ++s) part[s][0] = part[s][1] = 0.0f;
+#pragma unroll 1
+    for (int nt = 0; nt < 4; ++nt) {
+      float st[5][4];
+      load_state_c(SL, sW0, nt, g, t, st, D == 1);
 #pragma unroll
-    for (int j = 0; j < 16; ++j) {
-      const int u = 8 * (j >> 2) + 2 * t + (j & 1), r = (j >> 1) & 1;
-      const float wo = sWo[u];
-      float s1, s2;
-      derivs12<ACT>(hz[j], s1, s2);
-      part[0][r] = fmaf(wo, hz[j], part[0][r]);
-      part[1][r] = fmaf(wo, s1 * htx[j], part[1][r]);
-      part[2][r] = fmaf(wo, s1 * hty[j], part[2][r]);
-      part[3][r] = fmaf(wo, s2 * (htx[j] * htx[j]) + s1 * ht2x[j], part[3][r]);
-      part[4][r] = fmaf(wo, s2 * (hty[j] * hty[j]) + s1 * ht2y[j], part[4][r]);
+      for (int c = 0; c < 4; ++c) {
+        const int r = c >> 1;
+        const float wo = sWo[8 * nt + 2 * t + (c & 1)];
+        float x[5];
+        x_streams<ACT>(st[0][c], st[1][c], st[2][c], st[3][c], st[4][c], x[0], x[1], x[2], x[3], x[4]);
+#pragma unroll
+        for (int s = 0; s < 5; ++s) part[s][r] = fmaf(wo, x[s], part[s][r]);
+      }
     }
 #pragma unroll
     for (int s = 0; s < 5; ++s)
@@ -450,62 +472,45 @@ VPG_SF_PRAGMA_UNROLL(VPG_SF_ROLL)
 
     // ================= reverse, order 2 (network.hpp:287-372) =================
     // output layer: w_out gradient, Zbar_{D-1} = w_out (x) Ybar, and Abar of
-    // the last hidden layer straight from registers
-    {
-      float gwo_l[8], gb_l[8];
+    // the last hidden layer (in place of its state)
+#pragma unroll 1
+    for (int nt = 0; nt < 4; ++nt) {
+      float st[5][4];
+      load_state_c(SL, sW0, nt, g, t, st, D == 1);
+      float gw[2] = {0.f, 0.f}, gb[2] = {0.f, 0.f}, gx[2] = {0.f, 0.f}, gy[2] = {0.f, 0.f};
+      float ab[5][4];
 #pragma unroll
-      for (int j = 0; j < 8; ++j) gwo_l[j] = gb_l[j] = 0.0f;
-      float* Sl = slot + TILE_F + (D - 2) * 5 * TILE_F;  // slot of hidden D-1 (D >= 2)
-      float gx_l[8], gy_l[8];
+      for (int c = 0; c < 4; ++c) {
+        const int r = c >> 1, e = c & 1;
+        const float wo = sWo[8 * nt + 2 * t + e];
+        float x[5];
+        x_streams<ACT>(st[0][c], st[1][c], st[2][c], st[3][c], st[4][c], x[0], x[1], x[2], x[3], x[4]);
+        // w_out gradient (Wbar += Abar X^T + TAxbar TXx^T + ..., 326-334)
+        gw[e] += yb[0][r] * x[0] + yb[1][r] * x[1] + yb[2][r] * x[2] + yb[3][r] * x[3] + yb[4][r] * x[4];
+        // Xbar = W^T Abar (340-347), then through the activation (350-370)
+        float o[5];
+        act_reverse<ACT>(st[0][c], st[1][c], st[2][c], st[3][c], st[4][c], wo * yb[0][r], wo * yb[1][r],
+                         wo * yb[2][r], wo * yb[3][r], wo * yb[4][r], o);
 #pragma unroll
-      for (int j = 0; j < 8; ++j) gx_l[j] = gy_l[j] = 0.0f;
-#pragma unroll
-      for (int nt = 0; nt < 4; ++nt) {
-        float ab[5][4];
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          const int j = nt * 4 + c, r = c >> 1, e = c & 1;
-          const int u = 8 * nt + 2 * t + e;
-          const float wo = sWo[u];
-          const float z = hz[j], tax = htx[j], tay = hty[j], t2x = ht2x[j], t2y = ht2y[j];
-          float s1, s2, s3;
-          derivs<ACT>(z, s1, s2, s3);
-          // w_out gradient (Wbar += Abar X^T + TAxbar TXx^T + ... , 326-334)
-          const float xtx = s1 * tax, xty = s1 * tay;
-          const float xt2x = s2 * (tax * tax) + s1 * t2x, xt2y = s2 * (tay * tay) + s1 * t2y;
-          gwo_l[2 * nt + e] += yb[0][r] * z + yb[1][r] * xtx + yb[2][r] * xty + yb[3][r] * xt2x + yb[4][r] * xt2y;
-          // Xbar = W^T Abar (340-347)
-          const float zb = wo * yb[0][r], tzx = wo * yb[1][r], tzy = wo * yb[2][r];
-          const float t2zx = wo * yb[3][r], t2zy = wo * yb[4][r];
-          // through the activation (350-370)
-          float av = s1 * zb;
-          av += s2 * (tax * tzx) + s2 * (tay * tzy);
-          av += s3 * ((tax * tax) * t2zx) + s2 * (t2x * t2zx) + s3 * ((tay * tay) * t2zy) + s2 * (t2y * t2zy);
-          ab[0][c] = av;
-          ab[1][c] = s1 * tzx + 2.0f * (s2 * (tax * t2zx));
-          ab[2][c] = s1 * tzy + 2.0f * (s2 * (tay * t2zy));
-          ab[3][c] = s1 * t2zx;
-          ab[4][c] = s1 * t2zy;
-          gb_l[2 * nt + e] += av;
-          if constexpr (D == 1) {
-            // layer-0 gradient: X0 = (x, y), TX0 = unit vectors, T2X0 = 0
-            gx_l[2 * nt + e] += av * px[r] + ab[1][c];
-            gy_l[2 * nt + e] += av * py[r] + ab[2][c];
-          }
-        }
-        if constexpr (D >= 2) {
-#pragma unroll
-          for (int s = 0; s < 5; ++s) {
-            sts2(Sl + s * TILE_F + g * RS + 8 * nt + 2 * t, ab[s][0], ab[s][1]);
-            sts2(Sl + s * TILE_F + (g + 8) * RS + 8 * nt + 2 * t, ab[s][2], ab[s][3]);
-          }
+        for (int s = 0; s < 5; ++s) ab[s][c] = o[s];
+        gb[e] += o[0];
+        if constexpr (D == 1) {
+          // layer-0 gradient: X0 = (x, y), TX0 = unit vectors, T2X0 = 0
+          gx[e] += o[0] * px[r] + o[1];
+          gy[e] += o[0] * py[r] + o[2];
         }
       }
-      gwo_own += rs8(gwo_l, g);
-      gb_own[D - 1] += rs8(gb_l, g);
+      owner_add(gw[0], gw[1], nt, g, gwo_own);
+      owner_add(gb[0], gb[1], nt, g, gb_own[D - 1]);
       if constexpr (D == 1) {
-        gw0x_own += rs8(gx_l, g);
-        gw0y_own += rs8(gy_l, g);
+        owner_add(gx[0], gx[1], nt, g, gw0x_own);
+        owner_add(gy[0], gy[1], nt, g, gw0y_own);
+      } else {
+#pragma unroll
+        for (int s = 0; s < 5; ++s) {
+          sts2(SL + s * TILE_F + g * RS + 8 * nt + 2 * t, ab[s][0], ab[s][1]);
+          sts2(SL + s * TILE_F + (g + 8) * RS + 8 * nt + 2 * t, ab[s][2], ab[s][3]);
+        }
       }
     }
 
@@ -513,8 +518,8 @@ VPG_SF_PRAGMA_UNROLL(VPG_SF_ROLL)
 #pragma unroll
       for (int h = D - 1; h >= 1; --h) {
         // slot h holds Abar of hidden h; hidden h-1 holds its state
-        const float* Ah = slot + TILE_F + (h - 1) * 5 * TILE_F;
-        float* Sp = slot + (h >= 2 ? TILE_F + (h - 2) * 5 * TILE_F : 0);
+        float* Ah = state_slot(slot, h);
+        float* Sp = state_slot(slot, h - 1);
         __syncwarp();
         // ---- weight gradient of layer h: sum_s Abar_s^T X_s (M = i, N = k, K = points)
 VPG_SF_PRAGMA_UNROLL(VPG_SF_ROLL)
@@ -591,77 +596,49 @@ VPG_SF_PRAGMA_UNROLL(VPG_SF_ROLL)
             for (int nt = 0; nt < 4; ++nt) mma3(zacc[s][nt], ah, al, bh[nt][0], bh[nt][1], bl[nt][0], bl[nt][1]);
           }
         }
-        __syncwarp();  // every lane's transposed reads of hidden h-1's state are done
-        // ---- through the activation of hidden h-1 ----
-        float gb_l[8], gx_l[8], gy_l[8];
+        __syncwarp();  // every lane's reads of slot h and of hidden h-1's state are done
+        // Zbar of hidden h-1 parks in slot h (its Abar is consumed) so the
+        // activation pass below can run as a rolled loop
 #pragma unroll
-        for (int j = 0; j < 8; ++j) gb_l[j] = gx_l[j] = gy_l[j] = 0.0f;
+        for (int s = 0; s < 5; ++s)
 #pragma unroll
-        for (int nt = 0; nt < 4; ++nt) {
-          float zr[4], txr[4], tyr[4], t2xr[4], t2yr[4];
-#pragma unroll
-          for (int r = 0; r < 2; ++r) {
-            const int o = (g + 8 * r) * RS + 8 * nt + 2 * t;
-            const float2 zz = lds2(Sp + o);
-            zr[2 * r] = zz.x;
-            zr[2 * r + 1] = zz.y;
-            if (h >= 2) {
-              const float2 a1 = lds2(Sp + TILE_F + o), a2 = lds2(Sp + 2 * TILE_F + o);
-              const float2 a3 = lds2(Sp + 3 * TILE_F + o), a4 = lds2(Sp + 4 * TILE_F + o);
-              txr[2 * r] = a1.x;
-              txr[2 * r + 1] = a1.y;
-              tyr[2 * r] = a2.x;
-              tyr[2 * r + 1] = a2.y;
-              t2xr[2 * r] = a3.x;
-              t2xr[2 * r + 1] = a3.y;
-              t2yr[2 * r] = a4.x;
-              t2yr[2 * r + 1] = a4.y;
-            } else {
-#pragma unroll
-              for (int e = 0; e < 2; ++e) {
-                const float2 w = sW0[8 * nt + 2 * t + e];
-                txr[2 * r + e] = w.x;
-                tyr[2 * r + e] = w.y;
-                t2xr[2 * r + e] = 0.f;
-                t2yr[2 * r + e] = 0.f;
-              }
-            }
+          for (int nt = 0; nt < 4; ++nt) {
+            sts2(Ah + s * TILE_F + g * RS + 8 * nt + 2 * t, zacc[s][nt][0], zacc[s][nt][1]);
+            sts2(Ah + s * TILE_F + (g + 8) * RS + 8 * nt + 2 * t, zacc[s][nt][2], zacc[s][nt][3]);
           }
+        // ---- through the activation of hidden h-1 ----
+#pragma unroll 1
+        for (int nt = 0; nt < 4; ++nt) {
+          float st[5][4], zb[5][4];
+          load_state_c(Sp, sW0, nt, g, t, st, h == 1);
+          load_state_c(Ah, sW0, nt, g, t, zb, false);
+          float gb[2] = {0.f, 0.f}, gx[2] = {0.f, 0.f}, gy[2] = {0.f, 0.f};
           float out[5][4];
 #pragma unroll
           for (int c = 0; c < 4; ++c) {
-            const float z = zr[c], tax = txr[c], tay = tyr[c], t2x = t2xr[c], t2y = t2yr[c];
-            float s1, s2, s3;
-            derivs<ACT>(z, s1, s2, s3);
-            const float zb = zacc[0][nt][c], tzx = zacc[1][nt][c], tzy = zacc[2][nt][c];
-            const float t2zx = zacc[3][nt][c], t2zy = zacc[4][nt][c];
-            float av = s1 * zb;
-            av += s2 * (tax * tzx) + s2 * (tay * tzy);
-            av += s3 * ((tax * tax) * t2zx) + s2 * (t2x * t2zx) + s3 * ((tay * tay) * t2zy) + s2 * (t2y * t2zy);
-            out[0][c] = av;
-            out[1][c] = s1 * tzx + 2.0f * (s2 * (tax * t2zx));
-            out[2][c] = s1 * tzy + 2.0f * (s2 * (tay * t2zy));
-            out[3][c] = s1 * t2zx;
-            out[4][c] = s1 * t2zy;
+            float o[5];
+            act_reverse<ACT>(st[0][c], st[1][c], st[2][c], st[3][c], st[4][c], zb[0][c], zb[1][c], zb[2][c],
+                             zb[3][c], zb[4][c], o);
+#pragma unroll
+            for (int s = 0; s < 5; ++s) out[s][c] = o[s];
             const int e = c & 1, r = c >> 1;
-            gb_l[2 * nt + e] += av;
+            gb[e] += o[0];
             if (h == 1) {
-              gx_l[2 * nt + e] += av * px[r] + out[1][c];
-              gy_l[2 * nt + e] += av * py[r] + out[2][c];
+              gx[e] += o[0] * px[r] + o[1];
+              gy[e] += o[0] * py[r] + o[2];
             }
           }
-          if (h >= 2) {
+          owner_add(gb[0], gb[1], nt, g, gb_own[h - 1]);
+          if (h == 1) {
+            owner_add(gx[0], gx[1], nt, g, gw0x_own);
+            owner_add(gy[0], gy[1], nt, g, gw0y_own);
+          } else {
 #pragma unroll
             for (int s = 0; s < 5; ++s) {
               sts2(Sp + s * TILE_F + g * RS + 8 * nt + 2 * t, out[s][0], out[s][1]);
               sts2(Sp + s * TILE_F + (g + 8) * RS + 8 * nt + 2 * t, out[s][2], out[s][3]);
             }
           }
-        }
-        gb_own[h - 1] += rs8(gb_l, g);
-        if (h == 1) {
-          gw0x_own += rs8(gx_l, g);
-          gw0y_own += rs8(gy_l, g);
         }
       }
     }

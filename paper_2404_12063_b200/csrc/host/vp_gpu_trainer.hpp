@@ -4,8 +4,9 @@
 // include/vpinn_gpu.h, error metrics on the evaluation grid
 // (trainer.hpp:405-446) through the device forward, and the benchmark step
 // protocol of bench_case / time_epochs (commands.hpp:285-341,
-// trainer.hpp:134-172).  Only kernel "tensor", form "weak" is served:
-// loop/matrix/strong raise InvalidModeError (there is no CPU fallback).
+// trainer.hpp:134-172).  Kernel "tensor" for the weak form and the
+// strong-form collocation baseline are served; kernels loop/matrix raise
+// InvalidModeError (CPU formulations; there is no CPU fallback).
 #pragma once
 
 #include <algorithm>
@@ -57,9 +58,8 @@ inline PdeCoefficients coefficients_from_config(const FullConfig& c) {
 
 inline BuiltProblem build_problem(const FullConfig& cfg, std::optional<Mesh> premade = {},
                                   bool device_assembly = false) {
-  if (cfg.disc.form != LossForm::weak)
-    throw InvalidModeError("the B200 path implements the weak form (Algorithm 3); form 'strong' has no device kernel");
-  if (cfg.disc.kernel != KernelKind::tensor)
+  const bool strong = cfg.disc.form == LossForm::strong;
+  if (!strong && cfg.disc.kernel != KernelKind::tensor)
     throw InvalidModeError("the B200 path implements kernel 'tensor'; 'loop'/'matrix' are CPU formulations");
   BuiltProblem bp;
   bp.mesh = premade ? std::move(*premade) : build_domain_mesh(cfg.problem.domain);
@@ -95,6 +95,14 @@ inline BuiltProblem build_problem(const FullConfig& cfg, std::optional<Mesh> pre
   }
   pa.build_batch();
   if (device_assembly) pa.n_interior = static_cast<long long>(pa.tensors.n_elem) * pa.tensors.n_quad;
+  pa.strong = strong;
+  if (strong && !device_assembly) {
+    // commands.hpp:147-152 — strong_forcing = f at the quadrature points
+    const ScalarField2D f = lookup_field(cfg.problem.forcing);
+    pa.strong_forcing.resize(pa.tensors.quad_points.size());
+    for (size_t i = 0; i < pa.tensors.quad_points.size(); ++i)
+      pa.strong_forcing[i] = static_cast<float>(f(pa.tensors.quad_points[i].x, pa.tensors.quad_points[i].y));
+  }
   bp.weights = cfg.training.weights;
   bp.precision_downgraded = cfg.precision == Precision::f64;
   return bp;
@@ -151,6 +159,8 @@ inline std::unique_ptr<GpuView> make_gpu_view(const BuiltProblem& bp, int device
   p.device = device;
   p.rank = rank;
   p.world_size = world;
+  p.form = pa.strong ? VPINN_FORM_STRONG : VPINN_FORM_WEAK;
+  p.strong_forcing = pa.strong && !bp.device_assembly ? pa.strong_forcing.data() : nullptr;
   if (bp.device_assembly) {
     for (const auto& n : bp.mesh.nodes) {
       v->nodes.push_back(n.x);

@@ -264,6 +264,10 @@ struct ProblemAssembly {
   SampledPoints boundary, sensors;
   std::vector<Point2> batch;  // interior ++ boundary ++ sensors
   long long n_interior = 0, n_boundary = 0, n_sensors = 0;
+  // LossForm::strong (trainer.hpp:178-188): f at the interior points, cast
+  // to float as strong_residual_loss does at use (losses.hpp:450)
+  bool strong = false;
+  std::vector<float> strong_forcing;
   void build_batch() {
     n_interior = static_cast<long long>(tensors.quad_points.size());
     n_boundary = static_cast<long long>(boundary.points.size());

@@ -188,6 +188,8 @@ class HostProblem:
             "points": f64(pb.points, 2 * n_pts).reshape(-1, 2),
             "boundary_values": f64(pb.boundary_values, self.n_bnd),
             "sensor_values": f64(pb.sensor_values, self.n_sen),
+            "form": int(pb.form),
+            "strong_forcing": f32(pb.strong_forcing, self.n_int),
         }
 
     def init_params(self):

@@ -109,6 +109,26 @@ def test_skewed_bench_mesh_and_disk_with_sensors_bit_exact():
     assert_same_problem(hp, ob)
 
 
+def test_strong_form_config_builds_the_collocation_problem():
+    # commands.hpp:147-152: form "strong" -> f at the quadrature points, cast
+    # to float at use (losses.hpp:450); same batch as the weak form
+    c = cfg(problem={"forcing": "sin2pi_f", "boundary_g": "sin2pi_u"},
+            discretization={"form": "strong", "n_test_per_dim": 3, "n_quad_per_dim": 5},
+            network={"layers": [2, 12, 12, 1]})
+    hp = host.HostProblem(c, mesh=host.structured_source(3, 3))
+    a = hp.arrays()
+    assert a["form"] == 1
+    nodes, cells = po.structured_mesh(3, 3)
+    ob = po.OracleProblem(po.ProblemSpec(nodes=nodes, cells=cells, n_test_1d=3, n_quad_1d=5,
+                                         layers=(2, 12, 12, 1), strong=True), double=False)
+    assert np.array_equal(bits(a["points"], np.float64), bits(ob.array("points"), np.float64))
+    assert np.array_equal(bits(a["strong_forcing"], np.float32),
+                          bits(ob.array("strong_forcing").astype(np.float32), np.float32))
+    weak = host.HostProblem(cfg(problem={"forcing": "sin2pi_f", "boundary_g": "sin2pi_u"}),
+                            mesh=host.structured_source(3, 3))
+    assert weak.arrays()["form"] == 0 and weak.arrays()["strong_forcing"] is None
+
+
 def test_reference_configs_build_unchanged(tmp_path):
     # gear_cd2d.json points at data/meshes/gearlike_v41.msh relative to proj/
     (tmp_path / "data" / "meshes").mkdir(parents=True)
@@ -130,7 +150,6 @@ def test_reference_configs_build_unchanged(tmp_path):
     ('{"problem": {"forcing": "nope", "boundary_g": "zero"}}', 2, "problem.forcing: unknown field 'nope'"),
     ('{"problem": {"forcing": "one", "boundary_g": "zero", "pde": {"b": [1, 0]}}}', 2, "poisson mode requires zero convection"),
     ('{"problem": {"forcing": "one", "boundary_g": "zero"}, "discretization": {"kernel": "loop"}}', 2, "kernel 'tensor'"),
-    ('{"problem": {"forcing": "one", "boundary_g": "zero"}, "discretization": {"form": "strong"}}', 2, "weak form"),
     ('{"discretization": {}}', 2, "missing required section 'problem'"),
     ('{"problem": {"forcing": "one", "boundary_g": "zero"}, "training": {"lr_schedule": {"type": "cos"}}}', 2, "lr_schedule.type"),
     ('{not json', 2, "<config>"),
