@@ -56,8 +56,9 @@ constexpr int TILE_F = 16 * RS;   // floats per tile
 constexpr int WS = 40;            // weight row stride
 constexpr int kMaxWarps = 8;
 
-// per-warp slot: hidden 0 keeps z only; hidden 1..D-1 keep five tiles
-__host__ __device__ constexpr int warp_floats(int D) { return TILE_F + (D - 1) * 5 * TILE_F; }
+// per-warp slot: hidden 1..D-1 keep five tiles each (hidden 0 is recomputed;
+// D == 1 keeps one tile for the final gradient reduction)
+__host__ __device__ constexpr int warp_floats(int D) { return D == 1 ? TILE_F : (D - 1) * 5 * TILE_F; }
 // CTA-wide: W_l and W_l^T (l = 1..D-1), W0 as float2 rows, biases, w_out
 __host__ __device__ constexpr int fixed_floats(int D) {
   return (D - 1) * 2 * NU * WS + 2 * NU + D * NU + NU + 4;
@@ -148,44 +149,40 @@ __device__ __forceinline__ void owner_add(float v0, float v1, int nt, int g, flo
   if ((g >> 1) == nt) own += (g & 1) ? v1 : v0;
 }
 
-// slot of hidden layer l: hidden 0 keeps z only (TA0 = W0, T2A0 = 0)
-__device__ __forceinline__ float* state_slot(float* slot, int l) {
-  return l == 0 ? slot : slot + TILE_F + (l - 1) * 5 * TILE_F;
-}
+// slot of hidden layer l >= 1 (hidden 0 is not stored: z0 is recomputed
+// from the point, TA0 = W0 columns, T2A0 = 0)
+__device__ __forceinline__ float* state_slot(float* slot, int l) { return slot + (l - 1) * 5 * TILE_F; }
 
 // state (z, TAx, TAy, T2Ax, T2Ay) of column tile nt at the lane's four C
-// positions c = 2 r + e (row g + 8 r, unit 8 nt + 2 t + e); first: hidden 0
-__device__ __forceinline__ void load_state_c(const float* S, const float2* sW0, int nt, int g, int t,
-                                             float (&st)[5][4], bool first) {
+// positions c = 2 r + e (row g + 8 r, unit 8 nt + 2 t + e); first: hidden 0,
+// recomputed from the lane's points (px, py) and W0, b0
+template <int ACT>
+__device__ __forceinline__ void load_state_c(const float* S, const float2* sW0, const float* sB0, int nt, int g,
+                                             int t, float (&st)[5][4], bool first, const float (&px)[2],
+                                             const float (&py)[2]) {
 #pragma unroll
   for (int r = 0; r < 2; ++r) {
-    const int o = (g + 8 * r) * RS + 8 * nt + 2 * t;
-    const float2 zz = lds2(S + o);
-    st[0][2 * r] = zz.x;
-    st[0][2 * r + 1] = zz.y;
     if (first) {
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
-        const float2 w = sW0[8 * nt + 2 * t + e];
+        const int u = 8 * nt + 2 * t + e;
+        const float2 w = sW0[u];
+        st[0][2 * r + e] = Act<ACT>::value(fmaf(w.y, py[r], w.x * px[r]) + sB0[u]);
         st[1][2 * r + e] = w.x;
         st[2][2 * r + e] = w.y;
         st[3][2 * r + e] = 0.f;
         st[4][2 * r + e] = 0.f;
       }
     } else {
+      const int o = (g + 8 * r) * RS + 8 * nt + 2 * t;
 #pragma unroll
-      for (int s = 1; s < 5; ++s) {
+      for (int s = 0; s < 5; ++s) {
         const float2 v = lds2(S + s * TILE_F + o);
         st[s][2 * r] = v.x;
         st[s][2 * r + 1] = v.y;
       }
     }
   }
-}
-// the same positions read as k-tile kt of a GEMM A operand
-__device__ __forceinline__ void load_state(const float* S, const float2* sW0, int kt, int g, int t,
-                                           float (&st)[5][4], bool first) {
-  load_state_c(S, sW0, kt, g, t, st, first);
 }
 
 // layer outputs (network.hpp:262-276): X = z, TX = s1 TA, T2X = s2 TA^2 + s1 T2A
@@ -310,17 +307,7 @@ __global__ void __launch_bounds__(32 * sf::kMaxWarps, 1) sf_step_kernel(const St
     // C-layout position (nt, c): row g + 8 (c >> 1), unit 8 nt + 2 t + (c & 1).
     // Every hidden layer's state (z, TA, T2A) goes to its slot; the loops
     // over the 4 column tiles are rolled (instruction-cache footprint).
-    // layer 0: z0 = act(W0 (x, y) + b0) -> slot 0; TA0 = W0 columns, T2A0 = 0
-#pragma unroll 1
-    for (int nt = 0; nt < 4; ++nt) {
-      const int u = 8 * nt + 2 * t;
-      const float2 w0 = sW0[u], w1 = sW0[u + 1];
-      const float b0v = sB[u], b1v = sB[u + 1];
-#pragma unroll
-      for (int r = 0; r < 2; ++r)
-        sts2(slot + (g + 8 * r) * RS + u, Act<ACT>::value(fmaf(w0.y, py[r], w0.x * px[r]) + b0v),
-             Act<ACT>::value(fmaf(w1.y, py[r], w1.x * px[r]) + b1v));
-    }
+    // hidden 0 is recomputed where needed (z0 = act(W0 (x, y) + b0))
     if constexpr (D >= 2) {
 #pragma unroll
       for (int l = 1; l < D; ++l) {
@@ -338,7 +325,7 @@ VPG_SF_PRAGMA_UNROLL(VPG_SF_ROLL)
           // A fragments of the five input streams: positions (g, k0), (g+8, k0),
           // (g, k0+1), (g+8, k0+1) with k0 = 8 kt + 2 t (the permuted K order)
           float st[5][4];
-          load_state(Sprev, sW0, kt, g, t, st, l == 1);
+          load_state_c<ACT>(Sprev, sW0, sB, kt, g, t, st, l == 1, px, py);
           float xs[5][4];
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
@@ -397,7 +384,7 @@ VPG_SF_PRAGMA_UNROLL(VPG_SF_ROLL)
 #pragma unroll 1
     for (int nt = 0; nt < 4; ++nt) {
       float st[5][4];
-      load_state_c(SL, sW0, nt, g, t, st, D == 1);
+      load_state_c<ACT>(SL, sW0, sB, nt, g, t, st, D == 1, px, py);
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
         const int r = c >> 1;
@@ -476,7 +463,7 @@ VPG_SF_PRAGMA_UNROLL(VPG_SF_ROLL)
 #pragma unroll 1
     for (int nt = 0; nt < 4; ++nt) {
       float st[5][4];
-      load_state_c(SL, sW0, nt, g, t, st, D == 1);
+      load_state_c<ACT>(SL, sW0, sB, nt, g, t, st, D == 1, px, py);
       float gw[2] = {0.f, 0.f}, gb[2] = {0.f, 0.f}, gx[2] = {0.f, 0.f}, gy[2] = {0.f, 0.f};
       float ab[5][4];
 #pragma unroll
@@ -525,6 +512,23 @@ VPG_SF_PRAGMA_UNROLL(VPG_SF_ROLL)
 VPG_SF_PRAGMA_UNROLL(VPG_SF_ROLL)
         for (int kt = 0; kt < 2; ++kt) {
           const int pa = 8 * kt + t, pb = pa + 4;
+          // h == 1: hidden 0 at (points pa / pb, units 8 nt + g), recomputed
+          float z0t[4][2];
+          if (h == 1) {
+            float2 q[2];
+#pragma unroll
+            for (int i = 0; i < 2; ++i) {
+              const int pp = p0 + (i ? pb : pa);
+              q[i] = pp < n_pts ? pts[pp] : make_float2(0.f, 0.f);
+            }
+#pragma unroll
+            for (int nt = 0; nt < 4; ++nt) {
+              const int k = 8 * nt + g;
+              const float2 w = sW0[k];
+#pragma unroll
+              for (int i = 0; i < 2; ++i) z0t[nt][i] = Act<ACT>::value(fmaf(w.y, q[i].y, w.x * q[i].x) + sB[k]);
+            }
+          }
 VPG_SF_PRAGMA_UNROLL(VPG_SF_ROLL)
           for (int s = 0; s < 5; ++s) {
             const float* As = Ah + s * TILE_F;
@@ -542,7 +546,7 @@ VPG_SF_PRAGMA_UNROLL(VPG_SF_ROLL)
 #pragma unroll
               for (int q = 0; q < 2; ++q) {
                 const int o = (q ? pb : pa) * RS + k;
-                const float z = Sp[o];
+                const float z = h == 1 ? z0t[nt][q] : Sp[o];
                 if (s == 0) {
                   xb[q] = z;
                 } else {
@@ -610,8 +614,8 @@ VPG_SF_PRAGMA_UNROLL(VPG_SF_ROLL)
 #pragma unroll 1
         for (int nt = 0; nt < 4; ++nt) {
           float st[5][4], zb[5][4];
-          load_state_c(Sp, sW0, nt, g, t, st, h == 1);
-          load_state_c(Ah, sW0, nt, g, t, zb, false);
+          load_state_c<ACT>(Sp, sW0, sB, nt, g, t, st, h == 1, px, py);
+          load_state_c<ACT>(Ah, sW0, sB, nt, g, t, zb, false, px, py);
           float gb[2] = {0.f, 0.f}, gx[2] = {0.f, 0.f}, gy[2] = {0.f, 0.f};
           float out[5][4];
 #pragma unroll
