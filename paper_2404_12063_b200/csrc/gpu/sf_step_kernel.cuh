@@ -40,9 +40,6 @@
 #endif
 #define VPG_SF_STR_(x) #x
 #define VPG_SF_PRAGMA_UNROLL(n) _Pragma(VPG_SF_STR_(unroll n))
-#ifndef VPG_SF_SPLIT_ONCE
-#define VPG_SF_SPLIT_ONCE 1
-#endif
 #ifndef VPG_SF_CVT_RNA
 #define VPG_SF_CVT_RNA 0
 #endif
@@ -333,29 +330,30 @@ VPG_SF_PRAGMA_UNROLL(VPG_SF_ROLL)
             x_streams<ACT>(st[0][c], st[1][c], st[2][c], st[3][c], st[4][c], xs[0][q], xs[1][q], xs[2][q],
                            xs[3][q], xs[4][q]);
           }
-#if VPG_SF_SPLIT_ONCE
           uint32_t ah[5][4], al[5][4];
 #pragma unroll
           for (int s = 0; s < 5; ++s) split4(xs[s], ah[s], al[s]);
-#endif
+          uint32_t bh[4][2], bl[4][2];
 #pragma unroll
           for (int nt = 0; nt < 4; ++nt) {
             const float2 w = lds2(Wl + (8 * nt + g) * WS + 8 * kt + 2 * t);
-            uint32_t bh0, bl0, bh1, bl1;
-            split(w.x, bh0, bl0);
-            split(w.y, bh1, bl1);
-#pragma unroll
-            for (int s = 0; s < 5; ++s) {
-#if VPG_SF_SPLIT_ONCE
-              mma3(acc[s][nt], ah[s], al[s], bh0, bh1, bl0, bl1);
-#else
-              // splitting per use keeps 8 instead of 40 fragment registers live
-              uint32_t ah[4], al[4];
-              split4(xs[s], ah, al);
-              mma3(acc[s][nt], ah, al, bh0, bh1, bl0, bl1);
-#endif
-            }
+            split(w.x, bh[nt][0], bl[nt][0]);
+            split(w.y, bh[nt][1], bl[nt][1]);
           }
+          // the three split passes interleaved over the 20 independent
+          // accumulators (no back-to-back dependent HMMAs)
+#pragma unroll
+          for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+            for (int s = 0; s < 5; ++s) mma_tf32(acc[s][nt], al[s], bh[nt][0], bh[nt][1]);
+#pragma unroll
+          for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+            for (int s = 0; s < 5; ++s) mma_tf32(acc[s][nt], ah[s], bl[nt][0], bl[nt][1]);
+#pragma unroll
+          for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+            for (int s = 0; s < 5; ++s) mma_tf32(acc[s][nt], ah[s], bh[nt][0], bh[nt][1]);
         }
         // epilogue: z = act(A + b); state of hidden l into its slot
         float* Sl = state_slot(slot, l);
@@ -539,16 +537,17 @@ VPG_SF_PRAGMA_UNROLL(VPG_SF_ROLL)
                                   As[pb * RS + 16 * mt + g + 8]};
               split4(v, ah[mt], al[mt]);
             }
+            uint32_t bh[4][2], bl[4][2];
 #pragma unroll
             for (int nt = 0; nt < 4; ++nt) {
               const int k = 8 * nt + g;
-              float xb[2];
 #pragma unroll
               for (int q = 0; q < 2; ++q) {
                 const int o = (q ? pb : pa) * RS + k;
                 const float z = h == 1 ? z0t[nt][q] : Sp[o];
+                float xb;
                 if (s == 0) {
-                  xb[q] = z;
+                  xb = z;
                 } else {
                   float s1, s2;
                   derivs12<ACT>(z, s1, s2);
@@ -559,15 +558,23 @@ VPG_SF_PRAGMA_UNROLL(VPG_SF_ROLL)
                     ta = Sp[((s == 1 || s == 3) ? 1 : 2) * TILE_F + o];
                     if (s >= 3) t2a = Sp[s * TILE_F + o];
                   }
-                  xb[q] = s <= 2 ? s1 * ta : s2 * (ta * ta) + s1 * t2a;
+                  xb = s <= 2 ? s1 * ta : s2 * (ta * ta) + s1 * t2a;
                 }
+                split(xb, bh[nt][q], bl[nt][q]);
               }
-              uint32_t bh0, bl0, bh1, bl1;
-              split(xb[0], bh0, bl0);
-              split(xb[1], bh1, bl1);
-#pragma unroll
-              for (int mt = 0; mt < 2; ++mt) mma3(gacc[h - 1][mt][nt], ah[mt], al[mt], bh0, bh1, bl0, bl1);
             }
+#pragma unroll
+            for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+              for (int mt = 0; mt < 2; ++mt) mma_tf32(gacc[h - 1][mt][nt], al[mt], bh[nt][0], bh[nt][1]);
+#pragma unroll
+            for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+              for (int mt = 0; mt < 2; ++mt) mma_tf32(gacc[h - 1][mt][nt], ah[mt], bl[nt][0], bl[nt][1]);
+#pragma unroll
+            for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+              for (int mt = 0; mt < 2; ++mt) mma_tf32(gacc[h - 1][mt][nt], ah[mt], bh[nt][0], bh[nt][1]);
           }
         }
         // ---- propagation: Zbar_s = Abar_s W_h (M = points, N = k, K = i permuted)
@@ -588,17 +595,27 @@ VPG_SF_PRAGMA_UNROLL(VPG_SF_ROLL)
             split(w.x, bh[nt][0], bl[nt][0]);
             split(w.y, bh[nt][1], bl[nt][1]);
           }
+          uint32_t ah[5][4], al[5][4];
 #pragma unroll
           for (int s = 0; s < 5; ++s) {
             const float* As = Ah + s * TILE_F;
             const float2 r0 = lds2(As + g * RS + 8 * kt + 2 * t);
             const float2 r1 = lds2(As + (g + 8) * RS + 8 * kt + 2 * t);
             const float v[4] = {r0.x, r1.x, r0.y, r1.y};
-            uint32_t ah[4], al[4];
-            split4(v, ah, al);
-#pragma unroll
-            for (int nt = 0; nt < 4; ++nt) mma3(zacc[s][nt], ah, al, bh[nt][0], bh[nt][1], bl[nt][0], bl[nt][1]);
+            split4(v, ah[s], al[s]);
           }
+#pragma unroll
+          for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+            for (int s = 0; s < 5; ++s) mma_tf32(zacc[s][nt], al[s], bh[nt][0], bh[nt][1]);
+#pragma unroll
+          for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+            for (int s = 0; s < 5; ++s) mma_tf32(zacc[s][nt], ah[s], bl[nt][0], bl[nt][1]);
+#pragma unroll
+          for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+            for (int s = 0; s < 5; ++s) mma_tf32(zacc[s][nt], ah[s], bh[nt][0], bh[nt][1]);
         }
         __syncwarp();  // every lane's reads of slot h and of hidden h-1's state are done
         // Zbar of hidden h-1 parks in slot h (its Abar is consumed) so the
