@@ -40,6 +40,12 @@
 #endif
 #define VPG_SF_STR_(x) #x
 #define VPG_SF_PRAGMA_UNROLL(n) _Pragma(VPG_SF_STR_(unroll n))
+#ifndef VPG_SF_LO_RN
+#define VPG_SF_LO_RN 0
+#endif
+#ifndef VPG_SF_HI_TRUNC
+#define VPG_SF_HI_TRUNC 0
+#endif
 #ifndef VPG_SF_CVT_RNA
 #define VPG_SF_CVT_RNA 0
 #endif
@@ -79,8 +85,18 @@ __device__ __forceinline__ uint32_t to_tf32(float x) {
 }
 // x = hi + lo, both rounded to tf32
 __device__ __forceinline__ void split(float x, uint32_t& hi, uint32_t& lo) {
+#if VPG_SF_HI_TRUNC
+  hi = __float_as_uint(x) & 0xffffe000u;
+#else
   hi = to_tf32(x);
+#endif
+#if VPG_SF_LO_RN
   lo = to_tf32(x - __uint_as_float(hi));
+#else
+  // the MMA reads only the top 19 bits of lo (truncation): |lo| <= 2^-11 |x|,
+  // so the dropped bits are below 2^-21 |x|
+  lo = __float_as_uint(x - __uint_as_float(hi));
+#endif
 }
 __device__ __forceinline__ void mma_tf32(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
   asm("mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
