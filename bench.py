@@ -289,6 +289,7 @@ def main():
     e2e = _e2e(hp, device, rank, world, pg, args.steps)
     e2e_mesh = _e2e_from_mesh(mesh, device, rank, world, pg, args.steps)
     mf = _matrix_free(mesh, device, rank, world) if rank == 0 else None
+    strong = _strong_form(mesh, device, rank, world, pg, args.steps, med_epoch_ms)
 
     # ---- CPU baseline (rank 0, N=1 only) ----
     cpu = None
@@ -330,6 +331,7 @@ def main():
         "e2e": e2e,
         "e2e_from_mesh": e2e_mesh,
         "contraction_matrix_free": mf,
+        "strong_form": strong,
         "cpu_baseline": cpu,
     }
     if sweep:
@@ -465,6 +467,59 @@ def _matrix_free(mesh, device, rank, world):
     return {"kernel": "contract_mf_kernel", "ms_per_launch": ms, "bytes_per_launch": nbytes,
             "achieved_GBs": nbytes / (ms * 1e-3) / 1e9,
             "note": "HBM bytes 14x below the premultiplier stream; shared-memory-load bound on CUDA cores"}
+
+
+# mma.sync m16n8k8 TF32 issue rate measured on this pool's B200
+# (tools/micro/mma_sync_rate.cu, profiles/r01_mma_sync_rate.txt)
+MMA_SYNC_TF32_TFLOPS = 277.0
+
+
+def _strong_form(mesh, device, rank, world, pg, steps, weak_ms):
+    """the strong-form collocation baseline (the paper's
+    PINN comparison) on the same gear workload: order-2 network at the
+    354,800 interior quadrature points + the boundary penalty, one
+    warp-tiled mma.sync kernel + the same reduce/Adam.  Device-timed epochs,
+    L2 flushed between them, max over ranks."""
+    import copy
+    from paper_2404_12063_b200 import gpu as G, host
+    cfg = copy.deepcopy(GEAR_CFG)
+    cfg["discretization"]["form"] = "strong"
+    hp = host.HostProblem(cfg, mesh=mesh)
+    g = G.GpuStep.from_problem(hp.view(device, rank, world), keepalive=hp)
+    g.set_params(hp.init_params())
+    if world > 1:
+        uid = bcast_bytes(pg, G.nccl_unique_id() if rank == 0 else b"", rank)
+        g.attach_comm(uid, world, rank)
+    g.adam_reset()
+    g.run_steps(5, 1e-3)
+    g.synchronize()
+    barrier(pg)
+    times = []
+    for _ in range(max(5, min(steps, 30))):
+        g.flush_l2()
+        times.append(g.time_steps(1, 1e-3))
+    ms = allmax(pg, float(np.median(times)))
+    ms_k, ms_r, ms_a = g.profile_step(10)
+    kernel = g.step_kernel()
+    g.close()
+    n_pts = (hp.n_int + hp.n_bnd + hp.n_sen) // max(1, world)
+    tiles = -(-n_pts // 16)
+    # executed: 1,440 m16n8k8 MMAs (3-pass TF32 split, widths padded to 32) per
+    # 16-point tile; algorithmic: ~55,050 flop per point for [2,30,30,30,1]
+    # (5 streams x (2 forward + 2 propagation + 2 weight-gradient) 30x30
+    # products = 54,000 + the input / output layers)
+    exec_tflops = tiles * 1440 * 2 * 16 * 8 * 8 / (ms_k * 1e-3) / 1e12
+    alg_tflops = n_pts * 55050.0 / (ms_k * 1e-3) / 1e12
+    return {"workload": "C5 gear, form=strong: PINN collocation residual at the interior quadrature points "
+                        "+ boundary penalty, same network / points / Adam",
+            "kernel": kernel, "ms_per_epoch": ms, "points_per_s": (hp.n_int + hp.n_bnd + hp.n_sen) / (ms * 1e-3),
+            "strong_over_weak_epoch_time": ms / weak_ms if weak_ms else None,
+            "kernel_ms": {"step": ms_k, "reduce": ms_r, "adam": ms_a},
+            "roofline": {"bound": "tensor", "pipe": "mma.sync TF32 (legacy HMMA)", "achieved": exec_tflops,
+                         "peak": MMA_SYNC_TF32_TFLOPS, "unit": "TFLOP/s", "frac": exec_tflops / MMA_SYNC_TF32_TFLOPS,
+                         "algorithmic_tflops": alg_tflops,
+                         "peak_source": "tools/micro/mma_sync_rate.cu on this pool's B200"},
+            "l2": "flushed between timed epochs"}
 
 
 def _sweep(device):

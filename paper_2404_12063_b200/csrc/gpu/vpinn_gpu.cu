@@ -1745,7 +1745,6 @@ int64_t vpinn_gpu_launch_count(const vpinn_gpu_ctx* c) { return c ? c->launches 
 int vpinn_gpu_profile_step(vpinn_gpu_ctx* c, int reps, double* ms_mlp, double* ms_reduce,
                            double* ms_adam) {
   return guarded([&] {
-    weak_only(c, "vpinn_gpu_profile_step");
     set_dev(c);
     reset_state(c, LLONG_MAX, nullptr);
     const vpg::AdamArgs aa = adam_args(c, false, 1e-4f, false, 0);

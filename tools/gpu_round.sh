@@ -1,8 +1,8 @@
 #!/bin/bash
 # One gpurun call's worth of round evidence: GPU parity tests, smoke, the
 # default bench line, the ncu launch list of the bench command and one
-# `ncu --set full` capture each of the fused step kernel and the standalone
-# contraction.  Everything lands in gpurun_out/ (read back here with
+# `ncu --set full` capture each of the fused step kernel, the standalone
+# contraction and the strong-form kernel.  Everything lands in gpurun_out/ (read back here with
 # tools/make_profiles.py).  usage: bash tools/gpu_round.sh [TAG]
 TAG=${1:-r01}
 O=gpurun_out
@@ -18,4 +18,6 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:'tc2
   -o $O/${TAG}_step -f python tools/profile_step.py 4 > $O/${TAG}_ncu_step.log 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:contract -c 1 \
   -o $O/${TAG}_contract -f python tools/profile_step.py 1 > $O/${TAG}_ncu_contract.log 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:sf_step -c 1 \
+  -o $O/${TAG}_strong -f python tools/quick_strong.py > $O/${TAG}_ncu_strong.log 2>&1
 ls -la $O
