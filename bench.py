@@ -289,7 +289,7 @@ def main():
     e2e = _e2e(hp, device, rank, world, pg, args.steps)
     e2e_mesh = _e2e_from_mesh(mesh, device, rank, world, pg, args.steps)
     mf = _matrix_free(mesh, device, rank, world) if rank == 0 else None
-    strong = _strong_form(mesh, device, rank, world, pg, args.steps, med_epoch_ms)
+    strong = _strong_form(mesh, device, rank, world, pg, args.steps, ms_per_step)
 
     # ---- CPU baseline (rank 0, N=1 only) ----
     cpu = None
