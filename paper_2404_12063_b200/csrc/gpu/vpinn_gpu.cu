@@ -3,6 +3,9 @@
 #include <dlfcn.h>
 
 #include <algorithm>
+#include <condition_variable>
+#include <thread>
+#include <chrono>
 #include <climits>
 #include <cmath>
 #include <cstdio>
@@ -108,6 +111,148 @@ BlockCache& block_cache() {
   return *c;
 }
 
+
+// ---------------------------------------------------------------------------
+// Host -> device uploads of large pageable arrays (the premultiplier tensors
+// at vpinn_gpu_create): pageable cudaMemcpy runs at ~8 GB/s on the B200
+// boxes; staging through a pinned ring filled by a small host thread pool
+// overlaps the host copy of chunk i+1 with the DMA of chunk i at pinned
+// bandwidth.  Process-wide, never destroyed (no exit-order races).
+struct CopyPool {
+  int n = 1;
+  std::vector<std::thread> workers;
+  std::mutex mu;
+  std::condition_variable cv, cv_done;
+  char* dst = nullptr;
+  const char* src = nullptr;
+  size_t len = 0;
+  unsigned gen = 0;
+  int pending = 0;
+  CopyPool() {
+    const unsigned hc = std::thread::hardware_concurrency();
+    n = std::max(1, std::min(8, (int)(hc ? hc / 2 : 1)));
+    if (const char* e = std::getenv("VPINN_COPY_THREADS")) n = std::max(1, std::min(32, std::atoi(e)));
+    for (int i = 1; i < n; ++i) workers.emplace_back([this, i] { loop(i); });
+    for (auto& w : workers) w.detach();
+  }
+  void slice(int i, char*& d, const char*& s, size_t& l) const {
+    const size_t per = (len / n + 63) & ~size_t(63);
+    const size_t a = std::min(len, per * i), b = std::min(len, per * (i + 1));
+    d = dst + a;
+    s = src + a;
+    l = b - a;
+  }
+  void loop(int i) {
+    unsigned seen = 0;
+    for (;;) {
+      std::unique_lock<std::mutex> lk(mu);
+      cv.wait(lk, [&] { return gen != seen; });
+      seen = gen;
+      char* d;
+      const char* s;
+      size_t l;
+      slice(i, d, s, l);
+      lk.unlock();
+      if (l) std::memcpy(d, s, l);
+      lk.lock();
+      if (--pending == 0) cv_done.notify_one();
+    }
+  }
+  void copy(void* d, const void* s, size_t l) {
+    if (n == 1 || l < (size_t(1) << 20)) {
+      std::memcpy(d, s, l);
+      return;
+    }
+    {
+      std::lock_guard<std::mutex> g(mu);
+      dst = static_cast<char*>(d);
+      src = static_cast<const char*>(s);
+      len = l;
+      pending = n - 1;
+      ++gen;
+    }
+    cv.notify_all();
+    char* d0;
+    const char* s0;
+    size_t l0;
+    slice(0, d0, s0, l0);
+    if (l0) std::memcpy(d0, s0, l0);
+    std::unique_lock<std::mutex> lk(mu);
+    cv_done.wait(lk, [&] { return pending == 0; });
+  }
+};
+
+struct Stager {
+  static constexpr size_t kChunk = size_t(8) << 20;
+  static constexpr int kBufs = 3;
+  std::mutex mu;
+  char* buf[kBufs] = {};
+  cudaEvent_t ev[16][kBufs] = {};  // per device
+  bool pending[16][kBufs] = {};
+  CopyPool pool;
+  // false: caller falls back to a plain pageable copy
+  bool upload(void* dst, const void* src, size_t bytes, cudaStream_t s) {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 16) return false;
+    std::lock_guard<std::mutex> g(mu);
+    for (int k = 0; k < kBufs; ++k) {
+      if (!buf[k] && cudaHostAlloc(&buf[k], kChunk, cudaHostAllocPortable) != cudaSuccess) {
+        cudaGetLastError();
+        buf[k] = nullptr;
+        return false;
+      }
+      if (!ev[dev][k]) CK(cudaEventCreateWithFlags(&ev[dev][k], cudaEventDisableTiming));
+    }
+    const char* sp = static_cast<const char*>(src);
+    char* dp = static_cast<char*>(dst);
+    int k = 0;
+    for (size_t off = 0; off < bytes; off += kChunk, k = (k + 1) % kBufs) {
+      const size_t l = std::min(kChunk, bytes - off);
+      if (pending[dev][k]) CK(cudaEventSynchronize(ev[dev][k]));
+      pool.copy(buf[k], sp + off, l);
+      CK(cudaMemcpyAsync(dp + off, buf[k], l, cudaMemcpyHostToDevice, s));
+      CK(cudaEventRecord(ev[dev][k], s));
+      pending[dev][k] = true;
+    }
+    return true;
+  }
+};
+Stager& stager() {
+  static Stager* st = new Stager;
+  return *st;
+}
+void upload_bytes(void* dst, const void* src, size_t bytes, cudaStream_t s) {
+  if (bytes >= (size_t(4) << 20) && !std::getenv("VPINN_NO_STAGING") && stager().upload(dst, src, bytes, s)) return;
+  CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s));
+}
+
+// small pinned host words (per-context trainer flags) from one pinned slab:
+// cudaMallocHost per context costs ~1 ms
+struct PinnedWords {
+  std::mutex mu;
+  int* slab = nullptr;
+  std::vector<int*> free_slots;
+  int* get() {
+    std::lock_guard<std::mutex> g(mu);
+    if (free_slots.empty()) {
+      constexpr int kSlots = 1024;
+      if (cudaMallocHost(&slab, sizeof(int) * 4 * kSlots) != cudaSuccess) return nullptr;
+      for (int i = kSlots - 1; i >= 0; --i) free_slots.push_back(slab + 4 * i);
+    }
+    int* p = free_slots.back();
+    free_slots.pop_back();
+    return p;
+  }
+  void put(int* p) {
+    std::lock_guard<std::mutex> g(mu);
+    free_slots.push_back(p);
+  }
+};
+PinnedWords& pinned_words() {
+  static PinnedWords* w = new PinnedWords;
+  return *w;
+}
+
 template <typename T>
 struct DBuf {
   T* p = nullptr;
@@ -133,11 +278,12 @@ struct DBuf {
     if (!p) CK(cudaMalloc(&p, bytes));
     CK(cudaMemsetAsync(p, 0, bytes, s));
   }
+  // the host array may be freed as soon as this returns
   void upload(const T* h, size_t count, cudaStream_t s) {
-    if (count) CK(cudaMemcpyAsync(p, h, count * sizeof(T), cudaMemcpyHostToDevice, s));
+    if (count) upload_bytes(p, h, count * sizeof(T), s);
   }
   void upload_at(size_t at, const T* h, size_t count, cudaStream_t s) {
-    if (count) CK(cudaMemcpyAsync(p + at, h, count * sizeof(T), cudaMemcpyHostToDevice, s));
+    if (count) upload_bytes(p + at, h, count * sizeof(T), s);
   }
 };
 
@@ -338,7 +484,7 @@ struct vpinn_gpu_ctx {
     if (stream) cudaStreamSynchronize(stream);  // buffers go back to the block cache idle
     for (auto& kv : graphs) cudaGraphExecDestroy(kv.second);
     if (comm && nccl().comm_destroy) nccl().comm_destroy(comm);
-    if (h_flag) cudaFreeHost(h_flag);
+    if (h_flag) pinned_words().put(h_flag);
     if (stream) cudaStreamDestroy(stream);
   }
 };
@@ -1054,16 +1200,33 @@ int vpinn_gpu_create(const vpinn_gpu_problem* pb, vpinn_gpu_ctx** out) {
     }
     if (pb->device < 0 || pb->device >= ndev) throw Fail{VPINN_ERR_DEVICE, "device ordinal out of range"};
 
+    // VPINN_CREATE_TIMING=1: phase wall times of this call on stderr
+    const bool timing = std::getenv("VPINN_CREATE_TIMING") != nullptr;
+    auto tnow = [] { return std::chrono::steady_clock::now(); };
+    auto t_start = tnow();
+    auto mark = [&](const char* what, cudaStream_t st) {
+      if (!timing) return;
+      if (st) cudaStreamSynchronize(st);
+      const auto t = tnow();
+      std::fprintf(stderr, "create: %-22s %8.3f ms\n", what, std::chrono::duration<double, std::milli>(t - t_start).count());
+      t_start = t;
+    };
     auto c = std::make_unique<vpinn_gpu_ctx>();
     c->device = pb->device;
     set_dev(c.get());
-    cudaDeviceProp prop;
-    CK(cudaGetDeviceProperties(&prop, c->device));
-    if (prop.major != 10)
+    // attribute queries, not cudaGetDeviceProperties (~2 ms per call)
+    int cc_major = 0;
+    CK(cudaDeviceGetAttribute(&cc_major, cudaDevAttrComputeCapabilityMajor, c->device));
+    if (cc_major != 10) {
+      cudaDeviceProp prop;
+      CK(cudaGetDeviceProperties(&prop, c->device));
       throw Fail{VPINN_ERR_DEVICE, std::string("device ") + prop.name + " is not sm_100 (B200)"};
-    c->sm_count = prop.multiProcessorCount;
+    }
+    CK(cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, c->device));
     CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
-    CK(cudaMallocHost(&c->h_flag, sizeof(int) * 4));
+    mark("device + stream", c->stream);
+    c->h_flag = pinned_words().get();
+    if (!c->h_flag) throw Fail{VPINN_ERR_DEVICE, "pinned host allocation failed"};
     if (var) c->var = *var;
     c->strong = strong;
     if (strong) {
@@ -1205,7 +1368,9 @@ int vpinn_gpu_create(const vpinn_gpu_problem* pb, vpinn_gpu_ctx** out) {
     c->v.alloc(c->n_params, c->stream);
     c->st.alloc(1, c->stream);
     c->ticket.alloc(1, c->stream);
+    mark("uploads", c->stream);
     configure(c.get());
+    mark("configure", c->stream);
     reset_state(c.get(), LLONG_MAX, nullptr);
     CK(cudaStreamSynchronize(c->stream));
     *out = c.release();
