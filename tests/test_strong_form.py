@@ -150,3 +150,45 @@ def test_strong_rejects_unsupported_shapes():
     with pytest.raises(VpinnError) as e:
         make_strong_pair(strong_spec(layers=(2, 16, 2), eps_source=2))
     assert e.value.code == 4
+
+
+@pytest.mark.gpu
+def test_strong_form_through_host_pipeline_and_device_assembly():
+    """form: strong from a config (the C++ host pipeline's view) against the
+    same problem with the device assembling the points and f at them."""
+    from paper_2404_12063_b200 import host
+    cfg = {"problem": {"pde": {"type": "cd2d", "eps": 0.8, "b": [0.3, -0.2]}, "forcing": "sin2pi_f",
+                       "boundary_g": "sin2pi_u", "n_boundary_points": 96},
+           "discretization": {"form": "strong", "n_test_per_dim": 3, "n_quad_per_dim": 5},
+           "network": {"layers": [2, 24, 24, 1]},
+           "training": {"learning_rate": 1e-3, "seed": 3, "precision": "single"}}
+    mesh = host.Mesh.structured(6, 5, skew=0.2)
+    hp = host.HostProblem(cfg, mesh=mesh)
+    dp = host.HostProblem(cfg, mesh=mesh, device_assembly=True)
+    gh, gd = hp.gpu(), dp.gpu()
+    assert "sf_step_kernel" in gh.step_kernel() and "sf_step_kernel" in gd.step_kernel()
+    ph, grh = gh.loss_and_grad()
+    pd, grd = gd.loss_and_grad()
+    assert np.abs(ph - pd).max() <= 1e-6 * np.abs(ph).max(), (ph, pd)
+    assert np.abs(grh - grd).max() <= 1e-6 * np.abs(grh).max()
+    # the host view against the oracle on the same mesh
+    nodes, cells, _ = mesh.arrays()
+    spec = po.ProblemSpec(nodes=nodes, cells=cells, n_test_1d=3, n_quad_1d=5, forcing="sin2pi_f",
+                          boundary_g="sin2pi_u", n_boundary=96, eps=0.8, bx=0.3, by=-0.2,
+                          layers=(2, 24, 24, 1), seed=3, strong=True)
+    ob = po.OracleProblem(spec, double=False)
+    po_, _ = ob.loss_and_grad(hp.init_params())
+    assert rel(ph[0], po_[0]) < 1e-5
+    rep = gd.train(20, lr0=1e-3)
+    ref = ob.train(hp.init_params(), 20, lr0=1e-3, log_every=1)
+    r = np.abs(rep.records["total"] - ref["every_step"][:, 0]) / np.abs(ref["every_step"][:, 0])
+    assert r.max() < 1e-5
+
+
+@pytest.mark.gpu
+def test_weak_only_entry_points_reject_strong_contexts():
+    from paper_2404_12063_b200._capi import VpinnError
+    _, g, _ = make_strong_pair(CASES["acceptance_case4"]())
+    with pytest.raises(VpinnError) as e:
+        g.contract(np.zeros(g.n_elem * g.n_quad, np.float32), np.zeros(g.n_elem * g.n_quad, np.float32))
+    assert e.value.code == 2
