@@ -238,6 +238,8 @@ __global__ void __launch_bounds__(kRAThreads) reduce_adam_kernel(const float* __
                                                                    const double* __restrict__ loss_part,
                                                                    int n_loss_rows, double* __restrict__ red,
                                                                    unsigned* ticket, const AdamArgs a) {
+  pdl_trigger();
+  pdl_wait();
   if (a.st->stopped) return;
   __shared__ int last;
   reduce_body(grad_part, n_rows, stride, n_params, loss_part, n_loss_rows, red);

@@ -74,6 +74,15 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   }
 }
 
+// ---- programmatic dependent launch (PDL) -----------------------------------
+// A kernel launched with the programmatic-stream-serialization attribute may
+// be scheduled while its predecessor still runs; pdl_wait() blocks until the
+// predecessor grid has completed and its writes are visible (a no-op for a
+// normal launch), pdl_trigger() lets this kernel's successor be scheduled
+// early.  Called first thing, before any read of predecessor data.
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 __device__ __forceinline__ uint64_t globaltimer() {
   uint64_t t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));

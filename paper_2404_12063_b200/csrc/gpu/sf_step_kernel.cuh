@@ -236,6 +236,8 @@ template <int D, int ACT, int MODE>
 __global__ void __launch_bounds__(32 * sf::kMaxWarps, 1) sf_step_kernel(const StepArgs a) {
   using namespace sf;
   static_assert(D >= 1 && D <= 4, "hidden layers");
+  pdl_trigger();
+  pdl_wait();
   if constexpr (MODE == kModeFused) {
     if (a.stop_flag && *a.stop_flag) return;
   }

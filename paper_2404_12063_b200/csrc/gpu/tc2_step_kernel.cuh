@@ -263,6 +263,8 @@ __global__ void __maxnreg__(VPG_TC2_MAXNREG) tc2_step_kernel(const StepArgs a) {
   constexpr int NL = LY::NL;
   using AC = Act<ACT>;
 
+  pdl_trigger();
+  pdl_wait();
   if (a.stop_flag != nullptr && *a.stop_flag != 0) return;
   if constexpr (VPG_PHASE_CLOCK != 0) {  // entry clocks (diagnostics)
     if (a.phase_clk != nullptr && blockIdx.x == 0 && threadIdx.x == 0)

@@ -3,6 +3,7 @@
 #include <dlfcn.h>
 
 #include <algorithm>
+#include <utility>
 #include <condition_variable>
 #include <thread>
 #include <chrono>
@@ -873,11 +874,41 @@ void configure(vpinn_gpu_ctx* c) {
   c->e_scalar.alloc(1, c->stream);
 }
 
+// kernel launch with the programmatic-dependent-launch attribute when pdl:
+// the kernel (which starts with pdl_trigger / pdl_wait) is scheduled while
+// its predecessor's tail runs, hiding the launch latency between the
+// epoch's kernels
+template <typename... KArgs, typename... Args>
+void launch_k(bool pdl, void (*k)(KArgs...), int grid, int block, size_t smem, cudaStream_t s, Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = pdl ? at : nullptr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  CK(cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...));
+}
+
+// off by default: A/B on the gear, PDL made the weak epoch 1.3% slower (the
+// early-resident successor CTAs skew the step kernel's CTA placement) and
+// the strong epoch 0.1% faster; VPINN_PDL=1 enables it
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("VPINN_PDL");
+    return e && std::atoi(e) != 0;
+  }();
+  return on;
+}
+
 void launch_fused(vpinn_gpu_ctx* c, const vpg::StepArgs& a) {
   if (c->strong)
-    c->sfk.fused<<<c->grid_step, 32 * c->sf_warps, c->smem_step, c->stream>>>(a);
+    launch_k(pdl_enabled(), c->sfk.fused, c->grid_step, 32 * c->sf_warps, c->smem_step, c->stream, a);
   else if (c->tc2)
-    c->var.tc2<<<c->grid_step, vpg::t2::kNT, c->smem_step, c->stream>>>(a);
+    launch_k(pdl_enabled(), c->var.tc2, c->grid_step, vpg::t2::kNT, c->smem_step, c->stream, a);
   else if (c->tc)
     c->var.tc<<<c->grid_step, 128 * vpg::kTcNQ, c->smem_step, c->stream>>>(a);
   else
@@ -984,9 +1015,10 @@ void enqueue_epoch(vpinn_gpu_ctx* c, const vpg::AdamArgs& aa) {
     return;
   }
   enqueue_grad(c, &c->st.p->stopped, /*with_reduce=*/false);
-  vpg::reduce_adam_kernel<<<vpg::reduce_adam_grid(c->n_params), vpg::kRAThreads, 0, c->stream>>>(
-      c->grad_part.p, c->grad_rows, c->part_stride, c->n_params, c->loss_part.p, c->loss_rows, c->red.p,
-      c->ticket.p, aa);
+  const float* gp = c->grad_part.p;
+  const double* lp = c->loss_part.p;
+  launch_k(pdl_enabled() && !c->split, vpg::reduce_adam_kernel, vpg::reduce_adam_grid(c->n_params), vpg::kRAThreads,
+           0, c->stream, gp, c->grad_rows, c->part_stride, c->n_params, lp, c->loss_rows, c->red.p, c->ticket.p, aa);
   CK(cudaGetLastError());
   c->launches += 1;
 }
