@@ -147,14 +147,14 @@ def build_problem():
     return host.HostProblem(GEAR_CFG, mesh=mesh), mesh
 
 
-def cpu_oracle_rate(mesh, max_seconds=25.0, threads=1):
+def cpu_oracle_rate(mesh, max_seconds=25.0, threads=1, strong=False):
     """The reference algorithm (plain-C++ oracle port, fp32, serial) on the
     same gear problem: per-epoch seconds over a bounded sample."""
     from oracle import pyoracle as po
     nodes, cells, _ = mesh.arrays()
     spec = po.ProblemSpec(nodes=nodes, cells=cells, n_test_1d=5, n_quad_1d=5, forcing="gear_f",
                           boundary_g="zero", n_boundary=800, eps=1.0, bx=0.1, by=0.0,
-                          layers=(2, 30, 30, 30, 1), seed=42)
+                          layers=(2, 30, 30, 30, 1), seed=42, strong=strong)
     ob = po.OracleProblem(spec, double=False)
     p0 = ob.init_params()
     first = ob.time_steps(p0, lr=1e-3, warmup=0, reps=1)[0]  # also the warm-up
@@ -289,7 +289,8 @@ def main():
     e2e = _e2e(hp, device, rank, world, pg, args.steps)
     e2e_mesh = _e2e_from_mesh(mesh, device, rank, world, pg, args.steps)
     mf = _matrix_free(mesh, device, rank, world) if rank == 0 else None
-    strong = _strong_form(mesh, device, rank, world, pg, args.steps, ms_per_step)
+    strong = _strong_form(mesh, device, rank, world, pg, args.steps, ms_per_step,
+                          cpu=rank == 0 and world == 1 and not args.no_cpu_baseline)
 
     # ---- CPU baseline (rank 0, N=1 only) ----
     cpu = None
@@ -474,7 +475,7 @@ def _matrix_free(mesh, device, rank, world):
 MMA_SYNC_TF32_TFLOPS = 277.0
 
 
-def _strong_form(mesh, device, rank, world, pg, steps, weak_ms):
+def _strong_form(mesh, device, rank, world, pg, steps, weak_ms, cpu=False):
     """the strong-form collocation baseline (the paper's
     PINN comparison) on the same gear workload: order-2 network at the
     354,800 interior quadrature points + the boundary penalty, one
@@ -519,7 +520,20 @@ def _strong_form(mesh, device, rank, world, pg, steps, weak_ms):
                          "peak": MMA_SYNC_TF32_TFLOPS, "unit": "TFLOP/s", "frac": exec_tflops / MMA_SYNC_TF32_TFLOPS,
                          "algorithmic_tflops": alg_tflops,
                          "peak_source": "tools/micro/mma_sync_rate.cu on this pool's B200"},
-            "l2": "flushed between timed epochs"}
+            "l2": "flushed between timed epochs",
+            "cpu_baseline": _strong_cpu(mesh) if cpu else None}
+
+
+def _strong_cpu(mesh):
+    """The reference's strong-form algorithm (oracle port, fp32, 1 core) on
+    the same gear points: a bounded sample of full epochs."""
+    try:
+        c = cpu_oracle_rate(mesh, max_seconds=12.0, strong=True)
+        return {"value": c["n_interior"] / c["median_s"], "unit": UNIT, "cores": 1, "kind": "port",
+                "sample": f"median of {c['reps']} full strong-form gear epochs (after 1 warm-up), fp32 oracle port",
+                "median_s_per_epoch": c["median_s"]}
+    except Exception as ex:  # keep the GPU line even if the CPU leg fails
+        return {"value": None, "unit": UNIT, "cores": 1, "kind": "port", "sample": f"failed: {ex}"}
 
 
 def _sweep(device):
