@@ -15,11 +15,12 @@ from oracle import pyoracle as po
 from paper_2404_12063_b200 import _capi
 
 
-def _spec():
+def _spec(strong=False):
     nodes, cells = po.structured_mesh(5, 3, skew=0.15, skew_seed=1234)
     return po.ProblemSpec(nodes=nodes, cells=cells, n_test_1d=3, n_quad_1d=4, forcing="sin2pi_f",
                           boundary_g="sin2pi_u", n_boundary=37, n_sensors=11, sensor_seed=7,
-                          sensor_field="sin2pi_u", eps=0.7, bx=0.3, by=-0.2, layers=(2, 8, 8, 1), seed=3)
+                          sensor_field="sin2pi_u", eps=0.7, bx=0.3, by=-0.2, layers=(2, 8, 8, 1), seed=3,
+                          strong=strong)
 
 
 def _free_port():
@@ -30,11 +31,11 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, out_q):
+def _worker(rank, world, port, out_q, strong=False):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
-    ob = po.OracleProblem(_spec(), double=True)
+    ob = po.OracleProblem(_spec(strong), double=True)
     p0 = ob.init_params()
     e0, e1, b0, b1, s0, s1 = _capi.partition(ob.E, ob.n_bnd, ob.n_sen, rank, world)
     parts, grad = ob.loss_and_grad_part(p0, e0, e1, b0, b1, s0, s1)
@@ -49,19 +50,21 @@ def _worker(rank, world, port, out_q):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2, 3])
-def test_partitioned_objective_sums_to_single_rank(world):
+@pytest.mark.parametrize("world,strong", [(2, False), (3, False), (2, True)])
+def test_partitioned_objective_sums_to_single_rank(world, strong):
+    """weak form, and the strong-form collocation objective (whose residual
+    mean uses the global interior count on every rank)"""
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q, strong)) for r in range(world)]
     for p in procs:
         p.start()
     red, ranges = q.get(timeout=120)
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
-    ob = po.OracleProblem(_spec(), double=True)
+    ob = po.OracleProblem(_spec(strong), double=True)
     parts, grad = ob.loss_and_grad(ob.init_params())
     np.testing.assert_allclose(red[:4], parts, rtol=1e-12, atol=1e-14)
     np.testing.assert_allclose(red[4:], grad, rtol=1e-10, atol=1e-12 * np.abs(grad).max())
