@@ -303,6 +303,8 @@ def main():
         except Exception as ex:  # keep the GPU line even if the CPU leg fails
             cpu = {"value": None, "unit": UNIT, "cores": 1, "kind": "port", "sample": f"failed: {ex}"}
 
+    c4 = _c4_disk(device) if (not args.no_sweep and rank == 0 and world == 1) else None
+    c5i = _c5_inverse(mesh, device) if (not args.no_sweep and rank == 0 and world == 1) else None
     sweep = _sweep(device) if (not args.no_sweep and rank == 0 and world == 1) else None
     sweep3 = _sweep_c3(device) if (not args.no_sweep and rank == 0 and world == 1) else None
     if rank != 0:
@@ -339,6 +341,10 @@ def main():
         line["sweep_c2"] = sweep
     if sweep3:
         line["sweep_c3"] = sweep3
+    if c4:
+        line["c4_disk"] = c4
+    if c5i:
+        line["c5_inverse"] = c5i
     print(json.dumps(line), flush=True)
 
 
@@ -534,6 +540,53 @@ def _strong_cpu(mesh):
                 "median_s_per_epoch": c["median_s"]}
     except Exception as ex:  # keep the GPU line even if the CPU leg fails
         return {"value": None, "unit": UNIT, "cores": 1, "kind": "port", "sample": f"failed: {ex}"}
+
+
+def _flushed_epoch_ms(hp, device, reps=20):
+    from paper_2404_12063_b200 import gpu as G
+    g = G.GpuStep.from_problem(hp.view(device), keepalive=hp)
+    g.set_params(hp.init_params())
+    g.adam_reset()
+    g.run_steps(10, 1e-3)
+    g.synchronize()
+    times = []
+    for _ in range(reps):
+        g.flush_l2()
+        times.append(g.time_steps(1, 1e-3))
+    kernel = g.step_kernel()
+    g.close()
+    return float(np.median(times)), kernel
+
+
+def _c5_inverse(mesh, device):
+    """C5 inverse: the gear with a trainable scalar eps (init 2.0) and 50
+    sensors (values from a named field, seed 7); device-timed, L2 flushed."""
+    import copy
+    from paper_2404_12063_b200 import host
+    cfg = copy.deepcopy(GEAR_CFG)
+    cfg["problem"]["exact_solution"] = "sin2pi_u"
+    cfg["problem"]["sensors"] = {"count": 50, "seed": 7}
+    cfg["network"]["eps_scalar_init"] = 2.0
+    hp = host.HostProblem(cfg, mesh=mesh)
+    ms, kernel = _flushed_epoch_ms(hp, device)
+    return {"cells": hp.E, "sensors": hp.n_sen, "ms_per_epoch": ms, "kernel": kernel,
+            "quad_pt_evals_per_s": hp.n_int / (ms * 1e-3), "l2": "flushed between timed epochs"}
+
+
+def _c4_disk(device):
+    """C4: convection-diffusion on the circular domain, 32x32 = 1,024 skewed
+    cells with per-cell bilinear Jacobians, T=25, Q=100, b=(1,0), constant
+    forcing; device-timed epochs, L2 flushed."""
+    from paper_2404_12063_b200 import host
+    cfg = {"problem": {"pde": {"type": "cd2d", "eps": 1.0, "b": [1.0, 0.0]}, "forcing": "one",
+                       "boundary_g": "zero", "n_boundary_points": 400},
+           "discretization": {"n_test_per_dim": 5, "n_quad_per_dim": 10},
+           "network": {"layers": [2, 30, 30, 30, 1]},
+           "training": {"learning_rate": 1e-3, "seed": 42, "precision": "single"}}
+    hp = host.HostProblem(cfg, mesh=host.Mesh.disk(32))
+    ms, kernel = _flushed_epoch_ms(hp, device)
+    return {"cells": hp.E, "n_test": hp.T, "n_quad": hp.Q, "ms_per_epoch": ms, "kernel": kernel,
+            "quad_pt_evals_per_s": hp.n_int / (ms * 1e-3), "l2": "flushed between timed epochs"}
 
 
 def _sweep(device):

@@ -40,6 +40,14 @@ def gear_spec(**over):
     return po.ProblemSpec(nodes=nodes, cells=cells, **kw)
 
 
+def _disk_spec():
+    from paper_2404_12063_b200 import host
+    nodes, cells, _ = host.Mesh.disk(32).arrays()
+    return po.ProblemSpec(nodes=nodes, cells=cells, n_test_1d=5, n_quad_1d=10, forcing="one",
+                          boundary_g="zero", n_boundary=400, eps=1.0, bx=1.0, by=0.0,
+                          layers=(2, 30, 30, 30, 1), seed=42)
+
+
 CASES = {
     "c1_poisson": lambda: c1_spec(),
     "gear576_cd2d": lambda: gear_spec(),
@@ -53,6 +61,8 @@ CASES = {
         *po.structured_mesh(2, 2, (-1.0, 1.0), (-1.0, 1.0)), n_test_1d=5, n_quad_1d=10,
         forcing="bump_f", boundary_g="bump_u", n_boundary=400, n_sensors=50, sensor_seed=7,
         sensor_field="bump_u", eps_source=1, scalars=(2.0,), layers=(2, 20, 20, 1), seed=42),
+    # C4: circular domain, 1,024 skewed cells (per-cell bilinear Jacobians), b = (1, 0)
+    "c4_disk_cd2d": lambda: _disk_spec(),
     "split_path_q400": lambda: po.ProblemSpec(
         *po.structured_mesh(2, 2), n_test_1d=6, n_quad_1d=20, forcing="sin4pi_f",
         boundary_g="sin4pi_u", n_boundary=400, layers=(2, 30, 30, 30, 1), seed=42),
