@@ -104,13 +104,9 @@ __device__ __forceinline__ void mma_tf32(float (&d)[4], const uint32_t (&a)[4], 
       : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
       : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
 }
-// d += a b in three TF32 passes (the lo x lo term is below fp32 resolution)
-__device__ __forceinline__ void mma3(float (&d)[4], const uint32_t (&ah)[4], const uint32_t (&al)[4],
-                                     uint32_t bh0, uint32_t bh1, uint32_t bl0, uint32_t bl1) {
-  mma_tf32(d, al, bh0, bh1);
-  mma_tf32(d, ah, bl0, bl1);
-  mma_tf32(d, ah, bh0, bh1);
-}
+// d += a b in three TF32 passes (a_lo b_hi, a_hi b_lo, a_hi b_hi; the lo x lo
+// term is below fp32 resolution): the kernels issue the passes interleaved
+// over independent accumulators (see the GEMM loops)
 __device__ __forceinline__ void split4(const float (&v)[4], uint32_t (&h)[4], uint32_t (&l)[4]) {
 #pragma unroll
   for (int j = 0; j < 4; ++j) split(v[j], h[j], l[j]);
