@@ -524,21 +524,31 @@ VPG_SF_PRAGMA_UNROLL(VPG_SF_ROLL)
 VPG_SF_PRAGMA_UNROLL(VPG_SF_ROLL)
         for (int kt = 0; kt < 2; ++kt) {
           const int pa = 8 * kt + t, pb = pa + 4;
-          // h == 1: hidden 0 at (points pa / pb, units 8 nt + g), recomputed
-          float z0t[4][2];
-          if (h == 1) {
+          // z, s1, s2 of hidden h-1 at (points pa / pb, units 8 nt + g), shared
+          // by the five streams; hidden 0 is recomputed from the points
+          float zt[4][2], s1t[4][2], s2t[4][2];
+          {
             float2 q[2];
+            if (h == 1) {
 #pragma unroll
-            for (int i = 0; i < 2; ++i) {
-              const int pp = p0 + (i ? pb : pa);
-              q[i] = pp < n_pts ? pts[pp] : make_float2(0.f, 0.f);
+              for (int i = 0; i < 2; ++i) {
+                const int pp = p0 + (i ? pb : pa);
+                q[i] = pp < n_pts ? pts[pp] : make_float2(0.f, 0.f);
+              }
             }
 #pragma unroll
             for (int nt = 0; nt < 4; ++nt) {
               const int k = 8 * nt + g;
-              const float2 w = sW0[k];
 #pragma unroll
-              for (int i = 0; i < 2; ++i) z0t[nt][i] = Act<ACT>::value(fmaf(w.y, q[i].y, w.x * q[i].x) + sB[k]);
+              for (int i = 0; i < 2; ++i) {
+                if (h == 1) {
+                  const float2 w = sW0[k];
+                  zt[nt][i] = Act<ACT>::value(fmaf(w.y, q[i].y, w.x * q[i].x) + sB[k]);
+                } else {
+                  zt[nt][i] = Sp[(i ? pb : pa) * RS + k];
+                }
+                derivs12<ACT>(zt[nt][i], s1t[nt][i], s2t[nt][i]);
+              }
             }
           }
 VPG_SF_PRAGMA_UNROLL(VPG_SF_ROLL)
@@ -558,13 +568,11 @@ VPG_SF_PRAGMA_UNROLL(VPG_SF_ROLL)
 #pragma unroll
               for (int q = 0; q < 2; ++q) {
                 const int o = (q ? pb : pa) * RS + k;
-                const float z = h == 1 ? z0t[nt][q] : Sp[o];
                 float xb;
                 if (s == 0) {
-                  xb = z;
+                  xb = zt[nt][q];
                 } else {
-                  float s1, s2;
-                  derivs12<ACT>(z, s1, s2);
+                  const float s1 = s1t[nt][q], s2 = s2t[nt][q];
                   float ta, t2a = 0.f;
                   if (h == 1) {
                     ta = (s == 1 || s == 3) ? sW0[k].x : sW0[k].y;
