@@ -100,12 +100,19 @@ __host__ __device__ constexpr size_t cell_warp_smem_bytes(int nwarps, int stage_
          sizeof(uint64_t) * nwarps * kCCMaxStages + sizeof(double) * 2 * nwarps + 64;
 }
 
-template <int kCWWarps>
+// FT, FQ > 0: the cell shape fixed at compile time (T = FT, Q = FQ <= 32; the
+// benchmark gear's 5x5 / 5x5 cells): the point vectors of phase A and the
+// residual adjoints of phase B sit in registers and every loop is unrolled
+// without predication, so each premultiplier entry costs one shared-memory
+// load and one FMA per phase
+template <int kCWWarps, int FT = 0, int FQ = 0>
 __global__ void __launch_bounds__(32 * kCWWarps, 1) contract_warp_kernel(const CellContractArgs a) {
+  constexpr bool kFixed = FT > 0 && FQ > 0;
+  static_assert(!kFixed || (FT <= 32 && FQ <= 32), "fixed cell shape: T, Q <= 32");
   if (a.stop_flag != nullptr && *a.stop_flag != 0) return;
   extern __shared__ __align__(128) float cs[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int T = a.T, Q = a.Q;
+  const int T = kFixed ? FT : a.T, Q = kFixed ? FQ : a.Q;
   const size_t TQ = (size_t)T * Q;
   const int Q4 = (Q + 3) & ~3;
   float* ring = cs + (size_t)warp * a.nstage * a.stage_floats;
@@ -156,7 +163,40 @@ __global__ void __launch_bounds__(32 * kCWWarps, 1) contract_warp_kernel(const C
     __syncwarp();
     // phase A: residual rows
     float lsq = 0.f, lge = 0.f;
-    for (int j = lane; j < T; j += 32) {
+    if constexpr (kFixed) {
+      float sx[FQ], sy[FQ], cv[FQ];
+#pragma unroll
+      for (int q = 0; q < FQ; ++q) {
+        sx[q] = sxs[q];
+        sy[q] = sys[q];
+        cv[q] = cvs[q];
+      }
+      const int j = lane;
+      if (j < FT) {
+        const float* gxr = Gx + j * FQ;
+        const float* gyr = Gy + j * FQ;
+        const float* tr = conv ? Tv + j * FQ : gxr;
+        float ax[4] = {0.f, 0.f, 0.f, 0.f}, ay[4] = {0.f, 0.f, 0.f, 0.f}, at[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+        for (int q = 0; q < FQ; ++q) {
+          ax[q & 3] = fmaf(gxr[q], sx[q], ax[q & 3]);
+          ay[q & 3] = fmaf(gyr[q], sy[q], ay[q & 3]);
+          if (conv) at[q & 3] = fmaf(tr[q], cv[q], at[q & 3]);
+        }
+        const float gx = (ax[0] + ax[1]) + (ax[2] + ax[3]);
+        const float gy = (ay[0] + ay[1]) + (ay[2] + ay[3]);
+        const float tt = (at[0] + at[1]) + (at[2] + at[3]);
+        float r = spatial ? gx + gy : e_fixed * (gx + gy);
+        r += tt;
+        r -= vf[j];
+        if (a.res) a.res[(size_t)k * T + j] = r;
+        const float rb = a.rscale * r;
+        rbs[j] = rb;
+        lsq = fmaf(r, r, lsq);
+        lge = fmaf(rb, gx + gy, lge);
+      }
+    }
+    for (int j = kFixed ? T : lane; j < T; j += 32) {
       const float* gxr = Gx + (size_t)j * Q;
       const float* gyr = Gy + (size_t)j * Q;
       const float* tr = conv ? Tv + (size_t)j * Q : gxr;
@@ -190,7 +230,44 @@ __global__ void __launch_bounds__(32 * kCWWarps, 1) contract_warp_kernel(const C
     }
     __syncwarp();
     // phase B: adjoints per quadrature point
-    for (int q = lane; q < Q; q += 32) {
+    if constexpr (kFixed) {
+      float rb[FT];
+#pragma unroll
+      for (int j = 0; j < FT; ++j) rb[j] = rbs[j];
+      const int q = lane;
+      if (q < FQ) {
+        const float* gxc = Gx + q;
+        const float* gyc = Gy + q;
+        const float* tc = conv ? Tv + q : gxc;
+        float bx4[4] = {0.f, 0.f, 0.f, 0.f}, by4[4] = {0.f, 0.f, 0.f, 0.f}, bt4[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+        for (int j = 0; j < FT; ++j) {
+          bx4[j & 3] = fmaf(gxc[j * FQ], rb[j], bx4[j & 3]);
+          by4[j & 3] = fmaf(gyc[j * FQ], rb[j], by4[j & 3]);
+          if (conv) bt4[j & 3] = fmaf(tc[j * FQ], rb[j], bt4[j & 3]);
+        }
+        const float tx = (bx4[0] + bx4[1]) + (bx4[2] + bx4[3]);
+        const float ty = (by4[0] + by4[1]) + (by4[2] + by4[3]);
+        const float tt = (bt4[0] + bt4[1]) + (bt4[2] + bt4[3]);
+        float ox, oy;
+        if (spatial) {
+          const float ep = vep[q];
+          ox = ep * tx;
+          oy = ep * ty;
+          a.eb[pb + q] = vux[q] * tx + vuy[q] * ty;
+        } else {
+          ox = e_fixed * tx;
+          oy = e_fixed * ty;
+        }
+        if (conv) {
+          ox = fmaf(a.bx, tt, ox);
+          oy = fmaf(a.by, tt, oy);
+        }
+        a.uxb[pb + q] = ox;
+        a.uyb[pb + q] = oy;
+      }
+    }
+    for (int q = kFixed ? Q : lane; q < Q; q += 32) {
       const float* gxc = Gx + q;
       const float* gyc = Gy + q;
       const float* tc = conv ? Tv + q : gxc;

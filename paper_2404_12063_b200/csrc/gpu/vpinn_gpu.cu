@@ -453,6 +453,7 @@ struct vpinn_gpu_ctx {
   bool cell_contract = false;
   int grid_cc = 0;
   int cw_warps = 8;  // warps per CTA of the warp-per-cell contraction
+  bool cw_fixed = false;  // its 5x5 / 5x5 compile-time-shape variant
   size_t smem_cc = 0;
   int grid_contract = 0, grid_pen = 0, grid_fwd = 0;
   size_t smem_contract = 0, smem_fwd = 0;
@@ -556,6 +557,17 @@ void configure_strong(vpinn_gpu_ctx* c) {
   a.loss_part = c->loss_part.p;
   c->red.alloc((size_t)c->n_params + vpg::kLpWords, c->stream);
   c->e_scalar.alloc(1, c->stream);
+}
+
+// the warp-per-cell contraction: warps per CTA x the cell shape fixed at
+// compile time for 5x5 / 5x5 cells (the benchmark gear)
+const void* cw_kernel(int nw, bool fixed) {
+  if (fixed)
+    return nw == 16 ? (const void*)vpg::contract_warp_kernel<16, 25, 25>
+                    : (nw == 12 ? (const void*)vpg::contract_warp_kernel<12, 25, 25>
+                                : (const void*)vpg::contract_warp_kernel<8, 25, 25>);
+  return nw == 16 ? (const void*)vpg::contract_warp_kernel<16>
+                  : (nw == 12 ? (const void*)vpg::contract_warp_kernel<12> : (const void*)vpg::contract_warp_kernel<8>);
 }
 
 void configure(vpinn_gpu_ctx* c) {
@@ -837,8 +849,9 @@ void configure(vpinn_gpu_ctx* c) {
     if (c->smem_cc > budget) {
       c->cell_contract = false;  // cell larger than a warp's ring: row-chunked kernel
     } else {
-      const void* fn = nw == 16 ? (const void*)vpg::contract_warp_kernel<16>
-                                : (nw == 12 ? (const void*)vpg::contract_warp_kernel<12> : (const void*)vpg::contract_warp_kernel<8>);
+      const char* fx = std::getenv("VPINN_CW_FIXED");
+      c->cw_fixed = c->T == 25 && c->Q == 25 && !(fx && std::atoi(fx) == 0);
+      const void* fn = cw_kernel(nw, c->cw_fixed);
       CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem_cc));
       CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, 32 * nw, c->smem_cc));
       c->grid_cc = std::max(1, std::min(ceil_div(c->E, nw), std::max(1, occ) * c->sm_count));
@@ -1087,12 +1100,8 @@ int launch_contract(vpinn_gpu_ctx* c, const float* ux, const float* uy, const fl
     a.rscale = rscale;
     a.loss_part = loss_part;
     a.stop_flag = stop;
-    if (c->cw_warps == 16)
-      vpg::contract_warp_kernel<16><<<c->grid_cc, 32 * 16, c->smem_cc, c->stream>>>(a);
-    else if (c->cw_warps == 12)
-      vpg::contract_warp_kernel<12><<<c->grid_cc, 32 * 12, c->smem_cc, c->stream>>>(a);
-    else
-      vpg::contract_warp_kernel<8><<<c->grid_cc, 32 * 8, c->smem_cc, c->stream>>>(a);
+    auto fn = reinterpret_cast<void (*)(vpg::CellContractArgs)>(const_cast<void*>(cw_kernel(c->cw_warps, c->cw_fixed)));
+    fn<<<c->grid_cc, 32 * c->cw_warps, c->smem_cc, c->stream>>>(a);
     CK(cudaGetLastError());
     c->launches += 1;
     return c->grid_cc;
