@@ -324,7 +324,7 @@ def main():
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
         "roofline": _step_roofline(kernel_name, mlp_tflops, ffma.value, pk, ms_mlp / (ms_mlp + ms_red + ms_adam)),
-        "roofline_contraction": {"bound": "hbm", "kernel": "contract_warp_kernel (standalone, warp per cell)",
+        "roofline_contraction": {"bound": "hbm", "kernel": "contract_warp_kernel (standalone, warp per cell; compile-time 5x5/5x5 cell shape on the gear)",
                                  "achieved": contract_gbs, "peak": pk.get("hbm_gbs"), "unit": "GB/s",
                                  "frac": contract_gbs / pk["hbm_gbs"],
                                  "traffic": (_traffic("contract_warp") or {}).get("bytes"),
