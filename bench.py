@@ -305,6 +305,7 @@ def main():
 
     c4 = _c4_disk(device) if (not args.no_sweep and rank == 0 and world == 1) else None
     c5i = _c5_inverse(mesh, device) if (not args.no_sweep and rank == 0 and world == 1) else None
+    c5p = _c5_paper(mesh, device) if (not args.no_sweep and rank == 0 and world == 1) else None
     sweep = _sweep(device) if (not args.no_sweep and rank == 0 and world == 1) else None
     sweep3 = _sweep_c3(device) if (not args.no_sweep and rank == 0 and world == 1) else None
     if rank != 0:
@@ -345,6 +346,8 @@ def main():
         line["c4_disk"] = c4
     if c5i:
         line["c5_inverse"] = c5i
+    if c5p:
+        line["c5_paper_variant"] = c5p
     print(json.dumps(line), flush=True)
 
 
@@ -571,6 +574,22 @@ def _c5_inverse(mesh, device):
     ms, kernel = _flushed_epoch_ms(hp, device)
     return {"cells": hp.E, "sensors": hp.n_sen, "ms_per_epoch": ms, "kernel": kernel,
             "quad_pt_evals_per_s": hp.n_int / (ms * 1e-3), "l2": "flushed between timed epochs"}
+
+
+def _c5_paper(mesh, device):
+    """The paper's gear variant: T=16 (4x4), Q=25, 6,096 boundary
+    points, [2,50,50,50,1]; H = 50 runs on the CUDA-core step kernel."""
+    import copy
+    from paper_2404_12063_b200 import host
+    cfg = copy.deepcopy(GEAR_CFG)
+    cfg["discretization"]["n_test_per_dim"] = 4
+    cfg["problem"]["n_boundary_points"] = 6096
+    cfg["network"]["layers"] = [2, 50, 50, 50, 1]
+    hp = host.HostProblem(cfg, mesh=mesh)
+    ms, kernel = _flushed_epoch_ms(hp, device)
+    return {"cells": hp.E, "n_test": hp.T, "n_quad": hp.Q, "boundary_points": hp.n_bnd, "layers": [2, 50, 50, 50, 1],
+            "ms_per_epoch": ms, "kernel": kernel, "quad_pt_evals_per_s": hp.n_int / (ms * 1e-3),
+            "l2": "flushed between timed epochs"}
 
 
 def _c4_disk(device):

@@ -137,7 +137,11 @@ struct Layout {
   static constexpr int NPMAX = 3 * H + (D - 1) * (H * H + H) + C * (H + 1) + 8;
   static constexpr int NGR = (NPMAX + kThreads - 1) / kThreads;
   static constexpr int REV_UNION = kThreads * SG;
-  static constexpr int PART_FLOATS_H = kWarps * (HP * HP + HP);
+  // per-warp parameter-gradient partials of a hidden->hidden layer; wide
+  // layers (H = 50) combine them in two rounds of kWarps / 2 so the
+  // reverse-phase union fits shared memory next to the 128-point state
+  static constexpr int PART_GROUPS = kWarps * (HP * HP + HP) > 8192 ? 2 : 1;
+  static constexpr int PART_FLOATS_H = (kWarps / PART_GROUPS) * (HP * HP + HP);
   static constexpr int REV_NEED = REV_UNION > PART_FLOATS_H ? REV_UNION : PART_FLOATS_H;
   static constexpr int OFF_W = 0;
   static constexpr int OFF_EX = OFF_W + WTOT;
@@ -473,50 +477,55 @@ __device__ __forceinline__ void reverse_hidden(RevCtx& rc, float (&gA)[H], float
     }
     __syncthreads();
   }
-  // partials [warp][HP][HP] + bias [warp][HP]
-  {
-    float* pw = Part + warp * (HP * HP + HP);
+  // partials [warp][HP][HP] + bias [warp][HP], summed over warps in a fixed
+  // order (in PART_GROUPS rounds for wide layers)
+  constexpr int kGroups = LY::PART_GROUPS, kWpg = kWarps / kGroups;
+#pragma unroll 1
+  for (int grp = 0; grp < kGroups; ++grp) {
+    if (warp / kWpg == grp) {
+      float* pw = Part + (warp % kWpg) * (HP * HP + HP);
 #pragma unroll
-    for (int rr = 0; rr < NROUND; ++rr) {
-      const int t = lane + 32 * rr;
-      if (t < NTILE) {
-        const int ob = t % NOB, ib = t / NOB;
+      for (int rr = 0; rr < NROUND; ++rr) {
+        const int t = lane + 32 * rr;
+        if (t < NTILE) {
+          const int ob = t % NOB, ib = t / NOB;
 #pragma unroll
-        for (int a4 = 0; a4 < 4; ++a4) {
-          const int o = ob * 4 + a4;
-          if (o < HP && ib * 8 < HP)
-            sts4(pw + o * HP + ib * 8, make_float4(accr[rr][a4 * 8], accr[rr][a4 * 8 + 1], accr[rr][a4 * 8 + 2],
-                                                   accr[rr][a4 * 8 + 3]));
-          if (o < HP && ib * 8 + 4 < HP)
-            sts4(pw + o * HP + ib * 8 + 4, make_float4(accr[rr][a4 * 8 + 4], accr[rr][a4 * 8 + 5],
-                                                       accr[rr][a4 * 8 + 6], accr[rr][a4 * 8 + 7]));
+          for (int a4 = 0; a4 < 4; ++a4) {
+            const int o = ob * 4 + a4;
+            if (o < HP && ib * 8 < HP)
+              sts4(pw + o * HP + ib * 8, make_float4(accr[rr][a4 * 8], accr[rr][a4 * 8 + 1], accr[rr][a4 * 8 + 2],
+                                                     accr[rr][a4 * 8 + 3]));
+            if (o < HP && ib * 8 + 4 < HP)
+              sts4(pw + o * HP + ib * 8 + 4, make_float4(accr[rr][a4 * 8 + 4], accr[rr][a4 * 8 + 5],
+                                                         accr[rr][a4 * 8 + 6], accr[rr][a4 * 8 + 7]));
+          }
         }
       }
+#pragma unroll
+      for (int s = 0; s < (H + 31) / 32; ++s) {
+        const int col = lane + 32 * s;
+        if (col < H) pw[HP * HP + col] = bsum[s];
+      }
     }
+    __syncthreads();
+    {
+      const int fi = net.in_w[l], fo = net.out_w[l];
+      own_add(greg, tid, net.w_off[l], fo * fi, [&](int e) {
+        const int o = e / fi, i = e - o * fi;
+        float s = Part[o * HP + i];
 #pragma unroll
-    for (int s = 0; s < (H + 31) / 32; ++s) {
-      const int col = lane + 32 * s;
-      if (col < H) pw[HP * HP + col] = bsum[s];
+        for (int w = 1; w < kWpg; ++w) s += Part[w * (HP * HP + HP) + o * HP + i];
+        return s;
+      });
+      own_add(greg, tid, net.b_off[l], fo, [&](int o) {
+        float s = Part[HP * HP + o];
+#pragma unroll
+        for (int w = 1; w < kWpg; ++w) s += Part[w * (HP * HP + HP) + HP * HP + o];
+        return s;
+      });
     }
+    __syncthreads();
   }
-  __syncthreads();
-  {
-    const int fi = net.in_w[l], fo = net.out_w[l];
-    own_add(greg, tid, net.w_off[l], fo * fi, [&](int e) {
-      const int o = e / fi, i = e - o * fi;
-      float s = Part[o * HP + i];
-#pragma unroll
-      for (int w = 1; w < kWarps; ++w) s += Part[w * (HP * HP + HP) + o * HP + i];
-      return s;
-    });
-    own_add(greg, tid, net.b_off[l], fo, [&](int o) {
-      float s = Part[HP * HP + o];
-#pragma unroll
-      for (int w = 1; w < kWarps; ++w) s += Part[w * (HP * HP + HP) + HP * HP + o];
-      return s;
-    });
-  }
-  __syncthreads();
   // propagate: Xbar = W^T Abar etc.; through hidden l-1's activation
   if constexpr (l == 1) store_vec<H>(Gbuf + tid * SG, z0r);  // own row: z0 for the chunks
 #pragma unroll 1

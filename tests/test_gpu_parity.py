@@ -61,6 +61,8 @@ CASES = {
         *po.structured_mesh(2, 2, (-1.0, 1.0), (-1.0, 1.0)), n_test_1d=5, n_quad_1d=10,
         forcing="bump_f", boundary_g="bump_u", n_boundary=400, n_sensors=50, sensor_seed=7,
         sensor_field="bump_u", eps_source=1, scalars=(2.0,), layers=(2, 20, 20, 1), seed=42),
+    # the paper's gear variant: T = 16, Q = 25, [2,50,50,50,1] (CUDA-core step, H > 31)
+    "paper_gear_h50": lambda: gear_spec(n_test_1d=4, layers=(2, 50, 50, 50, 1), n_boundary=1200),
     # C4: circular domain, 1,024 skewed cells (per-cell bilinear Jacobians), b = (1, 0)
     "c4_disk_cd2d": lambda: _disk_spec(),
     "split_path_q400": lambda: po.ProblemSpec(
