@@ -334,16 +334,19 @@ __global__ void __maxnreg__(VPG_TC2_MAXNREG) tc2_step_kernel(const StepArgs a) {
 #pragma unroll
   for (int k = 0; k < 8; ++k) {
     const int i = 8 * wc + k;
-    wv[k] = (wl < NL && wo < H && i < H) ? P[net.w_off[wl + 1] + wo * H + i] : 0.f;
+    // narrower layers (out_w / in_w < H) are zero-padded: padded units get
+    // zero weights and biases, so they never reach the outputs
+    const int fo = wl < NL ? net.out_w[wl + 1] : 0, fi = wl < NL ? net.in_w[wl + 1] : 0;
+    wv[k] = (wo < fo && i < fi) ? P[net.w_off[wl + 1] + wo * fi + i] : 0.f;
   }
   for (int i = tid; i < 32; i += kNT) {
     float w0 = 0.f, w1 = 0.f, b = (i == H) ? kOneBias : 0.f, wd = 0.f;
-    if (i < H) {
+    if (i < net.out_w[0]) {
       w0 = P[net.w_off[0] + 2 * i];
       w1 = P[net.w_off[0] + 2 * i + 1];
       b = P[net.b_off[0] + i];
-      wd = P[net.w_off[D] + i];
     }
+    if (i < net.in_w[D]) wd = P[net.w_off[D] + i];
     sW0[4 * i] = w0;
     sW0[4 * i + 1] = w1;
     sW0[4 * i + 2] = b;
@@ -353,7 +356,7 @@ __global__ void __maxnreg__(VPG_TC2_MAXNREG) tc2_step_kernel(const StepArgs a) {
   if (tid == 0) sWd[32] = P[net.b_off[D]];
   for (int l = 1; l <= NL; ++l)
     for (int o = tid; o < 32; o += kNT)
-      sBias[(l - 1) * 32 + o] = o < H ? P[net.b_off[l] + o] : ((o == H) ? kOneBias : 0.f);
+      sBias[(l - 1) * 32 + o] = o < net.out_w[l] ? P[net.b_off[l] + o] : ((o == H) ? kOneBias : 0.f);
   // |W| into buffer A (free until the first tile) for the row / column sums
   float* sAbs = reinterpret_cast<float*>(bufA);  // [NL][32][33] (row stride 33: no bank conflicts)
   uint32_t* sNorm = sMax + kNW0;  // [0] w0x [1] w0y [2] wd
@@ -1355,9 +1358,10 @@ VPG_PRAGMA_UNROLL(VPG_TC2_CHUNK_UNROLL)
     const int fo = net.out_w[l], fi = net.in_w[l];
     for (int e = tid; e < fo * (fi + 1); e += kNT) {
       const int o = e / (fi + 1), i = e - o * (fi + 1);
+      const int c = i < fi ? i : H;  // the bias gradient is the constant unit's column
       float g = 0.f;
-      if (has)  // scr[row][col]: row = G part * 32 + o, col = X part * 32 + i
-        g = ((scr[o * 65 + i] + scr[o * 65 + 32 + i]) + scr[(32 + o) * 65 + i]) + scr[(32 + o) * 65 + 32 + i];
+      if (has)  // scr[row][col]: row = G part * 32 + o, col = X part * 32 + c
+        g = ((scr[o * 65 + c] + scr[o * 65 + 32 + c]) + scr[(32 + o) * 65 + c]) + scr[(32 + o) * 65 + 32 + c];
       const int idx = (i < fi) ? net.w_off[l] + o * fi + i : net.b_off[l] + o;
       a.grad_part[(size_t)idx * a.part_stride + blockIdx.x] = g;
     }
@@ -1375,10 +1379,12 @@ VPG_PRAGMA_UNROLL(VPG_TC2_CHUNK_UNROLL)
       wd += A[kAWd + j];
     }
     if (u < H) {
-      a.grad_part[(size_t)(net.w_off[0] + 2 * u) * a.part_stride + blockIdx.x] = w0x;
-      a.grad_part[(size_t)(net.w_off[0] + 2 * u + 1) * a.part_stride + blockIdx.x] = w0y;
-      a.grad_part[(size_t)(net.b_off[0] + u) * a.part_stride + blockIdx.x] = b0;
-      a.grad_part[(size_t)(net.w_off[D] + u) * a.part_stride + blockIdx.x] = wd;
+      if (u < net.out_w[0]) {
+        a.grad_part[(size_t)(net.w_off[0] + 2 * u) * a.part_stride + blockIdx.x] = w0x;
+        a.grad_part[(size_t)(net.w_off[0] + 2 * u + 1) * a.part_stride + blockIdx.x] = w0y;
+        a.grad_part[(size_t)(net.b_off[0] + u) * a.part_stride + blockIdx.x] = b0;
+      }
+      if (u < net.in_w[D]) a.grad_part[(size_t)(net.w_off[D] + u) * a.part_stride + blockIdx.x] = wd;
     } else {
       a.grad_part[(size_t)net.b_off[D] * a.part_stride + blockIdx.x] = wd;
     }

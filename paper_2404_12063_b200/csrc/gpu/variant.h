@@ -25,10 +25,13 @@ struct Variant {
   size_t (*smem)(int, int);
 };
 
-// (hidden width, hidden layers, output channels, activation 0 tanh / 1 sigmoid)
+// (hidden width, hidden layers, output channels, activation 0 tanh / 1 sigmoid);
+// a network uses the narrowest instantiated width >= its widest hidden layer,
+// narrower layers zero-padded exactly
 #define VPG_VARIANTS(X)                                                                          \
   X(30, 3, 1, 0) X(30, 3, 2, 0) X(20, 2, 1, 0) X(20, 2, 2, 0) X(50, 3, 1, 0) X(16, 1, 1, 0)      \
-  X(16, 1, 2, 0) X(16, 2, 1, 0) X(16, 1, 1, 1) X(16, 2, 1, 1) X(30, 3, 1, 1)
+  X(16, 1, 2, 0) X(16, 2, 1, 0) X(16, 1, 1, 1) X(16, 2, 1, 1) X(30, 3, 1, 1) X(30, 2, 1, 0)     \
+  X(30, 2, 1, 1) X(30, 1, 1, 0) X(30, 1, 1, 1)
 
 #define VPG_DECL(H, D, C, A) Variant variant_##H##_##D##_##C##_##A();
 VPG_VARIANTS(VPG_DECL)

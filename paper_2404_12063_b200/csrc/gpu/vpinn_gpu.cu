@@ -623,6 +623,11 @@ void configure(vpinn_gpu_ctx* c) {
     c->tc2 = c->tc && V.tc2 != nullptr && !(tck && std::atoi(tck) == 1) && c->Q >= 2 &&
              (size_t)(c->nt * round4(tile_rows * c->Q + 8) + vpg::t2::kTailFloats) * sizeof(float) <=
                  (size_t)vpg::t2::kBuf;
+    // the bf16-split kernel assumes every hidden layer exactly H wide; ragged
+    // widths go to tc2 (zero-padded exactly) or the CUDA-core step
+    bool uniform = c->net.in_w[c->net.n_layers - 1] == V.H;
+    for (int l = 0; l + 1 < c->net.n_layers; ++l) uniform = uniform && c->net.out_w[l] == V.H;
+    if (c->tc && !c->tc2 && !uniform) c->tc = false;
     if (c->tc && (std::getenv("VPINN_PHASE_CLOCK") && std::atoi(std::getenv("VPINN_PHASE_CLOCK")) != 0)) {
       c->phase_clk.alloc((size_t)vpg::kPhaseTiles * vpg::kPhaseMarks + 3 * 1024, c->stream);
       a.phase_clk = c->phase_clk.p;

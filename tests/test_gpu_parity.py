@@ -230,3 +230,50 @@ def test_fresh_contexts_are_bitwise_identical(name):
             ref = (parts, grad)
         else:
             assert np.array_equal(parts, ref[0]) and np.array_equal(grad, ref[1])
+
+
+EDGE = {
+    # one cell and the minimum of one boundary point (sample_boundary needs
+    # n >= 1, assembly.hpp:231-273)
+    "single_cell_one_boundary_point": lambda: po.ProblemSpec(
+        *po.structured_mesh(1, 1), n_test_1d=3, n_quad_1d=5, forcing="sin2pi_f", boundary_g="sin2pi_u",
+        n_boundary=1, layers=(2, 30, 30, 30, 1), seed=9),
+    # ragged hidden widths, zero-padded inside the tensor-core kernel
+    "ragged_widths_tc2": lambda: po.ProblemSpec(
+        *po.structured_mesh(3, 4), n_test_1d=4, n_quad_1d=6, forcing="sin2pi_f", boundary_g="sin2pi_u",
+        n_boundary=50, layers=(2, 7, 13, 5, 1), bx=0.4, seed=11),
+    # a cell count that leaves the last tile partly empty, boundary tile ragged
+    "partial_last_tile": lambda: po.ProblemSpec(
+        *po.structured_mesh(7, 3), n_test_1d=5, n_quad_1d=5, forcing="sin4pi_f", boundary_g="sin4pi_u",
+        n_boundary=131, layers=(2, 30, 30, 30, 1), seed=2),
+}
+
+
+@pytest.mark.parametrize("name", list(EDGE))
+def test_edge_shapes_match_oracle(name):
+    spec = EDGE[name]()
+    ob, g, p0 = make_pair(spec)
+    parts_o, _ = ob.loss_and_grad(p0)
+    parts_g, grad_g = g.loss_and_grad()
+    assert rel(parts_g[0], parts_o[0]) < 1e-5, (parts_g, parts_o)
+    assert (parts_g[2] == 0.0) == (parts_o[2] == 0.0)
+    grad_close(grad_g, spec, p0)
+    rep = g.train(20, lr0=1e-3)
+    ref = ob.train(p0, 20, lr0=1e-3, log_every=1)
+    r = np.abs(rep.records["total"] - ref["every_step"][:, 0]) / np.abs(ref["every_step"][:, 0])
+    assert r.max() < 1e-5
+
+
+@pytest.mark.parametrize("layers", [(2, 30, 13, 30, 1), (2, 13, 30, 30, 1), (2, 9, 20, 1), (2, 25, 25, 25, 1)])
+@pytest.mark.parametrize("sigmoid", [False, True])
+def test_ragged_hidden_widths_match_oracle(layers, sigmoid):
+    """Hidden layers narrower than the kernel width are zero-padded exactly
+    (tensor-core and CUDA-core steps; the padded units never reach the
+    outputs or the gradient)."""
+    spec = po.ProblemSpec(*po.structured_mesh(3, 4), n_test_1d=4, n_quad_1d=6, forcing="sin2pi_f",
+                          boundary_g="sin2pi_u", n_boundary=50, layers=layers, sigmoid=sigmoid, bx=0.4, seed=11)
+    ob, g, p0 = make_pair(spec)
+    parts_o, _ = ob.loss_and_grad(p0)
+    parts_g, grad_g = g.loss_and_grad()
+    assert rel(parts_g[0], parts_o[0]) < 1e-5, (g.step_kernel(), parts_g, parts_o)
+    grad_close(grad_g, spec, p0)
