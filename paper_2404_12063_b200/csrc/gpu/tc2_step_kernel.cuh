@@ -668,6 +668,11 @@ __global__ void __maxnreg__(VPG_TC2_MAXNREG) tc2_step_kernel(const StepArgs a) {
   };
 
   double acc_v = 0.0, acc_b = 0.0, acc_s = 0.0, acc_eg = 0.0;  // thread 0
+  // CONTRACT3: per-cell-slot loss sums kept by the thread that forms them
+  // (unit half 1, slot = cell within the tile) and combined across the CTA in
+  // a fixed order at the end.  Reading per-cell sums from buffer A after the
+  // tile's last barrier raced with the reverse's operand stores into it.
+  double cell_v = 0.0, cell_eg = 0.0;
   int bad = 0;
   const int n_pts_all = a.n_int + a.n_bnd + a.n_sen;
   struct TileGeo {
@@ -964,8 +969,10 @@ VPG_PRAGMA_UNROLL(VPG_TC2_CHUNK_UNROLL)
           s += rsqv[r];
           g += rgev[r];
         }
-        cellv[p] = s;
-        cellv[64 + p] = g;
+        if (MODE == kModeFused) {
+          cell_v += (double)(s * a.inv_nt);
+          cell_eg += (double)g;
+        }
       }
       mark(7);
 #else
@@ -1123,14 +1130,6 @@ VPG_PRAGMA_UNROLL(VPG_TC2_CHUNK_UNROLL)
     }
     load_xy(geo(tile + gridDim.x), nx, ny);  // next tile's points, in flight during the reverse
     __syncthreads();                          // adjoint rows + tile maxima visible; slab reads done
-#if VPG_TC2_CONTRACT3
-    if (MODE == kModeFused && interior && tid == 0) {
-      for (int k = 0; k < ncell; ++k) {
-        acc_v += (double)(cellv[k] * a.inv_nt);
-        acc_eg += (double)cellv[64 + k];
-      }
-    }
-#endif
     mark(8);
     const float ub = sEx[kUb * 128 + p], uxb = sEx[kUxb * 128 + p], uyb = sEx[kUyb * 128 + p];
 
@@ -1400,6 +1399,25 @@ VPG_PRAGMA_UNROLL(VPG_TC2_CHUNK_UNROLL)
   if constexpr (VPG_PHASE_CLOCK != 0)
     if (a.phase_clk != nullptr && tid == 0 && blockIdx.x < 1024)
       a.phase_clk[kPhaseTiles * kPhaseMarks + 3 * blockIdx.x + 1] = (long long)globaltimer();
+  {
+    double v = cell_v, g = cell_eg;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      v += __shfl_xor_sync(0xffffffffu, v, o);
+      g += __shfl_xor_sync(0xffffffffu, g, o);
+    }
+    __syncthreads();  // sRed is free
+    if (lane == 0) {
+      sRed[warp] = v;
+      sRed[8 + warp] = g;
+    }
+    __syncthreads();
+    if (tid == 0)
+      for (int w = 0; w < kNT / 32; ++w) {
+        acc_v += sRed[w];
+        acc_eg += sRed[8 + w];
+      }
+  }
   if (tid == 0) {
     double* lp = a.loss_part + (size_t)blockIdx.x * kLpWords;
     lp[kLpVar] = acc_v;

@@ -615,7 +615,7 @@ void configure(vpinn_gpu_ctx* c) {
     // tensor-core step: whole-tile slab in one of its operand buffers
     const char* tc_env = std::getenv("VPINN_TC");
     c->tc = V.tc != nullptr && !(tc_env && std::atoi(tc_env) == 0) && c->eps_source != VPINN_EPS_SPATIAL &&
-            tile_rows <= 128 && (size_t)c->nt * round4(tile_rows * c->Q + 8) * sizeof(float) <= (size_t)vpg::kTcBuf;
+            c->Q >= 2 && tile_rows <= 128 && (size_t)c->nt * round4(tile_rows * c->Q + 8) * sizeof(float) <= (size_t)vpg::kTcBuf;
     // the fp16-split two-CTA kernel (default) when the slab plus its
     // contraction scratch fit operand buffer A; VPINN_TC_KERNEL=1 selects the
     // bf16-split one-CTA kernel
@@ -797,7 +797,7 @@ void configure(vpinn_gpu_ctx* c) {
     ca.cells_per_tile = std::max(1, std::min(1024, 1024 / std::max(1, c->Q)));
     ca.cells_per_tile = std::max(1, std::min(ca.cells_per_tile, c->E));
     ca.n_tiles = c->E ? ceil_div(c->E, ca.cells_per_tile) : 0;
-    ca.pmax = ca.cells_per_tile * c->Q;
+    ca.pmax = round4(ca.cells_per_tile * c->Q);  // a stride: keeps the mbarriers after the vectors 8-byte aligned
     ca.nstage = 4;
     const size_t fixed = vpg::contract_smem_bytes(ca.pmax, 0, 0, ca.nstage);
     const size_t ring_budget = fixed < 200 * 1024 ? 200 * 1024 - fixed : 16 * 1024;
