@@ -41,3 +41,39 @@ def test_shape_grid_matches_oracle(pair):
             fails.append((mesh, layers, sig, conv, g.step_kernel(), lr, ge))
         g.close()
     assert not fails, fails
+
+
+@pytest.mark.parametrize("layers", NETS + [(2, 7, 13, 5, 1), (2, 50, 50, 50, 1)])
+@pytest.mark.parametrize("sig", [False, True])
+def test_evaluate_grid_matches_oracle(layers, sig):
+    """evaluate(order 0 / 1) at arbitrary points through whichever forward
+    kernel the context selects (tensor-core forward mode or CUDA cores)."""
+    if sig and (layers[-1] == 2 or layers[1] == 50):
+        pytest.skip("no sigmoid variant for this shape")
+    kw = dict(eps_source=2, bx=0.5, forcing="sinpi_vareps_f") if layers[-1] == 2 else {}
+    spec = po.ProblemSpec(*po.structured_mesh(2, 2), n_test_1d=3, n_quad_1d=4, boundary_g="sin2pi_u",
+                          n_boundary=20, layers=layers, sigmoid=sig, seed=8, **kw)
+    ob, g, p0 = make_pair(spec)
+    pts = np.random.default_rng(1).uniform(-1.5, 1.5, size=(777, 2))
+    for order in (0, 1):
+        ref = ob.evaluate(p0, pts, order)
+        got = g.forward(pts, order)
+        for k in range(1 + 2 * order):
+            assert np.abs(got[k] - ref[k]).max() <= 3e-5 * max(1.0, np.abs(ref[k]).max()), (order, k)
+        if layers[-1] == 2:
+            assert np.abs(got[3] - ref[3]).max() <= 3e-5 * max(1.0, np.abs(ref[3]).max())
+
+
+def test_ragged_training_with_schedule_and_plateau_matches_oracle():
+    """train() (trainer.hpp:275-382) on a ragged network through the tensor-core
+    step: exponential lr schedule, plateau stop, per-epoch loss within 1e-5."""
+    spec = po.ProblemSpec(*po.structured_mesh(3, 3), n_test_1d=3, n_quad_1d=5, forcing="sin2pi_f",
+                          boundary_g="sin2pi_u", n_boundary=60, layers=(2, 25, 12, 25, 1), bx=0.2, seed=4)
+    ob, g, p0 = make_pair(spec)
+    kw = dict(lr0=3e-3, lr_exponential=True, decay=0.9, every=7, loss_tol=0.2, plateau_window=6)
+    ref = ob.train(p0, 80, log_every=1, **kw)
+    rep = g.train(80, **kw)
+    assert "tc2" in g.step_kernel()
+    assert rep.steps_run == ref["steps_run"] and rep.stop_reason == ref["stop_reason"]
+    r = np.abs(rep.records["total"] - ref["every_step"][:, 0]) / np.abs(ref["every_step"][:, 0])
+    assert r.max() < 1e-5, r.max()
