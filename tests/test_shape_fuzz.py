@@ -77,3 +77,24 @@ def test_ragged_training_with_schedule_and_plateau_matches_oracle():
     assert rep.steps_run == ref["steps_run"] and rep.stop_reason == ref["stop_reason"]
     r = np.abs(rep.records["total"] - ref["every_step"][:, 0]) / np.abs(ref["every_step"][:, 0])
     assert r.max() < 1e-5, r.max()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("layers", [(2, 30, 30, 30, 1), (2, 16, 16, 16, 2), (2, 24, 11, 1)])
+def test_rank_partitions_sum_to_the_whole(world, layers):
+    """vpinn_gpu_create(rank, world) sub-contexts on one device (the multi-GPU
+    partition): their loss parts and gradients add up to the
+    single-rank ones; the per-epoch all-reduce of the device path is that sum."""
+    kw = dict(eps_source=2, bx=0.5, forcing="sinpi_vareps_f") if layers[-1] == 2 else dict(bx=0.3)
+    spec = po.ProblemSpec(*po.structured_mesh(5, 4), n_test_1d=4, n_quad_1d=5, boundary_g="sin2pi_u",
+                          n_boundary=41, n_sensors=9, sensor_field="sin2pi_u", layers=layers, seed=6, **kw)
+    _, g, _ = make_pair(spec)
+    whole, gw = g.loss_and_grad()
+    acc, gacc = np.zeros(4), np.zeros_like(gw)
+    for r in range(world):
+        _, gr, _ = make_pair(spec, rank=r, world_size=world)
+        pr, grr = gr.loss_and_grad()
+        acc += pr
+        gacc += grr
+    assert np.allclose(acc, whole, rtol=2e-6)
+    assert np.abs(gacc - gw).max() <= 2e-5 * np.abs(gw).max()
