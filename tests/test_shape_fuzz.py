@@ -98,3 +98,22 @@ def test_rank_partitions_sum_to_the_whole(world, layers):
         gacc += grr
     assert np.allclose(acc, whole, rtol=2e-6)
     assert np.abs(gacc - gw).max() <= 2e-5 * np.abs(gw).max()
+
+
+def test_single_rank_nccl_communicator_path():
+    """The NCCL plumbing of the multi-GPU path (dlopen'd libnccl, communicator
+    from a unique id, the per-epoch all-reduce inside the captured epoch graph)
+    exercised with a one-rank communicator: results equal the plain context."""
+    from paper_2404_12063_b200 import gpu as G
+    spec = po.ProblemSpec(*po.structured_mesh(4, 4), n_test_1d=3, n_quad_1d=5, forcing="sin2pi_f",
+                          boundary_g="sin2pi_u", n_boundary=40, layers=(2, 30, 30, 30, 1), seed=12)
+    _, g0, p0 = make_pair(spec)
+    _, g1, _ = make_pair(spec)
+    g1.attach_comm(G.nccl_unique_id(), 1, 0)
+    a, ga = g0.loss_and_grad()
+    b, gb = g1.loss_and_grad()
+    assert np.array_equal(a, b) and np.array_equal(ga, gb)
+    r0 = g0.train(15, lr0=1e-3)
+    r1 = g1.train(15, lr0=1e-3)
+    assert np.array_equal(r0.records["total"], r1.records["total"])
+    assert np.array_equal(g0.get_params(), g1.get_params())
