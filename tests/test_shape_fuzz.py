@@ -117,3 +117,19 @@ def test_single_rank_nccl_communicator_path():
     r1 = g1.train(15, lr0=1e-3)
     assert np.array_equal(r0.records["total"], r1.records["total"])
     assert np.array_equal(g0.get_params(), g1.get_params())
+
+
+@pytest.mark.parametrize("spg", [1, 7, 64])
+def test_stop_inside_a_multi_step_graph(spg):
+    """The epoch loop is replayed as CUDA graphs of steps_per_graph epochs; a
+    coefficient-tolerance stop inside a graph must end the run at the same
+    step as the reference, whatever the graph length (trainer.hpp:344-356)."""
+    spec = po.ProblemSpec(*po.structured_mesh(2, 2, (-1.0, 1.0), (-1.0, 1.0)), n_test_1d=5, n_quad_1d=10,
+                          forcing="bump_f", boundary_g="bump_u", n_boundary=400, n_sensors=50, sensor_seed=7,
+                          sensor_field="bump_u", eps_source=1, scalars=(2.0,), layers=(2, 20, 20, 1), seed=42)
+    ob, g, p0 = make_pair(spec)
+    ref = ob.train(p0, 60, lr0=1e-3, eps_abs_tol=1.6955, eps_actual=0.3)
+    rep = g.train(60, lr0=1e-3, eps_abs_tol=1.6955, eps_actual=0.3, steps_per_graph=spg)
+    assert rep.steps_run == ref["steps_run"] < 60 and rep.stop_reason == ref["stop_reason"] == 1
+    assert abs(rep.final_eps - ref["final_eps"]) < 1e-5
+    assert np.abs(g.get_params() - ref["params"]).max() < 1e-4
