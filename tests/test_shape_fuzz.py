@@ -133,3 +133,31 @@ def test_stop_inside_a_multi_step_graph(spg):
     assert rep.steps_run == ref["steps_run"] < 60 and rep.stop_reason == ref["stop_reason"] == 1
     assert abs(rep.final_eps - ref["final_eps"]) < 1e-5
     assert np.abs(g.get_params() - ref["params"]).max() < 1e-4
+
+
+def test_contexts_created_and_driven_from_two_threads():
+    """Distinct contexts may be driven from distinct host threads (the C-ABI
+    contract): concurrent creates share the staged-upload path and the block
+    cache, results equal a serial run."""
+    import threading
+    # 1,800 cells: each 4.5 MB premultiplier tensor goes through the staged uploader
+    spec = po.ProblemSpec(*po.structured_mesh(45, 40), n_test_1d=5, n_quad_1d=5, forcing="sin2pi_f",
+                          boundary_g="sin2pi_u", n_boundary=80, layers=(2, 30, 30, 30, 1), bx=0.2, seed=21)
+    ob = po.OracleProblem(spec, double=False)
+    _, g0, _ = make_pair(spec)
+    serial = g0.train(10, lr0=1e-3).records["total"].copy()
+    g0.close()
+    out = [None, None]
+
+    def run(i):
+        _, g, _ = make_pair(spec)
+        out[i] = g.train(10, lr0=1e-3).records["total"].copy()
+        g.close()
+
+    th = [threading.Thread(target=run, args=(i,)) for i in range(2)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert ob.n_int > 0
+    assert np.array_equal(out[0], serial) and np.array_equal(out[1], serial)
