@@ -20,14 +20,18 @@ MESHES = [(1, 1), (2, 3), (9, 7)]
 NETS = [(2, 30, 30, 30, 1), (2, 17, 1), (2, 24, 11, 1), (2, 16, 16, 16, 2)]
 
 
+@pytest.mark.parametrize("scalar", [False, True])
 @pytest.mark.parametrize("pair", PAIRS)
-def test_shape_grid_matches_oracle(pair):
+def test_shape_grid_matches_oracle(pair, scalar):
+    """scalar: a trainable coefficient and sensors on the one-output networks"""
     nt, nq = pair
     fails = []
     for mesh, layers, sig, conv in itertools.product(MESHES, NETS, [False, True], [False, True]):
         if layers[-1] == 2 and sig:
             continue  # no sigmoid two-output variant instantiated
         kw = dict(eps_source=2, bx=0.5) if layers[-1] == 2 else dict(bx=0.3 if conv else 0.0)
+        if scalar and layers[-1] == 1:
+            kw.update(eps_source=1, scalars=(1.3,), n_sensors=11, sensor_field="sin2pi_u")
         fx = "sinpi_vareps_f" if layers[-1] == 2 else "sin2pi_f"
         spec = po.ProblemSpec(*po.structured_mesh(*mesh), n_test_1d=nt, n_quad_1d=nq, forcing=fx,
                               boundary_g="sin2pi_u", n_boundary=37, layers=layers, sigmoid=sig, seed=5, **kw)

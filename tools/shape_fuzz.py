@@ -23,6 +23,8 @@ for (nt, nq), mesh, layers, sig, conv in itertools.product(
     if layers[-1] == 2 and sig:
         continue
     kw = dict(eps_source=2, bx=0.5) if layers[-1] == 2 else dict(bx=0.3 if conv else 0.0)
+    if os.environ.get("FUZZ_SCALAR") and layers[-1] == 1:  # trainable eps + sensors
+        kw.update(eps_source=1, scalars=(1.3,), n_sensors=11, sensor_field="sin2pi_u")
     fx = "sinpi_vareps_f" if layers[-1] == 2 else "sin2pi_f"
     spec = po.ProblemSpec(*po.structured_mesh(*mesh), n_test_1d=nt, n_quad_1d=nq, forcing=fx,
                           boundary_g="sin2pi_u", n_boundary=37, layers=layers, sigmoid=sig, seed=5, **kw)
