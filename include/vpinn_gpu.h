@@ -201,7 +201,11 @@ int vpinn_gpu_train(vpinn_gpu_ctx* ctx, const vpinn_gpu_train_spec* spec,
 
 /* Run n_steps further epochs of the current run with a constant learning
  * rate and NO host synchronisation (benchmark primitive; Adam state
- * persists across calls, reset by vpinn_gpu_train or vpinn_gpu_adam_reset). */
+ * persists across calls, reset by vpinn_gpu_train or vpinn_gpu_adam_reset).
+ * After vpinn_gpu_train the finished run's stop (budget, tolerance, plateau)
+ * is lifted and the epochs continue from its Adam state with no stop
+ * criteria; after a train() that aborted (non-finite values) run_steps
+ * returns VPINN_ERR_NUMERIC until vpinn_gpu_adam_reset. */
 int vpinn_gpu_adam_reset(vpinn_gpu_ctx* ctx);
 int vpinn_gpu_run_steps(vpinn_gpu_ctx* ctx, int n_steps, double lr);
 int vpinn_gpu_synchronize(vpinn_gpu_ctx* ctx);
@@ -244,7 +248,9 @@ int vpinn_gpu_download_tensor(vpinn_gpu_ctx* ctx, int which, float* out, int64_t
 int64_t vpinn_gpu_launch_count(const vpinn_gpu_ctx* ctx);
 /* Per-step share of the step kernels measured with CUDA events on the
  * context stream over reps run_steps: fused (or forward+contract+reverse),
- * reduce, adam — milliseconds per step each. */
+ * reduce, adam — milliseconds per step each.  The parameters, Adam moments
+ * and trainer state are saved before and restored after: profiling does not
+ * change the run. */
 int vpinn_gpu_profile_step(vpinn_gpu_ctx* ctx, int reps, double* ms_mlp, double* ms_reduce,
                            double* ms_adam);
 

@@ -8,6 +8,7 @@ reference hot path; see that header for the file:line map).
 from __future__ import annotations
 
 import ctypes as C
+import math
 import os
 import subprocess
 from dataclasses import dataclass, field as dc_field
@@ -33,6 +34,42 @@ def lib():
         _lib = C.CDLL(_LIB_PATH)
         _declare(_lib)
     return _lib
+
+
+_NATIVE_PATH = os.path.join(_HERE, "_build", "liboracle_native.so")
+_NATIVE_STAMP = _NATIVE_PATH + ".cpu"
+_native = None
+
+
+def _cpu_id() -> str:
+    try:
+        first = open("/proc/cpuinfo").read().split("\n\n")[0]
+    except OSError:
+        return "unknown"
+    keep = ("vendor_id", "cpu family", "model", "model name", "flags")
+    return "\n".join(ln for ln in first.splitlines() if ln.split(":")[0].strip() in keep)
+
+
+def lib_native():
+    """The TIMING build (Makefile target 'native': the reference's
+    -O3 -march=native flags + the Eigen-style float tanh).  Compiled on the
+    machine that runs it (the stamp holds that CPU's /proc/cpuinfo entry), so
+    -march=native never meets a different CPU.  Only bench.py's CPU-baseline
+    legs use it; every check runs on lib()."""
+    global _native
+    if _native is None:
+        cpu = _cpu_id()
+        stale = not os.path.exists(_NATIVE_PATH) or not os.path.exists(_NATIVE_STAMP) or \
+            open(_NATIVE_STAMP).read() != cpu
+        if stale:
+            if os.path.exists(_NATIVE_PATH):
+                os.remove(_NATIVE_PATH)
+            subprocess.run(["make", "-s", "-C", _HERE, "native"], check=True)
+            with open(_NATIVE_STAMP, "w") as fh:
+                fh.write(cpu)
+        _native = C.CDLL(_NATIVE_PATH)
+        _declare(_native)
+    return _native
 
 
 class OracleSpec(C.Structure):
@@ -147,6 +184,53 @@ def structured_mesh(nx, ny, x_range=(0.0, 1.0), y_range=(0.0, 1.0), skew=0.0, sk
     return nodes, cells
 
 
+def gear_msh41_text(n_r: int, n_t: int, teeth: int = 12, amp: float = 0.06, r_in: float = 0.35,
+                    r_out: float = 1.0) -> str:
+    """The reference fixture generator's gear recipe (proj/data/gen_fixtures.py
+    main(), lines 158-179: ring of n_t x n_r quads, radius modulated by
+    amp*sin(teeth*theta), inner and outer boundary lines) written as Gmsh 4.1
+    text the way its msh41() writer does (lines 40-75: one entity block per
+    dimension, '%.16g' coordinates).  Pure Python: the reference arm of
+    bench.py builds the C5 gear with it without loading the product library.
+    The SHA-256 at n_r=16, n_t=887 is pinned in tests/golden/gear_14192.json."""
+    out = ["$MeshFormat", "4.1 0 8", "$EndMeshFormat"]
+    nodes = []
+    for j in range(n_r + 1):
+        s = j / n_r
+        for i in range(n_t):
+            th = 2 * math.pi * i / n_t
+            r = r_in + s * (r_out + amp * math.sin(teeth * th) - r_in)
+            nodes.append((r * math.cos(th), r * math.sin(th)))
+    nid = lambda i, j: j * n_t + (i % n_t) + 1  # noqa: E731
+    n = len(nodes)
+    out += ["$Nodes", f"1 {n} 1 {n}", f"2 1 0 {n}"]
+    out += [str(i) for i in range(1, n + 1)]
+    out += [f"{x:.16g} {y:.16g} 0" for x, y in nodes]
+    out.append("$EndNodes")
+    lines = [(nid(i, 0), nid(i + 1, 0)) for i in range(n_t)]
+    lines += [(nid(i, n_r), nid(i + 1, n_r)) for i in range(n_t)]
+    quads = [(nid(i, j), nid(i, j + 1), nid(i + 1, j + 1), nid(i + 1, j)) for j in range(n_r) for i in range(n_t)]
+    total = len(lines) + len(quads)
+    out += ["$Elements", f"2 {total} 1 {total}", f"1 1 1 {len(lines)}"]
+    out += [f"{e + 1} {a} {b}" for e, (a, b) in enumerate(lines)]
+    out.append(f"2 1 3 {len(quads)}")
+    out += [f"{len(lines) + e + 1} {' '.join(map(str, q))}" for e, q in enumerate(quads)]
+    out.append("$EndElements")
+    return "\n".join(out) + "\n"
+
+
+def gear_mesh(n_r: int = 16, n_t: int = 887):
+    """(nodes [N][2] double, cells [E][4] 0-based) of gear_msh41_text, as the
+    Gmsh reader sees them (coordinates parsed back from the '%.16g' text)."""
+    lines = gear_msh41_text(n_r, n_t).split("\n")
+    n = (n_r + 1) * n_t
+    k = lines.index("$Nodes") + 3 + n  # past the block header and the node tags
+    nodes = np.array([[float(v) for v in ln.split()[:2]] for ln in lines[k:k + n]], dtype=np.float64)
+    k = lines.index("$Elements") + 3 + 2 * n_t + 1  # past the boundary-line block
+    cells = np.array([[int(v) - 1 for v in ln.split()[1:5]] for ln in lines[k:k + n_r * n_t]], dtype=np.int32)
+    return nodes, cells
+
+
 def init_params_f64(sizes: Sequence[int], seed: int):
     sz = np.ascontiguousarray(sizes, dtype=np.int32)
     n = sum(sizes[i + 1] * sizes[i] + sizes[i + 1] for i in range(len(sizes) - 1))
@@ -218,7 +302,9 @@ class ProblemSpec:
 
 
 class OracleProblem:
-    def __init__(self, spec: ProblemSpec, double: bool = False):
+    def __init__(self, spec: ProblemSpec, double: bool = False, timing_build: bool = False):
+        """timing_build: run on lib_native() (bench.py's CPU-baseline legs only)."""
+        self._L = lib_native() if timing_build else lib()
         self.spec = spec
         self.double = double
         self.dtype = np.float64 if double else np.float32
@@ -249,18 +335,18 @@ class OracleProblem:
         s.use_double = int(double)
         s.strong = int(spec.strong)
         self._spec_c = s
-        h = lib().vo_build(C.byref(s))
+        h = self._L.vo_build(C.byref(s))
         if not h:
-            raise OracleError(-1, lib().vo_last_error().decode())
+            raise OracleError(-1, self._L.vo_last_error().decode())
         self.h = h
         cnt = (C.c_longlong * 7)()
-        lib().vo_counts(h, cnt)
+        self._L.vo_counts(h, cnt)
         self.E, self.T, self.Q, self.n_int, self.n_bnd, self.n_sen, self.n_params = list(cnt)
 
     def __del__(self):
         h = getattr(self, "h", None)
         if h:
-            lib().vo_free(h)
+            self._L.vo_free(h)
             self.h = None
 
     @property
@@ -287,7 +373,7 @@ class OracleProblem:
             out = np.zeros(self.n_int)
         else:
             out = np.zeros((3, self.Q))
-        _check(lib().vo_get_array(self.h, idx, _p(out)))
+        _check(self._L.vo_get_array(self.h, idx, _p(out)))
         return out
 
     def init_params(self) -> np.ndarray:
@@ -297,7 +383,7 @@ class OracleProblem:
         par = np.ascontiguousarray(params, dtype=self.dtype)
         parts = (C.c_double * 4)()
         grad = np.zeros(self.n_params, dtype=self.dtype)
-        _check(lib().vo_loss_and_grad(self.h, _p(par), parts, _p(grad)))
+        _check(self._L.vo_loss_and_grad(self.h, _p(par), parts, _p(grad)))
         return np.array(list(parts)), grad
 
     def loss_and_grad_part(self, params, e0, e1, b0, b1, s0, s1):
@@ -305,7 +391,7 @@ class OracleProblem:
         par = np.ascontiguousarray(params, dtype=self.dtype)
         parts = (C.c_double * 4)()
         grad = np.zeros(self.n_params, dtype=self.dtype)
-        _check(lib().vo_loss_and_grad_part(self.h, _p(par), e0, e1, b0, b1, s0, s1, parts, _p(grad)))
+        _check(self._L.vo_loss_and_grad_part(self.h, _p(par), e0, e1, b0, b1, s0, s1, parts, _p(grad)))
         return np.array(list(parts)), grad
 
     def evaluate(self, params, points, order=1):
@@ -314,7 +400,7 @@ class OracleProblem:
         n = pts.shape[0]
         u, ux, uy = (np.zeros(n, dtype=self.dtype) for _ in range(3))
         eps = np.zeros(n, dtype=self.dtype) if self.spec.layers[-1] >= 2 else None
-        _check(lib().vo_evaluate(self.h, _p(par), _p(pts), n, order, _p(u),
+        _check(self._L.vo_evaluate(self.h, _p(par), _p(pts), n, order, _p(u),
                                  _p(ux) if order >= 1 else None, _p(uy) if order >= 1 else None,
                                  _p(eps) if eps is not None else None))
         return u, ux, uy, eps
@@ -325,7 +411,7 @@ class OracleProblem:
         pts = np.ascontiguousarray(points, dtype=np.float64).reshape(-1, 2)
         n = pts.shape[0]
         outs = [np.zeros(n, dtype=self.dtype) for _ in range(5)]
-        _check(lib().vo_evaluate2(self.h, _p(par), _p(pts), n, *[_p(o) for o in outs]))
+        _check(self._L.vo_evaluate2(self.h, _p(par), _p(pts), n, *[_p(o) for o in outs]))
         return tuple(outs)
 
     def var_loss(self, ux, uy, eps=None, scalars=(), weight=1.0, loop=False):
@@ -340,7 +426,7 @@ class OracleProblem:
         uyb = np.zeros(n, dtype=self.dtype)
         eb = np.zeros(n, dtype=self.dtype)
         sb = np.zeros(max(1, len(scalars)))
-        _check(lib().vo_var_loss(self.h, int(loop), _p(ux), _p(uy), None if e is None else _p(e),
+        _check(self._L.vo_var_loss(self.h, int(loop), _p(ux), _p(uy), None if e is None else _p(e),
                                  _p(sc), len(scalars), weight, C.byref(loss), _p(res), _p(uxb),
                                  _p(uyb), _p(eb), _p(sb)))
         return loss.value, res.reshape(self.E, self.T), uxb, uyb, eb, sb[: len(scalars)]
@@ -359,7 +445,7 @@ class OracleProblem:
         steps = C.c_longlong()
         reason = C.c_int()
         feps = C.c_double()
-        _check(lib().vo_train(self.h, _p(par), C.byref(ts), _p(hist), C.byref(steps),
+        _check(self._L.vo_train(self.h, _p(par), C.byref(ts), _p(hist), C.byref(steps),
                               C.byref(reason), C.byref(feps)))
         return {"params": par, "every_step": hist[: steps.value], "steps_run": steps.value,
                 "stop_reason": reason.value, "final_eps": feps.value}
@@ -367,5 +453,5 @@ class OracleProblem:
     def time_steps(self, params, lr=1e-3, warmup=1, reps=3):
         par = np.array(params, dtype=self.dtype)
         sec = np.zeros(reps)
-        _check(lib().vo_time_steps(self.h, _p(par), lr, warmup, reps, _p(sec)))
+        _check(self._L.vo_time_steps(self.h, _p(par), lr, warmup, reps, _p(sec)))
         return sec

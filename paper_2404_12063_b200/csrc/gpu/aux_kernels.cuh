@@ -255,6 +255,21 @@ __global__ void __launch_bounds__(kRAThreads) reduce_adam_kernel(const float* __
 
 __global__ void mark_start_kernel(TrainState* st) { st->t_prev = globaltimer(); }
 
+// vpinn_gpu_run_steps after a finished vpinn_gpu_train: the run's stop
+// (budget, coefficient tolerance, plateau) is lifted so further epochs run
+// with no stop criteria; Adam moments and the step count are kept.  An abort
+// (reason 3) stays stopped (the host refuses to resume it).
+__global__ void resume_kernel(TrainState* st) {
+  if (st->stopped && st->stop_reason != 3) {
+    st->stopped = 0;
+    st->stop_reason = 0;
+    st->iterations = 0x7fffffffffffffffLL;
+    st->has_eps_tol = 0;
+    st->has_loss_tol = 0;
+  }
+  st->t_prev = globaltimer();
+}
+
 // L2 flush, second half: after the flush buffer (> L2) has been written, read
 // it back so L2 holds clean lines of the flush buffer and no dirty write-back
 // of it is left to compete with the next timed kernel.

@@ -188,8 +188,12 @@ struct Stager {
   static constexpr int kBufs = 3;
   std::mutex mu;
   char* buf[kBufs] = {};
-  cudaEvent_t ev[16][kBufs] = {};  // per device
-  bool pending[16][kBufs] = {};
+  // one event per (device, buffer); last_dev[k] = the device whose copy out
+  // of buf[k] was enqueued last (-1: none).  The pinned buffers are shared by
+  // every device, so a reuse waits for the last DMA out of the buffer on
+  // whichever device issued it.
+  cudaEvent_t ev[16][kBufs] = {};
+  int last_dev[kBufs] = {-1, -1, -1};
   CopyPool pool;
   // false: caller falls back to a plain pageable copy
   bool upload(void* dst, const void* src, size_t bytes, cudaStream_t s) {
@@ -209,11 +213,11 @@ struct Stager {
     int k = 0;
     for (size_t off = 0; off < bytes; off += kChunk, k = (k + 1) % kBufs) {
       const size_t l = std::min(kChunk, bytes - off);
-      if (pending[dev][k]) CK(cudaEventSynchronize(ev[dev][k]));
+      if (last_dev[k] >= 0) CK(cudaEventSynchronize(ev[last_dev[k]][k]));
       pool.copy(buf[k], sp + off, l);
       CK(cudaMemcpyAsync(dp + off, buf[k], l, cudaMemcpyHostToDevice, s));
       CK(cudaEventRecord(ev[dev][k], s));
-      pending[dev][k] = true;
+      last_dev[k] = dev;
     }
     return true;
   }
@@ -439,6 +443,10 @@ struct vpinn_gpu_ctx {
   DBuf<vpg::StepRecord> rec;
   DBuf<float> lr_tab, c1_tab, c2_tab;
   int* h_flag = nullptr;  // pinned
+  // set by vpinn_gpu_train: the next run_steps lifts the finished run's stop
+  // (resume_kernel) or, after an abort, refuses until vpinn_gpu_adam_reset
+  bool resume_pending = false;
+  long long aborted_at = 0;
   // step configuration
   bool split = false;
   bool tc = false;  // tensor-core fused step
@@ -1061,6 +1069,8 @@ void reset_state(vpinn_gpu_ctx* c, long long iterations, const vpinn_gpu_train_s
     s.plateau_window = spec->plateau_window;
   }
   CK(cudaMemcpyAsync(c->st.p, &s, sizeof(s), cudaMemcpyHostToDevice, c->stream));
+  c->resume_pending = false;
+  c->aborted_at = 0;
   CK(cudaMemsetAsync(c->m.p, 0, sizeof(float) * c->n_params, c->stream));
   CK(cudaMemsetAsync(c->v.p, 0, sizeof(float) * c->n_params, c->stream));
   vpg::mark_start_kernel<<<1, 1, 0, c->stream>>>(c->st.p);
@@ -1483,7 +1493,15 @@ int vpinn_gpu_adam_reset(vpinn_gpu_ctx* c) {
 int vpinn_gpu_run_steps(vpinn_gpu_ctx* c, int n_steps, double lr) {
   return guarded([&] {
     set_dev(c);
+    if (c->aborted_at > 0)
+      throw Fail{VPINN_ERR_NUMERIC, "run_steps: the last train() aborted at step " + std::to_string(c->aborted_at) +
+                                        "; call vpinn_gpu_adam_reset first"};
     if (n_steps <= 0) return;
+    if (c->resume_pending) {
+      vpg::resume_kernel<<<1, 1, 0, c->stream>>>(c->st.p);
+      CK(cudaGetLastError());
+      c->resume_pending = false;
+    }
     const int chunk = std::min(n_steps, 64);
     cudaGraphExec_t g = graph_for(c, 1, chunk, lr, false, 0);
     int done = 0;
@@ -1588,6 +1606,8 @@ int vpinn_gpu_train(vpinn_gpu_ctx* c, const vpinn_gpu_train_spec* spec,
     CK(cudaMemcpyAsync(&s, c->st.p, sizeof(s), cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));
     const long long ran = s.step;
+    c->resume_pending = true;
+    c->aborted_at = s.stop_reason == 3 ? std::max(1LL, s.abort_step) : 0;
     if (records && ran > 0) {
       std::vector<vpg::StepRecord> r(ran);
       CK(cudaMemcpy(r.data(), c->rec.p, sizeof(vpg::StepRecord) * ran, cudaMemcpyDeviceToHost));
@@ -1957,6 +1977,21 @@ int vpinn_gpu_profile_step(vpinn_gpu_ctx* c, int reps, double* ms_mlp, double* m
                            double* ms_adam) {
   return guarded([&] {
     set_dev(c);
+    // a diagnostic: the live parameters, Adam moments and trainer state are
+    // saved here and restored at the end, so profiling leaves the run as it was
+    DBuf<float> save_p, save_m, save_v;
+    DBuf<vpg::TrainState> save_st;
+    save_p.alloc(c->n_params, c->stream);
+    save_m.alloc(c->n_params, c->stream);
+    save_v.alloc(c->n_params, c->stream);
+    save_st.alloc(1, c->stream);
+    const size_t pb = sizeof(float) * c->n_params;
+    CK(cudaMemcpyAsync(save_p.p, c->params.p, pb, cudaMemcpyDeviceToDevice, c->stream));
+    CK(cudaMemcpyAsync(save_m.p, c->m.p, pb, cudaMemcpyDeviceToDevice, c->stream));
+    CK(cudaMemcpyAsync(save_v.p, c->v.p, pb, cudaMemcpyDeviceToDevice, c->stream));
+    CK(cudaMemcpyAsync(save_st.p, c->st.p, sizeof(vpg::TrainState), cudaMemcpyDeviceToDevice, c->stream));
+    const bool resume_pending = c->resume_pending;
+    const long long aborted_at = c->aborted_at;
     reset_state(c, LLONG_MAX, nullptr);
     const vpg::AdamArgs aa = adam_args(c, false, 1e-4f, false, 0);
     cudaEvent_t ev[4];
@@ -2000,6 +2035,13 @@ int vpinn_gpu_profile_step(vpinn_gpu_ctx* c, int reps, double* ms_mlp, double* m
       }
     }
     for (auto& e : ev) cudaEventDestroy(e);
+    CK(cudaMemcpyAsync(c->params.p, save_p.p, pb, cudaMemcpyDeviceToDevice, c->stream));
+    CK(cudaMemcpyAsync(c->m.p, save_m.p, pb, cudaMemcpyDeviceToDevice, c->stream));
+    CK(cudaMemcpyAsync(c->v.p, save_v.p, pb, cudaMemcpyDeviceToDevice, c->stream));
+    CK(cudaMemcpyAsync(c->st.p, save_st.p, sizeof(vpg::TrainState), cudaMemcpyDeviceToDevice, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    c->resume_pending = resume_pending;
+    c->aborted_at = aborted_at;
     *ms_mlp = t[0] / reps;
     *ms_reduce = t[1] / reps;
     *ms_adam = t[2] / reps;

@@ -1,9 +1,11 @@
 // C-ABI of the host pipeline (include/vpinn_host.h) over the C++ API in
 // vp_gpu_trainer.hpp.
 #include <cstring>
+#include <map>
 #include <memory>
 #include <sstream>
 #include <string>
+#include <tuple>
 
 #include "vp_gpu_trainer.hpp"
 #include "vpinn_host.h"
@@ -16,7 +18,9 @@ struct vpinn_host_problem {
   vpinn::FullConfig cfg;
   vpinn::BuiltProblem bp;
   vpinn::QuadratureRule2D rule;
-  std::unique_ptr<vpinn::GpuView> view;
+  // one view per (device, rank, world), kept for the problem's lifetime: a
+  // vpinn_gpu_problem handed out earlier stays valid while the problem lives
+  std::map<std::tuple<int, int, int>, std::unique_ptr<vpinn::GpuView>> views;
 };
 
 namespace {
@@ -172,8 +176,9 @@ void vpinn_host_problem_counts(const vpinn_host_problem* p, int64_t* c) {
 int vpinn_host_problem_view(const vpinn_host_problem* p, int device, int rank, int world, vpinn_gpu_problem* view) {
   return guarded([&] {
     auto* mp = const_cast<vpinn_host_problem*>(p);
-    mp->view = vpinn::make_gpu_view(p->bp, device, rank, world);
-    *view = mp->view->p;
+    auto& slot = mp->views[std::make_tuple(device, rank, world)];
+    if (!slot) slot = vpinn::make_gpu_view(p->bp, device, rank, world);
+    *view = slot->p;
   });
 }
 

@@ -127,6 +127,41 @@ def test_matrix_free_contraction_matches_the_tensor_contraction(name):
     assert ms > 0 and nbytes > 0
 
 
+@pytest.mark.parametrize("name", ["gear_cd2d", "c1_square"])
+def test_matrix_free_contraction_matches_the_oracle(name):
+    """SURVEY 8f rank 3 against the CPU oracle's variational_loss_tensor
+    (losses.hpp:91-168) on the same cells and derivatives: loss 1e-5
+    relative, residuals / adjoints within 1e-5 of their max (fp32 rounding of
+    a different factorisation of the same sums)."""
+    from oracle import pyoracle as po
+    cfg, mk = CASES[name]
+    mesh = mk()
+    nodes, cells, _ = mesh.arrays()
+    pde = cfg["problem"].get("pde", {})
+    b = pde.get("b", [0.0, 0.0])
+    disc = cfg["discretization"]
+    spec = po.ProblemSpec(nodes=nodes, cells=cells, n_test_1d=disc["n_test_per_dim"],
+                          n_quad_1d=disc["n_quad_per_dim"], forcing=cfg["problem"]["forcing"],
+                          boundary_g=cfg["problem"]["boundary_g"],
+                          n_boundary=cfg["problem"]["n_boundary_points"], eps=pde.get("eps", 1.0),
+                          bx=b[0], by=b[1], layers=(2, 30, 30, 30, 1), seed=42)
+    ob = po.OracleProblem(spec, double=False)
+    dp = host.HostProblem(cfg, mesh=mesh, device_assembly=True)
+    g = dp.gpu()
+    rng = np.random.default_rng(5)
+    ni = dp.E * dp.Q
+    assert ni == ob.E * ob.Q
+    ux = rng.standard_normal(ni).astype(np.float32)
+    uy = rng.standard_normal(ni).astype(np.float32)
+    lo, ro, xbo, ybo, _, _ = ob.var_loss(ux, uy, None, (), weight=1.0)
+    lm, rm, xbm, ybm, _ = g.contract_matrix_free(ux, uy)
+    assert abs(lm - lo) / abs(lo) < 1e-5
+    for a, r in ((rm, ro), (xbm, xbo), (ybm, ybo)):
+        a = np.asarray(a).reshape(-1)
+        r = np.asarray(r).reshape(-1)
+        assert np.abs(a - r).max() / np.abs(r).max() < 1e-5
+
+
 def test_matrix_free_contraction_needs_the_geometry():
     cfg, mk = CASES["c1_square"]
     hp = host.HostProblem(cfg, mesh=mk())

@@ -22,7 +22,7 @@ def rel(a, b):
     return abs(a - b) / max(abs(b), 1e-30)
 
 
-def grad_close(g_gpu, spec, params, tol=2e-4):
+def grad_close(g_gpu, spec, params, tol=1e-5):
     """Gradient vs the fp64 oracle at the same (float) parameters."""
     o64 = po.OracleProblem(spec, double=True)
     _, g64 = o64.loss_and_grad(params.astype(np.float64))

@@ -85,6 +85,10 @@ def test_gear_14192_generator_reproduces_reference_recipe_bytes():
     g = host.Mesh.gear(16, 887)
     assert (g.n_elements, g.n_nodes) == (14192, 15079)
     assert g.health() == (0, 0)
+    # the oracle's pure-Python generator (bench.py's CPU legs) gives the same mesh
+    nodes, cells, _ = g.arrays()
+    pn, pcells = po.gear_mesh(16, 887)
+    assert np.array_equal(nodes.view(np.uint64), pn.view(np.uint64)) and np.array_equal(cells, pcells)
 
 
 def test_skewed_bench_mesh_and_disk_with_sensors_bit_exact():

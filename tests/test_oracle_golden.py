@@ -498,3 +498,41 @@ def test_strong_residual_is_mean_square_of_pointwise_operator():
     f = pb.array("strong_forcing")
     P = -0.7 * (uxx + uyy) + 0.6 * ux - 0.3 * uy - f
     assert abs(parts[1] - np.mean(P * P)) <= 1e-12 * parts[1]
+
+
+# ---------------------------------------------------------------------------
+# the committed parity fixtures (tests/golden/parity/*.npz) belong to this
+# oracle: the epoch-1 record of each fixture's 100-epoch run is the loss at
+# p0, and the fp32 gradient is the oracle's, bit for bit
+@pytest.mark.parametrize("case", ["c5_gear", "c5_inverse", "c5_paper", "c2_4096", "c3_t10_q40"])
+def test_parity_fixture_is_this_oracles_output(case):
+    import sys
+    sys.path.insert(0, os.path.join(os.path.dirname(__file__), "golden"))
+    import parity_cases as pc
+    fx = np.load(os.path.join(os.path.dirname(__file__), "golden", "parity", case + ".npz"))
+    ob = po.OracleProblem(pc.CASES[case](), double=False)
+    p0 = ob.init_params().astype(np.float32)
+    assert np.array_equal(p0.view(np.uint32), fx["p0"].view(np.uint32))
+    parts, grad = ob.loss_and_grad(p0)
+    assert np.array_equal(parts, fx["traj32"][0])
+    assert np.array_equal(grad.view(np.uint32), fx["grad32"].view(np.uint32))
+    assert fx["traj32"].shape == (pc.EPOCHS, 4) and np.all(np.isfinite(fx["traj32"]))
+    assert fx["traj32"][-1, 0] < fx["traj32"][0, 0]
+
+
+def test_pure_python_gear_is_the_reference_recipe(golden_dir):
+    """oracle/pyoracle.gear_mesh (used by bench.py's CPU legs so they load no
+    product code) writes the reference generator's bytes (SHA-256 pinned from
+    proj/data/gen_fixtures.py) and parses to the 14,192-cell C5 gear."""
+    import hashlib
+    import json
+    info = json.load(open(os.path.join(golden_dir, "gear_14192.json")))["gear_14192"]
+    text = po.gear_msh41_text(16, 887)
+    assert hashlib.sha256(text.encode()).hexdigest() == info["sha256"]
+    nodes, cells = po.gear_mesh(16, 887)
+    assert nodes.shape == (17 * 887, 2) and cells.shape == (14192, 4)
+    assert cells.min() == 0 and cells.max() == 17 * 887 - 1
+    small_n, small_c = po.gear_mesh(6, 96)
+    ref_n, ref_c = read_msh(os.path.join(golden_dir, "meshes", "gearlike_v41.msh"))
+    assert np.array_equal(small_n.view(np.uint64), ref_n.view(np.uint64))
+    assert np.array_equal(small_c, ref_c)

@@ -71,7 +71,7 @@ def test_strong_loss_and_gradient_match_oracle(name):
     spec = CASES[name]()
     ob, g, p0 = make_strong_pair(spec)
     assert "sf_step_kernel" in g.step_kernel()
-    parts_o, _ = ob.loss_and_grad(p0)
+    parts_o, go32 = ob.loss_and_grad(p0)
     parts_g, grad_g = g.loss_and_grad()
     assert rel(parts_g[0], parts_o[0]) < 1e-5, (parts_g, parts_o)
     for k in (1, 2, 3):
@@ -80,7 +80,8 @@ def test_strong_loss_and_gradient_match_oracle(name):
     o64 = po.OracleProblem(spec, double=True)
     _, g64 = o64.loss_and_grad(p0.astype(np.float64))
     err = np.abs(grad_g - g64).max() / np.abs(g64).max()
-    assert err < 2e-4, err
+    e32 = np.abs(go32 - g64).max() / np.abs(g64).max()
+    assert err < max(1e-5, 4.0 * e32), (err, e32)
 
 
 @pytest.mark.gpu

@@ -25,12 +25,15 @@ def test_strong_shape_grid_matches_oracle(layers):
                               boundary_g="sin2pi_u", n_boundary=23, layers=layers, sigmoid=sig, seed=3,
                               strong=True, **kw)
         ob, g, p0 = make_strong_pair(spec)
-        po_, _ = ob.loss_and_grad(p0)
+        po_, go32 = ob.loss_and_grad(p0)
         pg, gg = g.loss_and_grad()
         _, g64 = po.OracleProblem(spec, double=True).loss_and_grad(p0.astype(np.float64))
         lr = abs(pg[0] - po_[0]) / abs(po_[0])
         ge = np.abs(gg - g64).max() / max(np.abs(g64).max(), 1e-30)
-        if lr > 1e-5 or ge > 2e-4:
+        # gradient: 1e-5 of max|g| against fp64, or 4x the fp32 oracle's own
+        # distance from fp64 where that noise floor is higher (tiny problems)
+        e32 = np.abs(go32 - g64).max() / max(np.abs(g64).max(), 1e-30)
+        if lr > 1e-5 or ge > max(1e-5, 4.0 * e32):
             fails.append(((nt, nq), mesh, sig, inv, lr, ge))
         g.close()
     assert not fails, fails
