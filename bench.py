@@ -366,6 +366,7 @@ def main():
 
     aux = not args.no_sweep and rank == 0 and world == 1
     c4 = _aux(_c4_disk, device) if aux else None
+    c4i = _aux(_c4_disk_spatial_inverse, device) if aux else None
     c5i = _aux(_c5_inverse, mesh, device) if aux else None
     c5p = _aux(_c5_paper, mesh, device) if aux else None
     sweep = _aux(_sweep, device) if aux else None
@@ -411,6 +412,8 @@ def main():
         line["sweep_c3"] = sweep3
     if c4:
         line["c4_disk"] = c4
+    if c4i:
+        line["c4_disk_spatial_inverse"] = c4i
     if c5i:
         line["c5_inverse"] = c5i
     if c5p:
@@ -653,8 +656,12 @@ def _c5_inverse(mesh, device):
 
 
 def _c5_paper(mesh, device):
-    """The paper's gear variant: T=16 (4x4), Q=25, 6,096 boundary
-    points, [2,50,50,50,1]; H = 50 runs on the CUDA-core step kernel."""
+    """The paper's gear variant: T=16 (4x4), Q=25,
+    6,096 boundary points, [2,50,50,50,1]; H = 50 runs on the tensor-core
+    step in its 64-wide class (512 threads, 112-point tiles, one CTA per SM).
+    Algorithmic MLP work at H = 50 (SURVEY 8d formula): 2 (18 H^2 + 13 H) =
+    91,300 flop per interior point, 2 (6 H^2 + 7 H) = 30,700 per penalty
+    point, over the whole (L2-flushed) epoch time."""
     import copy
     from paper_2404_12063_b200 import host
     cfg = copy.deepcopy(GEAR_CFG)
@@ -663,8 +670,12 @@ def _c5_paper(mesh, device):
     cfg["network"]["layers"] = [2, 50, 50, 50, 1]
     hp = host.HostProblem(cfg, mesh=mesh)
     ms, kernel = _flushed_epoch_ms(hp, device)
+    flops = 91300.0 * hp.n_int + 30700.0 * (hp.n_bnd + hp.n_sen)
+    tflops = flops / (ms * 1e-3) / 1e12
+    peak = peaks()["bf16_tflops"] / 3.0
     return {"cells": hp.E, "n_test": hp.T, "n_quad": hp.Q, "boundary_points": hp.n_bnd, "layers": [2, 50, 50, 50, 1],
             "ms_per_epoch": ms, "kernel": kernel, "quad_pt_evals_per_s": hp.n_int / (ms * 1e-3),
+            "mlp_tflops_algorithmic": tflops, "frac_of_bf16_over_3": tflops / peak,
             "l2": "flushed between timed epochs"}
 
 
@@ -682,6 +693,27 @@ def _c4_disk(device):
     ms, kernel = _flushed_epoch_ms(hp, device)
     return {"cells": hp.E, "n_test": hp.T, "n_quad": hp.Q, "ms_per_epoch": ms, "kernel": kernel,
             "quad_pt_evals_per_s": hp.n_int / (ms * 1e-3), "l2": "flushed between timed epochs"}
+
+
+def _c4_disk_spatial_inverse(device):
+    """The paper's space-dependent-coefficient inverse on
+    C4's circular domain: 1,024 skewed cells, cd2d with b = (1, 0), the
+    network's second output channel eps(x, y) = softplus(y1)
+    (network.hpp:130-138, 477-483), 50 sensors; T = 25, Q = 100, constant
+    forcing (the reference's field set has no f = 10; the cost is the same).
+    Device-timed epochs, L2 flushed."""
+    from paper_2404_12063_b200 import host
+    cfg = {"problem": {"pde": {"type": "cd2d_variable_eps", "b": [1.0, 0.0]}, "forcing": "one",
+                       "boundary_g": "zero", "exact_solution": "sinpi_u", "n_boundary_points": 400,
+                       "sensors": {"count": 50, "seed": 7}},
+           "discretization": {"n_test_per_dim": 5, "n_quad_per_dim": 10},
+           "network": {"layers": [2, 30, 30, 30, 2]},
+           "training": {"learning_rate": 1e-3, "seed": 42, "precision": "single"}}
+    hp = host.HostProblem(cfg, mesh=host.Mesh.disk(32))
+    ms, kernel = _flushed_epoch_ms(hp, device)
+    return {"cells": hp.E, "n_test": hp.T, "n_quad": hp.Q, "sensors": hp.n_sen, "layers": [2, 30, 30, 30, 2],
+            "ms_per_epoch": ms, "kernel": kernel, "quad_pt_evals_per_s": hp.n_int / (ms * 1e-3),
+            "l2": "flushed between timed epochs"}
 
 
 def _sweep(device):

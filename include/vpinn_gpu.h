@@ -269,6 +269,20 @@ int vpinn_gpu_contract_matrix_free(vpinn_gpu_ctx* ctx, const float* du_dx, const
                                    float* du_dy_bar, double* scalar_bar);
 int vpinn_gpu_time_contract_matrix_free(vpinn_gpu_ctx* ctx, int reps, double* ms_per_launch, double* bytes);
 
+/* TEST HOOKS (parity tests of the alternate code paths; not for production
+ * use).  Process-wide, read by every later vpinn_gpu_create:
+ *   VPINN_HOOK_CUDA_CORE_STEP  the CUDA-core step kernel (step_kernel.cuh,
+ *                              the one serving shapes without a tensor-core
+ *                              variant) also for shapes the tensor-core step
+ *                              serves, so its parity is tested on them;
+ *   VPINN_HOOK_FORCE_SPILL     the tensor-core step spills its TMEM
+ *                              parameter-gradient accumulators every tile
+ *                              (the rare path of large scale drops).
+ * 0 restores the defaults. */
+#define VPINN_HOOK_CUDA_CORE_STEP 1
+#define VPINN_HOOK_FORCE_SPILL 2
+int vpinn_gpu_set_test_hooks(int flags);
+
 /* Device buffers released by destroyed contexts are cached per size for
  * the next context (no cudaMalloc / device-synchronizing cudaFree on
  * re-creation); this returns every cached block to the driver. */

@@ -109,6 +109,7 @@ def _declare(L):
         "vpinn_gpu_phase_clock": (i32, [vp, vp, i32]),
         "vpinn_gpu_assemble": (i32, [i32, i32, i32, i32, vp, vp, vp, vp, vp, vp]),
         "vpinn_gpu_release_cached_memory": (i32, []),
+        "vpinn_gpu_set_test_hooks": (i32, [i32]),
         "vpinn_gpu_contract_matrix_free": (i32, [vp, vp, vp, vp, C.c_float, pd, vp, vp, vp, vp]),
         "vpinn_gpu_time_contract_matrix_free": (i32, [vp, i32, pd, pd]),
         "vpinn_gpu_nccl_unique_id": (i32, [vp]),

@@ -3,6 +3,7 @@
 // the penalty kernel of the split path.
 #pragma once
 
+#include "contract_cells.cuh"
 #include "step_kernel.cuh"
 
 namespace vpg {
@@ -283,10 +284,27 @@ __global__ void flush_read_kernel(const int4* __restrict__ buf, size_t n16, int*
 }
 
 // ---------------------------------------------------------------------------
-// Standalone contraction (losses.hpp:91-168) over device-resident ux/uy/eps:
-// split path (Q > 128) and the HBM-roofline measurement.  256 threads; a
-// tile = whole cells with at most pmax points (or one cell); premultiplier
-// rows streamed through an NST-stage cp.async.bulk ring.
+// Standalone contraction (losses.hpp:91-168) over device-resident ux/uy/eps
+// for cells too large for a warp's ring (the split path, Q > 128: C3's
+// 40x40 rules, forward_sine.json, inverse_eps.json).  One pass over the
+// premultipliers with the work spread over (cell, row segment) ITEMS, not
+// cells, so a few big cells still fill every SM:
+//   contract_rows_kernel    persistent, 256 threads, two CTAs per SM; each
+//                           CTA streams its items' rows through an NST-stage
+//                           cp.async.bulk ring of R-row stages (~25 KB);
+//                           per stage every thread takes the quadrature
+//                           points q = t + 256 m of the R rows:
+//                             phase A  partial dot products G_x[r,:] s_x,
+//                                      G_y[r,:] s_y (, T[r,:] c) -> a fixed
+//                                      warp-then-CTA reduction -> r_j and the
+//                                      loss terms (losses.hpp:122-136)
+//                             phase B  adjoint columns sum_j G[j][q] rbar_j,
+//                                      accumulated in registers over the item
+//                           and writes the item's partial columns to part
+//   contract_rows_reduce    thread per (cell, q): the cell's item partials in
+//                           item order -> uxb / uyb / eb (losses.hpp:145-160)
+// Deterministic: fixed row / item / warp order everywhere, per-CTA loss words
+// from a static item assignment.
 struct ContractArgs {
   const float* tens[3];
   const float* forcing;
@@ -303,219 +321,288 @@ struct ContractArgs {
   int eps_source;
   float bx, by;
   float rscale, inv_nt;
-  int cells_per_tile, n_tiles;
-  int chunk_rows, stage_floats, tstride, nstage;
-  int pmax;
-  double* loss_part;  // [gridDim.x][kLpWords]
+  int rows;            // R: rows per ring stage (<= kCRowsMax)
+  int seg_rows;        // rows per item (a multiple of R, or the whole cell)
+  int items_per_cell;  // ceil(T / seg_rows)
+  int n_items;         // E * items_per_cell
+  int tstride;         // floats per tensor inside a stage (R * Q + 8, 16B multiple)
+  int stage_floats;    // nt * tstride
+  int nstage;          // ring depth (<= kCRMaxStages)
+  int qstride;         // floats per point vector in shared memory (Q rounded to 4)
+  float* part;         // [item][3][qstride] partial adjoint columns
+  double* loss_part;   // [gridDim.x][kLpWords]
   const int* stop_flag;
 };
 
 constexpr int kCThreads = 256;
+constexpr int kCRThreads = 512;  // contract_rows_kernel
+constexpr int kCRowsMax = 16;
+constexpr int kCQMax = 8192;  // points per cell this kernel serves
 
-__device__ __forceinline__ void c_issue(const ContractArgs& a, int cell0, int row0, int nrows,
-                                        float* stage, uint64_t* bar) {
-  const size_t grow0 = (size_t)cell0 * a.T + row0;
+// ring (nstage stages) | s_x, s_y, c | adjoint column accumulators (nt) | row scalars | barriers
+constexpr int kCRMaxStages = 6;
+__host__ __device__ constexpr size_t contract_rows_smem_bytes(int stage_floats, int qstride, int nt, int nstage) {
+  return sizeof(float) * ((size_t)nstage * stage_floats + (3 + (size_t)nt) * qstride + 3 * kCRowsMax +
+                          3 * (kCRThreads / 32)) +
+         sizeof(uint64_t) * kCRMaxStages + 64;
+}
+
+// rows [row0, row0 + nr) of cell k, nt tensors, into one ring stage
+__device__ __forceinline__ void cr_issue(const ContractArgs& a, int k, int row0, int nr, float* stage, uint64_t* bar) {
+  const size_t grow0 = (size_t)k * a.T + row0;
   uint32_t total = 0;
-  const char* src[3];
-  uint32_t n16[3];
-  for (int t = 0; t < a.nt; ++t) {
-    const char* s = reinterpret_cast<const char*>(a.tens[t] + grow0 * a.Q);
-    const char* al = reinterpret_cast<const char*>(reinterpret_cast<uintptr_t>(s) & ~uintptr_t(15));
-    const uint32_t pre = (uint32_t)(s - al);
-    n16[t] = (pre + (uint32_t)nrows * a.Q * 4u + 15u) & ~15u;
-    src[t] = al;
-    total += n16[t];
-  }
+  for (int t = 0; t < a.nt; ++t) total += seg_of(a.tens[t] + grow0 * a.Q, (size_t)nr * a.Q).bytes;
   fence_proxy_async();
   mbar_arrive_expect_tx(bar, total);
-  for (int t = 0; t < a.nt; ++t) bulk_g2s(stage + t * a.tstride, src[t], n16[t], bar);
+  for (int t = 0; t < a.nt; ++t) {
+    const Seg g = seg_of(a.tens[t] + grow0 * a.Q, (size_t)nr * a.Q);
+    bulk_g2s(stage + t * a.tstride, g.src, g.bytes, bar);
+  }
 }
 
-__device__ __forceinline__ const float* c_ptr(const ContractArgs& a, int cell0, int row0,
-                                              const float* stage, int t) {
-  const size_t grow0 = (size_t)cell0 * a.T + row0;
-  const uintptr_t s = reinterpret_cast<uintptr_t>(a.tens[t] + grow0 * a.Q);
-  return stage + t * a.tstride + ((s & 15u) >> 2);
+// this CTA's stage sequence: its contiguous item range [i0, i1) (consecutive
+// items mostly share a cell, so the cell's point vectors load rarely), each
+// item split into ceil(nrows / R) stages; a cursor walks it
+struct CrCursor {
+  int item, sub;
+};
+__device__ __forceinline__ void cr_geom(const ContractArgs& a, int item, int& k, int& r_begin, int& r_end) {
+  k = item / a.items_per_cell;
+  const int b = item - k * a.items_per_cell;
+  r_begin = b * a.seg_rows;
+  r_end = min(a.T, r_begin + a.seg_rows);
+}
+__device__ __forceinline__ void cr_next(const ContractArgs& a, CrCursor& c) {
+  int k, rb, re;
+  cr_geom(a, c.item, k, rb, re);
+  if (rb + (c.sub + 1) * a.rows < re) {
+    ++c.sub;
+  } else {
+    ++c.item;
+    c.sub = 0;
+  }
 }
 
-__host__ __device__ constexpr size_t contract_smem_bytes(int pmax, int chunk_rows, int stage_floats,
-                                                         int nstage) {
-  return sizeof(float) * ((size_t)9 * pmax + 4 * (size_t)((chunk_rows + 3) & ~3) + 2 * 1024 +
-                          (size_t)nstage * stage_floats) +
-         sizeof(uint64_t) * 8 + 64;
-}
-
-__global__ void __launch_bounds__(kCThreads) contract_kernel(const ContractArgs a) {
+__global__ void __launch_bounds__(kCRThreads, 1) contract_rows_kernel(const ContractArgs a) {
   if (a.stop_flag != nullptr && *a.stop_flag != 0) return;
+  constexpr int NW = kCRThreads / 32;
   extern __shared__ __align__(128) float cs[];
   float* ring = cs;
   float* sx = ring + (size_t)a.nstage * a.stage_floats;
-  float* sy = sx + a.pmax;
-  float* cv = sy + a.pmax;
-  float* vux = cv + a.pmax;
-  float* vuy = vux + a.pmax;
-  float* vep = vuy + a.pmax;
-  float* atx = vep + a.pmax;
-  float* aty = atx + a.pmax;
-  float* att = aty + a.pmax;
-  const int rows4 = (a.chunk_rows + 3) & ~3;
-  float* rbarv = att + a.pmax;
-  float* rsqv = rbarv + rows4;
-  float* rgev = rsqv + rows4;
-  float* cellsq = rgev + rows4 + rows4;  // 1024
-  float* cellge = cellsq + 1024;         // 1024
-  uint64_t* bars = reinterpret_cast<uint64_t*>(cellge + 1024);
-  const int tid = threadIdx.x;
+  float* sy = sx + a.qstride;
+  float* cv = sy + a.qstride;
+  float* acc = cv + a.qstride;                   // [nt][qstride] adjoint columns of the item
+  float* rbv = acc + (size_t)a.nt * a.qstride;   // [3][kCRowsMax] rbar, r^2, rbar (gx + gy)
+  float* segp = rbv + 3 * kCRowsMax;             // [row][segment][3] partial dots
+  uint64_t* bars = reinterpret_cast<uint64_t*>(segp + 3 * NW);
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const bool spatial = a.eps_source == 2;
+  const bool conv = a.nt == 3;
+  const float e_fixed = a.eps_source == 1 ? *a.e_param : a.e_fixed;
+  const int Q = a.Q;
+  const int i0 = (int)((long long)a.n_items * blockIdx.x / gridDim.x);
+  const int i1 = (int)((long long)a.n_items * (blockIdx.x + 1) / gridDim.x);
   if (tid == 0) {
     for (int s = 0; s < a.nstage; ++s) mbar_init(&bars[s], 1);
     fence_mbar_init();
   }
   __syncthreads();
-  uint32_t parity = 0u;  // bit s = phase parity of ring stage s
-  const bool spatial = a.eps_source == 2;
-  const bool conv = a.nt == 3;
-  const float e_fixed = a.eps_source == 1 ? *a.e_param : a.e_fixed;
-  double acc_v = 0.0, acc_eg = 0.0;
-  for (int tile = blockIdx.x; tile < a.n_tiles; tile += gridDim.x) {
-    const int cell0 = tile * a.cells_per_tile;
-    const int ncell = min(a.cells_per_tile, a.E - cell0);
-    const int np = ncell * a.Q;
-    const int nrows = ncell * a.T;
-    const int nchunks = (nrows + a.chunk_rows - 1) / a.chunk_rows;
-    if (tid == 0)
-      for (int c = 0; c < a.nstage && c < nchunks; ++c) {
-        const int r0 = c * a.chunk_rows;
-        c_issue(a, cell0, r0, min(a.chunk_rows, nrows - r0), ring + c * a.stage_floats, &bars[c]);
-      }
-    const size_t pb = (size_t)cell0 * a.Q;
-    for (int p = tid; p < np; p += kCThreads) {
-      const float ux = a.ux[pb + p], uy = a.uy[pb + p];
-      const float ep = spatial ? a.eps[pb + p] : 1.0f;
-      vux[p] = ux;
-      vuy[p] = uy;
-      vep[p] = ep;
-      sx[p] = spatial ? ep * ux : ux;
-      sy[p] = spatial ? ep * uy : uy;
-      cv[p] = a.bx * ux + a.by * uy;
-      atx[p] = 0.f;
-      aty[p] = 0.f;
-      att[p] = 0.f;
+  CrCursor pc{i0, 0};  // producer (thread 0)
+  if (tid == 0) {
+    for (int s = 0; s < a.nstage && pc.item < i1; ++s) {
+      int k, rb, re;
+      cr_geom(a, pc.item, k, rb, re);
+      const int r0 = rb + pc.sub * a.rows;
+      cr_issue(a, k, r0, min(a.rows, re - r0), ring + (size_t)s * a.stage_floats, &bars[s]);
+      cr_next(a, pc);
     }
-    for (int k = tid; k < ncell; k += kCThreads) {
-      cellsq[k] = 0.f;
-      cellge[k] = 0.f;
-    }
-    __syncthreads();
-    for (int c = 0; c < nchunks; ++c) {
-      const int st = c % a.nstage;
-      const int r0 = c * a.chunk_rows;
-      const int nr = min(a.chunk_rows, nrows - r0);
-      float* stage = ring + st * a.stage_floats;
-      mbar_wait(&bars[st], (parity >> st) & 1u);
-      parity ^= 1u << st;
-      const float* Gx = c_ptr(a, cell0, r0, stage, 0);
-      const float* Gy = c_ptr(a, cell0, r0, stage, 1);
-      const float* Tv = conv ? c_ptr(a, cell0, r0, stage, 2) : nullptr;
-      // row dot products, one WARP per row (lanes over q, fixed xor tree):
-      // the large cells this kernel serves (Q > 128) make a thread-serial
-      // dot of length Q the latency chain of the whole contraction
-      const int lane = tid & 31, wid = tid >> 5;
-      for (int r = wid; r < nr; r += kCThreads / 32) {
-        const int gr = r0 + r;
-        const int kk = gr / a.T;
-        const int j = gr - kk * a.T;
-        const float* xs = sx + kk * a.Q;
-        const float* ys = sy + kk * a.Q;
-        const float* gxr = Gx + (size_t)r * a.Q;
-        const float* gyr = Gy + (size_t)r * a.Q;
-        const float* cr = cv + kk * a.Q;
-        const float* tr = conv ? Tv + (size_t)r * a.Q : gxr;
-        float gx = 0.f, gy = 0.f, t = 0.f;
-        for (int q = lane; q < a.Q; q += 32) {
-          gx = fmaf(gxr[q], xs[q], gx);
-          gy = fmaf(gyr[q], ys[q], gy);
-          if (conv) t = fmaf(tr[q], cr[q], t);
+  }
+  double acc_v = 0.0, acc_eg = 0.0;  // thread 0
+  uint32_t parity = 0u;
+  int stage_i = 0, k_prev = -1;
+  for (CrCursor c{i0, 0}; c.item < i1;) {
+    int k, rb, re;
+    cr_geom(a, c.item, k, rb, re);
+    const int r0 = rb + c.sub * a.rows, nr = min(a.rows, re - r0);
+    if (c.sub == 0) {
+      const size_t pb = (size_t)k * Q;
+      for (int q = tid; q < Q; q += kCRThreads) {
+        if (k != k_prev) {  // the cell's point vectors (s_x, s_y, bx ux + by uy)
+          const float ux = a.ux[pb + q], uy = a.uy[pb + q];
+          const float ep = spatial ? a.eps[pb + q] : 1.0f;
+          sx[q] = spatial ? ep * ux : ux;
+          sy[q] = spatial ? ep * uy : uy;
+          cv[q] = a.bx * ux + a.by * uy;
         }
+        acc[q] = 0.f;
+        acc[a.qstride + q] = 0.f;
+        if (conv) acc[2 * a.qstride + q] = 0.f;
+      }
+      k_prev = k;
+      __syncthreads();
+    }
+    const int st = stage_i % a.nstage;
+    mbar_wait(&bars[st], (parity >> st) & 1u);
+    parity ^= 1u << st;
+    const float* stage = ring + (size_t)st * a.stage_floats;
+    const size_t grow0 = (size_t)k * a.T + r0;
+    const float* Gx = stage + pre_of(a.tens[0] + grow0 * Q);
+    const float* Gy = stage + a.tstride + pre_of(a.tens[1] + grow0 * Q);
+    const float* Tv = conv ? stage + 2 * a.tstride + pre_of(a.tens[2] + grow0 * Q) : Gx;
+    // phase A: warp task = (row, segment of the points); lanes over q with
+    // two interleaved chains per tensor; fixed xor tree, segments summed in
+    // order by one thread per row
+    const int nseg = max(1, NW / nr);
+    const int qseg = (Q + nseg - 1) / nseg;
+    for (int task = wid; task < nr * nseg; task += NW) {
+      const int r = task / nseg, sg = task - r * nseg;
+      const int qa = sg * qseg, qb = min(Q, qa + qseg);
+      const float* gxr = Gx + r * Q;
+      const float* gyr = Gy + r * Q;
+      const float* tr = Tv + r * Q;
+      float gx0 = 0.f, gy0 = 0.f, t0 = 0.f, gx1 = 0.f, gy1 = 0.f, t1 = 0.f;
+      int q = qa + lane;
+      for (; q + 32 < qb; q += 64) {
+        gx0 = fmaf(gxr[q], sx[q], gx0);
+        gy0 = fmaf(gyr[q], sy[q], gy0);
+        gx1 = fmaf(gxr[q + 32], sx[q + 32], gx1);
+        gy1 = fmaf(gyr[q + 32], sy[q + 32], gy1);
+        if (conv) {
+          t0 = fmaf(tr[q], cv[q], t0);
+          t1 = fmaf(tr[q + 32], cv[q + 32], t1);
+        }
+      }
+      if (q < qb) {
+        gx0 = fmaf(gxr[q], sx[q], gx0);
+        gy0 = fmaf(gyr[q], sy[q], gy0);
+        if (conv) t0 = fmaf(tr[q], cv[q], t0);
+      }
+      float gx = gx0 + gx1, gy = gy0 + gy1, t = t0 + t1;
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-          gx += __shfl_xor_sync(0xffffffffu, gx, o);
-          gy += __shfl_xor_sync(0xffffffffu, gy, o);
-          t += __shfl_xor_sync(0xffffffffu, t, o);
-        }
-        if (lane == 0) {
-          float res = spatial ? gx + gy : e_fixed * (gx + gy);
-          if (conv) res += t;
-          res -= a.forcing[(size_t)(cell0 + kk) * a.T + j];
-          if (a.res) a.res[(size_t)(cell0 + kk) * a.T + j] = res;
-          rsqv[r] = res * res;
-          const float rb = a.rscale * res;
-          rbarv[r] = rb;
-          rgev[r] = rb * (gx + gy);
-        }
+      for (int o = 16; o > 0; o >>= 1) {
+        gx += __shfl_xor_sync(0xffffffffu, gx, o);
+        gy += __shfl_xor_sync(0xffffffffu, gy, o);
+        if (conv) t += __shfl_xor_sync(0xffffffffu, t, o);
       }
-      __syncthreads();
-      // points of the cells touched by this chunk
-      const int k_lo = r0 / a.T, k_hi = (r0 + nr - 1) / a.T;
-      for (int p = k_lo * a.Q + tid; p < (k_hi + 1) * a.Q; p += kCThreads) {
-        const int kk = p / a.Q, q = p - kk * a.Q;
-        const int lo = max(r0, kk * a.T), hi = min(r0 + nr, (kk + 1) * a.T);
-        float tx = atx[p], ty = aty[p], tt = att[p];
-        for (int gr = lo; gr < hi; ++gr) {
-          const int r = gr - r0;
-          const float rb = rbarv[r];
-          tx = fmaf(Gx[(size_t)r * a.Q + q], rb, tx);
-          ty = fmaf(Gy[(size_t)r * a.Q + q], rb, ty);
-          if (conv) tt = fmaf(Tv[(size_t)r * a.Q + q], rb, tt);
-        }
-        atx[p] = tx;
-        aty[p] = ty;
-        att[p] = tt;
-      }
-      for (int kk = k_lo + tid; kk <= k_hi; kk += kCThreads) {
-        const int lo = max(r0, kk * a.T), hi = min(r0 + nr, (kk + 1) * a.T);
-        float s = cellsq[kk], g = cellge[kk];
-        for (int gr = lo; gr < hi; ++gr) {
-          s += rsqv[gr - r0];
-          g += rgev[gr - r0];
-        }
-        cellsq[kk] = s;
-        cellge[kk] = g;
-      }
-      __syncthreads();
-      if (tid == 0 && c + a.nstage < nchunks) {
-        const int r2 = (c + a.nstage) * a.chunk_rows;
-        c_issue(a, cell0, r2, min(a.chunk_rows, nrows - r2), stage, &bars[st]);
+      if (lane == 0) {
+        segp[3 * task + 0] = gx;
+        segp[3 * task + 1] = gy;
+        segp[3 * task + 2] = t;
       }
     }
-    for (int p = tid; p < np; p += kCThreads) {
-      float ox, oy;
-      if (spatial) {
-        ox = vep[p] * atx[p];
-        oy = vep[p] * aty[p];
-        if (a.eb) a.eb[pb + p] = vux[p] * atx[p] + vuy[p] * aty[p];
-      } else {
-        ox = e_fixed * atx[p];
-        oy = e_fixed * aty[p];
-      }
-      if (conv) {
-        ox = fmaf(a.bx, att[p], ox);
-        oy = fmaf(a.by, att[p], oy);
-      }
-      a.uxb[pb + p] = ox;
-      a.uyb[pb + p] = oy;
-    }
-    if (tid == 0)
-      for (int k = 0; k < ncell; ++k) {
-        acc_v += (double)(cellsq[k] * a.inv_nt);
-        acc_eg += (double)cellge[k];
-      }
     __syncthreads();
+    if (tid < nr) {  // one thread per row: segments in order -> r_j
+      const int r = tid;
+      float gx = 0.f, gy = 0.f, t = 0.f;
+      for (int sg = 0; sg < nseg; ++sg) {
+        gx += segp[3 * (r * nseg + sg) + 0];
+        gy += segp[3 * (r * nseg + sg) + 1];
+        t += segp[3 * (r * nseg + sg) + 2];
+      }
+      const int j = r0 + r;
+      float res = spatial ? gx + gy : e_fixed * (gx + gy);
+      if (conv) res += t;
+      res -= a.forcing[(size_t)k * a.T + j];
+      if (a.res) a.res[(size_t)k * a.T + j] = res;
+      const float rb2 = a.rscale * res;
+      rbv[r] = rb2;
+      rbv[kCRowsMax + r] = res * res;
+      rbv[2 * kCRowsMax + r] = rb2 * (gx + gy);
+    }
+    __syncthreads();
+    if (tid == 0)
+      for (int r = 0; r < nr; ++r) {
+        acc_v += (double)(rbv[kCRowsMax + r] * a.inv_nt);
+        acc_eg += (double)rbv[2 * kCRowsMax + r];
+      }
+    // phase B: thread per point, the item's adjoint columns (even / odd rows
+    // as two chains, joined in a fixed order)
+    for (int q = tid; q < Q; q += kCRThreads) {
+      float tx0 = acc[q], ty0 = acc[a.qstride + q], tt0 = conv ? acc[2 * a.qstride + q] : 0.f;
+      float tx1 = 0.f, ty1 = 0.f, tt1 = 0.f;
+      int r = 0;
+      for (; r + 1 < nr; r += 2) {
+        const float ra = rbv[r], rc = rbv[r + 1];
+        tx0 = fmaf(Gx[r * Q + q], ra, tx0);
+        ty0 = fmaf(Gy[r * Q + q], ra, ty0);
+        tx1 = fmaf(Gx[(r + 1) * Q + q], rc, tx1);
+        ty1 = fmaf(Gy[(r + 1) * Q + q], rc, ty1);
+        if (conv) {
+          tt0 = fmaf(Tv[r * Q + q], ra, tt0);
+          tt1 = fmaf(Tv[(r + 1) * Q + q], rc, tt1);
+        }
+      }
+      if (r < nr) {
+        const float ra = rbv[r];
+        tx0 = fmaf(Gx[r * Q + q], ra, tx0);
+        ty0 = fmaf(Gy[r * Q + q], ra, ty0);
+        if (conv) tt0 = fmaf(Tv[r * Q + q], ra, tt0);
+      }
+      acc[q] = tx0 + tx1;
+      acc[a.qstride + q] = ty0 + ty1;
+      if (conv) acc[2 * a.qstride + q] = tt0 + tt1;
+    }
+    __syncthreads();  // the stage and the row scalars are consumed
+    if (tid == 0 && pc.item < i1) {
+      int pk, prb, pre;
+      cr_geom(a, pc.item, pk, prb, pre);
+      const int pr0 = prb + pc.sub * a.rows;
+      cr_issue(a, pk, pr0, min(a.rows, pre - pr0), ring + (size_t)st * a.stage_floats, &bars[st]);
+      cr_next(a, pc);
+    }
+    ++stage_i;
+    const int item = c.item;
+    const bool last_sub = r0 + nr >= re;
+    cr_next(a, c);
+    if (last_sub) {  // the item's partial columns (each thread its own points)
+      float* pp = a.part + (size_t)item * 3 * a.qstride;
+      for (int q = tid; q < Q; q += kCRThreads) {
+        pp[q] = acc[q];
+        pp[a.qstride + q] = acc[a.qstride + q];
+        if (conv) pp[2 * a.qstride + q] = acc[2 * a.qstride + q];
+      }
+    }
   }
   if (tid == 0) {
     double* lp = a.loss_part + (size_t)blockIdx.x * kLpWords;
     for (int w = 0; w < kLpWords; ++w) lp[w] = 0.0;
     lp[kLpVar] = acc_v;
     lp[kLpEpsGrad] = acc_eg;
+  }
+}
+
+// thread per (cell, q): the cell's item partials in item order -> adjoints
+__global__ void contract_rows_reduce_kernel(const ContractArgs a) {
+  if (a.stop_flag != nullptr && *a.stop_flag != 0) return;
+  const size_t n = (size_t)a.E * a.Q;
+  const bool spatial = a.eps_source == 2;
+  const bool conv = a.nt == 3;
+  const float e_fixed = a.eps_source == 1 ? *a.e_param : a.e_fixed;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+    const int k = (int)(i / a.Q), q = (int)(i - (size_t)k * a.Q);
+    const float* pp = a.part + (size_t)k * a.items_per_cell * 3 * a.qstride + q;
+    float tx = 0.f, ty = 0.f, tt = 0.f;
+    for (int b = 0; b < a.items_per_cell; ++b, pp += 3 * a.qstride) {
+      tx += pp[0];
+      ty += pp[a.qstride];
+      if (conv) tt += pp[2 * a.qstride];
+    }
+    float ox, oy;
+    if (spatial) {
+      const float ep = a.eps[i];
+      ox = ep * tx;
+      oy = ep * ty;
+      if (a.eb) a.eb[i] = a.ux[i] * tx + a.uy[i] * ty;
+    } else {
+      ox = e_fixed * tx;
+      oy = e_fixed * ty;
+    }
+    if (conv) {
+      ox = fmaf(a.bx, tt, ox);
+      oy = fmaf(a.by, tt, oy);
+    }
+    a.uxb[i] = ox;
+    a.uyb[i] = oy;
   }
 }
 

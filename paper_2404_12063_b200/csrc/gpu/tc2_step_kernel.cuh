@@ -1,15 +1,26 @@
-// Tensor-core FastVPINNs training step, fp16 two-part split, two CTAs per SM.
+// Tensor-core FastVPINNs training step, fp16 two-part split.
 //
-// Same per-tile semantics as tc_step_kernel.cuh / step_kernel<..., kModeFused>:
-// forward with x/y tangents (network.hpp:204-282), the Algorithm-3 contraction
-// (losses.hpp:91-168) or the penalty terms (losses.hpp:406-415), and the
-// reverse sweep (network.hpp:287-372), every hidden->hidden GEMM on tcgen05:
-//   forward      D_s[p][o] = X_s[p][:] . W[o][:]        M = 128 points, N = 32, K = 32
-//   propagation  D_s[p][i] = G_s[p][:] . W[:][i]        M = 128 points, N = 32, K = 32 (B MN-major)
+// Per-tile semantics: forward with x/y tangents (network.hpp:204-282), the
+// Algorithm-3 contraction (losses.hpp:91-168) or the penalty terms
+// (losses.hpp:406-415), and the reverse sweep (network.hpp:287-372), every
+// hidden->hidden GEMM on tcgen05 (s = value / x-tangent / y-tangent stream):
+//   forward      D_s[p][o] = X_s[p][:] . W[o][:]        M = 128 points, N = HP, K = HP
+//   propagation  D_s[p][i] = G_s[p][:] . W[:][i]        M = 128 points, N = HP, K = HP (B MN-major)
 //   param grad   Wbar[o][i] = sum_{s,p} G_s[p][o] X_s[p][i]
-//                                                      M = 128 (G h | l | -), N = 64 (X h | l),
-//                                                      K = 3 streams x 128 points
-// (s = value / x-tangent / y-tangent stream).
+//                                                      M = 2 HP (G h | l), N = 2 HP (X h | l),
+//                                                      K = 3 streams x MP points
+//
+// Width classes.  Hidden units (plus the constant-one bias unit at index H)
+// are padded to HP = 32 NB, NB = 1 (H <= 31) or 2 (H <= 63, the paper's
+// [2,50,50,50,1] gear network); every operand tile is [MP][32] fp16 in the
+// 64-byte swizzle (tc_utils.cuh), a width of 64 is two such column blocks.
+//   NB = 1: 256 threads, MP = 128 points per tile, 113 KB of shared memory
+//           and 256 TMEM columns -> two CTAs per SM;
+//   NB = 2: 512 threads, MP = 112 points per tile (the operand buffers of
+//           128 points would not fit next to the weights), ~212 KB and all
+//           512 TMEM columns -> one CTA per SM.  The point GEMMs still run
+//           M = 128: rows MP..127 read whatever follows the tile and their
+//           accumulator lanes are never read.
 //
 // Precision.  Every operand is scaled by a power of two and split into two
 // fp16 parts (tc_utils.cuh st_split8_ho): 22 significant bits, three products
@@ -25,50 +36,21 @@
 // A loose bound costs nothing measurable: fp16 keeps 2^-24 absolute spacing
 // below 2^-14, i.e. ~2^-38 of the bound.  The parameter-gradient GEMM sums
 // three streams with different scales, so the G scales are chosen to make
-// S_G,s * S_X,s one common power of two P per tile; its TMEM accumulator is
-// read out and unscaled every tile (per-CTA fp32 scratch in global memory).
-// All scale factors are folded into per-layer / per-tile constants.
+// S_G,s * S_X,s one common power of two per tile; the accumulator stays in
+// TMEM across the CTA's tiles (scale-input-d when a tile needs a smaller
+// product scale, a per-CTA fp32 spill for drops beyond 2^15).
 //
-// Shape: 256 threads (8 warps): thread t owns point p = t % 128 (its TMEM
-// lane) and hidden units [16 (t / 128), +16), processed in chunks of 8.
-// Every unit runs the same branch-free code: the constant-one (bias) column H
-// is a unit with zero weights and bias 20 (act(20) == 1 exactly, act' == 0),
-// padding units have zero weights.  ~112 KB shared memory and 256 TMEM
-// columns per CTA, so TWO CTAs share an SM and one CTA's MMA / barrier / TMA
-// waits are filled by the other's elementwise work.  Hidden layers D in
-// {2, 3}, H <= 31, one output channel.  The slab (the tile's premultipliers,
-// cp.async.bulk) aliases operand buffer A.
+// Shape: thread t owns point p = t % 128 (its TMEM lane) and hidden units
+// [16 g, +16), g = t / 128, processed in chunks of 8.  Every unit runs the
+// same branch-free code: the constant-one (bias) column H is a unit with zero
+// weights and bias 20 (act(20) == 1 exactly, act' == 0), padding units have
+// zero weights.  Hidden layers D in {2, 3}, one output channel.  The slab (the
+// tile's premultipliers, cp.async.bulk) aliases operand buffer A.
 #pragma once
 
 #include "step_kernel.cuh"
 #include "tc_utils.cuh"
 
-#ifndef VPG_TC2_WARP_WAITS
-#define VPG_TC2_WARP_WAITS 1  // MMA completion: per-warp mbarrier polls (1) or one warp + CTA barrier (0)
-#endif
-#ifndef VPG_TC2_ISSUE_WARPS
-#define VPG_TC2_ISSUE_WARPS 3  // warps issuing the point GEMMs (1 or 3); the next warp issues the param GEMM
-#endif
-#ifndef VPG_TC2_PARAM_M64
-#define VPG_TC2_PARAM_M64 1  // parameter-gradient GEMM with M = 64 (G parts h | l only)
-#endif
-#ifndef VPG_TC2_Z1_CACHE
-#define VPG_TC2_Z1_CACHE 1  // hidden-1 z kept in TMEM (needs the M = 64 shared accumulator columns)
-#endif
-#ifndef VPG_TC2_CONTRACT3
-#define VPG_TC2_CONTRACT3 1  // one thread per row / point runs all three tensors (fewer barriers)
-#endif
-#define VPG_STR_(x) #x
-#define VPG_PRAGMA_UNROLL(n) _Pragma(VPG_STR_(unroll n))
-#ifndef VPG_TC2_ISSUE_UNROLL
-#define VPG_TC2_ISSUE_UNROLL 1  // (A/B: 3 is 3% slower, I-cache) MMA issue loops over streams: 3 = unrolled (constant offsets), 1 = rolled
-#endif
-#ifndef VPG_TC2_CHUNK_UNROLL
-#define VPG_TC2_CHUNK_UNROLL 1  // (A/B: 2 is 4% slower, I-cache) unroll of the two 8-unit chunk loops (1 or 2; code size vs ILP)
-#endif
-#ifndef VPG_TC2_MAXNREG
-#define VPG_TC2_MAXNREG 120  // two 256-thread CTAs per SM need <= 128
-#endif
 #ifndef VPG_PHASE_CLOCK
 #define VPG_PHASE_CLOCK 0  // build with -DVPG_PHASE_CLOCK=1 for tools/phase_clock.py
 #endif
@@ -76,28 +58,32 @@
 namespace vpg {
 namespace t2 {
 
-constexpr int kNT = 256;
-constexpr int kPart = 8192;           // [128][32] fp16 tile
-constexpr int kStream = 2 * kPart;    // h | l parts of one stream
-constexpr int kBuf = 3 * kStream;     // 3 streams (48 KB)
-constexpr int kWBytes = 4096;         // [64][32] fp16: W h rows 0..31 | l rows 32..63
-constexpr uint32_t kCols = 256;       // TMEM columns per CTA
-constexpr int kDCols = 32;            // stream accumulator columns
-// TMEM columns: 0..95 stream accumulators; kG0: parameter-gradient
-// accumulators (M = 64: layer l in lanes 16 (l - 1) .. + 15 of every lane
-// quarter, both layers in the same 64 columns; M = 128: 64 columns per
-// layer); kZ0: the last hidden layer's z; kZ1: the hidden-1 z (forward ->
-// reverse, so X_1 is rebuilt without the activation)
-constexpr int kG0 = 96;
-constexpr int kZ0 = 224;
-constexpr int kZ1 = 192;
-constexpr int kZ2 = 160;  // hidden-2 z (D == 3), forward -> reverse
-constexpr int kScratchPerLayer = 64 * 64;  // global fp32 [col 64][lane 64] per CTA and MMA layer
+// per width class (H = the instantiated hidden width)
+template <int H>
+struct Cfg {
+  static constexpr int NB = (H + 1 + 31) / 32;  // 32-unit column blocks (bias unit included)
+  static_assert(NB == 1 || NB == 2, "tc2 step: hidden width <= 63");
+  static constexpr int HP = 32 * NB;
+  static constexpr int NG = 2 * NB;              // unit groups of 16
+  static constexpr int NT = 128 * NG;            // threads
+  static constexpr int MP = NB == 1 ? 128 : 112;  // points per tile
+  static constexpr int kPart = MP * 64;          // [MP][32] fp16 tile
+  static constexpr int kStream = 2 * NB * kPart;  // tiles (part, block): part h blocks | part l blocks
+  static constexpr int kBuf = 3 * kStream;       // 3 streams
+  static constexpr int kWTile = 2 * HP * 64;     // W of one MMA layer and input block: h rows | l rows
+  static constexpr int kWL = NB * kWTile;        // W of one MMA layer
+  static constexpr uint32_t kCols = NB == 1 ? 256u : 512u;  // TMEM columns per CTA
+  static constexpr bool kZCache = NB == 1;       // hidden-1 / hidden-2 z kept in TMEM
+  static constexpr int kScratch = 4 * HP * HP;   // per-CTA fp32 spill [2HP][2HP] per MMA layer
+  static constexpr int kMaxReg = NB == 1 ? 120 : 128;
+};
+
 constexpr int kTailFloats = 8 * 128;  // contraction scratch after the slab in buffer A
 constexpr float kOneBias = 20.0f;     // bias of the constant-one unit: act(20) == 1.0f
 
-// exchange rows ([row][128] floats); the output-layer partials of unit half 1
-// (u, ux, uy) alias the adjoint rows, which are written only later
+// exchange rows ([row][128] floats).  The output-layer partials of unit
+// group 1 (u, ux, uy) alias the adjoint rows, which are written only later;
+// groups 2, 3 (NB = 2) have their own rows after kRows.
 enum : int { kX = 0, kY, kU, kUx, kUy, kUb, kUxb, kUyb, kRows };
 constexpr int kPu = kUb;
 
@@ -120,27 +106,41 @@ enum : int {
 // integer exponents (ints in S_SCI): kW[2], kXv[2], kXt[2]
 enum : int { kSiW = 0, kSiXv = 2, kSiXt = 4, kSiN = 6 };
 
-template <int D>
+template <int H, int D>
 struct Lay {
+  using CF = Cfg<H>;
   static constexpr int NL = D - 1;
-  static constexpr int OFF_A = 8192;  // W tiles (<= 2 x 4 KB) first; buffers 1024-aligned
-  static constexpr int OFF_B = OFF_A + kBuf;
-  static constexpr int OFF_SMALL = OFF_B + kBuf;
+  static constexpr int HP = CF::HP;
+  static constexpr int OFF_A = (NL * CF::kWL + 1023) & ~1023;  // W tiles first; buffers 1024-aligned
+  static constexpr int OFF_B = OFF_A + CF::kBuf;
+  static constexpr int OFF_SMALL = OFF_B + CF::kBuf;
+  static constexpr int EX_ROWS = kRows + 3 * (CF::NG - 2);
   // small region, in floats
-  static constexpr int S_W0 = 0;                       // [32][4] (w_x, w_y, b, 0)
-  static constexpr int S_W0S = S_W0 + 128;             // [32][2] (w_x, w_y) * 2^kXt of X_1
-  static constexpr int S_BIAS = S_W0S + 64;            // [2][32]
-  static constexpr int S_WD = S_BIAS + 64;             // [32] + output bias at 32 (40)
-  static constexpr int S_EX = S_WD + 40;               // [kRows][128]
-  static constexpr int S_ACC = S_EX + kRows * 128;     // [8 warps][kAccW]
-  static constexpr int S_RED = S_ACC + 8 * kAccW;      // 16 doubles
-  static constexpr int S_SC = S_RED + 32;              // [kScN] floats
+  static constexpr int S_W0 = 0;                       // [HP][4] (w_x, w_y, b, 0)
+  static constexpr int S_W0S = S_W0 + 4 * HP;          // [HP][2] (w_x, w_y) * 2^kXt of X_1
+  static constexpr int S_BIAS = S_W0S + 2 * HP;        // [2][HP]
+  static constexpr int S_WD = S_BIAS + 2 * HP;         // [HP] + output bias at HP (+8)
+  static constexpr int S_EX = S_WD + HP + 8;           // [EX_ROWS][128]
+  static constexpr int S_ACC = S_EX + EX_ROWS * 128;   // [warps][kAccW]
+  static constexpr int S_RED = S_ACC + (CF::NT / 32) * kAccW;  // 2 * warps doubles
+  static constexpr int S_SC = S_RED + 2 * 2 * (CF::NT / 32);   // [kScN] floats
   static constexpr int S_SCI = S_SC + kScN;            // [kSiN] ints
   static constexpr int S_MAX = S_SCI + kSiN;           // [16] uint: tile maxima, weight norms
   static constexpr int S_BAR = S_MAX + 16;             // 4 mbarriers + TMEM slot
   static constexpr int S_END = S_BAR + 12;
   static constexpr size_t BYTES = (size_t)OFF_SMALL + sizeof(float) * S_END;
-  static_assert(S_RED % 2 == 0 && S_BAR % 2 == 0 && S_W0 % 4 == 0, "alignment");
+  static_assert(S_RED % 2 == 0 && S_BAR % 2 == 0 && S_W0 % 4 == 0 && S_W0S % 4 == 0, "alignment");
+  // TMEM columns: 0 .. 3 HP: stream accumulators; kG0: parameter-gradient
+  // accumulators (NB = 1: M = 64, layer l in lanes 16 (l - 1) .. + 15 of every
+  // lane quarter, both layers in the same 64 columns; NB = 2: M = 128, 128
+  // columns per layer); kZ0: the last hidden layer's z; NB = 1 also keeps the
+  // hidden-1 (kZ1) and hidden-2 (kZ2, D == 3) z from the forward for the reverse
+  static constexpr int kG0 = 3 * HP;
+  static constexpr int kZ0 = CF::NB == 1 ? 224 : kG0 + 128 * NL;
+  static constexpr int kZ1 = 192;
+  static constexpr int kZ2 = 160;
+  static_assert(CF::NB == 2 || kG0 + 64 <= kZ2, "TMEM map");
+  static_assert(kZ0 + HP <= (int)CF::kCols, "TMEM columns");
 };
 
 // S_MAX words: tile maxima of |ub|, |uxb|, |uyb|; max |w0x|, |w0y|, |wd|; per MMA
@@ -183,54 +183,38 @@ __device__ __forceinline__ int rs8_index(int lane) { return ((lane >> 4) & 1) * 
 __device__ __forceinline__ void atomic_max_abs(uint32_t* w, float v) {
   atomicMax(w, __float_as_uint(fabsf(v)));  // non-negative floats order as their bits (NaN: largest)
 }
-// the same from a whole converged warp: a warp max (REDUX) first, then one
-// shared-memory atomic per warp instead of 32 on the same word
-#ifndef VPG_TC2_WARP_ATOMIC
-#define VPG_TC2_WARP_ATOMIC 0
-#endif
-__device__ __forceinline__ void warp_atomic_max_abs(uint32_t* w, float v) {
-#if VPG_TC2_WARP_ATOMIC
-  const uint32_t m = __reduce_max_sync(0xffffffffu, __float_as_uint(fabsf(v)));
-  if ((threadIdx.x & 31) == 0) atomicMax(w, m);
-#else
-  atomic_max_abs(w, v);
-#endif
-}
 __device__ __forceinline__ int clamp_exp(int k) { return max(-60, min(60, k)); }
 
-// out-of-line MMA issue sequences (called by whole converged warps): one
-// copy in the kernel's SASS instead of one per call site (the kernel is
-// I-cache sensitive)
-#ifndef VPG_TC2_ISSUE_NOINLINE
-#define VPG_TC2_ISSUE_NOINLINE 0  // (A/B: out-of-line issue is 1.6% slower)
-#endif
-#if VPG_TC2_ISSUE_NOINLINE
-#define VPG_ISSUE_ATTR static __device__ __noinline__
-#else
-#define VPG_ISSUE_ATTR static __device__ __forceinline__
-#endif
-// point GEMM of one stream: the three part products Al.Wh, Ah.Wl, Ah.Wh into D
-VPG_ISSUE_ATTR void issue_point_stream_fn(uint32_t d, uint64_t abase, uint64_t wbase, uint32_t idesc,
-                                          uint32_t wstep) {
+// point GEMM of one stream (called by a whole converged warp): the three part
+// products Al.Wh, Ah.Wl, Ah.Wh into D, K = HP in steps of 16.  ablk: byte
+// stride between the K blocks of A (= kPart; A part l at NB blocks); forward:
+// B K-major, K block kb in W tile kb (wblk = kWTile), K step of 16 = +32 B;
+// propagation: B MN-major (N across the W tiles via the descriptor's LBO),
+// K step of 16 W rows = +1024 B.
+template <int NB>
+__device__ __forceinline__ void issue_point_stream(uint32_t d, uint64_t abase, uint64_t wbase, uint32_t idesc,
+                                                   bool propagate, uint32_t kpart, uint32_t wtile, uint32_t wpart) {
 #pragma unroll
   for (int pr = 0; pr < 3; ++pr) {
     const int pa = pr == 0 ? 1 : 0, pb = pr == 1 ? 1 : 0;
 #pragma unroll
-    for (int ks = 0; ks < 2; ++ks) {
-      const uint64_t ad = abase + (uint64_t)((pa * kPart + 32 * ks) >> 4);
-      const uint64_t bd = wbase + (uint64_t)(((pb * 32 * tc::kRowBytes) >> 4) + wstep * ks);
-      tc::mma_warp(d, ad, bd, idesc, (pr > 0 || ks > 0) ? 1u : 0u);
+    for (int ks = 0; ks < 2 * NB; ++ks) {
+      const uint32_t kb = ks >> 1, kin = ks & 1;
+      const uint64_t ad = abase + (uint64_t)(((pa * NB + kb) * kpart + 32 * kin) >> 4);
+      const uint32_t boff = propagate ? pb * wpart + 1024u * ks : pb * wpart + kb * wtile + 32u * kin;
+      tc::mma_warp(d, ad, wbase + (uint64_t)(boff >> 4), idesc, (pr > 0 || ks > 0) ? 1u : 0u);
     }
   }
 }
-// parameter-gradient GEMM: 3 streams x 8 point blocks of K = 16 into acc
-VPG_ISSUE_ATTR void issue_param_fn(uint32_t acc, uint64_t da, uint64_t db, uint32_t idesc, int first, int shift,
-                                   uint64_t* bar) {
+// parameter-gradient GEMM: 3 streams x (MP / 16) point blocks of K = 16 into acc
+template <int MP>
+__device__ __forceinline__ void issue_param(uint32_t acc, uint64_t da, uint64_t db, uint32_t idesc, int first,
+                                            int shift, uint64_t* bar, uint32_t kstream) {
 #pragma unroll 1
   for (int s = 0; s < 3; ++s) {
 #pragma unroll
-    for (int kp = 0; kp < 8; ++kp) {
-      const uint64_t off = (uint64_t)((s * kStream + 1024 * kp) >> 4);
+    for (int kp = 0; kp < MP / 16; ++kp) {
+      const uint64_t off = (uint64_t)((s * kstream + 1024 * kp) >> 4);
       const uint64_t ad = da + off, bd = db + off;
       if (s == 0 && kp == 0) {
         if (first)
@@ -255,12 +239,14 @@ VPG_ISSUE_ATTR void issue_param_fn(uint32_t acc, uint64_t da, uint64_t db, uint3
 // (the split path of cells larger than a tile: forward -> contraction ->
 // penalty -> reverse)
 template <int H, int D, int ACT, int MODE = kModeFused>
-__global__ void __maxnreg__(VPG_TC2_MAXNREG) tc2_step_kernel(const StepArgs a) {
+__global__ void __maxnreg__(t2::Cfg<H>::kMaxReg) tc2_step_kernel(const StepArgs a) {
   using namespace t2;
-  static_assert(H <= 31 && (D == 2 || D == 3), "tc2 step: H <= 31, 2 or 3 hidden layers");
-  static_assert(!VPG_TC2_Z1_CACHE || VPG_TC2_PARAM_M64, "the z1 cache uses the columns the M = 64 accumulators free");
-  using LY = Lay<D>;
+  static_assert(D == 2 || D == 3, "tc2 step: 2 or 3 hidden layers");
+  using CF = Cfg<H>;
+  using LY = Lay<H, D>;
   constexpr int NL = LY::NL;
+  constexpr int NB = CF::NB, HP = CF::HP, NT = CF::NT, MP = CF::MP;
+  constexpr int kPart = CF::kPart, kStream = CF::kStream;
   using AC = Act<ACT>;
 
   pdl_trigger();
@@ -304,8 +290,14 @@ __global__ void __maxnreg__(VPG_TC2_MAXNREG) tc2_step_kernel(const StepArgs a) {
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int p = tid & 127;   // point of this thread == TMEM lane
-  const int hh = tid >> 7;   // unit half
-  const int u0 = 16 * hh;    // first hidden unit of this thread
+  const int ug = tid >> 7;   // unit group
+  const int u0 = 16 * ug;    // first hidden unit of this thread
+  const uint32_t tb = (uint32_t)(ug >> 1) * kPart;  // this thread's column block inside a part
+  // MP < 128 (NB = 2): the threads of TMEM lanes MP..127 hold no point; they
+  // compute on the accumulators' unused rows, never store an operand row
+  // (row p of an [MP][32] tile would be row p - MP of the next one) and add
+  // zeros to the per-warp gradient sums
+  const bool row_ok = MP == 128 || p < MP;
   const NetDesc& net = a.net;
   const float* P = a.params;
   const float kapmax = 2.0f;  // |act''/act'|: 2 |z| (tanh) or |1 - 2z| (sigmoid)
@@ -316,30 +308,36 @@ __global__ void __maxnreg__(VPG_TC2_MAXNREG) tc2_step_kernel(const StepArgs a) {
       if (a.phase_clk != nullptr && blockIdx.x == 0 && threadIdx.x == 0) a.phase_clk[7 * kPhaseMarks + 20 + i] = clock64();
   };
   smark(0);
-  if (warp == 0) tc::tmem_alloc(tslot, kCols);
+  if (warp == 0) tc::tmem_alloc(tslot, CF::kCols);
   smark(1);
   if (tid == 0) {
     mbar_init(bar_v, 1);
-    mbar_init(bar_t, VPG_TC2_ISSUE_WARPS == 3 ? 2 : 1);
+    mbar_init(bar_t, 2);
     mbar_init(bar_w, 1);
     mbar_init(tma_bar, 1);
     fence_mbar_init();
   }
   if (tid < 16) sMax[tid] = 0u;
-  for (int i = tid; i < 8 * kAccW; i += kNT) sAcc[i] = 0.f;
-  // every parameter load of the setup issued at once: thread t < 128 NL holds
-  // row (t / 4) % 32, columns [8 (t % 4), +8) of MMA layer t / 128 + 1
-  const int wl = tid >> 7, wo = (tid >> 2) & 31, wc = tid & 3;
-  float wv[8];
+  for (int i = tid; i < (NT / 32) * kAccW; i += NT) sAcc[i] = 0.f;
+  // every parameter load of the setup issued at once: item it = (MMA layer
+  // wl, row wo, 8-column chunk wc) of the [HP][HP] padded weight matrices
+  constexpr int kWItems = HP * HP / 8;
+  constexpr int IPT = (NL * kWItems + NT - 1) / NT;
+  float wv[IPT][8];
 #pragma unroll
-  for (int k = 0; k < 8; ++k) {
-    const int i = 8 * wc + k;
-    // narrower layers (out_w / in_w < H) are zero-padded: padded units get
-    // zero weights and biases, so they never reach the outputs
-    const int fo = wl < NL ? net.out_w[wl + 1] : 0, fi = wl < NL ? net.in_w[wl + 1] : 0;
-    wv[k] = (wo < fo && i < fi) ? P[net.w_off[wl + 1] + wo * fi + i] : 0.f;
+  for (int j = 0; j < IPT; ++j) {
+    const int it = tid + j * NT;
+    const int wl = it / kWItems, wo = (it % kWItems) / (HP / 8), wc = it % (HP / 8);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int i = 8 * wc + k;
+      // narrower layers (out_w / in_w < H) are zero-padded: padded units get
+      // zero weights and biases, so they never reach the outputs
+      const int fo = wl < NL ? net.out_w[wl + 1] : 0, fi = wl < NL ? net.in_w[wl + 1] : 0;
+      wv[j][k] = (wo < fo && i < fi) ? P[net.w_off[wl + 1] + wo * fi + i] : 0.f;
+    }
   }
-  for (int i = tid; i < 32; i += kNT) {
+  for (int i = tid; i < HP; i += NT) {
     float w0 = 0.f, w1 = 0.f, b = (i == H) ? kOneBias : 0.f, wd = 0.f;
     if (i < net.out_w[0]) {
       w0 = P[net.w_off[0] + 2 * i];
@@ -353,26 +351,35 @@ __global__ void __maxnreg__(VPG_TC2_MAXNREG) tc2_step_kernel(const StepArgs a) {
     sW0[4 * i + 3] = 0.f;
     sWd[i] = wd;
   }
-  if (tid == 0) sWd[32] = P[net.b_off[D]];
+  if (tid == 0) sWd[HP] = P[net.b_off[D]];
   for (int l = 1; l <= NL; ++l)
-    for (int o = tid; o < 32; o += kNT)
-      sBias[(l - 1) * 32 + o] = o < net.out_w[l] ? P[net.b_off[l] + o] : ((o == H) ? kOneBias : 0.f);
+    for (int o = tid; o < HP; o += NT)
+      sBias[(l - 1) * HP + o] = o < net.out_w[l] ? P[net.b_off[l] + o] : ((o == H) ? kOneBias : 0.f);
   // |W| into buffer A (free until the first tile) for the row / column sums
-  float* sAbs = reinterpret_cast<float*>(bufA);  // [NL][32][33] (row stride 33: no bank conflicts)
+  float* sAbs = reinterpret_cast<float*>(bufA);  // [NL][HP][HP + 1] (odd row stride: no bank conflicts)
   uint32_t* sNorm = sMax + kNW0;  // [0] w0x [1] w0y [2] wd
   uint32_t(*s_lnorm)[3] = reinterpret_cast<uint32_t(*)[3]>(sMax + kNLayer);  // [layer][maxabs, rowsum, colsum]
-  if (wl < NL) {
 #pragma unroll
-    for (int k = 0; k < 8; ++k) sAbs[(wl * 32 + wo) * 33 + 8 * wc + k] = fabsf(wv[k]);
+  for (int j = 0; j < IPT; ++j) {
+    const int it = tid + j * NT;
+    const int wl = it / kWItems, wo = (it % kWItems) / (HP / 8), wc = it % (HP / 8);
+    if (wl < NL) {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) sAbs[(wl * HP + wo) * (HP + 1) + 8 * wc + k] = fabsf(wv[j][k]);
+    }
   }
   smark(2);
   __syncthreads();  // (also orders the sMax zero fill before any atomic below)
   smark(3);
-  if (wl < NL) {
-    float m = 0.f;
 #pragma unroll
-    for (int k = 0; k < 8; ++k) m = fmaxf(m, fabsf(wv[k]));
-    atomic_max_abs(&s_lnorm[wl][0], m);  // max: order-free
+  for (int j = 0; j < IPT; ++j) {
+    const int wl = (tid + j * NT) / kWItems;
+    if (wl < NL) {
+      float m = 0.f;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) m = fmaxf(m, fabsf(wv[j][k]));
+      atomic_max_abs(&s_lnorm[wl][0], m);  // max: order-free
+    }
   }
   // weight norms (bounds for the scales): max |w0x|, |w0y|, |wd|; per MMA
   // layer max row abs-sum R and max column abs-sum C, each sum in index order
@@ -381,12 +388,12 @@ __global__ void __maxnreg__(VPG_TC2_MAXNREG) tc2_step_kernel(const StepArgs a) {
     atomic_max_abs(&sNorm[1], sW0[4 * tid + 1]);
     atomic_max_abs(&sNorm[2], sWd[tid]);
   }
-  if (tid < 64 * NL) {
-    const int l = tid >> 6, j = tid & 31;
-    const bool row = (tid & 32) == 0;
+  for (int t = tid; t < 2 * HP * NL; t += NT) {
+    const int l = t / (2 * HP), j = t % HP;
+    const bool row = ((t / HP) & 1) == 0;
     float sum = 0.f;
     if (j < H) {
-      for (int k = 0; k < H; ++k) sum += row ? sAbs[(l * 32 + j) * 33 + k] : sAbs[(l * 32 + k) * 33 + j];
+      for (int k = 0; k < H; ++k) sum += row ? sAbs[(l * HP + j) * (HP + 1) + k] : sAbs[(l * HP + k) * (HP + 1) + j];
     }
     atomic_max_abs(&s_lnorm[l][row ? 1 : 2], sum);
   }
@@ -419,14 +426,21 @@ __global__ void __maxnreg__(VPG_TC2_MAXNREG) tc2_step_kernel(const StepArgs a) {
     sSc[kScWd] = __uint_as_float(sNorm[2]);
   }
   __syncthreads();
-  for (int i = tid; i < 32; i += kNT) {  // layer-0 tangent weights pre-scaled for X_1
+  for (int i = tid; i < HP; i += NT) {  // layer-0 tangent weights pre-scaled for X_1
     sW0s[2 * i] = sW0[4 * i] * sSc[kScSt];
     sW0s[2 * i + 1] = sW0[4 * i + 1] * sSc[kScSt];
   }
   smark(4);
-  // W tiles, scaled by 2^kW: row o of part h at rows 0..31, part l at rows 32..63
-  if (wl < NL)
-    tc::st_split8_h(sWB + wl * kWBytes, 32 * tc::kRowBytes, wo, wc, wv, tc::exp2i(sSci[kSiW + wl]));
+  // W tiles, scaled by 2^kW: MMA layer wl, input block ib = wc / 4: row o of
+  // part h at rows 0..HP-1, part l at rows HP..2HP-1
+#pragma unroll
+  for (int j = 0; j < IPT; ++j) {
+    const int it = tid + j * NT;
+    const int wl = it / kWItems, wo = (it % kWItems) / (HP / 8), wc = it % (HP / 8);
+    if (wl < NL)
+      tc::st_split8_h(sWB + wl * CF::kWL + (wc >> 2) * CF::kWTile, HP * tc::kRowBytes, wo, wc & 3, wv[j],
+                      tc::exp2i(sSci[kSiW + wl]));
+  }
   tc::fence_smem_to_async();
   tc::fence_before_sync();
   __syncthreads();
@@ -434,93 +448,49 @@ __global__ void __maxnreg__(VPG_TC2_MAXNREG) tc2_step_kernel(const StepArgs a) {
   const uint32_t tmem = *tslot;
   const uint32_t lane_q = (uint32_t)(32 * (warp & 3)) << 16;  // TMEM lane quarter of this warp
   const uint32_t sA = smem_u32(bufA), sB = smem_u32(bufB), sW = smem_u32(sWB);
-  // swizzled byte offsets of this thread's two 8-unit chunks in a [128][32] fp16 tile
-  const uint32_t off0 = tc::sw_chunk(p, 2 * hh), off1 = tc::sw_chunk(p, 2 * hh + 1);
+  // swizzled byte offsets of this thread's two 8-unit chunks inside its block's tile
+  const uint32_t off0 = tc::sw_chunk(p, 2 * (ug & 1)) + tb, off1 = tc::sw_chunk(p, 2 * (ug & 1) + 1) + tb;
 
-  // ---------------- MMA issue (warp 0, one elected lane) ----------------
+  // ---------------- MMA issue ----------------
   // descriptors: start address >> 4 in the low 14 bits, so an address offset
   // is added as offset >> 4 (addresses < 256 KB: no carry out of the field)
-  const uint64_t dA_k = tc::kdesc(sA), dB_k = tc::kdesc(sB);           // K-major point operands
+  const uint64_t dA_k = tc::kdesc(sA), dB_k = tc::kdesc(sB);                    // K-major point operands
   const uint64_t dA_mn = tc::mndesc(sA, kPart), dB_mn = tc::mndesc(sB, kPart);  // MN-major (param GEMM)
-  const uint64_t dW_k = tc::kdesc(sW), dW_mn = tc::mndesc(sW, 32 * tc::kRowBytes);
+  const uint64_t dW_k = tc::kdesc(sW), dW_mn = tc::mndesc(sW, CF::kWTile);
   // layer l's parameter-gradient accumulator (MMA address) and this warp's
   // load address of it (lane quarter base)
   auto gacc = [&](int l) {
-    return VPG_TC2_PARAM_M64 ? tmem + kG0 + ((uint32_t)(16 * (l - 1)) << 16) : tmem + kG0 + 64 * (l - 1);
+    return NB == 1 ? tmem + LY::kG0 + ((uint32_t)(16 * (l - 1)) << 16) : tmem + LY::kG0 + 128 * (l - 1);
   };
-  auto gacc_ld = [&](int l) { return tmem + lane_q + kG0 + (VPG_TC2_PARAM_M64 ? 0 : 64 * (l - 1)); };
-  // point GEMM of MMA layer l (forward, or propagation with B MN-major): the
-  // three part products Al.Wh, Ah.Wl, Ah.Wh of stream s accumulate into D_s
-  // VPG_TC2_ISSUE_WARPS == 3: stream s is issued by warp s (the three
-  // streams' MMAs enter the tensor pipe in parallel instead of behind one
-  // warp's ~60-cycle-per-MMA issue; each stream's accumulation order stays
-  // fixed); bar_t then expects two arrivals.  == 1: warp 0 issues all.
-  auto issue_point_stream = [&](bool bufb, int l, bool propagate, int s) {
-    const uint64_t abase = (bufb ? dB_k : dA_k) + (uint64_t)((s * kStream) >> 4);
-    const uint64_t wbase = (propagate ? dW_mn : dW_k) + (uint64_t)(((l - 1) * kWBytes) >> 4);
-    const uint32_t idesc = tc::idesc_f16(128, 32, 0, propagate ? 1 : 0);
-    issue_point_stream_fn(tmem + kDCols * s, abase, wbase, idesc, propagate ? 1024u >> 4 : 32u >> 4);
-  };
-  // called by warps 0..2 (or by warp 0 alone)
+  auto gacc_ld = [&](int l) { return tmem + lane_q + LY::kG0 + (NB == 1 ? 0 : 128 * (l - 1)); };
+  // point GEMM of MMA layer l (forward, or propagation with B MN-major):
+  // stream s is issued by warp s (the three streams' MMAs enter the tensor
+  // pipe in parallel; each stream's accumulation order stays fixed); bar_t
+  // expects the two tangent-stream arrivals
   auto issue_point_gemm = [&](bool bufb, int l, bool propagate) {
-#if VPG_TC2_ISSUE_WARPS == 3
-#if VPG_TC2_ISSUE_UNROLL == 3
-    // the stream index as a constant per warp (uniform descriptor offsets)
-    if (warp == 0)
-      issue_point_stream(bufb, l, propagate, 0);
-    else if (warp == 1)
-      issue_point_stream(bufb, l, propagate, 1);
-    else
-      issue_point_stream(bufb, l, propagate, 2);
-#else
-    issue_point_stream(bufb, l, propagate, warp);
-#endif
+    const int s = warp;
+    const uint64_t abase = (bufb ? dB_k : dA_k) + (uint64_t)((s * kStream) >> 4);
+    const uint64_t wbase = (propagate ? dW_mn : dW_k) + (uint64_t)(((l - 1) * CF::kWL) >> 4);
+    const uint32_t idesc = tc::idesc_f16(128, HP, 0, propagate ? 1 : 0);
+    issue_point_stream<NB>(tmem + HP * s, abase, wbase, idesc, propagate, kPart, CF::kWTile, HP * tc::kRowBytes);
     tc::commit_warp(warp == 0 ? bar_v : bar_t);
-#else
-#pragma unroll 1
-    for (int s = 0; s < 3; ++s) {
-      issue_point_stream(bufb, l, propagate, s);
-      if (s == 0) tc::commit_warp(bar_v);
-    }
-    tc::commit_warp(bar_t);
-#endif
   };
-  // parameter gradient of MMA layer l: G parts in bufA (M blocks h | l | next
-  // stream's parts, unused), X parts in bufB (N = h | l).  Accumulates in
-  // TMEM across the CTA's tiles: fresh (first), or onto the accumulator
-  // scaled down by 2^-shift (scale-input-d) when this tile's product scale is
-  // smaller than the accumulated one
+  // parameter gradient of MMA layer l: G parts in bufA (M = Gh | Gl), X parts
+  // in bufB (N = Xh | Xl).  Accumulates in TMEM across the CTA's tiles:
+  // fresh (first), or onto the accumulator scaled down by 2^-shift
+  // (scale-input-d) when this tile's product scale is smaller than the
+  // accumulated one
   auto issue_param_gemm = [&](int l, bool first, int shift) {
-    issue_param_fn(gacc(l), dA_mn, dB_mn, tc::idesc_f16(VPG_TC2_PARAM_M64 ? 64 : 128, 64, 1, 1), first ? 1 : 0,
-                   shift, bar_w);
+    issue_param<MP>(gacc(l), dA_mn, dB_mn, tc::idesc_f16(2 * HP, 2 * HP, 1, 1), first ? 1 : 0, shift, bar_w,
+                    kStream);
   };
   uint32_t ph_v = 0, ph_t = 0, ph_w = 0, tma_phase = 0;
-  // CTA-wide wait for MMA completion: ONE warp polls the mbarrier(s), the
-  // others sleep in the CTA barrier instead of spinning on issue slots the
-  // co-resident CTA needs
-  auto cta_wait = [&](uint64_t* b1, uint32_t& p1, uint64_t* b2, uint32_t* p2, uint64_t* b3, uint32_t* p3) {
-#if VPG_TC2_WARP_WAITS
-    // every warp polls the mbarrier(s) itself: no CTA barrier, warps run ahead
+  // wait for MMA completion: every warp polls the mbarrier(s) itself (no CTA
+  // barrier, warps run ahead)
+  auto mma_wait = [&](uint64_t* b1, uint32_t& p1) {
     mbar_wait(b1, p1);
-    if (b2) mbar_wait(b2, *p2);
-    if (b3) mbar_wait(b3, *p3);
     p1 ^= 1u;
-    if (b2) *p2 ^= 1u;
-    if (b3) *p3 ^= 1u;
     tc::fence_after_sync();
-#else
-    if (warp == 0) {
-      mbar_wait(b1, p1);
-      if (b2) mbar_wait(b2, *p2);
-      if (b3) mbar_wait(b3, *p3);
-    }
-    p1 ^= 1u;
-    if (b2) *p2 ^= 1u;
-    if (b3) *p3 ^= 1u;
-    tc::fence_before_sync();
-    __syncthreads();
-    tc::fence_after_sync();
-#endif
   };
   auto operands_ready = [&]() {
     tc::fence_smem_to_async();
@@ -528,7 +498,7 @@ __global__ void __maxnreg__(VPG_TC2_MAXNREG) tc2_step_kernel(const StepArgs a) {
     __syncthreads();
     tc::fence_after_sync();
   };
-  auto dcol = [&](int s, int c) { return tmem + lane_q + kDCols * s + u0 + 8 * c; };
+  auto dcol = [&](int s, int c) { return tmem + lane_q + HP * s + u0 + 8 * c; };
   auto coff = [&](int c) { return c ? off1 : off0; };
 
   // layer 0 of this thread's chunk c (8 units) at (px, py): z and s1
@@ -547,12 +517,12 @@ __global__ void __maxnreg__(VPG_TC2_MAXNREG) tc2_step_kernel(const StepArgs a) {
     }
   };
   // X_1 (hidden-1 output) of chunk c, scaled, into buffer buf: from (x, y)
-  // through layer 0 (forward; its z kept in TMEM), or from that kept z
-  // (reverse: no activation evaluation)
+  // through layer 0 (forward; its z kept in TMEM when it fits), or from that
+  // kept z (reverse: no activation evaluation)
   auto store_x1 = [&](char* buf, int c, float px, float py, bool from_tmem) {
     float z[8], s1[8], tx[8], ty[8];
-    if (VPG_TC2_Z1_CACHE && from_tmem) {
-      tc::tmem_ld1x8_wait(tmem + lane_q + kZ1 + u0 + 8 * c, z);
+    if (CF::kZCache && from_tmem) {
+      tc::tmem_ld1x8_wait(tmem + lane_q + LY::kZ1 + u0 + 8 * c, z);
 #pragma unroll
       for (int k = 0; k < 8; k += 2) {
         const float2 ss = AC::s1_2(f2(z[k], z[k + 1]));
@@ -561,7 +531,7 @@ __global__ void __maxnreg__(VPG_TC2_MAXNREG) tc2_step_kernel(const StepArgs a) {
       }
     } else {
       layer0(c, px, py, z, s1);
-      if (VPG_TC2_Z1_CACHE) tc::tmem_st1x8_wait(tmem + lane_q + kZ1 + u0 + 8 * c, z);
+      if (CF::kZCache) tc::tmem_st1x8_wait(tmem + lane_q + LY::kZ1 + u0 + 8 * c, z);
     }
 #pragma unroll
     for (int k = 0; k < 8; k += 2) {
@@ -574,12 +544,18 @@ __global__ void __maxnreg__(VPG_TC2_MAXNREG) tc2_step_kernel(const StepArgs a) {
       ty[k + 1] = b.y;
     }
     const uint32_t o = coff(c);
-    tc::st_split8_ho<true>(buf, kPart, o, z, sSc[kScSv]);
-    tc::st_split8_ho<false>(buf + kStream, kPart, o, tx, 1.f);
-    tc::st_split8_ho<false>(buf + 2 * kStream, kPart, o, ty, 1.f);
+    if (row_ok) tc::st_split8_ho<true>(buf, NB * kPart, o, z, sSc[kScSv]);
+    if (row_ok) tc::st_split8_ho<false>(buf + kStream, NB * kPart, o, tx, 1.f);
+    if (row_ok) tc::st_split8_ho<false>(buf + 2 * kStream, NB * kPart, o, ty, 1.f);
   };
   // running per-warp sums of 8 unit values (units u0 + 8c + k) at slot base
   auto acc_units = [&](float (&v)[8], int slot, int c) {
+    if constexpr (MP < 128) {
+      if (!row_ok) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) v[k] = 0.f;
+      }
+    }
     const float r = warp_rs8(v);
     if ((lane & 3) == 0) sAcc[warp * kAccW + slot + 8 * c + rs8_index(lane)] += r;
   };
@@ -588,35 +564,35 @@ __global__ void __maxnreg__(VPG_TC2_MAXNREG) tc2_step_kernel(const StepArgs a) {
   // TMEM holds per MMA layer, and whether it holds anything yet
   int kacc0 = 0, kacc1 = 0;
   bool has0 = false, has1 = false, spill0 = false, spill1 = false;
-  // rare path (an accumulator would need more than 2^-15): add the layer-l
-  // accumulator, unscaled, into the per-CTA fp32 scratch ([col][lane]) and
-  // restart it; warps of lane quarters 0 / 1 (G rows h / l), unit half = X
-  // part h / l
-  // G row (part * 32 + o) held by this thread's TMEM lane in layer l's
-  // parameter-gradient accumulator, or -1: M = 128 puts row r in lane r
-  // (warps of lane quarters 0 / 1), M = 64 in lane 32 (r / 16) + r % 16 +
-  // the layer's lane offset 16 (l - 1)
+  // G row (part * HP + o) held by this thread's TMEM lane in layer l's
+  // parameter-gradient accumulator, or -1: NB = 2 (M = 128) puts row r in
+  // lane r; NB = 1 (M = 64) in lane 32 (r / 16) + r % 16 + the layer's lane
+  // offset 16 (l - 1)
   auto gacc_row = [&](int l) {
-    if (VPG_TC2_PARAM_M64) {
+    if (NB == 1) {
       const int lo = lane - 16 * (l - 1);
       return (lo >= 0 && lo < 16) ? 16 * (warp & 3) + lo : -1;
     }
-    return (warp & 3) < 2 ? 32 * (warp & 1) + lane : -1;
+    return 32 * (warp & 3) + lane;
   };
+  // this thread's 2HP / NG = 32 accumulator columns (X part * HP + i)
+  const int col_base = 32 * ug;
+  // rare path (an accumulator would need more than 2^-15): add the layer-l
+  // accumulator, unscaled, into the per-CTA fp32 scratch ([col][row]) and
+  // restart it
   auto spill_accumulator = [&](int l, int kacc, bool first) {
-    if (!VPG_TC2_PARAM_M64 && (warp & 3) >= 2) return;
-    float* S = a.tc_scratch + ((size_t)blockIdx.x * NL + (l - 1)) * kScratchPerLayer;
+    float* S = a.tc_scratch + ((size_t)blockIdx.x * NL + (l - 1)) * CF::kScratch;
     const float inv = tc::exp2i(-kacc);
 #pragma unroll 1
     for (int h2 = 0; h2 < 2; ++h2) {
-      const int col0 = 32 * hh + 16 * h2;
+      const int col0 = col_base + 16 * h2;
       float v[16];
       tc::tmem_ld1x16_wait(gacc_ld(l) + col0, v);
       const int grow = gacc_row(l);
       if (grow >= 0) {
 #pragma unroll
         for (int k = 0; k < 16; ++k) {
-          float* d = S + (col0 + k) * 64 + grow;
+          float* d = S + (col0 + k) * (2 * HP) + grow;
           *d = first ? v[k] * inv : fmaf(v[k], inv, *d);
         }
       }
@@ -667,11 +643,10 @@ __global__ void __maxnreg__(VPG_TC2_MAXNREG) tc2_step_kernel(const StepArgs a) {
     }
   };
 
-  double acc_v = 0.0, acc_b = 0.0, acc_s = 0.0, acc_eg = 0.0;  // thread 0
-  // CONTRACT3: per-cell-slot loss sums kept by the thread that forms them
-  // (unit half 1, slot = cell within the tile) and combined across the CTA in
-  // a fixed order at the end.  Reading per-cell sums from buffer A after the
-  // tile's last barrier raced with the reverse's operand stores into it.
+  double acc_b = 0.0, acc_s = 0.0;  // thread 0: penalty sums
+  // per-cell-slot loss sums kept by the thread that forms them (unit group
+  // 1, slot = cell within the tile) and combined across the CTA in a fixed
+  // order at the end
   double cell_v = 0.0, cell_eg = 0.0;
   int bad = 0;
   const int n_pts_all = a.n_int + a.n_bnd + a.n_sen;
@@ -679,14 +654,14 @@ __global__ void __maxnreg__(VPG_TC2_MAXNREG) tc2_step_kernel(const StepArgs a) {
     bool interior;
     int cell0, ncell, pbase, np;
   };
-  const int n_tiles = MODE == kModeForward ? (a.n_fwd + 127) / 128
-                      : (MODE == kModeReverse ? (n_pts_all + 127) / 128 : a.n_tiles);
+  const int n_tiles = MODE == kModeForward ? (a.n_fwd + MP - 1) / MP
+                      : (MODE == kModeReverse ? (n_pts_all + MP - 1) / MP : a.n_tiles);
   auto geo = [&](int tile) {
     TileGeo g{false, 0, 0, 0, 0};
     if (MODE != kModeFused) {
       if (tile < n_tiles) {
-        g.pbase = tile * 128;
-        g.np = min(128, (MODE == kModeForward ? a.n_fwd : n_pts_all) - g.pbase);
+        g.pbase = tile * MP;
+        g.np = min(MP, (MODE == kModeForward ? a.n_fwd : n_pts_all) - g.pbase);
       }
     } else if (tile < a.n_int_tiles) {
       g.interior = true;
@@ -695,8 +670,8 @@ __global__ void __maxnreg__(VPG_TC2_MAXNREG) tc2_step_kernel(const StepArgs a) {
       g.pbase = g.cell0 * a.Q;
       g.np = g.ncell * a.Q;
     } else if (tile < a.n_tiles) {
-      g.pbase = a.n_int + (tile - a.n_int_tiles) * 128;
-      g.np = min(128, n_pts_all - g.pbase);
+      g.pbase = a.n_int + (tile - a.n_int_tiles) * MP;
+      g.np = min(MP, n_pts_all - g.pbase);
     }
     return g;
   };
@@ -715,11 +690,9 @@ __global__ void __maxnreg__(VPG_TC2_MAXNREG) tc2_step_kernel(const StepArgs a) {
   // contraction scratch after the slab in buffer A
   float* tail = reinterpret_cast<float*>(bufA) + a.nt * a.tstride;
   float* cvr = tail;              // [128] bx ux + by uy
-  float* part = tail + 128;       // [3][128]
   float* rbarv = tail + 4 * 128;  // [128]
   float* rsqv = tail + 5 * 128;
   float* rgev = tail + 6 * 128;
-  float* cellv = tail + 7 * 128;  // [2][<=64]: per-cell sums
 
 #pragma unroll 1
   for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
@@ -731,8 +704,8 @@ __global__ void __maxnreg__(VPG_TC2_MAXNREG) tc2_step_kernel(const StepArgs a) {
     const bool valid = p < np;
     const float px = nx, py = ny;
     float frow = 0.f;
-    if (interior && hh == 0 && p < nrows_tile) frow = a.forcing[(size_t)cell0 * a.T + p];
-    if (hh == 0) {
+    if (interior && ug == 0 && p < nrows_tile) frow = a.forcing[(size_t)cell0 * a.T + p];
+    if (ug == 0) {
       sEx[kX * 128 + p] = px;
       sEx[kY * 128 + p] = py;
     }
@@ -743,10 +716,10 @@ __global__ void __maxnreg__(VPG_TC2_MAXNREG) tc2_step_kernel(const StepArgs a) {
 
     // =================== forward ===================
     char* x1buf = (D == 3) ? bufA : bufB;  // hidden-1 output (input of MMA layer 1)
-VPG_PRAGMA_UNROLL(VPG_TC2_CHUNK_UNROLL)
-    for (int c = 0; c < 2; ++c) store_x1(x1buf, c, px, py, false);
+#pragma unroll 1
+    for (int c = 0; c < 2; ++c) store_x1(x1buf + 0, c, px, py, false);
     operands_ready();
-    if (warp < VPG_TC2_ISSUE_WARPS) issue_point_gemm(D == 2, 1, false);
+    if (warp < 3) issue_point_gemm(D == 2, 1, false);
     mark(1);
     // epilogue of MMA layer l: hidden l+1 output.  Value stream first (it
     // overlaps the tangent-stream MMAs), stored (or consumed by the output
@@ -759,9 +732,9 @@ VPG_PRAGMA_UNROLL(VPG_TC2_CHUNK_UNROLL)
       // tangent factor: forward unscale, times the X_{l+1} scale when stored
       const float ft = last ? sSc[kScF1 + l - 1] : sSc[kScF1 + l - 1] * sSc[kScSt + l];
       const float sv = last ? 1.f : sSc[kScSv + l];
-      const float* bias = sBias + 32 * (l - 1);
+      const float* bias = sBias + HP * (l - 1);
       float s1v[16];
-      cta_wait(bar_v, ph_v, nullptr, nullptr, nullptr, nullptr);
+      mma_wait(bar_v, ph_v);
 #pragma unroll
       for (int c = 0; c < 2; ++c) {
         float d[8], z[8];
@@ -781,12 +754,12 @@ VPG_PRAGMA_UNROLL(VPG_TC2_CHUNK_UNROLL)
           }
         }
         if (!last) {
-          tc::st_split8_ho<true>(bufB, kPart, coff(c), z, sv);
-          if (VPG_TC2_Z1_CACHE && D == 3) tc::tmem_st1x8_wait(tmem + lane_q + kZ2 + u0 + 8 * c, z);
+          if (row_ok) tc::st_split8_ho<true>(bufB, NB * kPart, coff(c), z, sv);
+          if (CF::kZCache && D == 3) tc::tmem_st1x8_wait(tmem + lane_q + LY::kZ2 + u0 + 8 * c, z);
         } else
-          tc::tmem_st1x8_wait(tmem + lane_q + kZ0 + u0 + 8 * c, z);  // kept for the reverse
+          tc::tmem_st1x8_wait(tmem + lane_q + LY::kZ0 + u0 + 8 * c, z);  // kept for the reverse
       }
-      cta_wait(bar_t, ph_t, nullptr, nullptr, nullptr, nullptr);
+      mma_wait(bar_t, ph_t);
       // D == 3: buffer A (slab) is free once MMA layer 1 is done
       if (D == 3 && l == 1 && interior && tid == 0)
         issue_chunk(a, cell0, 0, nrows_tile, reinterpret_cast<float*>(bufA), tma_bar);
@@ -811,27 +784,35 @@ VPG_PRAGMA_UNROLL(VPG_TC2_CHUNK_UNROLL)
             dy[k] = b.x;
             dy[k + 1] = b.y;
           }
-          tc::st_split8_ho<false>(bufB + kStream, kPart, coff(c), dx, 1.f);
-          tc::st_split8_ho<false>(bufB + 2 * kStream, kPart, coff(c), dy, 1.f);
+          if (row_ok) tc::st_split8_ho<false>(bufB + kStream, NB * kPart, coff(c), dx, 1.f);
+          if (row_ok) tc::st_split8_ho<false>(bufB + 2 * kStream, NB * kPart, coff(c), dy, 1.f);
         }
       }
       if (!last) {
         operands_ready();
-        if (warp < VPG_TC2_ISSUE_WARPS) issue_point_gemm(true, l + 1, false);
+        if (warp < 3) issue_point_gemm(true, l + 1, false);
       }
       mark(1 + l);
     }
-    // output layer: halves combined in order (half 0 + half 1 + bias)
-    if (hh == 1) {
-      sEx[(kPu + 0) * 128 + p] = ou;
-      sEx[(kPu + 1) * 128 + p] = oux;
-      sEx[(kPu + 2) * 128 + p] = ouy;
+    // output layer: groups combined in order (group 0 + 1, + 2, + 3, + bias)
+    if (ug >= 1) {
+      const int r = ug == 1 ? kPu : kRows + 3 * (ug - 2);
+      sEx[(r + 0) * 128 + p] = ou;
+      sEx[(r + 1) * 128 + p] = oux;
+      sEx[(r + 2) * 128 + p] = ouy;
     }
     __syncthreads();
-    if (hh == 0) {
-      const float u = (ou + sEx[(kPu + 0) * 128 + p]) + sWd[32];
-      const float ux = oux + sEx[(kPu + 1) * 128 + p];
-      const float uy = ouy + sEx[(kPu + 2) * 128 + p];
+    if (ug == 0) {
+      float u = ou + sEx[(kPu + 0) * 128 + p], ux = oux + sEx[(kPu + 1) * 128 + p],
+            uy = ouy + sEx[(kPu + 2) * 128 + p];
+#pragma unroll
+      for (int g = 2; g < CF::NG; ++g) {
+        const int r = kRows + 3 * (g - 2);
+        u += sEx[(r + 0) * 128 + p];
+        ux += sEx[(r + 1) * 128 + p];
+        uy += sEx[(r + 2) * 128 + p];
+      }
+      u += sWd[HP];
       if (valid && !(finitef(u) && finitef(ux) && finitef(uy))) bad = 1;
       sEx[kU * 128 + p] = u;
       sEx[kUx * 128 + p] = ux;
@@ -853,7 +834,7 @@ VPG_PRAGMA_UNROLL(VPG_TC2_CHUNK_UNROLL)
     // =================== objective: adjoints of (u, ux, uy) ===================
     if (MODE == kModeReverse) {
       // the split path's contraction / penalty kernels computed them
-      if (hh == 0) {
+      if (ug == 0) {
         float ubv = 0.f, ox = 0.f, oy = 0.f;
         if (valid) {
           const int pi = G.pbase + p;
@@ -867,9 +848,9 @@ VPG_PRAGMA_UNROLL(VPG_TC2_CHUNK_UNROLL)
         sEx[kUb * 128 + p] = ubv;
         sEx[kUxb * 128 + p] = ox;
         sEx[kUyb * 128 + p] = oy;
-        warp_atomic_max_abs(&sMax[kMb], ubv);
-        warp_atomic_max_abs(&sMax[kMx], ox);
-        warp_atomic_max_abs(&sMax[kMy], oy);
+        atomic_max_abs(&sMax[kMb], ubv);
+        atomic_max_abs(&sMax[kMx], ox);
+        atomic_max_abs(&sMax[kMy], oy);
       }
     } else if (interior) {
       const bool conv = a.nt == 3;
@@ -882,11 +863,10 @@ VPG_PRAGMA_UNROLL(VPG_TC2_CHUNK_UNROLL)
       const float* T0 = chunk_ptr(a, cell0, 0, slab, 0);
       const float* T1 = chunk_ptr(a, cell0, 0, slab, 1);
       const float* T2 = conv ? chunk_ptr(a, cell0, 0, slab, 2) : T0;
-#if VPG_TC2_CONTRACT3
-      // phase A: one thread per row (unit half 0) runs the three dot products
+      // phase A: one thread per row (unit group 0) runs the three dot products
       // (G_x . ux, G_y . uy, T . (bx ux + by uy)) as interleaved chains and
-      // finishes the residual itself (losses.hpp:122-136): no exchange step
-      if (hh == 0 && p < nrows_tile) {
+      // finishes the residual itself (losses.hpp:122-136)
+      if (ug == 0 && p < nrows_tile) {
         const int r = p, kk = r / a.T;
         const float* sx = sEx + kUx * 128 + kk * a.Q;
         const float* sy = sEx + kUy * 128 + kk * a.Q;
@@ -922,9 +902,9 @@ VPG_PRAGMA_UNROLL(VPG_TC2_CHUNK_UNROLL)
       }
       __syncthreads();
       mark(6);
-      // phase B: one thread per point (unit half 0) runs the three adjoint
-      // columns and writes the point's adjoints; half 1 the per-cell sums
-      if (hh == 0) {
+      // phase B: one thread per point (unit group 0) runs the three adjoint
+      // columns and writes the point's adjoints; group 1 the per-cell sums
+      if (ug == 0) {
         float ox = 0.f, oy = 0.f;
         if (valid) {
           const int myk = p / a.Q, myq = p - myk * a.Q;
@@ -961,9 +941,9 @@ VPG_PRAGMA_UNROLL(VPG_TC2_CHUNK_UNROLL)
         sEx[kUb * 128 + p] = 0.f;
         sEx[kUxb * 128 + p] = ox;
         sEx[kUyb * 128 + p] = oy;
-        warp_atomic_max_abs(&sMax[kMx], ox);
-        warp_atomic_max_abs(&sMax[kMy], oy);
-      } else if (p < ncell) {
+        atomic_max_abs(&sMax[kMx], ox);
+        atomic_max_abs(&sMax[kMy], oy);
+      } else if (ug == 1 && p < ncell) {
         float s = 0.f, g = 0.f;
         for (int r = p * a.T; r < (p + 1) * a.T; ++r) {
           s += rsqv[r];
@@ -975,124 +955,11 @@ VPG_PRAGMA_UNROLL(VPG_TC2_CHUNK_UNROLL)
         }
       }
       mark(7);
-#else
-      // phase A: (tensor g, row r) dot products with (ux | uy | bx ux + by uy).
-      // Unit half 0 does tensors 0 and 2 (interleaved: two independent
-      // chains), half 1 tensor 1 (plus a discarded duplicate, keeping the
-      // loop uniform).  Each dot: four accumulators, combined in a fixed order.
-      {
-        const int r = p;
-        const bool rok = r < nrows_tile;
-        const int kk = rok ? r / a.T : 0;
-        const float* sv1 = (hh == 0 ? sEx + kUx * 128 : sEx + kUy * 128) + kk * a.Q;
-        const float* g1 = (hh == 0 ? T0 : T1) + (rok ? r : 0) * a.Q;
-        const bool two = hh == 0 && conv;
-        const float* sv2 = two ? cvr + kk * a.Q : sv1;
-        const float* g2 = two ? T2 + (rok ? r : 0) * a.Q : g1;
-        float a1[4] = {0.f, 0.f, 0.f, 0.f}, a2[4] = {0.f, 0.f, 0.f, 0.f};
-        int q = 0;
-#pragma unroll 2
-        for (; q + 3 < a.Q; q += 4) {
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            a1[u] = fmaf(g1[q + u], sv1[q + u], a1[u]);
-            a2[u] = fmaf(g2[q + u], sv2[q + u], a2[u]);
-          }
-        }
-        for (; q < a.Q; ++q) {
-          a1[0] = fmaf(g1[q], sv1[q], a1[0]);
-          a2[0] = fmaf(g2[q], sv2[q], a2[0]);
-        }
-        if (rok) {
-          part[hh * 128 + r] = (a1[0] + a1[1]) + (a1[2] + a1[3]);
-          if (two) part[256 + r] = (a2[0] + a2[1]) + (a2[2] + a2[3]);
-        }
-      }
-      __syncthreads();
-      // residuals r_j (losses.hpp:122-136)
-      if (hh == 0 && p < nrows_tile) {
-        const float gx = part[p], gy = part[128 + p];
-        float res = e_fixed * (gx + gy);
-        if (conv) res += part[256 + p];
-        res -= frow;
-        rsqv[p] = res * res;
-        const float rb = a.rscale * res;
-        rbarv[p] = rb;
-        rgev[p] = rb * (gx + gy);
-      }
-      __syncthreads();
-      mark(6);
-      // phase B: (tensor g, point) adjoint columns, same split as phase A;
-      // then half 1 does the per-cell sums in row order
-      {
-        const int pp = p;
-        const bool pok = pp < np;
-        const int myk = pok ? pp / a.Q : 0, myq = pok ? pp - myk * a.Q : 0;
-        const float* c1 = (hh == 0 ? T0 : T1) + myq;
-        const bool two = hh == 0 && conv;
-        const float* c2 = two ? T2 + myq : c1;
-        float b1[4] = {0.f, 0.f, 0.f, 0.f}, b2[4] = {0.f, 0.f, 0.f, 0.f};
-        int r = myk * a.T;
-        const int r1 = r + a.T;
-#pragma unroll 2
-        for (; r + 3 < r1; r += 4) {
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const float rb = rbarv[r + u];
-            b1[u] = fmaf(c1[(r + u) * a.Q], rb, b1[u]);
-            b2[u] = fmaf(c2[(r + u) * a.Q], rb, b2[u]);
-          }
-        }
-        for (; r < r1; ++r) {
-          b1[0] = fmaf(c1[r * a.Q], rbarv[r], b1[0]);
-          b2[0] = fmaf(c2[r * a.Q], rbarv[r], b2[0]);
-        }
-        if (pok) {
-          part[hh * 128 + pp] = (b1[0] + b1[1]) + (b1[2] + b1[3]);
-          if (two) part[256 + pp] = (b2[0] + b2[1]) + (b2[2] + b2[3]);
-        }
-      }
-      if (tid >= kNT - 64 && tid - (kNT - 64) < ncell) {
-        const int k = tid - (kNT - 64);
-        float s = 0.f, g = 0.f;
-        for (int r = k * a.T; r < (k + 1) * a.T; ++r) {
-          s += rsqv[r];
-          g += rgev[r];
-        }
-        cellv[k] = s;
-        cellv[64 + k] = g;
-      }
-      __syncthreads();
-      mark(7);
-      if (hh == 0) {
-        float ox = 0.f, oy = 0.f;
-        if (valid) {
-          ox = e_fixed * part[p];
-          oy = e_fixed * part[128 + p];
-          if (conv) {
-            const float tt = part[256 + p];
-            ox = fmaf(a.bx, tt, ox);
-            oy = fmaf(a.by, tt, oy);
-          }
-        }
-        sEx[kUb * 128 + p] = 0.f;
-        sEx[kUxb * 128 + p] = ox;
-        sEx[kUyb * 128 + p] = oy;
-        warp_atomic_max_abs(&sMax[kMx], ox);
-        warp_atomic_max_abs(&sMax[kMy], oy);
-      }
-      if (tid == 0) {
-        for (int k = 0; k < ncell; ++k) {
-          acc_v += (double)(cellv[k] * a.inv_nt);
-          acc_eg += (double)cellv[64 + k];
-        }
-      }
-#endif
     } else {
       // ---------- penalty tile (losses.hpp:389-415) ----------
       double sb = 0.0, ss = 0.0;
       float ubv = 0.f;
-      if (hh == 0 && valid) {
+      if (ug == 0 && valid) {
         const int pi = G.pbase + p - a.n_int;
         const float u = sEx[kU * 128 + p];
         if (pi < a.n_bnd) {
@@ -1110,11 +977,11 @@ VPG_PRAGMA_UNROLL(VPG_TC2_CHUNK_UNROLL)
         sb += __shfl_down_sync(0xffffffffu, sb, o);
         ss += __shfl_down_sync(0xffffffffu, ss, o);
       }
-      if (hh == 0) {
+      if (ug == 0) {
         sEx[kUb * 128 + p] = ubv;
         sEx[kUxb * 128 + p] = 0.f;
         sEx[kUyb * 128 + p] = 0.f;
-        warp_atomic_max_abs(&sMax[kMb], ubv);
+        atomic_max_abs(&sMax[kMb], ubv);
       }
       if (lane == 0 && warp < 4) {
         sRed[warp] = sb;
@@ -1166,10 +1033,10 @@ VPG_PRAGMA_UNROLL(VPG_TC2_CHUNK_UNROLL)
     {
       const float f1 = sSc[kScF1 + NL - 1];
       const float Ub = ub * sgv, Uxv = uxb * sgv, Uyv = uyb * sgv, Uxt = uxb * sgt, Uyt = uyb * sgt;
-VPG_PRAGMA_UNROLL(VPG_TC2_CHUNK_UNROLL)
+#pragma unroll 1
       for (int c = 0; c < 2; ++c) {
         float zs[8], dx[8], dy[8];
-        tc::tmem_ld1x8_wait(tmem + lane_q + kZ0 + u0 + 8 * c, zs);
+        tc::tmem_ld1x8_wait(tmem + lane_q + LY::kZ0 + u0 + 8 * c, zs);
         tc::tmem_ld2x8_wait(dcol(1, c), dcol(2, c), dx, dy);
         float v[8], gA[8], gX[8], gY[8];
 #pragma unroll
@@ -1195,19 +1062,19 @@ VPG_PRAGMA_UNROLL(VPG_TC2_CHUNK_UNROLL)
         }
         acc_units(v, kAWd, c);
         const uint32_t o = coff(c);
-        tc::st_split8_ho<false>(bufA, kPart, o, gA, 1.f);
-        tc::st_split8_ho<false>(bufA + kStream, kPart, o, gX, 1.f);
-        tc::st_split8_ho<false>(bufA + 2 * kStream, kPart, o, gY, 1.f);
+        if (row_ok) tc::st_split8_ho<false>(bufA, NB * kPart, o, gA, 1.f);
+        if (row_ok) tc::st_split8_ho<false>(bufA + kStream, NB * kPart, o, gX, 1.f);
+        if (row_ok) tc::st_split8_ho<false>(bufA + 2 * kStream, NB * kPart, o, gY, 1.f);
       }
     }
     operands_ready();
     // the parameter-gradient GEMM from the warp after the point-GEMM issuers
-    if (warp < VPG_TC2_ISSUE_WARPS) {
+    if (warp < 3) {
       mark(13);
       issue_point_gemm(false, NL, true);
       mark(14);
     }
-    if (warp == VPG_TC2_ISSUE_WARPS % 8) {
+    if (warp == 3) {
       issue_param_gemm(NL, pfirst, pshift);
       mark(15);
     }
@@ -1229,19 +1096,20 @@ VPG_PRAGMA_UNROLL(VPG_TC2_CHUNK_UNROLL)
       // propagation unscale ('), the state unscale and the store scale folded
       const float A0 = puv * sgv2, AT = it * put * sgv2, BT = put * sgt2;
       // l > 1: G of hidden l goes to buffer A and the recomputed hidden-1
-      // output to buffer B, so param GEMM l must have read both (bar_w)
-      // (param GEMM l is waited for per thread right before the first store,
-      // so the first chunk's G computation overlaps it)
-      cta_wait(bar_v, ph_v, bar_t, &ph_t, nullptr, nullptr);
-VPG_PRAGMA_UNROLL(VPG_TC2_CHUNK_UNROLL)
+      // output to buffer B, so param GEMM l must have read both (bar_w,
+      // waited for right before the first store, so the first chunk's G
+      // computation overlaps it)
+      mma_wait(bar_v, ph_v);
+      mma_wait(bar_t, ph_t);
+#pragma unroll 1
       for (int c = 0; c < 2; ++c) {
         float xa[8], xx[8], xy[8], z[8], tx[8], ty[8];
         tc::tmem_ld1x8_wait(dcol(0, c), xa);
         tc::tmem_ld2x8_wait(dcol(1, c), dcol(2, c), xx, xy);
         const uint32_t o = coff(c);
-        if (VPG_TC2_Z1_CACHE && l == 1) {
+        if (CF::kZCache && l == 1) {
           // hidden-1 state from the kept z: tangents s1 * w0 (scaled like X_1)
-          tc::tmem_ld1x8_wait(tmem + lane_q + kZ1 + u0 + 8 * c, z);
+          tc::tmem_ld1x8_wait(tmem + lane_q + LY::kZ1 + u0 + 8 * c, z);
 #pragma unroll
           for (int k = 0; k < 8; k += 2) {
             const float4 ws = *reinterpret_cast<const float4*>(sW0s + 2 * (u0 + 8 * c + k));
@@ -1253,12 +1121,12 @@ VPG_PRAGMA_UNROLL(VPG_TC2_CHUNK_UNROLL)
             ty[k + 1] = b2.y;
           }
         } else {
-          if (VPG_TC2_Z1_CACHE && D == 3 && l == 2)
-            tc::tmem_ld1x8_wait(tmem + lane_q + kZ2 + u0 + 8 * c, z);  // kept hidden-2 z
+          if (CF::kZCache && D == 3 && l == 2)
+            tc::tmem_ld1x8_wait(tmem + lane_q + LY::kZ2 + u0 + 8 * c, z);  // kept hidden-2 z
           else
-            tc::ld_join8_ho<true>(bufB, kPart, o, iv, z);
-          tc::ld_join8_ho<false>(bufB + kStream, kPart, o, 1.f, tx);
-          tc::ld_join8_ho<false>(bufB + 2 * kStream, kPart, o, 1.f, ty);
+            tc::ld_join8_ho<true>(bufB, NB * kPart, o, iv, z);
+          tc::ld_join8_ho<false>(bufB + kStream, NB * kPart, o, 1.f, tx);
+          tc::ld_join8_ho<false>(bufB + 2 * kStream, NB * kPart, o, 1.f, ty);
         }
         float ga[8], gx[8], gy[8];
 #pragma unroll
@@ -1293,16 +1161,16 @@ VPG_PRAGMA_UNROLL(VPG_TC2_CHUNK_UNROLL)
             ph_w ^= 1u;
             tc::fence_after_sync();
           }
-          tc::st_split8_ho<false>(bufA, kPart, o, ga, 1.f);
-          tc::st_split8_ho<false>(bufA + kStream, kPart, o, gx, 1.f);
-          tc::st_split8_ho<false>(bufA + 2 * kStream, kPart, o, gy, 1.f);
+          if (row_ok) tc::st_split8_ho<false>(bufA, NB * kPart, o, ga, 1.f);
+          if (row_ok) tc::st_split8_ho<false>(bufA + kStream, NB * kPart, o, gx, 1.f);
+          if (row_ok) tc::st_split8_ho<false>(bufA + 2 * kStream, NB * kPart, o, gy, 1.f);
           store_x1(bufB, c, px, py, true);  // hidden-1 output rebuilt (l - 1 == 1)
         }
       }
       if (l > 1) {
         operands_ready();
-        if (warp < VPG_TC2_ISSUE_WARPS) issue_point_gemm(false, l - 1, true);
-        if (warp == VPG_TC2_ISSUE_WARPS % 8) issue_param_gemm(l - 1, pfirst2, pshift2);
+        if (warp < 3) issue_point_gemm(false, l - 1, true);
+        if (warp == 3) issue_param_gemm(l - 1, pfirst2, pshift2);
         bGv = bv2;
         bGt = bt2;
         puv = puv2;
@@ -1310,7 +1178,7 @@ VPG_PRAGMA_UNROLL(VPG_TC2_CHUNK_UNROLL)
       }
       mark(9 + NL - l + 1);
     }
-    cta_wait(bar_w, ph_w, nullptr, nullptr, nullptr, nullptr);  // last param GEMM done: buffers A / B free
+    mma_wait(bar_w, ph_w);  // last param GEMM done: buffers A / B free
     mark(12);
     ++ph_tile;
   }
@@ -1321,24 +1189,25 @@ VPG_PRAGMA_UNROLL(VPG_TC2_CHUNK_UNROLL)
     __syncthreads();
     if (warp == 0) {
       tc::fence_after_sync();
-      tc::tmem_dealloc(tmem, kCols);
+      tc::tmem_dealloc(tmem, CF::kCols);
     }
     return;
   }
-  // parameter-gradient accumulators (TMEM lanes 0..63 = G rows h | l, columns
-  // 0..63 = X parts h | l), unscaled by 2^-kacc, plus any spilled part ->
-  // smem [64][65] (buffer A is free) -> the four-block sum
+  // parameter-gradient accumulators (G rows h | l x X columns h | l),
+  // unscaled by 2^-kacc, plus any spilled part -> smem [2HP][2HP + 1]
+  // (buffer A is free) -> the four-block sum
+  constexpr int SS = 2 * HP + 1;
   float* scr = reinterpret_cast<float*>(bufA);
   for (int l = 1; l <= NL; ++l) {
     const int kacc = (l == 1) ? kacc0 : kacc1;
     const bool has = (l == 1) ? has0 : has1, spill = (l == 1) ? spill0 : spill1;
-    const float* S = a.tc_scratch + ((size_t)blockIdx.x * NL + (l - 1)) * kScratchPerLayer;
+    const float* S = a.tc_scratch + ((size_t)blockIdx.x * NL + (l - 1)) * CF::kScratch;
     tc::fence_after_sync();
-    if ((VPG_TC2_PARAM_M64 || (warp & 3) < 2) && has) {
+    if (has) {
       const float inv = tc::exp2i(-kacc);
 #pragma unroll 1
       for (int h2 = 0; h2 < 2; ++h2) {
-        const int col0 = 32 * hh + 16 * h2;
+        const int col0 = col_base + 16 * h2;
         float v[16];
         tc::tmem_ld1x16_wait(gacc_ld(l) + col0, v);
         const int grow = gacc_row(l);
@@ -1346,8 +1215,8 @@ VPG_PRAGMA_UNROLL(VPG_TC2_CHUNK_UNROLL)
 #pragma unroll
           for (int k = 0; k < 16; ++k) {
             float x = v[k] * inv;
-            if (spill) x += S[(col0 + k) * 64 + grow];
-            scr[grow * 65 + col0 + k] = x;
+            if (spill) x += S[(col0 + k) * (2 * HP) + grow];
+            scr[grow * SS + col0 + k] = x;
           }
         }
       }
@@ -1355,19 +1224,19 @@ VPG_PRAGMA_UNROLL(VPG_TC2_CHUNK_UNROLL)
     tc::fence_before_sync();
     __syncthreads();
     const int fo = net.out_w[l], fi = net.in_w[l];
-    for (int e = tid; e < fo * (fi + 1); e += kNT) {
+    for (int e = tid; e < fo * (fi + 1); e += NT) {
       const int o = e / (fi + 1), i = e - o * (fi + 1);
       const int c = i < fi ? i : H;  // the bias gradient is the constant unit's column
       float g = 0.f;
-      if (has)  // scr[row][col]: row = G part * 32 + o, col = X part * 32 + c
-        g = ((scr[o * 65 + c] + scr[o * 65 + 32 + c]) + scr[(32 + o) * 65 + c]) + scr[(32 + o) * 65 + 32 + c];
+      if (has)  // scr[row][col]: row = G part * HP + o, col = X part * HP + c
+        g = ((scr[o * SS + c] + scr[o * SS + HP + c]) + scr[(HP + o) * SS + c]) + scr[(HP + o) * SS + HP + c];
       const int idx = (i < fi) ? net.w_off[l] + o * fi + i : net.b_off[l] + o;
       a.grad_part[(size_t)idx * a.part_stride + blockIdx.x] = g;
     }
     __syncthreads();
   }
   // CUDA-core gradients: per-warp sums combined in warp order
-  for (int u = tid; u <= H; u += kNT) {
+  for (int u = tid; u <= H; u += NT) {
     const int h2 = u >> 4, j = u & 15;
     float w0x = 0.f, w0y = 0.f, b0 = 0.f, wd = 0.f;
     for (int w = 4 * h2; w < 4 * h2 + 4; ++w) {
@@ -1399,7 +1268,9 @@ VPG_PRAGMA_UNROLL(VPG_TC2_CHUNK_UNROLL)
   if constexpr (VPG_PHASE_CLOCK != 0)
     if (a.phase_clk != nullptr && tid == 0 && blockIdx.x < 1024)
       a.phase_clk[kPhaseTiles * kPhaseMarks + 3 * blockIdx.x + 1] = (long long)globaltimer();
+  double acc_v = 0.0, acc_eg = 0.0;
   {
+    constexpr int NW = NT / 32;
     double v = cell_v, g = cell_eg;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
@@ -1409,13 +1280,13 @@ VPG_PRAGMA_UNROLL(VPG_TC2_CHUNK_UNROLL)
     __syncthreads();  // sRed is free
     if (lane == 0) {
       sRed[warp] = v;
-      sRed[8 + warp] = g;
+      sRed[NW + warp] = g;
     }
     __syncthreads();
     if (tid == 0)
-      for (int w = 0; w < kNT / 32; ++w) {
+      for (int w = 0; w < NW; ++w) {
         acc_v += sRed[w];
-        acc_eg += sRed[8 + w];
+        acc_eg += sRed[NW + w];
       }
   }
   if (tid == 0) {
@@ -1431,13 +1302,13 @@ VPG_PRAGMA_UNROLL(VPG_TC2_CHUNK_UNROLL)
   __syncthreads();
   if (warp == 0) {
     tc::fence_after_sync();
-    tc::tmem_dealloc(tmem, kCols);
+    tc::tmem_dealloc(tmem, CF::kCols);
   }
 }
 
 template <int H, int D>
 __host__ __device__ constexpr size_t tc2_step_smem_bytes() {
-  return t2::Lay<D>::BYTES;
+  return t2::Lay<H, D>::BYTES;
 }
 
 }  // namespace vpg

@@ -13,13 +13,15 @@ using StepFn = void (*)(StepArgs);
 
 struct Variant {
   int H, D, C, ACT;
-  StepFn fused, forward, reverse;
-  StepFn tc;       // tensor-core fused step (tc_step_kernel.cuh), nullptr if the shape has none
-  size_t tc_smem;
-  StepFn tc2;      // fp16-split two-CTA tensor-core step (tc2_step_kernel.cuh), nullptr if none
+  StepFn fused, forward, reverse;  // CUDA-core step (step_kernel.cuh): every shape
+  StepFn tc2;      // tensor-core step (tc2_step_kernel.cuh), nullptr if the shape has none
   StepFn tc2_fwd;  // its forward-only / reverse-only modes (split path, evaluate)
   StepFn tc2_rev;
   size_t tc2_smem;
+  int tc2_nt;        // threads per CTA
+  int tc2_mp;        // points per tile
+  int tc2_buf;       // bytes of one operand buffer (the slab aliases buffer A)
+  int tc2_scratch;   // floats of the per-CTA spill scratch per MMA layer
   int off_union;  // floats before the union
   int rev_need;   // floats the reverse phase needs in the union
   size_t (*smem)(int, int);
@@ -39,13 +41,12 @@ VPG_VARIANTS(VPG_DECL)
 
 #ifdef VPG_DEFINE_VARIANT
 }  // namespace vpg
-#include "tc_step_kernel.cuh"
 #include "tc2_step_kernel.cuh"
 namespace vpg {
 template <int H, int D, int C, int A>
 Variant make_variant() {
   using LY = Layout<H, D, C>;
-  Variant v;
+  Variant v{};
   v.H = H;
   v.D = D;
   v.C = C;
@@ -56,20 +57,16 @@ Variant make_variant() {
   v.off_union = LY::OFF_UNION;
   v.rev_need = LY::REV_NEED;
   v.smem = [](int u, int r) { return step_smem_bytes<H, D, C>(u, r); };
-  if constexpr (C == 1 && (D == 2 || D == 3) && H <= 31) {
-    v.tc = tc_step_kernel<H, D, A, kTcNQ>;
-    v.tc_smem = tc_step_smem_bytes<H, D>();
+  if constexpr (C == 1 && (D == 2 || D == 3) && H <= 63) {
+    using CF = t2::Cfg<H>;
     v.tc2 = tc2_step_kernel<H, D, A, kModeFused>;
     v.tc2_fwd = tc2_step_kernel<H, D, A, kModeForward>;
     v.tc2_rev = tc2_step_kernel<H, D, A, kModeReverse>;
     v.tc2_smem = tc2_step_smem_bytes<H, D>();
-  } else {
-    v.tc = nullptr;
-    v.tc_smem = 0;
-    v.tc2 = nullptr;
-    v.tc2_fwd = nullptr;
-    v.tc2_rev = nullptr;
-    v.tc2_smem = 0;
+    v.tc2_nt = CF::NT;
+    v.tc2_mp = CF::MP;
+    v.tc2_buf = CF::kBuf;
+    v.tc2_scratch = CF::kScratch;
   }
   return v;
 }

@@ -3,6 +3,7 @@
 #include <dlfcn.h>
 
 #include <algorithm>
+#include <atomic>
 #include <utility>
 #include <condition_variable>
 #include <thread>
@@ -28,7 +29,6 @@
 #include "contract_mf.cuh"
 #include "sf_step.h"
 #include "tc_selftest.cuh"
-#include "tc_step_kernel.cuh"
 #include "tc2_step_kernel.cuh"
 #include "variant.h"
 #include "vpinn_gpu.h"
@@ -36,6 +36,9 @@
 namespace {
 
 thread_local std::string g_err;
+
+// vpinn_gpu_set_test_hooks: read by every later vpinn_gpu_create
+std::atomic<int> g_test_hooks{0};
 
 struct Fail {
   int code;
@@ -132,7 +135,6 @@ struct CopyPool {
   CopyPool() {
     const unsigned hc = std::thread::hardware_concurrency();
     n = std::max(1, std::min(8, (int)(hc ? hc / 2 : 1)));
-    if (const char* e = std::getenv("VPINN_COPY_THREADS")) n = std::max(1, std::min(32, std::atoi(e)));
     for (int i = 1; i < n; ++i) workers.emplace_back([this, i] { loop(i); });
     for (auto& w : workers) w.detach();
   }
@@ -227,7 +229,7 @@ Stager& stager() {
   return *st;
 }
 void upload_bytes(void* dst, const void* src, size_t bytes, cudaStream_t s) {
-  if (bytes >= (size_t(4) << 20) && !std::getenv("VPINN_NO_STAGING") && stager().upload(dst, src, bytes, s)) return;
+  if (bytes >= (size_t(4) << 20) && stager().upload(dst, src, bytes, s)) return;
   CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s));
 }
 
@@ -449,7 +451,6 @@ struct vpinn_gpu_ctx {
   long long aborted_at = 0;
   // step configuration
   bool split = false;
-  bool tc = false;  // tensor-core fused step
   std::string kernel_name;  // the epoch's dominant kernel (diagnostics)
   vpg::StepArgs sargs{};  // template (fused or reverse)
   int grid_step = 0;
@@ -463,7 +464,8 @@ struct vpinn_gpu_ctx {
   int cw_warps = 8;  // warps per CTA of the warp-per-cell contraction
   bool cw_fixed = false;  // its 5x5 / 5x5 compile-time-shape variant
   size_t smem_cc = 0;
-  int grid_contract = 0, grid_pen = 0, grid_fwd = 0;
+  int grid_contract = 0, grid_pen = 0, grid_fwd = 0, grid_creduce = 0;
+  DBuf<float> cpart;  // row-block contraction partial adjoint columns
   size_t smem_contract = 0, smem_fwd = 0;
   // graphs
   std::map<std::tuple<int, int, double>, cudaGraphExec_t> graphs;
@@ -539,7 +541,6 @@ void configure_strong(vpinn_gpu_ctx* c) {
   int optin = 0;
   CK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, c->device));
   int w = vpg::kSfMaxWarps;
-  if (const char* e = std::getenv("VPINN_SF_WARPS")) w = std::max(1, std::min(vpg::kSfMaxWarps, std::atoi(e)));
   while (w > 1 && vpg::sf_smem_bytes(D, w) > (size_t)optin) --w;
   if (vpg::sf_smem_bytes(D, w) > (size_t)optin) throw Fail{VPINN_ERR_CONFIG, "strong-form kernel does not fit shared memory"};
   c->sf_warps = w;
@@ -615,28 +616,31 @@ void configure(vpinn_gpu_ctx* c) {
 
   const size_t two_cta = 113 * 1024;
   int occ = 0;
+  // CTAs per SM of a tensor-core step kernel: two when two of them fit the
+  // SM's shared memory (width class 32: 113 KB, 256 TMEM columns each), else
+  // one (width class 64: ~212 KB, all 512 TMEM columns).  The occupancy query
+  // reports 1 for tcgen05 kernels; the hardware co-schedules 2 (measured).
+  auto tc2_ctas_per_sm = [&](size_t smem) {
+    int smsm = 0, resv = 0;
+    CK(cudaDeviceGetAttribute(&smsm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, c->device));
+    CK(cudaDeviceGetAttribute(&resv, cudaDevAttrReservedSharedMemoryPerBlock, c->device));
+    return 2 * (smem + resv) <= (size_t)smsm ? 2 : 1;
+  };
   if (!c->split) {
-    a.cells_per_tile = std::max(1, vpg::kThreads / c->Q);
+    // tensor-core step: whole-cell tiles of at most tc2_mp points, the tile's
+    // slab plus its contraction scratch in operand buffer A
+    const int tc_cells = V.tc2 ? std::max(1, V.tc2_mp / c->Q) : 1;
+    const int tc_rows = tc_cells * c->T;
+    c->tc2 = V.tc2 != nullptr && !(g_test_hooks.load() & VPINN_HOOK_CUDA_CORE_STEP) &&
+             c->eps_source != VPINN_EPS_SPATIAL && c->Q >= 2 && c->Q <= V.tc2_mp &&
+             tc_rows <= 128 &&
+             (size_t)(c->nt * round4(tc_rows * c->Q + 8) + vpg::t2::kTailFloats) * sizeof(float) <=
+                 (size_t)V.tc2_buf;
+    a.cells_per_tile = std::max(1, (c->tc2 ? V.tc2_mp : vpg::kThreads) / c->Q);
     a.n_int_tiles = c->E ? ceil_div(c->E, a.cells_per_tile) : 0;
-    a.n_tiles = a.n_int_tiles + ceil_div(c->n_bnd + c->n_sen, vpg::kThreads);
+    a.n_tiles = a.n_int_tiles + ceil_div(c->n_bnd + c->n_sen, c->tc2 ? V.tc2_mp : vpg::kThreads);
     const int tile_rows = a.cells_per_tile * c->T;
-    // tensor-core step: whole-tile slab in one of its operand buffers
-    const char* tc_env = std::getenv("VPINN_TC");
-    c->tc = V.tc != nullptr && !(tc_env && std::atoi(tc_env) == 0) && c->eps_source != VPINN_EPS_SPATIAL &&
-            c->Q >= 2 && tile_rows <= 128 && (size_t)c->nt * round4(tile_rows * c->Q + 8) * sizeof(float) <= (size_t)vpg::kTcBuf;
-    // the fp16-split two-CTA kernel (default) when the slab plus its
-    // contraction scratch fit operand buffer A; VPINN_TC_KERNEL=1 selects the
-    // bf16-split one-CTA kernel
-    const char* tck = std::getenv("VPINN_TC_KERNEL");
-    c->tc2 = c->tc && V.tc2 != nullptr && !(tck && std::atoi(tck) == 1) && c->Q >= 2 &&
-             (size_t)(c->nt * round4(tile_rows * c->Q + 8) + vpg::t2::kTailFloats) * sizeof(float) <=
-                 (size_t)vpg::t2::kBuf;
-    // the bf16-split kernel assumes every hidden layer exactly H wide; ragged
-    // widths go to tc2 (zero-padded exactly) or the CUDA-core step
-    bool uniform = c->net.in_w[c->net.n_layers - 1] == V.H;
-    for (int l = 0; l + 1 < c->net.n_layers; ++l) uniform = uniform && c->net.out_w[l] == V.H;
-    if (c->tc && !c->tc2 && !uniform) c->tc = false;
-    if (c->tc && (std::getenv("VPINN_PHASE_CLOCK") && std::atoi(std::getenv("VPINN_PHASE_CLOCK")) != 0)) {
+    if (c->tc2 && (std::getenv("VPINN_PHASE_CLOCK") && std::atoi(std::getenv("VPINN_PHASE_CLOCK")) != 0)) {
       c->phase_clk.alloc((size_t)vpg::kPhaseTiles * vpg::kPhaseMarks + 3 * 1024, c->stream);
       a.phase_clk = c->phase_clk.p;
     }
@@ -648,56 +652,16 @@ void configure(vpinn_gpu_ctx* c) {
       c->smem_step = V.tc2_smem;
       CK(cudaFuncSetAttribute(V.tc2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem_step));
       CK(cudaFuncSetAttribute(V.tc2, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, V.tc2, vpg::t2::kNT, c->smem_step));
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, V.tc2, V.tc2_nt, c->smem_step));
       if (occ < 1) throw Fail{VPINN_ERR_DEVICE, "tc2 step kernel cannot be resident"};
-      if (std::getenv("VPINN_DEBUG")) {
-        cudaFuncAttributes fa{};
-        CK(cudaFuncGetAttributes(&fa, V.tc2));
-        int smsm = 0, resv = 0;
-        CK(cudaDeviceGetAttribute(&smsm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, c->device));
-        CK(cudaDeviceGetAttribute(&resv, cudaDevAttrReservedSharedMemoryPerBlock, c->device));
-        for (size_t sb : {(size_t)0, (size_t)64 * 1024, (size_t)100 * 1024, (size_t)110 * 1024, (size_t)112 * 1024}) {
-          int o2 = 0;
-          CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o2, V.tc2, vpg::t2::kNT, sb));
-          std::fprintf(stderr, "  occ(smem %zu) = %d\n", sb, o2);
-        }
-        std::fprintf(stderr, "tc2: regs %d static smem %zu local %zu dyn %zu maxdyn %d; SM smem %d reserved %d; occ %d\n",
-                     fa.numRegs, fa.sharedSizeBytes, fa.localSizeBytes, c->smem_step, fa.maxDynamicSharedSizeBytes, smsm,
-                     resv, occ);
-      }
-      // two CTAs per SM by design (113 KB smem, 256 TMEM columns, 120
-      // registers); the occupancy query reports 1 for tcgen05 kernels, the
-      // hardware co-schedules 2 (measured)
-      {
-        int smsm = 0, resv = 0;
-        CK(cudaDeviceGetAttribute(&smsm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, c->device));
-        CK(cudaDeviceGetAttribute(&resv, cudaDevAttrReservedSharedMemoryPerBlock, c->device));
-        if (2 * (c->smem_step + resv) <= (size_t)smsm) occ = 2;
-      }
-      if (const char* e = std::getenv("VPINN_TC2_CTAS")) occ = std::max(1, std::atoi(e));
+      occ = tc2_ctas_per_sm(c->smem_step);
       c->grid_step = std::max(1, std::min(a.n_tiles, occ * c->sm_count));
-      c->tc_scratch.alloc((size_t)c->grid_step * (V.D - 1) * vpg::t2::kScratchPerLayer, c->stream);
+      c->tc_scratch.alloc((size_t)c->grid_step * (V.D - 1) * V.tc2_scratch, c->stream);
       a.tc_scratch = c->tc_scratch.p;
-      if (const char* e = std::getenv("VPINN_TC2_FORCE_SPILL")) a.tc_force_spill = std::atoi(e);
+      a.tc_force_spill = (g_test_hooks.load() & VPINN_HOOK_FORCE_SPILL) ? 1 : 0;
       c->kernel_name = "tc2_step_kernel<" + std::to_string(V.H) + "," + std::to_string(V.D) + "," +
-                       (V.ACT ? "sigmoid" : "tanh") + "> (fp16 split, " + std::to_string(occ) + " CTAs/SM)";
-    } else if (c->tc) {
-      a.chunk_rows = tile_rows;
-      a.tstride = round4(tile_rows * c->Q + 8);
-      a.stage_floats = c->nt * a.tstride;
-      // a dedicated slab region when it fits next to the operand buffers
-      // (prefetched one tile ahead), else the slab aliases a free buffer
-      const size_t slab_bytes = sizeof(float) * (size_t)a.stage_floats;
-      const size_t tc_limit = (size_t)227 * 1024 - 1024;  // - static shared
-      a.union_floats = (V.tc_smem + slab_bytes <= tc_limit) ? a.stage_floats : 0;
-      if (const char* e = std::getenv("VPINN_TC_SLAB")) if (std::atoi(e) == 0) a.union_floats = 0;
-      c->smem_step = V.tc_smem + sizeof(float) * (size_t)a.union_floats;
-      CK(cudaFuncSetAttribute(V.tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem_step));
-      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, V.tc, 128 * vpg::kTcNQ, c->smem_step));
-      if (occ < 1) throw Fail{VPINN_ERR_DEVICE, "tensor-core step kernel cannot be resident"};
-      c->grid_step = std::max(1, std::min(a.n_tiles, c->sm_count));
-      c->kernel_name = "tc_step_kernel<" + std::to_string(V.H) + "," + std::to_string(V.D) + "," +
-                       (V.ACT ? "sigmoid" : "tanh") + ">" + (a.union_floats ? " (dedicated slab)" : " (aliased slab)");
+                       (V.ACT ? "sigmoid" : "tanh") + "> (fp16 split, " + std::to_string(V.tc2_nt) + " threads, " +
+                       std::to_string(occ) + " CTA" + (occ > 1 ? "s" : "") + "/SM)";
     } else {
       c->kernel_name = "step_kernel<" + std::to_string(V.H) + "," + std::to_string(V.D) + "," + std::to_string(V.C) +
                        "," + (V.ACT ? "sigmoid" : "tanh") + ",fused> (CUDA cores)";
@@ -751,28 +715,23 @@ void configure(vpinn_gpu_ctx* c) {
   }
 
   // ---- tc2 forward / reverse modes (split path, evaluate): any point
-  // count, tanh or sigmoid, 2-3 hidden layers of width <= 31, one output ----
+  // count, tanh or sigmoid, 2-3 hidden layers of width <= 63, one output ----
   {
-    const char* tck = std::getenv("VPINN_TC_KERNEL");
-    const char* tc_env = std::getenv("VPINN_TC");
-    c->tc2_modes = V.tc2_fwd != nullptr && !(tc_env && std::atoi(tc_env) == 0) && !(tck && std::atoi(tck) == 1) &&
+    c->tc2_modes = V.tc2_fwd != nullptr && !(g_test_hooks.load() & VPINN_HOOK_CUDA_CORE_STEP) &&
                    c->eps_source != VPINN_EPS_SPATIAL;
     if (c->tc2_modes) {
       for (vpg::StepFn fn : {V.tc2_fwd, V.tc2_rev}) {
         CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)V.tc2_smem));
         CK(cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
       }
-      int smsm = 0, resv = 0;
-      CK(cudaDeviceGetAttribute(&smsm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, c->device));
-      CK(cudaDeviceGetAttribute(&resv, cudaDevAttrReservedSharedMemoryPerBlock, c->device));
-      c->grid_tc2 = (2 * (V.tc2_smem + resv) <= (size_t)smsm ? 2 : 1) * c->sm_count;
+      c->grid_tc2 = tc2_ctas_per_sm(V.tc2_smem) * c->sm_count;
       if (c->split) {
         // the reverse stage on the tensor cores
-        a.n_tiles = ceil_div(P_local, 128);
+        a.n_tiles = ceil_div(P_local, V.tc2_mp);
         c->smem_step = V.tc2_smem;
         c->grid_step = std::max(1, std::min(a.n_tiles, c->grid_tc2));
         c->grad_rows = c->grid_step;
-        c->tc_scratch.alloc((size_t)c->grid_step * (V.D - 1) * vpg::t2::kScratchPerLayer, c->stream);
+        c->tc_scratch.alloc((size_t)c->grid_step * (V.D - 1) * V.tc2_scratch, c->stream);
         a.tc_scratch = c->tc_scratch.p;
         c->kernel_name = "tc2_step_kernel<" + std::to_string(V.H) + "," + std::to_string(V.D) + "," +
                          (V.ACT ? "sigmoid" : "tanh") + ",reverse> (split path, fp16 split)";
@@ -802,30 +761,39 @@ void configure(vpinn_gpu_ctx* c) {
     ca.by = c->by;
     ca.rscale = a.rscale;
     ca.inv_nt = a.inv_nt;
-    ca.cells_per_tile = std::max(1, std::min(1024, 1024 / std::max(1, c->Q)));
-    ca.cells_per_tile = std::max(1, std::min(ca.cells_per_tile, c->E));
-    ca.n_tiles = c->E ? ceil_div(c->E, ca.cells_per_tile) : 0;
-    ca.pmax = round4(ca.cells_per_tile * c->Q);  // a stride: keeps the mbarriers after the vectors 8-byte aligned
-    ca.nstage = 4;
-    const size_t fixed = vpg::contract_smem_bytes(ca.pmax, 0, 0, ca.nstage);
-    const size_t ring_budget = fixed < 200 * 1024 ? 200 * 1024 - fixed : 16 * 1024;
-    const size_t stage_bytes = ring_budget / ca.nstage;
-    ca.chunk_rows = (int)std::max<size_t>(1, stage_bytes / ((size_t)c->nt * (c->Q * 4 + 32)));
-    ca.chunk_rows = std::min(ca.chunk_rows, ca.cells_per_tile * c->T);
-    ca.tstride = round4(ca.chunk_rows * c->Q + 8);
+    // two ring stages of R rows (as many as fit ~200 KB, <= 16); items =
+    // (cell, segment of seg_rows rows), about four per CTA, contiguous ranges
+    if (c->split && c->Q > vpg::kCQMax)
+      throw Fail{VPINN_ERR_CONFIG, "contraction: more than 8,192 quadrature points per cell"};
+    ca.qstride = round4(c->Q);
+    const size_t row_bytes = sizeof(float) * (size_t)c->nt * c->Q;
+    const size_t fixed = sizeof(float) * (3 + (size_t)c->nt) * ca.qstride + 1024;
+    const size_t ring_budget = (size_t)200 * 1024 > fixed ? (size_t)200 * 1024 - fixed : 0;
+    // a 2-deep ring of R-row stages (measured on C3 40x40: 2 x 6 rows 41.7 us,
+    // 4 x 3 rows 63.9 us -- each stage costs three CTA barriers and a serial
+    // row-finish step, so fewer, larger stages win)
+    ca.nstage = 2;
+    ca.rows = (int)std::max<size_t>(1, std::min<size_t>({(size_t)vpg::kCRowsMax, (size_t)c->T,
+                                                         ring_budget / (ca.nstage * row_bytes + 64)}));
+    ca.tstride = round4(ca.rows * c->Q + 8);
     ca.stage_floats = c->nt * ca.tstride;
-    c->smem_contract = vpg::contract_smem_bytes(ca.pmax, ca.chunk_rows, ca.stage_floats, ca.nstage);
-    if (c->smem_contract > (size_t)227 * 1024) {
-      ca.nstage = 2;
-      c->smem_contract = vpg::contract_smem_bytes(ca.pmax, ca.chunk_rows, ca.stage_floats, ca.nstage);
-    }
+    c->smem_contract = vpg::contract_rows_smem_bytes(ca.stage_floats, ca.qstride, c->nt, ca.nstage);
     if (c->smem_contract > (size_t)227 * 1024)
       throw Fail{VPINN_ERR_CONFIG, "contraction kernel does not fit shared memory"};
-    CK(cudaFuncSetAttribute(vpg::contract_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    CK(cudaFuncSetAttribute(vpg::contract_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)c->smem_contract));
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, vpg::contract_kernel, vpg::kCThreads,
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, vpg::contract_rows_kernel, vpg::kCRThreads,
                                                      c->smem_contract));
-    c->grid_contract = std::max(1, std::min(std::max(1, ca.n_tiles), std::max(1, occ) * c->sm_count));
+    const int ctas = std::max(1, occ) * c->sm_count;
+    const long long rows_total = (long long)c->E * c->T;
+    const int seg = (int)std::min<long long>(c->T, std::max<long long>(1, (rows_total + 4 * ctas - 1) / (4 * ctas)));
+    ca.seg_rows = std::min(c->T, ceil_div(seg, ca.rows) * ca.rows);
+    ca.items_per_cell = ceil_div(c->T, ca.seg_rows);
+    ca.n_items = c->E * ca.items_per_cell;
+    c->grid_contract = std::max(1, std::min(ca.n_items, ctas));
+    c->grid_creduce = std::max(1, std::min(ceil_div(c->E * c->Q, 256), 4 * c->sm_count));
+    c->cpart.alloc((size_t)ca.n_items * 3 * ca.qstride, c->stream);
+    ca.part = c->cpart.p;
     c->grid_pen = (c->n_bnd + c->n_sen) ? std::min(64, ceil_div(c->n_bnd + c->n_sen, 256)) : 0;
   }
   // ---- whole-cell HBM-streaming contraction (warp per cell) ----
@@ -853,17 +821,14 @@ void configure(vpinn_gpu_ctx* c) {
     // the most warps per CTA (8 / 12 / 16) with a >= 2-stage ring each
     const size_t budget = (size_t)227 * 1024 - 1024;
     int nw = 16, ns = 2;
-    if (const char* e = std::getenv("VPINN_CW_STAGES")) ns = std::max(2, std::min(vpg::kCCMaxStages, std::atoi(e)));
     while (nw > 8 && vpg::cell_warp_smem_bytes(nw, cc.stage_floats, ns, c->T, c->Q) > budget) nw -= 4;
-    if (const char* e = std::getenv("VPINN_CW_WARPS")) nw = std::atoi(e) >= 16 ? 16 : (std::atoi(e) >= 12 ? 12 : 8);
     cc.nstage = ns;
     c->cw_warps = nw;
     c->smem_cc = vpg::cell_warp_smem_bytes(nw, cc.stage_floats, cc.nstage, c->T, c->Q);
     if (c->smem_cc > budget) {
       c->cell_contract = false;  // cell larger than a warp's ring: row-chunked kernel
     } else {
-      const char* fx = std::getenv("VPINN_CW_FIXED");
-      c->cw_fixed = c->T == 25 && c->Q == 25 && !(fx && std::atoi(fx) == 0);
+      c->cw_fixed = c->T == 25 && c->Q == 25;
       const void* fn = cw_kernel(nw, c->cw_fixed);
       CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem_cc));
       CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, 32 * nw, c->smem_cc));
@@ -919,24 +884,16 @@ void launch_k(bool pdl, void (*k)(KArgs...), int grid, int block, size_t smem, c
   CK(cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...));
 }
 
-// off by default: A/B on the gear, PDL made the weak epoch 1.3% slower (the
-// early-resident successor CTAs skew the step kernel's CTA placement) and
-// the strong epoch 0.1% faster; VPINN_PDL=1 enables it
-bool pdl_enabled() {
-  static const bool on = [] {
-    const char* e = std::getenv("VPINN_PDL");
-    return e && std::atoi(e) != 0;
-  }();
-  return on;
-}
+// programmatic dependent launch stays off: A/B on the gear, PDL made the weak
+// epoch 1.3% slower (the early-resident successor CTAs skew the step
+// kernel's CTA placement) and the strong epoch 0.1% faster
+constexpr bool pdl_enabled() { return false; }
 
 void launch_fused(vpinn_gpu_ctx* c, const vpg::StepArgs& a) {
   if (c->strong)
     launch_k(pdl_enabled(), c->sfk.fused, c->grid_step, 32 * c->sf_warps, c->smem_step, c->stream, a);
   else if (c->tc2)
-    launch_k(pdl_enabled(), c->var.tc2, c->grid_step, vpg::t2::kNT, c->smem_step, c->stream, a);
-  else if (c->tc)
-    c->var.tc<<<c->grid_step, 128 * vpg::kTcNQ, c->smem_step, c->stream>>>(a);
+    launch_k(pdl_enabled(), c->var.tc2, c->grid_step, c->var.tc2_nt, c->smem_step, c->stream, a);
   else
     c->var.fused<<<c->grid_step, vpg::kThreads, c->smem_step, c->stream>>>(a);
   CK(cudaGetLastError());
@@ -944,6 +901,17 @@ void launch_fused(vpinn_gpu_ctx* c, const vpg::StepArgs& a) {
 }
 
 // ---- one epoch: loss + gradient (+ Adam) enqueued on the context stream ----
+// row-block contraction (cells larger than a warp's ring): items, then the
+// fixed-order reduction of their partial adjoint columns
+void launch_contract_rows(vpinn_gpu_ctx* c, const vpg::ContractArgs& ca) {
+  if (ca.n_items <= 0) return;
+  vpg::contract_rows_kernel<<<c->grid_contract, vpg::kCRThreads, c->smem_contract, c->stream>>>(ca);
+  CK(cudaGetLastError());
+  vpg::contract_rows_reduce_kernel<<<c->grid_creduce, 256, 0, c->stream>>>(ca);
+  CK(cudaGetLastError());
+  c->launches += 2;
+}
+
 void enqueue_grad(vpinn_gpu_ctx* c, const int* stop, bool with_reduce = true) {
   const Variant& V = c->var;
   vpg::StepArgs a = c->sargs;
@@ -961,8 +929,8 @@ void enqueue_grad(vpinn_gpu_ctx* c, const int* stop, bool with_reduce = true) {
     f.out_eps = c->feps.p;
     f.union_floats = 0;
     if (c->tc2_modes) {
-      const int grid_f = std::max(1, std::min(c->grid_tc2, ceil_div(P_local, 128)));
-      V.tc2_fwd<<<grid_f, vpg::t2::kNT, V.tc2_smem, c->stream>>>(f);
+      const int grid_f = std::max(1, std::min(c->grid_tc2, ceil_div(P_local, V.tc2_mp)));
+      V.tc2_fwd<<<grid_f, V.tc2_nt, V.tc2_smem, c->stream>>>(f);
     } else {
       const int grid_f = std::max(1, std::min(c->grid_fwd, ceil_div(P_local, vpg::kThreads)));
       V.forward<<<grid_f, vpg::kThreads, c->smem_fwd, c->stream>>>(f);
@@ -979,11 +947,7 @@ void enqueue_grad(vpinn_gpu_ctx* c, const int* stop, bool with_reduce = true) {
     ca.loss_part = c->loss_part.p;
     ca.stop_flag = stop;
     c->launches += 1;
-    if (ca.n_tiles > 0) {
-      vpg::contract_kernel<<<c->grid_contract, vpg::kCThreads, c->smem_contract, c->stream>>>(ca);
-      CK(cudaGetLastError());
-      c->launches += 1;
-    }
+    launch_contract_rows(c, ca);
     if (c->grid_pen) {
       vpg::penalty_kernel<<<c->grid_pen, 256, 0, c->stream>>>(
           c->fu.p + c->n_int, c->n_bnd, c->n_sen, c->bval.p, c->sval.p, a.bscale, a.sscale,
@@ -992,7 +956,7 @@ void enqueue_grad(vpinn_gpu_ctx* c, const int* stop, bool with_reduce = true) {
       c->launches += 1;
     }
     if (c->tc2_modes)
-      V.tc2_rev<<<c->grid_step, vpg::t2::kNT, c->smem_step, c->stream>>>(a);
+      V.tc2_rev<<<c->grid_step, V.tc2_nt, c->smem_step, c->stream>>>(a);
     else
       V.reverse<<<c->grid_step, vpg::kThreads, c->smem_step, c->stream>>>(a);
     CK(cudaGetLastError());
@@ -1133,11 +1097,7 @@ int launch_contract(vpinn_gpu_ctx* c, const float* ux, const float* uy, const fl
   ca.rscale = rscale;
   ca.loss_part = loss_part;
   ca.stop_flag = stop;
-  if (ca.n_tiles > 0) {
-    vpg::contract_kernel<<<c->grid_contract, vpg::kCThreads, c->smem_contract, c->stream>>>(ca);
-    CK(cudaGetLastError());
-    c->launches += 1;
-  }
+  launch_contract_rows(c, ca);
   return c->grid_contract;
 }
 
@@ -1155,7 +1115,7 @@ void flush_l2_now(vpinn_gpu_ctx* c, char* buf) {
 long long launches_per_epoch(const vpinn_gpu_ctx* c) {
   // step kernel(s) + reduce + adam (fused into one kernel without a communicator)
   long long n = c->comm ? 3 : 2;
-  if (c->split) n += 1 + (c->cargs.n_tiles > 0) + (c->grid_pen > 0);  // forward, contraction, penalty
+  if (c->split) n += 1 + 2 * (c->cargs.n_items > 0) + (c->grid_pen > 0);  // forward, contraction (2), penalty
   return n;
 }
 
@@ -1670,8 +1630,8 @@ int vpinn_gpu_forward(vpinn_gpu_ctx* c, const double* points, int64_t n, int ord
       const int grid = std::max(1, std::min(c->grid_step, ceil_div(n, 16 * c->sf_warps)));
       c->sfk.forward<<<grid, 32 * c->sf_warps, c->smem_step, c->stream>>>(f);
     } else if (c->tc2_modes) {
-      const int grid = std::max(1, std::min(c->grid_tc2, ceil_div(n, 128)));
-      c->var.tc2_fwd<<<grid, vpg::t2::kNT, c->var.tc2_smem, c->stream>>>(f);
+      const int grid = std::max(1, std::min(c->grid_tc2, ceil_div(n, c->var.tc2_mp)));
+      c->var.tc2_fwd<<<grid, c->var.tc2_nt, c->var.tc2_smem, c->stream>>>(f);
     } else {
       const int grid = std::max(1, std::min(c->grid_fwd, ceil_div(n, vpg::kThreads)));
       c->var.forward<<<grid, vpg::kThreads, c->smem_fwd, c->stream>>>(f);
@@ -1854,7 +1814,7 @@ vpg::MfContractArgs mf_args(vpinn_gpu_ctx* c, const float* ux, const float* uy, 
 int mf_cpt(vpinn_gpu_ctx* c) { return vpg::kMfTileThreads / c->Q; }
 int mf_grid(vpinn_gpu_ctx* c) {
   const int cpt = mf_cpt(c);
-  static const int per_sm = std::getenv("VPINN_MF_CTAS") ? std::atoi(std::getenv("VPINN_MF_CTAS")) : 4;
+  constexpr int per_sm = 4;
   if (cpt) return std::max(1, std::min(ceil_div(c->E, cpt), per_sm * c->sm_count));
   return std::max(1, std::min(ceil_div(c->E, vpg::kMfWarps), 8 * c->sm_count));
 }
@@ -2045,6 +2005,14 @@ int vpinn_gpu_profile_step(vpinn_gpu_ctx* c, int reps, double* ms_mlp, double* m
     *ms_mlp = t[0] / reps;
     *ms_reduce = t[1] / reps;
     *ms_adam = t[2] / reps;
+  });
+}
+
+int vpinn_gpu_set_test_hooks(int flags) {
+  return guarded([&] {
+    if (flags & ~(VPINN_HOOK_CUDA_CORE_STEP | VPINN_HOOK_FORCE_SPILL))
+      throw Fail{VPINN_ERR_CONFIG, "set_test_hooks: unknown flag"};
+    g_test_hooks.store(flags);
   });
 }
 

@@ -191,24 +191,31 @@ def test_tcgen05_3xtf32_probe(mode):
     assert err < 2e-6, err
 
 
-@pytest.mark.parametrize("name", ["c1_poisson", "gear576_cd2d", "inverse_scalar_eps"])
-@pytest.mark.parametrize("mode", ["ffma", "tc_aliased_slab", "tc_bf16", "tc2_spill"])
-def test_alternate_step_kernels_match_oracle(name, mode, monkeypatch):
-    """The CUDA-core (FFMA) fused kernel, the bf16x3 tensor-core kernel (slab
-    dedicated or aliased into an operand buffer) and the tc2 kernel's spill
-    path are selectable by environment; all must meet the same parity bar as
-    the default path."""
-    if mode == "ffma":
-        monkeypatch.setenv("VPINN_TC", "0")
-    elif mode == "tc_bf16":  # the bf16x3 one-CTA tensor-core kernel (dedicated slab)
-        monkeypatch.setenv("VPINN_TC_KERNEL", "1")
-    elif mode == "tc_aliased_slab":
-        monkeypatch.setenv("VPINN_TC_KERNEL", "1")
-        monkeypatch.setenv("VPINN_TC_SLAB", "0")
-    else:  # tc2 with its parameter-gradient accumulators spilled every tile (rare path)
-        monkeypatch.setenv("VPINN_TC2_FORCE_SPILL", "1")
+@pytest.fixture
+def test_hooks():
+    """vpinn_gpu_set_test_hooks for one test, restored afterwards."""
+    from paper_2404_12063_b200 import _capi
+    L = _capi.lib()
+    yield lambda flags: _capi.check(L.vpinn_gpu_set_test_hooks(flags))
+    _capi.check(L.vpinn_gpu_set_test_hooks(0))
+
+
+HOOK_CUDA_CORE_STEP, HOOK_FORCE_SPILL = 1, 2
+
+
+@pytest.mark.parametrize("name", ["c1_poisson", "gear576_cd2d", "inverse_scalar_eps", "paper_gear_h50"])
+@pytest.mark.parametrize("mode", ["cuda_core", "tc2_spill"])
+def test_alternate_step_kernels_match_oracle(name, mode, test_hooks):
+    """The CUDA-core (FFMA) fused kernel (it serves every shape without a
+    tensor-core variant) on shapes the tensor-core step serves, and the
+    tensor-core step's accumulator spill path (a rare path forced every
+    tile), selected with vpinn_gpu_set_test_hooks: both meet the same parity
+    bar as the default path."""
+    test_hooks(HOOK_CUDA_CORE_STEP if mode == "cuda_core" else HOOK_FORCE_SPILL)
     spec = CASES[name]()
     ob, g, p0 = make_pair(spec)
+    kernel = g.step_kernel()
+    assert ("tc2_step" not in kernel) == (mode == "cuda_core"), kernel
     parts_o, _ = ob.loss_and_grad(p0)
     parts_g, grad_g = g.loss_and_grad()
     assert rel(parts_g[0], parts_o[0]) < 1e-5, (parts_g, parts_o)

@@ -517,6 +517,8 @@ def test_parity_fixture_is_this_oracles_output(case):
     assert np.array_equal(parts, fx["traj32"][0])
     assert np.array_equal(grad.view(np.uint32), fx["grad32"].view(np.uint32))
     assert fx["traj32"].shape == (pc.EPOCHS, 4) and np.all(np.isfinite(fx["traj32"]))
+    assert fx["traj64"].shape == (pc.EPOCHS, 4) and np.all(np.isfinite(fx["traj64"]))
+    assert np.allclose(fx["traj64"][0], fx["parts64"], rtol=1e-14, atol=0.0)  # epoch 1 = the loss at p0
     assert fx["traj32"][-1, 0] < fx["traj32"][0, 0]
 
 

@@ -19,7 +19,17 @@ NAMES2 = ["start", "L0+store+sync+issue", "epi1(+store,issue L2)", "epi2(last)",
 NAMES = ["start", "L0+store+sync", "L1 mma+epi", "store B+sync", "L2 mma+epi", "out layer+sync",
          "sEx sync+tma wait", "phase A+sync", "residual+sync", "phase B+sync", "adjoint sync",
          "out rev+colsum+G+sync", "state+L0+adj2", "bar_w+G1/X1+sync", "adj1", "bar_w", "colsum W0"]
-hp, _ = bench.build_problem()
+if len(sys.argv) > 1 and sys.argv[1].startswith("c2"):
+    # C2 sweep point: e x e unit-square cells, T=25, Q=100 (a lone tile per CTA)
+    from paper_2404_12063_b200 import host  # noqa: E402
+    e = int(sys.argv[1][3:] or 1)
+    cfg = {"problem": {"forcing": "sin2pi_f", "boundary_g": "sin2pi_u", "n_boundary_points": 400},
+           "discretization": {"n_test_per_dim": 5, "n_quad_per_dim": 10},
+           "network": {"layers": [2, 30, 30, 30, 1]},
+           "training": {"learning_rate": 1e-3, "seed": 42, "precision": "single"}}
+    hp = host.HostProblem(cfg, mesh=host.Mesh.structured(e, e))
+else:
+    hp, _ = bench.build_problem()
 g = G.GpuStep.from_problem(hp.view(0, 0, 1), keepalive=hp)
 g.set_params(hp.init_params())
 g.adam_reset()
