@@ -29,11 +29,21 @@ struct Variant {
 
 // (hidden width, hidden layers, output channels, activation 0 tanh / 1 sigmoid);
 // a network uses the narrowest instantiated width >= its widest hidden layer,
-// narrower layers zero-padded exactly
-#define VPG_VARIANTS(X)                                                                          \
-  X(30, 3, 1, 0) X(30, 3, 2, 0) X(20, 2, 1, 0) X(20, 2, 2, 0) X(50, 3, 1, 0) X(16, 1, 1, 0)      \
-  X(16, 1, 2, 0) X(16, 2, 1, 0) X(16, 1, 1, 1) X(16, 2, 1, 1) X(30, 3, 1, 1) X(30, 2, 1, 0)     \
-  X(30, 2, 1, 1) X(30, 1, 1, 0) X(30, 1, 1, 1)
+// narrower layers zero-padded exactly.  Served (reference networks are
+// [2, hidden..., n_out], config.hpp:429-434):
+//   1-2 hidden layers, width <= 64, 1 or 2 outputs;
+//   3 hidden layers, width <= 62 with one output (tensor cores), <= 50 with two;
+//   4 hidden layers, width <= 36 (CUDA cores: the per-point state of wider
+//   nets exceeds shared memory);
+// tanh or sigmoid everywhere.  Tensor-core step (tc2) for 2-3 hidden layers,
+// one output, width <= 62; the CUDA-core step for everything else.
+#define VPG_VARIANTS(X) \
+  X(30, 1, 1, 0) X(30, 1, 1, 1) X(30, 1, 2, 0) X(30, 1, 2, 1) X(64, 1, 1, 0) X(64, 1, 1, 1) \
+  X(64, 1, 2, 0) X(64, 1, 2, 1) X(30, 2, 1, 0) X(30, 2, 1, 1) X(62, 2, 1, 0) X(62, 2, 1, 1) \
+  X(64, 2, 1, 0) X(64, 2, 1, 1) X(30, 2, 2, 0) X(30, 2, 2, 1) X(64, 2, 2, 0) X(64, 2, 2, 1) \
+  X(30, 3, 1, 0) X(30, 3, 1, 1) X(50, 3, 1, 0) X(50, 3, 1, 1) X(62, 3, 1, 0) X(62, 3, 1, 1) \
+  X(30, 3, 2, 0) X(30, 3, 2, 1) X(50, 3, 2, 0) X(50, 3, 2, 1) X(36, 4, 1, 0) X(36, 4, 1, 1) \
+  X(36, 4, 2, 0) X(36, 4, 2, 1)
 
 #define VPG_DECL(H, D, C, A) Variant variant_##H##_##D##_##C##_##A();
 VPG_VARIANTS(VPG_DECL)

@@ -1,0 +1,6 @@
+// step kernels instantiated for hidden width 36, 4 hidden layer(s), 2 output channel(s), tanh
+#define VPG_DEFINE_VARIANT
+#include "variant.h"
+namespace vpg {
+VPG_DEFINE(36, 4, 2, 0)
+}  // namespace vpg

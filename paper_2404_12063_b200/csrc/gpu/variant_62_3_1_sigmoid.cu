@@ -1,0 +1,6 @@
+// step kernels instantiated for hidden width 62, 3 hidden layer(s), 1 output channel(s), sigmoid
+#define VPG_DEFINE_VARIANT
+#include "variant.h"
+namespace vpg {
+VPG_DEFINE(62, 3, 1, 1)
+}  // namespace vpg

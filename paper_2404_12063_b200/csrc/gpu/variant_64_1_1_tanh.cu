@@ -1,0 +1,6 @@
+// step kernels instantiated for hidden width 64, 1 hidden layer(s), 1 output channel(s), tanh
+#define VPG_DEFINE_VARIANT
+#include "variant.h"
+namespace vpg {
+VPG_DEFINE(64, 1, 1, 0)
+}  // namespace vpg

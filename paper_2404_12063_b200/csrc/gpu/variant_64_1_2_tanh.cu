@@ -1,0 +1,6 @@
+// step kernels instantiated for hidden width 64, 1 hidden layer(s), 2 output channel(s), tanh
+#define VPG_DEFINE_VARIANT
+#include "variant.h"
+namespace vpg {
+VPG_DEFINE(64, 1, 2, 0)
+}  // namespace vpg

@@ -626,6 +626,9 @@ void configure(vpinn_gpu_ctx* c) {
     CK(cudaDeviceGetAttribute(&resv, cudaDevAttrReservedSharedMemoryPerBlock, c->device));
     return 2 * (smem + resv) <= (size_t)smsm ? 2 : 1;
   };
+  // the tensor-core forward / reverse modes (split path, evaluate)
+  const bool tc2_modes_ok = V.tc2_fwd != nullptr && !(g_test_hooks.load() & VPINN_HOOK_CUDA_CORE_STEP) &&
+                            c->eps_source != VPINN_EPS_SPATIAL;
   if (!c->split) {
     // tensor-core step: whole-cell tiles of at most tc2_mp points, the tile's
     // slab plus its contraction scratch in operand buffer A
@@ -699,14 +702,17 @@ void configure(vpinn_gpu_ctx* c) {
     }
     c->grad_rows = c->grid_step;
     c->loss_rows = c->grid_step;
-  } else {
-    // reverse kernel over all local points
+  } else if (!tc2_modes_ok) {
+    // reverse kernel over all local points (the tensor-core reverse mode
+    // takes this stage when the shape has one, below)
     c->kernel_name = "step_kernel<" + std::to_string(V.H) + "," + std::to_string(V.D) + "," + std::to_string(V.C) +
                      ",reverse> (split path)";
     a.n_tiles = ceil_div(P_local, vpg::kThreads);
     a.chunk_rows = 1;
     a.union_floats = V.rev_need;
     c->smem_step = V.smem(a.union_floats, 1);
+    if (c->smem_step > (size_t)227 * 1024)
+      throw Fail{VPINN_ERR_CONFIG, "reverse kernel does not fit shared memory"};
     CK(cudaFuncSetAttribute(V.reverse, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem_step));
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, V.reverse, vpg::kThreads, c->smem_step));
     if (occ < 1) throw Fail{VPINN_ERR_DEVICE, "reverse kernel cannot be resident"};
@@ -717,8 +723,7 @@ void configure(vpinn_gpu_ctx* c) {
   // ---- tc2 forward / reverse modes (split path, evaluate): any point
   // count, tanh or sigmoid, 2-3 hidden layers of width <= 63, one output ----
   {
-    c->tc2_modes = V.tc2_fwd != nullptr && !(g_test_hooks.load() & VPINN_HOOK_CUDA_CORE_STEP) &&
-                   c->eps_source != VPINN_EPS_SPATIAL;
+    c->tc2_modes = tc2_modes_ok;
     if (c->tc2_modes) {
       for (vpg::StepFn fn : {V.tc2_fwd, V.tc2_rev}) {
         CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)V.tc2_smem));
@@ -740,10 +745,14 @@ void configure(vpinn_gpu_ctx* c) {
   }
 
   // ---- forward kernel (evaluate; split-path first stage) ----
-  c->smem_fwd = V.smem(0, 1);
-  CK(cudaFuncSetAttribute(V.forward, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem_fwd));
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, V.forward, vpg::kThreads, c->smem_fwd));
-  c->grid_fwd = std::max(1, occ) * c->sm_count;
+  // (not needed, and possibly too large, when the tensor-core forward mode serves)
+  if (!c->tc2_modes) {
+    c->smem_fwd = V.smem(0, 1);
+    if (c->smem_fwd > (size_t)227 * 1024) throw Fail{VPINN_ERR_CONFIG, "forward kernel does not fit shared memory"};
+    CK(cudaFuncSetAttribute(V.forward, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem_fwd));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, V.forward, vpg::kThreads, c->smem_fwd));
+    c->grid_fwd = std::max(1, occ) * c->sm_count;
+  }
 
   // ---- standalone contraction (split path, roofline) ----
   {

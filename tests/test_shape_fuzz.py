@@ -27,8 +27,6 @@ def test_shape_grid_matches_oracle(pair, scalar):
     nt, nq = pair
     fails = []
     for mesh, layers, sig, conv in itertools.product(MESHES, NETS, [False, True], [False, True]):
-        if layers[-1] == 2 and sig:
-            continue  # no sigmoid two-output variant instantiated
         kw = dict(eps_source=2, bx=0.5) if layers[-1] == 2 else dict(bx=0.3 if conv else 0.0)
         if scalar and layers[-1] == 1:
             kw.update(eps_source=1, scalars=(1.3,), n_sensors=11, sensor_field="sin2pi_u")
@@ -55,8 +53,6 @@ def test_shape_grid_matches_oracle(pair, scalar):
 def test_evaluate_grid_matches_oracle(layers, sig):
     """evaluate(order 0 / 1) at arbitrary points through whichever forward
     kernel the context selects (tensor-core forward mode or CUDA cores)."""
-    if sig and (layers[-1] == 2 or layers[1] == 50):
-        pytest.skip("no sigmoid variant for this shape")
     kw = dict(eps_source=2, bx=0.5, forcing="sinpi_vareps_f") if layers[-1] == 2 else {}
     spec = po.ProblemSpec(*po.structured_mesh(2, 2), n_test_1d=3, n_quad_1d=4, boundary_g="sin2pi_u",
                           n_boundary=20, layers=layers, sigmoid=sig, seed=8, **kw)
@@ -168,3 +164,50 @@ def test_contexts_created_and_driven_from_two_threads():
         t.join()
     assert ob.n_int > 0
     assert np.array_equal(out[0], serial) and np.array_equal(out[1], serial)
+
+
+# the network shapes the GPU path serves (variant.h): depth 1-4, widths up to
+# 64 (62 for three hidden layers with one output, 50 with two, 36 for four),
+# one or two outputs, tanh and sigmoid -- each through the kernel the context
+# selects (tensor-core step in its 32- or 64-wide class, or the CUDA-core step)
+WIDE_NETS = [(2, 64, 1), (2, 64, 2), (2, 60, 60, 1), (2, 33, 1, 1), (2, 64, 64, 1), (2, 48, 64, 2),
+             (2, 55, 40, 55, 1), (2, 62, 62, 62, 1), (2, 40, 40, 40, 2), (2, 50, 50, 50, 2),
+             (2, 36, 36, 36, 36, 1), (2, 20, 30, 36, 10, 2), (2, 8, 8, 8, 8, 1)]
+
+
+@pytest.mark.parametrize("layers", WIDE_NETS)
+@pytest.mark.parametrize("sig", [False, True])
+def test_served_network_shapes_match_oracle(layers, sig):
+    kw = dict(eps_source=2, bx=0.5, forcing="sinpi_vareps_f") if layers[-1] == 2 else dict(bx=0.3)
+    fails = []
+    for (nt, nq), mesh in ((3, 4), (2, 3)), ((5, 10), (1, 1)), ((4, 5), (9, 7)):
+        spec = po.ProblemSpec(*po.structured_mesh(*mesh), n_test_1d=nt, n_quad_1d=nq, boundary_g="sin2pi_u",
+                              n_boundary=37, layers=layers, sigmoid=sig, seed=11, **kw)
+        ob, g, p0 = make_pair(spec)
+        po_, go32 = ob.loss_and_grad(p0)
+        pg, gg = g.loss_and_grad()
+        _, g64 = po.OracleProblem(spec, double=True).loss_and_grad(p0.astype(np.float64))
+        lr = abs(pg[0] - po_[0]) / abs(po_[0])
+        ge = np.abs(gg - g64).max() / max(np.abs(g64).max(), 1e-30)
+        e32 = np.abs(go32 - g64).max() / max(np.abs(g64).max(), 1e-30)
+        if lr > 1e-5 or ge > max(1e-5, 4.0 * e32):
+            fails.append(((nt, nq), mesh, g.step_kernel(), lr, ge, e32))
+        pts = np.random.default_rng(2).uniform(-1.2, 1.2, size=(300, 2))
+        ref = ob.evaluate(p0, pts, 1)
+        got = g.forward(pts, 1)
+        for k in range(3):
+            if np.abs(got[k] - ref[k]).max() > 3e-5 * max(1.0, np.abs(ref[k]).max()):
+                fails.append(("evaluate", k, g.step_kernel()))
+        g.close()
+    assert not fails, fails
+
+
+@pytest.mark.parametrize("layers", [(2, 64, 64, 64, 1), (2, 60, 60, 60, 2), (2, 40, 40, 40, 40, 1)])
+def test_unserved_network_shapes_fail_with_a_config_error(layers):
+    from paper_2404_12063_b200._capi import VpinnError
+    kw = dict(eps_source=2, forcing="sinpi_vareps_f") if layers[-1] == 2 else {}
+    spec = po.ProblemSpec(*po.structured_mesh(1, 1), n_test_1d=2, n_quad_1d=3, boundary_g="sin2pi_u",
+                          n_boundary=5, layers=layers, seed=1, **kw)
+    with pytest.raises(VpinnError) as e:
+        make_pair(spec)
+    assert e.value.code == 2
