@@ -566,9 +566,9 @@ MMA_SYNC_TF32_TFLOPS = 277.0
 def _strong_form(mesh, device, rank, world, pg, steps, weak_ms, cpu=False):
     """the strong-form collocation baseline (the paper's
     PINN comparison) on the same gear workload: order-2 network at the
-    354,800 interior quadrature points + the boundary penalty, one
-    warp-tiled mma.sync kernel + the same reduce/Adam.  Device-timed epochs,
-    L2 flushed between them, max over ranks."""
+    354,800 interior quadrature points + the boundary penalty, one tcgen05
+    step kernel (sf2_step_kernel.cuh) + the same reduce/Adam.  Device-timed
+    epochs, L2 flushed between them, max over ranks."""
     import copy
     from paper_2404_12063_b200 import gpu as G, host
     cfg = copy.deepcopy(GEAR_CFG)
@@ -592,22 +592,28 @@ def _strong_form(mesh, device, rank, world, pg, steps, weak_ms, cpu=False):
     kernel = g.step_kernel()
     g.close()
     n_pts = (hp.n_int + hp.n_bnd + hp.n_sen) // max(1, world)
-    tiles = -(-n_pts // 16)
-    # executed: 1,440 m16n8k8 MMAs (3-pass TF32 split, widths padded to 32) per
-    # 16-point tile; algorithmic: ~55,050 flop per point for [2,30,30,30,1]
-    # (5 streams x (2 forward + 2 propagation + 2 weight-gradient) 30x30
-    # products = 54,000 + the input / output layers)
-    exec_tflops = tiles * 1440 * 2 * 16 * 8 * 8 / (ms_k * 1e-3) / 1e12
+    # algorithmic: ~55,050 flop per point for [2,30,30,30,1] (5 streams x
+    # (2 forward + 2 propagation + 2 weight-gradient) 30x30 products = 54,000
+    # + the input / output layers)
     alg_tflops = n_pts * 55050.0 / (ms_k * 1e-3) / 1e12
+    if kernel.startswith("sf2_step"):
+        peak = peaks()["bf16_tflops"] / 3.0
+        roof = {"bound": "tensor", "pipe": "tcgen05 kind::f16, fp16 two-part split (3 products per fp32 product)",
+                "achieved": alg_tflops, "peak": peak, "unit": "TFLOP/s", "frac": alg_tflops / peak,
+                "peak_source": "MEASURED_PEAKS.json bf16_tflops (burst) / 3"}
+    else:
+        # executed: 1,440 m16n8k8 MMAs (3-pass TF32 split, widths padded to 32)
+        # per 16-point tile
+        exec_tflops = -(-n_pts // 16) * 1440 * 2 * 16 * 8 * 8 / (ms_k * 1e-3) / 1e12
+        roof = {"bound": "tensor", "pipe": "mma.sync TF32 (legacy HMMA)", "achieved": exec_tflops,
+                "peak": MMA_SYNC_TF32_TFLOPS, "unit": "TFLOP/s", "frac": exec_tflops / MMA_SYNC_TF32_TFLOPS,
+                "algorithmic_tflops": alg_tflops, "peak_source": "tools/micro/mma_sync_rate.cu on this pool's B200"}
     return {"workload": "C5 gear, form=strong: PINN collocation residual at the interior quadrature points "
                         "+ boundary penalty, same network / points / Adam",
             "kernel": kernel, "ms_per_epoch": ms, "points_per_s": (hp.n_int + hp.n_bnd + hp.n_sen) / (ms * 1e-3),
             "strong_over_weak_epoch_time": ms / weak_ms if weak_ms else None,
             "kernel_ms": {"step": ms_k, "reduce": ms_r, "adam": ms_a},
-            "roofline": {"bound": "tensor", "pipe": "mma.sync TF32 (legacy HMMA)", "achieved": exec_tflops,
-                         "peak": MMA_SYNC_TF32_TFLOPS, "unit": "TFLOP/s", "frac": exec_tflops / MMA_SYNC_TF32_TFLOPS,
-                         "algorithmic_tflops": alg_tflops,
-                         "peak_source": "tools/micro/mma_sync_rate.cu on this pool's B200"},
+            "roofline": roof,
             "l2": "flushed between timed epochs",
             "cpu_baseline": _strong_cpu(mesh) if cpu else None}
 

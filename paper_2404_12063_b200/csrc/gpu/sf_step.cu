@@ -1,5 +1,6 @@
 // Strong-form step kernels (sf_step_kernel.cuh) for 1-4 hidden layers of
 // width <= 32, tanh / sigmoid.
+#include "sf2_step_kernel.cuh"
 #include "sf_step.h"
 #include "sf_step_kernel.cuh"
 
@@ -8,7 +9,11 @@ namespace vpg {
 namespace {
 template <int D, int A>
 SfKernels make() {
-  return {sf_step_kernel<D, A, kModeFused>, sf_step_kernel<D, A, kModeForward>};
+  if constexpr (D == 2 || D == 3)
+    return {sf_step_kernel<D, A, kModeFused>, sf_step_kernel<D, A, kModeForward>, sf2_step_kernel<31, D, A, kModeFused>,
+            sf2_step_kernel<31, D, A, kModeForward>, sf2_step_smem_bytes<D>()};
+  else
+    return {sf_step_kernel<D, A, kModeFused>, sf_step_kernel<D, A, kModeForward>, nullptr, nullptr, 0};
 }
 }  // namespace
 
@@ -23,7 +28,7 @@ SfKernels sf_kernels(int D, int act) {
     case 7: return make<3, 1>();
     case 8: return make<4, 0>();
     case 9: return make<4, 1>();
-    default: return {nullptr, nullptr};
+    default: return {nullptr, nullptr, nullptr, nullptr, 0};
   }
 }
 

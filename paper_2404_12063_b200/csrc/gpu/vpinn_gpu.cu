@@ -486,6 +486,8 @@ struct vpinn_gpu_ctx {
   DBuf<float> sforce;
   vpg::SfKernels sfk{};
   int sf_warps = 0;
+  bool sf_tc = false;               // the tcgen05 strong-form kernel (sfk.tc_*)
+  int sf_block = 0, sf_pts = 0;     // its threads per CTA, points per CTA and tile
   long long n_int_global = 0;
   bool tc2 = false;           // fp16-split two-CTA tensor-core step
   bool tc2_modes = false;     // tc2 forward / reverse modes serve the split path and evaluate
@@ -538,12 +540,45 @@ void configure_strong(vpinn_gpu_ctx* c) {
   a.net = c->net;
   a.params = c->params.p;
   const int D = c->net.n_layers - 1;
+  int maxH = 0;
+  for (int l = 0; l < D; ++l) maxH = std::max(maxH, c->net.out_w[l]);
+  // the tcgen05 strong-form step (sf2_step_kernel.cuh) for 2-3 hidden layers
+  // of width <= 31; the warp-tiled mma.sync kernel for the other shapes
+  c->sf_tc = c->sfk.tc_fused != nullptr && maxH <= 31 && !(g_test_hooks.load() & VPINN_HOOK_CUDA_CORE_STEP);
+  if (c->sf_tc) {
+    c->smem_step = c->sfk.tc_smem;
+    for (auto fn : {c->sfk.tc_fused, c->sfk.tc_forward}) {
+      CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem_step));
+      CK(cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+    }
+    const int P_local = c->n_int + c->n_bnd + c->n_sen;
+    c->grid_step = std::max(1, std::min(c->sm_count, ceil_div(P_local, vpg::kSf2Points)));
+    c->grad_rows = c->loss_rows = c->grid_step;
+    c->sf_block = vpg::kSf2Threads;
+    c->sf_pts = vpg::kSf2Points;
+    c->tc_scratch.alloc((size_t)c->grid_step * (D - 1) * 64 * 64, c->stream);
+    a.tc_scratch = c->tc_scratch.p;
+    a.tc_force_spill = (g_test_hooks.load() & VPINN_HOOK_FORCE_SPILL) ? 1 : 0;
+    c->kernel_name = "sf2_step_kernel<" + std::to_string(D) + "," + (c->net.sigmoid ? "sigmoid" : "tanh") +
+                     "> (strong form, tcgen05 fp16 split, 256 threads, 1 CTA/SM)";
+    c->part_stride = (c->grad_rows + 31) & ~31;
+    c->grad_part.alloc((size_t)c->part_stride * c->n_params, c->stream);
+    a.part_stride = c->part_stride;
+    a.grad_part = c->grad_part.p;
+    c->loss_part.alloc((size_t)c->loss_rows * vpg::kLpWords, c->stream);
+    a.loss_part = c->loss_part.p;
+    c->red.alloc((size_t)c->n_params + vpg::kLpWords, c->stream);
+    c->e_scalar.alloc(1, c->stream);
+    return;
+  }
   int optin = 0;
   CK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, c->device));
   int w = vpg::kSfMaxWarps;
   while (w > 1 && vpg::sf_smem_bytes(D, w) > (size_t)optin) --w;
   if (vpg::sf_smem_bytes(D, w) > (size_t)optin) throw Fail{VPINN_ERR_CONFIG, "strong-form kernel does not fit shared memory"};
   c->sf_warps = w;
+  c->sf_block = 32 * w;
+  c->sf_pts = 16 * w;
   c->smem_step = vpg::sf_smem_bytes(D, w);
   for (auto fn : {c->sfk.fused, c->sfk.forward}) {
     CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem_step));
@@ -900,7 +935,8 @@ constexpr bool pdl_enabled() { return false; }
 
 void launch_fused(vpinn_gpu_ctx* c, const vpg::StepArgs& a) {
   if (c->strong)
-    launch_k(pdl_enabled(), c->sfk.fused, c->grid_step, 32 * c->sf_warps, c->smem_step, c->stream, a);
+    launch_k(pdl_enabled(), c->sf_tc ? c->sfk.tc_fused : c->sfk.fused, c->grid_step, c->sf_block, c->smem_step,
+             c->stream, a);
   else if (c->tc2)
     launch_k(pdl_enabled(), c->var.tc2, c->grid_step, c->var.tc2_nt, c->smem_step, c->stream, a);
   else
@@ -1636,8 +1672,8 @@ int vpinn_gpu_forward(vpinn_gpu_ctx* c, const double* points, int64_t n, int ord
     f.union_floats = 0;
     f.stop_flag = nullptr;
     if (c->strong) {
-      const int grid = std::max(1, std::min(c->grid_step, ceil_div(n, 16 * c->sf_warps)));
-      c->sfk.forward<<<grid, 32 * c->sf_warps, c->smem_step, c->stream>>>(f);
+      const int grid = std::max(1, std::min(c->grid_step, ceil_div(n, c->sf_pts)));
+      (c->sf_tc ? c->sfk.tc_forward : c->sfk.forward)<<<grid, c->sf_block, c->smem_step, c->stream>>>(f);
     } else if (c->tc2_modes) {
       const int grid = std::max(1, std::min(c->grid_tc2, ceil_div(n, c->var.tc2_mp)));
       c->var.tc2_fwd<<<grid, c->var.tc2_nt, c->var.tc2_smem, c->stream>>>(f);
@@ -1685,8 +1721,8 @@ int vpinn_gpu_forward2(vpinn_gpu_ctx* c, const double* points, int64_t n, float*
     f.out_uxx = o[3].p;
     f.out_uyy = o[4].p;
     f.stop_flag = nullptr;
-    const int grid = std::max(1, std::min(c->grid_step, ceil_div(n, 16 * c->sf_warps)));
-    c->sfk.forward<<<grid, 32 * c->sf_warps, c->smem_step, c->stream>>>(f);
+    const int grid = std::max(1, std::min(c->grid_step, ceil_div(n, c->sf_pts)));
+    (c->sf_tc ? c->sfk.tc_forward : c->sfk.forward)<<<grid, c->sf_block, c->smem_step, c->stream>>>(f);
     CK(cudaGetLastError());
     c->launches += 1;
     for (int k = 0; k < 5; ++k)

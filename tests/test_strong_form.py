@@ -1,8 +1,10 @@
 """Strong-form collocation on the GPU against the oracle.
 
 The oracle's strong form is pinned by the reference's order-2 / strong-residual
-known answers (tests/test_oracle_golden.py).  Here the B200 kernel
-(sf_step_kernel.cuh, mma.sync 3xTF32) must reproduce, on the same inputs:
+known answers (tests/test_oracle_golden.py).  Here the B200 kernels -- the
+tcgen05 step (sf2_step_kernel.cuh, fp16 split) for 2-3 hidden layers of width
+<= 31 and the warp-tiled mma.sync one (sf_step_kernel.cuh, 3xTF32) for the
+other shapes -- must reproduce, on the same inputs:
 order-2 evaluate(), the composite objective and its gradient, and a 100-epoch
 training trajectory (loss within 1e-5 relative per epoch, the north-star
 tolerance).  CPU-side tests check the host plumbing only.
@@ -46,6 +48,11 @@ def make_strong_pair(spec, **kw):
     return ob, g, p0
 
 
+def expected_kernel(spec):
+    hidden = spec.layers[1:-1]
+    return "sf2_step_kernel" if len(hidden) in (2, 3) and max(hidden) <= 31 else "sf_step_kernel<"
+
+
 CASES = {
     "poisson_d3": lambda: strong_spec(),
     "acceptance_case4": lambda: strong_spec(mesh=(2, 2), n_test_1d=3, n_quad_1d=4, forcing="one",
@@ -70,7 +77,7 @@ CASES = {
 def test_strong_loss_and_gradient_match_oracle(name):
     spec = CASES[name]()
     ob, g, p0 = make_strong_pair(spec)
-    assert "sf_step_kernel" in g.step_kernel()
+    assert expected_kernel(spec) in g.step_kernel()
     parts_o, go32 = ob.loss_and_grad(p0)
     parts_g, grad_g = g.loss_and_grad()
     assert rel(parts_g[0], parts_o[0]) < 1e-5, (parts_g, parts_o)
@@ -167,7 +174,7 @@ def test_strong_form_through_host_pipeline_and_device_assembly():
     hp = host.HostProblem(cfg, mesh=mesh)
     dp = host.HostProblem(cfg, mesh=mesh, device_assembly=True)
     gh, gd = hp.gpu(), dp.gpu()
-    assert "sf_step_kernel" in gh.step_kernel() and "sf_step_kernel" in gd.step_kernel()
+    assert "step_kernel" in gh.step_kernel() and gh.step_kernel() == gd.step_kernel()
     ph, grh = gh.loss_and_grad()
     pd, grd = gd.loss_and_grad()
     assert np.abs(ph - pd).max() <= 1e-6 * np.abs(ph).max(), (ph, pd)
@@ -193,3 +200,28 @@ def test_weak_only_entry_points_reject_strong_contexts():
     with pytest.raises(VpinnError) as e:
         g.contract(np.zeros(g.n_elem * g.n_quad, np.float32), np.zeros(g.n_elem * g.n_quad, np.float32))
     assert e.value.code == 2
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["poisson_d3", "cd2d_sensors_scalar_eps", "gear_many_tiles"])
+@pytest.mark.parametrize("mode", ["mma_sync", "tc_spill"])
+def test_strong_alternate_kernels_match_oracle(name, mode):
+    """The warp-tiled mma.sync strong-form kernel on shapes the tcgen05 one
+    serves, and the tcgen05 kernel's accumulator spill path forced every
+    tile (vpinn_gpu_set_test_hooks): same parity bar."""
+    from paper_2404_12063_b200 import _capi
+    L = _capi.lib()
+    _capi.check(L.vpinn_gpu_set_test_hooks(1 if mode == "mma_sync" else 2))
+    try:
+        spec = CASES[name]()
+        ob, g, p0 = make_strong_pair(spec)
+        assert ("sf2_step" in g.step_kernel()) == (mode == "tc_spill"), g.step_kernel()
+        parts_o, go32 = ob.loss_and_grad(p0)
+        parts_g, grad_g = g.loss_and_grad()
+        assert rel(parts_g[0], parts_o[0]) < 1e-5, (parts_g, parts_o)
+        _, g64 = po.OracleProblem(spec, double=True).loss_and_grad(p0.astype(np.float64))
+        err = np.abs(grad_g - g64).max() / np.abs(g64).max()
+        e32 = np.abs(go32 - g64).max() / np.abs(g64).max()
+        assert err < max(1e-5, 4.0 * e32), (err, e32)
+    finally:
+        _capi.check(L.vpinn_gpu_set_test_hooks(0))
