@@ -28,6 +28,8 @@
 // its own column block, so layer 1's block survives layer 2.
 #pragma once
 
+#include <type_traits>
+
 #include "tc2_step_kernel.cuh"
 
 namespace vpg {
@@ -100,6 +102,8 @@ enum : int { kSiW = 0, kSiXv = 2, kSiXt = 4, kSiXs = 6, kSiN = 8 };
 
 template <int ACT>
 struct Deriv;
+// s1, s2 (and s3) of two units at once in packed fp32x2 (ActDerivs::fill,
+// network.hpp:171-192, from the activation output z)
 template <>
 struct Deriv<kActTanh> {
   static constexpr float s2max = 0.77f, s3max = 2.0f;
@@ -107,6 +111,14 @@ struct Deriv<kActTanh> {
     s1 = fmaf(-z, z, 1.0f);
     s2 = -2.0f * z * s1;
     s3 = s1 * (4.0f * (z * z) - 2.0f * s1);
+  }
+  static __device__ __forceinline__ void d12(float2 z, float2& s1, float2& s2) {
+    s1 = fma2(f2(-z.x, -z.y), z, f2s(1.0f));
+    s2 = mul2(mul2(f2s(-2.0f), z), s1);
+  }
+  static __device__ __forceinline__ void d123(float2 z, float2& s1, float2& s2, float2& s3) {
+    d12(z, s1, s2);
+    s3 = mul2(s1, fma2(f2s(4.0f), mul2(z, z), mul2(f2s(-2.0f), s1)));
   }
 };
 template <>
@@ -116,6 +128,14 @@ struct Deriv<kActSigmoid> {
     s1 = z * (1.0f - z);
     s2 = s1 * (1.0f - 2.0f * z);
     s3 = s1 * (1.0f - 6.0f * z + 6.0f * (z * z));
+  }
+  static __device__ __forceinline__ void d12(float2 z, float2& s1, float2& s2) {
+    s1 = mul2(z, add2(f2s(1.0f), f2(-z.x, -z.y)));
+    s2 = mul2(s1, fma2(f2s(-2.0f), z, f2s(1.0f)));
+  }
+  static __device__ __forceinline__ void d123(float2 z, float2& s1, float2& s2, float2& s3) {
+    d12(z, s1, s2);
+    s3 = mul2(s1, fma2(f2s(6.0f), mul2(z, z), fma2(f2s(-6.0f), z, f2s(1.0f))));
   }
 };
 
@@ -339,19 +359,23 @@ __global__ void __maxnreg__(255) sf2_step_kernel(const StepArgs a) {
     if ((lane & 3) == 0) sAcc[warp * kAccW + slot + 8 * c + t2::rs8_index(lane)] += r;
   };
   // five-stream store of 8 units (chunk c) into buffer buf with per-class scales
-  auto store5 = [&](char* buf, int c, const float (&v)[8], const float (&tx)[8], const float (&ty)[8],
+  // (SCALE = false: the values already carry their scales)
+  auto store5 = [&](auto scale_tag, char* buf, int c, const float (&v)[8], const float (&tx)[8], const float (&ty)[8],
                     const float (&sx)[8], const float (&sy)[8], float scv, float sct, float scs) {
+    constexpr bool SC = decltype(scale_tag)::value;
     const uint32_t o = coff(c);
-    tc::st_split8_ho<true>(buf, kPart, o, v, scv);
-    tc::st_split8_ho<true>(buf + kStream, kPart, o, tx, sct);
-    tc::st_split8_ho<true>(buf + 2 * kStream, kPart, o, ty, sct);
-    tc::st_split8_ho<true>(buf + 3 * kStream, kPart, o, sx, scs);
-    tc::st_split8_ho<true>(buf + 4 * kStream, kPart, o, sy, scs);
+    tc::st_split8_ho<SC>(buf, kPart, o, v, scv);
+    tc::st_split8_ho<SC>(buf + kStream, kPart, o, tx, sct);
+    tc::st_split8_ho<SC>(buf + 2 * kStream, kPart, o, ty, sct);
+    tc::st_split8_ho<SC>(buf + 3 * kStream, kPart, o, sx, scs);
+    tc::st_split8_ho<SC>(buf + 4 * kStream, kPart, o, sy, scs);
   };
+  using kScaled = std::true_type;
+  using kUnscaled = std::false_type;
   // X_1 of chunk c into buf: from (x, y) through layer 0 (z kept in TMEM),
   // or from that kept z (reverse)
   auto store_x1 = [&](char* buf, int c, float px, float py, bool from_tmem) {
-    float z[8], s1[8], s2[8], tx[8], ty[8], sx[8], sy[8];
+    float z[8], tx[8], ty[8], sx[8], sy[8];
     if (from_tmem) {
       tc::tmem_ld1x8_wait(zcol(kZ1, c), z);
     } else {
@@ -363,17 +387,27 @@ __global__ void __maxnreg__(255) sf2_step_kernel(const StepArgs a) {
       tc::tmem_st1x8_wait(zcol(kZ1, c), z);
     }
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      float d3;
-      DV::d(z[k], s1[k], s2[k], d3);
-      const float2 wt = *reinterpret_cast<const float2*>(sW0t + 2 * (u0 + 8 * c + k));
-      const float2 ws = *reinterpret_cast<const float2*>(sW0s + 2 * (u0 + 8 * c + k));
-      tx[k] = s1[k] * wt.x;
-      ty[k] = s1[k] * wt.y;
-      sx[k] = s2[k] * ws.x;
-      sy[k] = s2[k] * ws.y;
+    for (int k = 0; k < 8; k += 2) {
+      float2 a1, a2;
+      DV::d12(f2(z[k], z[k + 1]), a1, a2);
+      const float4 wt = *reinterpret_cast<const float4*>(sW0t + 2 * (u0 + 8 * c + k));  // (wx, wy) of k, k+1
+      const float4 ws = *reinterpret_cast<const float4*>(sW0s + 2 * (u0 + 8 * c + k));
+      const float2 t1 = mul2(a1, f2(wt.x, wt.z)), t2 = mul2(a1, f2(wt.y, wt.w));
+      const float2 q1 = mul2(a2, f2(ws.x, ws.z)), q2 = mul2(a2, f2(ws.y, ws.w));
+      tx[k] = t1.x;
+      tx[k + 1] = t1.y;
+      ty[k] = t2.x;
+      ty[k + 1] = t2.y;
+      sx[k] = q1.x;
+      sx[k + 1] = q1.y;
+      sy[k] = q2.x;
+      sy[k + 1] = q2.y;
     }
-    store5(buf, c, z, tx, ty, sx, sy, sSc[kScXv], 1.f, 1.f);
+    tc::st_split8_ho<true>(buf, kPart, coff(c), z, sSc[kScXv]);
+    tc::st_split8_ho<false>(buf + kStream, kPart, coff(c), tx, 1.f);
+    tc::st_split8_ho<false>(buf + 2 * kStream, kPart, coff(c), ty, 1.f);
+    tc::st_split8_ho<false>(buf + 3 * kStream, kPart, coff(c), sx, 1.f);
+    tc::st_split8_ho<false>(buf + 4 * kStream, kPart, coff(c), sy, 1.f);
   };
 
   // per-CTA sums (thread-owned, combined in a fixed order at the end)
@@ -474,27 +508,39 @@ __global__ void __maxnreg__(255) sf2_step_kernel(const StepArgs a) {
         tc::tmem_ld2x8_wait(dcol(l, 3, c), dcol(l, 4, c), bx2, by2);
         float z[8], tx[8], ty[8], sx[8], sy[8];
 #pragma unroll
-        for (int k = 0; k < 8; ++k) {
+        for (int k = 0; k < 8; k += 2) {
           const int u = u0 + 8 * c + k;
-          z[k] = AC::value(fmaf(d[k], fv, bias[u]));
-          float s1, s2v, s3;
-          DV::d(z[k], s1, s2v, s3);
-          const float tax = ax[k] * ft, tay = ay[k] * ft, t2ax = bx2[k] * fs, t2ay = by2[k] * fs;
-          tx[k] = s1 * tax;
-          ty[k] = s1 * tay;
-          sx[k] = fmaf(s2v, tax * tax, s1 * t2ax);
-          sy[k] = fmaf(s2v, tay * tay, s1 * t2ay);
+          const float2 zz = AC::value2(fma2(f2(d[k], d[k + 1]), f2s(fv), f2(bias[u], bias[u + 1])));
+          float2 s1, s2v;
+          DV::d12(zz, s1, s2v);
+          const float2 tax = mul2(f2(ax[k], ax[k + 1]), f2s(ft)), tay = mul2(f2(ay[k], ay[k + 1]), f2s(ft));
+          const float2 t2ax = mul2(f2(bx2[k], bx2[k + 1]), f2s(fs)), t2ay = mul2(f2(by2[k], by2[k + 1]), f2s(fs));
+          const float2 vx = mul2(s1, tax), vy = mul2(s1, tay);
+          const float2 wx = fma2(s2v, mul2(tax, tax), mul2(s1, t2ax)), wy = fma2(s2v, mul2(tay, tay), mul2(s1, t2ay));
+          z[k] = zz.x;
+          z[k + 1] = zz.y;
+          tx[k] = vx.x;
+          tx[k + 1] = vx.y;
+          ty[k] = vy.x;
+          ty[k + 1] = vy.y;
+          sx[k] = wx.x;
+          sx[k + 1] = wx.y;
+          sy[k] = wy.x;
+          sy[k + 1] = wy.y;
           if (last) {
-            const float w = sWd[u];
-            ou[0] = fmaf(w, z[k], ou[0]);
-            ou[1] = fmaf(w, tx[k], ou[1]);
-            ou[2] = fmaf(w, ty[k], ou[2]);
-            ou[3] = fmaf(w, sx[k], ou[3]);
-            ou[4] = fmaf(w, sy[k], ou[4]);
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              const float w = sWd[u + e];
+              ou[0] = fmaf(w, z[k + e], ou[0]);
+              ou[1] = fmaf(w, tx[k + e], ou[1]);
+              ou[2] = fmaf(w, ty[k + e], ou[2]);
+              ou[3] = fmaf(w, sx[k + e], ou[3]);
+              ou[4] = fmaf(w, sy[k + e], ou[4]);
+            }
           }
         }
         if (!last) {
-          store5(bufB, c, z, tx, ty, sx, sy, sSc[kScXv + l], sSc[kScXt + l], sSc[kScXs + l]);
+          store5(kScaled{}, bufB, c, z, tx, ty, sx, sy, sSc[kScXv + l], sSc[kScXt + l], sSc[kScXs + l]);
           tc::tmem_st1x8_wait(zcol(kZ2, c), z);  // hidden l + 1 = 2 (D == 3)
         } else {
           tc::tmem_st1x8_wait(zcol(kZ0, c), z);
@@ -615,28 +661,41 @@ __global__ void __maxnreg__(255) sf2_step_kernel(const StepArgs a) {
         tc::tmem_ld1x8_wait(zcol(kZ0, c), z);
         tc::tmem_ld2x8_wait(dcol(NL, 1, c), dcol(NL, 2, c), ax, ay);
         tc::tmem_ld2x8_wait(dcol(NL, 3, c), dcol(NL, 4, c), bx2, by2);
-        float v[8], gA[8], gTx[8], gTy[8], gSx[8], gSy[8];
+        float v[8], gA[8], gTx[8], gTy[8], gSx[8];
 #pragma unroll
-        for (int k = 0; k < 8; ++k) {
+        for (int k = 0; k < 8; k += 2) {
           const int u = u0 + 8 * c + k;
-          float s1, s2v, s3;
-          DV::d(z[k], s1, s2v, s3);
-          const float tax = ax[k] * ftl, tay = ay[k] * ftl, t2ax = bx2[k] * fsl, t2ay = by2[k] * fsl;
-          const float txv = s1 * tax, tyv = s1 * tay;
-          const float sxv = fmaf(s2v, tax * tax, s1 * t2ax), syv = fmaf(s2v, tay * tay, s1 * t2ay);
-          v[k] = ub * z[k] + uxb * txv + uyb * tyv + usb * (sxv + syv);
-          const float w = sWd[u];
-          const float xb = w * ub, tzx = w * uxb, tzy = w * uyb, t2z = w * usb;
-          const float ga = s1 * xb + s2v * (tax * tzx + tay * tzy) + s3 * ((tax * tax) * t2z + (tay * tay) * t2z) +
-                           s2v * (t2ax * t2z + t2ay * t2z);
-          gA[k] = ga * gsc.v;
-          gTx[k] = (s1 * tzx + 2.f * (s2v * (tax * t2z))) * gsc.t;
-          gTy[k] = (s1 * tzy + 2.f * (s2v * (tay * t2z))) * gsc.t;
-          gSx[k] = (s1 * t2z) * gsc.s;
-          gSy[k] = gSx[k];
+          float2 s1, s2v, s3;
+          const float2 zz = f2(z[k], z[k + 1]);
+          DV::d123(zz, s1, s2v, s3);
+          const float2 tax = mul2(f2(ax[k], ax[k + 1]), f2s(ftl)), tay = mul2(f2(ay[k], ay[k + 1]), f2s(ftl));
+          const float2 t2ax = mul2(f2(bx2[k], bx2[k + 1]), f2s(fsl)), t2ay = mul2(f2(by2[k], by2[k + 1]), f2s(fsl));
+          const float2 txv = mul2(s1, tax), tyv = mul2(s1, tay);
+          const float2 sxy = add2(fma2(s2v, mul2(tax, tax), mul2(s1, t2ax)), fma2(s2v, mul2(tay, tay), mul2(s1, t2ay)));
+          const float2 vv = fma2(f2s(ub), zz, fma2(f2s(uxb), txv, fma2(f2s(uyb), tyv, mul2(f2s(usb), sxy))));
+          const float2 w = f2(sWd[u], sWd[u + 1]);
+          const float2 xb = mul2(w, f2s(ub)), tzx = mul2(w, f2s(uxb)), tzy = mul2(w, f2s(uyb)), t2z = mul2(w, f2s(usb));
+          const float2 tt = fma2(tax, tax, mul2(tay, tay));  // t2z is the same for x and y (u_xxbar = u_yybar)
+          float2 ga = fma2(s1, xb, mul2(s2v, fma2(tax, tzx, mul2(tay, tzy))));
+          ga = fma2(s3, mul2(tt, t2z), fma2(s2v, mul2(add2(t2ax, t2ay), t2z), ga));
+          const float2 s2t = mul2(mul2(f2s(2.0f), s2v), t2z);
+          const float2 gtx = fma2(s1, tzx, mul2(s2t, tax)), gty = fma2(s1, tzy, mul2(s2t, tay));
+          const float2 gs = mul2(s1, t2z);
+          const float2 ga2 = mul2(ga, f2s(gsc.v)), gtx2 = mul2(gtx, f2s(gsc.t)), gty2 = mul2(gty, f2s(gsc.t)),
+                       gs2 = mul2(gs, f2s(gsc.s));
+          v[k] = vv.x;
+          v[k + 1] = vv.y;
+          gA[k] = ga2.x;
+          gA[k + 1] = ga2.y;
+          gTx[k] = gtx2.x;
+          gTx[k + 1] = gtx2.y;
+          gTy[k] = gty2.x;
+          gTy[k + 1] = gty2.y;
+          gSx[k] = gs2.x;
+          gSx[k + 1] = gs2.y;
         }
         acc_units(v, kAWd, c);
-        store5(bufA, c, gA, gTx, gTy, gSx, gSy, 1.f, 1.f, 1.f);
+        store5(kUnscaled{}, bufA, c, gA, gTx, gTy, gSx, gSx, 1.f, 1.f, 1.f);
       }
     }
     operands_ready();
@@ -669,30 +728,44 @@ __global__ void __maxnreg__(255) sf2_step_kernel(const StepArgs a) {
           tc::tmem_ld2x8_wait(dcol(h - 1, 3, c), dcol(h - 1, 4, c), bx2, by2);
         }
         float gA[8], gTx[8], gTy[8], gSx[8], gSy[8];
+        // G of hidden h, scaled for the store (h >= 2) or not (h == 1: the input layer)
+        const float2 sv2 = f2s(h >= 2 ? g2.v : 1.f), st2 = f2s(h >= 2 ? g2.t : 1.f), ss2 = f2s(h >= 2 ? g2.s : 1.f);
 #pragma unroll
-        for (int k = 0; k < 8; ++k) {
+        for (int k = 0; k < 8; k += 2) {
           const int u = u0 + 8 * c + k;
-          float s1, s2v, s3;
-          DV::d(z[k], s1, s2v, s3);
-          float tax, tay, t2ax = 0.f, t2ay = 0.f;
+          float2 s1, s2v, s3;
+          DV::d123(f2(z[k], z[k + 1]), s1, s2v, s3);
+          float2 tax, tay, t2ax = f2s(0.f), t2ay = f2s(0.f);
           if (h >= 2) {
-            tax = ax[k] * fth;
-            tay = ay[k] * fth;
-            t2ax = bx2[k] * fsh;
-            t2ay = by2[k] * fsh;
+            tax = mul2(f2(ax[k], ax[k + 1]), f2s(fth));
+            tay = mul2(f2(ay[k], ay[k + 1]), f2s(fth));
+            t2ax = mul2(f2(bx2[k], bx2[k + 1]), f2s(fsh));
+            t2ay = mul2(f2(by2[k], by2[k + 1]), f2s(fsh));
           } else {
-            tax = sW0[4 * u];
-            tay = sW0[4 * u + 1];
+            tax = f2(sW0[4 * u], sW0[4 * u + 4]);
+            tay = f2(sW0[4 * u + 1], sW0[4 * u + 5]);
           }
-          const float xb = pa[k] * gsc.pv, tzx = ptx[k] * gsc.pt, tzy = pty[k] * gsc.pt, t2zx = psx[k] * gsc.ps,
-                      t2zy = psy[k] * gsc.ps;
-          const float ga = s1 * xb + s2v * (tax * tzx + tay * tzy) + s3 * ((tax * tax) * t2zx + (tay * tay) * t2zy) +
-                           s2v * (t2ax * t2zx + t2ay * t2zy);
-          gA[k] = ga;
-          gTx[k] = s1 * tzx + 2.f * (s2v * (tax * t2zx));
-          gTy[k] = s1 * tzy + 2.f * (s2v * (tay * t2zy));
-          gSx[k] = s1 * t2zx;
-          gSy[k] = s1 * t2zy;
+          const float2 xb = mul2(f2(pa[k], pa[k + 1]), f2s(gsc.pv));
+          const float2 tzx = mul2(f2(ptx[k], ptx[k + 1]), f2s(gsc.pt)), tzy = mul2(f2(pty[k], pty[k + 1]), f2s(gsc.pt));
+          const float2 t2zx = mul2(f2(psx[k], psx[k + 1]), f2s(gsc.ps)), t2zy = mul2(f2(psy[k], psy[k + 1]), f2s(gsc.ps));
+          float2 ga = fma2(s1, xb, mul2(s2v, fma2(tax, tzx, mul2(tay, tzy))));
+          ga = fma2(s3, fma2(mul2(tax, tax), t2zx, mul2(mul2(tay, tay), t2zy)),
+                    fma2(s2v, fma2(t2ax, t2zx, mul2(t2ay, t2zy)), ga));
+          const float2 s22 = mul2(f2s(2.0f), s2v);
+          const float2 gtx = fma2(s1, tzx, mul2(s22, mul2(tax, t2zx)));
+          const float2 gty = fma2(s1, tzy, mul2(s22, mul2(tay, t2zy)));
+          const float2 a2 = mul2(ga, sv2), bx3 = mul2(gtx, st2), by3 = mul2(gty, st2);
+          const float2 cx3 = mul2(mul2(s1, t2zx), ss2), cy3 = mul2(mul2(s1, t2zy), ss2);
+          gA[k] = a2.x;
+          gA[k + 1] = a2.y;
+          gTx[k] = bx3.x;
+          gTx[k + 1] = bx3.y;
+          gTy[k] = by3.x;
+          gTy[k + 1] = by3.y;
+          gSx[k] = cx3.x;
+          gSx[k + 1] = cx3.y;
+          gSy[k] = cy3.x;
+          gSy[k + 1] = cy3.y;
         }
         if (h == 1) {
           // input layer: W0bar += Abar x^T + TAxbar e_x^T + TAybar e_y^T, b0bar += Abar
@@ -710,15 +783,7 @@ __global__ void __maxnreg__(255) sf2_step_kernel(const StepArgs a) {
             ph_w ^= 1u;
             tc::fence_after_sync();
           }
-#pragma unroll
-          for (int k = 0; k < 8; ++k) {
-            gA[k] *= g2.v;
-            gTx[k] *= g2.t;
-            gTy[k] *= g2.t;
-            gSx[k] *= g2.s;
-            gSy[k] *= g2.s;
-          }
-          store5(bufA, c, gA, gTx, gTy, gSx, gSy, 1.f, 1.f, 1.f);
+          store5(kUnscaled{}, bufA, c, gA, gTx, gTy, gSx, gSy, 1.f, 1.f, 1.f);
           store_x1(bufB, c, px, py, true);  // hidden-1 output rebuilt (h - 1 == 1)
         }
       }
