@@ -123,15 +123,18 @@ BlockCache& block_cache() {
 // overlaps the host copy of chunk i+1 with the DMA of chunk i at pinned
 // bandwidth.  Process-wide, never destroyed (no exit-order races).
 struct CopyPool {
+  // workers spin briefly on a generation counter between the chunks of one
+  // upload (a condition-variable wake-up per 8 MB chunk cost ~30 us each),
+  // then block on the condition variable when idle
   int n = 1;
   std::vector<std::thread> workers;
   std::mutex mu;
-  std::condition_variable cv, cv_done;
+  std::condition_variable cv;
+  std::atomic<unsigned> gen{0};
+  std::atomic<int> pending{0};
   char* dst = nullptr;
   const char* src = nullptr;
   size_t len = 0;
-  unsigned gen = 0;
-  int pending = 0;
   CopyPool() {
     const unsigned hc = std::thread::hardware_concurrency();
     n = std::max(1, std::min(8, (int)(hc ? hc / 2 : 1)));
@@ -148,17 +151,23 @@ struct CopyPool {
   void loop(int i) {
     unsigned seen = 0;
     for (;;) {
-      std::unique_lock<std::mutex> lk(mu);
-      cv.wait(lk, [&] { return gen != seen; });
-      seen = gen;
+      // spin ~1 ms for the next chunk, then sleep until notified
+      const auto t0 = std::chrono::steady_clock::now();
+      while (gen.load(std::memory_order_acquire) == seen) {
+        if (std::chrono::steady_clock::now() - t0 > std::chrono::milliseconds(1)) {
+          std::unique_lock<std::mutex> lk(mu);
+          cv.wait(lk, [&] { return gen.load(std::memory_order_acquire) != seen; });
+          break;
+        }
+        std::this_thread::yield();
+      }
+      seen = gen.load(std::memory_order_acquire);
       char* d;
       const char* s;
       size_t l;
       slice(i, d, s, l);
-      lk.unlock();
       if (l) std::memcpy(d, s, l);
-      lk.lock();
-      if (--pending == 0) cv_done.notify_one();
+      pending.fetch_sub(1, std::memory_order_acq_rel);
     }
   }
   void copy(void* d, const void* s, size_t l) {
@@ -166,13 +175,13 @@ struct CopyPool {
       std::memcpy(d, s, l);
       return;
     }
+    dst = static_cast<char*>(d);
+    src = static_cast<const char*>(s);
+    len = l;
+    pending.store(n - 1, std::memory_order_relaxed);
     {
       std::lock_guard<std::mutex> g(mu);
-      dst = static_cast<char*>(d);
-      src = static_cast<const char*>(s);
-      len = l;
-      pending = n - 1;
-      ++gen;
+      gen.fetch_add(1, std::memory_order_acq_rel);
     }
     cv.notify_all();
     char* d0;
@@ -180,13 +189,12 @@ struct CopyPool {
     size_t l0;
     slice(0, d0, s0, l0);
     if (l0) std::memcpy(d0, s0, l0);
-    std::unique_lock<std::mutex> lk(mu);
-    cv_done.wait(lk, [&] { return pending == 0; });
+    while (pending.load(std::memory_order_acquire) != 0) std::this_thread::yield();
   }
 };
 
 struct Stager {
-  static constexpr size_t kChunk = size_t(8) << 20;
+  static constexpr size_t kChunk = size_t(16) << 20;
   static constexpr int kBufs = 3;
   std::mutex mu;
   char* buf[kBufs] = {};
