@@ -247,6 +247,10 @@ __global__ void __maxnreg__(t2::Cfg<H>::kMaxReg) tc2_step_kernel(const StepArgs 
   constexpr int NL = LY::NL;
   constexpr int NB = CF::NB, HP = CF::HP, NT = CF::NT, MP = CF::MP;
   constexpr int kPart = CF::kPart, kStream = CF::kStream;
+  // contraction threads per row / per point: all of them when the CTA is
+  // alone on its SM (NB = 2); one (unit group 0) when two CTAs share the SM,
+  // whose other CTA fills the idle issue slots (splitting measured slower)
+  constexpr int kCS = NB == 1 ? 1 : NT / 128;
   using AC = Act<ACT>;
 
   pdl_trigger();
@@ -704,7 +708,8 @@ __global__ void __maxnreg__(t2::Cfg<H>::kMaxReg) tc2_step_kernel(const StepArgs 
     const bool valid = p < np;
     const float px = nx, py = ny;
     float frow = 0.f;
-    if (interior && ug == 0 && p < nrows_tile) frow = a.forcing[(size_t)cell0 * a.T + p];
+    // contraction row of this thread (kCS adjacent threads per row, part 0 finishes it)
+    if (interior && tid % kCS == 0 && tid / kCS < nrows_tile) frow = a.forcing[(size_t)cell0 * a.T + tid / kCS];
     if (ug == 0) {
       sEx[kX * 128 + p] = px;
       sEx[kY * 128 + p] = py;
@@ -863,57 +868,74 @@ __global__ void __maxnreg__(t2::Cfg<H>::kMaxReg) tc2_step_kernel(const StepArgs 
       const float* T0 = chunk_ptr(a, cell0, 0, slab, 0);
       const float* T1 = chunk_ptr(a, cell0, 0, slab, 1);
       const float* T2 = conv ? chunk_ptr(a, cell0, 0, slab, 2) : T0;
-      // phase A: one thread per row (unit group 0) runs the three dot products
-      // (G_x . ux, G_y . uy, T . (bx ux + by uy)) as interleaved chains and
-      // finishes the residual itself (losses.hpp:122-136)
-      if (ug == 0 && p < nrows_tile) {
-        const int r = p, kk = r / a.T;
-        const float* sx = sEx + kUx * 128 + kk * a.Q;
-        const float* sy = sEx + kUy * 128 + kk * a.Q;
-        const float* sc = cvr + kk * a.Q;
-        const float* gx_r = T0 + r * a.Q;
-        const float* gy_r = T1 + r * a.Q;
-        const float* gt_r = T2 + r * a.Q;
+      // phase A: kCS = NT / 128 adjacent threads per row, each running the
+      // three dot products (G_x . ux, G_y . uy, T . (bx ux + by uy)) over its
+      // share of the quadrature points as two interleaved chains; the shares
+      // are combined by a fixed xor tree and part 0 finishes the residual
+      // (losses.hpp:122-136)
+      {
+        const int r = tid / kCS, part = tid % kCS;
         float ax[4] = {0.f, 0.f, 0.f, 0.f}, ay[4] = {0.f, 0.f, 0.f, 0.f}, at[4] = {0.f, 0.f, 0.f, 0.f};
-        int q = 0;
+        if (r < nrows_tile) {
+          const int kk = r / a.T;
+          const int q1 = (a.Q * (part + 1)) / kCS;
+          const float* sx = sEx + kUx * 128 + kk * a.Q;
+          const float* sy = sEx + kUy * 128 + kk * a.Q;
+          const float* sc = cvr + kk * a.Q;
+          const float* gx_r = T0 + r * a.Q;
+          const float* gy_r = T1 + r * a.Q;
+          const float* gt_r = T2 + r * a.Q;
+          int q = (a.Q * part) / kCS;
 #pragma unroll 2
-        for (; q + 3 < a.Q; q += 4) {
+          for (; q + 3 < q1; q += 4) {
 #pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            ax[u] = fmaf(gx_r[q + u], sx[q + u], ax[u]);
-            ay[u] = fmaf(gy_r[q + u], sy[q + u], ay[u]);
-            if (conv) at[u] = fmaf(gt_r[q + u], sc[q + u], at[u]);
+            for (int u = 0; u < 4; ++u) {
+              ax[u] = fmaf(gx_r[q + u], sx[q + u], ax[u]);
+              ay[u] = fmaf(gy_r[q + u], sy[q + u], ay[u]);
+              if (conv) at[u] = fmaf(gt_r[q + u], sc[q + u], at[u]);
+            }
+          }
+          for (; q < q1; ++q) {
+            ax[0] = fmaf(gx_r[q], sx[q], ax[0]);
+            ay[0] = fmaf(gy_r[q], sy[q], ay[0]);
+            if (conv) at[0] = fmaf(gt_r[q], sc[q], at[0]);
           }
         }
-        for (; q < a.Q; ++q) {
-          ax[0] = fmaf(gx_r[q], sx[q], ax[0]);
-          ay[0] = fmaf(gy_r[q], sy[q], ay[0]);
-          if (conv) at[0] = fmaf(gt_r[q], sc[q], at[0]);
+        float gx = (ax[0] + ax[1]) + (ax[2] + ax[3]);
+        float gy = (ay[0] + ay[1]) + (ay[2] + ay[3]);
+        float gt = (at[0] + at[1]) + (at[2] + at[3]);
+#pragma unroll
+        for (int o = 1; o < kCS; o <<= 1) {
+          gx += __shfl_xor_sync(0xffffffffu, gx, o);
+          gy += __shfl_xor_sync(0xffffffffu, gy, o);
+          gt += __shfl_xor_sync(0xffffffffu, gt, o);
         }
-        const float gx = (ax[0] + ax[1]) + (ax[2] + ax[3]);
-        const float gy = (ay[0] + ay[1]) + (ay[2] + ay[3]);
-        float res = e_fixed * (gx + gy);
-        if (conv) res += (at[0] + at[1]) + (at[2] + at[3]);
-        res -= frow;
-        rsqv[r] = res * res;
-        const float rb = a.rscale * res;
-        rbarv[r] = rb;
-        rgev[r] = rb * (gx + gy);
+        if (part == 0 && r < nrows_tile) {
+          float res = e_fixed * (gx + gy);
+          if (conv) res += gt;
+          res -= frow;
+          rsqv[r] = res * res;
+          const float rb = a.rscale * res;
+          rbarv[r] = rb;
+          rgev[r] = rb * (gx + gy);
+        }
       }
       __syncthreads();
       mark(6);
-      // phase B: one thread per point (unit group 0) runs the three adjoint
-      // columns and writes the point's adjoints; group 1 the per-cell sums
-      if (ug == 0) {
-        float ox = 0.f, oy = 0.f;
-        if (valid) {
-          const int myk = p / a.Q, myq = p - myk * a.Q;
+      // phase B: kCS adjacent threads per point, each running the three
+      // adjoint columns over its share of the cell's rows; part 0 writes the
+      // point's adjoints.  The last ncell threads then form the per-cell sums.
+      {
+        const int pt = tid / kCS, part = tid % kCS;
+        float bx4[4] = {0.f, 0.f, 0.f, 0.f}, by4[4] = {0.f, 0.f, 0.f, 0.f}, bt4[4] = {0.f, 0.f, 0.f, 0.f};
+        const bool pv = pt < np;
+        if (pv) {
+          const int myk = pt / a.Q, myq = pt - myk * a.Q;
           const float* cx = T0 + myq;
           const float* cy = T1 + myq;
           const float* ct = T2 + myq;
-          float bx4[4] = {0.f, 0.f, 0.f, 0.f}, by4[4] = {0.f, 0.f, 0.f, 0.f}, bt4[4] = {0.f, 0.f, 0.f, 0.f};
-          int r = myk * a.T;
-          const int r1 = r + a.T;
+          int r = myk * a.T + (a.T * part) / kCS;
+          const int r1 = myk * a.T + (a.T * (part + 1)) / kCS;
 #pragma unroll 2
           for (; r + 3 < r1; r += 4) {
 #pragma unroll
@@ -930,28 +952,43 @@ __global__ void __maxnreg__(t2::Cfg<H>::kMaxReg) tc2_step_kernel(const StepArgs 
             by4[0] = fmaf(cy[r * a.Q], rb, by4[0]);
             if (conv) bt4[0] = fmaf(ct[r * a.Q], rb, bt4[0]);
           }
-          ox = e_fixed * ((bx4[0] + bx4[1]) + (bx4[2] + bx4[3]));
-          oy = e_fixed * ((by4[0] + by4[1]) + (by4[2] + by4[3]));
-          if (conv) {
-            const float tt = (bt4[0] + bt4[1]) + (bt4[2] + bt4[3]);
-            ox = fmaf(a.bx, tt, ox);
-            oy = fmaf(a.by, tt, oy);
+        }
+        float sbx = (bx4[0] + bx4[1]) + (bx4[2] + bx4[3]);
+        float sby = (by4[0] + by4[1]) + (by4[2] + by4[3]);
+        float sbt = (bt4[0] + bt4[1]) + (bt4[2] + bt4[3]);
+#pragma unroll
+        for (int o = 1; o < kCS; o <<= 1) {
+          sbx += __shfl_xor_sync(0xffffffffu, sbx, o);
+          sby += __shfl_xor_sync(0xffffffffu, sby, o);
+          sbt += __shfl_xor_sync(0xffffffffu, sbt, o);
+        }
+        if (part == 0 && pt < 128) {
+          float ox = 0.f, oy = 0.f;
+          if (pv) {
+            ox = e_fixed * sbx;
+            oy = e_fixed * sby;
+            if (conv) {
+              ox = fmaf(a.bx, sbt, ox);
+              oy = fmaf(a.by, sbt, oy);
+            }
           }
+          sEx[kUb * 128 + pt] = 0.f;
+          sEx[kUxb * 128 + pt] = ox;
+          sEx[kUyb * 128 + pt] = oy;
+          atomic_max_abs(&sMax[kMx], ox);
+          atomic_max_abs(&sMax[kMy], oy);
         }
-        sEx[kUb * 128 + p] = 0.f;
-        sEx[kUxb * 128 + p] = ox;
-        sEx[kUyb * 128 + p] = oy;
-        atomic_max_abs(&sMax[kMx], ox);
-        atomic_max_abs(&sMax[kMy], oy);
-      } else if (ug == 1 && p < ncell) {
-        float s = 0.f, g = 0.f;
-        for (int r = p * a.T; r < (p + 1) * a.T; ++r) {
-          s += rsqv[r];
-          g += rgev[r];
-        }
-        if (MODE == kModeFused) {
-          cell_v += (double)(s * a.inv_nt);
-          cell_eg += (double)g;
+        const int cs = tid - (NT - ncell);
+        if (cs >= 0) {
+          float s = 0.f, g = 0.f;
+          for (int r = cs * a.T; r < (cs + 1) * a.T; ++r) {
+            s += rsqv[r];
+            g += rgev[r];
+          }
+          if (MODE == kModeFused) {
+            cell_v += (double)(s * a.inv_nt);
+            cell_eg += (double)g;
+          }
         }
       }
       mark(7);
