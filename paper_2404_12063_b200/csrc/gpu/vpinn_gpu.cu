@@ -936,10 +936,12 @@ void launch_k(bool pdl, void (*k)(KArgs...), int grid, int block, size_t smem, c
   CK(cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...));
 }
 
-// programmatic dependent launch stays off: A/B on the gear, PDL made the weak
-// epoch 1.3% slower (the early-resident successor CTAs skew the step
-// kernel's CTA placement) and the strong epoch 0.1% faster
-constexpr bool pdl_enabled() { return false; }
+// programmatic dependent launch: the tensor-core step triggers its dependents
+// after its tile loop (VPG_PDL_LATE), so the reduce + Adam kernel launches
+// while the step CTAs write their outputs and the next epoch's step launches
+// while Adam runs.  A/B (C5 gear epoch, C2 1-64 cells): 1-3% faster than no
+// PDL; an early trigger (at kernel entry) was 1% slower on the gear.
+constexpr bool pdl_enabled() { return true; }
 
 void launch_fused(vpinn_gpu_ctx* c, const vpg::StepArgs& a) {
   if (c->strong)

@@ -7,7 +7,7 @@ cp $LIB /tmp/lib_default.so
 for r in $(seq $R); do
   for i in $(seq 0 $((N-1))); do
     cp ab/lib$i.so $LIB
-    echo "$i $($CMD 2>&1 | tail -1 | cut -c1-200)"
+    echo "$i $($CMD 2>&1 | tail -1 | cut -c1-400)"
   done
 done
 cp /tmp/lib_default.so $LIB
