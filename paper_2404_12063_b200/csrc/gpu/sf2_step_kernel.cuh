@@ -142,25 +142,22 @@ struct Deriv<kActSigmoid> {
 // parameter-gradient GEMM: NS streams x 8 point blocks of K = 16
 __device__ __forceinline__ void issue_param5(uint32_t acc, uint64_t da, uint64_t db, uint32_t idesc, int first,
                                              int shift, uint64_t* bar) {
+  if (tc::elect_one()) {  // one elect for the group (tc2_step_kernel.cuh VPG_MMA_ELECT1)
 #pragma unroll 1
-  for (int s = 0; s < NS; ++s) {
+    for (int s = 0; s < NS; ++s) {
 #pragma unroll
-    for (int kp = 0; kp < kMP / 16; ++kp) {
-      const uint64_t off = (uint64_t)((s * kStream + 1024 * kp) >> 4);
-      const uint64_t ad = da + off, bd = db + off;
-      if (s == 0 && kp == 0) {
-        if (first)
-          tc::mma_warp(acc, ad, bd, idesc, 0u);
-        else if (shift > 0)
-          tc::mma_warp_sd(acc, ad, bd, idesc, shift);
+      for (int kp = 0; kp < kMP / 16; ++kp) {
+        const uint64_t off = (uint64_t)((s * kStream + 1024 * kp) >> 4);
+        const uint64_t ad = da + off, bd = db + off;
+        if (s == 0 && kp == 0 && !first && shift > 0)
+          tc::mma_f16_sd(acc, ad, bd, idesc, shift);
         else
-          tc::mma_warp(acc, ad, bd, idesc, 1u);
-      } else {
-        tc::mma_warp(acc, ad, bd, idesc, 1u);
+          tc::mma_bf16(acc, ad, bd, idesc, (s == 0 && kp == 0 && first) ? 0u : 1u);
       }
     }
+    tc::mma_commit(bar);
   }
-  tc::commit_warp(bar);
+  __syncwarp();
 }
 
 }  // namespace s2
@@ -175,7 +172,9 @@ __global__ void __maxnreg__(255) sf2_step_kernel(const StepArgs a) {
   constexpr int NL = LY::NL;
   using AC = Act<ACT>;
   using DV = Deriv<ACT>;
+#if !VPG_PDL_LATE
   pdl_trigger();
+#endif
   pdl_wait();
   if (a.stop_flag != nullptr && *a.stop_flag != 0) return;
   extern __shared__ __align__(1024) char s2_raw[];
@@ -493,7 +492,7 @@ __global__ void __maxnreg__(255) sf2_step_kernel(const StepArgs a) {
     operands_ready();
     if (warp < NS) issue_point_gemm(D == 2, 1, false);
     float ou[5] = {0.f, 0.f, 0.f, 0.f, 0.f};  // output-layer partials (last hidden)
-#pragma unroll 1
+#pragma unroll t2::kUL
     for (int l = 1; l <= NL; ++l) {
       const bool last = l == NL;
       const float fv = sSc[kScFv + l - 1], ft = sSc[kScFt + l - 1], fs = sSc[kScFs + l - 1];
@@ -702,7 +701,7 @@ __global__ void __maxnreg__(255) sf2_step_kernel(const StepArgs a) {
     if (warp < NS) issue_point_gemm(false, NL, true);
     if (warp == NS) issue_param_gemm(NL, gsc.first, gsc.shift);
     // ---- hidden layers, last-but-one first: G of hidden h from the propagated adjoints ----
-#pragma unroll 1
+#pragma unroll t2::kUL
     for (int h = NL; h >= 1; --h) {
       // incoming adjoint bounds at hidden h: through W_h^T
       const float C = sSc[kScC + h - 1];
@@ -798,6 +797,9 @@ __global__ void __maxnreg__(255) sf2_step_kernel(const StepArgs a) {
   }
 
   // =================== per-CTA outputs ===================
+#if VPG_PDL_LATE
+  pdl_trigger();
+#endif
   if constexpr (MODE == kModeForward) {
     tc::fence_before_sync();
     __syncthreads();
