@@ -3,6 +3,8 @@
 // the penalty kernel of the split path.
 #pragma once
 
+#include <type_traits>
+
 #include "contract_cells.cuh"
 #include "step_kernel.cuh"
 
@@ -332,6 +334,7 @@ struct ContractArgs {
   float* part;         // [item][3][qstride] partial adjoint columns
   double* loss_part;   // [gridDim.x][kLpWords]
   const int* stop_flag;
+  int rr_mq;  // contract_rowreg_kernel: M4 (> 0, float4 rows) or -M (scalar); 0: contract_rows_kernel.  items_per_cell = segments per CTA
 };
 
 constexpr int kCThreads = 256;
@@ -600,6 +603,331 @@ __global__ void contract_rows_reduce_kernel(const ContractArgs a) {
     if (conv) {
       ox = fmaf(a.bx, tt, ox);
       oy = fmaf(a.by, tt, oy);
+    }
+    a.uxb[i] = ox;
+    a.uyb[i] = oy;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Row contraction with WARP-OWNED rows (nt = 2, Q <= 1,664): the split
+// path's Algorithm 3 (losses.hpp:111-166) without CTA barriers on the
+// streaming path.
+//   * CTA b owns the contiguous global row range [R0(b), R1(b)) of the
+//     cell-major row sequence (row g = k T + j), R0(b) = floor(E T b / G):
+//     row-level balance whatever E, T;
+//   * inside a cell segment of that range warp w takes rows w, w + 8, ...;
+//     each warp streams its rows through its OWN ring of nsw one-row
+//     cp.async.bulk stages, copies a row into registers and re-issues the
+//     stage for its next row at once;
+//   * per row: r_j = e (G_x[j,:] s_x + G_y[j,:] s_y) - f_j (a fixed xor
+//     tree), then the adjoint columns acc[q] += rbar_j G[j][q] in registers;
+//   * the cell's point vectors (ux, uy, eps) arrive by cp.async.bulk into one
+//     of two buffers, issued a segment ahead (float4 layout);
+//   * at the end of a cell segment the eight warps' columns meet in shared
+//     memory (x, then y) and are summed in warp order into the segment's
+//     partial part[b * cmax + s] (s = the segment's index in the CTA's range).
+// contract_rowreg_reduce_kernel then sums, per (cell, q), the partials of the
+// CTAs covering the cell in CTA order.  Deterministic throughout.
+constexpr int kRRThreads = 256;
+constexpr int kRRWarps = kRRThreads / 32;
+// points per lane: NV = 4 M4 (VEC: lane l holds q = 128 m + 4 l + i, float4
+// rows, Q % 4 == 0) or M4 (scalar: q = 32 m + l); every row / vector buffer is
+// padded to VP = 32 NV points; vector pads are zero and row pads finite, so
+// no point needs a bounds check
+__host__ __device__ constexpr int rr_pad_points(int m4, bool vec) { return vec ? 128 * m4 : 32 * m4; }
+constexpr int kRRMaxStages = 8;  // row stages per warp
+__host__ __device__ constexpr size_t contract_rowreg_smem_bytes(int rs, int qstride, int vpad, int nsw) {
+  // per-warp ring [nsw][2][rs] | warp column slots [8][qstride] | vectors [2][3][vpad] | loss words | barriers
+  return sizeof(float) * ((size_t)kRRWarps * nsw * 2 * rs + (size_t)kRRWarps * qstride + 6 * (size_t)vpad) +
+         sizeof(double) * 2 * kRRWarps + sizeof(uint64_t) * (kRRWarps * kRRMaxStages + 2);
+}
+__device__ __forceinline__ int rr_row0(long long rows_total, int b, int G) {
+  return (int)(rows_total * b / G);
+}
+
+template <int M4, bool VEC>
+__global__ void __launch_bounds__(kRRThreads, 1) contract_rowreg_kernel(const ContractArgs a) {
+  if (a.stop_flag != nullptr && *a.stop_flag != 0) return;
+  constexpr int NW = kRRWarps;
+  constexpr int NV = VEC ? 4 * M4 : M4;  // points per lane
+  constexpr int VP = 32 * NV;            // padded points per row / vector
+  extern __shared__ __align__(128) float cs[];
+  const int Q = a.Q, T = a.T, rs = a.tstride, qs = a.qstride, nsw = a.nstage;
+  const float* __restrict__ tx0 = a.tens[0];
+  const float* __restrict__ ty0 = a.tens[1];
+  float* ring = cs;                                   // [NW][nsw][2][rs], rs >= VP + 8
+  float* slots = ring + (size_t)NW * nsw * 2 * rs;    // [NW][qs]
+  float* vbuf = slots + (size_t)NW * qs;              // [2][3][VP]: ux, uy, eps of a segment
+  double* lw = reinterpret_cast<double*>(vbuf + 6 * VP);  // [2][NW]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(lw + 2 * NW);  // [NW][kRRMaxStages] rows, then [2] vectors
+  uint64_t* vbar = bars + NW * kRRMaxStages;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const bool spatial = a.eps_source == 2;
+  const float e_fixed = a.eps_source == 1 ? *a.e_param : a.e_fixed;
+  const float rscale = a.rscale, inv_nt = a.inv_nt;
+  const long long rows_total = (long long)a.E * T;
+  const int R0 = rr_row0(rows_total, blockIdx.x, gridDim.x), R1 = rr_row0(rows_total, blockIdx.x + 1, gridDim.x);
+  float* wring = ring + (size_t)w * nsw * 2 * rs;
+  uint64_t* wbar = bars + w * kRRMaxStages;
+  // pads: rows [Q, rs) of every stage and vectors [Q, VP) zero (the bulk
+  // copies write [0, Q) plus at most 12 bytes of finite slop)
+  for (int slot = w; slot < NW * nsw * 2; slot += NW)
+    for (int i = Q + lane; i < rs; i += 32) ring[(size_t)slot * rs + i] = 0.f;
+  for (int v = w; v < 6; v += NW)
+    for (int i = Q + lane; i < VP; i += 32) vbuf[v * VP + i] = 0.f;
+  if (tid == 0) {
+    for (int i = 0; i < NW * kRRMaxStages + 2; ++i) mbar_init(&bars[i], 1);
+    fence_mbar_init();
+  }
+  fence_proxy_async();
+  __syncthreads();
+  auto seg_end = [&](int g) { return min(R1, (g / T + 1) * T); };
+  // the point vectors of the segment starting at row s0 into buffer vb (VEC: by
+  // cp.async.bulk on vbar[vb]; scalar layout: plain loads, pads stay zero)
+  auto issue_vec = [&](int s0, int vb) {
+    const size_t pb = (size_t)(s0 / T) * Q;
+    float* d = vbuf + vb * 3 * VP;
+    const uint32_t bytes = 4u * (uint32_t)Q;
+    mbar_arrive_expect_tx(&vbar[vb], (spatial ? 3u : 2u) * bytes);
+    bulk_g2s(d, a.ux + pb, bytes, &vbar[vb]);
+    bulk_g2s(d + VP, a.uy + pb, bytes, &vbar[vb]);
+    if (spatial) bulk_g2s(d + 2 * VP, a.eps + pb, bytes, &vbar[vb]);
+  };
+  if constexpr (VEC) {
+    if (tid == 0) {
+      if (R0 < R1) issue_vec(R0, 0);
+      if (seg_end(R0) < R1) issue_vec(seg_end(R0), 1);
+    }
+  }
+  // this warp's rows: in each cell segment [s0, s1) of [R0, R1), s0 + w + NW i
+  auto first_in = [&](int s0) {  // the warp's first row at or after segment start s0 (or R1)
+    for (; s0 < R1; s0 = seg_end(s0))
+      if (s0 + w < seg_end(s0)) return s0 + w;
+    return R1;
+  };
+  // producer cursor (pg, end of its segment pe)
+  auto next_row = [&](int& g, int& e) {
+    if (g + NW < e) {
+      g += NW;
+    } else {
+      g = first_in(e);
+      e = g < R1 ? seg_end(g) : R1;
+    }
+  };
+  auto issue = [&](int g, int st) {
+    const Seg sxg = seg_of(tx0 + (size_t)g * Q, (size_t)Q), syg = seg_of(ty0 + (size_t)g * Q, (size_t)Q);
+    float* stage = wring + (size_t)st * 2 * rs;
+    fence_proxy_async();
+    mbar_arrive_expect_tx(&wbar[st], sxg.bytes + syg.bytes);
+    bulk_g2s(stage, sxg.src, sxg.bytes, &wbar[st]);
+    bulk_g2s(stage + rs, syg.src, syg.bytes, &wbar[st]);
+  };
+  // the warp's producer cursor: nsw rows in flight, row i of the warp's
+  // sequence in stage i % nsw
+  int pg = first_in(R0), pe = pg < R1 ? seg_end(pg) : R1;
+  for (int st = 0; st < nsw; ++st) {
+    if (lane == 0 && pg < R1) issue(pg, st);
+    if (pg < R1) next_row(pg, pe);
+  }
+  uint32_t parity = 0u;
+  int cst = 0;  // consumer stage
+  double lv = 0.0, leg = 0.0;  // lane 0: this warp's loss terms
+  float ax[NV], ay[NV];
+  // lane-local point offset of value v: VEC 128 (v / 4) + 4 lane + v % 4, scalar 32 v + lane
+  auto qof = [&](int v) { return VEC ? 128 * (v >> 2) + 4 * lane + (v & 3) : 32 * v + lane; };
+  int s_idx = 0;
+  for (int s0 = R0; s0 < R1; s0 = seg_end(s0), ++s_idx) {
+    const int s1 = seg_end(s0), k = s0 / T, vb = s_idx & 1;
+    const float* vx_ = vbuf + vb * 3 * VP;
+    const float* vy_ = vx_ + VP;
+    const float* ve_ = vx_ + 2 * VP;
+    if constexpr (VEC) {
+      mbar_wait(&vbar[vb], (s_idx >> 1) & 1);
+    } else {
+      float* d = vbuf + vb * 3 * VP;
+      const size_t pb = (size_t)k * Q;
+      for (int q = tid; q < Q; q += kRRThreads) {
+        d[q] = a.ux[pb + q];
+        d[VP + q] = a.uy[pb + q];
+        if (spatial) d[2 * VP + q] = a.eps[pb + q];
+      }
+      __syncthreads();
+    }
+#pragma unroll
+    for (int v = 0; v < NV; ++v) ax[v] = ay[v] = 0.f;
+    for (int g = s0 + w; g < s1; g += NW) {
+      const float frow = a.forcing[g];  // forcing (k, j) at k T + j = g
+      mbar_wait(&wbar[cst], (parity >> cst) & 1u);
+      parity ^= 1u << cst;
+      const float* stage = wring + (size_t)cst * 2 * rs;
+      float rx[NV], ry[NV];
+      if constexpr (VEC) {
+#pragma unroll
+        for (int m = 0; m < M4; ++m) {
+          const float4 x4 = lds4(stage + 128 * m + 4 * lane), y4 = lds4(stage + rs + 128 * m + 4 * lane);
+          rx[4 * m] = x4.x, rx[4 * m + 1] = x4.y, rx[4 * m + 2] = x4.z, rx[4 * m + 3] = x4.w;
+          ry[4 * m] = y4.x, ry[4 * m + 1] = y4.y, ry[4 * m + 2] = y4.z, ry[4 * m + 3] = y4.w;
+        }
+      } else {
+        const float* gx = stage + pre_of(tx0 + (size_t)g * Q);
+        const float* gy = stage + rs + pre_of(ty0 + (size_t)g * Q);
+#pragma unroll
+        for (int v = 0; v < NV; ++v) {
+          rx[v] = gx[32 * v + lane];
+          ry[v] = gy[32 * v + lane];
+        }
+      }
+      __syncwarp();  // every lane has its share of the row: the stage is free
+      if (lane == 0 && pg < R1) issue(pg, cst);
+      if (pg < R1) next_row(pg, pe);
+      cst = cst + 1 == nsw ? 0 : cst + 1;
+      float d[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+      auto dot = [&](auto sp) {
+        constexpr bool SP = decltype(sp)::value;
+#pragma unroll
+        for (int v = 0; v < NV; v += (VEC ? 4 : 1)) {
+          float vx[4], vy[4];
+          if constexpr (VEC) {
+            const float4 x4 = lds4(vx_ + qof(v)), y4 = lds4(vy_ + qof(v));
+            vx[0] = x4.x, vx[1] = x4.y, vx[2] = x4.z, vx[3] = x4.w;
+            vy[0] = y4.x, vy[1] = y4.y, vy[2] = y4.z, vy[3] = y4.w;
+            if constexpr (SP) {
+              const float4 e4 = lds4(ve_ + qof(v));
+              vx[0] *= e4.x, vx[1] *= e4.y, vx[2] *= e4.z, vx[3] *= e4.w;
+              vy[0] *= e4.x, vy[1] *= e4.y, vy[2] *= e4.z, vy[3] *= e4.w;
+            }
+          } else {
+            vx[0] = vx_[qof(v)];
+            vy[0] = vy_[qof(v)];
+            if constexpr (SP) {
+              vx[0] *= ve_[qof(v)];
+              vy[0] *= ve_[qof(v)];
+            }
+          }
+#pragma unroll
+          for (int i = 0; i < (VEC ? 4 : 1); ++i) {
+            d[(v + i) & 3] = fmaf(rx[v + i], vx[i], d[(v + i) & 3]);
+            d[4 + ((v + i) & 3)] = fmaf(ry[v + i], vy[i], d[4 + ((v + i) & 3)]);
+          }
+        }
+      };
+      if (spatial)
+        dot(std::true_type{});
+      else
+        dot(std::false_type{});
+      float dx = (d[0] + d[1]) + (d[2] + d[3]), dy = (d[4] + d[5]) + (d[6] + d[7]);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        dx += __shfl_xor_sync(0xffffffffu, dx, o);
+        dy += __shfl_xor_sync(0xffffffffu, dy, o);
+      }
+      float res = spatial ? dx + dy : e_fixed * (dx + dy);
+      res -= frow;
+      const float rb = rscale * res;
+      if (lane == 0) {
+        if (a.res) a.res[g] = res;
+        lv += (double)(res * res * inv_nt);
+        leg += (double)(rb * (dx + dy));
+      }
+#pragma unroll
+      for (int v = 0; v < NV; ++v) {
+        ax[v] = fmaf(rx[v], rb, ax[v]);
+        ay[v] = fmaf(ry[v], rb, ay[v]);
+      }
+    }
+    // the segment's columns (x, then y): warps' slots, summed in warp order
+    float* pp = a.part + ((size_t)blockIdx.x * a.items_per_cell + s_idx) * 3 * qs;
+    float* my = slots + (size_t)w * qs;
+#pragma unroll
+    for (int t = 0; t < 2; ++t) {
+      if constexpr (VEC) {
+#pragma unroll
+        for (int m = 0; m < M4; ++m) {
+          const int q = 128 * m + 4 * lane;
+          if (q < Q)
+            sts4(my + q, t ? make_float4(ay[4 * m], ay[4 * m + 1], ay[4 * m + 2], ay[4 * m + 3])
+                           : make_float4(ax[4 * m], ax[4 * m + 1], ax[4 * m + 2], ax[4 * m + 3]));
+        }
+      } else {
+#pragma unroll
+        for (int v = 0; v < NV; ++v) {
+          const int q = qof(v);
+          if (q < Q) my[q] = t ? ay[v] : ax[v];
+        }
+      }
+      __syncthreads();
+      if constexpr (VEC) {
+        for (int q = 4 * tid; q < Q; q += 4 * kRRThreads) {
+          float4 v = lds4(slots + q);
+#pragma unroll
+          for (int ww = 1; ww < NW; ++ww) {
+            const float4 u = lds4(slots + (size_t)ww * qs + q);
+            v.x += u.x, v.y += u.y, v.z += u.z, v.w += u.w;
+          }
+          *reinterpret_cast<float4*>(pp + t * qs + q) = v;
+        }
+      } else {
+        for (int q = tid; q < Q; q += kRRThreads) {
+          float v = slots[q];
+#pragma unroll
+          for (int ww = 1; ww < NW; ++ww) v += slots[(size_t)ww * qs + q];
+          pp[t * qs + q] = v;
+        }
+      }
+      __syncthreads();  // slots read; after t = 1 also every warp is done with vector buffer vb
+    }
+    if constexpr (VEC) {
+      const int s2 = seg_end(s1 < R1 ? s1 : R1);  // start of segment s_idx + 2
+      if (tid == 0 && s1 < R1 && s2 < R1) issue_vec(s2, vb);
+    }
+  }
+  if (lane == 0) {
+    lw[w] = lv;
+    lw[NW + w] = leg;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    double v = 0.0, g = 0.0;
+    for (int ww = 0; ww < NW; ++ww) {
+      v += lw[ww];
+      g += lw[NW + ww];
+    }
+    double* lp = a.loss_part + (size_t)blockIdx.x * kLpWords;
+    for (int i = 0; i < kLpWords; ++i) lp[i] = 0.0;
+    lp[kLpVar] = v;
+    lp[kLpEpsGrad] = g;
+  }
+}
+
+// thread per (cell, q): the partials of the CTAs covering the cell, in CTA
+// order.  cover[k] = (first CTA b, its segment index for cell k, last CTA):
+// the CTAs after the first start inside cell k (segment 0)
+__global__ void contract_rowreg_reduce_kernel(const ContractArgs a, const int4* __restrict__ cover) {
+  if (a.stop_flag != nullptr && *a.stop_flag != 0) return;
+  const size_t n = (size_t)a.E * a.Q;
+  const bool spatial = a.eps_source == 2;
+  const float e_fixed = a.eps_source == 1 ? *a.e_param : a.e_fixed;
+  const int qs = a.qstride, cmax = a.items_per_cell;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+    const int k = (int)(i / a.Q), q = (int)(i - (size_t)k * a.Q);
+    const int4 cv = cover[k];
+    const float* pp = a.part + ((size_t)cv.x * cmax + cv.y) * 3 * qs + q;
+    float tx = pp[0], ty = pp[qs];
+    for (int b = cv.x + 1; b <= cv.z; ++b) {
+      pp = a.part + (size_t)b * cmax * 3 * qs + q;
+      tx += pp[0];
+      ty += pp[qs];
+    }
+    float ox, oy;
+    if (spatial) {
+      const float ep = a.eps[i];
+      ox = ep * tx;
+      oy = ep * ty;
+      if (a.eb) a.eb[i] = a.ux[i] * tx + a.uy[i] * ty;
+    } else {
+      ox = e_fixed * tx;
+      oy = e_fixed * ty;
     }
     a.uxb[i] = ox;
     a.uyb[i] = oy;

@@ -474,6 +474,7 @@ struct vpinn_gpu_ctx {
   size_t smem_cc = 0;
   int grid_contract = 0, grid_pen = 0, grid_fwd = 0, grid_creduce = 0;
   DBuf<float> cpart;  // row-block contraction partial adjoint columns
+  DBuf<int> rr_cover;  // warp-owned-row contraction: per cell (first CTA, segment, last CTA, 0)
   size_t smem_contract = 0, smem_fwd = 0;
   // graphs
   std::map<std::tuple<int, int, double>, cudaGraphExec_t> graphs;
@@ -621,6 +622,19 @@ const void* cw_kernel(int nw, bool fixed) {
   return nw == 16 ? (const void*)vpg::contract_warp_kernel<16>
                   : (nw == 12 ? (const void*)vpg::contract_warp_kernel<12> : (const void*)vpg::contract_warp_kernel<8>);
 }
+
+// the warp-owned-row contraction by points per lane (Q <= 32 MQ)
+const void* rowreg_kernel(int mq) {  // mq > 0: float4 rows, M4 = mq; mq < 0: scalar, M = -mq
+  switch (mq) {
+    case 4: return (const void*)vpg::contract_rowreg_kernel<4, true>;
+    case 8: return (const void*)vpg::contract_rowreg_kernel<8, true>;
+    case 13: return (const void*)vpg::contract_rowreg_kernel<13, true>;
+    case -16: return (const void*)vpg::contract_rowreg_kernel<16, false>;
+    case -32: return (const void*)vpg::contract_rowreg_kernel<32, false>;
+    default: return (const void*)vpg::contract_rowreg_kernel<52, false>;
+  }
+}
+inline long long ceil_div_ll(long long a, long long b) { return (a + b - 1) / b; }
 
 void configure(vpinn_gpu_ctx* c) {
   if (c->strong) {
@@ -844,6 +858,49 @@ void configure(vpinn_gpu_ctx* c) {
     ca.n_items = c->E * ca.items_per_cell;
     c->grid_contract = std::max(1, std::min(ca.n_items, ctas));
     c->grid_creduce = std::max(1, std::min(ceil_div(c->E * c->Q, 256), 4 * c->sm_count));
+    // two premultipliers and at most 52 points per lane: warp-owned rows
+    // (contract_rowreg_kernel), one CTA per SM, row-balanced ranges
+    ca.rr_mq = 0;
+    if (c->nt == 2 && c->Q <= 32 * 52 && rows_total > 0) {
+      const bool vec = c->Q % 4 == 0;
+      const int m4 = vec ? (c->Q <= 512 ? 4 : (c->Q <= 1024 ? 8 : 13)) : (c->Q <= 512 ? 16 : (c->Q <= 1024 ? 32 : 52));
+      const int vp = vpg::rr_pad_points(m4, vec);
+      const int rs = round4(vp + 8);
+      // row stages per warp: as many as fit (one row in flight per stage)
+      int nsw = vpg::kRRMaxStages;
+      while (nsw > 1 && vpg::contract_rowreg_smem_bytes(rs, ca.qstride, vp, nsw) > (size_t)227 * 1024) --nsw;
+      const size_t smem = vpg::contract_rowreg_smem_bytes(rs, ca.qstride, vp, nsw);
+      if (smem <= (size_t)227 * 1024) {
+        ca.rr_mq = vec ? m4 : -m4;
+        ca.tstride = rs;
+        ca.nstage = nsw;
+        const void* fn = rowreg_kernel(ca.rr_mq);
+        CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        c->smem_contract = smem;
+        c->grid_contract = (int)std::max<long long>(1, std::min<long long>(rows_total, c->sm_count));
+        const long long per = ceil_div_ll(rows_total, c->grid_contract);
+        ca.items_per_cell = (int)std::min<long long>(c->E, (per + c->T - 1) / c->T + 1);  // segments per CTA
+        ca.n_items = c->grid_contract * ca.items_per_cell;
+        // per cell: the first covering CTA, the cell's segment index in it, the last covering CTA
+        const int G = c->grid_contract;
+        auto row0 = [&](int b) { return (long long)(rows_total * b / G); };
+        std::vector<int> cov(4 * (size_t)c->E);
+        int b = 0;
+        for (int k = 0; k < c->E; ++k) {
+          const long long g0 = (long long)k * c->T, g1 = g0 + c->T;
+          while (b + 1 < G && row0(b + 1) <= g0) ++b;
+          int e = b;
+          while (e + 1 < G && row0(e + 1) < g1) ++e;
+          cov[4 * k] = b;
+          cov[4 * k + 1] = (int)(k - row0(b) / c->T);
+          cov[4 * k + 2] = e;
+          cov[4 * k + 3] = 0;
+        }
+        c->rr_cover.alloc(cov.size(), c->stream);
+        CK(cudaMemcpyAsync(c->rr_cover.p, cov.data(), cov.size() * sizeof(int), cudaMemcpyHostToDevice, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+      }
+    }
     c->cpart.alloc((size_t)ca.n_items * 3 * ca.qstride, c->stream);
     ca.part = c->cpart.p;
     c->grid_pen = (c->n_bnd + c->n_sen) ? std::min(64, ceil_div(c->n_bnd + c->n_sen, 256)) : 0;
@@ -960,6 +1017,16 @@ void launch_fused(vpinn_gpu_ctx* c, const vpg::StepArgs& a) {
 // fixed-order reduction of their partial adjoint columns
 void launch_contract_rows(vpinn_gpu_ctx* c, const vpg::ContractArgs& ca) {
   if (ca.n_items <= 0) return;
+  if (ca.rr_mq) {
+    auto fn = reinterpret_cast<void (*)(vpg::ContractArgs)>(const_cast<void*>(rowreg_kernel(ca.rr_mq)));
+    fn<<<c->grid_contract, vpg::kRRThreads, c->smem_contract, c->stream>>>(ca);
+    CK(cudaGetLastError());
+    vpg::contract_rowreg_reduce_kernel<<<c->grid_creduce, 256, 0, c->stream>>>(
+        ca, reinterpret_cast<const int4*>(c->rr_cover.p));
+    CK(cudaGetLastError());
+    c->launches += 2;
+    return;
+  }
   vpg::contract_rows_kernel<<<c->grid_contract, vpg::kCRThreads, c->smem_contract, c->stream>>>(ca);
   CK(cudaGetLastError());
   vpg::contract_rows_reduce_kernel<<<c->grid_creduce, 256, 0, c->stream>>>(ca);

@@ -211,3 +211,43 @@ def test_unserved_network_shapes_fail_with_a_config_error(layers):
     with pytest.raises(VpinnError) as e:
         make_pair(spec)
     assert e.value.code == 2
+
+
+# the split path's row contraction (Q > 128 points per cell): the warp-owned-row
+# kernel in its float4 (Q % 4 == 0, 4 / 8 / 13 float4 per lane) and scalar
+# (Q % 4 != 0) layouts, CTA row ranges spanning several small cells, fewer rows
+# than SMs, a trainable and a spatial coefficient, and the row-block kernel
+# beyond 1,664 points (or with convection)
+ROW_CASES = {
+    "vec4_many_cells": dict(mesh=(15, 14), nt=2, nq=12),
+    "scalar_many_cells": dict(mesh=(15, 14), nt=2, nq=13, eps_source=1, scalars=(1.3,), n_sensors=11,
+                              sensor_field="sin2pi_u"),
+    "vec8_3x3": dict(mesh=(3, 3), nt=3, nq=24),
+    "vec13_one_cell": dict(mesh=(1, 1), nt=6, nq=40),
+    "scalar52_spatial": dict(mesh=(2, 1), nt=4, nq=35, layers=(2, 16, 16, 16, 2), eps_source=2, bx=0.0,
+                             forcing="sinpi_vareps_f"),
+    "rows_kernel_q1681": dict(mesh=(1, 2), nt=5, nq=41),
+    "rows_kernel_conv": dict(mesh=(2, 2), nt=4, nq=20, bx=0.4, by=-0.3),
+}
+
+
+@pytest.mark.parametrize("case", list(ROW_CASES))
+def test_row_contraction_layouts_match_oracle(case):
+    kw = dict(ROW_CASES[case])
+    mesh, nt, nq = kw.pop("mesh"), kw.pop("nt"), kw.pop("nq")
+    kw.setdefault("layers", (2, 30, 30, 30, 1))
+    kw.setdefault("forcing", "sin2pi_f")
+    spec = po.ProblemSpec(*po.structured_mesh(*mesh), n_test_1d=nt, n_quad_1d=nq, boundary_g="sin2pi_u",
+                          n_boundary=37, seed=9, **kw)
+    ob, g, p0 = make_pair(spec)
+    assert ob.Q > 128  # the split path
+    po_, go32 = ob.loss_and_grad(p0)
+    pg, gg = g.loss_and_grad()
+    _, g64 = po.OracleProblem(spec, double=True).loss_and_grad(p0.astype(np.float64))
+    assert abs(pg[0] - po_[0]) / abs(po_[0]) < 1e-5, (pg, po_)
+    e32 = np.abs(go32 - g64).max() / np.abs(g64).max()
+    assert np.abs(gg - g64).max() / np.abs(g64).max() < max(1e-5, 4.0 * e32)
+    # bitwise reproducible (fixed summation order everywhere)
+    pg2, gg2 = g.loss_and_grad()
+    assert np.array_equal(np.asarray(pg2), np.asarray(pg)) and np.array_equal(gg2, gg)
+    g.close()
