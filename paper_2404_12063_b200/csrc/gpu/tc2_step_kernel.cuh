@@ -92,7 +92,14 @@ struct Cfg {
 
 constexpr int kUC = VPG_TC2_UC;
 constexpr int kUL = VPG_TC2_UL;
-constexpr int kTailFloats = 8 * 128;  // contraction scratch after the slab in buffer A
+// contraction scratch after the slab in buffer A, [rows][128]: 0 bx ux + by uy,
+// 4 rbar, 5 r^2, 6 rbar (gx + gy); two outputs also 1 eps, 2 y1, 3 eps ux,
+// 7 eps uy, 8 y1bar, 8 + g the y1 partial of unit group g (all live between
+// the forward's output layer and the reverse's first operand store)
+template <int C>
+constexpr int tail_floats() { return (C == 2 ? 12 : 8) * 128; }
+constexpr int kTailFloats = tail_floats<1>();
+enum : int { kTE = 1, kTY1 = 2, kTSx = 3, kTSy = 7, kTY1b = 8, kTY1p = 8 };
 constexpr float kOneBias = 20.0f;     // bias of the constant-one unit: act(20) == 1.0f
 
 // exchange rows ([row][128] floats).  The output-layer partials of unit
@@ -102,7 +109,10 @@ enum : int { kX = 0, kY, kU, kUx, kUy, kUb, kUxb, kUyb, kRows };
 constexpr int kPu = kUb;
 
 // per-warp running sums of the CUDA-core gradients: W0x | W0y | b0 | Wd (16 units each)
-enum : int { kAW0x = 0, kAW0y = 16, kAB0 = 32, kAWd = 48, kAccW = 64 };
+// (two outputs: Wd of channel 1 at kAWd2)
+enum : int { kAW0x = 0, kAW0y = 16, kAB0 = 32, kAWd = 48, kAWd2 = 64 };
+template <int C>
+constexpr int acc_w() { return C == 2 ? 80 : 64; }
 
 // uniform constants (floats in S_SC)
 enum : int {
@@ -115,12 +125,13 @@ enum : int {
   kScBt = 12,  // [4] tangent bounds of hidden 1..D outputs
   kScC = 16,   // [2] max column abs-sum of W_l
   kScWd = 18,  // max |wd|
+  kScWd2 = 19,  // max |wd| of output channel 1 (two outputs)
   kScN = 20
 };
 // integer exponents (ints in S_SCI): kW[2], kXv[2], kXt[2]
 enum : int { kSiW = 0, kSiXv = 2, kSiXt = 4, kSiN = 6 };
 
-template <int H, int D>
+template <int H, int D, int C = 1>
 struct Lay {
   using CF = Cfg<H>;
   static constexpr int NL = D - 1;
@@ -133,10 +144,11 @@ struct Lay {
   static constexpr int S_W0 = 0;                       // [HP][4] (w_x, w_y, b, 0)
   static constexpr int S_W0S = S_W0 + 4 * HP;          // [HP][2] (w_x, w_y) * 2^kXt of X_1
   static constexpr int S_BIAS = S_W0S + 2 * HP;        // [2][HP]
-  static constexpr int S_WD = S_BIAS + 2 * HP;         // [HP] + output bias at HP (+8)
-  static constexpr int S_EX = S_WD + HP + 8;           // [EX_ROWS][128]
-  static constexpr int S_ACC = S_EX + EX_ROWS * 128;   // [warps][kAccW]
-  static constexpr int S_RED = S_ACC + (CF::NT / 32) * kAccW;  // 2 * warps doubles
+  // output weights: channel 0 [HP], biases at HP, HP + 1; channel 1 at HP + 8
+  static constexpr int S_WD = S_BIAS + 2 * HP;
+  static constexpr int S_EX = S_WD + 2 * HP + 8;       // [EX_ROWS][128]
+  static constexpr int S_ACC = S_EX + EX_ROWS * 128;   // [warps][acc_w<C>()]
+  static constexpr int S_RED = S_ACC + (CF::NT / 32) * acc_w<C>();  // 2 * warps doubles
   static constexpr int S_SC = S_RED + 2 * 2 * (CF::NT / 32);   // [kScN] floats
   static constexpr int S_SCI = S_SC + kScN;            // [kSiN] ints
   static constexpr int S_MAX = S_SCI + kSiN;           // [16] uint: tile maxima, weight norms
@@ -158,8 +170,9 @@ struct Lay {
 };
 
 // S_MAX words: tile maxima of |ub|, |uxb|, |uyb|; max |w0x|, |w0y|, |wd|; per MMA
-// layer (max |W|, max row abs-sum, max column abs-sum)
-enum : int { kMb = 0, kMx = 1, kMy = 2, kNW0 = 3, kNLayer = 6 };
+// layer (max |W|, max row abs-sum, max column abs-sum); two outputs: max |wd|
+// of channel 1, tile maximum of |y1bar|
+enum : int { kMb = 0, kMx = 1, kMy = 2, kNW0 = 3, kNLayer = 6, kNWd2 = 12, kMe = 13 };
 
 // 8-value butterfly reduce-scatter over the warp's 32 lanes: afterwards lane
 // l holds the sum over all lanes of value index ((l>>4)&1)*4 + ((l>>3)&1)*2 +
@@ -282,12 +295,14 @@ __device__ __forceinline__ void issue_param(uint32_t acc, uint64_t da, uint64_t 
 // kModeReverse = forward recompute + reverse from the adjoints in a.in_*
 // (the split path of cells larger than a tile: forward -> contraction ->
 // penalty -> reverse)
-template <int H, int D, int ACT, int MODE = kModeFused>
+template <int H, int D, int ACT, int MODE = kModeFused, int C = 1>
 __global__ void __maxnreg__(t2::Cfg<H>::kMaxReg) tc2_step_kernel(const StepArgs a) {
   using namespace t2;
   static_assert(D == 2 || D == 3, "tc2 step: 2 or 3 hidden layers");
+  static_assert(C == 1 || C == 2, "tc2 step: one output, or two (spatial-eps head)");
   using CF = Cfg<H>;
-  using LY = Lay<H, D>;
+  using LY = Lay<H, D, C>;
+  constexpr int kAccW = acc_w<C>();
   constexpr int NL = LY::NL;
   constexpr int NB = CF::NB, HP = CF::HP, NT = CF::NT, MP = CF::MP;
   constexpr int kPart = CF::kPart, kStream = CF::kStream;
@@ -326,6 +341,8 @@ __global__ void __maxnreg__(t2::Cfg<H>::kMaxReg) tc2_step_kernel(const StepArgs 
   float* sW0s = sf + LY::S_W0S;
   float* sBias = sf + LY::S_BIAS;
   float* sWd = sf + LY::S_WD;
+  float* sWd2 = sWd + HP + 8;  // output channel 1 (C == 2)
+  const bool spatial = C == 2 && a.eps_source == 2;
   float* sEx = sf + LY::S_EX;
   float* sAcc = sf + LY::S_ACC;
   double* sRed = reinterpret_cast<double*>(sf + LY::S_RED);
@@ -400,8 +417,12 @@ __global__ void __maxnreg__(t2::Cfg<H>::kMaxReg) tc2_step_kernel(const StepArgs 
     sW0[4 * i + 2] = b;
     sW0[4 * i + 3] = 0.f;
     sWd[i] = wd;
+    if constexpr (C == 2) sWd2[i] = i < net.in_w[D] ? P[net.w_off[D] + net.in_w[D] + i] : 0.f;
   }
-  if (tid == 0) sWd[HP] = P[net.b_off[D]];
+  if (tid == 0) {
+    sWd[HP] = P[net.b_off[D]];
+    if constexpr (C == 2) sWd[HP + 1] = P[net.b_off[D] + 1];
+  }
   for (int l = 1; l <= NL; ++l)
     for (int o = tid; o < HP; o += NT)
       sBias[(l - 1) * HP + o] = o < net.out_w[l] ? P[net.b_off[l] + o] : ((o == H) ? kOneBias : 0.f);
@@ -437,6 +458,7 @@ __global__ void __maxnreg__(t2::Cfg<H>::kMaxReg) tc2_step_kernel(const StepArgs 
     atomic_max_abs(&sNorm[0], sW0[4 * tid]);
     atomic_max_abs(&sNorm[1], sW0[4 * tid + 1]);
     atomic_max_abs(&sNorm[2], sWd[tid]);
+    if constexpr (C == 2) atomic_max_abs(&sMax[kNWd2], sWd2[tid]);
   }
   for (int t = tid; t < 2 * HP * NL; t += NT) {
     const int l = t / (2 * HP), j = t % HP;
@@ -474,6 +496,7 @@ __global__ void __maxnreg__(t2::Cfg<H>::kMaxReg) tc2_step_kernel(const StepArgs 
       sSc[kScC + l] = __uint_as_float(s_lnorm[l][2]);
     }
     sSc[kScWd] = __uint_as_float(sNorm[2]);
+    sSc[kScWd2] = C == 2 ? __uint_as_float(sMax[kNWd2]) : 0.f;
   }
   __syncthreads();
   for (int i = tid; i < HP; i += NT) {  // layer-0 tangent weights pre-scaled for X_1
@@ -743,7 +766,13 @@ __global__ void __maxnreg__(t2::Cfg<H>::kMaxReg) tc2_step_kernel(const StepArgs 
   float nx, ny;
   load_xy(geo(blockIdx.x), nx, ny);
   // contraction scratch after the slab in buffer A
-  float* tail = reinterpret_cast<float*>(bufA) + a.nt * a.tstride;
+  float* tail = reinterpret_cast<float*>(bufA) + (MODE == kModeFused ? a.nt * a.tstride : 0);
+  // two outputs: the spatial-eps head's rows (tail_floats)
+  float* tE = tail + kTE * 128;
+  float* tY1 = tail + kTY1 * 128;
+  float* tSx = tail + kTSx * 128;
+  float* tSy = tail + kTSy * 128;
+  float* tY1b = tail + kTY1b * 128;
   float* cvr = tail;              // [128] bx ux + by uy
   float* rbarv = tail + 4 * 128;  // [128]
   float* rsqv = tail + 5 * 128;
@@ -766,6 +795,7 @@ __global__ void __maxnreg__(t2::Cfg<H>::kMaxReg) tc2_step_kernel(const StepArgs 
       sEx[kY * 128 + p] = py;
     }
     if (tid < 3) sMax[tid] = 0u;  // tile maxima of |ub|, |uxb|, |uyb| (first read after 3+ barriers)
+    if (C == 2 && tid == 3) sMax[kMe] = 0u;
     // D == 2: buffer A (slab) is free from the tile start
     if (D == 2 && interior && tid == 0)
       issue_chunk(a, cell0, 0, nrows_tile, reinterpret_cast<float*>(bufA), tma_bar);
@@ -781,6 +811,7 @@ __global__ void __maxnreg__(t2::Cfg<H>::kMaxReg) tc2_step_kernel(const StepArgs 
     // overlaps the tangent-stream MMAs), stored (or consumed by the output
     // layer when hidden l+1 is the last), then the tangents.
     float ou = 0.f, oux = 0.f, ouy = 0.f;  // output-layer partials (last hidden)
+    float oy1 = 0.f;                      // output channel 1 (C == 2)
 #pragma unroll kUL
     for (int l = 1; l <= NL; ++l) {
       const bool last = l == NL;
@@ -807,6 +838,10 @@ __global__ void __maxnreg__(t2::Cfg<H>::kMaxReg) tc2_step_kernel(const StepArgs 
           if (last) {
             ou = fmaf(sWd[u], zz.x, ou);
             ou = fmaf(sWd[u + 1], zz.y, ou);
+            if constexpr (C == 2) {
+              oy1 = fmaf(sWd2[u], zz.x, oy1);
+              oy1 = fmaf(sWd2[u + 1], zz.y, oy1);
+            }
           }
         }
         if (!last) {
@@ -856,6 +891,7 @@ __global__ void __maxnreg__(t2::Cfg<H>::kMaxReg) tc2_step_kernel(const StepArgs 
       sEx[(r + 0) * 128 + p] = ou;
       sEx[(r + 1) * 128 + p] = oux;
       sEx[(r + 2) * 128 + p] = ouy;
+      if constexpr (C == 2) tail[(kTY1p + ug) * 128 + p] = oy1;
     }
     __syncthreads();
     if (ug == 0) {
@@ -874,10 +910,27 @@ __global__ void __maxnreg__(t2::Cfg<H>::kMaxReg) tc2_step_kernel(const StepArgs 
       sEx[kUx * 128 + p] = ux;
       sEx[kUy * 128 + p] = uy;
       if (interior) cvr[p] = a.bx * ux + a.by * uy;
+      float ep = 0.f;
+      if constexpr (C == 2) {
+        // channel 1 -> eps = softplus(y1) (network.hpp:130-138, 477-483)
+        float y1 = oy1;
+#pragma unroll
+        for (int g = 1; g < CF::NG; ++g) y1 += tail[(kTY1p + g) * 128 + p];
+        y1 += sWd[HP + 1];
+        if (valid && !finitef(y1)) bad = 1;
+        ep = softplusf(y1);
+        tY1[p] = y1;
+        tE[p] = ep;
+        if (spatial) {
+          tSx[p] = ep * ux;
+          tSy[p] = ep * uy;
+        }
+      }
       if (MODE == kModeForward && valid) {
         if (a.out_u) a.out_u[G.pbase + p] = u;
         if (a.out_ux) a.out_ux[G.pbase + p] = ux;
         if (a.out_uy) a.out_uy[G.pbase + p] = uy;
+        if (C == 2 && a.out_eps) a.out_eps[G.pbase + p] = ep;
       }
     }
     mark(4);
@@ -891,12 +944,13 @@ __global__ void __maxnreg__(t2::Cfg<H>::kMaxReg) tc2_step_kernel(const StepArgs 
     if (MODE == kModeReverse) {
       // the split path's contraction / penalty kernels computed them
       if (ug == 0) {
-        float ubv = 0.f, ox = 0.f, oy = 0.f;
+        float ubv = 0.f, ox = 0.f, oy = 0.f, y1b = 0.f;
         if (valid) {
           const int pi = G.pbase + p;
           if (pi < a.n_int) {
             ox = a.in_uxb[pi];
             oy = a.in_uyb[pi];
+            if (C == 2 && spatial && a.in_eb) y1b = a.in_eb[pi] * sigmoidf(tY1[p]);
           } else {
             ubv = a.in_ub[pi - a.n_int];
           }
@@ -907,6 +961,10 @@ __global__ void __maxnreg__(t2::Cfg<H>::kMaxReg) tc2_step_kernel(const StepArgs 
         atomic_max_abs(&sMax[kMb], ubv);
         atomic_max_abs(&sMax[kMx], ox);
         atomic_max_abs(&sMax[kMy], oy);
+        if constexpr (C == 2) {
+          tY1b[p] = y1b;
+          atomic_max_abs(&sMax[kMe], y1b);
+        }
       }
     } else if (interior) {
       const bool conv = a.nt == 3;
@@ -930,8 +988,9 @@ __global__ void __maxnreg__(t2::Cfg<H>::kMaxReg) tc2_step_kernel(const StepArgs 
         if (r < nrows_tile) {
           const int kk = r / a.T;
           const int q1 = (a.Q * (part + 1)) / kCS;
-          const float* sx = sEx + kUx * 128 + kk * a.Q;
-          const float* sy = sEx + kUy * 128 + kk * a.Q;
+          // spatial eps: eps ux, eps uy (the coefficient inside the integral)
+          const float* sx = (spatial ? tSx : sEx + kUx * 128) + kk * a.Q;
+          const float* sy = (spatial ? tSy : sEx + kUy * 128) + kk * a.Q;
           const float* sc = cvr + kk * a.Q;
           const float* gx_r = T0 + r * a.Q;
           const float* gy_r = T1 + r * a.Q;
@@ -962,7 +1021,7 @@ __global__ void __maxnreg__(t2::Cfg<H>::kMaxReg) tc2_step_kernel(const StepArgs 
           gt += __shfl_xor_sync(0xffffffffu, gt, o);
         }
         if (part == 0 && r < nrows_tile) {
-          float res = e_fixed * (gx + gy);
+          float res = spatial ? gx + gy : e_fixed * (gx + gy);
           if (conv) res += gt;
           res -= frow;
           rsqv[r] = res * res;
@@ -1014,10 +1073,20 @@ __global__ void __maxnreg__(t2::Cfg<H>::kMaxReg) tc2_step_kernel(const StepArgs 
           sbt += __shfl_xor_sync(0xffffffffu, sbt, o);
         }
         if (part == 0 && pt < 128) {
-          float ox = 0.f, oy = 0.f;
+          float ox = 0.f, oy = 0.f, y1b = 0.f;
           if (pv) {
-            ox = e_fixed * sbx;
-            oy = e_fixed * sby;
+            if (spatial) {
+              // uxbar = eps Gx^T rbar, epsbar = ux Gx^T rbar + uy Gy^T rbar,
+              // y1bar = epsbar softplus'(y1) (losses.hpp:145-160)
+              const float ep = tE[pt];
+              ox = ep * sbx;
+              oy = ep * sby;
+              const float eb = sEx[kUx * 128 + pt] * sbx + sEx[kUy * 128 + pt] * sby;
+              y1b = eb * sigmoidf(tY1[pt]);
+            } else {
+              ox = e_fixed * sbx;
+              oy = e_fixed * sby;
+            }
             if (conv) {
               ox = fmaf(a.bx, sbt, ox);
               oy = fmaf(a.by, sbt, oy);
@@ -1028,6 +1097,10 @@ __global__ void __maxnreg__(t2::Cfg<H>::kMaxReg) tc2_step_kernel(const StepArgs 
           sEx[kUyb * 128 + pt] = oy;
           atomic_max_abs(&sMax[kMx], ox);
           atomic_max_abs(&sMax[kMy], oy);
+          if constexpr (C == 2) {
+            tY1b[pt] = y1b;
+            atomic_max_abs(&sMax[kMe], y1b);
+          }
         }
         const int cs = tid - (NT - ncell);
         if (cs >= 0) {
@@ -1069,6 +1142,7 @@ __global__ void __maxnreg__(t2::Cfg<H>::kMaxReg) tc2_step_kernel(const StepArgs 
         sEx[kUb * 128 + p] = ubv;
         sEx[kUxb * 128 + p] = 0.f;
         sEx[kUyb * 128 + p] = 0.f;
+        if constexpr (C == 2) tY1b[p] = 0.f;
         atomic_max_abs(&sMax[kMb], ubv);
       }
       if (lane == 0 && warp < 4) {
@@ -1087,12 +1161,14 @@ __global__ void __maxnreg__(t2::Cfg<H>::kMaxReg) tc2_step_kernel(const StepArgs 
     __syncthreads();                          // adjoint rows + tile maxima visible; slab reads done
     mark(8);
     const float ub = sEx[kUb * 128 + p], uxb = sEx[kUxb * 128 + p], uyb = sEx[kUyb * 128 + p];
+    const float y1b = C == 2 ? tY1b[p] : 0.f;  // adjoint of output channel 1 (read before the G stores)
 
     // =================== reverse ===================
     // magnitude bounds of G at the last hidden layer (value | tangents)
     const float Mb = __uint_as_float(sMax[kMb]), Mx = __uint_as_float(sMax[kMx]), My = __uint_as_float(sMax[kMy]);
     const float Wd = sSc[kScWd];
     float bGv = Wd * (Mb + kapmax * sSc[kScBt + D - 1] * (Mx + My));
+    if constexpr (C == 2) bGv += sSc[kScWd2] * __uint_as_float(sMax[kMe]);
     float bGt = Wd * fmaxf(Mx, My);
     // G scales for param layer l: S_G,s = 2^(kP - kX_s) with the common
     // product exponent kP = min_s (14 - e(B_s) + kX_s); returns kP
@@ -1121,12 +1197,13 @@ __global__ void __maxnreg__(t2::Cfg<H>::kMaxReg) tc2_step_kernel(const StepArgs 
     {
       const float f1 = sSc[kScF1 + NL - 1];
       const float Ub = ub * sgv, Uxv = uxb * sgv, Uyv = uyb * sgv, Uxt = uxb * sgt, Uyt = uyb * sgt;
+      const float Y1 = y1b * sgv;
 #pragma unroll kUC
       for (int c = 0; c < 2; ++c) {
         float zs[8], dx[8], dy[8];
         tc::tmem_ld1x8_wait(tmem + lane_q + LY::kZ0 + u0 + 8 * c, zs);
         tc::tmem_ld2x8_wait(dcol(1, c), dcol(2, c), dx, dy);
-        float v[8], gA[8], gX[8], gY[8];
+        float v[8], gA[8], gX[8], gY[8], v1[8];
 #pragma unroll
         for (int k = 0; k < 8; k += 2) {
           const int u = u0 + 8 * c + k;
@@ -1136,7 +1213,13 @@ __global__ void __maxnreg__(t2::Cfg<H>::kMaxReg) tc2_step_kernel(const StepArgs 
           const float2 tx = mul2(cc, f2(dx[k], dx[k + 1])), ty = mul2(cc, f2(dy[k], dy[k + 1]));
           const float2 vv = fma2(f2s(ub), z, fma2(f2s(uxb), tx, mul2(f2s(uyb), ty)));
           const float2 wd = f2(sWd[u], sWd[u + 1]);
-          const float2 ga = mul2(wd, fma2(s1, f2s(Ub), mul2(kp, fma2(tx, f2s(Uxv), mul2(ty, f2s(Uyv))))));
+          float2 ga = mul2(wd, fma2(s1, f2s(Ub), mul2(kp, fma2(tx, f2s(Uxv), mul2(ty, f2s(Uyv))))));
+          if constexpr (C == 2) {  // + s1 wd1 y1bar (channel 1 sees the value stream only)
+            ga = fma2(mul2(s1, f2(sWd2[u], sWd2[u + 1])), f2s(Y1), ga);
+            const float2 v2 = mul2(f2s(y1b), z);
+            v1[k] = v2.x;
+            v1[k + 1] = v2.y;
+          }
           const float2 sw = mul2(s1, wd);
           const float2 gx = mul2(sw, f2s(Uxt)), gy = mul2(sw, f2s(Uyt));
           v[k] = vv.x;
@@ -1149,6 +1232,7 @@ __global__ void __maxnreg__(t2::Cfg<H>::kMaxReg) tc2_step_kernel(const StepArgs 
           gY[k + 1] = gy.y;
         }
         acc_units(v, kAWd, c);
+        if constexpr (C == 2) acc_units(v1, kAWd2, c);
         const uint32_t o = coff(c);
         if (row_ok) tc::st_split8_ho<false>(bufA, NB * kPart, o, gA, 1.f);
         if (row_ok) tc::st_split8_ho<false>(bufA + kStream, NB * kPart, o, gX, 1.f);
@@ -1329,13 +1413,14 @@ __global__ void __maxnreg__(t2::Cfg<H>::kMaxReg) tc2_step_kernel(const StepArgs 
   // CUDA-core gradients: per-warp sums combined in warp order
   for (int u = tid; u <= H; u += NT) {
     const int h2 = u >> 4, j = u & 15;
-    float w0x = 0.f, w0y = 0.f, b0 = 0.f, wd = 0.f;
+    float w0x = 0.f, w0y = 0.f, b0 = 0.f, wd = 0.f, wd1 = 0.f;
     for (int w = 4 * h2; w < 4 * h2 + 4; ++w) {
       const float* A = sAcc + w * kAccW;
       w0x += A[kAW0x + j];
       w0y += A[kAW0y + j];
       b0 += A[kAB0 + j];
       wd += A[kAWd + j];
+      if constexpr (C == 2) wd1 += A[kAWd2 + j];
     }
     if (u < H) {
       if (u < net.out_w[0]) {
@@ -1343,9 +1428,14 @@ __global__ void __maxnreg__(t2::Cfg<H>::kMaxReg) tc2_step_kernel(const StepArgs 
         a.grad_part[(size_t)(net.w_off[0] + 2 * u + 1) * a.part_stride + blockIdx.x] = w0y;
         a.grad_part[(size_t)(net.b_off[0] + u) * a.part_stride + blockIdx.x] = b0;
       }
-      if (u < net.in_w[D]) a.grad_part[(size_t)(net.w_off[D] + u) * a.part_stride + blockIdx.x] = wd;
+      if (u < net.in_w[D]) {
+        a.grad_part[(size_t)(net.w_off[D] + u) * a.part_stride + blockIdx.x] = wd;
+        if constexpr (C == 2)
+          a.grad_part[(size_t)(net.w_off[D] + net.in_w[D] + u) * a.part_stride + blockIdx.x] = wd1;
+      }
     } else {
       a.grad_part[(size_t)net.b_off[D] * a.part_stride + blockIdx.x] = wd;
+      if constexpr (C == 2) a.grad_part[(size_t)(net.b_off[D] + 1) * a.part_stride + blockIdx.x] = wd1;
     }
   }
   if (tid == 0)
@@ -1397,9 +1487,9 @@ __global__ void __maxnreg__(t2::Cfg<H>::kMaxReg) tc2_step_kernel(const StepArgs 
   }
 }
 
-template <int H, int D>
+template <int H, int D, int C = 1>
 __host__ __device__ constexpr size_t tc2_step_smem_bytes() {
-  return t2::Lay<H, D>::BYTES;
+  return t2::Lay<H, D, C>::BYTES;
 }
 
 }  // namespace vpg

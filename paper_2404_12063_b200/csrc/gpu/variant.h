@@ -35,8 +35,9 @@ struct Variant {
 //   3 hidden layers, width <= 62 with one output (tensor cores), <= 50 with two;
 //   4 hidden layers, width <= 36 (CUDA cores: the per-point state of wider
 //   nets exceeds shared memory);
-// tanh or sigmoid everywhere.  Tensor-core step (tc2) for 2-3 hidden layers,
-// one output, width <= 62; the CUDA-core step for everything else.
+// tanh or sigmoid everywhere.  Tensor-core step (tc2) for 2-3 hidden layers of
+// width <= 62, one output or two (the spatial-eps head); the CUDA-core step
+// for everything else.
 #define VPG_VARIANTS(X) \
   X(30, 1, 1, 0) X(30, 1, 1, 1) X(30, 1, 2, 0) X(30, 1, 2, 1) X(64, 1, 1, 0) X(64, 1, 1, 1) \
   X(64, 1, 2, 0) X(64, 1, 2, 1) X(30, 2, 1, 0) X(30, 2, 1, 1) X(62, 2, 1, 0) X(62, 2, 1, 1) \
@@ -67,16 +68,18 @@ Variant make_variant() {
   v.off_union = LY::OFF_UNION;
   v.rev_need = LY::REV_NEED;
   v.smem = [](int u, int r) { return step_smem_bytes<H, D, C>(u, r); };
-  if constexpr (C == 1 && (D == 2 || D == 3) && H <= 63) {
+  if constexpr ((D == 2 || D == 3) && H <= 63) {
+    if constexpr (tc2_step_smem_bytes<H, D, C>() <= 227 * 1024) {
     using CF = t2::Cfg<H>;
-    v.tc2 = tc2_step_kernel<H, D, A, kModeFused>;
-    v.tc2_fwd = tc2_step_kernel<H, D, A, kModeForward>;
-    v.tc2_rev = tc2_step_kernel<H, D, A, kModeReverse>;
-    v.tc2_smem = tc2_step_smem_bytes<H, D>();
+    v.tc2 = tc2_step_kernel<H, D, A, kModeFused, C>;
+    v.tc2_fwd = tc2_step_kernel<H, D, A, kModeForward, C>;
+    v.tc2_rev = tc2_step_kernel<H, D, A, kModeReverse, C>;
+    v.tc2_smem = tc2_step_smem_bytes<H, D, C>();
     v.tc2_nt = CF::NT;
     v.tc2_mp = CF::MP;
     v.tc2_buf = CF::kBuf;
     v.tc2_scratch = CF::kScratch;
+    }
   }
   return v;
 }

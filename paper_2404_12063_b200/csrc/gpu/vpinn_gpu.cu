@@ -684,17 +684,17 @@ void configure(vpinn_gpu_ctx* c) {
     return 2 * (smem + resv) <= (size_t)smsm ? 2 : 1;
   };
   // the tensor-core forward / reverse modes (split path, evaluate)
-  const bool tc2_modes_ok = V.tc2_fwd != nullptr && !(g_test_hooks.load() & VPINN_HOOK_CUDA_CORE_STEP) &&
-                            c->eps_source != VPINN_EPS_SPATIAL;
+  const bool tc2_modes_ok = V.tc2_fwd != nullptr && !(g_test_hooks.load() & VPINN_HOOK_CUDA_CORE_STEP);
   if (!c->split) {
     // tensor-core step: whole-cell tiles of at most tc2_mp points, the tile's
     // slab plus its contraction scratch in operand buffer A
     const int tc_cells = V.tc2 ? std::max(1, V.tc2_mp / c->Q) : 1;
     const int tc_rows = tc_cells * c->T;
     c->tc2 = V.tc2 != nullptr && !(g_test_hooks.load() & VPINN_HOOK_CUDA_CORE_STEP) &&
-             c->eps_source != VPINN_EPS_SPATIAL && c->Q >= 2 && c->Q <= V.tc2_mp &&
+             c->Q >= 2 && c->Q <= V.tc2_mp &&
              tc_rows <= 128 &&
-             (size_t)(c->nt * round4(tc_rows * c->Q + 8) + vpg::t2::kTailFloats) * sizeof(float) <=
+             (size_t)(c->nt * round4(tc_rows * c->Q + 8) +
+                      (V.C == 2 ? vpg::t2::tail_floats<2>() : vpg::t2::tail_floats<1>())) * sizeof(float) <=
                  (size_t)V.tc2_buf;
     a.cells_per_tile = std::max(1, (c->tc2 ? V.tc2_mp : vpg::kThreads) / c->Q);
     a.n_int_tiles = c->E ? ceil_div(c->E, a.cells_per_tile) : 0;
@@ -720,7 +720,7 @@ void configure(vpinn_gpu_ctx* c) {
       a.tc_scratch = c->tc_scratch.p;
       a.tc_force_spill = (g_test_hooks.load() & VPINN_HOOK_FORCE_SPILL) ? 1 : 0;
       c->kernel_name = "tc2_step_kernel<" + std::to_string(V.H) + "," + std::to_string(V.D) + "," +
-                       (V.ACT ? "sigmoid" : "tanh") + "> (fp16 split, " + std::to_string(V.tc2_nt) + " threads, " +
+                       (V.ACT ? "sigmoid" : "tanh") + (V.C == 2 ? ",2 outputs" : "") + "> (fp16 split, " + std::to_string(V.tc2_nt) + " threads, " +
                        std::to_string(occ) + " CTA" + (occ > 1 ? "s" : "") + "/SM)";
     } else {
       c->kernel_name = "step_kernel<" + std::to_string(V.H) + "," + std::to_string(V.D) + "," + std::to_string(V.C) +
