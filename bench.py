@@ -371,6 +371,7 @@ def main():
     c5p = _aux(_c5_paper, mesh, device) if aux else None
     sweep = _aux(_sweep, device) if aux else None
     sweep3 = _aux(_sweep_c3, device) if aux else None
+    split = _aux(_c3_contraction, device, pk) if rank == 0 else None
     if rank != 0:
         return
     # the north star's "contraction HBM GB/s vs peak", kept inside roofline
@@ -396,7 +397,7 @@ def main():
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
         "roofline": dict(_step_roofline(kernel_name, mlp_tflops, ffma.value, pk, ms_mlp / (ms_mlp + ms_red + ms_adam)),
-                         contraction=contraction),
+                         contraction=contraction, contraction_split=split),
     }
     line.update({
         "kernel_ms": {"fused_step": ms_mlp, "reduce": ms_red, "adam": ms_adam},
@@ -720,6 +721,29 @@ def _c4_disk_spatial_inverse(device):
     return {"cells": hp.E, "n_test": hp.T, "n_quad": hp.Q, "sensors": hp.n_sen, "layers": [2, 30, 30, 30, 2],
             "ms_per_epoch": ms, "kernel": kernel, "quad_pt_evals_per_s": hp.n_int / (ms * 1e-3),
             "l2": "flushed between timed epochs"}
+
+
+def _c3_contraction(device, pk):
+    """The split path's contraction (cells larger than a tile: C3's 10x10
+    test functions on 40x40 Gauss points, 64 cells) on device-resident
+    derivatives, L2 flushed per launch: contract_rowreg_kernel (warp-owned
+    rows) + contract_rowreg_reduce_kernel (the per-cell sum of the CTA
+    partials), against the measured HBM copy bandwidth."""
+    from paper_2404_12063_b200 import gpu as G, host
+    cfg = {"problem": {"forcing": "sin4pi_f", "boundary_g": "sin4pi_u", "n_boundary_points": 400},
+           "discretization": {"n_test_per_dim": 10, "n_quad_per_dim": 40},
+           "network": {"layers": [2, 30, 30, 30, 1]},
+           "training": {"learning_rate": 1e-3, "seed": 42, "precision": "single"}}
+    hp = host.HostProblem(cfg, mesh=host.Mesh.structured(8, 8))
+    g = G.GpuStep.from_problem(hp.view(device), keepalive=hp)
+    ms, nbytes = g.time_contract(20)
+    g.close()
+    gbs = nbytes / (ms * 1e-3) / 1e9
+    return {"bound": "hbm", "kernel": "contract_rowreg_kernel + contract_rowreg_reduce_kernel (C3: 64 cells, "
+                                      "T = 100, Q = 1,600)",
+            "achieved": gbs, "peak": pk.get("hbm_gbs"), "unit": "GB/s", "frac": gbs / pk["hbm_gbs"],
+            "traffic": (_traffic("contract_rowreg") or {}).get("bytes"),
+            "bytes_per_launch": nbytes, "ms_per_launch": ms, "peak_source": "MEASURED_PEAKS.json hbm_gbs"}
 
 
 def _sweep(device):
