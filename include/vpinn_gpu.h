@@ -239,6 +239,13 @@ int vpinn_gpu_contract(vpinn_gpu_ctx* ctx, const float* du_dx, const float* du_d
  * and the algorithmic bytes per launch. */
 int vpinn_gpu_time_contract(vpinn_gpu_ctx* ctx, int reps, double* ms_per_launch,
                             double* bytes_per_launch);
+/* The same, also timing the streaming kernel alone (*ms_stream): on the split
+ * path (cells larger than a warp's ring) the launch is the row kernel plus the
+ * per-cell sum of its partial columns; for whole-cell contexts *ms_stream ==
+ * *ms_per_launch.  Diagnostic (bench.py's roofline), replaces nothing in the
+ * reference. */
+int vpinn_gpu_time_contract_kernels(vpinn_gpu_ctx* ctx, int reps, double* ms_per_launch, double* ms_stream,
+                                    double* bytes);
 
 /* Read the uploaded tensors back (layout parity: must equal the host
  * arrays byte for byte).  which: 0 grad_x, 1 grad_y, 2 test, 3 forcing. */

@@ -475,6 +475,7 @@ struct vpinn_gpu_ctx {
   int grid_contract = 0, grid_pen = 0, grid_fwd = 0, grid_creduce = 0;
   DBuf<float> cpart;  // row-block contraction partial adjoint columns
   DBuf<int> rr_cover;  // warp-owned-row contraction: per cell (first CTA, segment, last CTA, 0)
+  cudaEvent_t contract_mid = nullptr;  // vpinn_gpu_time_contract_kernels: recorded after the streaming kernel
   size_t smem_contract = 0, smem_fwd = 0;
   // graphs
   std::map<std::tuple<int, int, double>, cudaGraphExec_t> graphs;
@@ -1021,6 +1022,7 @@ void launch_contract_rows(vpinn_gpu_ctx* c, const vpg::ContractArgs& ca) {
     auto fn = reinterpret_cast<void (*)(vpg::ContractArgs)>(const_cast<void*>(rowreg_kernel(ca.rr_mq)));
     fn<<<c->grid_contract, vpg::kRRThreads, c->smem_contract, c->stream>>>(ca);
     CK(cudaGetLastError());
+    if (c->contract_mid) CK(cudaEventRecord(c->contract_mid, c->stream));
     vpg::contract_rowreg_reduce_kernel<<<c->grid_creduce, 256, 0, c->stream>>>(
         ca, reinterpret_cast<const int4*>(c->rr_cover.p));
     CK(cudaGetLastError());
@@ -1029,6 +1031,7 @@ void launch_contract_rows(vpinn_gpu_ctx* c, const vpg::ContractArgs& ca) {
   }
   vpg::contract_rows_kernel<<<c->grid_contract, vpg::kCRThreads, c->smem_contract, c->stream>>>(ca);
   CK(cudaGetLastError());
+  if (c->contract_mid) CK(cudaEventRecord(c->contract_mid, c->stream));
   vpg::contract_rows_reduce_kernel<<<c->grid_creduce, 256, 0, c->stream>>>(ca);
   CK(cudaGetLastError());
   c->launches += 2;
@@ -1859,6 +1862,11 @@ int vpinn_gpu_contract(vpinn_gpu_ctx* c, const float* du_dx, const float* du_dy,
 }
 
 int vpinn_gpu_time_contract(vpinn_gpu_ctx* c, int reps, double* ms_per_launch, double* bytes) {
+  return vpinn_gpu_time_contract_kernels(c, reps, ms_per_launch, nullptr, bytes);
+}
+
+int vpinn_gpu_time_contract_kernels(vpinn_gpu_ctx* c, int reps, double* ms_per_launch, double* ms_stream,
+                                    double* bytes) {
   return guarded([&] {
     weak_only(c, "vpinn_gpu_time_contract");
     set_dev(c);
@@ -1876,23 +1884,35 @@ int vpinn_gpu_time_contract(vpinn_gpu_ctx* c, int reps, double* ms_per_launch, d
     // L2 flush buffer (> 126 MB L2) between launches so each launch streams HBM
     DBuf<char> flush;
     flush.alloc((size_t)256 << 20, c->stream);
-    cudaEvent_t e0, e1;
+    cudaEvent_t e0, e1, em;
     CK(cudaEventCreate(&e0));
     CK(cudaEventCreate(&e1));
-    double total = 0.0;
+    CK(cudaEventCreate(&em));
+    // the streaming kernel alone: an event between it and the partial-column
+    // reduction of the split path (the cell kernel is one launch)
+    c->contract_mid = c->cell_contract ? nullptr : em;
+    double total = 0.0, stream_ms = 0.0;
     for (int r = 0; r < reps + 2; ++r) {
       flush_l2_now(c, flush.p);
       CK(cudaEventRecord(e0, c->stream));
       launch_contract(c, ux.p, uy.p, ep.p, oxb.p, oyb.p, oeb.p, nullptr, es.p, c->sargs.rscale, lp.p, nullptr);
       CK(cudaEventRecord(e1, c->stream));
       CK(cudaEventSynchronize(e1));
-      float ms = 0;
+      float ms = 0, ms1 = 0;
       CK(cudaEventElapsedTime(&ms, e0, e1));
-      if (r >= 2) total += ms;
+      if (c->contract_mid) CK(cudaEventElapsedTime(&ms1, e0, em));
+      else ms1 = ms;
+      if (r >= 2) {
+        total += ms;
+        stream_ms += ms1;
+      }
     }
+    c->contract_mid = nullptr;
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
+    cudaEventDestroy(em);
     *ms_per_launch = total / std::max(1, reps);
+    if (ms_stream) *ms_stream = stream_ms / std::max(1, reps);
     const double EQ = (double)c->E * c->Q;
     double b = 4.0 * ((double)c->nt * c->E * c->T * c->Q + (double)c->E * c->T + 4.0 * EQ);
     if (c->eps_source == VPINN_EPS_SPATIAL) b += 8.0 * EQ;

@@ -227,6 +227,12 @@ class GpuStep:
         _capi.check(_capi.lib().vpinn_gpu_time_contract(self.h, reps, C.byref(ms), C.byref(b)))
         return ms.value, b.value
 
+    def time_contract_kernels(self, reps=20):
+        """(ms per launch, ms of the streaming kernel alone, algorithmic bytes)."""
+        ms, ms1, b = C.c_double(), C.c_double(), C.c_double()
+        _capi.check(_capi.lib().vpinn_gpu_time_contract_kernels(self.h, reps, C.byref(ms), C.byref(ms1), C.byref(b)))
+        return ms.value, ms1.value, b.value
+
     def step_kernel(self) -> str:
         """Name of the kernel running this context's fused epoch step."""
         return _capi.lib().vpinn_gpu_step_kernel(self.h).decode()
