@@ -296,14 +296,17 @@ def test_edge_shapes_match_oracle(name):
     assert r.max() < 1e-5
 
 
-@pytest.mark.parametrize("layers", [(2, 30, 13, 30, 1), (2, 13, 30, 30, 1), (2, 9, 20, 1), (2, 25, 25, 25, 1)])
+@pytest.mark.parametrize("layers", [(2, 30, 13, 30, 1), (2, 13, 30, 30, 1), (2, 9, 20, 1), (2, 25, 25, 25, 1),
+                                    (2, 30, 13, 30, 2), (2, 21, 7, 2), (2, 44, 17, 50, 2)])
 @pytest.mark.parametrize("sigmoid", [False, True])
 def test_ragged_hidden_widths_match_oracle(layers, sigmoid):
     """Hidden layers narrower than the kernel width are zero-padded exactly
     (tensor-core and CUDA-core steps; the padded units never reach the
-    outputs or the gradient)."""
-    spec = po.ProblemSpec(*po.structured_mesh(3, 4), n_test_1d=4, n_quad_1d=6, forcing="sin2pi_f",
-                          boundary_g="sin2pi_u", n_boundary=50, layers=layers, sigmoid=sigmoid, bx=0.4, seed=11)
+    outputs or the gradient), also with the spatial-eps head."""
+    kw = dict(eps_source=2, forcing="sinpi_vareps_f", n_sensors=9, sensor_field="sinpi_u") if layers[-1] == 2 \
+        else dict(forcing="sin2pi_f")
+    spec = po.ProblemSpec(*po.structured_mesh(3, 4), n_test_1d=4, n_quad_1d=6, boundary_g="sin2pi_u",
+                          n_boundary=50, layers=layers, sigmoid=sigmoid, bx=0.4, seed=11, **kw)
     ob, g, p0 = make_pair(spec)
     parts_o, _ = ob.loss_and_grad(p0)
     parts_g, grad_g = g.loss_and_grad()
