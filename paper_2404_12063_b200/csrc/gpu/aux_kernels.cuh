@@ -18,35 +18,33 @@ namespace vpg {
 constexpr int kRedThreads = 256;
 constexpr int kRedWarps = kRedThreads / 32;
 
-__device__ __forceinline__ void reduce_body(const float* __restrict__ grad_part, int n_rows, int stride,
-                                            int n_params, const double* __restrict__ loss_part, int n_loss_rows,
-                                            double* __restrict__ red) {
+// row gw of red by one converged warp: lane c sums entries c, c + 32, ... in
+// double, then a fixed xor tree; every lane returns the row's value
+__device__ __forceinline__ double reduce_row(int gw, const float* __restrict__ grad_part, int n_rows, int stride,
+                                             int n_params, const double* __restrict__ loss_part, int n_loss_rows,
+                                             double* __restrict__ red) {
   const int lane = threadIdx.x & 31;
-  const int gw = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  const double* src_d = nullptr;
-  const float* src_f = nullptr;
-  int n = 0, step = 1;
-  if (gw < n_params) {
-    src_f = grad_part + (size_t)gw * stride;
-    n = n_rows;
-  } else if (gw < n_params + kLpWords) {
-    src_d = loss_part + (gw - n_params);
-    n = n_loss_rows;
-    step = kLpWords;
-  } else {
-    return;
-  }
   double acc = 0.0;
-  if (src_f != nullptr) {
+  if (gw < n_params) {
+    const float* src_f = grad_part + (size_t)gw * stride;
 #pragma unroll 8
-    for (int c = lane; c < n; c += 32) acc += (double)src_f[c];
+    for (int c = lane; c < n_rows; c += 32) acc += (double)src_f[c];
   } else {
+    const double* src_d = loss_part + (gw - n_params);
 #pragma unroll 8
-    for (int c = lane; c < n; c += 32) acc += src_d[(size_t)c * step];
+    for (int c = lane; c < n_loss_rows; c += 32) acc += src_d[(size_t)c * kLpWords];
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
   if (lane == 0) red[gw] = acc;
+  return acc;
+}
+
+__device__ __forceinline__ void reduce_body(const float* __restrict__ grad_part, int n_rows, int stride,
+                                            int n_params, const double* __restrict__ loss_part, int n_loss_rows,
+                                            double* __restrict__ red) {
+  const int gw = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (gw < n_params + kLpWords) reduce_row(gw, grad_part, n_rows, stride, n_params, loss_part, n_loss_rows, red);
 }
 
 __host__ __device__ constexpr int reduce_grid(int n_params) { return (n_params + kLpWords + kRedWarps - 1) / kRedWarps; }
@@ -104,15 +102,85 @@ struct AdamArgs {
   int eps_grad_slot;  // parameter index receiving the scalar-eps gradient (-1 none)
 };
 
+// adam_step (trainer.hpp:34-59) for one parameter: IEEE intrinsics keep the
+// update in the reference's operation order (no FMA contraction)
+__device__ __forceinline__ void adam_update(float g, float m0, float v0, float p0, float lr, float c1, float c2,
+                                            float& m_out, float& v_out, float& p_out) {
+  const float b1 = 0.9f, b2 = 0.999f, omb1 = 1.0f - b1, omb2 = 1.0f - b2;
+  const float m = __fadd_rn(__fmul_rn(b1, m0), __fmul_rn(omb1, g));
+  const float v = __fadd_rn(__fmul_rn(b2, v0), __fmul_rn(omb2, __fmul_rn(g, g)));
+  m_out = m;
+  v_out = v;
+  const float mh = __fdiv_rn(m, c1);
+  const float vh = __fdiv_rn(v, c2);
+  p_out = __fsub_rn(p0, __fdiv_rn(__fmul_rn(lr, mh), __fadd_rn(__fsqrt_rn(vh), 1e-8f)));
+}
+
+// the loss parts in the reference's Real semantics and the train-loop
+// bookkeeping after an update (trainer.hpp:316-370): history record,
+// coefficient-tolerance / plateau / budget stops.  Thread 0.
+__device__ __forceinline__ void train_bookkeeping(const AdamArgs& a, long long t, float lr) {
+  TrainState* st = a.st;
+  const int n = a.n_params;
+  const double* red = a.red;
+  // L2 loads: red and the parameters may come from other CTAs (reduce_adam_kernel)
+  const float Lv = (float)__ldcg(&red[n + kLpVar]);
+  const float Lb = a.n_bnd > 0 ? (float)(__ldcg(&red[n + kLpBnd]) / a.n_bnd) : 0.0f;
+  const float Ls = a.n_sen > 0 ? (float)(__ldcg(&red[n + kLpSen]) / a.n_sen) : 0.0f;
+  const float total_f = __fadd_rn(__fadd_rn(Lv, __fmul_rn(a.tau_f, Lb)), __fmul_rn(a.gamma_f, Ls));
+  const double total = (double)total_f;
+  const unsigned long long now = globaltimer();
+  st->step = t;
+  double eps_now = __longlong_as_double(0x7ff8000000000000ll);
+  if (st->tracks_eps) eps_now = (double)__ldcg(&a.params[st->eps_slot]);
+  if (a.rec && t - 1 < a.rec_cap) {
+    StepRecord r;
+    r.total = total;
+    r.v = (double)Lv;
+    r.b = (double)Lb;
+    r.s = (double)Ls;
+    r.lr = (double)lr;
+    r.eps = eps_now;
+    r.seconds = (double)(now - st->t_prev) * 1e-9;
+    r.pad = 0.0;
+    a.rec[t - 1] = r;
+  }
+  st->t_prev = now;
+  // convergence checks, after the update (trainer.hpp:343-369)
+  int stop = 0, reason = 0;
+  if (st->tracks_eps && st->has_eps_tol && st->has_eps_actual) {
+    if (fabs(eps_now - st->eps_actual) < st->eps_abs_tol) {
+      stop = 1;
+      reason = 1;
+    }
+  }
+  if (!stop && st->has_loss_tol) {
+    if (total < st->best_loss * (1.0 - st->loss_tol)) {
+      st->best_loss = total;
+      st->best_step = t;
+    } else if (t - st->best_step >= st->plateau_window) {
+      stop = 1;
+      reason = 2;
+    }
+    if (!stop && total < st->best_loss) st->best_loss = total;
+  }
+  if (!stop && t >= st->iterations) {
+    stop = 1;
+    reason = 0;
+  }
+  if (stop) {
+    st->stopped = 1;
+    st->stop_reason = reason;
+  }
+}
+
 // adam_step (trainer.hpp:34-59) + train-loop bookkeeping (trainer.hpp:316-370)
-// for one epoch.  One CTA of 1024 threads.  IEEE intrinsics keep the update
-// in the reference's operation order (no FMA contraction).
+// for one epoch.  One CTA of 1024 threads.
 __device__ __forceinline__ void adam_body(const AdamArgs& a) {
   TrainState* st = a.st;
   const long long t = st->step + 1;
   const int n = a.n_params;
   const double* red = a.red;
-  const double lw_v = red[n + kLpVar], lw_b = red[n + kLpBnd], lw_s = red[n + kLpSen];
   const double eg = red[n + kLpEpsGrad];
   int bad = red[n + kLpBad] != 0.0;
   // every load of this thread's parameters issued before the abort check
@@ -132,11 +200,6 @@ __device__ __forceinline__ void adam_body(const AdamArgs& a) {
     }
   }
   bad = __syncthreads_or(bad);
-  // loss parts in the reference's Real semantics
-  const float Lv = (float)lw_v;
-  const float Lb = a.n_bnd > 0 ? (float)(lw_b / a.n_bnd) : 0.0f;
-  const float Ls = a.n_sen > 0 ? (float)(lw_s / a.n_sen) : 0.0f;
-  const float total_f = __fadd_rn(__fadd_rn(Lv, __fmul_rn(a.tau_f, Lb)), __fmul_rn(a.gamma_f, Ls));
   float lr, c1, c2;
   if (a.lr_tab) {
     lr = a.lr_tab[t - 1];
@@ -155,7 +218,6 @@ __device__ __forceinline__ void adam_body(const AdamArgs& a) {
     }
     return;
   }
-  const float b1 = 0.9f, b2 = 0.999f, omb1 = 1.0f - b1, omb2 = 1.0f - b2;
   cnt = 0;
   for (int p = threadIdx.x; p < n; p += blockDim.x, ++cnt) {
     float g, m0, v0, p0;
@@ -172,61 +234,10 @@ __device__ __forceinline__ void adam_body(const AdamArgs& a) {
       v0 = a.v[p];
       p0 = a.params[p];
     }
-    const float m = __fadd_rn(__fmul_rn(b1, m0), __fmul_rn(omb1, g));
-    const float v = __fadd_rn(__fmul_rn(b2, v0), __fmul_rn(omb2, __fmul_rn(g, g)));
-    a.m[p] = m;
-    a.v[p] = v;
-    const float mh = __fdiv_rn(m, c1);
-    const float vh = __fdiv_rn(v, c2);
-    a.params[p] = __fsub_rn(p0, __fdiv_rn(__fmul_rn(lr, mh), __fadd_rn(__fsqrt_rn(vh), 1e-8f)));
+    adam_update(g, m0, v0, p0, lr, c1, c2, a.m[p], a.v[p], a.params[p]);
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
-    const double total = (double)total_f;
-    const unsigned long long now = globaltimer();
-    st->step = t;
-    double eps_now = __longlong_as_double(0x7ff8000000000000ll);
-    if (st->tracks_eps) eps_now = (double)a.params[st->eps_slot];
-    if (a.rec && t - 1 < a.rec_cap) {
-      StepRecord r;
-      r.total = total;
-      r.v = (double)Lv;
-      r.b = (double)Lb;
-      r.s = (double)Ls;
-      r.lr = (double)lr;
-      r.eps = eps_now;
-      r.seconds = (double)(now - st->t_prev) * 1e-9;
-      r.pad = 0.0;
-      a.rec[t - 1] = r;
-    }
-    st->t_prev = now;
-    // convergence checks, after the update (trainer.hpp:343-369)
-    int stop = 0, reason = 0;
-    if (st->tracks_eps && st->has_eps_tol && st->has_eps_actual) {
-      if (fabs(eps_now - st->eps_actual) < st->eps_abs_tol) {
-        stop = 1;
-        reason = 1;
-      }
-    }
-    if (!stop && st->has_loss_tol) {
-      if (total < st->best_loss * (1.0 - st->loss_tol)) {
-        st->best_loss = total;
-        st->best_step = t;
-      } else if (t - st->best_step >= st->plateau_window) {
-        stop = 1;
-        reason = 2;
-      }
-      if (!stop && total < st->best_loss) st->best_loss = total;
-    }
-    if (!stop && t >= st->iterations) {
-      stop = 1;
-      reason = 0;
-    }
-    if (stop) {
-      st->stopped = 1;
-      st->stop_reason = reason;
-    }
-  }
+  if (threadIdx.x == 0) train_bookkeeping(a, t, lr);
 }
 
 __global__ void __launch_bounds__(1024) adam_kernel(const AdamArgs a) {
@@ -234,26 +245,92 @@ __global__ void __launch_bounds__(1024) adam_kernel(const AdamArgs a) {
   adam_body(a);
 }
 
-// single-GPU epoch tail: the cross-CTA reduction of reduce_kernel, then the
-// last CTA to finish (atomic ticket, release/acquire fences) applies Adam
+// single-GPU epoch tail: one warp per row reduces the CTA partials exactly
+// as reduce_kernel does and, for a parameter row, applies Adam to that
+// parameter right away (adam_update: the same expressions as adam_body),
+// keeping the old (p, m, v) in bk; the last CTA to finish (atomic ticket,
+// release / acquire fences) then only does the bookkeeping, or -- when a
+// gradient or the step kernel's loss words were non-finite -- restores every
+// parameter from bk and records the abort (adam_body's all-or-nothing
+// semantics).  Two dependent global round trips fewer than reducing first
+// and updating in the last CTA.  ticket[0]: CTA ticket, ticket[1]: non-finite
+// gradient flag (both re-armed by the last CTA).
 __global__ void __launch_bounds__(kRAThreads) reduce_adam_kernel(const float* __restrict__ grad_part, int n_rows,
                                                                    int stride, int n_params,
                                                                    const double* __restrict__ loss_part,
                                                                    int n_loss_rows, double* __restrict__ red,
-                                                                   unsigned* ticket, const AdamArgs a) {
+                                                                   unsigned* ticket, float* bk, const AdamArgs a) {
   pdl_trigger();
+  // the trainer state is this epoch's before the wait: the previous epoch's
+  // tail completed before this epoch's step kernel passed its own wait
+  __shared__ int last, s_stopped;
+  __shared__ long long s_t;
+  if (threadIdx.x == 0) {
+    s_stopped = a.st->stopped;
+    s_t = a.st->step + 1;
+  }
+  __syncthreads();
   pdl_wait();
-  if (a.st->stopped) return;
-  __shared__ int last;
-  reduce_body(grad_part, n_rows, stride, n_params, loss_part, n_loss_rows, red);
+  if (s_stopped) return;
+  const long long t = s_t;
+  const int lane = threadIdx.x & 31;
+  const int gw = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  float lr = 0.f, c1 = 0.f, c2 = 0.f;
+  if (a.lr_tab) {
+    lr = a.lr_tab[t - 1];
+    c1 = a.c1_tab[t - 1];
+    c2 = a.c2_tab[t - 1];
+  } else {
+    lr = a.lr_const;
+    c1 = 1.0f - (float)pow(0.9, (double)t);
+    c2 = 1.0f - (float)pow(0.999, (double)t);
+  }
+  if (gw < n_params + kLpWords) {
+    float p0 = 0.f, m0 = 0.f, v0 = 0.f;
+    if (gw < n_params && lane == 0) {  // in flight with the partial loads
+      p0 = a.params[gw];
+      m0 = a.m[gw];
+      v0 = a.v[gw];
+    }
+    double gd = reduce_row(gw, grad_part, n_rows, stride, n_params, loss_part, n_loss_rows, red);
+    if (gw == a.eps_grad_slot)  // the scalar-eps gradient's loss word, reduced the same way
+      gd += reduce_row(n_params + kLpEpsGrad, grad_part, n_rows, stride, n_params, loss_part, n_loss_rows, red);
+    if (gw < n_params && lane == 0) {
+      const float g = (float)gd;
+      if (!isfinite(g)) atomicOr(&ticket[1], 1u);
+      bk[gw] = p0;
+      bk[n_params + gw] = m0;
+      bk[2 * n_params + gw] = v0;
+      adam_update(g, m0, v0, p0, lr, c1, c2, a.m[gw], a.v[gw], a.params[gw]);
+    }
+  }
   __threadfence();
   __syncthreads();
-  if (threadIdx.x == 0) last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+  if (threadIdx.x == 0) last = atomicAdd(&ticket[0], 1u) == gridDim.x - 1;
   __syncthreads();
   if (!last) return;
   __threadfence();
-  if (threadIdx.x == 0) *ticket = 0u;  // re-arm for the next epoch (graph replay)
-  adam_body(a);
+  // (other CTAs' results: L2 loads, this SM's L1 may hold lines of them)
+  const int bad = __ldcg(&ticket[1]) != 0u || __ldcg(&red[n_params + kLpBad]) != 0.0;
+  if (bad) {  // all or nothing: the parameters and moments of before the step
+    for (int p = threadIdx.x; p < n_params; p += blockDim.x) {
+      a.params[p] = __ldcg(&bk[p]);
+      a.m[p] = __ldcg(&bk[n_params + p]);
+      a.v[p] = __ldcg(&bk[2 * n_params + p]);
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    ticket[0] = 0u;  // re-armed for the next epoch (graph replay)
+    ticket[1] = 0u;
+    if (bad) {
+      a.st->stopped = 1;
+      a.st->stop_reason = 3;
+      a.st->abort_step = t;
+    } else {
+      train_bookkeeping(a, t, lr);
+    }
+  }
 }
 
 __global__ void mark_start_kernel(TrainState* st) { st->t_prev = globaltimer(); }

@@ -449,7 +449,8 @@ struct vpinn_gpu_ctx {
   int grad_rows = 0, loss_rows = 0, part_stride = 0;
   // trainer
   DBuf<vpg::TrainState> st;
-  DBuf<unsigned> ticket;  // reduce_adam_kernel last-CTA ticket
+  DBuf<unsigned> ticket;  // reduce_adam_kernel: last-CTA ticket, non-finite gradient flag
+  DBuf<float> adam_bk;    // reduce_adam_kernel: (p, m, v) before the step, for an abort
   DBuf<vpg::StepRecord> rec;
   DBuf<float> lr_tab, c1_tab, c2_tab;
   int* h_flag = nullptr;  // pinned
@@ -1133,7 +1134,8 @@ void enqueue_epoch(vpinn_gpu_ctx* c, const vpg::AdamArgs& aa) {
   const float* gp = c->grad_part.p;
   const double* lp = c->loss_part.p;
   launch_k(pdl_enabled() && !c->split, vpg::reduce_adam_kernel, vpg::reduce_adam_grid(c->n_params), vpg::kRAThreads,
-           0, c->stream, gp, c->grad_rows, c->part_stride, c->n_params, lp, c->loss_rows, c->red.p, c->ticket.p, aa);
+           0, c->stream, gp, c->grad_rows, c->part_stride, c->n_params, lp, c->loss_rows, c->red.p, c->ticket.p,
+           c->adam_bk.p, aa);
   CK(cudaGetLastError());
   c->launches += 1;
 }
@@ -1508,7 +1510,8 @@ int vpinn_gpu_create(const vpinn_gpu_problem* pb, vpinn_gpu_ctx** out) {
     c->m.alloc(c->n_params, c->stream);
     c->v.alloc(c->n_params, c->stream);
     c->st.alloc(1, c->stream);
-    c->ticket.alloc(1, c->stream);
+    c->ticket.alloc(2, c->stream);
+    c->adam_bk.alloc(3 * (size_t)c->n_params, c->stream);
     mark("uploads", c->stream);
     configure(c.get());
     mark("configure", c->stream);

@@ -193,6 +193,8 @@ def test_nonfinite_gradient_aborts_with_step_index():
     with pytest.raises(VpinnError) as e:
         g.train(5)
     assert e.value.code == 4 and e.value.report.abort_step == 1
+    # all or nothing: the aborted step left every parameter as it was
+    assert np.array_equal(g.get_params(), bad)
 
 
 @pytest.mark.parametrize("mode", [0, 1, 2, 3])
