@@ -1368,16 +1368,20 @@ __global__ void __maxnreg__(t2::Cfg<H>::kMaxReg) tc2_step_kernel(const StepArgs 
     }
     return;
   }
-  // parameter-gradient accumulators (G rows h | l x X columns h | l),
-  // unscaled by 2^-kacc, plus any spilled part -> smem [2HP][2HP + 1]
-  // (buffer A is free) -> the four-block sum
+  // (1) every MMA layer's parameter-gradient accumulator (G rows h | l x X
+  // columns h | l), unscaled by 2^-kacc, plus any spilled part -> shared
+  // memory [2HP][2HP + 1] per layer (buffers A and B are free); the per-warp
+  // loss sums -> sRed; one barrier (which also ORs the non-finite flags and
+  // publishes the per-warp CUDA-core gradient sums)
   constexpr int SS = 2 * HP + 1;
-  float* scr = reinterpret_cast<float*>(bufA);
+  static_assert((size_t)NL * 2 * HP * SS * sizeof(float) <= 2 * (size_t)CF::kBuf, "readout scratch");
+  float* scr0 = reinterpret_cast<float*>(bufA);
+  tc::fence_after_sync();
   for (int l = 1; l <= NL; ++l) {
     const int kacc = (l == 1) ? kacc0 : kacc1;
     const bool has = (l == 1) ? has0 : has1, spill = (l == 1) ? spill0 : spill1;
     const float* S = a.tc_scratch + ((size_t)blockIdx.x * NL + (l - 1)) * CF::kScratch;
-    tc::fence_after_sync();
+    float* scr = scr0 + (l - 1) * 2 * HP * SS;
     if (has) {
       const float inv = tc::exp2i(-kacc);
 #pragma unroll 1
@@ -1396,21 +1400,42 @@ __global__ void __maxnreg__(t2::Cfg<H>::kMaxReg) tc2_step_kernel(const StepArgs 
         }
       }
     }
-    tc::fence_before_sync();
-    __syncthreads();
-    const int fo = net.out_w[l], fi = net.in_w[l];
-    for (int e = tid; e < fo * (fi + 1); e += NT) {
-      const int o = e / (fi + 1), i = e - o * (fi + 1);
+  }
+  constexpr int NW = NT / 32;
+  {
+    double v = cell_v, g = cell_eg;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      v += __shfl_xor_sync(0xffffffffu, v, o);
+      g += __shfl_xor_sync(0xffffffffu, g, o);
+    }
+    if (lane == 0) {  // (sRed is free after the tile loop)
+      sRed[warp] = v;
+      sRed[NW + warp] = g;
+    }
+  }
+  tc::fence_before_sync();
+  const int any_bad = __syncthreads_or(bad);
+  // (2) the four-block sums of both MMA layers, the CUDA-core gradients
+  // (per-warp sums combined in warp order) and the loss words
+  {
+    const int n1 = net.out_w[1] * (net.in_w[1] + 1);
+    const int n_all = n1 + (NL == 2 ? net.out_w[2] * (net.in_w[2] + 1) : 0);
+    for (int e = tid; e < n_all; e += NT) {
+      const int l = e < n1 ? 1 : 2;
+      const int ee = l == 1 ? e : e - n1;
+      const int fi = net.in_w[l];
+      const int o = ee / (fi + 1), i = ee - o * (fi + 1);
       const int c = i < fi ? i : H;  // the bias gradient is the constant unit's column
+      const bool has = (l == 1) ? has0 : has1;
+      const float* scr = scr0 + (l - 1) * 2 * HP * SS;
       float g = 0.f;
       if (has)  // scr[row][col]: row = G part * HP + o, col = X part * HP + c
         g = ((scr[o * SS + c] + scr[o * SS + HP + c]) + scr[(HP + o) * SS + c]) + scr[(HP + o) * SS + HP + c];
       const int idx = (i < fi) ? net.w_off[l] + o * fi + i : net.b_off[l] + o;
       a.grad_part[(size_t)idx * a.part_stride + blockIdx.x] = g;
     }
-    __syncthreads();
   }
-  // CUDA-core gradients: per-warp sums combined in warp order
   for (int u = tid; u <= H; u += NT) {
     const int h2 = u >> 4, j = u & 15;
     float w0x = 0.f, w0y = 0.f, b0 = 0.f, wd = 0.f, wd1 = 0.f;
@@ -1438,9 +1463,6 @@ __global__ void __maxnreg__(t2::Cfg<H>::kMaxReg) tc2_step_kernel(const StepArgs 
       if constexpr (C == 2) a.grad_part[(size_t)(net.b_off[D] + 1) * a.part_stride + blockIdx.x] = wd1;
     }
   }
-  if (tid == 0)
-    for (int e = net.scal_off; e < net.n_params; ++e) a.grad_part[(size_t)e * a.part_stride + blockIdx.x] = 0.f;
-  const int any_bad = __syncthreads_or(bad);
   if constexpr (VPG_PHASE_CLOCK != 0)  // CTA 0 exit clock and tile count (diagnostics)
     if (a.phase_clk != nullptr && blockIdx.x == 0 && tid == 0) {
       a.phase_clk[kPhaseTiles * kPhaseMarks - 2] = clock64();
@@ -1449,28 +1471,13 @@ __global__ void __maxnreg__(t2::Cfg<H>::kMaxReg) tc2_step_kernel(const StepArgs 
   if constexpr (VPG_PHASE_CLOCK != 0)
     if (a.phase_clk != nullptr && tid == 0 && blockIdx.x < 1024)
       a.phase_clk[kPhaseTiles * kPhaseMarks + 3 * blockIdx.x + 1] = (long long)globaltimer();
-  double acc_v = 0.0, acc_eg = 0.0;
-  {
-    constexpr int NW = NT / 32;
-    double v = cell_v, g = cell_eg;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      v += __shfl_xor_sync(0xffffffffu, v, o);
-      g += __shfl_xor_sync(0xffffffffu, g, o);
-    }
-    __syncthreads();  // sRed is free
-    if (lane == 0) {
-      sRed[warp] = v;
-      sRed[NW + warp] = g;
-    }
-    __syncthreads();
-    if (tid == 0)
-      for (int w = 0; w < NW; ++w) {
-        acc_v += sRed[w];
-        acc_eg += sRed[NW + w];
-      }
-  }
   if (tid == 0) {
+    for (int e = net.scal_off; e < net.n_params; ++e) a.grad_part[(size_t)e * a.part_stride + blockIdx.x] = 0.f;
+    double acc_v = 0.0, acc_eg = 0.0;
+    for (int w = 0; w < NW; ++w) {
+      acc_v += sRed[w];
+      acc_eg += sRed[NW + w];
+    }
     double* lp = a.loss_part + (size_t)blockIdx.x * kLpWords;
     lp[kLpVar] = acc_v;
     lp[kLpBnd] = acc_b;
