@@ -324,6 +324,18 @@ int vpinn_gpu_tc_probe(int device, int mode, const float* A, const float* W, con
 int vpinn_gpu_nccl_unique_id(void* id128);
 int vpinn_gpu_attach_comm(vpinn_gpu_ctx* ctx, const void* id128, int nranks, int rank);
 
+/* Multi-GPU over peer memory (one process per GPU, CUDA IPC over NVLink /
+ * NVSwitch): every rank exports its mailbox (64-byte IPC handle), gathers all
+ * ranks' handles in rank order (host plumbing, e.g. a gloo all-gather) and
+ * attaches them.  Each epoch's tail is then ONE kernel: this rank's
+ * cross-CTA reduction, the rows stored into every rank's mailbox, the
+ * cross-rank sum in rank order (bitwise-identical replicas) and Adam --
+ * replacing reduce -> ncclAllReduce -> Adam (the reference's train loop,
+ * trainer.hpp:316-370, partitioned across ranks).  At most 8 ranks; every
+ * rank must run the same epochs (the exchange is a barrier). */
+int vpinn_gpu_peer_handle(vpinn_gpu_ctx* ctx, void* handle64);
+int vpinn_gpu_attach_peers(vpinn_gpu_ctx* ctx, const void* handles, int nranks, int rank);
+
 #ifdef __cplusplus
 }
 #endif

@@ -100,6 +100,8 @@ def _declare(L):
         "vpinn_gpu_forward2": (i32, [vp, vp, i64, vp, vp, vp, vp, vp]),
         "vpinn_gpu_contract": (i32, [vp, vp, vp, vp, vp, C.c_float, pd, vp, vp, vp, vp, vp]),
         "vpinn_gpu_time_contract": (i32, [vp, i32, pd, pd]),
+        "vpinn_gpu_peer_handle": (i32, [vp, vp]),
+        "vpinn_gpu_attach_peers": (i32, [vp, vp, i32, i32]),
         "vpinn_gpu_time_contract_kernels": (i32, [vp, i32, pd, pd, pd]),
         "vpinn_gpu_download_tensor": (i32, [vp, i32, vp, i64]),
         "vpinn_gpu_launch_count": (i64, [vp]),

@@ -333,6 +333,158 @@ __global__ void __launch_bounds__(kRAThreads) reduce_adam_kernel(const float* __
   }
 }
 
+// ---------------------------------------------------------------------------
+// Multi-GPU epoch tail over peer memory (one process per GPU,
+// every rank's mailbox mapped into every other rank through CUDA IPC over
+// NVLink / NVSwitch): the cross-CTA reduction, the cross-RANK sum and Adam in
+// ONE kernel, instead of reduce -> ncclAllReduce -> Adam.
+//   phase 1  each warp reduces one row of this rank's CTA partials (as
+//            reduce_kernel) and its lanes r < W store the row into slot
+//            [set][rank] of rank r's mailbox (peer stores); the last CTA to
+//            finish publishes the epoch's sequence number into every rank's
+//            flag[set][rank] (system-scope release after a system fence)
+//   phase 2  every CTA waits for the W flags of its own mailbox, then each
+//            warp sums its row over the ranks in rank order (the same bits on
+//            every rank: replicas stay identical) and applies Adam to that
+//            parameter (adam_update, rollback copy); the last CTA does the
+//            bookkeeping (or the abort) exactly as reduce_adam_kernel.
+// With adam = 0 it is the cross-rank gradient sum alone (loss_and_grad).
+// Two slot sets alternate by sequence parity: a rank can run at most one
+// epoch ahead of the slowest (its next tail waits for everyone's flags).
+constexpr int kMaxRanks = 8;
+struct PeerMailbox {
+  unsigned long long flag[2][kMaxRanks];  // [set][source rank]: sequence number of the source's rows
+  unsigned long long seq;                 // this rank's completed exchanges (local)
+  unsigned long long pad[7];
+  // double slot[2][kMaxRanks][rows] follows
+};
+__host__ __device__ constexpr size_t peer_mailbox_bytes(int rows) {
+  return sizeof(PeerMailbox) + sizeof(double) * 2 * kMaxRanks * (size_t)rows;
+}
+__device__ __forceinline__ double* mbox_slot(PeerMailbox* m, int set, int src, int rows) {
+  return reinterpret_cast<double*>(m + 1) + ((size_t)set * kMaxRanks + src) * rows;
+}
+__device__ __forceinline__ unsigned long long ld_acquire_sys_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_sys_u64(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+struct PeerArgs {
+  PeerMailbox* box[kMaxRanks];  // every rank's mailbox in this process's address space
+  int world, rank;
+};
+
+__global__ void __launch_bounds__(kRAThreads) reduce_adam_peer_kernel(const float* __restrict__ grad_part,
+                                                                        int n_rows, int stride, int n_params,
+                                                                        const double* __restrict__ loss_part,
+                                                                        int n_loss_rows, double* __restrict__ red,
+                                                                        unsigned* ticket, float* bk, const AdamArgs a,
+                                                                        const PeerArgs pa, int adam,
+                                                                        const int* stop_flag) {
+  pdl_trigger();
+  __shared__ int last, s_stopped;
+  __shared__ long long s_t;
+  __shared__ unsigned long long s_seq;
+  PeerMailbox* mine = pa.box[pa.rank];
+  if (threadIdx.x == 0) {
+    s_stopped = stop_flag != nullptr ? *stop_flag : 0;
+    s_t = a.st->step + 1;
+    s_seq = mine->seq + 1;
+  }
+  __syncthreads();
+  pdl_wait();
+  if (s_stopped) return;
+  const long long t = s_t;
+  const unsigned long long seq = s_seq;
+  const int set = (int)(seq & 1ull);
+  const int rows = n_params + kLpWords;
+  const int lane = threadIdx.x & 31;
+  const int gw = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  // ---- phase 1: this rank's rows into every rank's mailbox ----
+  float p0 = 0.f, m0 = 0.f, v0 = 0.f;
+  if (gw < rows) {
+    if (adam && gw < n_params && lane == 0) {  // in flight with the partial loads
+      p0 = a.params[gw];
+      m0 = a.m[gw];
+      v0 = a.v[gw];
+    }
+    const double v = reduce_row(gw, grad_part, n_rows, stride, n_params, loss_part, n_loss_rows, red);
+    if (lane < pa.world) mbox_slot(pa.box[lane], set, pa.rank, rows)[gw] = v;
+  }
+  __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(&ticket[0], 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (last) {
+    if (threadIdx.x == 0) ticket[0] = 0u;
+    __threadfence_system();
+    if (threadIdx.x < pa.world) st_release_sys_u64(&pa.box[threadIdx.x]->flag[set][pa.rank], seq);
+  }
+  // ---- phase 2: the rank sum (fixed rank order) and the update ----
+  if (threadIdx.x == 0)
+    for (int r = 0; r < pa.world; ++r)
+      while (ld_acquire_sys_u64(&mine->flag[set][r]) < seq) __nanosleep(64);
+  __syncthreads();
+  auto rank_sum = [&](int row) {
+    double s = 0.0;
+    for (int r = 0; r < pa.world; ++r) s += __ldcv(&mbox_slot(mine, set, r, rows)[row]);
+    return s;
+  };
+  if (gw < rows && lane == 0) {
+    const double total = rank_sum(gw);
+    red[gw] = total;
+    if (adam && gw < n_params) {
+      double gd = total;
+      if (gw == a.eps_grad_slot) gd += rank_sum(n_params + kLpEpsGrad);
+      const float g = (float)gd;
+      if (!isfinite(g)) atomicOr(&ticket[1], 1u);
+      bk[gw] = p0;
+      bk[n_params + gw] = m0;
+      bk[2 * n_params + gw] = v0;
+      adam_update(g, m0, v0, p0, a.lr_tab ? a.lr_tab[t - 1] : a.lr_const,
+                  a.lr_tab ? a.c1_tab[t - 1] : 1.0f - (float)pow(0.9, (double)t),
+                  a.lr_tab ? a.c2_tab[t - 1] : 1.0f - (float)pow(0.999, (double)t), a.m[gw], a.v[gw], a.params[gw]);
+    }
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(&ticket[2], 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  if (!adam) {
+    if (threadIdx.x == 0) {
+      ticket[2] = 0u;
+      mine->seq = seq;
+    }
+    return;
+  }
+  const int bad = __ldcg(&ticket[1]) != 0u || __ldcg(&red[n_params + kLpBad]) != 0.0;
+  if (bad) {  // all or nothing (identical decision on every rank: the same sums)
+    for (int p = threadIdx.x; p < n_params; p += blockDim.x) {
+      a.params[p] = __ldcg(&bk[p]);
+      a.m[p] = __ldcg(&bk[n_params + p]);
+      a.v[p] = __ldcg(&bk[2 * n_params + p]);
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    ticket[1] = 0u;
+    ticket[2] = 0u;
+    mine->seq = seq;
+    if (bad) {
+      a.st->stopped = 1;
+      a.st->stop_reason = 3;
+      a.st->abort_step = t;
+    } else {
+      train_bookkeeping(a, t, a.lr_tab ? a.lr_tab[t - 1] : a.lr_const);
+    }
+  }
+}
+
 __global__ void mark_start_kernel(TrainState* st) { st->t_prev = globaltimer(); }
 
 // vpinn_gpu_run_steps after a finished vpinn_gpu_train: the run's stop

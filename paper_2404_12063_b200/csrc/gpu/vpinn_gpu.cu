@@ -483,6 +483,11 @@ struct vpinn_gpu_ctx {
   // nccl
   void* comm = nullptr;
   int nranks = 1, rank = 0;
+  // peer-memory exchange (vpinn_gpu_attach_peers): this rank's mailbox, every
+  // rank's mailbox mapped here (CUDA IPC)
+  vpg::PeerMailbox* pbox = nullptr;
+  vpg::PeerArgs peers{};
+  bool peer = false;
   long long launches = 0;
   DBuf<char> flush;  // L2 flush scratch (bench)
   DBuf<long long> phase_clk;  // VPINN_PHASE_CLOCK diagnostics
@@ -509,6 +514,10 @@ struct vpinn_gpu_ctx {
     if (stream) cudaStreamSynchronize(stream);  // buffers go back to the block cache idle
     for (auto& kv : graphs) cudaGraphExecDestroy(kv.second);
     if (comm && nccl().comm_destroy) nccl().comm_destroy(comm);
+    if (peer)
+      for (int r = 0; r < peers.world; ++r)
+        if (r != rank && peers.box[r]) cudaIpcCloseMemHandle(peers.box[r]);
+    if (pbox) cudaFree(pbox);
     if (h_flag) pinned_words().put(h_flag);
     if (stream) cudaStreamDestroy(stream);
   }
@@ -1038,6 +1047,8 @@ void launch_contract_rows(vpinn_gpu_ctx* c, const vpg::ContractArgs& ca) {
   c->launches += 2;
 }
 
+vpg::AdamArgs adam_args(vpinn_gpu_ctx* c, bool tables, float lr_const, bool records, int rec_cap);
+
 void enqueue_grad(vpinn_gpu_ctx* c, const int* stop, bool with_reduce = true) {
   const Variant& V = c->var;
   vpg::StepArgs a = c->sargs;
@@ -1089,6 +1100,15 @@ void enqueue_grad(vpinn_gpu_ctx* c, const int* stop, bool with_reduce = true) {
     c->launches += 1;
   }
   if (!with_reduce) return;
+  if (c->peer) {  // this rank's sum and the cross-rank sum in one kernel
+    launch_k(pdl_enabled() && !c->split, vpg::reduce_adam_peer_kernel, vpg::reduce_adam_grid(c->n_params),
+             vpg::kRAThreads, 0, c->stream, c->grad_part.p, c->grad_rows, c->part_stride, c->n_params,
+             (const double*)c->loss_part.p, c->loss_rows, c->red.p, c->ticket.p, c->adam_bk.p,
+             adam_args(c, false, 0.f, false, 0), c->peers, 0, stop);
+    CK(cudaGetLastError());
+    c->launches += 1;
+    return;
+  }
   vpg::reduce_kernel<<<vpg::reduce_grid(c->n_params), vpg::kRedThreads, 0, c->stream>>>(
       c->grad_part.p, c->grad_rows, c->part_stride, c->n_params, c->loss_part.p, c->loss_rows, c->red.p, stop);
   CK(cudaGetLastError());
@@ -1122,6 +1142,17 @@ vpg::AdamArgs adam_args(vpinn_gpu_ctx* c, bool tables, float lr_const, bool reco
 }
 
 void enqueue_epoch(vpinn_gpu_ctx* c, const vpg::AdamArgs& aa) {
+  if (c->peer) {
+    // reduce, the cross-rank sum over peer memory and Adam: one kernel
+    enqueue_grad(c, &c->st.p->stopped, /*with_reduce=*/false);
+    launch_k(pdl_enabled() && !c->split, vpg::reduce_adam_peer_kernel, vpg::reduce_adam_grid(c->n_params),
+             vpg::kRAThreads, 0, c->stream, (const float*)c->grad_part.p, c->grad_rows, c->part_stride, c->n_params,
+             (const double*)c->loss_part.p, c->loss_rows, c->red.p, c->ticket.p, c->adam_bk.p, aa, c->peers, 1,
+             (const int*)&c->st.p->stopped);
+    CK(cudaGetLastError());
+    c->launches += 1;
+    return;
+  }
   if (c->comm) {
     // reduce -> ncclAllReduce -> Adam (the all-reduce sits between them)
     enqueue_grad(c, &c->st.p->stopped);
@@ -1510,7 +1541,7 @@ int vpinn_gpu_create(const vpinn_gpu_problem* pb, vpinn_gpu_ctx** out) {
     c->m.alloc(c->n_params, c->stream);
     c->v.alloc(c->n_params, c->stream);
     c->st.alloc(1, c->stream);
-    c->ticket.alloc(2, c->stream);
+    c->ticket.alloc(3, c->stream);
     c->adam_bk.alloc(3 * (size_t)c->n_params, c->stream);
     mark("uploads", c->stream);
     configure(c.get());
@@ -2269,6 +2300,50 @@ int vpinn_gpu_nccl_unique_id(void* id128) {
     NcclUid u;
     NK(nccl().get_unique_id(&u));
     std::memcpy(id128, u.b, sizeof(u.b));
+  });
+}
+
+int vpinn_gpu_peer_handle(vpinn_gpu_ctx* c, void* handle64) {
+  return guarded([&] {
+    set_dev(c);
+    if (!c->pbox) {
+      const size_t bytes = vpg::peer_mailbox_bytes(c->n_params + vpg::kLpWords);
+      CK(cudaMalloc(&c->pbox, bytes));  // its own allocation: an IPC handle maps a whole allocation
+      CK(cudaMemset(c->pbox, 0, bytes));
+      CK(cudaDeviceSynchronize());
+    }
+    cudaIpcMemHandle_t h;
+    CK(cudaIpcGetMemHandle(&h, c->pbox));
+    static_assert(sizeof(h) == 64, "IPC handle size");
+    std::memcpy(handle64, &h, sizeof(h));
+  });
+}
+
+int vpinn_gpu_attach_peers(vpinn_gpu_ctx* c, const void* handles, int nranks, int rank) {
+  return guarded([&] {
+    if (nranks != c->nranks || rank != c->rank)
+      throw Fail{VPINN_ERR_CONFIG, "attach_peers: rank/world differ from the partition"};
+    if (nranks < 1 || nranks > vpg::kMaxRanks) throw Fail{VPINN_ERR_CONFIG, "attach_peers: 1..8 ranks"};
+    if (!c->pbox) throw Fail{VPINN_ERR_CONFIG, "attach_peers: call vpinn_gpu_peer_handle first"};
+    set_dev(c);
+    vpg::PeerArgs pa{};
+    pa.world = nranks;
+    pa.rank = rank;
+    for (int r = 0; r < nranks; ++r) {
+      if (r == rank) {
+        pa.box[r] = c->pbox;
+        continue;
+      }
+      cudaIpcMemHandle_t h;
+      std::memcpy(&h, static_cast<const char*>(handles) + 64 * (size_t)r, sizeof(h));
+      void* p = nullptr;
+      CK(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+      pa.box[r] = static_cast<vpg::PeerMailbox*>(p);
+    }
+    c->peers = pa;
+    c->peer = true;
+    for (auto& kv : c->graphs) cudaGraphExecDestroy(kv.second);
+    c->graphs.clear();
   });
 }
 

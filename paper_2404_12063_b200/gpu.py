@@ -252,6 +252,19 @@ class GpuStep:
         buf = C.create_string_buffer(uid, 128)
         _capi.check(_capi.lib().vpinn_gpu_attach_comm(self.h, buf, nranks, rank))
 
+    def peer_handle(self) -> bytes:
+        """This rank's mailbox as a 64-byte CUDA IPC handle (vpinn_gpu_peer_handle)."""
+        buf = C.create_string_buffer(64)
+        _capi.check(_capi.lib().vpinn_gpu_peer_handle(self.h, buf))
+        return buf.raw
+
+    def attach_peers(self, handles, nranks: int, rank: int):
+        """Every rank's handle in rank order (vpinn_gpu_attach_peers)."""
+        blob = b"".join(handles)
+        assert len(blob) == 64 * nranks
+        buf = C.create_string_buffer(blob, len(blob))
+        _capi.check(_capi.lib().vpinn_gpu_attach_peers(self.h, buf, nranks, rank))
+
 
 def nccl_unique_id() -> bytes:
     buf = C.create_string_buffer(128)

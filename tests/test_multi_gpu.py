@@ -105,3 +105,86 @@ def test_thousand_step_history_bitwise_identical(case):
     assert np.array_equal(h1.view(np.uint64), h3.view(np.uint64))
     assert np.array_equal(ga.get_params().view(np.uint32), gb.get_params().view(np.uint32))
     assert np.all(np.isfinite(h1)) and h1[0, -1] < h1[0, 0]
+
+
+# ---- the epoch tail over peer memory (vpinn_gpu_attach_peers) ----
+def test_peer_exchange_single_rank_is_bitwise_the_plain_path():
+    """world = 1 through the peer kernel (its own mailbox): the rank sum of
+    one rank is exact, so loss, gradient, a 50-epoch history and the final
+    parameters are the plain path's bits."""
+    spec = c1_spec()
+    ob = po.OracleProblem(spec, double=False)
+    p0 = ob.init_params().astype(np.float32)
+    ga = gpu_from_oracle(ob, spec)
+    gb = gpu_from_oracle(ob, spec)
+    gb.attach_peers([gb.peer_handle()], 1, 0)
+    for g in (ga, gb):
+        g.set_params(p0)
+    pa, grad_a = ga.loss_and_grad()
+    pb, grad_b = gb.loss_and_grad()
+    assert np.array_equal(np.asarray(pa).view(np.uint64), np.asarray(pb).view(np.uint64))
+    assert np.array_equal(grad_a.view(np.uint32), grad_b.view(np.uint32))
+    ha, hb = _history(ga, p0, 50), _history(gb, p0, 50)
+    assert np.array_equal(ha.view(np.uint64), hb.view(np.uint64))
+    assert np.array_equal(ga.get_params().view(np.uint32), gb.get_params().view(np.uint32))
+
+
+def _peer_worker(rank, world, spec, epochs, q_out, q_handles, q_in):
+    try:
+        ob = po.OracleProblem(spec, double=False)
+        g = gpu_from_oracle(ob, spec, device=0, rank=rank, world_size=world)
+        g.set_params(ob.init_params().astype(np.float32))
+        q_handles.put((rank, g.peer_handle()))
+        handles = q_in.get(timeout=300)
+        g.attach_peers(handles, world, rank)
+        parts, grad = g.loss_and_grad()
+        rep = g.train(epochs, lr0=1e-3)
+        q_out.put((rank, parts, grad, rep.records["total"].copy(), g.get_params()))
+        g.close()
+    except Exception as ex:  # noqa: BLE001
+        q_out.put((rank, repr(ex)))
+        raise
+
+
+@pytest.mark.parametrize("case", ["c1", "gear576"])
+def test_peer_exchange_two_ranks_match_single_rank(case):
+    """Two processes (both on device 0, where CUDA IPC maps each other's
+    mailbox; on an 8-GPU node the same protocol runs over NVLink), each with
+    its partition: the one-kernel epoch tail (reduce, rows into every
+    rank's mailbox, rank-ordered sum, Adam) gives bitwise-identical replicas
+    and the single-rank result within the reordered-sum tolerance."""
+    import multiprocessing as mp
+    from tests.test_gpu_parity import gear_spec
+    spec = c1_spec() if case == "c1" else gear_spec()
+    epochs, world = 20, 2
+    ctx = mp.get_context("spawn")
+    q_out, q_handles = ctx.Queue(), ctx.Queue()
+    q_in = [ctx.Queue() for _ in range(world)]
+    procs = [ctx.Process(target=_peer_worker, args=(r, world, spec, epochs, q_out, q_handles, q_in[r]))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    hs = dict(q_handles.get(timeout=300) for _ in range(world))
+    for r in range(world):
+        q_in[r].put([hs[i] for i in range(world)])
+    res = [q_out.get(timeout=600) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=120)
+    for r in res:
+        assert len(r) == 5, r
+    out = dict((r[0], r[1:]) for r in res)
+    for p in procs:
+        assert p.exitcode == 0
+    for k in range(4):
+        assert np.array_equal(np.asarray(out[0][k]).view(np.uint8), np.asarray(out[1][k]).view(np.uint8)), k
+    ob = po.OracleProblem(spec, double=False)
+    g1 = gpu_from_oracle(ob, spec)
+    g1.set_params(ob.init_params().astype(np.float32))
+    parts1, grad1 = g1.loss_and_grad()
+    rep1 = g1.train(epochs, lr0=1e-3)
+    parts2, grad2, tot2, par2 = out[0]
+    assert np.all(np.abs(parts2 - parts1) <= 1e-6 * np.abs(parts1) + 1e-30)
+    assert np.abs(grad2 - grad1).max() <= 1e-6 * np.abs(grad1).max()
+    r = np.abs(tot2 - rep1.records["total"]) / np.abs(rep1.records["total"])
+    assert r.max() < 1e-5
+    assert np.abs(par2 - g1.get_params()).max() < 1e-5
