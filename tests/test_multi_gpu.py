@@ -66,9 +66,7 @@ def test_nccl_two_ranks_match_single_rank(case):
     # replicas bitwise identical: every rank applies Adam to the same reduced vector
     for k in range(4):
         assert np.array_equal(np.asarray(out[0][k]).view(np.uint8), np.asarray(out[1][k]).view(np.uint8)), k
-    ob = po.OracleProblem(spec, double=False)
-    g1 = gpu_from_oracle(ob, spec)
-    g1.set_params(ob.init_params().astype(np.float32))
+    _, g1 = _make(spec)
     parts1, grad1 = g1.loss_and_grad()
     rep1 = g1.train(epochs, lr0=1e-3)
     parts2, grad2, tot2, par2 = out[0]
@@ -129,11 +127,21 @@ def test_peer_exchange_single_rank_is_bitwise_the_plain_path():
     assert np.array_equal(ga.get_params().view(np.uint32), gb.get_params().view(np.uint32))
 
 
+def _make(spec, **kw):
+    """(oracle, GPU context with the oracle's p0) for a weak- or strong-form spec."""
+    if spec.strong:
+        from tests.test_strong_form import make_strong_pair
+        ob, g, _ = make_strong_pair(spec, **kw)
+        return ob, g
+    ob = po.OracleProblem(spec, double=False)
+    g = gpu_from_oracle(ob, spec, **kw)
+    g.set_params(ob.init_params().astype(np.float32))
+    return ob, g
+
+
 def _peer_worker(rank, world, spec, epochs, q_out, q_handles, q_in):
     try:
-        ob = po.OracleProblem(spec, double=False)
-        g = gpu_from_oracle(ob, spec, device=0, rank=rank, world_size=world)
-        g.set_params(ob.init_params().astype(np.float32))
+        ob, g = _make(spec, device=0, rank=rank, world_size=world)
         q_handles.put((rank, g.peer_handle()))
         handles = q_in.get(timeout=300)
         g.attach_peers(handles, world, rank)
@@ -146,7 +154,7 @@ def _peer_worker(rank, world, spec, epochs, q_out, q_handles, q_in):
         raise
 
 
-@pytest.mark.parametrize("case", ["c1", "gear576"])
+@pytest.mark.parametrize("case", ["c1", "gear576", "strong_sensors"])
 def test_peer_exchange_two_ranks_match_single_rank(case):
     """Two processes (both on device 0, where CUDA IPC maps each other's
     mailbox; on an 8-GPU node the same protocol runs over NVLink), each with
@@ -155,7 +163,10 @@ def test_peer_exchange_two_ranks_match_single_rank(case):
     and the single-rank result within the reordered-sum tolerance."""
     import multiprocessing as mp
     from tests.test_gpu_parity import gear_spec
-    spec = c1_spec() if case == "c1" else gear_spec()
+    from tests.test_strong_form import strong_spec
+    spec = {"c1": c1_spec, "gear576": gear_spec,
+            "strong_sensors": lambda: strong_spec(bx=0.7, by=-0.4, eps_source=1, scalars=(1.5,), n_sensors=21,
+                                                  sensor_field="sin2pi_u")}[case]()
     epochs, world = 20, 2
     ctx = mp.get_context("spawn")
     q_out, q_handles = ctx.Queue(), ctx.Queue()
@@ -177,14 +188,15 @@ def test_peer_exchange_two_ranks_match_single_rank(case):
         assert p.exitcode == 0
     for k in range(4):
         assert np.array_equal(np.asarray(out[0][k]).view(np.uint8), np.asarray(out[1][k]).view(np.uint8)), k
-    ob = po.OracleProblem(spec, double=False)
-    g1 = gpu_from_oracle(ob, spec)
-    g1.set_params(ob.init_params().astype(np.float32))
+    _, g1 = _make(spec)
     parts1, grad1 = g1.loss_and_grad()
     rep1 = g1.train(epochs, lr0=1e-3)
     parts2, grad2, tot2, par2 = out[0]
     assert np.all(np.abs(parts2 - parts1) <= 1e-6 * np.abs(parts1) + 1e-30)
-    assert np.abs(grad2 - grad1).max() <= 1e-6 * np.abs(grad1).max()
+    # the partition regroups the fp32 per-CTA sums (1e-5 for the order-2
+    # strong form, as test_strong_rank_partition_sums_to_whole)
+    gtol = 1e-5 if spec.strong else 1e-6
+    assert np.abs(grad2 - grad1).max() <= gtol * np.abs(grad1).max()
     r = np.abs(tot2 - rep1.records["total"]) / np.abs(rep1.records["total"])
     assert r.max() < 1e-5
     assert np.abs(par2 - g1.get_params()).max() < 1e-5
