@@ -284,10 +284,14 @@ int vpinn_gpu_time_contract_matrix_free(vpinn_gpu_ctx* ctx, int reps, double* ms
  *                              serves, so its parity is tested on them;
  *   VPINN_HOOK_FORCE_SPILL     the tensor-core step spills its TMEM
  *                              parameter-gradient accumulators every tile
- *                              (the rare path of large scale drops).
+ *                              (the rare path of large scale drops);
+ *   VPINN_HOOK_THROUGHPUT_LAYOUT  the tensor-core step keeps 16 units per
+ *                              thread also on grids of at most one tile per
+ *                              SM (where it takes the 8-unit latency layout).
  * 0 restores the defaults. */
 #define VPINN_HOOK_CUDA_CORE_STEP 1
 #define VPINN_HOOK_FORCE_SPILL 2
+#define VPINN_HOOK_THROUGHPUT_LAYOUT 4
 int vpinn_gpu_set_test_hooks(int flags);
 
 /* Device buffers released by destroyed contexts are cached per size for

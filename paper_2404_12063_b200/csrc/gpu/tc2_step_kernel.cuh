@@ -70,14 +70,19 @@
 namespace vpg {
 namespace t2 {
 
-// per width class (H = the instantiated hidden width)
-template <int H>
+// per width class (H = the instantiated hidden width) and hidden units per
+// thread (UPT = 16: the throughput layout; UPT = 8: twice the threads on the
+// same tile, the latency layout for grids of at most one tile per SM)
+template <int H, int UPT = 16>
 struct Cfg {
   static constexpr int NB = (H + 1 + 31) / 32;  // 32-unit column blocks (bias unit included)
   static_assert(NB == 1 || NB == 2, "tc2 step: hidden width <= 63");
+  static_assert(UPT == 16 || UPT == 8, "tc2 step: 8 or 16 units per thread");
   static constexpr int HP = 32 * NB;
-  static constexpr int NG = 2 * NB;              // unit groups of 16
+  static constexpr int NCH = UPT / 8;            // 8-unit chunks per thread
+  static constexpr int NG = HP / UPT;            // unit groups
   static constexpr int NT = 128 * NG;            // threads
+  static_assert(NT <= 512, "tc2 step: at most 512 threads");
   static constexpr int MP = NB == 1 ? 128 : 112;  // points per tile
   static constexpr int kPart = MP * 64;          // [MP][32] fp16 tile
   static constexpr int kStream = 2 * NB * kPart;  // tiles (part, block): part h blocks | part l blocks
@@ -131,9 +136,9 @@ enum : int {
 // integer exponents (ints in S_SCI): kW[2], kXv[2], kXt[2]
 enum : int { kSiW = 0, kSiXv = 2, kSiXt = 4, kSiN = 6 };
 
-template <int H, int D, int C = 1>
+template <int H, int D, int C = 1, int UPT = 16>
 struct Lay {
-  using CF = Cfg<H>;
+  using CF = Cfg<H, UPT>;
   static constexpr int NL = D - 1;
   static constexpr int HP = CF::HP;
   static constexpr int OFF_A = (NL * CF::kWL + 1023) & ~1023;  // W tiles first; buffers 1024-aligned
@@ -295,13 +300,14 @@ __device__ __forceinline__ void issue_param(uint32_t acc, uint64_t da, uint64_t 
 // kModeReverse = forward recompute + reverse from the adjoints in a.in_*
 // (the split path of cells larger than a tile: forward -> contraction ->
 // penalty -> reverse)
-template <int H, int D, int ACT, int MODE = kModeFused, int C = 1>
-__global__ void __maxnreg__(t2::Cfg<H>::kMaxReg) tc2_step_kernel(const StepArgs a) {
+template <int H, int D, int ACT, int MODE = kModeFused, int C = 1, int UPT = 16>
+__global__ void __maxnreg__((t2::Cfg<H, UPT>::kMaxReg)) tc2_step_kernel(const StepArgs a) {
   using namespace t2;
   static_assert(D == 2 || D == 3, "tc2 step: 2 or 3 hidden layers");
   static_assert(C == 1 || C == 2, "tc2 step: one output, or two (spatial-eps head)");
-  using CF = Cfg<H>;
-  using LY = Lay<H, D, C>;
+  using CF = Cfg<H, UPT>;
+  using LY = Lay<H, D, C, UPT>;
+  constexpr int NCH = CF::NCH;
   constexpr int kAccW = acc_w<C>();
   constexpr int NL = LY::NL;
   constexpr int NB = CF::NB, HP = CF::HP, NT = CF::NT, MP = CF::MP;
@@ -309,7 +315,7 @@ __global__ void __maxnreg__(t2::Cfg<H>::kMaxReg) tc2_step_kernel(const StepArgs 
   // contraction threads per row / per point: all of them when the CTA is
   // alone on its SM (NB = 2); one (unit group 0) when two CTAs share the SM,
   // whose other CTA fills the idle issue slots (splitting measured slower)
-  constexpr int kCS = NB == 1 ? 1 : NT / 128;
+  constexpr int kCS = NT >= 512 ? NT / 128 : 1;
   using AC = Act<ACT>;
 
 #if !VPG_PDL_LATE
@@ -358,8 +364,8 @@ __global__ void __maxnreg__(t2::Cfg<H>::kMaxReg) tc2_step_kernel(const StepArgs 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int p = tid & 127;   // point of this thread == TMEM lane
   const int ug = tid >> 7;   // unit group
-  const int u0 = 16 * ug;    // first hidden unit of this thread
-  const uint32_t tb = (uint32_t)(ug >> 1) * kPart;  // this thread's column block inside a part
+  const int u0 = UPT * ug;   // first hidden unit of this thread
+  const uint32_t tb = (uint32_t)(u0 >> 5) * kPart;  // this thread's column block inside a part
   // MP < 128 (NB = 2): the threads of TMEM lanes MP..127 hold no point; they
   // compute on the accumulators' unused rows, never store an operand row
   // (row p of an [MP][32] tile would be row p - MP of the next one) and add
@@ -522,7 +528,8 @@ __global__ void __maxnreg__(t2::Cfg<H>::kMaxReg) tc2_step_kernel(const StepArgs 
   const uint32_t lane_q = (uint32_t)(32 * (warp & 3)) << 16;  // TMEM lane quarter of this warp
   const uint32_t sA = smem_u32(bufA), sB = smem_u32(bufB), sW = smem_u32(sWB);
   // swizzled byte offsets of this thread's two 8-unit chunks inside its block's tile
-  const uint32_t off0 = tc::sw_chunk(p, 2 * (ug & 1)) + tb, off1 = tc::sw_chunk(p, 2 * (ug & 1) + 1) + tb;
+  const uint32_t off0 = tc::sw_chunk(p, (u0 & 31) >> 3) + tb;
+  const uint32_t off1 = NCH == 2 ? tc::sw_chunk(p, ((u0 & 31) >> 3) + 1) + tb : off0;
 
   // ---------------- MMA issue ----------------
   // descriptors: start address >> 4 in the low 14 bits, so an address offset
@@ -653,8 +660,9 @@ __global__ void __maxnreg__(t2::Cfg<H>::kMaxReg) tc2_step_kernel(const StepArgs 
     }
     return 32 * (warp & 3) + lane;
   };
-  // this thread's 2HP / NG = 32 accumulator columns (X part * HP + i)
-  const int col_base = 32 * ug;
+  // this thread's 2HP / NG accumulator columns (X part * HP + i)
+  constexpr int kColsT = 2 * HP / CF::NG;
+  const int col_base = kColsT * ug;
   // rare path (an accumulator would need more than 2^-15): add the layer-l
   // accumulator, unscaled, into the per-CTA fp32 scratch ([col][row]) and
   // restart it
@@ -662,7 +670,7 @@ __global__ void __maxnreg__(t2::Cfg<H>::kMaxReg) tc2_step_kernel(const StepArgs 
     float* S = a.tc_scratch + ((size_t)blockIdx.x * NL + (l - 1)) * CF::kScratch;
     const float inv = tc::exp2i(-kacc);
 #pragma unroll 1
-    for (int h2 = 0; h2 < 2; ++h2) {
+    for (int h2 = 0; h2 < kColsT / 16; ++h2) {
       const int col0 = col_base + 16 * h2;
       float v[16];
       tc::tmem_ld1x16_wait(gacc_ld(l) + col0, v);
@@ -803,7 +811,7 @@ __global__ void __maxnreg__(t2::Cfg<H>::kMaxReg) tc2_step_kernel(const StepArgs 
     // =================== forward ===================
     char* x1buf = (D == 3) ? bufA : bufB;  // hidden-1 output (input of MMA layer 1)
 #pragma unroll kUC
-    for (int c = 0; c < 2; ++c) store_x1(x1buf + 0, c, px, py, false);
+    for (int c = 0; c < NCH; ++c) store_x1(x1buf + 0, c, px, py, false);
     operands_ready();
     if (warp < 3) issue_point_gemm(D == 2, 1, false);
     mark(1);
@@ -820,10 +828,10 @@ __global__ void __maxnreg__(t2::Cfg<H>::kMaxReg) tc2_step_kernel(const StepArgs 
       const float ft = last ? sSc[kScF1 + l - 1] : sSc[kScF1 + l - 1] * sSc[kScSt + l];
       const float sv = last ? 1.f : sSc[kScSv + l];
       const float* bias = sBias + HP * (l - 1);
-      float s1v[16];
+      float s1v[UPT];
       mma_wait(bar_v, ph_v);
 #pragma unroll
-      for (int c = 0; c < 2; ++c) {
+      for (int c = 0; c < NCH; ++c) {
         float d[8], z[8];
         tc::tmem_ld1x8_wait(dcol(0, c), d);
 #pragma unroll
@@ -855,7 +863,7 @@ __global__ void __maxnreg__(t2::Cfg<H>::kMaxReg) tc2_step_kernel(const StepArgs 
       if (D == 3 && l == 1 && interior && tid == 0)
         issue_chunk(a, cell0, 0, nrows_tile, reinterpret_cast<float*>(bufA), tma_bar);
 #pragma unroll
-      for (int c = 0; c < 2; ++c) {
+      for (int c = 0; c < NCH; ++c) {
         float dx[8], dy[8];
         tc::tmem_ld2x8_wait(dcol(1, c), dcol(2, c), dx, dy);
         if (last) {
@@ -1199,7 +1207,7 @@ __global__ void __maxnreg__(t2::Cfg<H>::kMaxReg) tc2_step_kernel(const StepArgs 
       const float Ub = ub * sgv, Uxv = uxb * sgv, Uyv = uyb * sgv, Uxt = uxb * sgt, Uyt = uyb * sgt;
       const float Y1 = y1b * sgv;
 #pragma unroll kUC
-      for (int c = 0; c < 2; ++c) {
+      for (int c = 0; c < NCH; ++c) {
         float zs[8], dx[8], dy[8];
         tc::tmem_ld1x8_wait(tmem + lane_q + LY::kZ0 + u0 + 8 * c, zs);
         tc::tmem_ld2x8_wait(dcol(1, c), dcol(2, c), dx, dy);
@@ -1274,7 +1282,7 @@ __global__ void __maxnreg__(t2::Cfg<H>::kMaxReg) tc2_step_kernel(const StepArgs 
       mma_wait(bar_v, ph_v);
       mma_wait(bar_t, ph_t);
 #pragma unroll kUC
-      for (int c = 0; c < 2; ++c) {
+      for (int c = 0; c < NCH; ++c) {
         float xa[8], xx[8], xy[8], z[8], tx[8], ty[8];
         tc::tmem_ld1x8_wait(dcol(0, c), xa);
         tc::tmem_ld2x8_wait(dcol(1, c), dcol(2, c), xx, xy);
@@ -1385,7 +1393,7 @@ __global__ void __maxnreg__(t2::Cfg<H>::kMaxReg) tc2_step_kernel(const StepArgs 
     if (has) {
       const float inv = tc::exp2i(-kacc);
 #pragma unroll 1
-      for (int h2 = 0; h2 < 2; ++h2) {
+      for (int h2 = 0; h2 < kColsT / 16; ++h2) {
         const int col0 = col_base + 16 * h2;
         float v[16];
         tc::tmem_ld1x16_wait(gacc_ld(l) + col0, v);
@@ -1437,9 +1445,9 @@ __global__ void __maxnreg__(t2::Cfg<H>::kMaxReg) tc2_step_kernel(const StepArgs 
     }
   }
   for (int u = tid; u <= H; u += NT) {
-    const int h2 = u >> 4, j = u & 15;
+    const int grp = u / UPT, j = u % UPT;  // unit group (warps 4 grp .. +3), unit within it
     float w0x = 0.f, w0y = 0.f, b0 = 0.f, wd = 0.f, wd1 = 0.f;
-    for (int w = 4 * h2; w < 4 * h2 + 4; ++w) {
+    for (int w = 4 * grp; w < 4 * grp + 4; ++w) {
       const float* A = sAcc + w * kAccW;
       w0x += A[kAW0x + j];
       w0y += A[kAW0y + j];
@@ -1494,9 +1502,9 @@ __global__ void __maxnreg__(t2::Cfg<H>::kMaxReg) tc2_step_kernel(const StepArgs 
   }
 }
 
-template <int H, int D, int C = 1>
+template <int H, int D, int C = 1, int UPT = 16>
 __host__ __device__ constexpr size_t tc2_step_smem_bytes() {
-  return t2::Lay<H, D, C>::BYTES;
+  return t2::Lay<H, D, C, UPT>::BYTES;
 }
 
 }  // namespace vpg

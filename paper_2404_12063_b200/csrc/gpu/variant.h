@@ -17,6 +17,9 @@ struct Variant {
   StepFn tc2;      // tensor-core step (tc2_step_kernel.cuh), nullptr if the shape has none
   StepFn tc2_fwd;  // its forward-only / reverse-only modes (split path, evaluate)
   StepFn tc2_rev;
+  StepFn tc2_lat;       // the fused step with 8 units per thread (512 threads): grids of <= 1 tile per SM
+  size_t tc2_lat_smem;
+  int tc2_lat_nt;
   size_t tc2_smem;
   int tc2_nt;        // threads per CTA
   int tc2_mp;        // points per tile
@@ -79,6 +82,11 @@ Variant make_variant() {
     v.tc2_mp = CF::MP;
     v.tc2_buf = CF::kBuf;
     v.tc2_scratch = CF::kScratch;
+    if constexpr (CF::NB == 1) {
+      v.tc2_lat = tc2_step_kernel<H, D, A, kModeFused, C, 8>;
+      v.tc2_lat_smem = tc2_step_smem_bytes<H, D, C, 8>();
+      v.tc2_lat_nt = t2::Cfg<H, 8>::NT;
+    }
     }
   }
   return v;

@@ -506,6 +506,7 @@ struct vpinn_gpu_ctx {
   int sf_block = 0, sf_pts = 0;     // its threads per CTA, points per CTA and tile
   long long n_int_global = 0;
   bool tc2 = false;           // fp16-split two-CTA tensor-core step
+  bool tc2_lat = false;       // ... in its latency layout (tc2_lat: grids of <= 1 tile per SM)
   bool tc2_modes = false;     // tc2 forward / reverse modes serve the split path and evaluate
   int grid_tc2 = 0;           // 2 CTAs per SM
 
@@ -727,11 +728,22 @@ void configure(vpinn_gpu_ctx* c) {
       if (occ < 1) throw Fail{VPINN_ERR_DEVICE, "tc2 step kernel cannot be resident"};
       occ = tc2_ctas_per_sm(c->smem_step);
       c->grid_step = std::max(1, std::min(a.n_tiles, occ * c->sm_count));
+      // at most one tile per SM: the latency layout (8 units per thread, 512
+      // threads) halves every thread's elementwise chain on the lone tile
+      c->tc2_lat = V.tc2_lat != nullptr && a.n_tiles <= c->sm_count &&
+                   !(g_test_hooks.load() & VPINN_HOOK_THROUGHPUT_LAYOUT);
+      if (c->tc2_lat) {
+        c->smem_step = V.tc2_lat_smem;
+        CK(cudaFuncSetAttribute(V.tc2_lat, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem_step));
+        occ = 1;
+        c->grid_step = std::max(1, a.n_tiles);
+      }
       c->tc_scratch.alloc((size_t)c->grid_step * (V.D - 1) * V.tc2_scratch, c->stream);
       a.tc_scratch = c->tc_scratch.p;
       a.tc_force_spill = (g_test_hooks.load() & VPINN_HOOK_FORCE_SPILL) ? 1 : 0;
       c->kernel_name = "tc2_step_kernel<" + std::to_string(V.H) + "," + std::to_string(V.D) + "," +
-                       (V.ACT ? "sigmoid" : "tanh") + (V.C == 2 ? ",2 outputs" : "") + "> (fp16 split, " + std::to_string(V.tc2_nt) + " threads, " +
+                       (V.ACT ? "sigmoid" : "tanh") + (V.C == 2 ? ",2 outputs" : "") + (c->tc2_lat ? ",8 units/thread" : "") +
+                       "> (fp16 split, " + std::to_string(c->tc2_lat ? V.tc2_lat_nt : V.tc2_nt) + " threads, " +
                        std::to_string(occ) + " CTA" + (occ > 1 ? "s" : "") + "/SM)";
     } else {
       c->kernel_name = "step_kernel<" + std::to_string(V.H) + "," + std::to_string(V.D) + "," + std::to_string(V.C) +
@@ -1016,7 +1028,8 @@ void launch_fused(vpinn_gpu_ctx* c, const vpg::StepArgs& a) {
     launch_k(pdl_enabled(), c->sf_tc ? c->sfk.tc_fused : c->sfk.fused, c->grid_step, c->sf_block, c->smem_step,
              c->stream, a);
   else if (c->tc2)
-    launch_k(pdl_enabled(), c->var.tc2, c->grid_step, c->var.tc2_nt, c->smem_step, c->stream, a);
+    launch_k(pdl_enabled(), c->tc2_lat ? c->var.tc2_lat : c->var.tc2, c->grid_step,
+             c->tc2_lat ? c->var.tc2_lat_nt : c->var.tc2_nt, c->smem_step, c->stream, a);
   else
     c->var.fused<<<c->grid_step, vpg::kThreads, c->smem_step, c->stream>>>(a);
   CK(cudaGetLastError());
@@ -2186,7 +2199,7 @@ int vpinn_gpu_profile_step(vpinn_gpu_ctx* c, int reps, double* ms_mlp, double* m
 
 int vpinn_gpu_set_test_hooks(int flags) {
   return guarded([&] {
-    if (flags & ~(VPINN_HOOK_CUDA_CORE_STEP | VPINN_HOOK_FORCE_SPILL))
+    if (flags & ~(VPINN_HOOK_CUDA_CORE_STEP | VPINN_HOOK_FORCE_SPILL | VPINN_HOOK_THROUGHPUT_LAYOUT))
       throw Fail{VPINN_ERR_CONFIG, "set_test_hooks: unknown flag"};
     g_test_hooks.store(flags);
   });

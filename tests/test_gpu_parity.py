@@ -226,19 +226,23 @@ def test_hooks():
     _capi.check(L.vpinn_gpu_set_test_hooks(0))
 
 
-HOOK_CUDA_CORE_STEP, HOOK_FORCE_SPILL = 1, 2
+HOOK_CUDA_CORE_STEP, HOOK_FORCE_SPILL, HOOK_THROUGHPUT_LAYOUT = 1, 2, 4
 
 
 @pytest.mark.parametrize("name", ["c1_poisson", "gear576_cd2d", "inverse_scalar_eps", "paper_gear_h50",
                                   "spatial_eps_head"])
-@pytest.mark.parametrize("mode", ["cuda_core", "tc2_spill"])
+@pytest.mark.parametrize("mode", ["cuda_core", "tc2_spill", "tc2_throughput", "tc2_throughput_spill"])
 def test_alternate_step_kernels_match_oracle(name, mode, test_hooks):
     """The CUDA-core (FFMA) fused kernel (it serves every shape without a
-    tensor-core variant) on shapes the tensor-core step serves, and the
+    tensor-core variant) on shapes the tensor-core step serves, the
     tensor-core step's accumulator spill path (a rare path forced every
-    tile), selected with vpinn_gpu_set_test_hooks: both meet the same parity
-    bar as the default path."""
-    test_hooks(HOOK_CUDA_CORE_STEP if mode == "cuda_core" else HOOK_FORCE_SPILL)
+    tile) and its 16-units-per-thread throughput layout on these small grids
+    (which default to the 8-unit latency layout), selected with
+    vpinn_gpu_set_test_hooks: all meet the same parity bar as the default
+    path."""
+    test_hooks({"cuda_core": HOOK_CUDA_CORE_STEP, "tc2_spill": HOOK_FORCE_SPILL,
+                "tc2_throughput": HOOK_THROUGHPUT_LAYOUT,
+                "tc2_throughput_spill": HOOK_THROUGHPUT_LAYOUT | HOOK_FORCE_SPILL}[mode])
     spec = CASES[name]()
     ob, g, p0 = make_pair(spec)
     kernel = g.step_kernel()
