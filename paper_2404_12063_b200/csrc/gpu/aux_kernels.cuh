@@ -424,9 +424,16 @@ __global__ void __launch_bounds__(kRAThreads) reduce_adam_peer_kernel(const floa
     if (threadIdx.x < pa.world) st_release_sys_u64(&pa.box[threadIdx.x]->flag[set][pa.rank], seq);
   }
   // ---- phase 2: the rank sum (fixed rank order) and the update ----
-  if (threadIdx.x == 0)
+  if (threadIdx.x == 0) {
+    // a peer that never arrives (a dead rank) must not hang the device: trap
+    // after 30 s, the host sees a launch error instead of a hang
+    const unsigned long long t0 = globaltimer();
     for (int r = 0; r < pa.world; ++r)
-      while (ld_acquire_sys_u64(&mine->flag[set][r]) < seq) __nanosleep(64);
+      while (ld_acquire_sys_u64(&mine->flag[set][r]) < seq) {
+        __nanosleep(64);
+        if (globaltimer() - t0 > 30000000000ull) __trap();
+      }
+  }
   __syncthreads();
   auto rank_sum = [&](int row) {
     double s = 0.0;
