@@ -154,7 +154,7 @@ def _peer_worker(rank, world, spec, epochs, q_out, q_handles, q_in):
         raise
 
 
-@pytest.mark.parametrize("case", ["c1", "gear576", "strong_sensors"])
+@pytest.mark.parametrize("case", ["c1", "gear576", "strong_sensors", "split_path"])
 def test_peer_exchange_two_ranks_match_single_rank(case):
     """Two processes (both on device 0, where CUDA IPC maps each other's
     mailbox; on an 8-GPU node the same protocol runs over NVLink), each with
@@ -165,6 +165,9 @@ def test_peer_exchange_two_ranks_match_single_rank(case):
     from tests.test_gpu_parity import gear_spec
     from tests.test_strong_form import strong_spec
     spec = {"c1": c1_spec, "gear576": gear_spec,
+            "split_path": lambda: po.ProblemSpec(*po.structured_mesh(3, 2), n_test_1d=6, n_quad_1d=20,
+                                                 forcing="sin4pi_f", boundary_g="sin4pi_u", n_boundary=200,
+                                                 layers=(2, 30, 30, 30, 1), seed=42),
             "strong_sensors": lambda: strong_spec(bx=0.7, by=-0.4, eps_source=1, scalars=(1.5,), n_sensors=21,
                                                   sensor_field="sin2pi_u")}[case]()
     epochs, world = 20, 2
