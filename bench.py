@@ -134,14 +134,20 @@ def attach_ranks(g, pg, world, rank):
     if world <= 1:
         return
     from paper_2404_12063_b200 import gpu as G
-    try:
-        obj = [None] * world
-        pg.all_gather_object(obj, g.peer_handle())
-        g.attach_peers(obj, world, rank)
-        ok = 1
-    except Exception:  # noqa: BLE001
-        ok = 0
     import torch
+    try:
+        mine = g.peer_handle()
+    except Exception:  # noqa: BLE001
+        mine = None
+    obj = [None] * world
+    pg.all_gather_object(obj, mine)  # every rank joins the gather, also after a failure
+    ok = 0
+    if all(h is not None for h in obj):
+        try:
+            g.attach_peers(obj, world, rank)
+            ok = 1
+        except Exception:  # noqa: BLE001
+            ok = 0
     t = torch.tensor([ok], dtype=torch.int32)
     pg.all_reduce(t, op=pg.ReduceOp.MIN)  # every rank takes the same path
     if int(t.item()) == 1:

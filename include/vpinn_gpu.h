@@ -337,6 +337,7 @@ int vpinn_gpu_attach_comm(vpinn_gpu_ctx* ctx, const void* id128, int nranks, int
  * replacing reduce -> ncclAllReduce -> Adam (the reference's train loop,
  * trainer.hpp:316-370, partitioned across ranks).  At most 8 ranks; every
  * rank must run the same epochs (the exchange is a barrier). */
+/* (A later vpinn_gpu_attach_comm replaces an attached peer exchange.) */
 int vpinn_gpu_peer_handle(vpinn_gpu_ctx* ctx, void* handle64);
 int vpinn_gpu_attach_peers(vpinn_gpu_ctx* ctx, const void* handles, int nranks, int rank);
 

@@ -2067,6 +2067,12 @@ int vpinn_gpu_attach_comm(vpinn_gpu_ctx* c, const void* id128, int nranks, int r
     void* comm = nullptr;
     NK(nccl().comm_init_rank(&comm, nranks, u, rank));
     c->comm = comm;
+    if (c->peer) {  // the last attachment wins: peers detached
+      for (int r = 0; r < c->peers.world; ++r)
+        if (r != c->rank && c->peers.box[r]) cudaIpcCloseMemHandle(c->peers.box[r]);
+      c->peers = vpg::PeerArgs{};
+      c->peer = false;
+    }
     for (auto& kv : c->graphs) cudaGraphExecDestroy(kv.second);
     c->graphs.clear();
   });
