@@ -227,6 +227,8 @@ ROW_CASES = {
     "scalar52_spatial": dict(mesh=(2, 1), nt=4, nq=35, layers=(2, 16, 16, 16, 2), eps_source=2, bx=0.0,
                              forcing="sinpi_vareps_f"),
     "rows_kernel_q1681": dict(mesh=(1, 2), nt=5, nq=41),
+    "fewer_rows_than_warps": dict(mesh=(1, 1), nt=2, nq=12),
+    "rows_spanning_cells_scalar": dict(mesh=(7, 5), nt=3, nq=17, bx=0.0),
     "rows_kernel_conv": dict(mesh=(2, 2), nt=4, nq=20, bx=0.4, by=-0.3),
 }
 
