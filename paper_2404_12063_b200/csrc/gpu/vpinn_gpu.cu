@@ -352,8 +352,11 @@ void configure(vpinn_gpu_ctx* c) {
   }
   // ---- fused path when a cell fits a CTA, split path otherwise ----
   const int P_local = c->n_int + c->n_bnd + c->n_sen;
-  c->split = c->Q > vpg::kThreads;
   const Variant& V = c->var;
+  // a cell larger than the tensor-core step's tile (the 64 class: 112
+  // points) takes the split path too, on its tensor-core modes
+  c->split = c->Q > vpg::kThreads ||
+             (V.tc2 != nullptr && c->Q > V.tc2_mp && !(g_test_hooks.load() & VPINN_HOOK_CUDA_CORE_STEP));
   vpg::StepArgs& a = c->sargs;
   std::memset(&a, 0, sizeof(a));
   for (int t = 0; t < 3; ++t) a.tens[t] = c->tens[t].p;
@@ -397,7 +400,9 @@ void configure(vpinn_gpu_ctx* c) {
   if (!c->split) {
     // tensor-core step: whole-cell tiles of at most tc2_mp points, the tile's
     // slab plus its contraction scratch in operand buffer A
-    const int tc_cells = V.tc2 ? std::max(1, V.tc2_mp / c->Q) : 1;
+    // whole cells per tile: as many as the points allow, at most 128 test
+    // rows (the contraction's per-row scratch)
+    const int tc_cells = V.tc2 ? std::max(1, std::min(V.tc2_mp / c->Q, 128 / std::max(1, c->T))) : 1;
     const int tc_rows = tc_cells * c->T;
     c->tc2 = V.tc2 != nullptr && !(g_test_hooks.load() & VPINN_HOOK_CUDA_CORE_STEP) &&
              c->Q >= 2 && c->Q <= V.tc2_mp &&
@@ -405,7 +410,7 @@ void configure(vpinn_gpu_ctx* c) {
              (size_t)(c->nt * round4(tc_rows * c->Q + 8) +
                       (V.C == 2 ? vpg::t2::tail_floats<2>() : vpg::t2::tail_floats<1>())) * sizeof(float) <=
                  (size_t)V.tc2_buf;
-    a.cells_per_tile = std::max(1, (c->tc2 ? V.tc2_mp : vpg::kThreads) / c->Q);
+    a.cells_per_tile = c->tc2 ? tc_cells : std::max(1, vpg::kThreads / c->Q);
     a.n_int_tiles = c->E ? ceil_div(c->E, a.cells_per_tile) : 0;
     a.n_tiles = a.n_int_tiles + ceil_div(c->n_bnd + c->n_sen, c->tc2 ? V.tc2_mp : vpg::kThreads);
     const int tile_rows = a.cells_per_tile * c->T;

@@ -253,3 +253,25 @@ def test_row_contraction_layouts_match_oracle(case):
     pg2, gg2 = g.loss_and_grad()
     assert np.array_equal(np.asarray(pg2), np.asarray(pg)) and np.array_equal(gg2, gg)
     g.close()
+
+
+# served-shape gaps the randomised fuzz (tools/random_fuzz.py) found: the
+# 64-wide class with many small cells per tile (more than 128 test rows at
+# 112 points: fewer cells per tile) and with 112 < Q <= 128 (cells larger than
+# its tile: the split path)
+@pytest.mark.parametrize("mesh,nt,nq,layers", [((12, 8), 5, 3, (2, 53, 10, 13, 1)),
+                                               ((1, 1), 7, 5, (2, 53, 53, 53, 1)),
+                                               ((6, 6), 4, 11, (2, 62, 62, 62, 1)),
+                                               ((12, 2), 3, 11, (2, 15, 51, 59, 1))])
+def test_wide_class_tiling_gaps_match_oracle(mesh, nt, nq, layers):
+    spec = po.ProblemSpec(*po.structured_mesh(*mesh), n_test_1d=nt, n_quad_1d=nq, forcing="sin4pi_f",
+                          boundary_g="sin2pi_u", n_boundary=60, layers=layers, bx=0.3, seed=3)
+    ob, g, p0 = make_pair(spec)
+    assert "tc2_step" in g.step_kernel(), g.step_kernel()
+    po_, go32 = ob.loss_and_grad(p0)
+    pg, gg = g.loss_and_grad()
+    _, g64 = po.OracleProblem(spec, double=True).loss_and_grad(p0.astype(np.float64))
+    assert abs(pg[0] - po_[0]) / abs(po_[0]) < 1e-5
+    e32 = np.abs(go32 - g64).max() / np.abs(g64).max()
+    assert np.abs(gg - g64).max() / np.abs(g64).max() < max(1e-5, 4.0 * e32)
+    g.close()
