@@ -262,7 +262,10 @@ __global__ void __launch_bounds__(kRAThreads) reduce_adam_kernel(const float* __
                                                                    unsigned* ticket, float* bk, const AdamArgs a) {
   pdl_trigger();
   // the trainer state is this epoch's before the wait: the previous epoch's
-  // tail completed before this epoch's step kernel passed its own wait
+  // tail completed before this epoch's step kernel passed its own wait, and
+  // every step kernel triggers this launch only after that wait (tc2 / sf2:
+  // after the tile loop; sf_step: right after the wait; step_kernel and the
+  // split path: no programmatic launch)
   __shared__ int last, s_stopped;
   __shared__ long long s_t;
   if (threadIdx.x == 0) {

@@ -232,8 +232,11 @@ template <int D, int ACT, int MODE>
 __global__ void __launch_bounds__(32 * sf::kMaxWarps, 1) sf_step_kernel(const StepArgs a) {
   using namespace sf;
   static_assert(D >= 1 && D <= 4, "hidden layers");
-  pdl_trigger();
+  // the trigger after the wait: the epoch tail launched early reads the
+  // trainer state before its own wait (reduce_adam_kernel), which is only
+  // sound once this kernel's predecessor -- the previous tail -- completed
   pdl_wait();
+  pdl_trigger();
   if constexpr (MODE == kModeFused) {
     if (a.stop_flag && *a.stop_flag) return;
   }
@@ -291,7 +294,10 @@ __global__ void __launch_bounds__(32 * sf::kMaxWarps, 1) sf_step_kernel(const St
   float gb_own[D];
 #pragma unroll
   for (int l = 0; l < D; ++l) gb_own[l] = 0.0f;
-  float gw0x_own = 0.f, gw0y_own = 0.f, gwo_own = 0.f, gbo = 0.f;
+  // the output bias gradient sums the boundary / sensor adjoints, which
+  // cancel (sum of O(tau / N) terms -> a small total): double, like the loss
+  float gw0x_own = 0.f, gw0y_own = 0.f, gwo_own = 0.f;
+  double gbo = 0.0;
   double acc_v = 0.0, acc_b = 0.0, acc_s = 0.0, acc_eg = 0.0;
   int bad = 0;
 
@@ -467,7 +473,7 @@ VPG_SF_PRAGMA_UNROLL(VPG_SF_ROLL)
         yb[0][r] = a.sscale * d;
       }
     }
-    if (t == 0) gbo += yb[0][0] + yb[0][1];
+    if (t == 0) gbo += (double)yb[0][0] + (double)yb[0][1];
 
     // ================= reverse, order 2 (network.hpp:287-372) =================
     // output layer: w_out gradient, Zbar_{D-1} = w_out (x) Ybar, and Abar of
@@ -702,10 +708,8 @@ VPG_SF_PRAGMA_UNROLL(VPG_SF_ROLL)
     for (int l = 0; l < D; ++l)
       if (u_own < net.out_w[l]) gv[net.b_off[l] + u_own] = gb_own[l];
     if (u_own < net.in_w[D]) gv[net.w_off[D] + u_own] = gwo_own;
-    float gbo_w = gbo;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) gbo_w += __shfl_xor_sync(0xffffffffu, gbo_w, o);
-    if (lane == 0) gv[net.b_off[D]] = gbo_w;
+    const double gbo_w = sf::warp_sum_d(gbo);
+    if (lane == 0) gv[net.b_off[D]] = (float)gbo_w;
     if constexpr (D >= 2) {
 #pragma unroll
       for (int l = 1; l < D; ++l) {
