@@ -225,3 +225,24 @@ def test_strong_alternate_kernels_match_oracle(name, mode):
         assert err < max(1e-5, 4.0 * e32), (err, e32)
     finally:
         _capi.check(L.vpinn_gpu_set_test_hooks(0))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("layers", [(2, 30, 1), (2, 17, 7, 8, 9, 1), (2, 32, 32, 1)])
+def test_strong_training_on_the_mma_sync_step_matches_oracle(layers):
+    """train() through the mma.sync strong-form step (1 or 4 hidden layers,
+    width 32): every epoch runs (the epoch tail reads the trainer state it
+    updates; a step kernel that released the tail before its own wait once
+    let it read a stale step count and skip epochs) and the history follows
+    the oracle's."""
+    spec = strong_spec(mesh=(6, 5), n_test_1d=2, n_quad_1d=6, layers=layers, bx=0.3, n_boundary=80)
+    ob, g, p0 = make_strong_pair(spec)
+    assert "sf_step_kernel<" in g.step_kernel(), g.step_kernel()
+    ref = ob.train(p0, 12, lr0=1e-3, log_every=1)["every_step"][:, 0]
+    ref64 = po.OracleProblem(spec, double=True).train(p0.astype(np.float64), 12, lr0=1e-3,
+                                                       log_every=1)["every_step"][:, 0]
+    rep = g.train(12, lr0=1e-3)
+    assert rep.steps_run == 12
+    r = np.abs(rep.records["total"] - ref) / np.abs(ref)
+    floor = np.abs(ref64 - ref) / np.abs(ref)
+    assert r.max() < max(1e-5, 2.0 * floor.max()), (r.max(), floor.max())
