@@ -387,16 +387,20 @@ __global__ void __launch_bounds__(kRAThreads) reduce_adam_peer_kernel(const floa
                                                                         unsigned* ticket, float* bk, const AdamArgs a,
                                                                         const PeerArgs pa, int adam,
                                                                         const int* stop_flag) {
+  // the grid is at most what the device holds at once (every CTA waits in
+  // phase 2 for flags the last CTA of phase 1 sets): warps stride over rows
   pdl_trigger();
   __shared__ int last, s_stopped;
   __shared__ long long s_t;
   __shared__ unsigned long long s_seq;
+  __shared__ PeerMailbox* s_box[kMaxRanks];
   PeerMailbox* mine = pa.box[pa.rank];
   if (threadIdx.x == 0) {
     s_stopped = stop_flag != nullptr ? *stop_flag : 0;
     s_t = a.st->step + 1;
     s_seq = mine->seq + 1;
   }
+  if (threadIdx.x < kMaxRanks) s_box[threadIdx.x] = pa.box[threadIdx.x];
   __syncthreads();
   pdl_wait();
   if (s_stopped) return;
@@ -405,17 +409,12 @@ __global__ void __launch_bounds__(kRAThreads) reduce_adam_peer_kernel(const floa
   const int set = (int)(seq & 1ull);
   const int rows = n_params + kLpWords;
   const int lane = threadIdx.x & 31;
-  const int gw = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int nw = blockDim.x >> 5, gstride = gridDim.x * nw;
+  const int w0 = blockIdx.x * nw + (int)(threadIdx.x >> 5);
   // ---- phase 1: this rank's rows into every rank's mailbox ----
-  float p0 = 0.f, m0 = 0.f, v0 = 0.f;
-  if (gw < rows) {
-    if (adam && gw < n_params && lane == 0) {  // in flight with the partial loads
-      p0 = a.params[gw];
-      m0 = a.m[gw];
-      v0 = a.v[gw];
-    }
+  for (int gw = w0; gw < rows; gw += gstride) {
     const double v = reduce_row(gw, grad_part, n_rows, stride, n_params, loss_part, n_loss_rows, red);
-    if (lane < pa.world) mbox_slot(pa.box[lane], set, pa.rank, rows)[gw] = v;
+    if (lane < pa.world) mbox_slot(s_box[lane], set, pa.rank, rows)[gw] = v;
   }
   __threadfence_system();
   __syncthreads();
@@ -424,7 +423,7 @@ __global__ void __launch_bounds__(kRAThreads) reduce_adam_peer_kernel(const floa
   if (last) {
     if (threadIdx.x == 0) ticket[0] = 0u;
     __threadfence_system();
-    if (threadIdx.x < pa.world) st_release_sys_u64(&pa.box[threadIdx.x]->flag[set][pa.rank], seq);
+    if (threadIdx.x < pa.world) st_release_sys_u64(&s_box[threadIdx.x]->flag[set][pa.rank], seq);
   }
   // ---- phase 2: the rank sum (fixed rank order) and the update ----
   if (threadIdx.x == 0) {
@@ -443,22 +442,25 @@ __global__ void __launch_bounds__(kRAThreads) reduce_adam_peer_kernel(const floa
     for (int r = 0; r < pa.world; ++r) s += __ldcv(&mbox_slot(mine, set, r, rows)[row]);
     return s;
   };
-  if (gw < rows && lane == 0) {
-    const double total = rank_sum(gw);
-    red[gw] = total;
-    if (adam && gw < n_params) {
-      double gd = total;
-      if (gw == a.eps_grad_slot) gd += rank_sum(n_params + kLpEpsGrad);
-      const float g = (float)gd;
-      if (!isfinite(g)) atomicOr(&ticket[1], 1u);
-      bk[gw] = p0;
-      bk[n_params + gw] = m0;
-      bk[2 * n_params + gw] = v0;
-      adam_update(g, m0, v0, p0, a.lr_tab ? a.lr_tab[t - 1] : a.lr_const,
-                  a.lr_tab ? a.c1_tab[t - 1] : 1.0f - (float)pow(0.9, (double)t),
-                  a.lr_tab ? a.c2_tab[t - 1] : 1.0f - (float)pow(0.999, (double)t), a.m[gw], a.v[gw], a.params[gw]);
+  const float lr = a.lr_tab ? a.lr_tab[t - 1] : a.lr_const;
+  const float c1 = a.lr_tab ? a.c1_tab[t - 1] : 1.0f - (float)pow(0.9, (double)t);
+  const float c2 = a.lr_tab ? a.c2_tab[t - 1] : 1.0f - (float)pow(0.999, (double)t);
+  if (lane == 0)
+    for (int gw = w0; gw < rows; gw += gstride) {
+      const double total = rank_sum(gw);
+      red[gw] = total;
+      if (adam && gw < n_params) {
+        const float p0 = a.params[gw], m0 = a.m[gw], v0 = a.v[gw];
+        double gd = total;
+        if (gw == a.eps_grad_slot) gd += rank_sum(n_params + kLpEpsGrad);
+        const float g = (float)gd;
+        if (!isfinite(g)) atomicOr(&ticket[1], 1u);
+        bk[gw] = p0;
+        bk[n_params + gw] = m0;
+        bk[2 * n_params + gw] = v0;
+        adam_update(g, m0, v0, p0, lr, c1, c2, a.m[gw], a.v[gw], a.params[gw]);
+      }
     }
-  }
   __threadfence();
   __syncthreads();
   if (threadIdx.x == 0) last = atomicAdd(&ticket[2], 1u) == gridDim.x - 1;

@@ -185,6 +185,7 @@ struct vpinn_gpu_ctx {
   vpg::PeerMailbox* pbox = nullptr;
   vpg::PeerArgs peers{};
   bool peer = false;
+  int grid_peer = 1;
   long long launches = 0;
   DBuf<char> flush;  // L2 flush scratch (bench)
   DBuf<long long> phase_clk;  // VPINN_PHASE_CLOCK diagnostics
@@ -816,7 +817,7 @@ void enqueue_grad(vpinn_gpu_ctx* c, const int* stop, bool with_reduce = true) {
   }
   if (!with_reduce) return;
   if (c->peer) {  // this rank's sum and the cross-rank sum in one kernel
-    launch_k(pdl_enabled() && !c->split, vpg::reduce_adam_peer_kernel, vpg::reduce_adam_grid(c->n_params),
+    launch_k(pdl_enabled() && !c->split, vpg::reduce_adam_peer_kernel, c->grid_peer,
              vpg::kRAThreads, 0, c->stream, c->grad_part.p, c->grad_rows, c->part_stride, c->n_params,
              (const double*)c->loss_part.p, c->loss_rows, c->red.p, c->ticket.p, c->adam_bk.p,
              adam_args(c, false, 0.f, false, 0), c->peers, 0, stop);
@@ -860,7 +861,7 @@ void enqueue_epoch(vpinn_gpu_ctx* c, const vpg::AdamArgs& aa) {
   if (c->peer) {
     // reduce, the cross-rank sum over peer memory and Adam: one kernel
     enqueue_grad(c, &c->st.p->stopped, /*with_reduce=*/false);
-    launch_k(pdl_enabled() && !c->split, vpg::reduce_adam_peer_kernel, vpg::reduce_adam_grid(c->n_params),
+    launch_k(pdl_enabled() && !c->split, vpg::reduce_adam_peer_kernel, c->grid_peer,
              vpg::kRAThreads, 0, c->stream, (const float*)c->grad_part.p, c->grad_rows, c->part_stride, c->n_params,
              (const double*)c->loss_part.p, c->loss_rows, c->red.p, c->ticket.p, c->adam_bk.p, aa, c->peers, 1,
              (const int*)&c->st.p->stopped);
@@ -2057,6 +2058,11 @@ int vpinn_gpu_attach_peers(vpinn_gpu_ctx* c, const void* handles, int nranks, in
     }
     c->peers = pa;
     c->peer = true;
+    // every CTA of the exchange must be resident at once (phase 2 waits for
+    // all of phase 1): the grid is capped at what the device holds
+    int occ = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, vpg::reduce_adam_peer_kernel, vpg::kRAThreads, 0));
+    c->grid_peer = std::max(1, std::min(vpg::reduce_adam_grid(c->n_params), std::max(1, occ) * c->sm_count));
     for (auto& kv : c->graphs) cudaGraphExecDestroy(kv.second);
     c->graphs.clear();
   });

@@ -106,11 +106,12 @@ def test_thousand_step_history_bitwise_identical(case):
 
 
 # ---- the epoch tail over peer memory (vpinn_gpu_attach_peers) ----
-def test_peer_exchange_single_rank_is_bitwise_the_plain_path():
+@pytest.mark.parametrize("layers", [(2, 30, 30, 30, 1), (2, 50, 50, 50, 1)])
+def test_peer_exchange_single_rank_is_bitwise_the_plain_path(layers):
     """world = 1 through the peer kernel (its own mailbox): the rank sum of
     one rank is exact, so loss, gradient, a 50-epoch history and the final
     parameters are the plain path's bits."""
-    spec = c1_spec()
+    spec = c1_spec(layers=layers)
     ob = po.OracleProblem(spec, double=False)
     p0 = ob.init_params().astype(np.float32)
     ga = gpu_from_oracle(ob, spec)
@@ -154,7 +155,7 @@ def _peer_worker(rank, world, spec, epochs, q_out, q_handles, q_in):
         raise
 
 
-@pytest.mark.parametrize("case", ["c1", "gear576", "strong_sensors", "split_path"])
+@pytest.mark.parametrize("case", ["c1", "gear576", "strong_sensors", "split_path", "paper_net"])
 def test_peer_exchange_two_ranks_match_single_rank(case):
     """Two processes (both on device 0, where CUDA IPC maps each other's
     mailbox; on an 8-GPU node the same protocol runs over NVLink), each with
@@ -165,6 +166,9 @@ def test_peer_exchange_two_ranks_match_single_rank(case):
     from tests.test_gpu_parity import gear_spec
     from tests.test_strong_form import strong_spec
     spec = {"c1": c1_spec, "gear576": gear_spec,
+            # 5,301 parameters: more rows than the device holds warps at once
+            # (the exchange's grid is capped, warps stride over the rows)
+            "paper_net": lambda: c1_spec(layers=(2, 50, 50, 50, 1)),
             "split_path": lambda: po.ProblemSpec(*po.structured_mesh(3, 2), n_test_1d=6, n_quad_1d=20,
                                                  forcing="sin4pi_f", boundary_g="sin4pi_u", n_boundary=200,
                                                  layers=(2, 30, 30, 30, 1), seed=42),
