@@ -116,6 +116,20 @@ __device__ __forceinline__ void adam_update(float g, float m0, float v0, float p
   p_out = __fsub_rn(p0, __fdiv_rn(__fmul_rn(lr, mh), __fadd_rn(__fsqrt_rn(vh), 1e-8f)));
 }
 
+// lr and the bias corrections of step t (trainer.hpp:49-52, 73-78): the host
+// tables, or lr_const and (float)(1 - beta^t) in double
+__device__ __forceinline__ void step_factors(const AdamArgs& a, long long t, float& lr, float& c1, float& c2) {
+  if (a.lr_tab) {
+    lr = a.lr_tab[t - 1];
+    c1 = a.c1_tab[t - 1];
+    c2 = a.c2_tab[t - 1];
+  } else {
+    lr = a.lr_const;
+    c1 = 1.0f - (float)pow(0.9, (double)t);
+    c2 = 1.0f - (float)pow(0.999, (double)t);
+  }
+}
+
 // the loss parts in the reference's Real semantics and the train-loop
 // bookkeeping after an update (trainer.hpp:316-370): history record,
 // coefficient-tolerance / plateau / budget stops.  Thread 0.
@@ -268,9 +282,11 @@ __global__ void __launch_bounds__(kRAThreads) reduce_adam_kernel(const float* __
   // split path: no programmatic launch)
   __shared__ int last, s_stopped;
   __shared__ long long s_t;
+  __shared__ float s_f[3];  // lr, c1, c2 of this step: once per CTA, before the wait
   if (threadIdx.x == 0) {
     s_stopped = a.st->stopped;
     s_t = a.st->step + 1;
+    if (!s_stopped) step_factors(a, s_t, s_f[0], s_f[1], s_f[2]);
   }
   __syncthreads();
   pdl_wait();
@@ -278,16 +294,7 @@ __global__ void __launch_bounds__(kRAThreads) reduce_adam_kernel(const float* __
   const long long t = s_t;
   const int lane = threadIdx.x & 31;
   const int gw = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  float lr = 0.f, c1 = 0.f, c2 = 0.f;
-  if (a.lr_tab) {
-    lr = a.lr_tab[t - 1];
-    c1 = a.c1_tab[t - 1];
-    c2 = a.c2_tab[t - 1];
-  } else {
-    lr = a.lr_const;
-    c1 = 1.0f - (float)pow(0.9, (double)t);
-    c2 = 1.0f - (float)pow(0.999, (double)t);
-  }
+  const float lr = s_f[0], c1 = s_f[1], c2 = s_f[2];
   if (gw < n_params + kLpWords) {
     float p0 = 0.f, m0 = 0.f, v0 = 0.f;
     if (gw < n_params && lane == 0) {  // in flight with the partial loads
@@ -393,12 +400,14 @@ __global__ void __launch_bounds__(kRAThreads) reduce_adam_peer_kernel(const floa
   __shared__ int last, s_stopped;
   __shared__ long long s_t;
   __shared__ unsigned long long s_seq;
+  __shared__ float s_f[3];
   __shared__ PeerMailbox* s_box[kMaxRanks];
   PeerMailbox* mine = pa.box[pa.rank];
   if (threadIdx.x == 0) {
     s_stopped = stop_flag != nullptr ? *stop_flag : 0;
     s_t = a.st->step + 1;
     s_seq = mine->seq + 1;
+    if (adam && !s_stopped) step_factors(a, s_t, s_f[0], s_f[1], s_f[2]);
   }
   if (threadIdx.x < kMaxRanks) s_box[threadIdx.x] = pa.box[threadIdx.x];
   __syncthreads();
@@ -442,9 +451,7 @@ __global__ void __launch_bounds__(kRAThreads) reduce_adam_peer_kernel(const floa
     for (int r = 0; r < pa.world; ++r) s += __ldcv(&mbox_slot(mine, set, r, rows)[row]);
     return s;
   };
-  const float lr = a.lr_tab ? a.lr_tab[t - 1] : a.lr_const;
-  const float c1 = a.lr_tab ? a.c1_tab[t - 1] : 1.0f - (float)pow(0.9, (double)t);
-  const float c2 = a.lr_tab ? a.c2_tab[t - 1] : 1.0f - (float)pow(0.999, (double)t);
+  const float lr = s_f[0], c1 = s_f[1], c2 = s_f[2];
   if (lane == 0)
     for (int gw = w0; gw < rows; gw += gstride) {
       const double total = rank_sum(gw);
@@ -492,7 +499,7 @@ __global__ void __launch_bounds__(kRAThreads) reduce_adam_peer_kernel(const floa
       a.st->stop_reason = 3;
       a.st->abort_step = t;
     } else {
-      train_bookkeeping(a, t, a.lr_tab ? a.lr_tab[t - 1] : a.lr_const);
+      train_bookkeeping(a, t, s_f[0]);
     }
   }
 }
