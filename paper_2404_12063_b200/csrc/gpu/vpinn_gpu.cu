@@ -1382,6 +1382,10 @@ int vpinn_gpu_time_steps(vpinn_gpu_ctx* c, int n_steps, double lr, double* ms_to
   });
 }
 
+namespace {
+constexpr long long kGraphMinIters = 256;  // vpinn_gpu_train: shorter first runs launch directly
+}
+
 int vpinn_gpu_train(vpinn_gpu_ctx* c, const vpinn_gpu_train_spec* spec,
                     vpinn_gpu_step_record* records, vpinn_gpu_train_result* result) {
   return guarded([&] {
@@ -1403,38 +1407,56 @@ int vpinn_gpu_train(vpinn_gpu_ctx* c, const vpinn_gpu_train_spec* spec,
       c1[t - 1] = 1.0f - (float)std::pow(0.9, double(t));
       c2[t - 1] = 1.0f - (float)std::pow(0.999, double(t));
     }
-    c->lr_tab.alloc(iters, c->stream);
-    c->c1_tab.alloc(iters, c->stream);
-    c->c2_tab.alloc(iters, c->stream);
+    // the tables and the record buffer keep their device addresses across
+    // calls (capacity grows to a power of two): the captured epoch graphs
+    // stay valid, so a repeated train() does not re-instantiate them
+    if ((long long)c->lr_tab.n < iters) {
+      size_t cap = 64;
+      while ((long long)cap < iters) cap *= 2;
+      c->lr_tab.alloc(cap, c->stream);
+      c->c1_tab.alloc(cap, c->stream);
+      c->c2_tab.alloc(cap, c->stream);
+      c->rec.alloc(cap, c->stream);
+      // tables were reallocated: drop graphs that captured the old pointers
+      for (auto it = c->graphs.begin(); it != c->graphs.end();) {
+        if (std::get<0>(it->first) == 2) {
+          cudaGraphExecDestroy(it->second);
+          it = c->graphs.erase(it);
+        } else {
+          ++it;
+        }
+      }
+    }
     c->lr_tab.upload(lr.data(), iters, c->stream);
     c->c1_tab.upload(c1.data(), iters, c->stream);
     c->c2_tab.upload(c2.data(), iters, c->stream);
-    c->rec.alloc(iters, c->stream);
-    // tables were reallocated: drop graphs that captured the old pointers
-    for (auto it = c->graphs.begin(); it != c->graphs.end();) {
-      if (std::get<0>(it->first) == 2) {
-        cudaGraphExecDestroy(it->second);
-        it = c->graphs.erase(it);
-      } else {
-        ++it;
-      }
-    }
     reset_state(c, iters, spec);
     const int S = spec->steps_per_graph > 0 ? spec->steps_per_graph : 50;
     const int per = (int)std::min<long long>(S, iters);
-    cudaGraphExec_t g = graph_for(c, 2, per, 0.0, true, (int)iters);
-    long long launched = 0;
-    int since_check = 0;
-    while (launched < iters) {
-      CK(cudaGraphLaunch(g, c->stream));
-      c->launches += launches_per_epoch(c) * per;
-      launched += per;
-      if (++since_check >= 20 && launched < iters) {
-        since_check = 0;
-        CK(cudaMemcpyAsync(c->h_flag, &c->st.p->stopped, sizeof(int), cudaMemcpyDeviceToHost,
-                           c->stream));
-        CK(cudaStreamSynchronize(c->stream));
-        if (*c->h_flag) break;
+    // a short run on a context without the captured epoch graph launches its
+    // epochs directly (programmatic launches, the same kernels and
+    // arguments): instantiating the graph costs more than the launches of a
+    // few tens of epochs; longer runs capture once and replay
+    const bool direct = spec->steps_per_graph <= 0 && iters < kGraphMinIters &&
+                        c->graphs.find(std::make_tuple(2, per, 0.0)) == c->graphs.end();
+    if (direct) {
+      const vpg::AdamArgs aa = adam_args(c, true, 0.0f, true, (int)c->rec.n);
+      for (long long t = 0; t < iters; ++t) enqueue_epoch(c, aa);
+    } else {
+      cudaGraphExec_t g = graph_for(c, 2, per, 0.0, true, (int)c->rec.n);
+      long long launched = 0;
+      int since_check = 0;
+      while (launched < iters) {
+        CK(cudaGraphLaunch(g, c->stream));
+        c->launches += launches_per_epoch(c) * per;
+        launched += per;
+        if (++since_check >= 20 && launched < iters) {
+          since_check = 0;
+          CK(cudaMemcpyAsync(c->h_flag, &c->st.p->stopped, sizeof(int), cudaMemcpyDeviceToHost,
+                             c->stream));
+          CK(cudaStreamSynchronize(c->stream));
+          if (*c->h_flag) break;
+        }
       }
     }
     vpg::TrainState s;
