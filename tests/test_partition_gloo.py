@@ -85,3 +85,67 @@ def test_partition_edge_cases():
             cover.append((e0, e1))
         assert cover[0][0] == 0 and cover[-1][1] == 5
         assert all(a[1] == b[0] for a, b in zip(cover, cover[1:]))
+
+
+# ---- bench.attach_ranks: the cross-rank attachment at N > 1 (host plumbing) ----
+class _FakeCtx:
+    """Stands in for GpuStep: records which attachment the rank made."""
+
+    def __init__(self, rank, fail_handle=False, fail_attach=False):
+        self.rank, self.fail_handle, self.fail_attach = rank, fail_handle, fail_attach
+        self.peers = None
+        self.comm = None
+
+    def peer_handle(self):
+        if self.fail_handle:
+            raise RuntimeError("no IPC")
+        return bytes([self.rank]) * 64
+
+    def attach_peers(self, handles, world, rank):
+        if self.fail_attach:
+            raise RuntimeError("cannot map a peer")
+        self.peers = list(handles)
+
+    def attach_comm(self, uid, world, rank):
+        self.comm = uid
+
+
+def _attach_worker(rank, world, port, out_q, fail_rank, mode):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import bench
+    import paper_2404_12063_b200.gpu as G
+    G.nccl_unique_id = lambda: b"U" * 128  # no NCCL on the CPU box: the fallback's id only
+    g = _FakeCtx(rank, fail_handle=(mode == "handle" and rank == fail_rank),
+                 fail_attach=(mode == "attach" and rank == fail_rank))
+    bench.attach_ranks(g, dist, world, rank)
+    out_q.put((rank, g.peers is not None, g.comm is not None, g.peers))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("mode", ["ok", "handle", "attach"])
+def test_attach_ranks_agrees_on_one_collective(mode):
+    """Every rank gathers the peer handles in rank order and attaches them;
+    when any rank cannot export or map (mode handle / attach on rank 1) all
+    ranks take NCCL together -- a rank that failed still joins the gather, so
+    nobody blocks."""
+    world = 3
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_attach_worker, args=(r, world, port, q, 1, mode)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict((r[0], r[1:]) for r in (q.get(timeout=120) for _ in procs))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    if mode == "ok":
+        for r in range(world):
+            assert res[r][0] and not res[r][1]
+            assert res[r][2] == [bytes([i]) * 64 for i in range(world)]
+    else:
+        for r in range(world):
+            assert res[r][1], (mode, r, res[r])  # NCCL attached on every rank
