@@ -1437,7 +1437,10 @@ int vpinn_gpu_train(vpinn_gpu_ctx* c, const vpinn_gpu_train_spec* spec,
     // epochs directly (programmatic launches, the same kernels and
     // arguments): instantiating the graph costs more than the launches of a
     // few tens of epochs; longer runs capture once and replay
-    const bool direct = spec->steps_per_graph <= 0 && iters < kGraphMinIters &&
+    // (two kernels per epoch with programmatic launch; the split path's
+    // five-plus launches per epoch keep the graph: their launch gaps cost
+    // ~10 us an epoch)
+    const bool direct = spec->steps_per_graph <= 0 && iters < kGraphMinIters && !c->split &&
                         c->graphs.find(std::make_tuple(2, per, 0.0)) == c->graphs.end();
     if (direct) {
       const vpg::AdamArgs aa = adam_args(c, true, 0.0f, true, (int)c->rec.n);
