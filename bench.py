@@ -383,7 +383,12 @@ def main():
     # (the timed context is released first: a user re-creating contexts gets
     # its device blocks from the library's block cache, as the e2e does here)
     step.close()
-    e2e = _e2e(hp, device, rank, world, pg, args.steps)
+    # the end-to-end call chain three times (fresh contexts each), the median
+    # reported: the first run in a process also pays one-time allocations
+    e2e_runs = [_e2e(hp, device, rank, world, pg, args.steps) for _ in range(3)]
+    e2e = sorted(e2e_runs, key=lambda r: r["seconds"])[1]
+    e2e["runs_seconds"] = [r["seconds"] for r in e2e_runs]
+    e2e["statistic"] = "median of 3 runs, each a fresh context
     e2e_mesh = _e2e_from_mesh(mesh, device, rank, world, pg, args.steps)
     mf = _aux(_matrix_free, mesh, device, rank, world) if rank == 0 else None
     strong = _strong_form(mesh, device, rank, world, pg, args.steps, ms_per_step,
