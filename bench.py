@@ -388,7 +388,7 @@ def main():
     e2e_runs = [_e2e(hp, device, rank, world, pg, args.steps) for _ in range(3)]
     e2e = sorted(e2e_runs, key=lambda r: r["seconds"])[1]
     e2e["runs_seconds"] = [r["seconds"] for r in e2e_runs]
-    e2e["statistic"] = "median of 3 runs, each a fresh context
+    e2e["statistic"] = "median of 3 runs, each a fresh context"
     e2e_mesh = _e2e_from_mesh(mesh, device, rank, world, pg, args.steps)
     mf = _aux(_matrix_free, mesh, device, rank, world) if rank == 0 else None
     strong = _strong_form(mesh, device, rank, world, pg, args.steps, ms_per_step,
