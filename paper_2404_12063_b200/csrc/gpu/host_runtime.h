@@ -221,8 +221,18 @@ Stager& stager() {
   static Stager* st = new Stager;
   return *st;
 }
+// page-locked host memory (cudaHostAlloc / cudaHostRegister by the caller):
+// the DMA reads it directly, no staging copy
+bool host_pinned(const void* p) {
+  cudaPointerAttributes at{};
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return at.type == cudaMemoryTypeHost;
+}
 void upload_bytes(void* dst, const void* src, size_t bytes, cudaStream_t s) {
-  if (bytes >= (size_t(4) << 20) && stager().upload(dst, src, bytes, s)) return;
+  if (bytes >= (size_t(4) << 20) && !host_pinned(src) && stager().upload(dst, src, bytes, s)) return;
   CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s));
 }
 

@@ -30,6 +30,29 @@ class TrainReport:
     final_eps: float
 
 
+def pin_problem(pb: "_capi.Problem"):
+    """A copy of a filled vpinn_gpu_problem whose premultiplier tensors,
+    forcing, points and strong-form forcing live in page-locked host memory
+    (the caller's pinned input buffers): vpinn_gpu_create then DMAs them
+    straight from there instead of staging them.  Returns (problem, keepalive)."""
+    import torch
+    out = _capi.Problem()
+    C.pointer(out)[0] = pb
+    E, T, Q = pb.n_elem, pb.n_test, pb.n_quad
+    n_pts = pb.n_interior + pb.n_boundary + pb.n_sensors
+    keep = []
+    for name, nbytes in (("grad_x", 4 * E * T * Q), ("grad_y", 4 * E * T * Q), ("test", 4 * E * T * Q),
+                         ("forcing", 4 * E * T), ("points", 16 * n_pts), ("strong_forcing", 4 * pb.n_interior)):
+        src = getattr(pb, name)
+        if not src:
+            continue
+        buf = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
+        C.memmove(buf.data_ptr(), src, nbytes)
+        keep.append(buf)
+        setattr(out, name, buf.data_ptr())
+    return out, keep
+
+
 class GpuStep:
     """One device context: the uploaded ProblemAssembly + network parameters."""
 

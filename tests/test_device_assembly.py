@@ -170,3 +170,30 @@ def test_matrix_free_contraction_needs_the_geometry():
     with pytest.raises(_capi.VpinnError) as e:
         g.contract_matrix_free(np.zeros(ni), np.zeros(ni))
     assert e.value.code == 2
+
+
+def test_pinned_input_upload_is_bit_identical():
+    """vpinn_gpu_create DMAs page-locked caller arrays directly (no staging
+    ring): the uploaded bytes, the loss / gradient and a 10-epoch history are
+    identical to the staged upload of the same pageable arrays.  The gear is
+    large enough (3 x 9.4 MB tensors) that both go through the chunked path."""
+    from paper_2404_12063_b200 import gpu as G
+    cfg = GEAR_CFG
+    hp = host.HostProblem(cfg, mesh=host.Mesh.gear(8, 470))
+    E, T, Q = hp.E, hp.T, hp.Q
+    assert 4 * E * T * Q >= 4 << 20
+    pv, keep = G.pin_problem(hp.view(0))
+    g_page = G.GpuStep.from_problem(hp.view(0), keepalive=hp)
+    g_pin = G.GpuStep.from_problem(pv, keepalive=(hp, keep))
+    for which, n in ((0, E * T * Q), (1, E * T * Q), (2, E * T * Q), (3, E * T)):
+        a, b = g_page.download_tensor(which, n), g_pin.download_tensor(which, n)
+        assert a.tobytes() == b.tobytes(), (which, int(np.sum(a != b)))
+    p0 = hp.init_params()
+    for g in (g_page, g_pin):
+        g.set_params(p0)
+    la, ga = g_page.loss_and_grad()
+    lb, gb = g_pin.loss_and_grad()
+    assert np.array_equal(la, lb) and np.array_equal(ga, gb)
+    ra, rb = g_page.train(10), g_pin.train(10)
+    assert np.array_equal(ra.records["total"], rb.records["total"])
+    assert np.array_equal(g_page.get_params(), g_pin.get_params())

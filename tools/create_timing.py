@@ -1,5 +1,6 @@
 """Phase times of vpinn_gpu_create for the bench gear (host arrays path),
-repeated: VPINN_CREATE_TIMING=1 python tools/create_timing.py"""
+repeated, from pageable and from page-locked inputs:
+VPINN_CREATE_TIMING=1 python tools/create_timing.py"""
 import os
 import sys
 import time
@@ -10,12 +11,14 @@ from paper_2404_12063_b200 import gpu as G, host  # noqa: E402
 
 mesh = host.Mesh.gear(bench.GEAR_NR, bench.GEAR_NT)
 hp = host.HostProblem(bench.GEAR_CFG, mesh=mesh)
-for rep in range(4):
+pv, keep = G.pin_problem(hp.view(0))
+for rep in range(8):
+    pinned = rep % 2 == 1
     t0 = time.perf_counter()
-    g = G.GpuStep.from_problem(hp.view(0), keepalive=hp)
+    g = G.GpuStep.from_problem(pv if pinned else hp.view(0), keepalive=hp)
     t1 = time.perf_counter()
     g.set_params(hp.init_params())
     g.train(50)
     t2 = time.perf_counter()
     g.close()
-    print(f"rep {rep}: create {1e3*(t1-t0):.2f} ms, train(50) {1e3*(t2-t1):.2f} ms", file=sys.stderr, flush=True)
+    print(f"rep {rep} {'pinned' if pinned else 'pageable'}: create {1e3*(t1-t0):.2f} ms, train(50) {1e3*(t2-t1):.2f} ms", file=sys.stderr, flush=True)
