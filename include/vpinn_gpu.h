@@ -181,6 +181,11 @@ int vpinn_gpu_device_ok(void);
 void vpinn_gpu_partition(int64_t n_elem, int64_t n_boundary, int64_t n_sensors, int rank, int world,
                          int64_t* out6);
 
+/* Uploads this rank's share of the problem's host arrays.  Arrays in
+ * page-locked memory (cudaHostAlloc / cudaHostRegister) are DMA'd straight
+ * from the caller's buffers at the link rate; pageable arrays of 4 MB or more
+ * are staged through a process-wide pinned ring filled by a host thread pool.
+ * The arrays are not referenced after the call returns. */
 int vpinn_gpu_create(const vpinn_gpu_problem* problem, vpinn_gpu_ctx** out);
 void vpinn_gpu_destroy(vpinn_gpu_ctx* ctx);
 
