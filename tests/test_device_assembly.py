@@ -197,3 +197,11 @@ def test_pinned_input_upload_is_bit_identical():
     ra, rb = g_page.train(10), g_pin.train(10)
     assert np.array_equal(ra.records["total"], rb.records["total"])
     assert np.array_equal(g_page.get_params(), g_pin.get_params())
+    # rank 1 of 2: the upload starts inside the page-locked allocation
+    pv1, keep1 = G.pin_problem(hp.view(0, 1, 2))
+    r_page = G.GpuStep.from_problem(hp.view(0, 1, 2), keepalive=hp)
+    r_pin = G.GpuStep.from_problem(pv1, keepalive=(hp, keep1))
+    e0, e1 = _capi.partition(E, hp.n_bnd, hp.n_sen, 1, 2)[:2]
+    n = (e1 - e0) * T * Q
+    for which in (0, 1, 2):
+        assert r_page.download_tensor(which, n).tobytes() == r_pin.download_tensor(which, n).tobytes()
