@@ -391,9 +391,12 @@ def main():
         r["runs_seconds"] = [x["seconds"] for x in runs]
         r["statistic"] = "median of 3 runs, each a fresh context"
         return r
-    e2e = _median_e2e(True)
+    e2e_arrays = _median_e2e(True)
     e2e_pageable = _median_e2e(False)
-    e2e_mesh = _e2e_from_mesh(mesh, device, rank, world, pg, args.steps)
+    mesh_runs = [_e2e_from_mesh(mesh, device, rank, world, pg, args.steps) for _ in range(3)]
+    e2e = sorted(mesh_runs, key=lambda r: r["seconds"])[1]
+    e2e["runs_seconds"] = [x["seconds"] for x in mesh_runs]
+    e2e["statistic"] = "median of 3 runs, each a fresh problem build and context"
     mf = _aux(_matrix_free, mesh, device, rank, world) if rank == 0 else None
     strong = _strong_form(mesh, device, rank, world, pg, args.steps, ms_per_step,
                           cpu=rank == 0 and world == 1 and not args.no_cpu_baseline)
@@ -449,8 +452,8 @@ def main():
     line.update({
         "kernel_ms": {"fused_step": ms_mlp, "reduce": ms_red, "adam": ms_adam},
         "e2e": e2e,
+        "e2e_host_arrays": e2e_arrays,
         "e2e_pageable": e2e_pageable,
-        "e2e_from_mesh": e2e_mesh,
         "contraction_matrix_free": mf,
         "strong_form": strong,
         "cpu_baseline": cpu,
@@ -575,11 +578,16 @@ def _e2e(hp, device, rank, world, pg, steps, pinned=True):
 
 
 def _e2e_from_mesh(mesh, device, rank, world, pg, steps):
-    """Config + mesh -> trained parameters with the premultipliers assembled
-    on the device: host side builds only the rule, the
-    basis tables, the boundary samples and the initial network; the timed
-    region also covers the problem build, which the drop-in e2e leaves to
-    the caller.  Beside it, the same build with the host assembly."""
+    """The headline e2e: config + mesh in host memory -> trained parameters
+    on the host, through the public API (HostProblem(device_assembly) ->
+    vpinn_gpu_create with the assembly input -> train(K) -> get_params).
+    The timed region covers the host problem build (config, rule and basis
+    tables, boundary samples, Glorot init), the H2D copies of the mesh,
+    tables, penalty points and parameters, the device assembly of the
+    premultipliers (bit-identical to the host assembly:
+    tests/test_device_assembly.py), K epochs and the D2H of the result.
+    Beside it (e2e_host_arrays) the drop-in call with the host-assembled
+    113 MB of premultipliers uploaded from page-locked memory."""
     from paper_2404_12063_b200 import gpu as G, host
     barrier(pg)
     t0 = time.perf_counter()
@@ -587,17 +595,23 @@ def _e2e_from_mesh(mesh, device, rank, world, pg, steps):
     g = G.GpuStep.from_problem(dp.view(device, rank, world), keepalive=dp)
     g.set_params(dp.init_params())
     attach_ranks(g, pg, world, rank)
-    g.train(steps, lr0=1e-3)
-    g.get_params()
+    rep = g.train(steps, lr0=1e-3)
+    params = g.get_params()
     t1 = time.perf_counter()
     g.close()
     dt = allmax(pg, t1 - t0)
-    t2 = time.perf_counter()
-    host.HostProblem(GEAR_CFG, mesh=mesh)
-    host_build = allmax(pg, time.perf_counter() - t2)
-    return {"value": dp.E * dp.Q * steps / dt, "unit": UNIT, "seconds": dt,
-            "host_assembly_build_seconds": host_build,
-            "path": "HostProblem(device_assembly) + vpinn_gpu_create(assembly input) + train(K) + get_params"}
+    E, T, Q = dp.E, dp.T, dp.Q
+    e_local = E // world if world > 1 else E
+    # nodes (double2), cell node ids (int4), rule (3 Q doubles), basis tables
+    # (3 T Q doubles), penalty points (double2) and targets, parameters
+    h2d = (16 * mesh.n_nodes + 16 * e_local + 8 * 3 * Q + 8 * 3 * T * Q
+           + 24 * (dp.n_bnd + dp.n_sen) + 4 * dp.n_params)
+    d2h = 4 * params.size + 7 * 8 * rep.steps_run
+    return {"value": E * Q * steps / dt, "unit": UNIT, "h2d_bytes_per_step": int(h2d / steps),
+            "d2h_bytes_per_step": int(d2h / steps), "seconds": dt,
+            "inputs": "config + mesh (nodes, cells) in host memory",
+            "path": "HostProblem(config, mesh, device_assembly) + vpinn_gpu_create(assembly input) + "
+                    "vpinn_gpu_train(K) + vpinn_gpu_get_params"}
 
 
 def _matrix_free(mesh, device, rank, world):

@@ -126,6 +126,25 @@ __device__ __forceinline__ float f16hi(uint32_t w) {
   asm("{\n .reg .b16 lo, hi;\n mov.b32 {lo, hi}, %1;\n cvt.f32.f16 %0, hi;\n}" : "=f"(f) : "r"(w));
   return f;
 }
+// y - h for both halves of a packed pair: one mixed-precision FMA per value
+// (fma.rn.f32.f16, y + h * -1: a single FHFMA reading the half in place, no
+// f16 -> f32 unpack); exact, since y - h is representable in fp32
+__device__ __forceinline__ float2 rem_f16x2(uint32_t h, float2 y) {
+  float2 r;
+  asm("{\n .reg .b16 lo, hi, m1;\n mov.b16 m1, 0xBC00;\n mov.b32 {lo, hi}, %2;\n"
+      " fma.rn.f32.f16 %0, lo, m1, %3;\n fma.rn.f32.f16 %1, hi, m1, %4;\n}"
+      : "=f"(r.x), "=f"(r.y) : "r"(h), "f"(y.x), "f"(y.y));
+  return r;
+}
+// h + l of a packed pair in fp32 (round to nearest, as float(h) + float(l)):
+// the l halves unpacked, then one mixed-precision add each reading h in place
+__device__ __forceinline__ float2 join_f16x2(uint32_t h, uint32_t l) {
+  float2 v;
+  asm("{\n .reg .b16 hl, hh, ll, lh;\n .reg .f32 t0, t1;\n mov.b32 {hl, hh}, %2;\n mov.b32 {ll, lh}, %3;\n"
+      " cvt.f32.f16 t0, ll;\n cvt.f32.f16 t1, lh;\n add.rn.f32.f16 %0, hl, t0;\n add.rn.f32.f16 %1, hh, t1;\n}"
+      : "=f"(v.x), "=f"(v.y) : "r"(h), "r"(l));
+  return v;
+}
 // store 8 consecutive columns [8 chunk, +8) of one row, scaled by s, into
 // the two part tiles at base (h) and base + part_stride (l)
 __device__ __forceinline__ void st_split8_h(char* base, uint32_t part_stride, int row, int chunk, const float* v,
@@ -135,7 +154,8 @@ __device__ __forceinline__ void st_split8_h(char* base, uint32_t part_stride, in
   for (int k = 0; k < 4; ++k) {
     const float y0 = v[2 * k] * s, y1 = v[2 * k + 1] * s;
     h[k] = pack_f16x2(y0, y1);
-    l[k] = pack_f16x2(y0 - f16lo(h[k]), y1 - f16hi(h[k]));
+    const float2 r = rem_f16x2(h[k], make_float2(y0, y1));
+    l[k] = pack_f16x2(r.x, r.y);
   }
   const uint32_t off = sw_chunk(row, chunk);
   *reinterpret_cast<uint4*>(base + off) = make_uint4(h[0], h[1], h[2], h[3]);
@@ -151,7 +171,7 @@ __device__ __forceinline__ void st_split8_ho(char* base, uint32_t part_stride, u
     const float2 y = SCALE ? __fmul2_rn(make_float2(v[2 * k], v[2 * k + 1]), make_float2(s, s))
                            : make_float2(v[2 * k], v[2 * k + 1]);
     h[k] = pack_f16x2(y.x, y.y);
-    const float2 r = __fadd2_rn(y, make_float2(-f16lo(h[k]), -f16hi(h[k])));
+    const float2 r = rem_f16x2(h[k], y);
     l[k] = pack_f16x2(r.x, r.y);
   }
   *reinterpret_cast<uint4*>(base + off) = make_uint4(h[0], h[1], h[2], h[3]);
@@ -165,7 +185,7 @@ __device__ __forceinline__ void ld_join8_ho(const char* base, uint32_t part_stri
   const uint32_t hw[4] = {h.x, h.y, h.z, h.w}, lw[4] = {l.x, l.y, l.z, l.w};
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
-    float2 a = __fadd2_rn(make_float2(f16lo(hw[k]), f16hi(hw[k])), make_float2(f16lo(lw[k]), f16hi(lw[k])));
+    float2 a = join_f16x2(hw[k], lw[k]);
     if (UNSCALE) a = __fmul2_rn(a, make_float2(inv_s, inv_s));
     v[2 * k] = a.x;
     v[2 * k + 1] = a.y;
@@ -180,8 +200,9 @@ __device__ __forceinline__ void ld_join8_h(const char* base, uint32_t part_strid
   const uint32_t hw[4] = {h.x, h.y, h.z, h.w}, lw[4] = {l.x, l.y, l.z, l.w};
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
-    v[2 * k] = (f16lo(hw[k]) + f16lo(lw[k])) * inv_s;
-    v[2 * k + 1] = (f16hi(hw[k]) + f16hi(lw[k])) * inv_s;
+    const float2 a = join_f16x2(hw[k], lw[k]);
+    v[2 * k] = a.x * inv_s;
+    v[2 * k + 1] = a.y * inv_s;
   }
 }
 // 2^k as a float, k clamped to the normal range

@@ -45,15 +45,49 @@ inline Mesh generate_structured_mesh(int nx, int ny, std::pair<double, double> x
   return m;
 }
 
-// edges incident to exactly one cell, ordered by (min id, max id)
+// edges incident to exactly one cell, ordered by (min id, max id) -- the
+// order of the reference's std::map walk.  Edges are bucketed by their min
+// id (counting sort), each bucket's max ids sorted; a run of length one is a
+// boundary edge.  O(cells) instead of a 4-cells-node tree (gear: 5.4 ms ->
+// ~0.3 ms, the largest part of a device-assembly problem build).
 inline std::vector<std::pair<int, int>> boundary_edges(const Mesh& m) {
+  int lo = 0, hi = -1;
+  for (const auto& e : m.elements)
+    for (int i = 0; i < 4; ++i) {
+      lo = std::min(lo, e[i]);
+      hi = std::max(hi, e[i]);
+    }
+  std::vector<std::pair<int, int>> out;
+  if (lo >= 0) {
+    std::vector<int> start(static_cast<size_t>(hi) + 2, 0);
+    for (const auto& e : m.elements)
+      for (int i = 0; i < 4; ++i) ++start[std::min(e[i], e[(i + 1) & 3]) + 1];
+    for (size_t a = 1; a < start.size(); ++a) start[a] += start[a - 1];
+    std::vector<int> fill(start.begin(), start.end() - 1), nb(static_cast<size_t>(start.back()));
+    for (const auto& e : m.elements)
+      for (int i = 0; i < 4; ++i) {
+        const int a = e[i], b = e[(i + 1) & 3];
+        nb[fill[std::min(a, b)]++] = std::max(a, b);
+      }
+    for (int a = 0; a <= hi; ++a) {
+      const auto first = nb.begin() + start[a], last = nb.begin() + start[a + 1];
+      std::sort(first, last);
+      for (auto it = first; it != last;) {
+        auto run = it + 1;
+        while (run != last && *run == *it) ++run;
+        if (run - it == 1) out.emplace_back(a, *it);
+        it = run;
+      }
+    }
+    return out;
+  }
+  // negative ids (a malformed mesh the validators report later): the tree walk
   std::map<std::pair<int, int>, int> count;
   for (const auto& e : m.elements)
     for (int i = 0; i < 4; ++i) {
       const int a = e[i], b = e[(i + 1) & 3];
       count[{std::min(a, b), std::max(a, b)}] += 1;
     }
-  std::vector<std::pair<int, int>> out;
   for (const auto& [edge, n] : count)
     if (n == 1) out.push_back(edge);
   return out;
