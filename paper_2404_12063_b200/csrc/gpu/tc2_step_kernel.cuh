@@ -146,8 +146,8 @@ struct Lay {
   static constexpr int OFF_SMALL = OFF_B + CF::kBuf;
   static constexpr int EX_ROWS = kRows + 3 * (CF::NG - 2);
   // small region, in floats
-  static constexpr int S_W0 = 0;                       // [HP][4] (w_x, w_y, b, 0)
-  static constexpr int S_W0S = S_W0 + 4 * HP;          // [HP][2] (w_x, w_y) * 2^kXt of X_1
+  static constexpr int S_W0 = 0;                       // [HP/2][4][2] unit pairs: (w_x, w_y, b, 0) x (k, k+1)
+  static constexpr int S_W0S = S_W0 + 4 * HP;          // [HP/2][2][2] (w_x, w_y) x (k, k+1), * 2^kXt of X_1
   static constexpr int S_BIAS = S_W0S + 2 * HP;        // [2][HP]
   // output weights: channel 0 [HP], biases at HP, HP + 1; channel 1 at HP + 8
   static constexpr int S_WD = S_BIAS + 2 * HP;
@@ -345,6 +345,8 @@ __global__ void __maxnreg__((t2::Cfg<H, UPT>::kMaxReg)) tc2_step_kernel(const St
   float* sf = reinterpret_cast<float*>(sm + LY::OFF_SMALL);
   float* sW0 = sf + LY::S_W0;
   float* sW0s = sf + LY::S_W0S;
+  // field f (0 w_x, 1 w_y, 2 b, 3 pad) of hidden-1 unit i in sW0
+  auto w0_at = [](int i, int f) { return 8 * (i >> 1) + 2 * f + (i & 1); };
   float* sBias = sf + LY::S_BIAS;
   float* sWd = sf + LY::S_WD;
   float* sWd2 = sWd + HP + 8;  // output channel 1 (C == 2)
@@ -418,10 +420,12 @@ __global__ void __maxnreg__((t2::Cfg<H, UPT>::kMaxReg)) tc2_step_kernel(const St
       b = P[net.b_off[0] + i];
     }
     if (i < net.in_w[D]) wd = P[net.w_off[D] + i];
-    sW0[4 * i] = w0;
-    sW0[4 * i + 1] = w1;
-    sW0[4 * i + 2] = b;
-    sW0[4 * i + 3] = 0.f;
+    // unit pairs (k, k+1) adjacent per field: packed fp32x2 operands load
+    // as register pairs (no moves to assemble them)
+    sW0[w0_at(i, 0)] = w0;
+    sW0[w0_at(i, 1)] = w1;
+    sW0[w0_at(i, 2)] = b;
+    sW0[w0_at(i, 3)] = 0.f;
     sWd[i] = wd;
     if constexpr (C == 2) sWd2[i] = i < net.in_w[D] ? P[net.w_off[D] + net.in_w[D] + i] : 0.f;
   }
@@ -461,8 +465,8 @@ __global__ void __maxnreg__((t2::Cfg<H, UPT>::kMaxReg)) tc2_step_kernel(const St
   // weight norms (bounds for the scales): max |w0x|, |w0y|, |wd|; per MMA
   // layer max row abs-sum R and max column abs-sum C, each sum in index order
   if (tid < H) {
-    atomic_max_abs(&sNorm[0], sW0[4 * tid]);
-    atomic_max_abs(&sNorm[1], sW0[4 * tid + 1]);
+    atomic_max_abs(&sNorm[0], sW0[w0_at(tid, 0)]);
+    atomic_max_abs(&sNorm[1], sW0[w0_at(tid, 1)]);
     atomic_max_abs(&sNorm[2], sWd[tid]);
     if constexpr (C == 2) atomic_max_abs(&sMax[kNWd2], sWd2[tid]);
   }
@@ -506,8 +510,8 @@ __global__ void __maxnreg__((t2::Cfg<H, UPT>::kMaxReg)) tc2_step_kernel(const St
   }
   __syncthreads();
   for (int i = tid; i < HP; i += NT) {  // layer-0 tangent weights pre-scaled for X_1
-    sW0s[2 * i] = sW0[4 * i] * sSc[kScSt];
-    sW0s[2 * i + 1] = sW0[4 * i + 1] * sSc[kScSt];
+    sW0s[4 * (i >> 1) + (i & 1)] = sW0[w0_at(i, 0)] * sSc[kScSt];
+    sW0s[4 * (i >> 1) + 2 + (i & 1)] = sW0[w0_at(i, 1)] * sSc[kScSt];
   }
   smark(4);
   // W tiles, scaled by 2^kW: MMA layer wl, input block ib = wc / 4: row o of
@@ -591,9 +595,9 @@ __global__ void __maxnreg__((t2::Cfg<H, UPT>::kMaxReg)) tc2_step_kernel(const St
   auto layer0 = [&](int c, float px, float py, float (&z)[8], float (&s1)[8]) {
 #pragma unroll
     for (int k = 0; k < 8; k += 2) {
-      const float4 wa = *reinterpret_cast<const float4*>(sW0 + 4 * (u0 + 8 * c + k));
-      const float4 wb = *reinterpret_cast<const float4*>(sW0 + 4 * (u0 + 8 * c + k + 1));
-      const float2 pre = add2(fma2(f2(wa.y, wb.y), f2s(py), mul2(f2(wa.x, wb.x), f2s(px))), f2(wa.z, wb.z));
+      const float4 wa = *reinterpret_cast<const float4*>(sW0 + 4 * (u0 + 8 * c + k));      // w_x, w_y of k, k+1
+      const float2 wb = *reinterpret_cast<const float2*>(sW0 + 4 * (u0 + 8 * c + k) + 4);  // b of k, k+1
+      const float2 pre = add2(fma2(f2(wa.z, wa.w), f2s(py), mul2(f2(wa.x, wa.y), f2s(px))), wb);
       const float2 zz = AC::value2(pre), ss = AC::s1_2(zz);
       z[k] = zz.x;
       z[k + 1] = zz.y;
@@ -620,9 +624,9 @@ __global__ void __maxnreg__((t2::Cfg<H, UPT>::kMaxReg)) tc2_step_kernel(const St
     }
 #pragma unroll
     for (int k = 0; k < 8; k += 2) {
-      const float4 ws = *reinterpret_cast<const float4*>(sW0s + 2 * (u0 + 8 * c + k));  // (wx, wy) of k, k+1
+      const float4 ws = *reinterpret_cast<const float4*>(sW0s + 2 * (u0 + 8 * c + k));  // wx, wy of k, k+1
       const float2 ss = f2(s1[k], s1[k + 1]);
-      const float2 a = mul2(ss, f2(ws.x, ws.z)), b = mul2(ss, f2(ws.y, ws.w));
+      const float2 a = mul2(ss, f2(ws.x, ws.y)), b = mul2(ss, f2(ws.z, ws.w));
       tx[k] = a.x;
       tx[k + 1] = a.y;
       ty[k] = b.x;
@@ -1294,7 +1298,7 @@ __global__ void __maxnreg__((t2::Cfg<H, UPT>::kMaxReg)) tc2_step_kernel(const St
           for (int k = 0; k < 8; k += 2) {
             const float4 ws = *reinterpret_cast<const float4*>(sW0s + 2 * (u0 + 8 * c + k));
             const float2 ss = AC::s1_2(f2(z[k], z[k + 1]));
-            const float2 a2 = mul2(ss, f2(ws.x, ws.z)), b2 = mul2(ss, f2(ws.y, ws.w));
+            const float2 a2 = mul2(ss, f2(ws.x, ws.y)), b2 = mul2(ss, f2(ws.z, ws.w));
             tx[k] = a2.x;
             tx[k + 1] = a2.y;
             ty[k] = b2.x;
