@@ -68,8 +68,8 @@ struct Lay {
   static constexpr int OFF_SMALL = OFF_B + kBuf;
   // small region, in floats
   static constexpr int S_W0 = 0;               // [32][4] (w_x, w_y, b, 0)
-  static constexpr int S_W0T = S_W0 + 128;     // [32][2] (w_x, w_y) * 2^kXt of X_1
-  static constexpr int S_W0S = S_W0T + 64;     // [32][2] (w_x^2, w_y^2) * 2^kXs of X_1
+  static constexpr int S_W0T = S_W0 + 128;     // [16][2][2] (w_x, w_y) x unit pair, * 2^kXt of X_1
+  static constexpr int S_W0S = S_W0T + 64;     // [16][2][2] (w_x^2, w_y^2) x unit pair, * 2^kXs of X_1
   static constexpr int S_BIAS = S_W0S + 64;    // [2][32]
   static constexpr int S_WD = S_BIAS + 64;     // [32] + output bias at 32 (40)
   static constexpr int S_EX = S_WD + 40;       // [kRows][128]
@@ -305,10 +305,12 @@ __global__ void __maxnreg__(255) sf2_step_kernel(const StepArgs a) {
   __syncthreads();
   for (int i = tid; i < 32; i += kNT) {  // layer-0 tangent / second-derivative weights, scaled for X_1
     const float wx = sW0[4 * i], wy = sW0[4 * i + 1];
-    sW0t[2 * i] = wx * sSc[kScXt];
-    sW0t[2 * i + 1] = wy * sSc[kScXt];
-    sW0s[2 * i] = (wx * wx) * sSc[kScXs];
-    sW0s[2 * i + 1] = (wy * wy) * sSc[kScXs];
+    // unit pairs (k, k+1) adjacent per field: (wx_k, wx_k+1, wy_k, wy_k+1)
+    const int pb = 4 * (i >> 1) + (i & 1);
+    sW0t[pb] = wx * sSc[kScXt];
+    sW0t[pb + 2] = wy * sSc[kScXt];
+    sW0s[pb] = (wx * wx) * sSc[kScXs];
+    sW0s[pb + 2] = (wy * wy) * sSc[kScXs];
   }
   if (wl < NL) tc::st_split8_h(sWB + wl * kWL, 32 * tc::kRowBytes, wo, wc, wv, tc::exp2i(sSci[kSiW + wl]));
   tc::fence_smem_to_async();
@@ -391,8 +393,8 @@ __global__ void __maxnreg__(255) sf2_step_kernel(const StepArgs a) {
       DV::d12(f2(z[k], z[k + 1]), a1, a2);
       const float4 wt = *reinterpret_cast<const float4*>(sW0t + 2 * (u0 + 8 * c + k));  // (wx, wy) of k, k+1
       const float4 ws = *reinterpret_cast<const float4*>(sW0s + 2 * (u0 + 8 * c + k));
-      const float2 t1 = mul2(a1, f2(wt.x, wt.z)), t2 = mul2(a1, f2(wt.y, wt.w));
-      const float2 q1 = mul2(a2, f2(ws.x, ws.z)), q2 = mul2(a2, f2(ws.y, ws.w));
+      const float2 t1 = mul2(a1, f2(wt.x, wt.y)), t2 = mul2(a1, f2(wt.z, wt.w));
+      const float2 q1 = mul2(a2, f2(ws.x, ws.y)), q2 = mul2(a2, f2(ws.z, ws.w));
       tx[k] = t1.x;
       tx[k + 1] = t1.y;
       ty[k] = t2.x;

@@ -841,7 +841,7 @@ __global__ void __maxnreg__((t2::Cfg<H, UPT>::kMaxReg)) tc2_step_kernel(const St
 #pragma unroll
         for (int k = 0; k < 8; k += 2) {
           const int u = u0 + 8 * c + k;
-          const float2 zz = AC::value2(fma2(f2(d[k], d[k + 1]), f2s(f0), f2(bias[u], bias[u + 1])));
+          const float2 zz = AC::value2(fma2(f2(d[k], d[k + 1]), f2s(f0), *reinterpret_cast<const float2*>(bias + u)));
           const float2 ss = mul2(AC::s1_2(zz), f2s(ft));
           z[k] = zz.x;
           z[k + 1] = zz.y;
