@@ -187,3 +187,37 @@ def test_gmsh_reader_contracts():
         with pytest.raises(VpinnError) as e:
             host.Mesh.parse_gmsh(txt)
         assert e.value.code == 3
+
+
+def _msh22(nodes, cells):
+    """gmsh 2.2 ASCII text of a quad mesh (node ids 1-based in file order)."""
+    out = ["$MeshFormat", "2.2 0 8", "$EndMeshFormat", "$Nodes", str(len(nodes))]
+    out += [f"{i + 1} {float(x)!r} {float(y)!r} 0" for i, (x, y) in enumerate(nodes)]
+    out += ["$EndNodes", "$Elements", str(len(cells))]
+    out += [f"{k + 1} 3 2 0 1 " + " ".join(str(int(v) + 1) for v in c) for k, c in enumerate(cells)]
+    out += ["$EndElements", ""]
+    return "\n".join(out)
+
+
+@pytest.mark.parametrize("seed", [1, 2, 3])
+def test_boundary_samples_on_renumbered_meshes_match_oracle(seed):
+    """The host's boundary-edge pass (counting sort by min node id) walks the
+    single-incidence edges in the reference's (min id, max id) map order:
+    with node ids shuffled, the arc-length samples must still equal the
+    oracle's bit for bit (mesh.hpp boundary edges, problem.hpp sampling)."""
+    rng = np.random.default_rng(seed)
+    nx, ny = (int(v) for v in rng.integers(2, 9, size=2))
+    nodes, cells = po.structured_mesh(nx, ny, skew=0.2, skew_seed=seed)
+    perm = rng.permutation(len(nodes))  # new id of old node i is perm[i]
+    pn = np.empty_like(nodes)
+    pn[perm] = nodes
+    pc = perm[np.asarray(cells)]
+    m = host.Mesh.parse_gmsh(_msh22(pn, pc))
+    c = cfg(problem={"forcing": "sin2pi_f", "boundary_g": "sin2pi_u", "n_boundary_points": 97},
+            discretization={"n_test_per_dim": 2, "n_quad_per_dim": 3})
+    hp = host.HostProblem(c, mesh=m)
+    ob = po.OracleProblem(po.ProblemSpec(nodes=pn, cells=pc, n_test_1d=2, n_quad_1d=3, forcing="sin2pi_f",
+                                         boundary_g="sin2pi_u", n_boundary=97), double=False)
+    assert_same_problem(hp, ob)
+    dp = host.HostProblem(c, mesh=m, device_assembly=True)
+    assert np.array_equal(bits(dp.arrays()["boundary_values"], np.float64), bits(ob.array("boundary_values"), np.float64))
