@@ -603,9 +603,10 @@ def _e2e_from_mesh(mesh, device, rank, world, pg, steps):
     E, T, Q = dp.E, dp.T, dp.Q
     e_local = E // world if world > 1 else E
     # nodes (double2), cell node ids (int4), rule (3 Q doubles), basis tables
-    # (3 T Q doubles), penalty points (double2) and targets, parameters
-    h2d = (16 * mesh.n_nodes + 16 * e_local + 8 * 3 * Q + 8 * 3 * T * Q
-           + 24 * (dp.n_bnd + dp.n_sen) + 4 * dp.n_params)
+    # (3 T Q doubles) and their float copies for the matrix-free contraction,
+    # penalty points (float2) and targets (float), parameters
+    h2d = (16 * mesh.n_nodes + 16 * e_local + (8 + 4) * 3 * Q + (8 + 4) * 3 * T * Q
+           + 12 * (dp.n_bnd + dp.n_sen) + 4 * dp.n_params)
     d2h = 4 * params.size + 7 * 8 * rep.steps_run
     return {"value": E * Q * steps / dt, "unit": UNIT, "h2d_bytes_per_step": int(h2d / steps),
             "d2h_bytes_per_step": int(d2h / steps), "seconds": dt,
