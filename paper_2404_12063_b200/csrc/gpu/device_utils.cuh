@@ -169,6 +169,8 @@ struct Act<kActTanh> {
   }
   static __device__ __forceinline__ float2 s1_2(float2 z) { return __ffma2_rn(f2(-z.x, -z.y), z, f2s(1.0f)); }
   static __device__ __forceinline__ float2 kap2(float2 z) { return __fmul2_rn(f2s(-2.0f), z); }
+  // kap is -2 z: callers may fold the -2 into a scalar factor (exact)
+  static constexpr bool kKapLinear = true;
 };
 
 template <>
@@ -183,6 +185,7 @@ struct Act<kActSigmoid> {
   static __device__ __forceinline__ float2 value2(float2 x) { return f2(value(x.x), value(x.y)); }
   static __device__ __forceinline__ float2 s1_2(float2 z) { return __fmul2_rn(z, __fadd2_rn(f2s(1.0f), f2(-z.x, -z.y))); }
   static __device__ __forceinline__ float2 kap2(float2 z) { return __ffma2_rn(f2s(-2.0f), z, f2s(1.0f)); }
+  static constexpr bool kKapLinear = false;
 };
 
 // network.hpp:130-138

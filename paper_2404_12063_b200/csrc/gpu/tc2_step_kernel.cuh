@@ -63,6 +63,9 @@
 #ifndef VPG_PDL_LATE
 #define VPG_PDL_LATE 1  // PDL trigger after the tile loop (the epoch tail launches during the per-CTA outputs)
 #endif
+#ifndef VPG_KAP_FOLD
+#define VPG_KAP_FOLD 1  // tanh: kap = -2 z with the -2 folded into a scalar factor (bit-identical)
+#endif
 #ifndef VPG_PHASE_CLOCK
 #define VPG_PHASE_CLOCK 0  // build with -DVPG_PHASE_CLOCK=1 for tools/phase_clock.py
 #endif
@@ -1220,12 +1223,16 @@ __global__ void __maxnreg__((t2::Cfg<H, UPT>::kMaxReg)) tc2_step_kernel(const St
         for (int k = 0; k < 8; k += 2) {
           const int u = u0 + 8 * c + k;
           const float2 z = f2(zs[k], zs[k + 1]);
-          const float2 s1 = AC::s1_2(z), kp = AC::kap2(z);
+          const float2 s1 = AC::s1_2(z);
           const float2 cc = mul2(s1, f2s(f1));
           const float2 tx = mul2(cc, f2(dx[k], dx[k + 1])), ty = mul2(cc, f2(dy[k], dy[k + 1]));
           const float2 vv = fma2(f2s(ub), z, fma2(f2s(uxb), tx, mul2(f2s(uyb), ty)));
-          const float2 wd = f2(sWd[u], sWd[u + 1]);
-          float2 ga = mul2(wd, fma2(s1, f2s(Ub), mul2(kp, fma2(tx, f2s(Uxv), mul2(ty, f2s(Uyv))))));
+          const float2 wd = *reinterpret_cast<const float2*>(sWd + u);
+          // kap (tx Uxv + ty Uyv); for tanh z (tx (-2 Uxv) + ty (-2 Uyv)), the same bits
+          const float2 kin = (VPG_KAP_FOLD && AC::kKapLinear)
+                                 ? mul2(z, fma2(tx, f2s(-2.f * Uxv), mul2(ty, f2s(-2.f * Uyv))))
+                                 : mul2(AC::kap2(z), fma2(tx, f2s(Uxv), mul2(ty, f2s(Uyv))));
+          float2 ga = mul2(wd, fma2(s1, f2s(Ub), kin));
           if constexpr (C == 2) {  // + s1 wd1 y1bar (channel 1 sees the value stream only)
             ga = fma2(mul2(s1, f2(sWd2[u], sWd2[u + 1])), f2s(Y1), ga);
             const float2 v2 = mul2(f2s(y1b), z);
@@ -1316,10 +1323,13 @@ __global__ void __maxnreg__((t2::Cfg<H, UPT>::kMaxReg)) tc2_step_kernel(const St
 #pragma unroll
         for (int k = 0; k < 8; k += 2) {
           const float2 zz = f2(z[k], z[k + 1]);
-          const float2 s1 = AC::s1_2(zz), kp = AC::kap2(zz);
+          const float2 s1 = AC::s1_2(zz);
+          // kap AT; for tanh z (-2 AT), the same bits
+          const float2 kat = (VPG_KAP_FOLD && AC::kKapLinear) ? mul2(zz, f2s(-2.f * AT))
+                                                              : mul2(AC::kap2(zz), f2s(AT));
           const float2 xx2 = f2(xx[k], xx[k + 1]), xy2 = f2(xy[k], xy[k + 1]);
           const float2 inner = fma2(f2(tx[k], tx[k + 1]), xx2, mul2(f2(ty[k], ty[k + 1]), xy2));
-          const float2 g = fma2(mul2(s1, f2s(A0)), f2(xa[k], xa[k + 1]), mul2(mul2(kp, f2s(AT)), inner));
+          const float2 g = fma2(mul2(s1, f2s(A0)), f2(xa[k], xa[k + 1]), mul2(kat, inner));
           const float2 sb = mul2(s1, f2s(BT));
           const float2 gxx = mul2(sb, xx2), gyy = mul2(sb, xy2);
           ga[k] = g.x;
